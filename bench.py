@@ -1,0 +1,378 @@
+#!/usr/bin/env python
+"""bench.py — BASELINE.json's metric on one B200 (or N independent replicas).
+
+Metric: "sort Gkeys/s at n=2^28 int32 (1 B200); partition-pass HBM GB/s vs
+peak".  A *step* is one full bq_sort (every hot-path row a1-a9) of config 2:
+n = 2^28 int32 keys, i.i.d. uniform over the full int32 range (bqgen, seeded;
+synthetic like the paper's mt19937 inputs).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl bq|reference]
+
+Timing (device, CUDA events on the stream the library launches on):
+  * value / ms_per_step: sum over the K timed steps of the event time around
+    the bq_sort call; before each step the input is restored from a pristine
+    device copy outside the events.  Inputs (1 GiB) are larger than the
+    126 MB L2, and the restore copy streams 2 GiB through it as well.
+  * roofline: the dominant kernel is the tile-partition pass; the library
+    records CUDA events around each of its launches (bq_sort_options.timing);
+    achieved = algorithmic bytes (2 * 4 B * element_passes) / summed launch time.
+  * partition_pass: BASELINE.md's roofline measurement — 10 single out-of-place
+    passes over the pristine input around its Mo3 pivot, L2 flushed before each.
+  * e2e: bq_sort_host (H2D from pinned memory + sort + D2H) per step.
+  * cpu_baseline: the oracle (oracle/, single-threaded) on a bounded sample.
+Multi-GPU (--gpus N under torchrun): replicas only — every rank
+sorts its own copy; the time is the max over ranks; value = N*n / time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_FULL = 1 << 28
+WORKLOAD = "c2: int32 keys, n=2^28, iid uniform over the full int32 range (seeded SplitMix64); full bq_sort"
+METRIC = "sort Gkeys/s at n=2^28 int32 (1 B200); partition-pass HBM GB/s vs peak"
+FALLBACK_HBM_GBS = 6650.0   # /opt/skills/guides/B200_PROFILING.md fallback
+
+
+def load_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def load_traffic():
+    """dram bytes per launch of the partition kernel from the committed ncu
+    summary (profiles/ncu_partition_summary.json), or None."""
+    p = os.path.join(ROOT, "profiles", "ncu_partition_summary.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get("dram_bytes_per_element_pass"), d
+    except Exception:
+        return None, None
+
+
+# ------------------------------------------------------------ distributed ----
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def reduce_max(value: float, world: int, device=None) -> float:
+    """Max over ranks (replica timing).  Works for nccl (device tensor) and gloo."""
+    if world <= 1:
+        return value
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([value], dtype=torch.float64, device=device if device is not None else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def aggregate(n_per_rank: int, ms_total_max: float, steps: int, world: int):
+    """Whole-job throughput of `world` replicas each sorting n_per_rank keys per
+    step: (Gkeys/s, ms_per_step)."""
+    ms_per_step = ms_total_max / steps
+    return world * n_per_rank / (ms_per_step * 1e-3) / 1e9, ms_per_step
+
+
+# ---------------------------------------------------------------- clocks -----
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_rank{gpu_index}.csv")
+
+    def start(self):
+        os.makedirs(os.path.dirname(self.path), exist_ok=True)
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.f.close()
+        rows = []
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                rows.append(parts)
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        smax = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if "Active" in r[5 + i]})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ----------------------------------------------------------- cpu baselines ---
+
+def cpu_baseline(keys_np, sample_n: int):
+    """The oracle (as it stands) and std::sort, single-threaded, on the first
+    sample_n keys of the workload."""
+    import oracle
+    s = keys_np[:sample_n].copy()
+    t0 = time.perf_counter()
+    out = oracle.sort(s, inplace=True)
+    t_or = time.perf_counter() - t0
+    s2 = keys_np[:sample_n].copy()
+    t0 = time.perf_counter()
+    oracle.std_sort(s2, inplace=True)
+    t_std = time.perf_counter() - t0
+    import numpy as np
+    assert np.array_equal(out, s2)
+    return {"value": sample_n / t_or / 1e9, "unit": "Gkeys/s", "cores": 1, "kind": "oracle",
+            "sample": f"first {sample_n} keys of the c2 input (2^{int(math.log2(sample_n))}), one run",
+            "seconds": t_or,
+            "std_sort": {"value": sample_n / t_std / 1e9, "unit": "Gkeys/s", "cores": 1, "seconds": t_std}}
+
+
+# ------------------------------------------------------------- reference -----
+
+def run_reference(args, rank, world):
+    """--impl reference: the oracle (CPU, as it stands) on bounded samples of the
+    same workload.  Under torchrun only rank 0 runs and prints."""
+    if rank != 0:
+        return 0
+    import numpy as np
+    import bqgen
+    import oracle
+    sample = 1 << 22
+    keys = bqgen.i32_full(sample, 1)
+    for _ in range(args.warmup):
+        oracle.sort(keys)
+    ts = []
+    for _ in range(args.steps):
+        s = keys.copy()
+        t0 = time.perf_counter()
+        oracle.sort(s, inplace=True)
+        ts.append(time.perf_counter() - t0)
+    ms = 1e3 * sum(ts) / len(ts)
+    value = sample / (ms * 1e-3) / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "Gkeys/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+        "data": "synthetic",
+        "config": {"workload": WORKLOAD, "sample": f"each step sorts the first 2^22 keys of the c2 input"},
+        "cpu_baseline": {"value": value, "unit": "Gkeys/s", "cores": 1, "kind": "oracle",
+                         "sample": "first 2^22 keys of the c2 input per step"},
+        "e2e": {"value": value, "unit": "Gkeys/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------- main ----
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="bq", choices=["bq", "reference"])
+    ap.add_argument("--n", type=int, default=N_FULL, help="keys per GPU (default 2^28)")
+    ap.add_argument("--pivot-rule", type=int, default=1, help="0 Mo3, 1 ninther")
+    ap.add_argument("--passes", type=int, default=10)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-sample", type=int, default=1 << 27)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-verify", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import numpy as np
+    import torch
+    import bqgen
+    import paper_1604_06697_b200 as bq
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    n = args.n
+    keys_np = bqgen.i32_full(n, seed=1 + rank)
+    src = torch.from_numpy(keys_np).to(dev)
+    data = torch.empty_like(src)
+    ws = bq.workspace(bq.BQ_I32, n, dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step(timing=True):
+        return bq.bq_sort_ex(data, pivot_rule=args.pivot_rule, timing=timing, ws=ws, stream=stream)
+
+    for _ in range(args.warmup):
+        data.copy_(src)
+        step()
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local)
+    barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    stats = []
+    for i in range(args.steps):
+        data.copy_(src)
+        ev[i][0].record(stream)
+        stats.append(step())
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    ms_total = sum(step_ms)
+    ms_total_max = reduce_max(ms_total, world, dev)
+    value, ms_per_step = aggregate(n, ms_total_max, args.steps, world)
+
+    verified = None
+    if not args.no_verify:
+        ref = torch.sort(src)[0]          # a library routine (CUB radix sort), test-only check
+        verified = bool(torch.equal(ref, data))
+        del ref
+
+    # roofline of the dominant kernel (partition), live from the timed steps
+    part_ms = sum(s["partition_ms"] for s in stats)
+    part_bytes = sum(s["partition_bytes"] for s in stats)
+    peak, peak_src = load_peak()
+    achieved = part_bytes / (part_ms * 1e-3) / 1e9
+    elem_passes = stats[-1]["element_passes"]
+    traffic_per_ep, traffic_doc = load_traffic()
+    launches = stats[-1]["partition_launches"]
+    roofline = {
+        "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+        "peak_source": peak_src,
+        "kernel": "k_partition (tile partition pass, all levels of the sort)",
+        "algorithmic_bytes_per_launch": part_bytes / len(stats) / launches,
+        "launch_ms_avg": part_ms / len(stats) / launches,
+        "launches_per_step": launches,
+        "share_of_step": part_ms / ms_total,
+        "traffic": (traffic_per_ep * elem_passes / launches) if traffic_per_ep else None,
+    }
+
+    # BASELINE.md partition-pass measurement: 10 single passes, L2 flushed
+    ppass = None
+    if args.passes > 0:
+        pv = bq.bq_pivot_i32(src, bq.BQ_PIVOT_MO3, ws=ws, stream=stream)
+        counts = torch.zeros(3, dtype=torch.int64, device=dev)
+        flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+        times = []
+        for _ in range(args.passes + 1):
+            flush.fill_(1)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            bq.bq_partition_pass(src, data, pv, counts, ws=ws, stream=stream)
+            b.record(stream)
+            torch.cuda.synchronize()
+            times.append(a.elapsed_time(b))
+        times = times[1:]
+        del flush
+        pbytes = 2 * 4 * n
+        med, mn = statistics.median(times), min(times)
+        c = counts.cpu().tolist()
+        ppass = {"passes": args.passes, "bytes": pbytes, "pivot": pv, "split": c[0], "n_equal": c[1],
+                 "ms_median": med, "ms_min": mn,
+                 "gbs_median": pbytes / (med * 1e-3) / 1e9, "gbs_max": pbytes / (mn * 1e-3) / 1e9,
+                 "frac_median": pbytes / (med * 1e-3) / 1e9 / peak,
+                 "frac_of_8tbs_median": pbytes / (med * 1e-3) / 1e9 / 8000.0,
+                 "note": "pass + equal-band fill kernel, L2 flushed (512 MiB write) before each"}
+
+    # end to end through the public API with host buffers
+    e2e = None
+    if args.e2e_steps > 0:
+        host = torch.from_numpy(keys_np.copy()).pin_memory()
+        t_e2e = []
+        for i in range(args.e2e_steps + 1):
+            host.copy_(torch.from_numpy(keys_np))
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            bq.bq_sort_host(host, data, pivot_rule=args.pivot_rule, ws=ws, stream=stream)
+            b.record(stream)
+            torch.cuda.synchronize()
+            if i > 0:
+                t_e2e.append(a.elapsed_time(b))
+        e2e_ms = reduce_max(sum(t_e2e), world, dev) / len(t_e2e)
+        e2e = {"value": world * n / (e2e_ms * 1e-3) / 1e9, "unit": "Gkeys/s",
+               "h2d_bytes_per_step": 4 * n, "d2h_bytes_per_step": 4 * n, "ms_per_step": e2e_ms}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(keys_np, min(args.cpu_sample, n))
+
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    if rank != 0:
+        return 0
+    last = stats[-1]
+    line = {
+        "metric": METRIC, "value": value, "unit": "Gkeys/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "n_per_gpu": n, "pivot_rule": "ninther" if args.pivot_rule else "mo3",
+                   "parallelism": f"replicas{world}" if world > 1 else "1gpu",
+                   "l2": "inputs (1 GiB) larger than L2 (126 MB); restore copy between steps is untimed",
+                   "timing": "sum of per-step CUDA events around bq_sort on the launch stream"},
+        "roofline": roofline,
+        "partition_pass": ppass,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": int(sum(s["kernel_launches"] for s in stats)),
+        "clocks": clk,
+        "sort_stats": {k: last[k] for k in ("levels", "partition_launches", "kernel_launches", "element_passes",
+                                            "partitioned_segments", "leaves", "fallback_segments",
+                                            "band_elements")},
+        "passes_per_element": last["element_passes"] / n,
+        "verified_vs_torch_sort": verified,
+        "step_ms": step_ms,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

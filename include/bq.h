@@ -1,0 +1,182 @@
+/*
+ * bq.h — C-ABI of libbq.so, the B200-native (sm_100a) BlockQuicksort hot path.
+ *
+ * Paper: S. Edelkamp, A. Weiß, "BlockQuicksort: How Branch Mispredictions
+ * don't affect Quicksort", arXiv 1604.06697 (PAPER.md; P:n = line n).
+ *
+ * The operations follow the paper's problem statements:
+ *   - partition: "returns a pointer p ... all elements left of p are smaller
+ *     or equal the pivot and all elements on the right are greater or equal"
+ *     (§2); realised three-way (< | == | >), so the returned split
+ *     is #{k < pivot} and the equal band is reported separately (the paper's
+ *     duplicate check "dc", always on);
+ *   - sort: Quicksort/Introsort driven by that partitioner (Alg. 1 P:272-284;
+ *     §2 "Quicksort and improvements" P:286-330; Appendix B).
+ *
+ * Conventions for every entry point
+ *   - Data pointers (keys, recs, src, dst) are DEVICE pointers owned by the
+ *     caller (e.g. torch tensors); the library keeps none of them after the
+ *     call returns.  Host pointers appear only where stated (bq_sort_host,
+ *     split/n_equal/pivot/stats out-params).
+ *   - `ws` is caller-allocated DEVICE workspace of at least
+ *     bq_workspace_bytes(kind, n) bytes, 256-byte aligned, not aliasing the
+ *     data.  It may be reused across calls on the same stream.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default
+ *     stream).  All device work is enqueued on it.
+ *   - n must satisfy n <= 2^31 - 1 (BQ_ERR_INVALID_ARGUMENT otherwise);
+ *     n = 0 and n = 1 are valid no-ops.
+ *   - Errors are returned as bq_status; no exception crosses the ABI.  On
+ *     BQ_ERR_CUDA the CUDA error text is available from bq_last_error()
+ *     (thread-local).  A device that is not sm_100 gives BQ_ERR_UNSUPPORTED.
+ *   - The library holds no global mutable state except an immutable per-device
+ *     cache of launch limits; concurrent calls on disjoint data and distinct
+ *     workspaces are safe.
+ *
+ * Orders
+ *   - int32, uint64: natural order (signed / unsigned).
+ *   - float64: IEEE 754 totalOrder restricted to non-NaN values (-0.0 < +0.0)
+ *     (reading R9; the paper sorts ints).  NaN inputs are
+ *     outside the contract (they are ordered deterministically by bit pattern).
+ *   - records: by `key` only ("Only the first component is compared",
+ *     P:671-672); the order among equal keys is unspecified, as in Quicksort.
+ */
+#ifndef BQ_H
+#define BQ_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define BQ_API __attribute__((visibility("default")))
+#else
+#define BQ_API
+#endif
+
+typedef enum {
+    BQ_OK = 0,
+    BQ_ERR_INVALID_ARGUMENT = 1, /* NULL with n > 0, n >= 2^31, bad alignment, bad enum */
+    BQ_ERR_WORKSPACE = 2,        /* ws NULL or ws_bytes < bq_workspace_bytes(kind, n) */
+    BQ_ERR_CUDA = 3,             /* a CUDA runtime call failed; see bq_last_error() */
+    BQ_ERR_UNSUPPORTED = 4       /* no CUDA device, or the device is not sm_100 */
+} bq_status;
+
+typedef enum { BQ_I32 = 0, BQ_U64 = 1, BQ_F64 = 2, BQ_REC32 = 3 } bq_kind;
+
+/* Pivot sample rules (§2; §4 "pivot selection" P:719-753):
+ *   MO3     median of the keys at segment positions {b, b+floor(len/2), e-1}
+ *           (Appendix B median_of_3, P:1069-1075, P:1215 read with e-1);
+ *   NINTHER pseudomedian of 9 = median of the medians of three triples, at
+ *           positions b + floor(k*(len-1)/8), k = 0..8. */
+typedef enum { BQ_PIVOT_MO3 = 0, BQ_PIVOT_NINTHER = 1 } bq_pivot_rule;
+
+/* 32-byte record: key + 24-byte payload, 16-byte aligned in device memory
+ * (BASELINE.json config 5; the paper's "Record" element). */
+typedef struct {
+    uint64_t key;
+    uint64_t payload[3];
+} bq_record32;
+
+typedef struct {
+    int32_t pivot_rule;   /* bq_pivot_rule for segments > leaf size; default NINTHER */
+    int32_t depth_limit;  /* < 0: Introsort limit 2*floor(log2 n)+3 */
+    int32_t timing;       /* != 0: time every partition launch with CUDA events */
+    int32_t reserved[5];  /* must be 0 */
+} bq_sort_options;
+
+typedef struct {
+    uint32_t levels;               /* breadth-first partition levels executed */
+    uint32_t partition_launches;   /* launches of the tile-partition kernel */
+    uint32_t kernel_launches;      /* all libbq kernel launches of the call */
+    uint32_t reserved0;
+    uint64_t element_passes;       /* sum of segment lengths over all partition passes */
+    uint64_t partitioned_segments; /* segments partitioned (calls of the partitioner) */
+    uint64_t leaves;               /* segments finished by the shared-memory leaf sort */
+    uint64_t fallback_segments;    /* segments that hit the depth limit (fallback sort) */
+    uint64_t band_elements;        /* keys placed by the equal-band fill */
+    double partition_ms;           /* sum of partition-kernel times (timing != 0) */
+    double partition_bytes;        /* algorithmic bytes of those launches: 2*w*element_passes */
+} bq_sort_stats;
+
+/* Workspace bytes every call below needs for `n` elements of `kind`:
+ * an n*w scratch buffer for the out-of-place partition passes plus O(n/T)
+ * bytes of tile status words, segment descriptors and leaf lists. */
+BQ_API size_t bq_workspace_bytes(bq_kind kind, size_t n);
+
+/* ---- pivot selection (hot-path step a1) -------------------------------------
+ * Computes the pivot value of keys[0, n) with `rule` on the device and
+ * returns it in *pivot (host).  Synchronises `stream`.  n >= 1.
+ * (For records the "pivot" is a key.) */
+BQ_API bq_status bq_pivot_i32(const int32_t *keys, size_t n, bq_pivot_rule rule, int32_t *pivot,
+                              void *ws, size_t ws_bytes, void *stream);
+BQ_API bq_status bq_pivot_u64(const uint64_t *keys, size_t n, bq_pivot_rule rule, uint64_t *pivot,
+                              void *ws, size_t ws_bytes, void *stream);
+BQ_API bq_status bq_pivot_f64(const double *keys, size_t n, bq_pivot_rule rule, double *pivot,
+                              void *ws, size_t ws_bytes, void *stream);
+BQ_API bq_status bq_pivot_records(const bq_record32 *recs, size_t n, bq_pivot_rule rule,
+                                  uint64_t *pivot_key, void *ws, size_t ws_bytes, void *stream);
+
+/* ---- partition (hot-path steps a2-a6; Alg. 3) ---------------------
+ * Permutes keys[0, n) in place so that
+ *     [0, split)                  < pivot
+ *     [split, split + n_equal)   == pivot
+ *     [split + n_equal, n)        > pivot
+ * with split = #{k < pivot}, and preserves the multiset.  The layout is
+ * deterministic: the < keys keep their input order, the > keys appear in
+ * reverse input order.  Returns split and n_equal to the host (synchronises
+ * `stream`).  A NaN f64 pivot is BQ_ERR_INVALID_ARGUMENT. */
+BQ_API bq_status bq_partition_i32(int32_t *keys, size_t n, int32_t pivot, size_t *split,
+                                  size_t *n_equal, void *ws, size_t ws_bytes, void *stream);
+BQ_API bq_status bq_partition_u64(uint64_t *keys, size_t n, uint64_t pivot, size_t *split,
+                                  size_t *n_equal, void *ws, size_t ws_bytes, void *stream);
+BQ_API bq_status bq_partition_f64(double *keys, size_t n, double pivot, size_t *split,
+                                  size_t *n_equal, void *ws, size_t ws_bytes, void *stream);
+BQ_API bq_status bq_partition_records(bq_record32 *recs, size_t n, uint64_t pivot_key,
+                                      size_t *split, size_t *n_equal, void *ws, size_t ws_bytes,
+                                      void *stream);
+
+/* One out-of-place partition pass, fully asynchronous (no host sync): reads
+ * src[0, n), writes the three-way partitioned permutation to dst[0, n)
+ * (same layout as bq_partition_*), and writes {split, n_equal, n_greater} as
+ * three uint64 to the DEVICE pointer d_counts.  `pivot` points to a HOST
+ * value of the kind's storage type (int32 / uint64 / double; a uint64 key for
+ * records).  src and dst must not overlap.  This is the timed unit of the
+ * partition-pass roofline. */
+BQ_API bq_status bq_partition_pass(bq_kind kind, const void *src, void *dst, size_t n,
+                                   const void *pivot, uint64_t *d_counts, void *ws,
+                                   size_t ws_bytes, void *stream);
+
+/* ---- sort (hot-path steps a1-a9) ---------------------------------------------
+ * Sorts data[0, n) ascending in place (orders above).  Enqueued on `stream`;
+ * the level loop reads one small counter block back per partition level
+ * (the call returns after the stream has drained). */
+BQ_API bq_status bq_sort_i32(int32_t *keys, size_t n, void *ws, size_t ws_bytes, void *stream);
+BQ_API bq_status bq_sort_u64(uint64_t *keys, size_t n, void *ws, size_t ws_bytes, void *stream);
+BQ_API bq_status bq_sort_f64(double *keys, size_t n, void *ws, size_t ws_bytes, void *stream);
+BQ_API bq_status bq_sort_records(bq_record32 *recs, size_t n, void *ws, size_t ws_bytes,
+                                 void *stream);
+
+/* Kind-generic sort with options (NULL = defaults) and statistics (NULL = none). */
+BQ_API bq_status bq_sort_ex(bq_kind kind, void *data, size_t n, const bq_sort_options *opt,
+                            bq_sort_stats *stats, void *ws, size_t ws_bytes, void *stream);
+
+/* End-to-end sort of a HOST array: copies host_data[0,n) to dev_data (a
+ * caller-owned device buffer of n elements), sorts it there, copies the
+ * result back into host_data and synchronises `stream`.  host_data should be
+ * pinned for full PCIe bandwidth. */
+BQ_API bq_status bq_sort_host(bq_kind kind, void *host_data, size_t n, void *dev_data,
+                              const bq_sort_options *opt, void *ws, size_t ws_bytes,
+                              void *stream);
+
+BQ_API const char *bq_status_string(bq_status s);
+BQ_API const char *bq_last_error(void);
+/* Library version as 10000*major + 100*minor + patch. */
+BQ_API int bq_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BQ_H */

@@ -1,0 +1,292 @@
+"""Python binding of libbq.so — argument marshalling only.
+
+Every step of the hot path runs in the CUDA kernels behind the C-ABI
+(include/bq.h); this module only turns torch tensors into device pointers and
+the current CUDA stream into a ``cudaStream_t``.  There is no CPU fallback:
+if ``libbq.so`` is missing or fails to load, importing this module raises.
+
+Function names are the C names.  Tensors must be CUDA, contiguous, and of the
+kind's dtype: int32 (``i32``), uint64 or int64 (``u64``, reinterpreted as
+uint64), float64 (``f64``), and records as an (n, 4) uint64/int64 tensor whose
+column 0 is the key (``rec32``, 32 bytes per row).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libbq.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} not found: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+        "(there is no CPU fallback)")
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+BQ_OK, BQ_ERR_INVALID_ARGUMENT, BQ_ERR_WORKSPACE, BQ_ERR_CUDA, BQ_ERR_UNSUPPORTED = range(5)
+BQ_I32, BQ_U64, BQ_F64, BQ_REC32 = range(4)
+BQ_PIVOT_MO3, BQ_PIVOT_NINTHER = range(2)
+KIND = {"i32": BQ_I32, "u64": BQ_U64, "f64": BQ_F64, "rec32": BQ_REC32}
+WIDTH = {BQ_I32: 4, BQ_U64: 8, BQ_F64: 8, BQ_REC32: 32}
+
+
+class bq_sort_options(ctypes.Structure):
+    _fields_ = [("pivot_rule", ctypes.c_int32), ("depth_limit", ctypes.c_int32),
+                ("timing", ctypes.c_int32), ("reserved", ctypes.c_int32 * 5)]
+
+
+class bq_sort_stats(ctypes.Structure):
+    _fields_ = [("levels", ctypes.c_uint32), ("partition_launches", ctypes.c_uint32),
+                ("kernel_launches", ctypes.c_uint32), ("reserved0", ctypes.c_uint32),
+                ("element_passes", ctypes.c_uint64), ("partitioned_segments", ctypes.c_uint64),
+                ("leaves", ctypes.c_uint64), ("fallback_segments", ctypes.c_uint64),
+                ("band_elements", ctypes.c_uint64), ("partition_ms", ctypes.c_double),
+                ("partition_bytes", ctypes.c_double)]
+
+    def as_dict(self):
+        return {f: (getattr(self, f) if not isinstance(getattr(self, f), ctypes.Array) else None)
+                for f, _ in self._fields_}
+
+
+_vp, _sz, _st = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int
+_psz = ctypes.POINTER(ctypes.c_size_t)
+
+_SIGS = {
+    "bq_workspace_bytes": (_sz, [_st, _sz]),
+    "bq_pivot_i32": (_st, [_vp, _sz, _st, ctypes.POINTER(ctypes.c_int32), _vp, _sz, _vp]),
+    "bq_pivot_u64": (_st, [_vp, _sz, _st, ctypes.POINTER(ctypes.c_uint64), _vp, _sz, _vp]),
+    "bq_pivot_f64": (_st, [_vp, _sz, _st, ctypes.POINTER(ctypes.c_double), _vp, _sz, _vp]),
+    "bq_pivot_records": (_st, [_vp, _sz, _st, ctypes.POINTER(ctypes.c_uint64), _vp, _sz, _vp]),
+    "bq_partition_i32": (_st, [_vp, _sz, ctypes.c_int32, _psz, _psz, _vp, _sz, _vp]),
+    "bq_partition_u64": (_st, [_vp, _sz, ctypes.c_uint64, _psz, _psz, _vp, _sz, _vp]),
+    "bq_partition_f64": (_st, [_vp, _sz, ctypes.c_double, _psz, _psz, _vp, _sz, _vp]),
+    "bq_partition_records": (_st, [_vp, _sz, ctypes.c_uint64, _psz, _psz, _vp, _sz, _vp]),
+    "bq_partition_pass": (_st, [_st, _vp, _vp, _sz, _vp, _vp, _vp, _sz, _vp]),
+    "bq_sort_i32": (_st, [_vp, _sz, _vp, _sz, _vp]),
+    "bq_sort_u64": (_st, [_vp, _sz, _vp, _sz, _vp]),
+    "bq_sort_f64": (_st, [_vp, _sz, _vp, _sz, _vp]),
+    "bq_sort_records": (_st, [_vp, _sz, _vp, _sz, _vp]),
+    "bq_sort_ex": (_st, [_st, _vp, _sz, ctypes.POINTER(bq_sort_options),
+                         ctypes.POINTER(bq_sort_stats), _vp, _sz, _vp]),
+    "bq_sort_host": (_st, [_st, _vp, _sz, _vp, ctypes.POINTER(bq_sort_options), _vp, _sz, _vp]),
+    "bq_status_string": (ctypes.c_char_p, [_st]),
+    "bq_last_error": (ctypes.c_char_p, []),
+    "bq_version": (ctypes.c_int, []),
+}
+for _name, (_res, _args) in _SIGS.items():
+    _f = getattr(_lib, _name)
+    _f.restype, _f.argtypes = _res, _args
+
+
+class BQError(RuntimeError):
+    def __init__(self, status: int):
+        self.status = status
+        msg = _lib.bq_status_string(status).decode()
+        detail = _lib.bq_last_error().decode()
+        super().__init__(f"{msg}: {detail}" if detail else msg)
+
+
+def _check(status: int):
+    if status != BQ_OK:
+        raise BQError(status)
+
+
+# --- marshalling helpers -------------------------------------------------------
+
+def kind_of(t: torch.Tensor) -> int:
+    if t.dim() == 2 and t.shape[1] == 4 and t.dtype in (torch.uint64, torch.int64):
+        return BQ_REC32
+    if t.dtype == torch.int32:
+        return BQ_I32
+    if t.dtype in (torch.uint64, torch.int64):
+        return BQ_U64
+    if t.dtype == torch.float64:
+        return BQ_F64
+    raise TypeError(f"unsupported tensor {t.dtype} {tuple(t.shape)}")
+
+
+def _n(t: torch.Tensor) -> int:
+    return t.shape[0] if t.dim() >= 1 else 0
+
+
+def _dev(t: torch.Tensor) -> int:
+    if not t.is_cuda:
+        raise ValueError("expected a CUDA tensor")
+    if not t.is_contiguous():
+        raise ValueError("expected a contiguous tensor")
+    return t.data_ptr()
+
+
+def _stream(stream) -> int:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def workspace_bytes(kind: int, n: int) -> int:
+    return int(_lib.bq_workspace_bytes(kind, n))
+
+
+def bq_workspace_bytes(kind: int, n: int) -> int:
+    return workspace_bytes(kind, n)
+
+
+def workspace(kind: int, n: int, device=None) -> torch.Tensor:
+    """A device workspace tensor of bq_workspace_bytes(kind, n) bytes."""
+    return torch.empty(workspace_bytes(kind, n), dtype=torch.uint8,
+                       device=device if device is not None else "cuda")
+
+
+def _ws(ws, kind, n, like):
+    if ws is None:
+        ws = workspace(kind, n, like.device)
+    return ws.data_ptr(), ws.numel() * ws.element_size()
+
+
+# --- entry points ---------------------------------------------------------------
+
+def _pivot(name, ctype, t, rule, ws, stream):
+    kind = kind_of(t)
+    w, wb = _ws(ws, kind, _n(t), t)
+    out = ctype()
+    _check(getattr(_lib, name)(_dev(t), _n(t), rule, ctypes.byref(out), w, wb, _stream(stream)))
+    return out.value
+
+
+def bq_pivot_i32(keys, rule=BQ_PIVOT_MO3, ws=None, stream=None):
+    return _pivot("bq_pivot_i32", ctypes.c_int32, keys, rule, ws, stream)
+
+
+def bq_pivot_u64(keys, rule=BQ_PIVOT_MO3, ws=None, stream=None):
+    return _pivot("bq_pivot_u64", ctypes.c_uint64, keys, rule, ws, stream)
+
+
+def bq_pivot_f64(keys, rule=BQ_PIVOT_MO3, ws=None, stream=None):
+    return _pivot("bq_pivot_f64", ctypes.c_double, keys, rule, ws, stream)
+
+
+def bq_pivot_records(recs, rule=BQ_PIVOT_MO3, ws=None, stream=None):
+    return _pivot("bq_pivot_records", ctypes.c_uint64, recs, rule, ws, stream)
+
+
+def _partition(name, cpivot, t, pivot, ws, stream):
+    kind = kind_of(t)
+    w, wb = _ws(ws, kind, _n(t), t)
+    s, e = ctypes.c_size_t(0), ctypes.c_size_t(0)
+    _check(getattr(_lib, name)(_dev(t), _n(t), cpivot(pivot), ctypes.byref(s), ctypes.byref(e),
+                               w, wb, _stream(stream)))
+    return s.value, e.value
+
+
+def bq_partition_i32(keys, pivot, ws=None, stream=None):
+    return _partition("bq_partition_i32", ctypes.c_int32, keys, pivot, ws, stream)
+
+
+def bq_partition_u64(keys, pivot, ws=None, stream=None):
+    return _partition("bq_partition_u64", ctypes.c_uint64, keys, pivot, ws, stream)
+
+
+def bq_partition_f64(keys, pivot, ws=None, stream=None):
+    return _partition("bq_partition_f64", ctypes.c_double, keys, pivot, ws, stream)
+
+
+def bq_partition_records(recs, pivot_key, ws=None, stream=None):
+    return _partition("bq_partition_records", ctypes.c_uint64, recs, pivot_key, ws, stream)
+
+
+_PIVOT_CTYPE = {BQ_I32: ctypes.c_int32, BQ_U64: ctypes.c_uint64, BQ_F64: ctypes.c_double,
+                BQ_REC32: ctypes.c_uint64}
+
+
+def bq_partition_pass(src, dst, pivot, d_counts, ws=None, stream=None):
+    """Asynchronous out-of-place pass; d_counts is a CUDA uint64/int64 tensor of >= 3."""
+    kind = kind_of(src)
+    w, wb = _ws(ws, kind, _n(src), src)
+    pv = _PIVOT_CTYPE[kind](pivot)
+    _check(_lib.bq_partition_pass(kind, _dev(src), _dev(dst), _n(src), ctypes.byref(pv),
+                                  _dev(d_counts), w, wb, _stream(stream)))
+
+
+def _sort(name, t, ws, stream):
+    kind = kind_of(t)
+    w, wb = _ws(ws, kind, _n(t), t)
+    _check(getattr(_lib, name)(_dev(t), _n(t), w, wb, _stream(stream)))
+    return t
+
+
+def bq_sort_i32(keys, ws=None, stream=None):
+    return _sort("bq_sort_i32", keys, ws, stream)
+
+
+def bq_sort_u64(keys, ws=None, stream=None):
+    return _sort("bq_sort_u64", keys, ws, stream)
+
+
+def bq_sort_f64(keys, ws=None, stream=None):
+    return _sort("bq_sort_f64", keys, ws, stream)
+
+
+def bq_sort_records(recs, ws=None, stream=None):
+    return _sort("bq_sort_records", recs, ws, stream)
+
+
+def _opts(pivot_rule, depth_limit, timing):
+    o = bq_sort_options()
+    o.pivot_rule = pivot_rule
+    o.depth_limit = depth_limit
+    o.timing = int(timing)
+    return o
+
+
+def bq_sort_ex(data, pivot_rule=BQ_PIVOT_NINTHER, depth_limit=-1, timing=False, ws=None, stream=None):
+    """Kind-generic sort; returns the bq_sort_stats as a dict."""
+    kind = kind_of(data)
+    w, wb = _ws(ws, kind, _n(data), data)
+    o = _opts(pivot_rule, depth_limit, timing)
+    st = bq_sort_stats()
+    _check(_lib.bq_sort_ex(kind, _dev(data), _n(data), ctypes.byref(o), ctypes.byref(st), w, wb,
+                           _stream(stream)))
+    return st.as_dict()
+
+
+def bq_sort_host(host, dev, pivot_rule=BQ_PIVOT_NINTHER, ws=None, stream=None):
+    """End-to-end sort of a host (ideally pinned) tensor through dev (same shape/dtype)."""
+    kind = kind_of(dev)
+    if host.is_cuda or not host.is_contiguous():
+        raise ValueError("host must be a contiguous CPU tensor")
+    w, wb = _ws(ws, kind, _n(dev), dev)
+    o = _opts(pivot_rule, -1, False)
+    _check(_lib.bq_sort_host(kind, host.data_ptr(), _n(dev), _dev(dev), ctypes.byref(o), w, wb,
+                             _stream(stream)))
+    return host
+
+
+# --- conveniences ---------------------------------------------------------------
+
+_SORT_BY_KIND = {BQ_I32: bq_sort_i32, BQ_U64: bq_sort_u64, BQ_F64: bq_sort_f64,
+                 BQ_REC32: bq_sort_records}
+_PART_BY_KIND = {BQ_I32: bq_partition_i32, BQ_U64: bq_partition_u64, BQ_F64: bq_partition_f64,
+                 BQ_REC32: bq_partition_records}
+_PIVOT_BY_KIND = {BQ_I32: bq_pivot_i32, BQ_U64: bq_pivot_u64, BQ_F64: bq_pivot_f64,
+                  BQ_REC32: bq_pivot_records}
+
+
+def sort(t, ws=None, stream=None):
+    """Sort a CUDA tensor in place (kind from dtype/shape)."""
+    return _SORT_BY_KIND[kind_of(t)](t, ws, stream)
+
+
+def partition(t, pivot, ws=None, stream=None):
+    return _PART_BY_KIND[kind_of(t)](t, pivot, ws, stream)
+
+
+def pivot(t, rule=BQ_PIVOT_MO3, ws=None, stream=None):
+    return _PIVOT_BY_KIND[kind_of(t)](t, rule, ws, stream)
+
+
+def version() -> int:
+    return int(_lib.bq_version())

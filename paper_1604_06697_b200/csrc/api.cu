@@ -1,0 +1,119 @@
+// api.cu — kind-independent entry points of libbq.so: errors, device check,
+// workspace sizing and the kind-generic calls (see include/bq.h).
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+
+#include "api_kind.cuh"
+
+namespace bq {
+
+static thread_local char g_last_error[512] = "";
+
+bq_status set_error(bq_status st, const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    std::vsnprintf(g_last_error, sizeof g_last_error, fmt, ap);
+    va_end(ap);
+    return st;
+}
+
+// Immutable per-device cache: 1 = sm_100, -1 = unsupported, 0 = unknown.
+static int g_dev_ok[64];
+
+bq_status check_device() {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return set_error(BQ_ERR_UNSUPPORTED, "no CUDA device: %s", cudaGetErrorString(e));
+    if (dev < 0 || dev >= 64) return set_error(BQ_ERR_UNSUPPORTED, "device ordinal %d", dev);
+    int ok = __atomic_load_n(&g_dev_ok[dev], __ATOMIC_RELAXED);
+    if (ok == 0) {
+        int major = 0, minor = 0;
+        if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess ||
+            cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev) != cudaSuccess)
+            return set_error(BQ_ERR_UNSUPPORTED, "cannot query device %d", dev);
+        ok = (major == 10 && minor == 0) ? 1 : -1;
+        __atomic_store_n(&g_dev_ok[dev], ok, __ATOMIC_RELAXED);
+    }
+    if (ok < 0) return set_error(BQ_ERR_UNSUPPORTED, "libbq.so is built for sm_100a only");
+    return BQ_OK;
+}
+
+}  // namespace bq
+
+using namespace bq::detail;
+
+extern "C" {
+
+BQ_API size_t bq_workspace_bytes(bq_kind kind, size_t n) {
+    switch (kind) {
+        case BQ_I32: return ws_i32(n);
+        case BQ_U64: return ws_u64(n);
+        case BQ_F64: return ws_f64(n);
+        case BQ_REC32: return ws_rec(n);
+    }
+    return 0;
+}
+
+BQ_API bq_status bq_partition_pass(bq_kind kind, const void *src, void *dst, size_t n, const void *pivot,
+                                   uint64_t *d_counts, void *ws, size_t ws_bytes, void *stream) {
+    if (pivot == nullptr) return bq::set_error(BQ_ERR_INVALID_ARGUMENT, "NULL pivot");
+    cudaStream_t s = (cudaStream_t)stream;
+    switch (kind) {
+        case BQ_I32: return pass_i32(src, dst, n, pivot, d_counts, ws, ws_bytes, s);
+        case BQ_U64: return pass_u64(src, dst, n, pivot, d_counts, ws, ws_bytes, s);
+        case BQ_F64: {
+            double d;
+            std::memcpy(&d, pivot, 8);
+            if (d != d) return bq::set_error(BQ_ERR_INVALID_ARGUMENT, "NaN pivot");
+            return pass_f64(src, dst, n, pivot, d_counts, ws, ws_bytes, s);
+        }
+        case BQ_REC32: return pass_rec(src, dst, n, pivot, d_counts, ws, ws_bytes, s);
+    }
+    return bq::set_error(BQ_ERR_INVALID_ARGUMENT, "bad kind %d", (int)kind);
+}
+
+BQ_API bq_status bq_sort_ex(bq_kind kind, void *data, size_t n, const bq_sort_options *opt, bq_sort_stats *stats,
+                            void *ws, size_t ws_bytes, void *stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    switch (kind) {
+        case BQ_I32: return sort_i32(data, n, opt, stats, ws, ws_bytes, s);
+        case BQ_U64: return sort_u64(data, n, opt, stats, ws, ws_bytes, s);
+        case BQ_F64: return sort_f64(data, n, opt, stats, ws, ws_bytes, s);
+        case BQ_REC32: return sort_rec(data, n, opt, stats, ws, ws_bytes, s);
+    }
+    return bq::set_error(BQ_ERR_INVALID_ARGUMENT, "bad kind %d", (int)kind);
+}
+
+BQ_API bq_status bq_sort_host(bq_kind kind, void *host_data, size_t n, void *dev_data, const bq_sort_options *opt,
+                              void *ws, size_t ws_bytes, void *stream) {
+    static const size_t W[4] = {4, 8, 8, 32};
+    if ((int)kind < 0 || (int)kind > 3) return bq::set_error(BQ_ERR_INVALID_ARGUMENT, "bad kind %d", (int)kind);
+    if (n > 0 && (host_data == nullptr || dev_data == nullptr))
+        return bq::set_error(BQ_ERR_INVALID_ARGUMENT, "NULL buffer with n > 0");
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t bytes = n * W[kind];
+    if (bytes) BQ_CK(cudaMemcpyAsync(dev_data, host_data, bytes, cudaMemcpyHostToDevice, s));
+    bq_status st = bq_sort_ex(kind, dev_data, n, opt, nullptr, ws, ws_bytes, stream);
+    if (st != BQ_OK) return st;
+    if (bytes) BQ_CK(cudaMemcpyAsync(host_data, dev_data, bytes, cudaMemcpyDeviceToHost, s));
+    BQ_CK(cudaStreamSynchronize(s));
+    return BQ_OK;
+}
+
+BQ_API const char *bq_status_string(bq_status s) {
+    switch (s) {
+        case BQ_OK: return "BQ_OK";
+        case BQ_ERR_INVALID_ARGUMENT: return "BQ_ERR_INVALID_ARGUMENT";
+        case BQ_ERR_WORKSPACE: return "BQ_ERR_WORKSPACE";
+        case BQ_ERR_CUDA: return "BQ_ERR_CUDA";
+        case BQ_ERR_UNSUPPORTED: return "BQ_ERR_UNSUPPORTED";
+    }
+    return "BQ_ERR_UNKNOWN";
+}
+
+BQ_API const char *bq_last_error(void) { return bq::g_last_error; }
+
+BQ_API int bq_version(void) { return 100; }
+
+}

@@ -1,0 +1,222 @@
+// common.cuh — key traits, tile geometry, status words and PTX helpers shared
+// by the sm_100a kernels of libbq.so.  (The CPU oracle in oracle/ shares
+// nothing with this file.)
+#pragma once
+
+#include <cstdint>
+#include <cstddef>
+#include <cuda_runtime.h>
+
+#include "bq.h"
+
+namespace bq {
+
+// ---------------------------------------------------------------------------
+// Key traits.  `T` is the storage type moved by the passes, `K` the unsigned
+// or signed type compared.  H0: float64 is compared through the
+// order-preserving bijection  sign set -> ~bits, else bits | 2^63  (IEEE 754
+// totalOrder on non-NaN values, R9); the stored bits are never
+// changed, so decode(encode(x)) == x bit for bit.
+// ---------------------------------------------------------------------------
+struct alignas(16) Rec32 {
+    uint64_t key;
+    uint64_t p[3];
+};
+
+struct KI32 {
+    using T = int32_t;
+    using K = int32_t;
+    static constexpr bq_kind kind = BQ_I32;
+    static constexpr int W = 4;          // bytes per element
+    static constexpr bool is_record = false;
+    __host__ __device__ static K key(T v) { return v; }
+    __host__ __device__ static T from_key(K k) { return k; }
+    static constexpr K KMAX = 0x7fffffff;
+};
+
+struct KU64 {
+    using T = uint64_t;
+    using K = uint64_t;
+    static constexpr bq_kind kind = BQ_U64;
+    static constexpr int W = 8;
+    static constexpr bool is_record = false;
+    __host__ __device__ static K key(T v) { return v; }
+    __host__ __device__ static T from_key(K k) { return k; }
+    static constexpr K KMAX = ~0ull;
+};
+
+struct KF64 {
+    using T = uint64_t;                  // the double's bit pattern
+    using K = uint64_t;
+    static constexpr bq_kind kind = BQ_F64;
+    static constexpr int W = 8;
+    static constexpr bool is_record = false;
+    __host__ __device__ static K key(T b) {
+        return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+    }
+    __host__ __device__ static T from_key(K k) {
+        return (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+    }
+    static constexpr K KMAX = ~0ull;
+};
+
+struct KRec {
+    using T = Rec32;
+    using K = uint64_t;
+    static constexpr bq_kind kind = BQ_REC32;
+    static constexpr int W = 32;
+    static constexpr bool is_record = true;
+    __host__ __device__ static K key(const T &r) { return r.key; }
+    static constexpr K KMAX = ~0ull;
+};
+
+// Per-kind tuning constants.  TILE = elements per partition tile (one CTA),
+// LEAF = largest segment finished by the shared-memory leaf sort (S).
+template <class KT> struct Tune;
+template <> struct Tune<KI32> {
+    static constexpr int PART_THREADS = 256, PART_IPT = 16;   // 4096-element tiles
+    static constexpr int LEAF = 8192, LEAF_THREADS = 512;
+};
+template <> struct Tune<KU64> {
+    static constexpr int PART_THREADS = 256, PART_IPT = 8;    // 2048-element tiles
+    static constexpr int LEAF = 4096, LEAF_THREADS = 512;
+};
+template <> struct Tune<KF64> : Tune<KU64> {};
+template <> struct Tune<KRec> {
+    static constexpr int PART_THREADS = 256, PART_IPT = 4;    // 1024-record tiles
+    static constexpr int LEAF = 2048, LEAF_THREADS = 512;
+};
+
+template <class KT> constexpr int tile_elems() { return Tune<KT>::PART_THREADS * Tune<KT>::PART_IPT; }
+
+// Tiles are anchored at absolute multiples of TILE so that every interior tile
+// is 16-byte aligned: a segment [b, e) covers the tiles
+// floor(b/T) .. ceil(e/T)-1.
+__host__ __device__ inline uint32_t seg_ntiles(uint32_t b, uint32_t len, uint32_t T) {
+    if (len == 0) return 0;
+    uint64_t e = (uint64_t)b + len;
+    return (uint32_t)((e + T - 1) / T - b / T);
+}
+
+// ---------------------------------------------------------------------------
+// Segment descriptor (the GPU form of the paper's explicit stack frame,
+// P:1225-1229, plus the pivot and the tile range of the current level).
+// ---------------------------------------------------------------------------
+struct alignas(16) Seg {
+    uint64_t pivot;      // key (K) of the pivot; raw bits recovered via from_key
+    uint32_t begin;
+    uint32_t len;
+    uint32_t tile_base;  // first tile id of this segment in the level
+    uint32_t ntiles;
+    uint16_t depth;      // recursion depth (Introsort counter)
+    uint8_t parity;      // 0: data in the user buffer, 1: in scratch
+    uint8_t pad0;
+    uint32_t pad1;
+};
+static_assert(sizeof(Seg) == 32, "Seg layout");
+
+struct alignas(16) Leaf {
+    uint32_t begin;
+    uint32_t len;
+    uint32_t parity;
+    uint32_t pad;
+};
+
+// Per-level control block.  One per level, zeroed once per sort, so no
+// counter is reused within a call.
+struct alignas(64) LevelCtrl {
+    uint32_t ticket;         // partition tile tickets (ordered claiming)
+    uint32_t nseg_next;      // children appended to the next level
+    uint32_t ntiles_next;    // tiles of the next level
+    uint32_t maxtiles_next;  // largest child tile count
+    uint32_t nleaf;          // leaves appended by this level
+    uint32_t nfallback;      // depth-capped segments appended by this level
+    uint32_t pad[2];
+    unsigned long long element_passes;  // sum of partitioned lengths this level
+    unsigned long long band_elems;      // equal-band elements this level
+    unsigned long long pad2[2];
+};
+static_assert(sizeof(LevelCtrl) == 64, "LevelCtrl layout");
+
+// ---------------------------------------------------------------------------
+// Decoupled look-back status word: flag:2 | lt:31 | gt:31.
+// ---------------------------------------------------------------------------
+constexpr uint64_t ST_AGG = 1ull << 62;
+constexpr uint64_t ST_INC = 2ull << 62;
+constexpr uint64_t M31 = 0x7fffffffull;
+__host__ __device__ inline uint64_t st_pack(uint64_t flag, uint32_t lt, uint32_t gt) {
+    return flag | ((uint64_t)lt << 31) | (uint64_t)gt;
+}
+__host__ __device__ inline uint32_t st_lt(uint64_t w) { return (uint32_t)((w >> 31) & M31); }
+__host__ __device__ inline uint32_t st_gt(uint64_t w) { return (uint32_t)(w & M31); }
+__host__ __device__ inline uint32_t st_flag(uint64_t w) { return (uint32_t)(w >> 62); }
+
+__device__ __forceinline__ void st_release_u64(uint64_t *p, uint64_t v) {
+    asm volatile("st.release.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_acquire_u64(const uint64_t *p) {
+    uint64_t v;
+    asm volatile("ld.acquire.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+// Streaming 128-bit loads of read-once data (no L1 allocation).
+__device__ __forceinline__ uint4 ldg_stream(const uint4 *p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+// Plain (coherent) streaming load, for buffers written during the same kernel.
+__device__ __forceinline__ uint4 ldg_cs(const uint4 *p) { return __ldcs(p); }
+
+// Pivot sample selection (hot-path step a1; Appendix B sort_pair /
+// median_of_3): a three-comparator network with selects.
+template <class K>
+__device__ __forceinline__ void sort_pair(K &a, K &b) {
+    K lo = b < a ? b : a;
+    K hi = b < a ? a : b;
+    a = lo;
+    b = hi;
+}
+template <class K>
+__device__ __forceinline__ K median3(K a, K b, K c) {
+    sort_pair(a, b);
+    sort_pair(b, c);
+    sort_pair(a, b);
+    return b;
+}
+
+template <class KT>
+__device__ __forceinline__ typename KT::K load_key(const typename KT::T *buf, uint64_t i) {
+    return KT::key(buf[i]);
+}
+
+// Mo3 over {b, b+len/2, e-1}; ninther over b + floor(k*(len-1)/8), k=0..8.
+template <class KT>
+__device__ typename KT::K select_pivot(const typename KT::T *buf, uint32_t b, uint32_t len, int rule) {
+    using K = typename KT::K;
+    if (rule == BQ_PIVOT_NINTHER && len >= 9) {
+        K m[3];
+#pragma unroll
+        for (int g = 0; g < 3; g++) {
+            K x[3];
+#pragma unroll
+            for (int k = 0; k < 3; k++)
+                x[k] = load_key<KT>(buf, (uint64_t)b + ((uint64_t)(3 * g + k) * (len - 1)) / 8);
+            m[g] = median3(x[0], x[1], x[2]);
+        }
+        return median3(m[0], m[1], m[2]);
+    }
+    return median3(load_key<KT>(buf, b), load_key<KT>(buf, (uint64_t)b + len / 2),
+                   load_key<KT>(buf, (uint64_t)b + len - 1));
+}
+
+}  // namespace bq

@@ -1,0 +1,426 @@
+// driver.cuh — host driver of the hot path (H8): workspace layout, the
+// single-pass partition, and the breadth-first level loop that replaces the
+// paper's recursion / explicit stack.
+//
+// Level loop (one iteration per recursion level, all segments of the level at
+// once):
+//   k_map        tile -> segment map, look-back words reset
+//   k_partition  a2-a5 for every tile of every segment of the level
+//   k_post       a6 equal bands, a7 children -> next level / leaves / fallback
+//   (records) k_band2
+//   one 64-byte counter read-back per level (host decides whether to go on)
+//   k_leaf       a8 for this level's leaves
+// then a9 for depth-capped segments.  Every launch goes to the caller's stream.
+#pragma once
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "common.cuh"
+#include "fallback.cuh"
+#include "leaf.cuh"
+#include "partition.cuh"
+
+namespace bq {
+
+constexpr int MAX_LEVELS = 128;
+constexpr int POST_THREADS = 256;
+constexpr int MERGE_THREADS = 256, MERGE_IPT = 8;
+
+bq_status set_error(bq_status st, const char *fmt, ...);
+bq_status check_device();
+
+#define BQ_CK(call)                                                                     \
+    do {                                                                                \
+        cudaError_t e_ = (call);                                                        \
+        if (e_ != cudaSuccess)                                                          \
+            return ::bq::set_error(BQ_ERR_CUDA, "%s: %s (%s:%d)", #call,                \
+                                   cudaGetErrorString(e_), __FILE__, __LINE__);         \
+    } while (0)
+#define BQ_CK_LAUNCH() BQ_CK(cudaGetLastError())
+#define BQ_LAUNCHED(st) ((st).kernel_launches++)
+
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+template <class KT>
+struct Layout {
+    size_t scratch, status, tile_map, segs[2], leaves[2], fallback, ctrl, misc, total;
+    size_t max_tiles, max_segs, max_leaves, max_fb;
+};
+
+template <class KT>
+Layout<KT> make_layout(size_t n) {
+    constexpr size_t TILE = tile_elems<KT>();
+    constexpr size_t S = Tune<KT>::LEAF;
+    Layout<KT> L;
+    L.max_segs = n / (S + 1) + 2;                 // segments > S are disjoint
+    L.max_tiles = n / TILE + 2 * L.max_segs + 2;
+    L.max_leaves = 2 * L.max_segs + 2 + (n / S + 2);   // per level; also fallback chunks
+    L.max_fb = n / (S + 1) + 2;
+    size_t off = 0;
+    auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + bytes, 256); return o; };
+    L.scratch = take(n * sizeof(typename KT::T));
+    L.status = take(L.max_tiles * sizeof(uint64_t));
+    L.tile_map = take(L.max_tiles * sizeof(uint32_t));
+    L.segs[0] = take(L.max_segs * sizeof(Seg));
+    L.segs[1] = take(L.max_segs * sizeof(Seg));
+    L.leaves[0] = take(L.max_leaves * sizeof(Leaf));
+    L.leaves[1] = take(L.max_leaves * sizeof(Leaf));
+    L.fallback = take(L.max_fb * sizeof(Leaf));
+    L.ctrl = take(MAX_LEVELS * sizeof(LevelCtrl));
+    L.misc = take(256);
+    L.total = off;
+    return L;
+}
+
+template <class KT>
+struct Kernels {
+    static constexpr int NT = Tune<KT>::PART_THREADS;
+    static constexpr int IPT = Tune<KT>::PART_IPT;
+    static constexpr int LNT = Tune<KT>::LEAF_THREADS;
+};
+
+template <class KT>
+bq_status prepare_leaf_kernel() {
+    // dynamic shared memory beyond 48 KB must be opted into per kernel
+    static int done = 0;
+    if (!done) {
+        BQ_CK(cudaFuncSetAttribute(k_leaf<KT, Kernels<KT>::LNT>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)leaf_smem_bytes<KT>()));
+        done = 1;
+    }
+    return BQ_OK;
+}
+
+inline bool aligned16(const void *p) { return ((uintptr_t)p & 15) == 0; }
+
+template <class KT>
+bq_status validate(const void *data, size_t n, void *ws, size_t ws_bytes) {
+    if (n > 0x7fffffffull) return set_error(BQ_ERR_INVALID_ARGUMENT, "n = %zu exceeds 2^31-1", n);
+    if (n > 0 && data == nullptr) return set_error(BQ_ERR_INVALID_ARGUMENT, "NULL data with n > 0");
+    if (KT::is_record && !aligned16(data))
+        return set_error(BQ_ERR_INVALID_ARGUMENT, "records must be 16-byte aligned");
+    if (!KT::is_record && ((uintptr_t)data % sizeof(typename KT::T)) != 0)
+        return set_error(BQ_ERR_INVALID_ARGUMENT, "keys not aligned to their size");
+    const size_t need = make_layout<KT>(n).total;
+    if (ws == nullptr || ws_bytes < need)
+        return set_error(BQ_ERR_WORKSPACE, "workspace %zu B < required %zu B", ws ? ws_bytes : 0, need);
+    if (((uintptr_t)ws & 255) != 0) return set_error(BQ_ERR_WORKSPACE, "workspace not 256-byte aligned");
+    return check_device();
+}
+
+// One out-of-place three-way pass over a single segment [0, n).
+template <class KT>
+bq_status run_pass(const typename KT::T *src, typename KT::T *dst, typename KT::T *stage, size_t n,
+                   typename KT::K pivot_key, uint64_t *d_counts, void *ws, cudaStream_t s) {
+    using T = typename KT::T;
+    constexpr uint32_t TILE = tile_elems<KT>();
+    const Layout<KT> L = make_layout<KT>(n);
+    char *w = static_cast<char *>(ws);
+    uint64_t *status = reinterpret_cast<uint64_t *>(w + L.status);
+    LevelCtrl *ctrl = reinterpret_cast<LevelCtrl *>(w + L.ctrl);
+    if (n == 0) {
+        BQ_CK(cudaMemsetAsync(d_counts, 0, 3 * sizeof(uint64_t), s));
+        return BQ_OK;
+    }
+    const uint32_t ntiles = seg_ntiles(0, (uint32_t)n, TILE);
+    BQ_CK(cudaMemsetAsync(status, 0, ntiles * sizeof(uint64_t), s));
+    BQ_CK(cudaMemsetAsync(ctrl, 0, sizeof(LevelCtrl), s));
+    PassParams<KT> P{};
+    P.bufs[0] = const_cast<T *>(src);
+    P.bufs[1] = dst;
+    P.stage[0] = P.stage[1] = stage;
+    P.final_buf = dst;
+    P.segs = nullptr;
+    P.tile_map = nullptr;
+    P.seg0 = Seg{(uint64_t)pivot_key, 0, (uint32_t)n, 0, ntiles, 0, 0, 0, 0};
+    P.status = status;
+    P.ctrl = ctrl;
+    P.ntiles = ntiles;
+    P.aligned = aligned16(src) && aligned16(dst);
+    k_partition<KT, Kernels<KT>::NT, Kernels<KT>::IPT><<<ntiles, Kernels<KT>::NT, 0, s>>>(P);
+    BQ_CK_LAUNCH();
+    PostParams<KT> Q{};
+    Q.pass = P;
+    Q.d_counts = d_counts;
+    Q.emit_children = 0;
+    k_post<KT, POST_THREADS><<<ntiles, POST_THREADS, 0, s>>>(Q);
+    BQ_CK_LAUNCH();
+    return BQ_OK;
+}
+
+template <class KT>
+bq_status run_pivot(const typename KT::T *data, size_t n, int rule, uint64_t *key_out, void *ws,
+                    size_t ws_bytes, cudaStream_t s) {
+    if (n == 0) return set_error(BQ_ERR_INVALID_ARGUMENT, "pivot of an empty array");
+    if (rule != BQ_PIVOT_MO3 && rule != BQ_PIVOT_NINTHER)
+        return set_error(BQ_ERR_INVALID_ARGUMENT, "bad pivot rule %d", rule);
+    bq_status st = validate<KT>(data, n, ws, ws_bytes);
+    if (st != BQ_OK) return st;
+    const Layout<KT> L = make_layout<KT>(n);
+    uint64_t *misc = reinterpret_cast<uint64_t *>(static_cast<char *>(ws) + L.misc);
+    k_pivot<KT><<<1, 1, 0, s>>>(data, (uint32_t)n, rule, misc);
+    BQ_CK_LAUNCH();
+    BQ_CK(cudaMemcpyAsync(key_out, misc, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+    BQ_CK(cudaStreamSynchronize(s));
+    return BQ_OK;
+}
+
+// In-place three-way partition: keys -> scratch pass, copy back, read counts.
+template <class KT>
+bq_status run_partition_inplace(typename KT::T *data, size_t n, typename KT::K pivot_key, size_t *split,
+                                size_t *n_equal, void *ws, size_t ws_bytes, cudaStream_t s) {
+    using T = typename KT::T;
+    bq_status st = validate<KT>(data, n, ws, ws_bytes);
+    if (st != BQ_OK) return st;
+    const Layout<KT> L = make_layout<KT>(n);
+    char *w = static_cast<char *>(ws);
+    T *scratch = reinterpret_cast<T *>(w + L.scratch);
+    uint64_t *counts = reinterpret_cast<uint64_t *>(w + L.misc);
+    // records stage their equal elements in the (already consumed) input
+    st = run_pass<KT>(data, scratch, data, n, pivot_key, counts, ws, s);
+    if (st != BQ_OK) return st;
+    if (n) BQ_CK(cudaMemcpyAsync(data, scratch, n * sizeof(T), cudaMemcpyDeviceToDevice, s));
+    uint64_t h[3] = {0, 0, 0};
+    BQ_CK(cudaMemcpyAsync(h, counts, sizeof h, cudaMemcpyDeviceToHost, s));
+    BQ_CK(cudaStreamSynchronize(s));
+    if (split) *split = (size_t)h[0];
+    if (n_equal) *n_equal = (size_t)h[1];
+    return BQ_OK;
+}
+
+template <class KT>
+bq_status run_partition_pass(const typename KT::T *src, typename KT::T *dst, size_t n,
+                             typename KT::K pivot_key, uint64_t *d_counts, void *ws, size_t ws_bytes,
+                             cudaStream_t s) {
+    using T = typename KT::T;
+    bq_status st = validate<KT>(src, n, ws, ws_bytes);
+    if (st != BQ_OK) return st;
+    if (n > 0 && dst == nullptr) return set_error(BQ_ERR_INVALID_ARGUMENT, "NULL dst");
+    if (d_counts == nullptr) return set_error(BQ_ERR_INVALID_ARGUMENT, "NULL d_counts");
+    if (KT::is_record && !aligned16(dst)) return set_error(BQ_ERR_INVALID_ARGUMENT, "dst not 16-byte aligned");
+    const size_t bytes = n * sizeof(T);
+    const char *a = reinterpret_cast<const char *>(src), *c = reinterpret_cast<const char *>(dst);
+    if (n && a < c + bytes && c < a + bytes) return set_error(BQ_ERR_INVALID_ARGUMENT, "src and dst overlap");
+    const Layout<KT> L = make_layout<KT>(n);
+    T *scratch = reinterpret_cast<T *>(static_cast<char *>(ws) + L.scratch);
+    return run_pass<KT>(src, dst, scratch, n, pivot_key, d_counts, ws, s);
+}
+
+// Depth-capped segment: chunk leaf sorts + merge passes, result in the user buffer.
+template <class KT>
+bq_status run_fallback(const Leaf &f, typename KT::T *user, typename KT::T *scratch, Leaf *chunk_list,
+                       cudaStream_t s) {
+    using T = typename KT::T;
+    constexpr uint32_t S = Tune<KT>::LEAF;
+    T *bufs[2] = {user, scratch};
+    const uint32_t nch = (f.len + S - 1) / S;
+    k_chunk_leaves<<<(nch + 255) / 256, 256, 0, s>>>(chunk_list, f.begin, f.len, f.parity, S);
+    BQ_CK_LAUNCH();
+    LeafParams<KT> LP{};
+    LP.leaves = chunk_list;
+    LP.bufs[0] = user;
+    LP.bufs[1] = scratch;
+    LP.out = nullptr;
+    LP.out_inplace = 1;
+    k_leaf<KT, Kernels<KT>::LNT><<<nch, Kernels<KT>::LNT, leaf_smem_bytes<KT>(), s>>>(LP);
+    BQ_CK_LAUNCH();
+    uint32_t cur = f.parity;
+    for (uint64_t w = S; w < f.len; w *= 2) {
+        const uint64_t threads = (f.len + MERGE_IPT - 1) / MERGE_IPT;
+        const uint32_t grid = (uint32_t)((threads + MERGE_THREADS - 1) / MERGE_THREADS);
+        k_merge<KT, MERGE_THREADS, MERGE_IPT><<<grid, MERGE_THREADS, 0, s>>>(bufs[cur], bufs[cur ^ 1], f.begin,
+                                                                          f.len, (uint32_t)w);
+        BQ_CK_LAUNCH();
+        cur ^= 1;
+    }
+    if (cur != 0)
+        BQ_CK(cudaMemcpyAsync(user + f.begin, scratch + f.begin, (size_t)f.len * sizeof(T),
+                              cudaMemcpyDeviceToDevice, s));
+    return BQ_OK;
+}
+
+template <class KT>
+bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, bq_sort_stats *stats, void *ws,
+                   size_t ws_bytes, cudaStream_t s) {
+    using T = typename KT::T;
+    constexpr uint32_t TILE = tile_elems<KT>();
+    constexpr uint32_t S = Tune<KT>::LEAF;
+    using Kn = Kernels<KT>;
+    bq_sort_stats local;
+    std::memset(&local, 0, sizeof local);
+    int rule = BQ_PIVOT_NINTHER, depth_limit = -1, timing = 0;
+    if (opt) {
+        rule = opt->pivot_rule;
+        depth_limit = opt->depth_limit;
+        timing = opt->timing;
+        if (rule != BQ_PIVOT_MO3 && rule != BQ_PIVOT_NINTHER)
+            return set_error(BQ_ERR_INVALID_ARGUMENT, "bad pivot rule %d", rule);
+        if (depth_limit >= MAX_LEVELS - 2)
+            return set_error(BQ_ERR_INVALID_ARGUMENT, "depth_limit %d too large", depth_limit);
+    }
+    bq_status st = validate<KT>(data, n, ws, ws_bytes);
+    if (st != BQ_OK) return st;
+    if (n <= 1) {
+        if (stats) *stats = local;
+        return BQ_OK;
+    }
+    if (depth_limit < 0) {
+        int lg = 0;
+        for (size_t m = n; m > 1; m >>= 1) lg++;
+        depth_limit = 2 * lg + 3;   // P:295, P:1224 (2*ilogb(n)+3)
+    }
+    st = prepare_leaf_kernel<KT>();
+    if (st != BQ_OK) return st;
+
+    const Layout<KT> L = make_layout<KT>(n);
+    char *w = static_cast<char *>(ws);
+    T *user = data;
+    T *scratch = reinterpret_cast<T *>(w + L.scratch);
+    uint64_t *status = reinterpret_cast<uint64_t *>(w + L.status);
+    uint32_t *tile_map = reinterpret_cast<uint32_t *>(w + L.tile_map);
+    Seg *segs[2] = {reinterpret_cast<Seg *>(w + L.segs[0]), reinterpret_cast<Seg *>(w + L.segs[1])};
+    Leaf *leaves[2] = {reinterpret_cast<Leaf *>(w + L.leaves[0]), reinterpret_cast<Leaf *>(w + L.leaves[1])};
+    Leaf *fallback = reinterpret_cast<Leaf *>(w + L.fallback);
+    LevelCtrl *ctrl = reinterpret_cast<LevelCtrl *>(w + L.ctrl);
+    uint32_t *fb_count = reinterpret_cast<uint32_t *>(w + L.misc);
+
+    LeafParams<KT> LP{};
+    LP.bufs[0] = user;
+    LP.bufs[1] = scratch;
+    LP.out = user;
+    LP.out_inplace = 0;
+
+    if (n <= S) {
+        k_single_leaf<<<1, 1, 0, s>>>(leaves[0], (uint32_t)n);
+        BQ_CK_LAUNCH();
+        local.kernel_launches++;
+        LP.leaves = leaves[0];
+        k_leaf<KT, Kn::LNT><<<1, Kn::LNT, leaf_smem_bytes<KT>(), s>>>(LP);
+        BQ_CK_LAUNCH();
+        local.kernel_launches++;
+        local.leaves = 1;
+        if (stats) *stats = local;
+        return BQ_OK;
+    }
+
+    BQ_CK(cudaMemsetAsync(ctrl, 0, MAX_LEVELS * sizeof(LevelCtrl), s));
+    BQ_CK(cudaMemsetAsync(fb_count, 0, sizeof(uint32_t), s));
+    k_init_root<KT><<<1, 1, 0, s>>>(segs[0], user, (uint32_t)n, rule);
+    BQ_CK_LAUNCH();
+        local.kernel_launches++;
+
+    std::vector<cudaEvent_t> evs;
+    auto cleanup = [&]() { for (auto e : evs) cudaEventDestroy(e); };
+
+    uint32_t nseg = 1, ntiles = seg_ntiles(0, (uint32_t)n, TILE), maxtiles = ntiles;
+    uint32_t nfb_total = 0;
+    const int aligned = aligned16(user) && aligned16(scratch);
+    int level = 0;
+    for (; nseg > 0; level++) {
+        if (level >= MAX_LEVELS - 1) {
+            cleanup();
+            return set_error(BQ_ERR_CUDA, "level loop did not terminate");
+        }
+        Seg *cur = segs[level & 1];
+        Seg *nxt = segs[(level + 1) & 1];
+        dim3 mg(nseg, (maxtiles + 255) / 256);
+        k_map<<<mg, 256, 0, s>>>(cur, tile_map, status);
+        BQ_CK_LAUNCH();
+        local.kernel_launches++;
+
+        PassParams<KT> P{};
+        P.bufs[0] = user;
+        P.bufs[1] = scratch;
+        P.stage[0] = user;
+        P.stage[1] = scratch;
+        P.final_buf = user;
+        P.segs = cur;
+        P.tile_map = tile_map;
+        P.status = status;
+        P.ctrl = ctrl + level;
+        P.ntiles = ntiles;
+        P.aligned = aligned;
+        if (timing) {
+            cudaEvent_t e0, e1;
+            BQ_CK(cudaEventCreate(&e0));
+            evs.push_back(e0);
+            BQ_CK(cudaEventCreate(&e1));
+            evs.push_back(e1);
+            BQ_CK(cudaEventRecord(e0, s));
+        }
+        k_partition<KT, Kn::NT, Kn::IPT><<<ntiles, Kn::NT, 0, s>>>(P);
+        BQ_CK_LAUNCH();
+        local.kernel_launches++;
+        if (timing) BQ_CK(cudaEventRecord(evs.back(), s));
+        local.partition_launches++;
+
+        PostParams<KT> Q{};
+        Q.pass = P;
+        Q.next_segs = nxt;
+        Q.leaves = leaves[level & 1];
+        Q.fallback = fallback;
+        Q.fallback_count = fb_count;
+        Q.d_counts = nullptr;
+        Q.leaf_max = S;
+        Q.depth_limit = depth_limit;
+        Q.pivot_rule = rule;
+        Q.emit_children = 1;
+        k_post<KT, POST_THREADS><<<ntiles, POST_THREADS, 0, s>>>(Q);
+        BQ_CK_LAUNCH();
+        local.kernel_launches++;
+        if (KT::is_record) {
+            k_band2<KT, POST_THREADS><<<ntiles, POST_THREADS, 0, s>>>(P);
+            BQ_CK_LAUNCH();
+        local.kernel_launches++;
+        }
+        LevelCtrl hc;
+        BQ_CK(cudaMemcpyAsync(&hc, ctrl + level, sizeof hc, cudaMemcpyDeviceToHost, s));
+        BQ_CK(cudaStreamSynchronize(s));
+        if (hc.nleaf) {
+            LP.leaves = leaves[level & 1];
+            k_leaf<KT, Kn::LNT><<<hc.nleaf, Kn::LNT, leaf_smem_bytes<KT>(), s>>>(LP);
+            BQ_CK_LAUNCH();
+        local.kernel_launches++;
+        }
+        local.partitioned_segments += nseg;
+        local.element_passes += hc.element_passes;
+        local.band_elements += hc.band_elems;
+        local.leaves += hc.nleaf;
+        nfb_total += hc.nfallback;
+        nseg = hc.nseg_next;
+        ntiles = hc.ntiles_next;
+        maxtiles = hc.maxtiles_next;
+    }
+    local.levels = (uint32_t)level;
+    local.fallback_segments = nfb_total;
+
+    if (nfb_total) {
+        std::vector<Leaf> fl(nfb_total);
+        BQ_CK(cudaMemcpyAsync(fl.data(), fallback, nfb_total * sizeof(Leaf), cudaMemcpyDeviceToHost, s));
+        BQ_CK(cudaStreamSynchronize(s));
+        for (const Leaf &f : fl) {
+            st = run_fallback<KT>(f, user, scratch, leaves[0], s);
+            if (st != BQ_OK) { cleanup(); return st; }
+        }
+    }
+    local.partition_bytes = 2.0 * (double)sizeof(T) * (double)local.element_passes;
+    if (timing) {
+        BQ_CK(cudaStreamSynchronize(s));
+        double ms = 0;
+        for (size_t i = 0; i + 1 < evs.size(); i += 2) {
+            float f = 0;
+            BQ_CK(cudaEventElapsedTime(&f, evs[i], evs[i + 1]));
+            ms += f;
+        }
+        local.partition_ms = ms;
+    }
+    cleanup();
+    if (stats) *stats = local;
+    return BQ_OK;
+}
+
+}  // namespace bq

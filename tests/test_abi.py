@@ -1,0 +1,84 @@
+"""The C-ABI library (CPU, -m "not gpu"): it builds, loads, and exports every
+symbol include/bq.h declares; argument validation needs no GPU."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "bq.h")
+
+
+def _declared():
+    src = open(HEADER).read()
+    return sorted(set(re.findall(r"BQ_API\s+[\w\s\*]+?\b(bq_\w+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from tools import build
+    path = build.build_bq()
+    return ctypes.CDLL(path), path
+
+
+def test_header_declares_entry_points():
+    names = _declared()
+    for must in ["bq_workspace_bytes", "bq_partition_i32", "bq_partition_u64", "bq_partition_f64",
+                 "bq_sort_i32", "bq_sort_u64", "bq_sort_f64", "bq_sort_records", "bq_pivot_i32",
+                 "bq_partition_pass", "bq_sort_ex", "bq_sort_host", "bq_last_error"]:
+        assert must in names
+
+
+def test_exports_every_declared_symbol(lib):
+    so, path = lib
+    out = subprocess.run(["nm", "-D", "--defined-only", path], capture_output=True, text=True).stdout
+    exported = set(re.findall(r"\bT (bq_\w+)", out))
+    missing = [n for n in _declared() if n not in exported]
+    assert not missing, missing
+    for n in _declared():
+        getattr(so, n)
+    # nothing but the C-ABI is exported
+    assert all(e in _declared() for e in exported), sorted(exported - set(_declared()))
+
+
+def test_sm100a_cubin(lib):
+    _, path = lib
+    out = subprocess.run(["cuobjdump", "--list-elf", path], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_host_only_calls(lib):
+    so, _ = lib
+    so.bq_workspace_bytes.restype = ctypes.c_size_t
+    so.bq_workspace_bytes.argtypes = [ctypes.c_int, ctypes.c_size_t]
+    n = 1 << 20
+    for kind, w in [(0, 4), (1, 8), (2, 8), (3, 32)]:
+        b = so.bq_workspace_bytes(kind, n)
+        assert n * w <= b < n * w + n * w // 4 + (1 << 16)
+    so.bq_status_string.restype = ctypes.c_char_p
+    assert so.bq_status_string(0) == b"BQ_OK"
+    assert so.bq_status_string(4) == b"BQ_ERR_UNSUPPORTED"
+    assert so.bq_version() >= 100
+
+
+def test_argument_validation_without_gpu(lib):
+    so, _ = lib
+    vp, sz = ctypes.c_void_p, ctypes.c_size_t
+    so.bq_sort_i32.argtypes = [vp, sz, vp, sz, vp]
+    so.bq_last_error.restype = ctypes.c_char_p
+    assert so.bq_sort_i32(None, 1 << 31, None, 0, None) == 1          # n >= 2^31
+    assert so.bq_sort_i32(None, 10, None, 0, None) == 1               # NULL data
+    assert so.bq_sort_i32(ctypes.c_void_p(256), 10, None, 0, None) == 2   # no workspace
+    assert b"workspace" in so.bq_last_error()
+
+
+def test_product_path_never_touches_oracle():
+    pkg = os.path.join(ROOT, "paper_1604_06697_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in txt and "from oracle" not in txt, f
+                assert "liboracle" not in txt and "bq_oracle" not in txt, f

@@ -1,0 +1,282 @@
+"""Parity of the CUDA path (through the C-ABI) against the CPU oracle (-m gpu).
+
+Bars: everything here is integer / byte work, so every
+comparison is bit-exact — float64 is compared by bit pattern, records by key
+sequence plus the payload rule of SURVEY §8(c) (the order inside runs of
+equal keys is unspecified, as in Quicksort).
+"""
+import numpy as np
+import pytest
+import torch
+
+import bqgen
+import oracle
+from gpu_util import three_list, to_dev, to_host
+
+pytestmark = pytest.mark.gpu
+
+# tile T and leaf S per kind (csrc/common.cuh Tune<>)
+TILE = {"i32": 4096, "u64": 2048, "f64": 2048, "rec32": 1024}
+LEAF = {"i32": 8192, "u64": 4096, "f64": 4096, "rec32": 2048}
+
+
+def edge_sizes(kind):
+    T, S = TILE[kind], LEAF[kind]
+    return sorted({0, 1, 2, 3, 31, 32, 33, T - 1, T, T + 1, 2 * T - 1, 2 * T + 1,
+                   S - 1, S, S + 1, 3 * S + 7, (1 << 16) + 3})
+
+
+def make(kind, n, seed=1, dist="random"):
+    if kind == "i32":
+        if dist == "dups":
+            return bqgen.i32_range(n, 17, seed) - 8
+        return bqgen.i32_full(n, seed)
+    if kind == "u64":
+        if dist == "dups":
+            return bqgen.u64(n, seed) >> np.uint64(60)
+        return bqgen.u64(n, seed)
+    if kind == "f64":
+        a = bqgen.f64(n, seed) * 2.0 - 1.0
+        if dist == "dups":
+            a = np.round(a, 1)
+            a[a == 0] = 0.0
+            a[::5] = -0.0      # signed zeros: -0.0 < +0.0 (R9)
+        return a
+    if kind == "rec32":
+        return bqgen.rec32(n, seed, dup_keys=23 if dist == "dups" else None)
+    raise KeyError(kind)
+
+
+def keys_of(a):
+    return a[:, 0] if a.ndim == 2 else a
+
+
+def f64_key(a):
+    """The totalOrder rank key of doubles, for the three-list layout pin."""
+    b = a.view(np.uint64)
+    return np.where(b >> np.uint64(63), ~b, b | np.uint64(1 << 63))
+
+
+def check_sorted_equal(kind, got, inp):
+    exp = oracle.sort(inp)
+    if kind == "rec32":
+        assert np.array_equal(got[:, 0], exp[:, 0])
+        idx = got[:, 1].astype(np.int64)
+        assert np.array_equal(np.sort(idx), np.arange(len(inp)))
+        assert (got[:, 1] == got[:, 2]).all() and (got[:, 2] == got[:, 3]).all()
+        assert np.array_equal(got[:, 0], inp[idx, 0])
+    elif kind == "f64":
+        assert np.array_equal(got.view(np.uint64), exp.view(np.uint64))
+    else:
+        assert np.array_equal(got, exp)
+
+
+@pytest.fixture(scope="module")
+def B(bq):
+    assert torch.cuda.is_available()
+    return bq
+
+
+# ------------------------------------------------------------------ sort ------
+
+@pytest.mark.parametrize("kind", ["i32", "u64", "f64", "rec32"])
+@pytest.mark.parametrize("dist", ["random", "dups"])
+def test_sort_edge_sizes(B, kind, dist):
+    for n in edge_sizes(kind):
+        a = make(kind, n, seed=n + 11, dist=dist)
+        t = to_dev(a)
+        B.sort(t)
+        check_sorted_equal(kind, to_host(t, a), a)
+
+
+@pytest.mark.parametrize("kind", ["i32", "u64", "f64", "rec32"])
+@pytest.mark.parametrize("rule", [0, 1])
+def test_sort_medium(B, kind, rule):
+    for n in [100003, (1 << 20) + 17]:
+        a = make(kind, n, seed=7)
+        t = to_dev(a)
+        st = B.bq_sort_ex(t, pivot_rule=rule)
+        check_sorted_equal(kind, to_host(t, a), a)
+        assert st["levels"] >= 1 and st["fallback_segments"] == 0
+
+
+@pytest.mark.parametrize("kind", ["i32", "u64", "f64"])
+def test_sort_unaligned_pointer(B, kind):
+    for n in [5000, 70001]:
+        a = make(kind, n, seed=3)
+        t = to_dev(a, offset=1)
+        assert t.data_ptr() % 16 != 0
+        B.sort(t)
+        check_sorted_equal(kind, to_host(t, a), a)
+
+
+def test_sort_configs_reduced(B):
+    n = 1 << 20
+    for name in ["c1", "c2", "c4a", "c4b", "c5"]:
+        a = bqgen.config(name, n, seed=2)
+        t = to_dev(a)
+        B.sort(t)
+        check_sorted_equal("rec32" if name == "c5" else "i32", to_host(t, a), a)
+    for ordering in ["random", "ascending", "descending", "swapped"]:
+        a = bqgen.config("c3", n, seed=2, ordering=ordering)
+        t = to_dev(a)
+        st = B.bq_sort_ex(t)
+        got = to_host(t, a)
+        check_sorted_equal("f64", got, a)
+        if ordering != "random":
+            assert np.array_equal(got, bqgen.f64(n, 2, "ascending"))   # closed form
+
+
+def test_sort_closed_forms(B):
+    n = (1 << 20) + 3
+    a = bqgen.i32_perm(n, 5)
+    t = to_dev(a)
+    B.sort(t)
+    assert np.array_equal(t.cpu().numpy(), np.arange(n, dtype=np.int32))
+    c = bqgen.i32_const(n)
+    t = to_dev(c)
+    st = B.bq_sort_ex(t)
+    assert np.array_equal(t.cpu().numpy(), c)
+    assert st["levels"] == 1 and st["band_elements"] == n
+
+
+def test_sort_special_f64(B):
+    table = np.array([0xfff0000000000000, 0xffefffffffffffff, 0xbff0000000000000, 0x8010000000000000,
+                      0x8000000000000001, 0x8000000000000000, 0x0, 0x1, 0x0010000000000000,
+                      0x3ff0000000000000, 0x7fefffffffffffff, 0x7ff0000000000000],
+                     dtype=np.uint64).view(np.float64)
+    rng = np.random.default_rng(3)
+    for n in [12, 1000, 50000]:
+        a = table[rng.integers(0, len(table), size=n)]
+        t = to_dev(a)
+        B.sort(t)
+        got = t.cpu().numpy()
+        assert np.array_equal(got.view(np.uint64), oracle.sort(a).view(np.uint64))
+
+
+@pytest.mark.parametrize("kind", ["i32", "f64", "rec32"])
+def test_depth_cap_fallback(B, kind):
+    # a tiny Introsort limit sends segments to the merge-based fallback (a9)
+    n = 300007
+    a = make(kind, n, seed=9)
+    for limit in [0, 1, 3]:
+        t = to_dev(a)
+        st = B.bq_sort_ex(t, depth_limit=limit)
+        check_sorted_equal(kind, to_host(t, a), a)
+        assert st["fallback_segments"] >= 1
+
+
+def test_sort_deterministic(B):
+    a = make("rec32", 200000, seed=4, dist="dups")
+    outs = []
+    for _ in range(2):
+        t = to_dev(a)
+        B.sort(t)
+        outs.append(t.cpu().numpy())
+    assert np.array_equal(outs[0], outs[1])
+
+
+# ------------------------------------------------------------- partition ------
+
+def _pivots(kind, a):
+    k = keys_of(a)
+    if len(k) == 0:
+        return [0]
+    ps = [k[len(k) // 2], k.min(), k.max()]
+    if kind == "i32":
+        ps += [np.int32(0), np.int32(-(1 << 31)), np.int32((1 << 31) - 1)]
+    elif kind in ("u64", "rec32"):
+        ps += [np.uint64(0), np.uint64(1 << 63), np.uint64((1 << 64) - 1)]
+    else:
+        ps += [0.0, -0.0, 0.5, -2.0]
+    return ps
+
+
+@pytest.mark.parametrize("kind", ["i32", "u64", "f64", "rec32"])
+@pytest.mark.parametrize("dist", ["random", "dups"])
+def test_partition_vs_oracle(B, kind, dist):
+    for n in edge_sizes(kind):
+        a = make(kind, n, seed=n + 5, dist=dist)
+        for p in _pivots(kind, a):
+            t = to_dev(a)
+            pv = float(p) if kind == "f64" else int(p)
+            split, neq = B.partition(t, pv)
+            _, s_o, e_o = oracle.partition(a, pv)
+            assert (split, neq) == (s_o, e_o)
+            got = to_host(t, a)
+            if kind == "f64":
+                exp = three_list(a, f64_key(np.array([pv]))[0], key=f64_key)
+                assert np.array_equal(got.view(np.uint64), exp.view(np.uint64))
+            elif kind == "rec32":
+                exp = three_list(a, np.uint64(pv), key=lambda x: x[:, 0])
+                assert np.array_equal(got, exp)
+            else:
+                exp = three_list(a, np.array(pv, dtype=a.dtype))
+                assert np.array_equal(got, exp)
+
+
+def test_partition_config1_closed_form(B):
+    a = bqgen.config("c1")
+    t = to_dev(a)
+    p = B.bq_pivot_i32(t, B.BQ_PIVOT_MO3)
+    assert p == oracle.pivot(a, oracle.MO3)
+    split, neq = B.bq_partition_i32(t, p)
+    assert split == p and neq == 1          # permutation of 0..n-1
+    got = t.cpu().numpy()
+    assert (got[:split] < p).all() and got[split] == p and (got[split + 1:] > p).all()
+
+
+@pytest.mark.parametrize("kind", ["i32", "u64", "f64", "rec32"])
+def test_partition_pass_out_of_place(B, kind):
+    n = (1 << 18) + 77
+    a = make(kind, n, seed=21, dist="dups")
+    src = to_dev(a)
+    dst = torch.empty_like(src)
+    counts = torch.zeros(3, dtype=torch.int64, device="cuda")
+    p = keys_of(a)[n // 3]
+    pv = float(p) if kind == "f64" else int(p)
+    B.bq_partition_pass(src, dst, pv, counts)
+    torch.cuda.synchronize()
+    assert np.array_equal(to_host(src, a), a)            # src untouched
+    _, s_o, e_o = oracle.partition(a, pv)
+    c = counts.cpu().numpy()
+    assert (c[0], c[1], c[2]) == (s_o, e_o, n - s_o - e_o)
+    got = to_host(dst, a)
+    if kind == "f64":
+        exp = three_list(a, f64_key(np.array([pv]))[0], key=f64_key)
+        assert np.array_equal(got.view(np.uint64), exp.view(np.uint64))
+    elif kind == "rec32":
+        assert np.array_equal(got, three_list(a, np.uint64(pv), key=lambda x: x[:, 0]))
+    else:
+        assert np.array_equal(got, three_list(a, np.array(pv, dtype=a.dtype)))
+
+
+@pytest.mark.parametrize("kind", ["i32", "u64", "f64", "rec32"])
+def test_pivot_rules(B, kind):
+    for n in [1, 2, 3, 8, 9, 10, 1000, 123457]:
+        a = make(kind, n, seed=n)
+        t = to_dev(a)
+        for rule in [0, 1]:
+            got = B.pivot(t, rule)
+            exp = oracle.pivot(a, rule)
+            if kind == "f64":
+                assert np.array([got]).view(np.uint64)[0] == np.array([exp]).view(np.uint64)[0]
+            else:
+                assert got == exp
+
+
+def test_errors_are_loud(B):
+    t = torch.zeros(10, dtype=torch.int32, device="cuda")
+    small_ws = torch.empty(16, dtype=torch.uint8, device="cuda")
+    with pytest.raises(B.BQError):
+        B.bq_sort_i32(t, ws=small_ws)
+    with pytest.raises(B.BQError):
+        B.bq_partition_f64(torch.zeros(4, dtype=torch.float64, device="cuda"), float("nan"))
+
+
+def test_sort_host_e2e(B):
+    a = bqgen.i32_full((1 << 20) + 9, 13)
+    host = torch.from_numpy(a.copy()).pin_memory()
+    dev = torch.empty_like(host, device="cuda")
+    B.bq_sort_host(host, dev)
+    assert np.array_equal(host.numpy(), oracle.sort(a))
