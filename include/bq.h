@@ -149,6 +149,22 @@ BQ_API bq_status bq_partition_pass(bq_kind kind, const void *src, void *dst, siz
                                    const void *pivot, uint64_t *d_counts, void *ws,
                                    size_t ws_bytes, void *stream);
 
+/* Batched pass over `nseg` disjoint segments of src (one breadth-first level
+ * of the Quicksort recursion, executed at once): segment i is
+ * [begins[i], begins[i] + lens[i]) with pivot pivots[i] (HOST arrays; pivots
+ * of the kind's storage type, uint64 keys for records).  Each segment's
+ * three-way partition (layout as bq_partition_*) is written to the same range
+ * of dst; {split, n_equal, n_greater} of segment i go to d_counts[3i..3i+2]
+ * (DEVICE).  Positions of dst outside every segment are left untouched.
+ * Requires lens[i] >= 1, segments inside [0, n) and pairwise disjoint, and
+ * nseg <= n / (leaf size + 1) + 2 for the workspace of (kind, n)
+ * (BQ_ERR_INVALID_ARGUMENT otherwise).  Synchronises `stream` before
+ * returning (the host arrays are read during the call). */
+BQ_API bq_status bq_partition_segments(bq_kind kind, const void *src, void *dst, size_t n,
+                                       const uint32_t *begins, const uint32_t *lens,
+                                       const void *pivots, size_t nseg, uint64_t *d_counts,
+                                       void *ws, size_t ws_bytes, void *stream);
+
 /* ---- sort (hot-path steps a1-a9) ---------------------------------------------
  * Sorts data[0, n) ascending in place (orders above).  Enqueued on `stream`;
  * the level loop reads one small counter block back per partition level

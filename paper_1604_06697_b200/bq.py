@@ -66,6 +66,7 @@ _SIGS = {
     "bq_partition_f64": (_st, [_vp, _sz, ctypes.c_double, _psz, _psz, _vp, _sz, _vp]),
     "bq_partition_records": (_st, [_vp, _sz, ctypes.c_uint64, _psz, _psz, _vp, _sz, _vp]),
     "bq_partition_pass": (_st, [_st, _vp, _vp, _sz, _vp, _vp, _vp, _sz, _vp]),
+    "bq_partition_segments": (_st, [_st, _vp, _vp, _sz, _vp, _vp, _vp, _sz, _vp, _vp, _sz, _vp]),
     "bq_sort_i32": (_st, [_vp, _sz, _vp, _sz, _vp]),
     "bq_sort_u64": (_st, [_vp, _sz, _vp, _sz, _vp]),
     "bq_sort_f64": (_st, [_vp, _sz, _vp, _sz, _vp]),
@@ -209,6 +210,21 @@ def bq_partition_pass(src, dst, pivot, d_counts, ws=None, stream=None):
     pv = _PIVOT_CTYPE[kind](pivot)
     _check(_lib.bq_partition_pass(kind, _dev(src), _dev(dst), _n(src), ctypes.byref(pv),
                                   _dev(d_counts), w, wb, _stream(stream)))
+
+
+def bq_partition_segments(src, dst, begins, lens, pivots, d_counts, ws=None, stream=None):
+    """Batched pass over disjoint segments; begins/lens/pivots are host sequences,
+    d_counts a CUDA int64 tensor of >= 3*len(begins).  Synchronises the stream."""
+    import numpy as np
+    kind = kind_of(src)
+    w, wb = _ws(ws, kind, _n(src), src)
+    nseg = len(begins)
+    b = np.ascontiguousarray(np.asarray(begins, dtype=np.uint32))
+    ln = np.ascontiguousarray(np.asarray(lens, dtype=np.uint32))
+    pdt = {BQ_I32: np.int32, BQ_U64: np.uint64, BQ_F64: np.float64, BQ_REC32: np.uint64}[kind]
+    pv = np.ascontiguousarray(np.asarray(pivots).astype(pdt))
+    _check(_lib.bq_partition_segments(kind, _dev(src), _dev(dst), _n(src), b.ctypes.data, ln.ctypes.data,
+                                      pv.ctypes.data, nseg, _dev(d_counts), w, wb, _stream(stream)))
 
 
 def _sort(name, t, ws, stream):

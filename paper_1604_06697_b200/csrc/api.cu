@@ -73,6 +73,26 @@ BQ_API bq_status bq_partition_pass(bq_kind kind, const void *src, void *dst, siz
     return bq::set_error(BQ_ERR_INVALID_ARGUMENT, "bad kind %d", (int)kind);
 }
 
+BQ_API bq_status bq_partition_segments(bq_kind kind, const void *src, void *dst, size_t n, const uint32_t *begins,
+                                       const uint32_t *lens, const void *pivots, size_t nseg, uint64_t *d_counts,
+                                       void *ws, size_t ws_bytes, void *stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (nseg && pivots == nullptr) return bq::set_error(BQ_ERR_INVALID_ARGUMENT, "NULL pivots");
+    if (kind == BQ_F64)
+        for (size_t i = 0; i < nseg; i++) {
+            double d;
+            std::memcpy(&d, static_cast<const char *>(pivots) + 8 * i, 8);
+            if (d != d) return bq::set_error(BQ_ERR_INVALID_ARGUMENT, "NaN pivot");
+        }
+    switch (kind) {
+        case BQ_I32: return segs_i32(src, dst, n, begins, lens, pivots, nseg, d_counts, ws, ws_bytes, s);
+        case BQ_U64: return segs_u64(src, dst, n, begins, lens, pivots, nseg, d_counts, ws, ws_bytes, s);
+        case BQ_F64: return segs_f64(src, dst, n, begins, lens, pivots, nseg, d_counts, ws, ws_bytes, s);
+        case BQ_REC32: return segs_rec(src, dst, n, begins, lens, pivots, nseg, d_counts, ws, ws_bytes, s);
+    }
+    return bq::set_error(BQ_ERR_INVALID_ARGUMENT, "bad kind %d", (int)kind);
+}
+
 BQ_API bq_status bq_sort_ex(bq_kind kind, void *data, size_t n, const bq_sort_options *opt, bq_sort_stats *stats,
                             void *ws, size_t ws_bytes, void *stream) {
     cudaStream_t s = (cudaStream_t)stream;

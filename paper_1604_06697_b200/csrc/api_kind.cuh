@@ -15,6 +15,9 @@
                          void *ws, size_t wsb, cudaStream_t s);                                     \
     bq_status pass_##SUF(const void *src, void *dst, size_t n, const void *pivot, uint64_t *dc,     \
                          void *ws, size_t wsb, cudaStream_t s);                                     \
+    bq_status segs_##SUF(const void *src, void *dst, size_t n, const uint32_t *begins,              \
+                         const uint32_t *lens, const void *pivots, size_t nseg, uint64_t *dc,       \
+                         void *ws, size_t wsb, cudaStream_t s);                                     \
     }                                                                                               \
     }
 
@@ -37,6 +40,18 @@ BQ_DETAIL_DECLS(rec)
         std::memcpy(&pv, pivot, sizeof pv);                                                         \
         return run_partition_pass<KT>(static_cast<const KT::T *>(src), static_cast<KT::T *>(dst),  \
                                       n, KT::key(pv), dc, ws, wsb, s);                              \
+    }                                                                                               \
+    bq_status segs_##SUF(const void *src, void *dst, size_t n, const uint32_t *begins,              \
+                         const uint32_t *lens, const void *pivots, size_t nseg, uint64_t *dc,       \
+                         void *ws, size_t wsb, cudaStream_t s) {                                    \
+        std::vector<KT::K> keys(nseg);                                                             \
+        for (size_t i = 0; i < nseg; i++) {                                                         \
+            KT::T pv;                                                                               \
+            std::memcpy(&pv, static_cast<const char *>(pivots) + i * sizeof(KT::T), sizeof pv);    \
+            keys[i] = KT::key(pv);                                                                  \
+        }                                                                                           \
+        return run_partition_segments<KT>(static_cast<const KT::T *>(src), static_cast<KT::T *>(dst), \
+                                          n, begins, lens, keys.data(), nseg, dc, ws, wsb, s);      \
     }                                                                                               \
     }                                                                                               \
     }

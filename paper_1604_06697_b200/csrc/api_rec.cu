@@ -16,6 +16,11 @@ bq_status pass_rec(const void *src, void *dst, size_t n, const void *pivot, uint
     return run_partition_pass<KRec>(static_cast<const Rec32 *>(src), static_cast<Rec32 *>(dst), n, pk, dc, ws,
                                     wsb, s);
 }
+bq_status segs_rec(const void *src, void *dst, size_t n, const uint32_t *begins, const uint32_t *lens,
+                   const void *pivots, size_t nseg, uint64_t *dc, void *ws, size_t wsb, cudaStream_t s) {
+    return run_partition_segments<KRec>(static_cast<const Rec32 *>(src), static_cast<Rec32 *>(dst), n, begins, lens,
+                                        static_cast<const uint64_t *>(pivots), nseg, dc, ws, wsb, s);
+}
 }  // namespace detail
 }  // namespace bq
 

@@ -72,18 +72,21 @@ struct KRec {
 
 // Per-kind tuning constants.  TILE = elements per partition tile (one CTA),
 // LEAF = largest segment finished by the shared-memory leaf sort (S).
+// PART_THREADS = consumer threads of the partition kernel (one more producer
+// warp is added), PART_IPT = elements per consumer thread, PART_STAGES = TMA
+// load pipeline depth, PART_MINB = CTAs per SM the register budget targets.
 template <class KT> struct Tune;
 template <> struct Tune<KI32> {
-    static constexpr int PART_THREADS = 256, PART_IPT = 16;   // 4096-element tiles
+    static constexpr int PART_THREADS = 256, PART_IPT = 16, PART_STAGES = 2, PART_MINB = 3;  // 16 KB tiles
     static constexpr int LEAF = 8192, LEAF_THREADS = 512;
 };
 template <> struct Tune<KU64> {
-    static constexpr int PART_THREADS = 256, PART_IPT = 8;    // 2048-element tiles
+    static constexpr int PART_THREADS = 256, PART_IPT = 8, PART_STAGES = 2, PART_MINB = 4;   // 16 KB tiles
     static constexpr int LEAF = 4096, LEAF_THREADS = 512;
 };
 template <> struct Tune<KF64> : Tune<KU64> {};
 template <> struct Tune<KRec> {
-    static constexpr int PART_THREADS = 256, PART_IPT = 4;    // 1024-record tiles
+    static constexpr int PART_THREADS = 256, PART_IPT = 2, PART_STAGES = 2, PART_MINB = 3;   // 16 KB tiles
     static constexpr int LEAF = 2048, LEAF_THREADS = 512;
 };
 
@@ -151,13 +154,68 @@ __host__ __device__ inline uint32_t st_lt(uint64_t w) { return (uint32_t)((w >> 
 __host__ __device__ inline uint32_t st_gt(uint64_t w) { return (uint32_t)(w & M31); }
 __host__ __device__ inline uint32_t st_flag(uint64_t w) { return (uint32_t)(w >> 62); }
 
-__device__ __forceinline__ void st_release_u64(uint64_t *p, uint64_t v) {
-    asm volatile("st.release.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+// Status words carry self-contained counts, so publishing and polling need no
+// acquire/release ordering: relaxed gpu-scope 64-bit accesses (single-copy
+// atomic) avoid the L1 invalidation (CCTL.IVALL) an acquire load costs per poll.
+// A tile's word is published twice by different threads (aggregate by the
+// producer warp, inclusive by the consumers) and the two stores are not
+// ordered in L2, so both are published with atom.max: ST_INC > ST_AGG in the
+// flag bits, so the inclusive word wins whatever the arrival order.
+__device__ __forceinline__ void st_publish_u64(uint64_t *p, uint64_t v) {
+    atomicMax(reinterpret_cast<unsigned long long *>(p), (unsigned long long)v);
 }
-__device__ __forceinline__ uint64_t ld_acquire_u64(const uint64_t *p) {
+__device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t *p) {
     uint64_t v;
-    asm volatile("ld.acquire.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
+}
+
+// ---- mbarrier / bulk-copy (TMA) helpers (sm_90+ PTX, used on sm_100a) --------
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// 1D bulk copy global -> shared, completion counted on an mbarrier (UBLKCP).
+__device__ __forceinline__ void tma_load_1d(void *smem_dst, const void *gsrc, uint32_t bytes, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(smem_dst)),
+        "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+// 1D bulk copy shared -> global (bulk-group completion).
+__device__ __forceinline__ void tma_store_1d(void *gdst, const void *smem_src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
+                 "r"(smem_u32(smem_src)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+// make generic-proxy shared-memory writes visible to the async (TMA) proxy
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
 __device__ __forceinline__ uint32_t lanemask_lt() {

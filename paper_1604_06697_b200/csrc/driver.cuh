@@ -13,6 +13,8 @@
 // then a9 for depth-capped segments.  Every launch goes to the caller's stream.
 #pragma once
 
+#include <algorithm>
+#include <cstdlib>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -79,8 +81,32 @@ template <class KT>
 struct Kernels {
     static constexpr int NT = Tune<KT>::PART_THREADS;
     static constexpr int IPT = Tune<KT>::PART_IPT;
+    static constexpr int STAGES = Tune<KT>::PART_STAGES;
+    static constexpr int MINB = Tune<KT>::PART_MINB;
     static constexpr int LNT = Tune<KT>::LEAF_THREADS;
 };
+
+// Persistent launch of the partition kernel: min(ntiles, resident CTAs).
+template <class KT>
+bq_status launch_partition(const PassParams<KT> &P, cudaStream_t s) {
+    using Kn = Kernels<KT>;
+    auto kern = k_partition<KT, Kn::NT, Kn::IPT, Kn::STAGES, Kn::MINB>;
+    constexpr int smem = part_smem_bytes<KT>();
+    static int cap = 0;
+    if (cap == 0) {
+        BQ_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        int nb = 0, dev = 0, sms = 0;
+        BQ_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, Kn::NT + 32, smem));
+        BQ_CK(cudaGetDevice(&dev));
+        BQ_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        if (nb < 1) return set_error(BQ_ERR_CUDA, "partition kernel does not fit on an SM");
+        cap = nb * sms;
+    }
+    uint32_t grid = P.ntiles < (uint32_t)cap ? P.ntiles : (uint32_t)cap;
+    kern<<<grid, Kn::NT + 32, smem, s>>>(P);
+    BQ_CK_LAUNCH();
+    return BQ_OK;
+}
 
 template <class KT>
 bq_status prepare_leaf_kernel() {
@@ -140,9 +166,10 @@ bq_status run_pass(const typename KT::T *src, typename KT::T *dst, typename KT::
     P.status = status;
     P.ctrl = ctrl;
     P.ntiles = ntiles;
+    P.n_total = n;
     P.aligned = aligned16(src) && aligned16(dst);
-    k_partition<KT, Kernels<KT>::NT, Kernels<KT>::IPT><<<ntiles, Kernels<KT>::NT, 0, s>>>(P);
-    BQ_CK_LAUNCH();
+    bq_status st = launch_partition<KT>(P, s);
+    if (st != BQ_OK) return st;
     PostParams<KT> Q{};
     Q.pass = P;
     Q.d_counts = d_counts;
@@ -208,6 +235,76 @@ bq_status run_partition_pass(const typename KT::T *src, typename KT::T *dst, siz
     const Layout<KT> L = make_layout<KT>(n);
     T *scratch = reinterpret_cast<T *>(static_cast<char *>(ws) + L.scratch);
     return run_pass<KT>(src, dst, scratch, n, pivot_key, d_counts, ws, s);
+}
+
+// Batched pass over caller-given disjoint segments (bq_partition_segments).
+template <class KT>
+bq_status run_partition_segments(const typename KT::T *src, typename KT::T *dst, size_t n, const uint32_t *begins,
+                                 const uint32_t *lens, const typename KT::K *pivot_keys, size_t nseg,
+                                 uint64_t *d_counts, void *ws, size_t ws_bytes, cudaStream_t s) {
+    using T = typename KT::T;
+    constexpr uint32_t TILE = tile_elems<KT>();
+    bq_status st = validate<KT>(src, n, ws, ws_bytes);
+    if (st != BQ_OK) return st;
+    if (nseg == 0) return BQ_OK;
+    if (!dst || !begins || !lens || !pivot_keys || !d_counts)
+        return set_error(BQ_ERR_INVALID_ARGUMENT, "NULL argument");
+    if (KT::is_record && !aligned16(dst)) return set_error(BQ_ERR_INVALID_ARGUMENT, "dst not 16-byte aligned");
+    const Layout<KT> L = make_layout<KT>(n);
+    if (nseg > L.max_segs) return set_error(BQ_ERR_INVALID_ARGUMENT, "nseg %zu > %zu", nseg, L.max_segs);
+    std::vector<Seg> hs(nseg);
+    std::vector<std::pair<uint64_t, uint64_t>> iv(nseg);
+    uint64_t tiles = 0;
+    uint32_t maxtiles = 0;
+    for (size_t i = 0; i < nseg; i++) {
+        if (lens[i] == 0 || (uint64_t)begins[i] + lens[i] > n)
+            return set_error(BQ_ERR_INVALID_ARGUMENT, "segment %zu out of range or empty", i);
+        const uint32_t nt = seg_ntiles(begins[i], lens[i], TILE);
+        hs[i] = Seg{(uint64_t)pivot_keys[i], begins[i], lens[i], (uint32_t)tiles, nt, 0, 0, 0, 0};
+        tiles += nt;
+        maxtiles = nt > maxtiles ? nt : maxtiles;
+        iv[i] = {begins[i], (uint64_t)begins[i] + lens[i]};
+    }
+    if (tiles > L.max_tiles) return set_error(BQ_ERR_INVALID_ARGUMENT, "segments need too many tiles");
+    std::sort(iv.begin(), iv.end());
+    for (size_t i = 1; i < nseg; i++)
+        if (iv[i].first < iv[i - 1].second) return set_error(BQ_ERR_INVALID_ARGUMENT, "segments overlap");
+    const size_t bytes = n * sizeof(T);
+    const char *a = reinterpret_cast<const char *>(src), *c = reinterpret_cast<const char *>(dst);
+    if (a < c + bytes && c < a + bytes) return set_error(BQ_ERR_INVALID_ARGUMENT, "src and dst overlap");
+
+    char *w = static_cast<char *>(ws);
+    T *scratch = reinterpret_cast<T *>(w + L.scratch);
+    uint64_t *status = reinterpret_cast<uint64_t *>(w + L.status);
+    uint32_t *tile_map = reinterpret_cast<uint32_t *>(w + L.tile_map);
+    Seg *segs = reinterpret_cast<Seg *>(w + L.segs[0]);
+    LevelCtrl *ctrl = reinterpret_cast<LevelCtrl *>(w + L.ctrl);
+    BQ_CK(cudaMemcpyAsync(segs, hs.data(), nseg * sizeof(Seg), cudaMemcpyHostToDevice, s));
+    BQ_CK(cudaMemsetAsync(ctrl, 0, sizeof(LevelCtrl), s));
+    k_map<<<dim3((uint32_t)nseg, (maxtiles + 255) / 256), 256, 0, s>>>(segs, tile_map, status);
+    BQ_CK_LAUNCH();
+    PassParams<KT> P{};
+    P.bufs[0] = const_cast<T *>(src);
+    P.bufs[1] = dst;
+    P.stage[0] = P.stage[1] = scratch;
+    P.final_buf = dst;
+    P.segs = segs;
+    P.tile_map = tile_map;
+    P.status = status;
+    P.ctrl = ctrl;
+    P.ntiles = (uint32_t)tiles;
+    P.n_total = n;
+    P.aligned = aligned16(src) && aligned16(dst);
+    st = launch_partition<KT>(P, s);
+    if (st != BQ_OK) return st;
+    PostParams<KT> Q{};
+    Q.pass = P;
+    Q.d_counts = d_counts;
+    Q.emit_children = 0;
+    k_post<KT, POST_THREADS><<<(uint32_t)tiles, POST_THREADS, 0, s>>>(Q);
+    BQ_CK_LAUNCH();
+    BQ_CK(cudaStreamSynchronize(s));
+    return BQ_OK;
 }
 
 // Depth-capped segment: chunk leaf sorts + merge passes, result in the user buffer.
@@ -343,6 +440,7 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
         P.status = status;
         P.ctrl = ctrl + level;
         P.ntiles = ntiles;
+        P.n_total = n;
         P.aligned = aligned;
         if (timing) {
             cudaEvent_t e0, e1;
@@ -352,8 +450,8 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
             evs.push_back(e1);
             BQ_CK(cudaEventRecord(e0, s));
         }
-        k_partition<KT, Kn::NT, Kn::IPT><<<ntiles, Kn::NT, 0, s>>>(P);
-        BQ_CK_LAUNCH();
+        st = launch_partition<KT>(P, s);
+        if (st != BQ_OK) { cleanup(); return st; }
         local.kernel_launches++;
         if (timing) BQ_CK(cudaEventRecord(evs.back(), s));
         local.partition_launches++;

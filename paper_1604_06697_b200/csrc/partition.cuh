@@ -39,258 +39,15 @@ struct PassParams {
     uint64_t *status;      // one look-back word per tile, zeroed before the pass
     LevelCtrl *ctrl;       // ticket + counters of this level
     uint32_t ntiles;
-    int aligned;           // both data buffers 16-byte aligned -> vector loads
+    uint64_t n_total;      // length of each data buffer (bounds the TMA reads)
+    int aligned;           // both data buffers 16-byte aligned -> TMA bulk copies
 };
 
-// Swizzled staging index: items of consecutive lanes land in distinct banks
-// for 4- and 8-byte keys.
-template <class T>
-__device__ __forceinline__ uint32_t stage_phys(uint32_t s) {
-    if constexpr (sizeof(T) == 4) return s ^ ((s >> 5) & 3);
-    else if constexpr (sizeof(T) == 8) return s ^ ((s >> 4) & 1);
-    else return s;
-}
+}  // namespace bq
 
-template <class T>
-__device__ __forceinline__ void store_stream(T *p, const T &v) {
-    if constexpr (sizeof(T) == 32) {
-        const uint4 *q = reinterpret_cast<const uint4 *>(&v);
-        __stcs(reinterpret_cast<uint4 *>(p), q[0]);
-        __stcs(reinterpret_cast<uint4 *>(p) + 1, q[1]);
-    } else {
-        __stcs(p, v);
-    }
-}
+#include "partition_kernel.cuh"
 
-template <class KT, int NT, int IPT>
-__global__ void __launch_bounds__(NT) k_partition(PassParams<KT> P) {
-    using T = typename KT::T;
-    using K = typename KT::K;
-    constexpr bool REC = KT::is_record;
-    constexpr int VEC = REC ? 1 : (int)(16 / sizeof(T));
-    constexpr int V = IPT / VEC;
-    constexpr int NW = NT / 32;
-    constexpr int TILE = NT * IPT;
-    constexpr int NE = V * NW;                 // warp chunks per tile
-    constexpr int PER = (NE + 31) / 32;
-    static_assert(IPT % VEC == 0, "IPT must be a multiple of the vector width");
-    static_assert(IPT <= 32, "bitmasks hold 32 items");
-
-    __shared__ __align__(16) T s_stage[TILE];
-    __shared__ uint32_t s_wl[NE], s_wg[NE], s_we[REC ? NE : 1];
-    __shared__ uint32_t s_tile, s_tl, s_tg, s_te, s_lp, s_gp;
-
-    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-
-    // ordered tile claiming: every look-back predecessor is already running
-    if (tid == 0) s_tile = atomicAdd(&P.ctrl->ticket, 1u);
-    __syncthreads();
-    const uint32_t t = s_tile;
-    const Seg sg = P.tile_map ? P.segs[P.tile_map[t]] : P.seg0;
-    const uint32_t k = t - sg.tile_base;
-    const uint64_t b = sg.begin, e = b + sg.len;
-    const uint64_t tbeg = (b / TILE) * TILE + (uint64_t)k * TILE;
-    const uint64_t lo = tbeg > b ? tbeg : b;
-    const uint64_t hi = (tbeg + TILE) < e ? (tbeg + TILE) : e;
-    const T *src = sg.parity ? P.bufs[1] : P.bufs[0];
-    T *dst = sg.parity ? P.bufs[0] : P.bufs[1];
-    const K pk = (K)sg.pivot;
-
-    // ---- a2: load ------------------------------------------------------------
-    T it[V][VEC];
-    uint32_t lt_bits = 0, gt_bits = 0, eq_bits = 0;
-#pragma unroll
-    for (int v = 0; v < V; v++) {
-        const uint64_t i0 = tbeg + (uint64_t)(v * NT + tid) * VEC;
-        if (P.aligned && i0 >= lo && i0 + VEC <= hi) {
-            if constexpr (REC) {
-                const uint4 *q = reinterpret_cast<const uint4 *>(src + i0);
-                uint4 *d = reinterpret_cast<uint4 *>(&it[v][0]);
-                d[0] = ldg_cs(q);
-                d[1] = ldg_cs(q + 1);
-            } else {
-                uint4 r = ldg_stream(reinterpret_cast<const uint4 *>(src + i0));
-                const T *rv = reinterpret_cast<const T *>(&r);
-#pragma unroll
-                for (int c = 0; c < VEC; c++) it[v][c] = rv[c];
-            }
-#pragma unroll
-            for (int c = 0; c < VEC; c++) {
-                const K kk = KT::key(it[v][c]);
-                const int bit = v * VEC + c;
-                lt_bits |= (uint32_t)(kk < pk) << bit;
-                gt_bits |= (uint32_t)(pk < kk) << bit;
-                if constexpr (REC) eq_bits |= (uint32_t)(!(kk < pk) && !(pk < kk)) << bit;
-            }
-        } else {
-#pragma unroll
-            for (int c = 0; c < VEC; c++) {
-                const uint64_t i = i0 + c;
-                const bool valid = i >= lo && i < hi;
-                if (valid) it[v][c] = src[i];
-                const K kk = valid ? KT::key(it[v][c]) : pk;
-                const int bit = v * VEC + c;
-                lt_bits |= (uint32_t)(valid && kk < pk) << bit;
-                gt_bits |= (uint32_t)(valid && pk < kk) << bit;
-                if constexpr (REC) eq_bits |= (uint32_t)(valid && !(kk < pk) && !(pk < kk)) << bit;
-            }
-        }
-    }
-
-    // ---- a3: offsets via ballot / popc ------------------------------------------
-    const uint32_t lm = lanemask_lt();
-    uint32_t rk_l[V][VEC], rk_g[V][VEC], rk_e[REC ? V : 1][VEC];
-#pragma unroll
-    for (int v = 0; v < V; v++) {
-        uint32_t cl = 0, cg = 0, ce = 0, tl = 0, tg = 0, te = 0;
-#pragma unroll
-        for (int c = 0; c < VEC; c++) {
-            const int bit = v * VEC + c;
-            const uint32_t ml = __ballot_sync(0xffffffffu, (lt_bits >> bit) & 1);
-            const uint32_t mg = __ballot_sync(0xffffffffu, (gt_bits >> bit) & 1);
-            cl += __popc(ml & lm);
-            cg += __popc(mg & lm);
-            tl += __popc(ml);
-            tg += __popc(mg);
-            if constexpr (REC) {
-                const uint32_t me = __ballot_sync(0xffffffffu, (eq_bits >> bit) & 1);
-                ce += __popc(me & lm);
-                te += __popc(me);
-            }
-        }
-#pragma unroll
-        for (int c = 0; c < VEC; c++) {
-            const int bit = v * VEC + c;
-            rk_l[v][c] = cl;
-            cl += (lt_bits >> bit) & 1;
-            rk_g[v][c] = cg;
-            cg += (gt_bits >> bit) & 1;
-            if constexpr (REC) {
-                rk_e[v][c] = ce;
-                ce += (eq_bits >> bit) & 1;
-            }
-        }
-        if (lane == 0) {
-            s_wl[v * NW + warp] = tl;
-            s_wg[v * NW + warp] = tg;
-            if constexpr (REC) s_we[v * NW + warp] = te;
-        }
-    }
-    __syncthreads();
-
-    // ---- warp 0: scan warp-chunk counts, then a4 look-back ------------------------
-    if (warp == 0) {
-        uint32_t al[PER], ag[PER], ae[PER];
-        uint32_t sl = 0, sgt = 0, se = 0;
-#pragma unroll
-        for (int i = 0; i < PER; i++) {
-            const int idx = lane * PER + i;
-            const uint32_t xl = idx < NE ? s_wl[idx] : 0;
-            const uint32_t xg = idx < NE ? s_wg[idx] : 0;
-            uint32_t xe = 0;
-            if constexpr (REC) xe = idx < NE ? s_we[idx] : 0;
-            al[i] = sl; ag[i] = sgt; ae[i] = se;
-            sl += xl; sgt += xg; se += xe;
-        }
-        uint32_t il = sl, ig = sgt, ie = se;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const uint32_t ol = __shfl_up_sync(0xffffffffu, il, d);
-            const uint32_t og = __shfl_up_sync(0xffffffffu, ig, d);
-            const uint32_t oe = __shfl_up_sync(0xffffffffu, ie, d);
-            if (lane >= (uint32_t)d) { il += ol; ig += og; ie += oe; }
-        }
-#pragma unroll
-        for (int i = 0; i < PER; i++) {
-            const int idx = lane * PER + i;
-            if (idx < NE) {
-                s_wl[idx] = il - sl + al[i];
-                s_wg[idx] = ig - sgt + ag[i];
-                if constexpr (REC) s_we[idx] = ie - se + ae[i];
-            }
-        }
-        const uint32_t TL = __shfl_sync(0xffffffffu, il, 31);
-        const uint32_t TG = __shfl_sync(0xffffffffu, ig, 31);
-        const uint32_t TE = __shfl_sync(0xffffffffu, ie, 31);
-
-        uint64_t *st = P.status;
-        uint32_t accl = 0, accg = 0;
-        if (k == 0) {
-            if (lane == 0) st_release_u64(st + t, st_pack(ST_INC, TL, TG));
-        } else {
-            if (lane == 0) st_release_u64(st + t, st_pack(ST_AGG, TL, TG));
-            int64_t pred = (int64_t)t - 1;
-            const int64_t first_tile = sg.tile_base;
-            while (true) {
-                const int64_t idx = pred - (int64_t)lane;
-                uint64_t w;
-                if (idx >= first_tile) {
-                    do { w = ld_acquire_u64(st + idx); } while (st_flag(w) == 0);
-                } else {
-                    w = ST_INC;   // before the segment start: inclusive zero
-                }
-                const uint32_t inc = __ballot_sync(0xffffffffu, st_flag(w) == 2);
-                const int first = inc ? (__ffs(inc) - 1) : 31;
-                uint32_t l = (int)lane <= first ? st_lt(w) : 0;
-                uint32_t g = (int)lane <= first ? st_gt(w) : 0;
-#pragma unroll
-                for (int d = 16; d > 0; d >>= 1) {
-                    l += __shfl_xor_sync(0xffffffffu, l, d);
-                    g += __shfl_xor_sync(0xffffffffu, g, d);
-                }
-                accl += l;
-                accg += g;
-                if (inc) break;
-                pred -= 32;
-            }
-            if (lane == 0) st_release_u64(st + t, st_pack(ST_INC, accl + TL, accg + TG));
-        }
-        if (lane == 0) {
-            s_tl = TL; s_tg = TG; s_te = TE;
-            s_lp = accl; s_gp = accg;
-        }
-    }
-    __syncthreads();
-
-    // ---- a5: stage in shared memory as [< | > | =] ---------------------------------
-    const uint32_t TL = s_tl, TG = s_tg;
-    const uint32_t TE = REC ? s_te : 0;
-#pragma unroll
-    for (int v = 0; v < V; v++) {
-        const uint32_t bl = s_wl[v * NW + warp];
-        const uint32_t bg = TL + s_wg[v * NW + warp];
-        uint32_t be = 0;
-        if constexpr (REC) be = TL + TG + s_we[v * NW + warp];
-#pragma unroll
-        for (int c = 0; c < VEC; c++) {
-            const int bit = v * VEC + c;
-            if ((lt_bits >> bit) & 1) s_stage[stage_phys<T>(bl + rk_l[v][c])] = it[v][c];
-            else if ((gt_bits >> bit) & 1) s_stage[stage_phys<T>(bg + rk_g[v][c])] = it[v][c];
-            else if constexpr (REC) {
-                if ((eq_bits >> bit) & 1) s_stage[stage_phys<T>(be + rk_e[v][c])] = it[v][c];
-            }
-        }
-    }
-    __syncthreads();
-
-    // ---- coalesced write-out ----------------------------------------------------
-    const uint64_t lp = s_lp, gp = s_gp;
-    const uint32_t cnt = TL + TG + TE;
-    const uint64_t lbase = b + lp;
-    const uint64_t gtop = e - 1 - gp;
-    T *estage = nullptr;
-    uint64_t ebase = 0;
-    if constexpr (REC) {
-        estage = sg.parity ? P.stage[1] : P.stage[0];
-        ebase = b + ((lo - b) - lp - gp);   // + Eprefix
-    }
-    for (uint32_t s = tid; s < cnt; s += NT) {
-        const T x = s_stage[stage_phys<T>(s)];
-        if (s < TL) store_stream(dst + lbase + s, x);
-        else if (s < TL + TG) store_stream(dst + (gtop - (s - TL)), x);
-        else if constexpr (REC) store_stream(estage + ebase + (s - TL - TG), x);
-    }
-}
+namespace bq {
 
 // ---------------------------------------------------------------------------
 // Level bookkeeping.
@@ -346,9 +103,10 @@ __global__ void __launch_bounds__(NT) k_post(PostParams<KT> Q) {
     if (k != 0 || threadIdx.x != 0) return;
 
     if (Q.d_counts) {
-        Q.d_counts[0] = L;
-        Q.d_counts[1] = E;
-        Q.d_counts[2] = G;
+        const uint32_t si = P.tile_map ? P.tile_map[t] : 0;
+        Q.d_counts[3 * si + 0] = L;
+        Q.d_counts[3 * si + 1] = E;
+        Q.d_counts[3 * si + 2] = G;
     }
     if (!Q.emit_children) return;
     LevelCtrl *C = P.ctrl;

@@ -252,6 +252,75 @@ def test_partition_pass_out_of_place(B, kind):
 
 
 @pytest.mark.parametrize("kind", ["i32", "u64", "f64", "rec32"])
+def test_partition_pass_persistent_reuse(B, kind):
+    # enough tiles that every persistent CTA cycles its TMA ring many times
+    n = ((1 << 23) if kind != "rec32" else (1 << 21)) + 13
+    a = make(kind, n, seed=31)
+    src = to_dev(a)
+    dst = torch.empty_like(src)
+    counts = torch.zeros(3, dtype=torch.int64, device="cuda")
+    p = keys_of(a)[7]
+    pv = float(p) if kind == "f64" else int(p)
+    B.bq_partition_pass(src, dst, pv, counts)
+    got = to_host(dst, a)
+    if kind == "f64":
+        exp = three_list(a, f64_key(np.array([pv]))[0], key=f64_key)
+        assert np.array_equal(got.view(np.uint64), exp.view(np.uint64))
+    elif kind == "rec32":
+        assert np.array_equal(got, three_list(a, np.uint64(pv), key=lambda x: x[:, 0]))
+    else:
+        assert np.array_equal(got, three_list(a, np.array(pv, dtype=a.dtype)))
+
+
+@pytest.mark.parametrize("kind", ["i32", "u64", "f64", "rec32"])
+@pytest.mark.parametrize("nseg", [2, 8, 37, 100])
+def test_partition_segments(B, kind, nseg):
+    """One breadth-first level of many segments at once (segment boundaries
+    inside tiles, every alignment), each against its own three-list layout."""
+    rng = np.random.default_rng(nseg)
+    n = (1 << 22) + 5 if kind != "rec32" else (1 << 20) + 5
+    a = make(kind, n, seed=nseg, dist="dups" if nseg % 2 else "random")
+    cuts = np.sort(rng.choice(np.arange(1, n), size=nseg, replace=False))
+    bounds = np.concatenate([[0], cuts, [n]])
+    keep = rng.random(nseg + 1) < 0.8            # leave some gaps uncovered
+    begins = bounds[:-1][keep]
+    lens = np.diff(bounds)[keep]
+    k = keys_of(a)
+    pivots = [k[b + rng.integers(0, l)] for b, l in zip(begins, lens)]
+    src = to_dev(a)
+    dst = torch.zeros_like(src)
+    counts = torch.zeros(3 * len(begins), dtype=torch.int64, device="cuda")
+    B.bq_partition_segments(src, dst, begins, lens, pivots, counts)
+    got = to_host(dst, a)
+    c = counts.cpu().numpy().reshape(-1, 3)
+    for i, (b, l, p) in enumerate(zip(begins, lens, pivots)):
+        seg = a[b:b + l]
+        if kind == "f64":
+            exp = three_list(seg, f64_key(np.array([p]))[0], key=f64_key)
+            assert np.array_equal(got[b:b + l].view(np.uint64), exp.view(np.uint64)), i
+            sk, pk = f64_key(seg), f64_key(np.array([p]))[0]
+        elif kind == "rec32":
+            exp = three_list(seg, p, key=lambda x: x[:, 0])
+            assert np.array_equal(got[b:b + l], exp), i
+            sk, pk = seg[:, 0], p
+        else:
+            exp = three_list(seg, p)
+            assert np.array_equal(got[b:b + l], exp), i
+            sk, pk = seg, p
+        assert tuple(c[i]) == (int((sk < pk).sum()), int((sk == pk).sum()), int((sk > pk).sum())), i
+
+
+def test_sort_large_levels(B):
+    # many multi-segment levels with persistent CTAs: the shape that exposed
+    # the staging-overflow bug (DESIGN.md log)
+    for lg in [22, 24]:
+        a = bqgen.i32_full((1 << lg) + 7, lg)
+        t = to_dev(a)
+        B.sort(t)
+        assert np.array_equal(t.cpu().numpy(), np.sort(a))
+
+
+@pytest.mark.parametrize("kind", ["i32", "u64", "f64", "rec32"])
 def test_pivot_rules(B, kind):
     for n in [1, 2, 3, 8, 9, 10, 1000, 123457]:
         a = make(kind, n, seed=n)

@@ -74,7 +74,7 @@ def build_bq(force=False, verbose_ptxas=False):
     srcs = _bq_sources()
     if not (force or _stale(BQ_SO, _bq_deps())):
         return BQ_SO
-    flags = list(NVCC_FLAGS)
+    flags = list(NVCC_FLAGS) + os.environ.get("BQ_NVCC_EXTRA", "").split()
     if verbose_ptxas:
         flags += ["-Xptxas", "-v"]
     objdir = os.path.join(ROOT, "build", "obj")
