@@ -84,7 +84,11 @@ typedef struct {
     int32_t pivot_rule;   /* bq_pivot_rule for segments > leaf size; default NINTHER */
     int32_t depth_limit;  /* < 0: Introsort limit 2*floor(log2 n)+3 */
     int32_t timing;       /* != 0: time every partition launch with CUDA events */
-    int32_t reserved[5];  /* must be 0 */
+    int32_t ordered;      /* != 0: ticket-ordered tile placement (decoupled look-back),
+                             deterministic layout; 0: one atomicAdd per tile (faster; tiles
+                             of a segment placed in completion order).  Records always
+                             use the ordered placement.  Sorted keys are identical. */
+    int32_t reserved[4];  /* must be 0 */
 } bq_sort_options;
 
 typedef struct {
@@ -139,14 +143,18 @@ BQ_API bq_status bq_partition_records(bq_record32 *recs, size_t n, uint64_t pivo
                                       void *stream);
 
 /* One out-of-place partition pass, fully asynchronous (no host sync): reads
- * src[0, n), writes the three-way partitioned permutation to dst[0, n)
- * (same layout as bq_partition_*), and writes {split, n_equal, n_greater} as
- * three uint64 to the DEVICE pointer d_counts.  `pivot` points to a HOST
- * value of the kind's storage type (int32 / uint64 / double; a uint64 key for
- * records).  src and dst must not overlap.  This is the timed unit of the
+ * src[0, n), writes the three-way partitioned permutation to dst[0, n) and
+ * writes {split, n_equal, n_greater} as three uint64 to the DEVICE pointer
+ * d_counts.  `pivot` points to a HOST value of the kind's storage type (int32
+ * / uint64 / double; a uint64 key for records).  src and dst must not
+ * overlap.  ordered != 0 gives the bq_partition_* layout (< keys in input
+ * order, > keys reversed, tiles in ticket order, via decoupled look-back);
+ * ordered == 0 places each tile's runs with one atomicAdd per tile (runs in
+ * input order within a tile, tiles in completion order) — the sort's default.
+ * Records always use the ordered placement.  This is the timed unit of the
  * partition-pass roofline. */
 BQ_API bq_status bq_partition_pass(bq_kind kind, const void *src, void *dst, size_t n,
-                                   const void *pivot, uint64_t *d_counts, void *ws,
+                                   const void *pivot, uint64_t *d_counts, int ordered, void *ws,
                                    size_t ws_bytes, void *stream);
 
 /* Batched pass over `nseg` disjoint segments of src (one breadth-first level
@@ -154,8 +162,8 @@ BQ_API bq_status bq_partition_pass(bq_kind kind, const void *src, void *dst, siz
  * [begins[i], begins[i] + lens[i]) with pivot pivots[i] (HOST arrays; pivots
  * of the kind's storage type, uint64 keys for records).  Each segment's
  * three-way partition (layout as bq_partition_*) is written to the same range
- * of dst; {split, n_equal, n_greater} of segment i go to d_counts[3i..3i+2]
- * (DEVICE).  Positions of dst outside every segment are left untouched.
+ * of dst (`ordered` as in bq_partition_pass); {split, n_equal, n_greater} of
+ * segment i go to d_counts[3i..3i+2] (DEVICE).  Positions of dst outside every segment are left untouched.
  * Requires lens[i] >= 1, segments inside [0, n) and pairwise disjoint, and
  * nseg <= n / (leaf size + 1) + 2 for the workspace of (kind, n)
  * (BQ_ERR_INVALID_ARGUMENT otherwise).  Synchronises `stream` before
@@ -163,7 +171,7 @@ BQ_API bq_status bq_partition_pass(bq_kind kind, const void *src, void *dst, siz
 BQ_API bq_status bq_partition_segments(bq_kind kind, const void *src, void *dst, size_t n,
                                        const uint32_t *begins, const uint32_t *lens,
                                        const void *pivots, size_t nseg, uint64_t *d_counts,
-                                       void *ws, size_t ws_bytes, void *stream);
+                                       int ordered, void *ws, size_t ws_bytes, void *stream);
 
 /* ---- sort (hot-path steps a1-a9) ---------------------------------------------
  * Sorts data[0, n) ascending in place (orders above).  Enqueued on `stream`;

@@ -18,7 +18,8 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libbq.so")
+# BQ_LIB may point at a tuning variant of the same library (tools/tune.py)
+LIB_PATH = os.environ.get("BQ_LIB", os.path.join(_HERE, "libbq.so"))
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(
@@ -36,7 +37,7 @@ WIDTH = {BQ_I32: 4, BQ_U64: 8, BQ_F64: 8, BQ_REC32: 32}
 
 class bq_sort_options(ctypes.Structure):
     _fields_ = [("pivot_rule", ctypes.c_int32), ("depth_limit", ctypes.c_int32),
-                ("timing", ctypes.c_int32), ("reserved", ctypes.c_int32 * 5)]
+                ("timing", ctypes.c_int32), ("ordered", ctypes.c_int32), ("reserved", ctypes.c_int32 * 4)]
 
 
 class bq_sort_stats(ctypes.Structure):
@@ -65,8 +66,8 @@ _SIGS = {
     "bq_partition_u64": (_st, [_vp, _sz, ctypes.c_uint64, _psz, _psz, _vp, _sz, _vp]),
     "bq_partition_f64": (_st, [_vp, _sz, ctypes.c_double, _psz, _psz, _vp, _sz, _vp]),
     "bq_partition_records": (_st, [_vp, _sz, ctypes.c_uint64, _psz, _psz, _vp, _sz, _vp]),
-    "bq_partition_pass": (_st, [_st, _vp, _vp, _sz, _vp, _vp, _vp, _sz, _vp]),
-    "bq_partition_segments": (_st, [_st, _vp, _vp, _sz, _vp, _vp, _vp, _sz, _vp, _vp, _sz, _vp]),
+    "bq_partition_pass": (_st, [_st, _vp, _vp, _sz, _vp, _vp, _st, _vp, _sz, _vp]),
+    "bq_partition_segments": (_st, [_st, _vp, _vp, _sz, _vp, _vp, _vp, _sz, _vp, _st, _vp, _sz, _vp]),
     "bq_sort_i32": (_st, [_vp, _sz, _vp, _sz, _vp]),
     "bq_sort_u64": (_st, [_vp, _sz, _vp, _sz, _vp]),
     "bq_sort_f64": (_st, [_vp, _sz, _vp, _sz, _vp]),
@@ -203,16 +204,16 @@ _PIVOT_CTYPE = {BQ_I32: ctypes.c_int32, BQ_U64: ctypes.c_uint64, BQ_F64: ctypes.
                 BQ_REC32: ctypes.c_uint64}
 
 
-def bq_partition_pass(src, dst, pivot, d_counts, ws=None, stream=None):
+def bq_partition_pass(src, dst, pivot, d_counts, ordered=True, ws=None, stream=None):
     """Asynchronous out-of-place pass; d_counts is a CUDA uint64/int64 tensor of >= 3."""
     kind = kind_of(src)
     w, wb = _ws(ws, kind, _n(src), src)
     pv = _PIVOT_CTYPE[kind](pivot)
     _check(_lib.bq_partition_pass(kind, _dev(src), _dev(dst), _n(src), ctypes.byref(pv),
-                                  _dev(d_counts), w, wb, _stream(stream)))
+                                  _dev(d_counts), int(ordered), w, wb, _stream(stream)))
 
 
-def bq_partition_segments(src, dst, begins, lens, pivots, d_counts, ws=None, stream=None):
+def bq_partition_segments(src, dst, begins, lens, pivots, d_counts, ordered=True, ws=None, stream=None):
     """Batched pass over disjoint segments; begins/lens/pivots are host sequences,
     d_counts a CUDA int64 tensor of >= 3*len(begins).  Synchronises the stream."""
     import numpy as np
@@ -224,7 +225,8 @@ def bq_partition_segments(src, dst, begins, lens, pivots, d_counts, ws=None, str
     pdt = {BQ_I32: np.int32, BQ_U64: np.uint64, BQ_F64: np.float64, BQ_REC32: np.uint64}[kind]
     pv = np.ascontiguousarray(np.asarray(pivots).astype(pdt))
     _check(_lib.bq_partition_segments(kind, _dev(src), _dev(dst), _n(src), b.ctypes.data, ln.ctypes.data,
-                                      pv.ctypes.data, nseg, _dev(d_counts), w, wb, _stream(stream)))
+                                      pv.ctypes.data, nseg, _dev(d_counts), int(ordered), w, wb,
+                                      _stream(stream)))
 
 
 def _sort(name, t, ws, stream):
@@ -250,19 +252,21 @@ def bq_sort_records(recs, ws=None, stream=None):
     return _sort("bq_sort_records", recs, ws, stream)
 
 
-def _opts(pivot_rule, depth_limit, timing):
+def _opts(pivot_rule, depth_limit, timing, ordered=False):
     o = bq_sort_options()
     o.pivot_rule = pivot_rule
     o.depth_limit = depth_limit
     o.timing = int(timing)
+    o.ordered = int(ordered)
     return o
 
 
-def bq_sort_ex(data, pivot_rule=BQ_PIVOT_NINTHER, depth_limit=-1, timing=False, ws=None, stream=None):
+def bq_sort_ex(data, pivot_rule=BQ_PIVOT_NINTHER, depth_limit=-1, timing=False, ordered=False, ws=None,
+               stream=None):
     """Kind-generic sort; returns the bq_sort_stats as a dict."""
     kind = kind_of(data)
     w, wb = _ws(ws, kind, _n(data), data)
-    o = _opts(pivot_rule, depth_limit, timing)
+    o = _opts(pivot_rule, depth_limit, timing, ordered)
     st = bq_sort_stats()
     _check(_lib.bq_sort_ex(kind, _dev(data), _n(data), ctypes.byref(o), ctypes.byref(st), w, wb,
                            _stream(stream)))

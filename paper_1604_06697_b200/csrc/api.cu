@@ -56,26 +56,26 @@ BQ_API size_t bq_workspace_bytes(bq_kind kind, size_t n) {
 }
 
 BQ_API bq_status bq_partition_pass(bq_kind kind, const void *src, void *dst, size_t n, const void *pivot,
-                                   uint64_t *d_counts, void *ws, size_t ws_bytes, void *stream) {
+                                   uint64_t *d_counts, int ordered, void *ws, size_t ws_bytes, void *stream) {
     if (pivot == nullptr) return bq::set_error(BQ_ERR_INVALID_ARGUMENT, "NULL pivot");
     cudaStream_t s = (cudaStream_t)stream;
     switch (kind) {
-        case BQ_I32: return pass_i32(src, dst, n, pivot, d_counts, ws, ws_bytes, s);
-        case BQ_U64: return pass_u64(src, dst, n, pivot, d_counts, ws, ws_bytes, s);
+        case BQ_I32: return pass_i32(src, dst, n, pivot, d_counts, ws, ws_bytes, s, ordered);
+        case BQ_U64: return pass_u64(src, dst, n, pivot, d_counts, ws, ws_bytes, s, ordered);
         case BQ_F64: {
             double d;
             std::memcpy(&d, pivot, 8);
             if (d != d) return bq::set_error(BQ_ERR_INVALID_ARGUMENT, "NaN pivot");
-            return pass_f64(src, dst, n, pivot, d_counts, ws, ws_bytes, s);
+            return pass_f64(src, dst, n, pivot, d_counts, ws, ws_bytes, s, ordered);
         }
-        case BQ_REC32: return pass_rec(src, dst, n, pivot, d_counts, ws, ws_bytes, s);
+        case BQ_REC32: return pass_rec(src, dst, n, pivot, d_counts, ws, ws_bytes, s, ordered);
     }
     return bq::set_error(BQ_ERR_INVALID_ARGUMENT, "bad kind %d", (int)kind);
 }
 
 BQ_API bq_status bq_partition_segments(bq_kind kind, const void *src, void *dst, size_t n, const uint32_t *begins,
                                        const uint32_t *lens, const void *pivots, size_t nseg, uint64_t *d_counts,
-                                       void *ws, size_t ws_bytes, void *stream) {
+                                       int ordered, void *ws, size_t ws_bytes, void *stream) {
     cudaStream_t s = (cudaStream_t)stream;
     if (nseg && pivots == nullptr) return bq::set_error(BQ_ERR_INVALID_ARGUMENT, "NULL pivots");
     if (kind == BQ_F64)
@@ -85,10 +85,10 @@ BQ_API bq_status bq_partition_segments(bq_kind kind, const void *src, void *dst,
             if (d != d) return bq::set_error(BQ_ERR_INVALID_ARGUMENT, "NaN pivot");
         }
     switch (kind) {
-        case BQ_I32: return segs_i32(src, dst, n, begins, lens, pivots, nseg, d_counts, ws, ws_bytes, s);
-        case BQ_U64: return segs_u64(src, dst, n, begins, lens, pivots, nseg, d_counts, ws, ws_bytes, s);
-        case BQ_F64: return segs_f64(src, dst, n, begins, lens, pivots, nseg, d_counts, ws, ws_bytes, s);
-        case BQ_REC32: return segs_rec(src, dst, n, begins, lens, pivots, nseg, d_counts, ws, ws_bytes, s);
+        case BQ_I32: return segs_i32(src, dst, n, begins, lens, pivots, nseg, d_counts, ws, ws_bytes, s, ordered);
+        case BQ_U64: return segs_u64(src, dst, n, begins, lens, pivots, nseg, d_counts, ws, ws_bytes, s, ordered);
+        case BQ_F64: return segs_f64(src, dst, n, begins, lens, pivots, nseg, d_counts, ws, ws_bytes, s, ordered);
+        case BQ_REC32: return segs_rec(src, dst, n, begins, lens, pivots, nseg, d_counts, ws, ws_bytes, s, ordered);
     }
     return bq::set_error(BQ_ERR_INVALID_ARGUMENT, "bad kind %d", (int)kind);
 }

@@ -19,6 +19,13 @@ BQ_API bq_status bq_partition_i32(int32_t *keys, size_t n, int32_t pivot, size_t
                                                (cudaStream_t)stream);
 }
 
+#ifdef BQ_TRACE
+// debug-only (not in bq.h): copy the per-tile phase trace of the int32 kernels
+BQ_API int bq_debug_trace(void *host, size_t bytes) {
+    return (int)cudaMemcpyFromSymbol(host, bq::g_trace, bytes);
+}
+#endif
+
 BQ_API bq_status bq_sort_i32(int32_t *keys, size_t n, void *ws, size_t ws_bytes, void *stream) {
     return bq::run_sort<bq::KI32>(keys, n, nullptr, nullptr, ws, ws_bytes, (cudaStream_t)stream);
 }

@@ -14,10 +14,10 @@
     bq_status sort_##SUF(void *data, size_t n, const bq_sort_options *opt, bq_sort_stats *st,       \
                          void *ws, size_t wsb, cudaStream_t s);                                     \
     bq_status pass_##SUF(const void *src, void *dst, size_t n, const void *pivot, uint64_t *dc,     \
-                         void *ws, size_t wsb, cudaStream_t s);                                     \
+                         void *ws, size_t wsb, cudaStream_t s, int ordered);                        \
     bq_status segs_##SUF(const void *src, void *dst, size_t n, const uint32_t *begins,              \
                          const uint32_t *lens, const void *pivots, size_t nseg, uint64_t *dc,       \
-                         void *ws, size_t wsb, cudaStream_t s);                                     \
+                         void *ws, size_t wsb, cudaStream_t s, int ordered);                        \
     }                                                                                               \
     }
 
@@ -35,15 +35,15 @@ BQ_DETAIL_DECLS(rec)
         return run_sort<KT>(static_cast<KT::T *>(data), n, opt, st, ws, wsb, s);                    \
     }                                                                                               \
     bq_status pass_##SUF(const void *src, void *dst, size_t n, const void *pivot, uint64_t *dc,     \
-                         void *ws, size_t wsb, cudaStream_t s) {                                    \
+                         void *ws, size_t wsb, cudaStream_t s, int ordered) {                       \
         KT::T pv;                                                                                   \
         std::memcpy(&pv, pivot, sizeof pv);                                                         \
         return run_partition_pass<KT>(static_cast<const KT::T *>(src), static_cast<KT::T *>(dst),  \
-                                      n, KT::key(pv), dc, ws, wsb, s);                              \
+                                      n, KT::key(pv), dc, ws, wsb, s, ordered);                     \
     }                                                                                               \
     bq_status segs_##SUF(const void *src, void *dst, size_t n, const uint32_t *begins,              \
                          const uint32_t *lens, const void *pivots, size_t nseg, uint64_t *dc,       \
-                         void *ws, size_t wsb, cudaStream_t s) {                                    \
+                         void *ws, size_t wsb, cudaStream_t s, int ordered) {                       \
         std::vector<KT::K> keys(nseg);                                                             \
         for (size_t i = 0; i < nseg; i++) {                                                         \
             KT::T pv;                                                                               \
@@ -51,7 +51,7 @@ BQ_DETAIL_DECLS(rec)
             keys[i] = KT::key(pv);                                                                  \
         }                                                                                           \
         return run_partition_segments<KT>(static_cast<const KT::T *>(src), static_cast<KT::T *>(dst), \
-                                          n, begins, lens, keys.data(), nseg, dc, ws, wsb, s);      \
+                                          n, begins, lens, keys.data(), nseg, dc, ws, wsb, s, ordered); \
     }                                                                                               \
     }                                                                                               \
     }

@@ -10,16 +10,16 @@ bq_status sort_rec(void *data, size_t n, const bq_sort_options *opt, bq_sort_sta
     return run_sort<KRec>(static_cast<Rec32 *>(data), n, opt, st, ws, wsb, s);
 }
 bq_status pass_rec(const void *src, void *dst, size_t n, const void *pivot, uint64_t *dc, void *ws, size_t wsb,
-                   cudaStream_t s) {
+                   cudaStream_t s, int ordered) {
     uint64_t pk;
     std::memcpy(&pk, pivot, sizeof pk);
     return run_partition_pass<KRec>(static_cast<const Rec32 *>(src), static_cast<Rec32 *>(dst), n, pk, dc, ws,
-                                    wsb, s);
+                                    wsb, s, ordered);
 }
 bq_status segs_rec(const void *src, void *dst, size_t n, const uint32_t *begins, const uint32_t *lens,
-                   const void *pivots, size_t nseg, uint64_t *dc, void *ws, size_t wsb, cudaStream_t s) {
+                   const void *pivots, size_t nseg, uint64_t *dc, void *ws, size_t wsb, cudaStream_t s, int ordered) {
     return run_partition_segments<KRec>(static_cast<const Rec32 *>(src), static_cast<Rec32 *>(dst), n, begins, lens,
-                                        static_cast<const uint64_t *>(pivots), nseg, dc, ws, wsb, s);
+                                        static_cast<const uint64_t *>(pivots), nseg, dc, ws, wsb, s, ordered);
 }
 }  // namespace detail
 }  // namespace bq

@@ -76,17 +76,27 @@ struct KRec {
 // warp is added), PART_IPT = elements per consumer thread, PART_STAGES = TMA
 // load pipeline depth, PART_MINB = CTAs per SM the register budget targets.
 template <class KT> struct Tune;
+#ifndef BQ_I32_IPT
+#define BQ_I32_IPT 16
+#endif
+#ifndef BQ_I32_STAGES
+#define BQ_I32_STAGES 4
+#endif
+#ifndef BQ_I32_MINB
+#define BQ_I32_MINB 2
+#endif
 template <> struct Tune<KI32> {
-    static constexpr int PART_THREADS = 256, PART_IPT = 16, PART_STAGES = 2, PART_MINB = 3;  // 16 KB tiles
+    static constexpr int PART_THREADS = 256, PART_IPT = BQ_I32_IPT, PART_STAGES = BQ_I32_STAGES,
+                         PART_MINB = BQ_I32_MINB;
     static constexpr int LEAF = 8192, LEAF_THREADS = 512;
 };
 template <> struct Tune<KU64> {
-    static constexpr int PART_THREADS = 256, PART_IPT = 8, PART_STAGES = 2, PART_MINB = 4;   // 16 KB tiles
+    static constexpr int PART_THREADS = 256, PART_IPT = 8, PART_STAGES = 4, PART_MINB = 2;   // 16 KB tiles
     static constexpr int LEAF = 4096, LEAF_THREADS = 512;
 };
 template <> struct Tune<KF64> : Tune<KU64> {};
 template <> struct Tune<KRec> {
-    static constexpr int PART_THREADS = 256, PART_IPT = 2, PART_STAGES = 2, PART_MINB = 3;   // 16 KB tiles
+    static constexpr int PART_THREADS = 256, PART_IPT = 2, PART_STAGES = 4, PART_MINB = 2;   // 16 KB tiles
     static constexpr int LEAF = 2048, LEAF_THREADS = 512;
 };
 
@@ -170,6 +180,34 @@ __device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t *p) {
     return v;
 }
 
+// ---- optional per-tile phase trace (tools/trace_pass.py; build with -DBQ_TRACE) --
+#ifdef BQ_TRACE
+static __device__ unsigned long long g_trace[1 << 17][8];
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define BQ_TR(t, k, v)                                   \
+    do {                                                 \
+        if ((t) < (1u << 17)) g_trace[(t)][(k)] = (v);   \
+    } while (0)
+#else
+#define BQ_TR(t, k, v) \
+    do {               \
+    } while (0)
+#endif
+
+// Waiting warps must not steal issue slots from the working ones: try_wait
+// suspends the thread for up to this many ns per attempt (it wakes as soon as
+// the phase completes), and look-back polls back off with nanosleep.
+#ifndef BQ_MBAR_SLEEP_NS
+#define BQ_MBAR_SLEEP_NS 1000000
+#endif
+#ifndef BQ_POLL_SLEEP_NS
+#define BQ_POLL_SLEEP_NS 64
+#endif
+
 // ---- mbarrier / bulk-copy (TMA) helpers (sm_90+ PTX, used on sm_100a) --------
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return (uint32_t)__cvta_generic_to_shared(p);
@@ -188,9 +226,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred p;\n"
         "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
         "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-        "r"(parity)
+        "r"(parity), "r"(BQ_MBAR_SLEEP_NS)
         : "memory");
 }
 // 1D bulk copy global -> shared, completion counted on an mbarrier (UBLKCP).

@@ -48,7 +48,7 @@ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 template <class KT>
 struct Layout {
-    size_t scratch, status, tile_map, segs[2], leaves[2], fallback, ctrl, misc, total;
+    size_t scratch, status, tile_map, segs[2], cursor, ecursor, leaves[2], fallback, ctrl, misc, total;
     size_t max_tiles, max_segs, max_leaves, max_fb;
 };
 
@@ -68,6 +68,8 @@ Layout<KT> make_layout(size_t n) {
     L.tile_map = take(L.max_tiles * sizeof(uint32_t));
     L.segs[0] = take(L.max_segs * sizeof(Seg));
     L.segs[1] = take(L.max_segs * sizeof(Seg));
+    L.cursor = take(L.max_segs * sizeof(unsigned long long));
+    L.ecursor = take(L.max_segs * sizeof(uint32_t));
     L.leaves[0] = take(L.max_leaves * sizeof(Leaf));
     L.leaves[1] = take(L.max_leaves * sizeof(Leaf));
     L.fallback = take(L.max_fb * sizeof(Leaf));
@@ -87,25 +89,34 @@ struct Kernels {
 };
 
 // Persistent launch of the partition kernel: min(ntiles, resident CTAs).
-template <class KT>
-bq_status launch_partition(const PassParams<KT> &P, cudaStream_t s) {
+template <class KT, bool ORDERED>
+bq_status launch_partition_t(const PassParams<KT> &P, cudaStream_t s) {
     using Kn = Kernels<KT>;
-    auto kern = k_partition<KT, Kn::NT, Kn::IPT, Kn::STAGES, Kn::MINB>;
+    auto kern = k_partition<KT, Kn::NT, Kn::IPT, Kn::STAGES, Kn::MINB, ORDERED>;
     constexpr int smem = part_smem_bytes<KT>();
+    constexpr int threads = Kn::NT + (ORDERED ? 96 : 64);
     static int cap = 0;
     if (cap == 0) {
         BQ_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         int nb = 0, dev = 0, sms = 0;
-        BQ_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, Kn::NT + 32, smem));
+        BQ_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, threads, smem));
         BQ_CK(cudaGetDevice(&dev));
         BQ_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
         if (nb < 1) return set_error(BQ_ERR_CUDA, "partition kernel does not fit on an SM");
         cap = nb * sms;
     }
-    uint32_t grid = P.ntiles < (uint32_t)cap ? P.ntiles : (uint32_t)cap;
-    kern<<<grid, Kn::NT + 32, smem, s>>>(P);
+    const uint32_t grid = P.ntiles < (uint32_t)cap ? P.ntiles : (uint32_t)cap;
+    kern<<<grid, threads, smem, s>>>(P);
     BQ_CK_LAUNCH();
     return BQ_OK;
+}
+
+// Records always use the ordered (look-back) mode: their equal elements are
+// staged in already-consumed input tiles, which needs ticket-ordered offsets.
+template <class KT>
+bq_status launch_partition(const PassParams<KT> &P, cudaStream_t s) {
+    if (P.ordered || KT::is_record) return launch_partition_t<KT, true>(P, s);
+    return launch_partition_t<KT, false>(P, s);
 }
 
 template <class KT>
@@ -141,20 +152,24 @@ bq_status validate(const void *data, size_t n, void *ws, size_t ws_bytes) {
 // One out-of-place three-way pass over a single segment [0, n).
 template <class KT>
 bq_status run_pass(const typename KT::T *src, typename KT::T *dst, typename KT::T *stage, size_t n,
-                   typename KT::K pivot_key, uint64_t *d_counts, void *ws, cudaStream_t s) {
+                   typename KT::K pivot_key, uint64_t *d_counts, void *ws, cudaStream_t s, int ordered) {
     using T = typename KT::T;
     constexpr uint32_t TILE = tile_elems<KT>();
     const Layout<KT> L = make_layout<KT>(n);
     char *w = static_cast<char *>(ws);
     uint64_t *status = reinterpret_cast<uint64_t *>(w + L.status);
+    unsigned long long *cursor = reinterpret_cast<unsigned long long *>(w + L.cursor);
+    uint32_t *ecursor = reinterpret_cast<uint32_t *>(w + L.ecursor);
     LevelCtrl *ctrl = reinterpret_cast<LevelCtrl *>(w + L.ctrl);
     if (n == 0) {
         BQ_CK(cudaMemsetAsync(d_counts, 0, 3 * sizeof(uint64_t), s));
         return BQ_OK;
     }
     const uint32_t ntiles = seg_ntiles(0, (uint32_t)n, TILE);
-    BQ_CK(cudaMemsetAsync(status, 0, ntiles * sizeof(uint64_t), s));
+    if (ordered || KT::is_record) BQ_CK(cudaMemsetAsync(status, 0, ntiles * sizeof(uint64_t), s));
     BQ_CK(cudaMemsetAsync(ctrl, 0, sizeof(LevelCtrl), s));
+    BQ_CK(cudaMemsetAsync(cursor, 0, sizeof(unsigned long long), s));
+    BQ_CK(cudaMemsetAsync(ecursor, 0, sizeof(uint32_t), s));
     PassParams<KT> P{};
     P.bufs[0] = const_cast<T *>(src);
     P.bufs[1] = dst;
@@ -164,10 +179,13 @@ bq_status run_pass(const typename KT::T *src, typename KT::T *dst, typename KT::
     P.tile_map = nullptr;
     P.seg0 = Seg{(uint64_t)pivot_key, 0, (uint32_t)n, 0, ntiles, 0, 0, 0, 0};
     P.status = status;
+    P.cursor = cursor;
+    P.ecursor = ecursor;
     P.ctrl = ctrl;
     P.ntiles = ntiles;
     P.n_total = n;
     P.aligned = aligned16(src) && aligned16(dst);
+    P.ordered = ordered;
     bq_status st = launch_partition<KT>(P, s);
     if (st != BQ_OK) return st;
     PostParams<KT> Q{};
@@ -208,7 +226,7 @@ bq_status run_partition_inplace(typename KT::T *data, size_t n, typename KT::K p
     T *scratch = reinterpret_cast<T *>(w + L.scratch);
     uint64_t *counts = reinterpret_cast<uint64_t *>(w + L.misc);
     // records stage their equal elements in the (already consumed) input
-    st = run_pass<KT>(data, scratch, data, n, pivot_key, counts, ws, s);
+    st = run_pass<KT>(data, scratch, data, n, pivot_key, counts, ws, s, /*ordered=*/1);
     if (st != BQ_OK) return st;
     if (n) BQ_CK(cudaMemcpyAsync(data, scratch, n * sizeof(T), cudaMemcpyDeviceToDevice, s));
     uint64_t h[3] = {0, 0, 0};
@@ -222,7 +240,7 @@ bq_status run_partition_inplace(typename KT::T *data, size_t n, typename KT::K p
 template <class KT>
 bq_status run_partition_pass(const typename KT::T *src, typename KT::T *dst, size_t n,
                              typename KT::K pivot_key, uint64_t *d_counts, void *ws, size_t ws_bytes,
-                             cudaStream_t s) {
+                             cudaStream_t s, int ordered) {
     using T = typename KT::T;
     bq_status st = validate<KT>(src, n, ws, ws_bytes);
     if (st != BQ_OK) return st;
@@ -234,14 +252,14 @@ bq_status run_partition_pass(const typename KT::T *src, typename KT::T *dst, siz
     if (n && a < c + bytes && c < a + bytes) return set_error(BQ_ERR_INVALID_ARGUMENT, "src and dst overlap");
     const Layout<KT> L = make_layout<KT>(n);
     T *scratch = reinterpret_cast<T *>(static_cast<char *>(ws) + L.scratch);
-    return run_pass<KT>(src, dst, scratch, n, pivot_key, d_counts, ws, s);
+    return run_pass<KT>(src, dst, scratch, n, pivot_key, d_counts, ws, s, ordered);
 }
 
 // Batched pass over caller-given disjoint segments (bq_partition_segments).
 template <class KT>
 bq_status run_partition_segments(const typename KT::T *src, typename KT::T *dst, size_t n, const uint32_t *begins,
                                  const uint32_t *lens, const typename KT::K *pivot_keys, size_t nseg,
-                                 uint64_t *d_counts, void *ws, size_t ws_bytes, cudaStream_t s) {
+                                 uint64_t *d_counts, void *ws, size_t ws_bytes, cudaStream_t s, int ordered) {
     using T = typename KT::T;
     constexpr uint32_t TILE = tile_elems<KT>();
     bq_status st = validate<KT>(src, n, ws, ws_bytes);
@@ -278,10 +296,12 @@ bq_status run_partition_segments(const typename KT::T *src, typename KT::T *dst,
     uint64_t *status = reinterpret_cast<uint64_t *>(w + L.status);
     uint32_t *tile_map = reinterpret_cast<uint32_t *>(w + L.tile_map);
     Seg *segs = reinterpret_cast<Seg *>(w + L.segs[0]);
+    unsigned long long *cursor = reinterpret_cast<unsigned long long *>(w + L.cursor);
+    uint32_t *ecursor = reinterpret_cast<uint32_t *>(w + L.ecursor);
     LevelCtrl *ctrl = reinterpret_cast<LevelCtrl *>(w + L.ctrl);
     BQ_CK(cudaMemcpyAsync(segs, hs.data(), nseg * sizeof(Seg), cudaMemcpyHostToDevice, s));
     BQ_CK(cudaMemsetAsync(ctrl, 0, sizeof(LevelCtrl), s));
-    k_map<<<dim3((uint32_t)nseg, (maxtiles + 255) / 256), 256, 0, s>>>(segs, tile_map, status);
+    k_map<<<dim3((uint32_t)nseg, (maxtiles + 255) / 256), 256, 0, s>>>(segs, tile_map, status, cursor, ecursor);
     BQ_CK_LAUNCH();
     PassParams<KT> P{};
     P.bufs[0] = const_cast<T *>(src);
@@ -291,10 +311,13 @@ bq_status run_partition_segments(const typename KT::T *src, typename KT::T *dst,
     P.segs = segs;
     P.tile_map = tile_map;
     P.status = status;
+    P.cursor = cursor;
+    P.ecursor = ecursor;
     P.ctrl = ctrl;
     P.ntiles = (uint32_t)tiles;
     P.n_total = n;
     P.aligned = aligned16(src) && aligned16(dst);
+    P.ordered = ordered;
     st = launch_partition<KT>(P, s);
     if (st != BQ_OK) return st;
     PostParams<KT> Q{};
@@ -349,11 +372,12 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
     using Kn = Kernels<KT>;
     bq_sort_stats local;
     std::memset(&local, 0, sizeof local);
-    int rule = BQ_PIVOT_NINTHER, depth_limit = -1, timing = 0;
+    int rule = BQ_PIVOT_NINTHER, depth_limit = -1, timing = 0, ordered = 0;
     if (opt) {
         rule = opt->pivot_rule;
         depth_limit = opt->depth_limit;
         timing = opt->timing;
+        ordered = opt->ordered;
         if (rule != BQ_PIVOT_MO3 && rule != BQ_PIVOT_NINTHER)
             return set_error(BQ_ERR_INVALID_ARGUMENT, "bad pivot rule %d", rule);
         if (depth_limit >= MAX_LEVELS - 2)
@@ -380,6 +404,8 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
     uint64_t *status = reinterpret_cast<uint64_t *>(w + L.status);
     uint32_t *tile_map = reinterpret_cast<uint32_t *>(w + L.tile_map);
     Seg *segs[2] = {reinterpret_cast<Seg *>(w + L.segs[0]), reinterpret_cast<Seg *>(w + L.segs[1])};
+    unsigned long long *cursor = reinterpret_cast<unsigned long long *>(w + L.cursor);
+    uint32_t *ecursor = reinterpret_cast<uint32_t *>(w + L.ecursor);
     Leaf *leaves[2] = {reinterpret_cast<Leaf *>(w + L.leaves[0]), reinterpret_cast<Leaf *>(w + L.leaves[1])};
     Leaf *fallback = reinterpret_cast<Leaf *>(w + L.fallback);
     LevelCtrl *ctrl = reinterpret_cast<LevelCtrl *>(w + L.ctrl);
@@ -425,7 +451,7 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
         Seg *cur = segs[level & 1];
         Seg *nxt = segs[(level + 1) & 1];
         dim3 mg(nseg, (maxtiles + 255) / 256);
-        k_map<<<mg, 256, 0, s>>>(cur, tile_map, status);
+        k_map<<<mg, 256, 0, s>>>(cur, tile_map, status, cursor, ecursor);
         BQ_CK_LAUNCH();
         local.kernel_launches++;
 
@@ -438,6 +464,9 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
         P.segs = cur;
         P.tile_map = tile_map;
         P.status = status;
+        P.cursor = cursor;
+        P.ecursor = ecursor;
+        P.ordered = ordered;
         P.ctrl = ctrl + level;
         P.ntiles = ntiles;
         P.n_total = n;

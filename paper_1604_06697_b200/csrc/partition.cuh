@@ -36,11 +36,14 @@ struct PassParams {
     const Seg *segs;       // segment descriptors of this level
     const uint32_t *tile_map;  // tile -> segment (nullptr: single segment `seg0`)
     Seg seg0;
-    uint64_t *status;      // one look-back word per tile, zeroed before the pass
+    uint64_t *status;      // one look-back word per tile, zeroed before the pass (ordered mode)
+    unsigned long long *cursor;  // per segment: packed (lt | gt << 32) running offsets / totals
+    uint32_t *ecursor;     // per segment: equal-record running offset (records, fast mode)
     LevelCtrl *ctrl;       // ticket + counters of this level
     uint32_t ntiles;
     uint64_t n_total;      // length of each data buffer (bounds the TMA reads)
     int aligned;           // both data buffers 16-byte aligned -> TMA bulk copies
+    int ordered;           // 1: decoupled look-back (deterministic layout), 0: atomic cursor
 };
 
 }  // namespace bq
@@ -83,8 +86,8 @@ __global__ void __launch_bounds__(NT) k_post(PostParams<KT> Q) {
     const uint32_t t = blockIdx.x;
     const Seg sg = P.tile_map ? P.segs[P.tile_map[t]] : P.seg0;
     const uint32_t k = t - sg.tile_base;
-    const uint64_t fin = P.status[sg.tile_base + sg.ntiles - 1];
-    const uint32_t L = st_lt(fin), G = st_gt(fin);
+    const unsigned long long fin = P.cursor[P.tile_map ? P.tile_map[t] : 0];
+    const uint32_t L = (uint32_t)fin, G = (uint32_t)(fin >> 32);
     const uint32_t E = sg.len - L - G;
     const uint64_t b = sg.begin;
     const uint64_t tbeg = (b / TILE) * TILE + (uint64_t)k * TILE;
@@ -155,8 +158,8 @@ __global__ void __launch_bounds__(NT) k_band2(PassParams<KT> P) {
     const Seg sg = P.tile_map ? P.segs[P.tile_map[t]] : P.seg0;
     if ((sg.parity ? P.stage[1] : P.stage[0]) != P.final_buf) return;
     const uint32_t k = t - sg.tile_base;
-    const uint64_t fin = P.status[sg.tile_base + sg.ntiles - 1];
-    const uint32_t L = st_lt(fin), G = st_gt(fin);
+    const unsigned long long fin = P.cursor[P.tile_map ? P.tile_map[t] : 0];
+    const uint32_t L = (uint32_t)fin, G = (uint32_t)(fin >> 32);
     const uint32_t E = sg.len - L - G;
     const uint64_t b = sg.begin;
     const uint64_t tbeg = (b / TILE) * TILE + (uint64_t)k * TILE;
@@ -168,9 +171,14 @@ __global__ void __launch_bounds__(NT) k_band2(PassParams<KT> P) {
 }
 
 // Tile map + status reset for a level: tile_map[tile_base + j] = segment.
-static __global__ void k_map(const Seg *segs, uint32_t *tile_map, uint64_t *status) {
+static __global__ void k_map(const Seg *segs, uint32_t *tile_map, uint64_t *status, unsigned long long *cursor,
+                             uint32_t *ecursor) {
     const uint32_t s = blockIdx.x;
     const Seg sg = segs[s];
+    if (blockIdx.y == 0 && threadIdx.x == 0) {
+        cursor[s] = 0;
+        ecursor[s] = 0;
+    }
     for (uint32_t j = blockIdx.y * blockDim.x + threadIdx.x; j < sg.ntiles; j += gridDim.y * blockDim.x) {
         tile_map[sg.tile_base + j] = s;
         status[sg.tile_base + j] = 0;

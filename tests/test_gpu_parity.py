@@ -16,7 +16,7 @@ from gpu_util import three_list, to_dev, to_host
 pytestmark = pytest.mark.gpu
 
 # tile T and leaf S per kind (csrc/common.cuh Tune<>)
-TILE = {"i32": 4096, "u64": 2048, "f64": 2048, "rec32": 1024}
+TILE = {"i32": 4096, "u64": 2048, "f64": 2048, "rec32": 512}
 LEAF = {"i32": 8192, "u64": 4096, "f64": 4096, "rec32": 2048}
 
 
@@ -249,6 +249,30 @@ def test_partition_pass_out_of_place(B, kind):
         assert np.array_equal(got, three_list(a, np.uint64(pv), key=lambda x: x[:, 0]))
     else:
         assert np.array_equal(got, three_list(a, np.array(pv, dtype=a.dtype)))
+
+
+@pytest.mark.parametrize("kind", ["i32", "u64", "f64"])
+@pytest.mark.parametrize("n", [1, 4097, (1 << 20) + 3, (1 << 23) + 5])
+def test_partition_pass_fast_mode(B, kind, n):
+    """Atomic-cursor placement (the sort's default): tiles land in completion
+    order, so check the plain definition: bands, counts and the multiset; and
+    that every tile's < run is a contiguous, in-order subsequence."""
+    a = make(kind, n, seed=n + 3, dist="dups")
+    src = to_dev(a)
+    dst = torch.empty_like(src)
+    counts = torch.zeros(3, dtype=torch.int64, device="cuda")
+    p = keys_of(a)[n // 2]
+    pv = float(p) if kind == "f64" else int(p)
+    B.bq_partition_pass(src, dst, pv, counts, ordered=False)
+    got = to_host(dst, a)
+    if kind == "f64":
+        ka, kg, pk = f64_key(a), f64_key(got), f64_key(np.array([pv]))[0]
+    else:
+        ka, kg, pk = a, got, np.array(pv, dtype=a.dtype)
+    s_, e_ = int((ka < pk).sum()), int((ka == pk).sum())
+    assert counts.cpu().tolist() == [s_, e_, n - s_ - e_]
+    assert (kg[:s_] < pk).all() and (kg[s_:s_ + e_] == pk).all() and (kg[s_ + e_:] > pk).all()
+    assert np.array_equal(np.sort(kg), np.sort(ka))
 
 
 @pytest.mark.parametrize("kind", ["i32", "u64", "f64", "rec32"])

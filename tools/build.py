@@ -70,14 +70,15 @@ def build_oracle(force=False):
     return ORACLE_SO
 
 
-def build_bq(force=False, verbose_ptxas=False):
+def build_bq(force=False, verbose_ptxas=False, out=None, extra=()):
     srcs = _bq_sources()
-    if not (force or _stale(BQ_SO, _bq_deps())):
-        return BQ_SO
-    flags = list(NVCC_FLAGS) + os.environ.get("BQ_NVCC_EXTRA", "").split()
+    target = out or BQ_SO
+    if not (force or _stale(target, _bq_deps())):
+        return target
+    flags = list(NVCC_FLAGS) + os.environ.get("BQ_NVCC_EXTRA", "").split() + list(extra)
     if verbose_ptxas:
         flags += ["-Xptxas", "-v"]
-    objdir = os.path.join(ROOT, "build", "obj")
+    objdir = os.path.join(ROOT, "build", "obj" if out is None else "obj_" + os.path.basename(target))
     os.makedirs(objdir, exist_ok=True)
     objs = []
     # compile translation units in parallel (each kernel family is its own .cu)
@@ -93,12 +94,12 @@ def build_bq(force=False, verbose_ptxas=False):
         logs.append(err)
         if p.returncode != 0:
             raise RuntimeError(f"nvcc failed on {s}\n{out}\n{err}")
-    tmp = BQ_SO + ".tmp"
+    tmp = target + ".tmp"
     _run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp] + objs)
-    os.replace(tmp, BQ_SO)
+    os.replace(tmp, target)
     if verbose_ptxas:
         return "\n".join(logs)
-    return BQ_SO
+    return target
 
 
 def build_all(force=False):
