@@ -1,0 +1,101 @@
+"""Full-size parity (-m gpu): BASELINE.json's five configs at their stated n,
+in the launch configuration bench.py times (bq_sort_ex defaults: ninther
+pivots, atomic-cursor placement, persistent partition CTAs).
+
+north_star target: "bit-exact sorted output versus the CPU oracle on all five
+configs".  The oracle (single-threaded CPU BlockQuicksort) finishes 2^28 int32
+keys in about ten seconds, so every config is compared with it in full, byte
+for byte; on top of that the plain definition of sorted position is checked
+on sampled outputs (#{a < out[i]} <= i < #{a <= out[i]}) and each config's
+closed form where it has one (SURVEY §8(c) "Sort" pins).
+"""
+import numpy as np
+import pytest
+import torch
+
+import bqgen
+import oracle
+from gpu_util import to_dev, to_host
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+
+@pytest.fixture(scope="module")
+def B(bq):
+    assert torch.cuda.is_available()
+    return bq
+
+
+def sampled_ranks(inp_keys, out_keys, samples=12, seed=0):
+    rng = np.random.default_rng(seed)
+    n = len(out_keys)
+    for i in rng.integers(0, n, size=samples):
+        v = out_keys[i]
+        lo = int(np.count_nonzero(inp_keys < v))
+        hi = int(np.count_nonzero(inp_keys <= v))
+        assert lo <= i < hi, (i, lo, hi)
+
+
+def run_sort(B, a):
+    t = to_dev(a)
+    st = B.bq_sort_ex(t)
+    got = to_host(t, a)
+    del t
+    torch.cuda.empty_cache()
+    return got, st
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c4a", "c4b"])
+def test_full_int32_configs(B, name):
+    a = bqgen.config(name, seed=1)
+    got, st = run_sort(B, a)
+    exp = oracle.sort(a)
+    assert np.array_equal(got, exp)                     # bit-exact vs oracle
+    assert st["fallback_segments"] == 0
+    sampled_ranks(a, got)
+    if name == "c1":
+        assert np.array_equal(got, np.arange(len(a), dtype=np.int32))
+    elif name == "c4a":
+        counts = np.bincount(a, minlength=int(a.max()) + 1)
+        assert np.array_equal(got, np.repeat(np.arange(len(counts), dtype=np.int32), counts))
+    elif name == "c4b":
+        assert np.array_equal(got, a) and st["levels"] == 1
+
+
+@pytest.mark.parametrize("ordering", ["random", "ascending", "descending", "swapped"])
+def test_full_c3_float64(B, ordering):
+    a = bqgen.config("c3", seed=1, ordering=ordering)
+    got, st = run_sort(B, a)
+    assert np.array_equal(got.view(np.uint64), oracle.sort(a).view(np.uint64))
+    assert st["fallback_segments"] == 0
+    sampled_ranks(a, got)
+    if ordering != "random":
+        assert np.array_equal(got, bqgen.f64(len(a), 1, "ascending"))   # closed form (R11)
+
+
+def test_full_c5_records(B):
+    a = bqgen.config("c5", seed=1)
+    got, st = run_sort(B, a)
+    exp = oracle.sort(a)
+    assert np.array_equal(got[:, 0], exp[:, 0])
+    idx = got[:, 1].astype(np.int64)
+    assert np.array_equal(np.sort(idx), np.arange(len(a)))
+    assert (got[:, 1] == got[:, 2]).all() and (got[:, 2] == got[:, 3]).all()
+    assert np.array_equal(got[:, 0], a[idx, 0])
+    sampled_ranks(a[:, 0], got[:, 0])
+
+
+def test_full_c2_partition(B):
+    """BASELINE config 2's roofline unit: one three-way partition of 2^28
+    int32 keys around the Mo3 pivot, checked against the oracle's counts and
+    the band predicates."""
+    a = bqgen.config("c2", seed=1)
+    t = to_dev(a)
+    p = B.bq_pivot_i32(t, B.BQ_PIVOT_MO3)
+    assert p == oracle.pivot(a, oracle.MO3)
+    split, neq = B.bq_partition_i32(t, p)
+    assert split == int(np.count_nonzero(a < p)) and neq == int(np.count_nonzero(a == p))
+    assert bool((t[:split] < p).all()) and bool((t[split:split + neq] == p).all())
+    assert bool((t[split + neq:] > p).all())
+    got = t.cpu().numpy()
+    assert np.array_equal(np.sort(got), np.sort(a))

@@ -1,0 +1,5 @@
+cd $GRAFT_REPO_ROOT
+python tools/prof_pass.py --passes 2 --sort 1 > gpurun_out/plain.log 2>&1 && \
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_sort.csv python tools/prof_pass.py --passes 2 --sort 1 > gpurun_out/ncu1.log 2>&1; echo NCU1 $?
+ncu --set full --clock-control none --import-source on -k regex:k_partition -s 1 -c 1 -o gpurun_out/prof_part python tools/prof_pass.py --passes 2 --sort 0 > gpurun_out/ncu2.log 2>&1; echo NCU2 $?
+ncu --set full --clock-control none --import-source on -k regex:k_leaf -c 1 -o gpurun_out/prof_leaf python tools/prof_pass.py --passes 0 --sort 1 > gpurun_out/ncu3.log 2>&1; echo NCU3 $?
