@@ -147,7 +147,7 @@ struct alignas(64) LevelCtrl {
     uint32_t pad[2];
     unsigned long long element_passes;  // sum of partitioned lengths this level
     unsigned long long band_elems;      // equal-band elements this level
-    unsigned long long pad2[2];
+    uint32_t nleaf_cls[4];              // leaves appended per network-size class
 };
 static_assert(sizeof(LevelCtrl) == 64, "LevelCtrl layout");
 

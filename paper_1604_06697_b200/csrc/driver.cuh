@@ -70,8 +70,9 @@ Layout<KT> make_layout(size_t n) {
     L.segs[1] = take(L.max_segs * sizeof(Seg));
     L.cursor = take(L.max_segs * sizeof(unsigned long long));
     L.ecursor = take(L.max_segs * sizeof(uint32_t));
-    L.leaves[0] = take(L.max_leaves * sizeof(Leaf));
-    L.leaves[1] = take(L.max_leaves * sizeof(Leaf));
+    // one list per leaf network-size class (leaf.cuh), max_leaves each
+    L.leaves[0] = take(leaf_nclass<KT>() * L.max_leaves * sizeof(Leaf));
+    L.leaves[1] = take(leaf_nclass<KT>() * L.max_leaves * sizeof(Leaf));
     L.fallback = take(L.max_fb * sizeof(Leaf));
     L.ctrl = take(MAX_LEVELS * sizeof(LevelCtrl));
     L.misc = take(256);
@@ -85,7 +86,6 @@ struct Kernels {
     static constexpr int IPT = Tune<KT>::PART_IPT;
     static constexpr int STAGES = Tune<KT>::PART_STAGES;
     static constexpr int MINB = Tune<KT>::PART_MINB;
-    static constexpr int LNT = Tune<KT>::LEAF_THREADS;
 };
 
 // Persistent launch of the partition kernel: min(ntiles, resident CTAs).
@@ -120,15 +120,9 @@ bq_status launch_partition(const PassParams<KT> &P, cudaStream_t s) {
 }
 
 template <class KT>
-bq_status prepare_leaf_kernel() {
-    // dynamic shared memory beyond 48 KB must be opted into per kernel
-    static int done = 0;
-    if (!done) {
-        BQ_CK(cudaFuncSetAttribute(k_leaf<KT, Kernels<KT>::LNT>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)leaf_smem_bytes<KT>()));
-        done = 1;
-    }
+bq_status launch_leaves(int cls, const LeafParams<KT> &LP, uint32_t count, cudaStream_t s) {
+    if (count == 0) return BQ_OK;
+    BQ_CK(launch_leaf_class<KT>(cls, LP, count, s));
     return BQ_OK;
 }
 
@@ -346,8 +340,8 @@ bq_status run_fallback(const Leaf &f, typename KT::T *user, typename KT::T *scra
     LP.bufs[1] = scratch;
     LP.out = nullptr;
     LP.out_inplace = 1;
-    k_leaf<KT, Kernels<KT>::LNT><<<nch, Kernels<KT>::LNT, leaf_smem_bytes<KT>(), s>>>(LP);
-    BQ_CK_LAUNCH();
+    bq_status st = launch_leaves<KT>(leaf_nclass<KT>() - 1, LP, nch, s);
+    if (st != BQ_OK) return st;
     uint32_t cur = f.parity;
     for (uint64_t w = S; w < f.len; w *= 2) {
         const uint64_t threads = (f.len + MERGE_IPT - 1) / MERGE_IPT;
@@ -394,8 +388,6 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
         for (size_t m = n; m > 1; m >>= 1) lg++;
         depth_limit = 2 * lg + 3;   // P:295, P:1224 (2*ilogb(n)+3)
     }
-    st = prepare_leaf_kernel<KT>();
-    if (st != BQ_OK) return st;
 
     const Layout<KT> L = make_layout<KT>(n);
     char *w = static_cast<char *>(ws);
@@ -422,8 +414,8 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
         BQ_CK_LAUNCH();
         local.kernel_launches++;
         LP.leaves = leaves[0];
-        k_leaf<KT, Kn::LNT><<<1, Kn::LNT, leaf_smem_bytes<KT>(), s>>>(LP);
-        BQ_CK_LAUNCH();
+        st = launch_leaves<KT>((int)leaf_class<KT>((uint32_t)n), LP, 1, s);
+        if (st != BQ_OK) return st;
         local.kernel_launches++;
         local.leaves = 1;
         if (stats) *stats = local;
@@ -493,6 +485,7 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
         Q.fallback_count = fb_count;
         Q.d_counts = nullptr;
         Q.leaf_max = S;
+        Q.leaf_cap = (uint32_t)L.max_leaves;
         Q.depth_limit = depth_limit;
         Q.pivot_rule = rule;
         Q.emit_children = 1;
@@ -507,11 +500,12 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
         LevelCtrl hc;
         BQ_CK(cudaMemcpyAsync(&hc, ctrl + level, sizeof hc, cudaMemcpyDeviceToHost, s));
         BQ_CK(cudaStreamSynchronize(s));
-        if (hc.nleaf) {
-            LP.leaves = leaves[level & 1];
-            k_leaf<KT, Kn::LNT><<<hc.nleaf, Kn::LNT, leaf_smem_bytes<KT>(), s>>>(LP);
-            BQ_CK_LAUNCH();
-        local.kernel_launches++;
+        for (int c = 0; c < leaf_nclass<KT>(); c++) {
+            if (!hc.nleaf_cls[c]) continue;
+            LP.leaves = leaves[level & 1] + (size_t)c * L.max_leaves;
+            st = launch_leaves<KT>(c, LP, hc.nleaf_cls[c], s);
+            if (st != BQ_OK) { cleanup(); return st; }
+            local.kernel_launches++;
         }
         local.partitioned_segments += nseg;
         local.element_passes += hc.element_passes;

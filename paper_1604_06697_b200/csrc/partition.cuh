@@ -24,6 +24,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "leaf.cuh"
 
 namespace bq {
 
@@ -66,6 +67,7 @@ struct PostParams {
     uint32_t *fallback_count;
     uint64_t *d_counts;     // pass mode: {split, n_equal, n_greater}
     uint32_t leaf_max;      // S
+    uint32_t leaf_cap;      // capacity of each leaf-class list
     int32_t depth_limit;
     int32_t pivot_rule;
     int emit_children;      // 0 in the standalone pass
@@ -124,8 +126,11 @@ __global__ void __launch_bounds__(NT) k_post(PostParams<KT> Q) {
     for (int c = 0; c < 2; c++) {
         if (cl[c] == 0) continue;
         if (cl[c] <= Q.leaf_max) {
-            const uint32_t li = atomicAdd(&C->nleaf, 1u);
-            Q.leaves[li] = Leaf{cb[c], cl[c], cp, 0};
+            // leaf lists are binned by sorting-network size (leaf.cuh)
+            const uint32_t lc = leaf_class<KT>(cl[c]);
+            const uint32_t li = atomicAdd(&C->nleaf_cls[lc], 1u);
+            atomicAdd(&C->nleaf, 1u);
+            Q.leaves[lc * Q.leaf_cap + li] = Leaf{cb[c], cl[c], cp, 0};
         } else if ((int)cd >= Q.depth_limit) {
             const uint32_t fi = atomicAdd(Q.fallback_count, 1u);
             atomicAdd(&C->nfallback, 1u);
