@@ -114,8 +114,31 @@ bq_status launch_partition_t(const PassParams<KT> &P, cudaStream_t s) {
 // Records always use the ordered (look-back) mode: their equal elements are
 // staged in already-consumed input tiles, which needs ticket-ordered offsets.
 template <class KT>
+bq_status launch_partition_fast(const PassParams<KT> &P, cudaStream_t s) {
+    using Kn = Kernels<KT>;
+    auto kern = k_part_fast<KT, Kn::NT, Kn::IPT, Kn::STAGES, Kn::MINB>;
+    constexpr int smem = fast_smem_bytes<KT>();
+    constexpr int threads = Kn::NT + 32;
+    static int cap = 0;
+    if (cap == 0) {
+        BQ_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        int nb = 0, dev = 0, sms = 0;
+        BQ_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, threads, smem));
+        BQ_CK(cudaGetDevice(&dev));
+        BQ_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        if (nb < 1) return set_error(BQ_ERR_CUDA, "partition kernel does not fit on an SM");
+        cap = nb * sms;
+    }
+    const uint32_t grid = P.ntiles < (uint32_t)cap ? P.ntiles : (uint32_t)cap;
+    kern<<<grid, threads, smem, s>>>(P);
+    BQ_CK_LAUNCH();
+    return BQ_OK;
+}
+
+template <class KT>
 bq_status launch_partition(const PassParams<KT> &P, cudaStream_t s) {
     if (P.ordered || KT::is_record) return launch_partition_t<KT, true>(P, s);
+    if constexpr (!KT::is_record) return launch_partition_fast<KT>(P, s);
     return launch_partition_t<KT, false>(P, s);
 }
 

@@ -50,6 +50,7 @@ struct PassParams {
 }  // namespace bq
 
 #include "partition_kernel.cuh"
+#include "partition_fast.cuh"
 
 namespace bq {
 
