@@ -144,7 +144,8 @@ struct alignas(64) LevelCtrl {
     uint32_t maxtiles_next;  // largest child tile count
     uint32_t nleaf;          // leaves appended by this level
     uint32_t nfallback;      // depth-capped segments appended by this level
-    uint32_t pad[2];
+    uint32_t nbig;           // equal bands left to k_fill
+    uint32_t pad;
     unsigned long long element_passes;  // sum of partitioned lengths this level
     unsigned long long band_elems;      // equal-band elements this level
     uint32_t nleaf_cls[4];              // leaves appended per network-size class

@@ -4,11 +4,11 @@
 //
 // Level loop (one iteration per recursion level, all segments of the level at
 // once):
-//   k_map        tile -> segment map, look-back words reset
 //   k_partition  a2-a5 for every tile of every segment of the level
-//   k_post       a6 equal bands, a7 children -> next level / leaves / fallback
-//   (records) k_band2
+//   k_post       one CTA per segment: a6 equal band, a7 children -> next level
+//                (pivot a1, tile map, cursor) / leaves / fallback
 //   one 64-byte counter read-back per level (host decides whether to go on)
+//   k_fill       (only if a band was too long for k_post) tile-parallel bands
 //   k_leaf       a8 for this level's leaves
 // then a9 for depth-capped segments.  Every launch goes to the caller's stream.
 #pragma once
@@ -48,7 +48,7 @@ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 template <class KT>
 struct Layout {
-    size_t scratch, status, tile_map, segs[2], cursor, ecursor, leaves[2], fallback, ctrl, misc, total;
+    size_t scratch, status, tile_map[2], segs[2], cursor[2], ecursor[2], leaves[2], fallback, ctrl, misc, total;
     size_t max_tiles, max_segs, max_leaves, max_fb;
 };
 
@@ -65,11 +65,14 @@ Layout<KT> make_layout(size_t n) {
     auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + bytes, 256); return o; };
     L.scratch = take(n * sizeof(typename KT::T));
     L.status = take(L.max_tiles * sizeof(uint64_t));
-    L.tile_map = take(L.max_tiles * sizeof(uint32_t));
-    L.segs[0] = take(L.max_segs * sizeof(Seg));
-    L.segs[1] = take(L.max_segs * sizeof(Seg));
-    L.cursor = take(L.max_segs * sizeof(unsigned long long));
-    L.ecursor = take(L.max_segs * sizeof(uint32_t));
+    // per-level arrays ping-pong between consecutive levels (k_post writes the
+    // next level's while k_fill may still read the current one)
+    for (int p = 0; p < 2; p++) {
+        L.tile_map[p] = take(L.max_tiles * sizeof(uint32_t));
+        L.segs[p] = take(L.max_segs * sizeof(Seg));
+        L.cursor[p] = take(L.max_segs * sizeof(unsigned long long));
+        L.ecursor[p] = take(L.max_segs * sizeof(uint32_t));
+    }
     // one list per leaf network-size class (leaf.cuh), max_leaves each
     L.leaves[0] = take(leaf_nclass<KT>() * L.max_leaves * sizeof(Leaf));
     L.leaves[1] = take(leaf_nclass<KT>() * L.max_leaves * sizeof(Leaf));
@@ -166,6 +169,39 @@ bq_status validate(const void *data, size_t n, void *ws, size_t ws_bytes) {
     return check_device();
 }
 
+constexpr uint32_t FILL_GRID = 148 * 8;
+// equal bands up to this many elements are filled by k_post's CTA for the
+// segment; longer ones (duplicate-heavy inputs) tile-parallel by k_fill
+constexpr uint32_t BAND_INLINE_MAX = 1u << 16;
+
+// Equal bands left to k_fill (records: both phases).
+template <class KT>
+bq_status launch_fill(const PostParams<KT> &Q, cudaStream_t s) {
+    const uint32_t grid = Q.pass.ntiles < FILL_GRID ? Q.pass.ntiles : FILL_GRID;
+    if (grid == 0) return BQ_OK;
+    k_fill<KT, POST_THREADS><<<grid, POST_THREADS, 0, s>>>(Q, 0);
+    BQ_CK_LAUNCH();
+    if (KT::is_record) {
+        k_fill<KT, POST_THREADS><<<grid, POST_THREADS, 0, s>>>(Q, 1);
+        BQ_CK_LAUNCH();
+    }
+    return BQ_OK;
+}
+
+// After a standalone pass (no children): per-segment counts, then every
+// equal band tile-parallel.  Fully asynchronous.
+template <class KT>
+bq_status launch_pass_post(const PassParams<KT> &P, uint32_t nseg, uint64_t *d_counts, cudaStream_t s) {
+    PostParams<KT> Q{};
+    Q.pass = P;
+    Q.d_counts = d_counts;
+    Q.emit_children = 0;
+    Q.band_inline_max = 0;
+    k_post<KT, POST_THREADS><<<nseg, POST_THREADS, 0, s>>>(Q);
+    BQ_CK_LAUNCH();
+    return launch_fill<KT>(Q, s);
+}
+
 // One out-of-place three-way pass over a single segment [0, n).
 template <class KT>
 bq_status run_pass(const typename KT::T *src, typename KT::T *dst, typename KT::T *stage, size_t n,
@@ -175,8 +211,8 @@ bq_status run_pass(const typename KT::T *src, typename KT::T *dst, typename KT::
     const Layout<KT> L = make_layout<KT>(n);
     char *w = static_cast<char *>(ws);
     uint64_t *status = reinterpret_cast<uint64_t *>(w + L.status);
-    unsigned long long *cursor = reinterpret_cast<unsigned long long *>(w + L.cursor);
-    uint32_t *ecursor = reinterpret_cast<uint32_t *>(w + L.ecursor);
+    unsigned long long *cursor = reinterpret_cast<unsigned long long *>(w + L.cursor[0]);
+    uint32_t *ecursor = reinterpret_cast<uint32_t *>(w + L.ecursor[0]);
     LevelCtrl *ctrl = reinterpret_cast<LevelCtrl *>(w + L.ctrl);
     if (n == 0) {
         BQ_CK(cudaMemsetAsync(d_counts, 0, 3 * sizeof(uint64_t), s));
@@ -205,13 +241,7 @@ bq_status run_pass(const typename KT::T *src, typename KT::T *dst, typename KT::
     P.ordered = ordered;
     bq_status st = launch_partition<KT>(P, s);
     if (st != BQ_OK) return st;
-    PostParams<KT> Q{};
-    Q.pass = P;
-    Q.d_counts = d_counts;
-    Q.emit_children = 0;
-    k_post<KT, POST_THREADS><<<ntiles, POST_THREADS, 0, s>>>(Q);
-    BQ_CK_LAUNCH();
-    return BQ_OK;
+    return launch_pass_post<KT>(P, 1, d_counts, s);
 }
 
 template <class KT>
@@ -311,10 +341,10 @@ bq_status run_partition_segments(const typename KT::T *src, typename KT::T *dst,
     char *w = static_cast<char *>(ws);
     T *scratch = reinterpret_cast<T *>(w + L.scratch);
     uint64_t *status = reinterpret_cast<uint64_t *>(w + L.status);
-    uint32_t *tile_map = reinterpret_cast<uint32_t *>(w + L.tile_map);
+    uint32_t *tile_map = reinterpret_cast<uint32_t *>(w + L.tile_map[0]);
     Seg *segs = reinterpret_cast<Seg *>(w + L.segs[0]);
-    unsigned long long *cursor = reinterpret_cast<unsigned long long *>(w + L.cursor);
-    uint32_t *ecursor = reinterpret_cast<uint32_t *>(w + L.ecursor);
+    unsigned long long *cursor = reinterpret_cast<unsigned long long *>(w + L.cursor[0]);
+    uint32_t *ecursor = reinterpret_cast<uint32_t *>(w + L.ecursor[0]);
     LevelCtrl *ctrl = reinterpret_cast<LevelCtrl *>(w + L.ctrl);
     BQ_CK(cudaMemcpyAsync(segs, hs.data(), nseg * sizeof(Seg), cudaMemcpyHostToDevice, s));
     BQ_CK(cudaMemsetAsync(ctrl, 0, sizeof(LevelCtrl), s));
@@ -337,12 +367,8 @@ bq_status run_partition_segments(const typename KT::T *src, typename KT::T *dst,
     P.ordered = ordered;
     st = launch_partition<KT>(P, s);
     if (st != BQ_OK) return st;
-    PostParams<KT> Q{};
-    Q.pass = P;
-    Q.d_counts = d_counts;
-    Q.emit_children = 0;
-    k_post<KT, POST_THREADS><<<(uint32_t)tiles, POST_THREADS, 0, s>>>(Q);
-    BQ_CK_LAUNCH();
+    st = launch_pass_post<KT>(P, (uint32_t)nseg, d_counts, s);
+    if (st != BQ_OK) return st;
     BQ_CK(cudaStreamSynchronize(s));
     return BQ_OK;
 }
@@ -417,10 +443,18 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
     T *user = data;
     T *scratch = reinterpret_cast<T *>(w + L.scratch);
     uint64_t *status = reinterpret_cast<uint64_t *>(w + L.status);
-    uint32_t *tile_map = reinterpret_cast<uint32_t *>(w + L.tile_map);
-    Seg *segs[2] = {reinterpret_cast<Seg *>(w + L.segs[0]), reinterpret_cast<Seg *>(w + L.segs[1])};
-    unsigned long long *cursor = reinterpret_cast<unsigned long long *>(w + L.cursor);
-    uint32_t *ecursor = reinterpret_cast<uint32_t *>(w + L.ecursor);
+    uint32_t *tile_map[2];
+    Seg *segs[2];
+    unsigned long long *cursor[2];
+    uint32_t *ecursor[2];
+    for (int p = 0; p < 2; p++) {
+        tile_map[p] = reinterpret_cast<uint32_t *>(w + L.tile_map[p]);
+        segs[p] = reinterpret_cast<Seg *>(w + L.segs[p]);
+        cursor[p] = reinterpret_cast<unsigned long long *>(w + L.cursor[p]);
+        ecursor[p] = reinterpret_cast<uint32_t *>(w + L.ecursor[p]);
+    }
+    // look-back words are only used by the ordered placement (records always)
+    uint64_t *lb_status = (ordered || KT::is_record) ? status : nullptr;
     Leaf *leaves[2] = {reinterpret_cast<Leaf *>(w + L.leaves[0]), reinterpret_cast<Leaf *>(w + L.leaves[1])};
     Leaf *fallback = reinterpret_cast<Leaf *>(w + L.fallback);
     LevelCtrl *ctrl = reinterpret_cast<LevelCtrl *>(w + L.ctrl);
@@ -447,14 +481,18 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
 
     BQ_CK(cudaMemsetAsync(ctrl, 0, MAX_LEVELS * sizeof(LevelCtrl), s));
     BQ_CK(cudaMemsetAsync(fb_count, 0, sizeof(uint32_t), s));
-    k_init_root<KT><<<1, 1, 0, s>>>(segs[0], user, (uint32_t)n, rule);
-    BQ_CK_LAUNCH();
+    {
+        const uint32_t nt0 = seg_ntiles(0, (uint32_t)n, TILE);
+        k_init_root<KT><<<(nt0 + 255) / 256, 256, 0, s>>>(segs[0], tile_map[0], cursor[0], ecursor[0], lb_status,
+                                                          user, (uint32_t)n, rule);
+        BQ_CK_LAUNCH();
         local.kernel_launches++;
+    }
 
     std::vector<cudaEvent_t> evs;
     auto cleanup = [&]() { for (auto e : evs) cudaEventDestroy(e); };
 
-    uint32_t nseg = 1, ntiles = seg_ntiles(0, (uint32_t)n, TILE), maxtiles = ntiles;
+    uint32_t nseg = 1, ntiles = seg_ntiles(0, (uint32_t)n, TILE);
     uint32_t nfb_total = 0;
     const int aligned = aligned16(user) && aligned16(scratch);
     int level = 0;
@@ -463,12 +501,7 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
             cleanup();
             return set_error(BQ_ERR_CUDA, "level loop did not terminate");
         }
-        Seg *cur = segs[level & 1];
-        Seg *nxt = segs[(level + 1) & 1];
-        dim3 mg(nseg, (maxtiles + 255) / 256);
-        k_map<<<mg, 256, 0, s>>>(cur, tile_map, status, cursor, ecursor);
-        BQ_CK_LAUNCH();
-        local.kernel_launches++;
+        const int cp = level & 1, np = cp ^ 1;
 
         PassParams<KT> P{};
         P.bufs[0] = user;
@@ -476,11 +509,11 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
         P.stage[0] = user;
         P.stage[1] = scratch;
         P.final_buf = user;
-        P.segs = cur;
-        P.tile_map = tile_map;
-        P.status = status;
-        P.cursor = cursor;
-        P.ecursor = ecursor;
+        P.segs = segs[cp];
+        P.tile_map = tile_map[cp];
+        P.status = lb_status;
+        P.cursor = cursor[cp];
+        P.ecursor = ecursor[cp];
         P.ordered = ordered;
         P.ctrl = ctrl + level;
         P.ntiles = ntiles;
@@ -502,7 +535,11 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
 
         PostParams<KT> Q{};
         Q.pass = P;
-        Q.next_segs = nxt;
+        Q.next_segs = segs[np];
+        Q.next_tile_map = tile_map[np];
+        Q.next_cursor = cursor[np];
+        Q.next_ecursor = ecursor[np];
+        Q.band_inline_max = BAND_INLINE_MAX;
         Q.leaves = leaves[level & 1];
         Q.fallback = fallback;
         Q.fallback_count = fb_count;
@@ -512,17 +549,17 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
         Q.depth_limit = depth_limit;
         Q.pivot_rule = rule;
         Q.emit_children = 1;
-        k_post<KT, POST_THREADS><<<ntiles, POST_THREADS, 0, s>>>(Q);
+        k_post<KT, POST_THREADS><<<nseg, POST_THREADS, 0, s>>>(Q);
         BQ_CK_LAUNCH();
         local.kernel_launches++;
-        if (KT::is_record) {
-            k_band2<KT, POST_THREADS><<<ntiles, POST_THREADS, 0, s>>>(P);
-            BQ_CK_LAUNCH();
-        local.kernel_launches++;
-        }
         LevelCtrl hc;
         BQ_CK(cudaMemcpyAsync(&hc, ctrl + level, sizeof hc, cudaMemcpyDeviceToHost, s));
         BQ_CK(cudaStreamSynchronize(s));
+        if (hc.nbig) {
+            st = launch_fill<KT>(Q, s);
+            if (st != BQ_OK) { cleanup(); return st; }
+            local.kernel_launches += KT::is_record ? 2 : 1;
+        }
         for (int c = 0; c < leaf_nclass<KT>(); c++) {
             if (!hc.nleaf_cls[c]) continue;
             LP.leaves = leaves[level & 1] + (size_t)c * L.max_leaves;
@@ -537,7 +574,6 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
         nfb_total += hc.nfallback;
         nseg = hc.nseg_next;
         ntiles = hc.ntiles_next;
-        maxtiles = hc.maxtiles_next;
     }
     local.levels = (uint32_t)level;
     local.fallback_segments = nfb_total;

@@ -60,120 +60,184 @@ namespace bq {
 template <class KT>
 struct PostParams {
     using T = typename KT::T;
-    PassParams<KT> pass;
-    // children (a7): next-level segments, leaves, depth-capped segments
+    PassParams<KT> pass;    // the level just partitioned
+    // children (a7): next-level segments with their tile map and cursors, leaves,
+    // depth-capped segments
     Seg *next_segs;
+    uint32_t *next_tile_map;
+    unsigned long long *next_cursor;
+    uint32_t *next_ecursor;
     Leaf *leaves;
     Leaf *fallback;
     uint32_t *fallback_count;
-    uint64_t *d_counts;     // pass mode: {split, n_equal, n_greater}
+    uint64_t *d_counts;     // pass mode: {split, n_equal, n_greater} per segment
     uint32_t leaf_max;      // S
     uint32_t leaf_cap;      // capacity of each leaf-class list
+    uint32_t band_inline_max;  // equal bands up to this size are filled by k_post, larger ones by k_fill
     int32_t depth_limit;
     int32_t pivot_rule;
     int emit_children;      // 0 in the standalone pass
 };
 
-// a6 + a7: one CTA per tile of the level.  Every CTA fills (keys) or copies
-// (records) the part of its segment's equal band that falls inside its tile;
-// the CTA of a segment's first tile pushes the children (the "push larger
-// side / continue on smaller" of P:1238-1252 becomes: both children are
-// appended to the next level, small ones to the leaf list, depth-capped ones
-// to the fallback list — P:293-299).
+template <class KT>
+struct SegCounts {
+    uint32_t L, G, E;
+};
+template <class KT>
+__device__ __forceinline__ SegCounts<KT> seg_counts(const PassParams<KT> &P, uint32_t si, const Seg &sg) {
+    const unsigned long long fin = P.cursor[si];
+    SegCounts<KT> c;
+    c.L = (uint32_t)fin;
+    c.G = (uint32_t)(fin >> 32);
+    c.E = sg.len - c.L - c.G;
+    return c;
+}
+
+// a6 + a7: one CTA per segment of the level.  The CTA fills (keys) or copies
+// (records) the segment's equal band when it is at most band_inline_max long
+// (larger bands are counted in ctrl->nbig and left to k_fill), and pushes the
+// children: the "push larger side / continue on smaller" of P:1238-1252
+// becomes: both children are appended to the next level (with their pivot,
+// a1, their slice of the next tile map and a reset cursor), small ones to the
+// leaf lists, depth-capped ones to the fallback list.
 template <class KT, int NT>
 __global__ void __launch_bounds__(NT) k_post(PostParams<KT> Q) {
     using T = typename KT::T;
     using K = typename KT::K;
     constexpr uint32_t TILE = (uint32_t)tile_elems<KT>();
     const PassParams<KT> &P = Q.pass;
-    const uint32_t t = blockIdx.x;
-    const Seg sg = P.tile_map ? P.segs[P.tile_map[t]] : P.seg0;
-    const uint32_t k = t - sg.tile_base;
-    const unsigned long long fin = P.cursor[P.tile_map ? P.tile_map[t] : 0];
-    const uint32_t L = (uint32_t)fin, G = (uint32_t)(fin >> 32);
-    const uint32_t E = sg.len - L - G;
+    const uint32_t si = blockIdx.x;
+    const Seg sg = P.segs ? P.segs[si] : P.seg0;
+    const SegCounts<KT> cn = seg_counts(P, si, sg);
+    const uint32_t L = cn.L, G = cn.G, E = cn.E;
     const uint64_t b = sg.begin;
-    const uint64_t tbeg = (b / TILE) * TILE + (uint64_t)k * TILE;
-    const uint64_t band0 = b + L, band1 = b + L + E;
-    const uint64_t x0 = tbeg > band0 ? tbeg : band0;
-    const uint64_t x1 = (tbeg + TILE) < band1 ? (tbeg + TILE) : band1;
-    if constexpr (KT::is_record) {
-        // staged equal records: stage[parity][b + j], j in [0, E)
-        const T *stg = sg.parity ? P.stage[1] : P.stage[0];
-        T *tgt = (stg == P.final_buf) ? (sg.parity ? P.bufs[0] : P.bufs[1]) : P.final_buf;
-        for (uint64_t i = x0 + threadIdx.x; i < x1; i += NT) tgt[i] = stg[b + (i - band0)];
-    } else {
-        const T pv = KT::from_key((K)sg.pivot);
-        for (uint64_t i = x0 + threadIdx.x; i < x1; i += NT) P.final_buf[i] = pv;
-    }
-    if (k != 0 || threadIdx.x != 0) return;
+    LevelCtrl *C = P.ctrl;
 
-    if (Q.d_counts) {
-        const uint32_t si = P.tile_map ? P.tile_map[t] : 0;
+    if (E > 0 && E <= Q.band_inline_max) {
+        const uint64_t band0 = b + L;
+        if constexpr (KT::is_record) {
+            // staged equal records: stage[parity][b + j], j < E
+            const T *stg = sg.parity ? P.stage[1] : P.stage[0];
+            if (stg != P.final_buf) {
+                for (uint32_t j = threadIdx.x; j < E; j += NT) P.final_buf[band0 + j] = stg[b + j];
+            } else {
+                // same buffer: move [b, b+E) right by L, last chunk first; a
+                // chunk is read completely before any of it is written
+                for (int64_t c0 = (int64_t)((E - 1) / NT) * NT; c0 >= 0; c0 -= NT) {
+                    const uint32_t j = (uint32_t)c0 + threadIdx.x;
+                    T v;
+                    if (j < E) v = stg[b + j];
+                    __syncthreads();
+                    if (j < E) P.final_buf[band0 + j] = v;
+                    __syncthreads();
+                }
+            }
+        } else {
+            const T pv = KT::from_key((K)sg.pivot);
+            for (uint32_t j = threadIdx.x; j < E; j += NT) P.final_buf[band0 + j] = pv;
+        }
+    }
+    if (threadIdx.x == 0 && E > Q.band_inline_max && Q.emit_children) atomicAdd(&C->nbig, 1u);
+    if (threadIdx.x == 0 && Q.d_counts) {
         Q.d_counts[3 * si + 0] = L;
         Q.d_counts[3 * si + 1] = E;
         Q.d_counts[3 * si + 2] = G;
     }
     if (!Q.emit_children) return;
-    LevelCtrl *C = P.ctrl;
-    atomicAdd(&C->element_passes, (unsigned long long)sg.len);
-    atomicAdd(&C->band_elems, (unsigned long long)E);
-    const uint8_t cp = sg.parity ^ 1;
-    const T *cbuf = cp ? P.bufs[1] : P.bufs[0];
-    const uint32_t cb[2] = {sg.begin, sg.begin + L + E};
-    const uint32_t cl[2] = {L, G};
-    const uint16_t cd = sg.depth + 1;
+
+    __shared__ uint32_t s_idx[2], s_tb[2], s_nt[2];
+    if (threadIdx.x == 0) {
+        atomicAdd(&C->element_passes, (unsigned long long)sg.len);
+        atomicAdd(&C->band_elems, (unsigned long long)E);
+        const uint8_t cp = sg.parity ^ 1;
+        const T *cbuf = cp ? P.bufs[1] : P.bufs[0];
+        const uint32_t cb[2] = {sg.begin, sg.begin + L + E};
+        const uint32_t cl[2] = {L, G};
+        const uint16_t cd = sg.depth + 1;
+#pragma unroll
+        for (int c = 0; c < 2; c++) {
+            s_nt[c] = 0;
+            if (cl[c] == 0) continue;
+            if (cl[c] <= Q.leaf_max) {
+                // leaf lists are binned by sorting-network size (leaf.cuh)
+                const uint32_t lc = leaf_class<KT>(cl[c]);
+                const uint32_t li = atomicAdd(&C->nleaf_cls[lc], 1u);
+                atomicAdd(&C->nleaf, 1u);
+                Q.leaves[lc * Q.leaf_cap + li] = Leaf{cb[c], cl[c], cp, 0};
+            } else if ((int)cd >= Q.depth_limit) {
+                const uint32_t fi = atomicAdd(Q.fallback_count, 1u);
+                atomicAdd(&C->nfallback, 1u);
+                Q.fallback[fi] = Leaf{cb[c], cl[c], cp, 0};
+            } else {
+                Seg ch;
+                ch.pivot = (uint64_t)select_pivot<KT>(cbuf, cb[c], cl[c], Q.pivot_rule);
+                ch.begin = cb[c];
+                ch.len = cl[c];
+                ch.ntiles = seg_ntiles(cb[c], cl[c], TILE);
+                ch.tile_base = atomicAdd(&C->ntiles_next, ch.ntiles);
+                ch.depth = cd;
+                ch.parity = cp;
+                ch.pad0 = 0;
+                ch.pad1 = 0;
+                atomicMax(&C->maxtiles_next, ch.ntiles);
+                const uint32_t ci = atomicAdd(&C->nseg_next, 1u);
+                Q.next_segs[ci] = ch;
+                Q.next_cursor[ci] = 0;
+                Q.next_ecursor[ci] = 0;
+                s_idx[c] = ci;
+                s_tb[c] = ch.tile_base;
+                s_nt[c] = ch.ntiles;
+            }
+        }
+    }
+    __syncthreads();
+    // the children's slices of the next level's tile map (and look-back words)
 #pragma unroll
     for (int c = 0; c < 2; c++) {
-        if (cl[c] == 0) continue;
-        if (cl[c] <= Q.leaf_max) {
-            // leaf lists are binned by sorting-network size (leaf.cuh)
-            const uint32_t lc = leaf_class<KT>(cl[c]);
-            const uint32_t li = atomicAdd(&C->nleaf_cls[lc], 1u);
-            atomicAdd(&C->nleaf, 1u);
-            Q.leaves[lc * Q.leaf_cap + li] = Leaf{cb[c], cl[c], cp, 0};
-        } else if ((int)cd >= Q.depth_limit) {
-            const uint32_t fi = atomicAdd(Q.fallback_count, 1u);
-            atomicAdd(&C->nfallback, 1u);
-            Q.fallback[fi] = Leaf{cb[c], cl[c], cp, 0};
-        } else {
-            Seg ch;
-            ch.pivot = (uint64_t)select_pivot<KT>(cbuf, cb[c], cl[c], Q.pivot_rule);
-            ch.begin = cb[c];
-            ch.len = cl[c];
-            ch.ntiles = seg_ntiles(cb[c], cl[c], TILE);
-            ch.tile_base = atomicAdd(&C->ntiles_next, ch.ntiles);
-            ch.depth = cd;
-            ch.parity = cp;
-            ch.pad0 = 0;
-            ch.pad1 = 0;
-            atomicMax(&C->maxtiles_next, ch.ntiles);
-            const uint32_t si = atomicAdd(&C->nseg_next, 1u);
-            Q.next_segs[si] = ch;
+        const uint32_t nt = s_nt[c], tb = s_tb[c], ci = s_idx[c];
+        for (uint32_t j = threadIdx.x; j < nt; j += NT) {
+            Q.next_tile_map[tb + j] = ci;
+            if (P.status) P.status[tb + j] = 0;
         }
     }
 }
 
-// Records whose equal band was staged in the user buffer itself were copied
-// to the other buffer by k_post; move them into the user buffer.
+// Equal bands longer than band_inline_max, tile-parallel over the level
+// (grid-stride): keys are filled with the pivot's bits; records are copied
+// from their staging area — phase 0 copies into the final buffer, or, when
+// the staging area is the final buffer itself (it may overlap the band), into
+// the other buffer, from where phase 1 copies them into the final buffer.
 template <class KT, int NT>
-__global__ void __launch_bounds__(NT) k_band2(PassParams<KT> P) {
+__global__ void __launch_bounds__(NT) k_fill(PostParams<KT> Q, int phase) {
     using T = typename KT::T;
+    using K = typename KT::K;
     constexpr uint32_t TILE = (uint32_t)tile_elems<KT>();
-    const uint32_t t = blockIdx.x;
-    const Seg sg = P.tile_map ? P.segs[P.tile_map[t]] : P.seg0;
-    if ((sg.parity ? P.stage[1] : P.stage[0]) != P.final_buf) return;
-    const uint32_t k = t - sg.tile_base;
-    const unsigned long long fin = P.cursor[P.tile_map ? P.tile_map[t] : 0];
-    const uint32_t L = (uint32_t)fin, G = (uint32_t)(fin >> 32);
-    const uint32_t E = sg.len - L - G;
-    const uint64_t b = sg.begin;
-    const uint64_t tbeg = (b / TILE) * TILE + (uint64_t)k * TILE;
-    const uint64_t band0 = b + L, band1 = b + L + E;
-    const uint64_t x0 = tbeg > band0 ? tbeg : band0;
-    const uint64_t x1 = (tbeg + TILE) < band1 ? (tbeg + TILE) : band1;
-    const T *from = sg.parity ? P.bufs[0] : P.bufs[1];
-    for (uint64_t i = x0 + threadIdx.x; i < x1; i += NT) P.final_buf[i] = from[i];
+    const PassParams<KT> &P = Q.pass;
+    for (uint32_t t = blockIdx.x; t < P.ntiles; t += gridDim.x) {
+        const uint32_t si = P.tile_map ? P.tile_map[t] : 0;
+        const Seg sg = P.segs ? P.segs[si] : P.seg0;
+        const SegCounts<KT> cn = seg_counts(P, si, sg);
+        if (cn.E <= Q.band_inline_max) continue;
+        const uint64_t b = sg.begin;
+        const uint64_t tbeg = (b / TILE) * TILE + (uint64_t)(t - sg.tile_base) * TILE;
+        const uint64_t band0 = b + cn.L, band1 = band0 + cn.E;
+        const uint64_t x0 = tbeg > band0 ? tbeg : band0;
+        const uint64_t x1 = (tbeg + TILE) < band1 ? (tbeg + TILE) : band1;
+        if constexpr (KT::is_record) {
+            const T *stg = sg.parity ? P.stage[1] : P.stage[0];
+            T *other = sg.parity ? P.bufs[0] : P.bufs[1];
+            if (phase == 0) {
+                T *tgt = (stg == P.final_buf) ? other : P.final_buf;
+                for (uint64_t i = x0 + threadIdx.x; i < x1; i += NT) tgt[i] = stg[b + (i - band0)];
+            } else if (stg == P.final_buf) {
+                for (uint64_t i = x0 + threadIdx.x; i < x1; i += NT) P.final_buf[i] = other[i];
+            }
+        } else {
+            if (phase != 0) continue;
+            const T pv = KT::from_key((K)sg.pivot);
+            for (uint64_t i = x0 + threadIdx.x; i < x1; i += NT) P.final_buf[i] = pv;
+        }
+    }
 }
 
 // Tile map + status reset for a level: tile_map[tile_base + j] = segment.
@@ -191,21 +255,32 @@ static __global__ void k_map(const Seg *segs, uint32_t *tile_map, uint64_t *stat
     }
 }
 
-// Root segment of a sort: [0, n) in the user buffer with its pivot (a1).
+// Root segment of a sort: [0, n) in the user buffer with its pivot (a1), its
+// tile map, cursor and look-back words.
 template <class KT>
-__global__ void k_init_root(Seg *segs, const typename KT::T *buf, uint32_t n, int rule) {
+__global__ void k_init_root(Seg *segs, uint32_t *tile_map, unsigned long long *cursor, uint32_t *ecursor,
+                            uint64_t *status, const typename KT::T *buf, uint32_t n, int rule) {
     constexpr uint32_t TILE = (uint32_t)tile_elems<KT>();
-    Seg s;
-    s.pivot = (uint64_t)select_pivot<KT>(buf, 0, n, rule);
-    s.begin = 0;
-    s.len = n;
-    s.tile_base = 0;
-    s.ntiles = seg_ntiles(0, n, TILE);
-    s.depth = 0;
-    s.parity = 0;
-    s.pad0 = 0;
-    s.pad1 = 0;
-    segs[0] = s;
+    const uint32_t nt = seg_ntiles(0, n, TILE);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        Seg s;
+        s.pivot = (uint64_t)select_pivot<KT>(buf, 0, n, rule);
+        s.begin = 0;
+        s.len = n;
+        s.tile_base = 0;
+        s.ntiles = nt;
+        s.depth = 0;
+        s.parity = 0;
+        s.pad0 = 0;
+        s.pad1 = 0;
+        segs[0] = s;
+        cursor[0] = 0;
+        ecursor[0] = 0;
+    }
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < nt; j += gridDim.x * blockDim.x) {
+        tile_map[j] = 0;
+        if (status) status[j] = 0;
+    }
 }
 
 // bq_pivot_*: the pivot key of buf[0, n).
