@@ -28,6 +28,9 @@
 namespace bq {
 
 constexpr int MAX_LEVELS = 128;
+// the level loop is enqueued LEVEL_BATCH levels at a time between host checks
+constexpr int LEVEL_BATCH = 4;
+constexpr uint32_t POST_GRID = 148 * 8;
 constexpr int POST_THREADS = 256;
 constexpr int MERGE_THREADS = 256, MERGE_IPT = 8;
 
@@ -59,7 +62,8 @@ Layout<KT> make_layout(size_t n) {
     Layout<KT> L;
     L.max_segs = n / (S + 1) + 2;                 // segments > S are disjoint
     L.max_tiles = n / TILE + 2 * L.max_segs + 2;
-    L.max_leaves = 2 * L.max_segs + 2 + (n / S + 2);   // per level; also fallback chunks
+    // leaves of one batch of LEVEL_BATCH levels per class list; also fallback chunks
+    L.max_leaves = LEVEL_BATCH * (2 * L.max_segs + 2) + (n / S + 2);
     L.max_fb = n / (S + 1) + 2;
     size_t off = 0;
     auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + bytes, 256); return o; };
@@ -77,8 +81,8 @@ Layout<KT> make_layout(size_t n) {
     L.leaves[0] = take(leaf_nclass<KT>() * L.max_leaves * sizeof(Leaf));
     L.leaves[1] = take(leaf_nclass<KT>() * L.max_leaves * sizeof(Leaf));
     L.fallback = take(L.max_fb * sizeof(Leaf));
-    L.ctrl = take(MAX_LEVELS * sizeof(LevelCtrl));
-    L.misc = take(256);
+    L.ctrl = take((MAX_LEVELS + 1) * sizeof(LevelCtrl));   // [MAX_LEVELS]: the root's counts
+    L.misc = take(256);   // fallback count, leaf-list counts (2 sets x 4 classes), pass counts
     L.total = off;
     return L;
 }
@@ -147,7 +151,7 @@ bq_status launch_partition(const PassParams<KT> &P, cudaStream_t s) {
 
 template <class KT>
 bq_status launch_leaves(int cls, const LeafParams<KT> &LP, uint32_t count, cudaStream_t s) {
-    if (count == 0) return BQ_OK;
+    if (count == 0 && LP.count_dev == nullptr) return BQ_OK;   // count 0 + count_dev: persistent grid
     BQ_CK(launch_leaf_class<KT>(cls, LP, count, s));
     return BQ_OK;
 }
@@ -197,7 +201,8 @@ bq_status launch_pass_post(const PassParams<KT> &P, uint32_t nseg, uint64_t *d_c
     Q.d_counts = d_counts;
     Q.emit_children = 0;
     Q.band_inline_max = 0;
-    k_post<KT, POST_THREADS><<<nseg, POST_THREADS, 0, s>>>(Q);
+    Q.nseg = nseg;
+    k_post<KT, POST_THREADS><<<nseg < POST_GRID ? nseg : POST_GRID, POST_THREADS, 0, s>>>(Q);
     BQ_CK_LAUNCH();
     return launch_fill<KT>(Q, s);
 }
@@ -412,7 +417,7 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
     using T = typename KT::T;
     constexpr uint32_t TILE = tile_elems<KT>();
     constexpr uint32_t S = Tune<KT>::LEAF;
-    using Kn = Kernels<KT>;
+    constexpr int NCLS = leaf_nclass<KT>();
     bq_sort_stats local;
     std::memset(&local, 0, sizeof local);
     int rule = BQ_PIVOT_NINTHER, depth_limit = -1, timing = 0, ordered = 0;
@@ -458,7 +463,9 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
     Leaf *leaves[2] = {reinterpret_cast<Leaf *>(w + L.leaves[0]), reinterpret_cast<Leaf *>(w + L.leaves[1])};
     Leaf *fallback = reinterpret_cast<Leaf *>(w + L.fallback);
     LevelCtrl *ctrl = reinterpret_cast<LevelCtrl *>(w + L.ctrl);
+    LevelCtrl *root = ctrl + MAX_LEVELS;
     uint32_t *fb_count = reinterpret_cast<uint32_t *>(w + L.misc);
+    uint32_t *leaf_counts[2] = {fb_count + 4, fb_count + 8};   // [set][class]
 
     LeafParams<KT> LP{};
     LP.bufs[0] = user;
@@ -479,109 +486,161 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
         return BQ_OK;
     }
 
-    BQ_CK(cudaMemsetAsync(ctrl, 0, MAX_LEVELS * sizeof(LevelCtrl), s));
-    BQ_CK(cudaMemsetAsync(fb_count, 0, sizeof(uint32_t), s));
+    // Leaves are sorted on a side stream, concurrently with the deeper
+    // partition levels: a batch's leaf lists (set batch & 1) are consumed
+    // there while the main stream partitions the next batch into the other set.
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_levels[2] = {nullptr, nullptr}, ev_leaves[2] = {nullptr, nullptr};
+    std::vector<cudaEvent_t> evs;
+    std::vector<LevelCtrl> hvec(MAX_LEVELS + 1);   // host copy of the control blocks
+    LevelCtrl *hctrl = hvec.data();
+    auto cleanup = [&]() {
+        for (auto e : evs) cudaEventDestroy(e);
+        for (int i = 0; i < 2; i++) {
+            if (ev_levels[i]) cudaEventDestroy(ev_levels[i]);
+            if (ev_leaves[i]) cudaEventDestroy(ev_leaves[i]);
+        }
+        if (side) cudaStreamDestroy(side);
+    };
+#define BQ_CKC(call)                \
+    do {                            \
+        bq_status st_ = [&]() -> bq_status { BQ_CK(call); return BQ_OK; }(); \
+        if (st_ != BQ_OK) { cleanup(); return st_; } \
+    } while (0)
+    BQ_CKC(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; i++) {
+        BQ_CKC(cudaEventCreateWithFlags(&ev_levels[i], cudaEventDisableTiming));
+        BQ_CKC(cudaEventCreateWithFlags(&ev_leaves[i], cudaEventDisableTiming));
+    }
+
+    BQ_CKC(cudaMemsetAsync(ctrl, 0, (MAX_LEVELS + 1) * sizeof(LevelCtrl), s));
+    BQ_CKC(cudaMemsetAsync(fb_count, 0, 12 * sizeof(uint32_t), s));
     {
         const uint32_t nt0 = seg_ntiles(0, (uint32_t)n, TILE);
         k_init_root<KT><<<(nt0 + 255) / 256, 256, 0, s>>>(segs[0], tile_map[0], cursor[0], ecursor[0], lb_status,
-                                                          user, (uint32_t)n, rule);
-        BQ_CK_LAUNCH();
+                                                          root, user, (uint32_t)n, rule);
+        BQ_CKC(cudaGetLastError());
         local.kernel_launches++;
     }
 
-    std::vector<cudaEvent_t> evs;
-    auto cleanup = [&]() { for (auto e : evs) cudaEventDestroy(e); };
-
-    uint32_t nseg = 1, ntiles = seg_ntiles(0, (uint32_t)n, TILE);
-    uint32_t nfb_total = 0;
     const int aligned = aligned16(user) && aligned16(scratch);
     int level = 0;
-    for (; nseg > 0; level++) {
-        if (level >= MAX_LEVELS - 1) {
+    bool done = false;
+    for (int batch = 0; !done; batch++) {
+        const int set = batch & 1;
+        if (level + LEVEL_BATCH >= MAX_LEVELS) {
             cleanup();
             return set_error(BQ_ERR_CUDA, "level loop did not terminate");
         }
-        const int cp = level & 1, np = cp ^ 1;
+        // the side stream has finished the leaves of batch-2 (same set)
+        if (batch >= 2) BQ_CKC(cudaStreamWaitEvent(s, ev_leaves[set], 0));
+        BQ_CKC(cudaMemsetAsync(leaf_counts[set], 0, 4 * sizeof(uint32_t), s));
+        for (int k = 0; k < LEVEL_BATCH; k++, level++) {
+            const int cp = level & 1, np = cp ^ 1;
+            const LevelCtrl *prev = level == 0 ? root : ctrl + level - 1;
+            PassParams<KT> P{};
+            P.bufs[0] = user;
+            P.bufs[1] = scratch;
+            P.stage[0] = user;
+            P.stage[1] = scratch;
+            P.final_buf = user;
+            P.segs = segs[cp];
+            P.tile_map = tile_map[cp];
+            P.status = lb_status;
+            P.cursor = cursor[cp];
+            P.ecursor = ecursor[cp];
+            P.ordered = ordered;
+            P.ctrl = ctrl + level;
+            P.ntiles = 0xffffffffu;             // upper bound: the grid is the resident capacity
+            P.ntiles_dev = &prev->ntiles_next;
+            P.n_total = n;
+            P.aligned = aligned;
+            if (timing) {
+                cudaEvent_t e0, e1;
+                BQ_CKC(cudaEventCreate(&e0));
+                evs.push_back(e0);
+                BQ_CKC(cudaEventCreate(&e1));
+                evs.push_back(e1);
+                BQ_CKC(cudaEventRecord(e0, s));
+            }
+            st = launch_partition<KT>(P, s);
+            if (st != BQ_OK) { cleanup(); return st; }
+            local.kernel_launches++;
+            if (timing) BQ_CKC(cudaEventRecord(evs.back(), s));
 
-        PassParams<KT> P{};
-        P.bufs[0] = user;
-        P.bufs[1] = scratch;
-        P.stage[0] = user;
-        P.stage[1] = scratch;
-        P.final_buf = user;
-        P.segs = segs[cp];
-        P.tile_map = tile_map[cp];
-        P.status = lb_status;
-        P.cursor = cursor[cp];
-        P.ecursor = ecursor[cp];
-        P.ordered = ordered;
-        P.ctrl = ctrl + level;
-        P.ntiles = ntiles;
-        P.n_total = n;
-        P.aligned = aligned;
-        if (timing) {
-            cudaEvent_t e0, e1;
-            BQ_CK(cudaEventCreate(&e0));
-            evs.push_back(e0);
-            BQ_CK(cudaEventCreate(&e1));
-            evs.push_back(e1);
-            BQ_CK(cudaEventRecord(e0, s));
-        }
-        st = launch_partition<KT>(P, s);
-        if (st != BQ_OK) { cleanup(); return st; }
-        local.kernel_launches++;
-        if (timing) BQ_CK(cudaEventRecord(evs.back(), s));
-        local.partition_launches++;
-
-        PostParams<KT> Q{};
-        Q.pass = P;
-        Q.next_segs = segs[np];
-        Q.next_tile_map = tile_map[np];
-        Q.next_cursor = cursor[np];
-        Q.next_ecursor = ecursor[np];
-        Q.band_inline_max = BAND_INLINE_MAX;
-        Q.leaves = leaves[level & 1];
-        Q.fallback = fallback;
-        Q.fallback_count = fb_count;
-        Q.d_counts = nullptr;
-        Q.leaf_max = S;
-        Q.leaf_cap = (uint32_t)L.max_leaves;
-        Q.depth_limit = depth_limit;
-        Q.pivot_rule = rule;
-        Q.emit_children = 1;
-        k_post<KT, POST_THREADS><<<nseg, POST_THREADS, 0, s>>>(Q);
-        BQ_CK_LAUNCH();
-        local.kernel_launches++;
-        LevelCtrl hc;
-        BQ_CK(cudaMemcpyAsync(&hc, ctrl + level, sizeof hc, cudaMemcpyDeviceToHost, s));
-        BQ_CK(cudaStreamSynchronize(s));
-        if (hc.nbig) {
-            st = launch_fill<KT>(Q, s);
+            PostParams<KT> Q{};
+            Q.pass = P;
+            Q.next_segs = segs[np];
+            Q.next_tile_map = tile_map[np];
+            Q.next_cursor = cursor[np];
+            Q.next_ecursor = ecursor[np];
+            Q.band_inline_max = BAND_INLINE_MAX;
+            Q.leaves = leaves[set];
+            Q.leaf_counts = leaf_counts[set];
+            Q.fallback = fallback;
+            Q.fallback_count = fb_count;
+            Q.d_counts = nullptr;
+            Q.nseg_dev = &prev->nseg_next;
+            Q.leaf_max = S;
+            Q.leaf_cap = (uint32_t)L.max_leaves;
+            Q.depth_limit = depth_limit;
+            Q.pivot_rule = rule;
+            Q.emit_children = 1;
+            k_post<KT, POST_THREADS><<<POST_GRID, POST_THREADS, 0, s>>>(Q);
+            BQ_CKC(cudaGetLastError());
+            local.kernel_launches++;
+            st = launch_fill<KT>(Q, s);   // exits at once unless a band was too long for k_post
             if (st != BQ_OK) { cleanup(); return st; }
             local.kernel_launches += KT::is_record ? 2 : 1;
         }
-        for (int c = 0; c < leaf_nclass<KT>(); c++) {
-            if (!hc.nleaf_cls[c]) continue;
-            LP.leaves = leaves[level & 1] + (size_t)c * L.max_leaves;
-            st = launch_leaves<KT>(c, LP, hc.nleaf_cls[c], s);
+        // leaves of this batch on the side stream
+#ifndef BQ_LEAF_MAIN
+        cudaStream_t ls = side;
+#else
+        cudaStream_t ls = s;
+#endif
+        BQ_CKC(cudaEventRecord(ev_levels[set], s));
+        BQ_CKC(cudaStreamWaitEvent(ls, ev_levels[set], 0));
+        for (int c = 0; c < NCLS; c++) {
+            LP.leaves = leaves[set] + (size_t)c * L.max_leaves;
+            LP.count_dev = leaf_counts[set] + c;
+            st = launch_leaves<KT>(c, LP, 0, ls);
             if (st != BQ_OK) { cleanup(); return st; }
             local.kernel_launches++;
         }
-        local.partitioned_segments += nseg;
+        BQ_CKC(cudaEventRecord(ev_leaves[set], ls));
+        // is there a next level?
+        BQ_CKC(cudaMemcpyAsync(hctrl + level - 1, ctrl + level - 1, sizeof(LevelCtrl), cudaMemcpyDeviceToHost, s));
+        BQ_CKC(cudaStreamSynchronize(s));
+        done = hctrl[level - 1].nseg_next == 0;
+    }
+    LP.count_dev = nullptr;
+    BQ_CKC(cudaStreamWaitEvent(s, ev_leaves[0], 0));
+    BQ_CKC(cudaStreamWaitEvent(s, ev_leaves[1], 0));
+
+    // statistics of every level, and the depth-capped segments
+    BQ_CKC(cudaMemcpyAsync(hctrl, ctrl, level * sizeof(LevelCtrl), cudaMemcpyDeviceToHost, s));
+    uint32_t nfb_total = 0;
+    BQ_CKC(cudaMemcpyAsync(&hctrl[MAX_LEVELS].pad, fb_count, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    BQ_CKC(cudaStreamSynchronize(s));
+    nfb_total = hctrl[MAX_LEVELS].pad;
+    for (int l = 0; l < level; l++) {
+        const LevelCtrl &hc = hctrl[l];
+        const uint32_t nseg_l = l == 0 ? 1u : hctrl[l - 1].nseg_next;
+        if (nseg_l == 0) break;
+        local.levels++;
+        local.partition_launches++;
+        local.partitioned_segments += nseg_l;
         local.element_passes += hc.element_passes;
         local.band_elements += hc.band_elems;
         local.leaves += hc.nleaf;
-        nfb_total += hc.nfallback;
-        nseg = hc.nseg_next;
-        ntiles = hc.ntiles_next;
     }
-    local.levels = (uint32_t)level;
     local.fallback_segments = nfb_total;
 
     if (nfb_total) {
         std::vector<Leaf> fl(nfb_total);
-        BQ_CK(cudaMemcpyAsync(fl.data(), fallback, nfb_total * sizeof(Leaf), cudaMemcpyDeviceToHost, s));
-        BQ_CK(cudaStreamSynchronize(s));
+        BQ_CKC(cudaMemcpyAsync(fl.data(), fallback, nfb_total * sizeof(Leaf), cudaMemcpyDeviceToHost, s));
+        BQ_CKC(cudaStreamSynchronize(s));
         for (const Leaf &f : fl) {
             st = run_fallback<KT>(f, user, scratch, leaves[0], s);
             if (st != BQ_OK) { cleanup(); return st; }
@@ -589,15 +648,17 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
     }
     local.partition_bytes = 2.0 * (double)sizeof(T) * (double)local.element_passes;
     if (timing) {
-        BQ_CK(cudaStreamSynchronize(s));
+        BQ_CKC(cudaStreamSynchronize(s));
         double ms = 0;
-        for (size_t i = 0; i + 1 < evs.size(); i += 2) {
+        // only the launches of non-empty levels count
+        for (size_t i = 0; i + 1 < evs.size() && (int)(i / 2) < (int)local.levels; i += 2) {
             float f = 0;
-            BQ_CK(cudaEventElapsedTime(&f, evs[i], evs[i + 1]));
+            BQ_CKC(cudaEventElapsedTime(&f, evs[i], evs[i + 1]));
             ms += f;
         }
         local.partition_ms = ms;
     }
+#undef BQ_CKC
     cleanup();
     if (stats) *stats = local;
     return BQ_OK;

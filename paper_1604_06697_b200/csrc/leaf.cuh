@@ -40,6 +40,7 @@ template <class KT>
 struct LeafParams {
     using T = typename KT::T;
     const Leaf *leaves;
+    const uint32_t *count_dev;   // non-null: persistent grid over *count_dev leaves; else one leaf per CTA
     T *bufs[2];
     T *out;            // destination buffer (the user buffer, or in-place for fallback chunks)
     int out_inplace;   // 1: write back into bufs[parity] (fallback chunk sort)
@@ -360,8 +361,10 @@ __global__ void __launch_bounds__(1 << (L - LeafTraits<KT>::R), (LeafTraits<KT>:
     extern __shared__ __align__(128) unsigned char smem_raw[];
     unsigned char *planes = smem_raw;
     const uint32_t t = threadIdx.x;
-
-    const Leaf lf = P.leaves[blockIdx.x];
+    const uint32_t nleaves = P.count_dev ? *P.count_dev : gridDim.x;
+    for (uint32_t li = blockIdx.x; li < nleaves; li += gridDim.x) {
+    if (li != blockIdx.x) __syncthreads();   // the previous leaf's shared-memory readers are done
+    const Leaf lf = P.leaves[li];
     const uint32_t len = lf.len;
     T *srcbuf = lf.parity ? P.bufs[1] : P.bufs[0];
     T *out = P.out_inplace ? srcbuf : P.out;
@@ -406,20 +409,27 @@ __global__ void __launch_bounds__(1 << (L - LeafTraits<KT>::R), (LeafTraits<KT>:
             if (i < len) out[b + i] = KT::from_key((K)x[r]);
         }
     }
+    }
 }
 
 // host: launch the leaf kernel of class c (NET = 2^(lmin + c)) over `count` leaves
+// count > 0: one CTA per leaf; count == 0: persistent grid (resident CTAs)
+// over LP.count_dev leaves
 template <class KT, int L>
 cudaError_t launch_leaf_l(const LeafParams<KT> &LP, uint32_t count, cudaStream_t s) {
     constexpr size_t smem = leaf_smem_bytes<KT, L>();
     constexpr int NT = 1 << (L - LeafTraits<KT>::R);
-    static bool attr = false;
-    if (!attr) {
+    static int cap = 0;
+    if (cap == 0) {
         cudaError_t e = cudaFuncSetAttribute(k_leaf<KT, L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        attr = true;
+        int nb = 0, dev = 0, sms = 0;
+        if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_leaf<KT, L>, NT, smem)) != cudaSuccess) return e;
+        if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+        if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+        cap = (nb > 0 ? nb : 1) * sms;
     }
-    k_leaf<KT, L><<<count, NT, smem, s>>>(LP);
+    k_leaf<KT, L><<<count ? count : (uint32_t)cap, NT, smem, s>>>(LP);
     return cudaGetLastError();
 }
 

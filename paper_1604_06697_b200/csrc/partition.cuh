@@ -29,6 +29,11 @@
 namespace bq {
 
 template <class KT>
+struct PassParams;
+template <class KT>
+__device__ __forceinline__ uint32_t pass_ntiles(const PassParams<KT> &P);
+
+template <class KT>
 struct PassParams {
     using T = typename KT::T;
     T *bufs[2];            // [parity]: segment data; the pass writes bufs[parity^1]
@@ -42,10 +47,16 @@ struct PassParams {
     uint32_t *ecursor;     // per segment: equal-record running offset (records, fast mode)
     LevelCtrl *ctrl;       // ticket + counters of this level
     uint32_t ntiles;
+    const uint32_t *ntiles_dev;  // non-null: the level's tile count lives in device memory
     uint64_t n_total;      // length of each data buffer (bounds the TMA reads)
     int aligned;           // both data buffers 16-byte aligned -> TMA bulk copies
     int ordered;           // 1: decoupled look-back (deterministic layout), 0: atomic cursor
 };
+
+template <class KT>
+__device__ __forceinline__ uint32_t pass_ntiles(const PassParams<KT> &P) {
+    return P.ntiles_dev ? *P.ntiles_dev : P.ntiles;
+}
 
 }  // namespace bq
 
@@ -67,10 +78,13 @@ struct PostParams {
     uint32_t *next_tile_map;
     unsigned long long *next_cursor;
     uint32_t *next_ecursor;
-    Leaf *leaves;
+    Leaf *leaves;           // leaf lists (one per network-size class, leaf_cap each)
+    uint32_t *leaf_counts;  // their fill counts
     Leaf *fallback;
     uint32_t *fallback_count;
     uint64_t *d_counts;     // pass mode: {split, n_equal, n_greater} per segment
+    uint32_t nseg;          // segments of the level (nseg_dev == nullptr)
+    const uint32_t *nseg_dev;  // non-null: the level's segment count lives in device memory
     uint32_t leaf_max;      // S
     uint32_t leaf_cap;      // capacity of each leaf-class list
     uint32_t band_inline_max;  // equal bands up to this size are filled by k_post, larger ones by k_fill
@@ -101,12 +115,20 @@ __device__ __forceinline__ SegCounts<KT> seg_counts(const PassParams<KT> &P, uin
 // a1, their slice of the next tile map and a reset cursor), small ones to the
 // leaf lists, depth-capped ones to the fallback list.
 template <class KT, int NT>
+__device__ __forceinline__ void post_segment(const PostParams<KT> &Q, uint32_t si);
+
+template <class KT, int NT>
 __global__ void __launch_bounds__(NT) k_post(PostParams<KT> Q) {
+    const uint32_t nseg = Q.nseg_dev ? *Q.nseg_dev : Q.nseg;
+    for (uint32_t si = blockIdx.x; si < nseg; si += gridDim.x) post_segment<KT, NT>(Q, si);
+}
+
+template <class KT, int NT>
+__device__ __forceinline__ void post_segment(const PostParams<KT> &Q, uint32_t si) {
     using T = typename KT::T;
     using K = typename KT::K;
     constexpr uint32_t TILE = (uint32_t)tile_elems<KT>();
     const PassParams<KT> &P = Q.pass;
-    const uint32_t si = blockIdx.x;
     const Seg sg = P.segs ? P.segs[si] : P.seg0;
     const SegCounts<KT> cn = seg_counts(P, si, sg);
     const uint32_t L = cn.L, G = cn.G, E = cn.E;
@@ -146,6 +168,7 @@ __global__ void __launch_bounds__(NT) k_post(PostParams<KT> Q) {
     if (!Q.emit_children) return;
 
     __shared__ uint32_t s_idx[2], s_tb[2], s_nt[2];
+    __syncthreads();   // the previous segment's readers of s_* are done
     if (threadIdx.x == 0) {
         atomicAdd(&C->element_passes, (unsigned long long)sg.len);
         atomicAdd(&C->band_elems, (unsigned long long)E);
@@ -161,7 +184,8 @@ __global__ void __launch_bounds__(NT) k_post(PostParams<KT> Q) {
             if (cl[c] <= Q.leaf_max) {
                 // leaf lists are binned by sorting-network size (leaf.cuh)
                 const uint32_t lc = leaf_class<KT>(cl[c]);
-                const uint32_t li = atomicAdd(&C->nleaf_cls[lc], 1u);
+                const uint32_t li = atomicAdd(&Q.leaf_counts[lc], 1u);
+                atomicAdd(&C->nleaf_cls[lc], 1u);
                 atomicAdd(&C->nleaf, 1u);
                 Q.leaves[lc * Q.leaf_cap + li] = Leaf{cb[c], cl[c], cp, 0};
             } else if ((int)cd >= Q.depth_limit) {
@@ -213,7 +237,9 @@ __global__ void __launch_bounds__(NT) k_fill(PostParams<KT> Q, int phase) {
     using K = typename KT::K;
     constexpr uint32_t TILE = (uint32_t)tile_elems<KT>();
     const PassParams<KT> &P = Q.pass;
-    for (uint32_t t = blockIdx.x; t < P.ntiles; t += gridDim.x) {
+    if (Q.emit_children && P.ctrl->nbig == 0) return;   // sort: no long band this level
+    const uint32_t ntiles = pass_ntiles(P);
+    for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         const uint32_t si = P.tile_map ? P.tile_map[t] : 0;
         const Seg sg = P.segs ? P.segs[si] : P.seg0;
         const SegCounts<KT> cn = seg_counts(P, si, sg);
@@ -259,7 +285,7 @@ static __global__ void k_map(const Seg *segs, uint32_t *tile_map, uint64_t *stat
 // tile map, cursor and look-back words.
 template <class KT>
 __global__ void k_init_root(Seg *segs, uint32_t *tile_map, unsigned long long *cursor, uint32_t *ecursor,
-                            uint64_t *status, const typename KT::T *buf, uint32_t n, int rule) {
+                            uint64_t *status, LevelCtrl *root, const typename KT::T *buf, uint32_t n, int rule) {
     constexpr uint32_t TILE = (uint32_t)tile_elems<KT>();
     const uint32_t nt = seg_ntiles(0, n, TILE);
     if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -276,6 +302,8 @@ __global__ void k_init_root(Seg *segs, uint32_t *tile_map, unsigned long long *c
         segs[0] = s;
         cursor[0] = 0;
         ecursor[0] = 0;
+        root->nseg_next = 1;   // level 0's counts, read by its kernels from device memory
+        root->ntiles_next = nt;
     }
     for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < nt; j += gridDim.x * blockDim.x) {
         tile_map[j] = 0;

@@ -68,6 +68,7 @@ __global__ void __launch_bounds__(NT + 32, MINB) k_part_fast(PassParams<KT> P) {
     extern __shared__ __align__(128) unsigned char smraw[];
     SM &sm = *reinterpret_cast<SM *>(smraw);
     const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t ntiles = pass_ntiles(P);   // device-resident in the sort's level loop
 
     if (tid == 0) {
         for (int s = 0; s < STAGES; s++) {
@@ -87,7 +88,7 @@ __global__ void __launch_bounds__(NT + 32, MINB) k_part_fast(PassParams<KT> P) {
             mbar_wait(&sm.empty[s], ((i / STAGES) & 1) ^ 1);
             const uint32_t t = atomicAdd(&P.ctrl->ticket, 1u);
             sm.tile[s] = t;
-            if (t >= P.ntiles) {
+            if (t >= ntiles) {
                 mbar_arrive(&sm.full[s]);
                 break;
             }
@@ -131,7 +132,7 @@ __global__ void __launch_bounds__(NT + 32, MINB) k_part_fast(PassParams<KT> P) {
         const uint32_t s = i % STAGES, par = i & 1;
         mbar_wait(&sm.full[s], (i / STAGES) & 1);
         const uint32_t t = sm.tile[s];
-        const bool cur = t < P.ntiles;
+        const bool cur = t < ntiles;
         // everything this iteration needs from the slot is read before the
         // slot is released to the loader
         const uint32_t si = sm.segidx[s];

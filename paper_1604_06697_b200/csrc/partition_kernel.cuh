@@ -97,6 +97,7 @@ __global__ void __launch_bounds__(NT + (ORDERED ? 96 : 64), MINB) k_partition(Pa
     extern __shared__ __align__(128) unsigned char smraw[];
     SM &sm = *reinterpret_cast<SM *>(smraw);
     const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t ntiles = pass_ntiles(P);   // device-resident in the sort's level loop
 
     if (tid == 0) {
         for (int s = 0; s < STAGES; s++) {
@@ -119,7 +120,7 @@ __global__ void __launch_bounds__(NT + (ORDERED ? 96 : 64), MINB) k_partition(Pa
             mbar_wait(&sm.empty[s], ((i / STAGES) & 1) ^ 1);
             const uint32_t t = atomicAdd(&P.ctrl->ticket, 1u);
             sm.tile[s] = t;
-            if (t >= P.ntiles) {
+            if (t >= ntiles) {
                 if (ORDERED) mbar_arrive(&sm.claimed[s]);
                 mbar_arrive(&sm.loaded[s]);
                 break;
@@ -165,7 +166,7 @@ __global__ void __launch_bounds__(NT + (ORDERED ? 96 : 64), MINB) k_partition(Pa
         unsigned long long pend_old = 0;
         uint32_t pend_eold = 0;
         auto finalize = [&](uint32_t ps, uint32_t pt, unsigned long long old, uint32_t eold) {
-            if (!ORDERED && lane == 0 && pt < P.ntiles) {
+            if (!ORDERED && lane == 0 && pt < ntiles) {
                 sm.meta[ps][2] = (uint32_t)old;
                 sm.meta[ps][3] = (uint32_t)(old >> 32);
                 sm.meta[ps][4] = eold;
@@ -180,7 +181,7 @@ __global__ void __launch_bounds__(NT + (ORDERED ? 96 : 64), MINB) k_partition(Pa
             const uint32_t t = sm.tile[s];
             unsigned long long old = 0;
             uint32_t eold = 0;
-            if (t < P.ntiles) {
+            if (t < ntiles) {
                 const Seg sg = sm.seg[s];
                 const TileGeom<KT, TILE> G(sg, t);
                 const K pk = (K)sg.pivot;
@@ -246,9 +247,9 @@ __global__ void __launch_bounds__(NT + (ORDERED ? 96 : 64), MINB) k_partition(Pa
                 pend_t = t;
                 pend_old = old;
                 pend_eold = eold;
-                if (t >= P.ntiles) finalize(s, t, 0, 0);   // release the end marker
+                if (t >= ntiles) finalize(s, t, 0, 0);   // release the end marker
             }
-            if (t >= P.ntiles) break;
+            if (t >= ntiles) break;
         }
         return;
     }
@@ -271,7 +272,7 @@ __global__ void __launch_bounds__(NT + (ORDERED ? 96 : 64), MINB) k_partition(Pa
             const uint32_t s = i % STAGES, ph = (i / STAGES) & 1;
             mbar_wait(&sm.claimed[s], ph);
             const uint32_t t = sm.tile[s];
-            if (t < P.ntiles) {
+            if (t < ntiles) {
                 const Seg sg = sm.seg[s];
                 uint64_t *st = P.status;
                 uint32_t accl = 0, accg = 0;
@@ -356,7 +357,7 @@ __global__ void __launch_bounds__(NT + (ORDERED ? 96 : 64), MINB) k_partition(Pa
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&sm.full[s]);
-            if (t >= P.ntiles) break;
+            if (t >= ntiles) break;
         }
         return;
     }
@@ -377,7 +378,7 @@ __global__ void __launch_bounds__(NT + (ORDERED ? 96 : 64), MINB) k_partition(Pa
         const uint32_t s = i % STAGES;
         mbar_wait(&sm.full[s], (i / STAGES) & 1);
         const uint32_t t = sm.tile[s];
-        if (t >= P.ntiles) break;
+        if (t >= ntiles) break;
         if (tid == 0) BQ_TR(t, 0, gtime());
         const Seg sg = sm.seg[s];
         const bool manual = sm.manual[s] != 0;
