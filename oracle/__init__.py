@@ -22,7 +22,7 @@ _lib = None
 
 KINDS = ("i32", "u64", "f64", "rec32")
 _DTYPES = {"i32": np.int32, "u64": np.uint64, "f64": np.float64}
-MO3, NINTHER = 0, 1
+MO3, NINTHER, SAMPLE64 = 0, 1, 2
 
 
 class OracleOpts(ctypes.Structure):
@@ -124,7 +124,8 @@ def partition(a: np.ndarray, pivot, block: int = 128, inplace: bool = False):
 
 
 def pivot(a: np.ndarray, rule: int = MO3):
-    """Pivot value of the Mo3 (rule 0) or ninther (rule 1) sample."""
+    """Pivot value of the Mo3 (rule 0), ninther (rule 1) or 64-key sample
+    median (rule 2) rule."""
     k = kind_of(a)
     a = np.ascontiguousarray(a)
     v = getattr(_load(), f"bq_oracle_pivot_{k}")(a.ctypes.data, len(a), rule)

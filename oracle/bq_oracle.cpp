@@ -365,13 +365,25 @@ void partition_value(T *A, long long n, const T &pivot, long long B, C &less,
     *n_equal = eqR - eqL;
 }
 
-/* Pivot sample rules, used to pin the GPU pivot kernel.
+/* Pivot sample rules, used to pin the GPU pivot kernel (SURVEY §8(a) a1 and
+ * §8(f) N1).
  * Mo3 over positions {0, floor(n/2), n-1} (P:313-317, P:1215 + R2);
  * pseudomedian of 9 ("median of three medians of three") over
  * positions floor(k*(n-1)/8), k=0..8, grouped as consecutive triples
  * (SURVEY §8(c) ambiguity 13).  Values are copied; the array is untouched. */
 template <class T, class C>
 T pivot_value(const T *A, long long n, int rule, C &less) {
+    if (rule == 2) {
+        /* median of a 64-key equidistant sample (R18, the paper's
+         * "median of a larger sample" idea, P:319-329 and P:729-736 with the
+         * sample size fixed at 64): positions floor(j*(n-1)/63), j = 0..63,
+         * sorted by insertion sort; the lower median (index 31) is the pivot. */
+        T smp[64];
+        for (int j = 0; j < 64; j++) smp[j] = A[((long long)j * (n - 1)) / 63];
+        for (int j = 1; j < 64; j++)
+            for (int k = j; k > 0 && less(smp[k], smp[k - 1]); k--) swap_elems(&smp[k], &smp[k - 1]);
+        return smp[31];
+    }
     if (rule == 0 || n < 9) {
         T a = A[0], b = A[n / 2], c = A[n - 1];
         return *median_of_3(&a, &b, &c, less);

@@ -245,6 +245,21 @@ def test_pivot_rules_vs_median():
                 assert oracle.pivot(a, oracle.NINTHER) == int(np.median(meds))
 
 
+def test_pivot_sample64_closed_forms():
+    # R18: lower median of the 64 keys at floor(j(n-1)/63).  On an ascending
+    # array the sample is ascending, so the pivot is the key at j = 31; on a
+    # descending one the 32nd smallest sampled key sits at j = 32.
+    for n in [1, 2, 63, 64, 65, 1000, 12345, 1 << 20]:
+        asc = np.arange(n, dtype=np.int32) * 3 - 7
+        assert oracle.pivot(asc, oracle.SAMPLE64) == asc[(31 * (n - 1)) // 63]
+        desc = asc[::-1].copy()
+        assert oracle.pivot(desc, oracle.SAMPLE64) == desc[(32 * (n - 1)) // 63]
+    # all keys equal: the pivot is that key; u64 keys above 2^63 compare unsigned
+    assert oracle.pivot(np.full(500, 9, dtype=np.int32), oracle.SAMPLE64) == 9
+    u = (np.arange(200, dtype=np.uint64) + np.uint64(1 << 63))
+    assert oracle.pivot(u, oracle.SAMPLE64) == u[(31 * 199) // 63]
+
+
 # ------------------------------------------ closed forms of config inputs ----
 
 def test_closed_form_c1():
