@@ -206,7 +206,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="bq", choices=["bq", "reference"])
     ap.add_argument("--n", type=int, default=N_FULL, help="keys per GPU (default 2^28)")
-    ap.add_argument("--pivot-rule", type=int, default=1, help="0 Mo3, 1 ninther")
+    ap.add_argument("--pivot-rule", type=int, default=2, help="0 Mo3, 1 ninther, 2 median of a 64-key sample")
     ap.add_argument("--passes", type=int, default=10)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-sample", type=int, default=1 << 27)
@@ -361,7 +361,7 @@ def main():
         "metric": METRIC, "value": value, "unit": "Gkeys/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "n_per_gpu": n, "pivot_rule": "ninther" if args.pivot_rule else "mo3",
+        "config": {"workload": WORKLOAD, "n_per_gpu": n, "pivot_rule": ["mo3", "ninther", "sample64"][args.pivot_rule],
                    "parallelism": f"replicas{world}" if world > 1 else "1gpu",
                    "l2": "inputs (1 GiB) larger than L2 (126 MB); restore copy between steps is untimed",
                    "timing": "sum of per-step CUDA events around bq_sort on the launch stream"},

@@ -70,8 +70,12 @@ typedef enum { BQ_I32 = 0, BQ_U64 = 1, BQ_F64 = 2, BQ_REC32 = 3 } bq_kind;
  *   MO3     median of the keys at segment positions {b, b+floor(len/2), e-1}
  *           (Appendix B median_of_3, P:1069-1075, P:1215 read with e-1);
  *   NINTHER pseudomedian of 9 = median of the medians of three triples, at
- *           positions b + floor(k*(len-1)/8), k = 0..8. */
-typedef enum { BQ_PIVOT_MO3 = 0, BQ_PIVOT_NINTHER = 1 } bq_pivot_rule;
+ *           positions b + floor(k*(len-1)/8), k = 0..8;
+ *   SAMPLE64 lower median (the 32nd smallest) of the 64 keys at positions
+ *           b + floor(j*(len-1)/63), j = 0..63: the paper's "larger sample"
+ *           idea (median of sqrt(n)) at a fixed sample
+ *           size (R18); computed by one warp with a shuffle network. */
+typedef enum { BQ_PIVOT_MO3 = 0, BQ_PIVOT_NINTHER = 1, BQ_PIVOT_SAMPLE64 = 2 } bq_pivot_rule;
 
 /* 32-byte record: key + 24-byte payload, 16-byte aligned in device memory
  * (BASELINE.json config 5; the paper's "Record" element). */
@@ -81,7 +85,7 @@ typedef struct {
 } bq_record32;
 
 typedef struct {
-    int32_t pivot_rule;   /* bq_pivot_rule for segments > leaf size; default NINTHER */
+    int32_t pivot_rule;   /* bq_pivot_rule for segments > leaf size; default SAMPLE64 */
     int32_t depth_limit;  /* < 0: Introsort limit 2*floor(log2 n)+3 */
     int32_t timing;       /* != 0: time every partition launch with CUDA events */
     int32_t ordered;      /* != 0: ticket-ordered tile placement (decoupled look-back),

@@ -7,7 +7,7 @@ three-way Quicksort/Introsort.  This package is only the thin ctypes binding
 """
 from . import bq  # noqa: F401  (raises ImportError when libbq.so is missing)
 from .bq import (  # noqa: F401
-    BQ_F64, BQ_I32, BQ_PIVOT_MO3, BQ_PIVOT_NINTHER, BQ_REC32, BQ_U64, BQError,
+    BQ_F64, BQ_I32, BQ_PIVOT_MO3, BQ_PIVOT_NINTHER, BQ_PIVOT_SAMPLE64, BQ_REC32, BQ_U64, BQError,
     bq_partition_f64, bq_partition_i32, bq_partition_pass, bq_partition_records, bq_partition_segments,
     bq_partition_u64,
     bq_pivot_f64, bq_pivot_i32, bq_pivot_records, bq_pivot_u64, bq_sort_ex, bq_sort_f64,

@@ -30,7 +30,7 @@ _lib = ctypes.CDLL(LIB_PATH)
 
 BQ_OK, BQ_ERR_INVALID_ARGUMENT, BQ_ERR_WORKSPACE, BQ_ERR_CUDA, BQ_ERR_UNSUPPORTED = range(5)
 BQ_I32, BQ_U64, BQ_F64, BQ_REC32 = range(4)
-BQ_PIVOT_MO3, BQ_PIVOT_NINTHER = range(2)
+BQ_PIVOT_MO3, BQ_PIVOT_NINTHER, BQ_PIVOT_SAMPLE64 = range(3)
 KIND = {"i32": BQ_I32, "u64": BQ_U64, "f64": BQ_F64, "rec32": BQ_REC32}
 WIDTH = {BQ_I32: 4, BQ_U64: 8, BQ_F64: 8, BQ_REC32: 32}
 
@@ -261,7 +261,7 @@ def _opts(pivot_rule, depth_limit, timing, ordered=False):
     return o
 
 
-def bq_sort_ex(data, pivot_rule=BQ_PIVOT_NINTHER, depth_limit=-1, timing=False, ordered=False, ws=None,
+def bq_sort_ex(data, pivot_rule=BQ_PIVOT_SAMPLE64, depth_limit=-1, timing=False, ordered=False, ws=None,
                stream=None):
     """Kind-generic sort; returns the bq_sort_stats as a dict."""
     kind = kind_of(data)
@@ -273,7 +273,7 @@ def bq_sort_ex(data, pivot_rule=BQ_PIVOT_NINTHER, depth_limit=-1, timing=False, 
     return st.as_dict()
 
 
-def bq_sort_host(host, dev, pivot_rule=BQ_PIVOT_NINTHER, ws=None, stream=None):
+def bq_sort_host(host, dev, pivot_rule=BQ_PIVOT_SAMPLE64, ws=None, stream=None):
     """End-to-end sort of a host (ideally pinned) tensor through dev (same shape/dtype)."""
     kind = kind_of(dev)
     if host.is_cuda or not host.is_contiguous():

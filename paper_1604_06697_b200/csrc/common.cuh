@@ -296,6 +296,47 @@ __device__ __forceinline__ typename KT::K load_key(const typename KT::T *buf, ui
     return KT::key(buf[i]);
 }
 
+// SAMPLE64 (N1, R18): one warp loads the 64 keys at
+// b + floor(j*(len-1)/63) (lane l holds j = l and j = l + 32), sorts them
+// with a bitonic network (register compare-exchange for index bit 5,
+// shuffles for bits 0-4) and returns the 32nd smallest to every lane.
+template <class KT>
+__device__ typename KT::K sample64_pivot_warp(const typename KT::T *buf, uint32_t b, uint32_t len, uint32_t lane) {
+    using K = typename KT::K;
+    K v[2];
+#pragma unroll
+    for (int r = 0; r < 2; r++)
+        v[r] = load_key<KT>(buf, (uint64_t)b + ((uint64_t)(lane + 32 * r) * (len - 1)) / 63);
+#pragma unroll
+    for (int m = 1; m <= 6; m++) {
+#pragma unroll
+        for (int bb = m - 1; bb >= 0; bb--) {
+            if (bb == 5) {   // only in the last merge: ascending
+                const K lo = v[1] < v[0] ? v[1] : v[0], hi = v[1] < v[0] ? v[0] : v[1];
+                v[0] = lo;
+                v[1] = hi;
+                continue;
+            }
+#pragma unroll
+            for (int r = 0; r < 2; r++) {
+                const uint32_t i = lane + 32 * r;
+                const K p = __shfl_xor_sync(0xffffffffu, v[r], 1 << bb);
+                const bool lower = ((lane >> bb) & 1) == 0;
+                const bool asc = m == 6 || ((i >> m) & 1) == 0;
+                const bool take_min = lower == asc;
+                v[r] = take_min ? (p < v[r] ? p : v[r]) : (v[r] < p ? p : v[r]);
+            }
+        }
+    }
+    return __shfl_sync(0xffffffffu, v[0], 31);
+}
+
+// Pivot of buf[b, b+len) by `rule`, computed by a whole warp (all 32 lanes
+// must call it; every lane gets the result).
+template <class KT>
+__device__ typename KT::K select_pivot_warp(const typename KT::T *buf, uint32_t b, uint32_t len, int rule,
+                                            uint32_t lane);
+
 // Mo3 over {b, b+len/2, e-1}; ninther over b + floor(k*(len-1)/8), k=0..8.
 template <class KT>
 __device__ typename KT::K select_pivot(const typename KT::T *buf, uint32_t b, uint32_t len, int rule) {
@@ -314,6 +355,16 @@ __device__ typename KT::K select_pivot(const typename KT::T *buf, uint32_t b, ui
     }
     return median3(load_key<KT>(buf, b), load_key<KT>(buf, (uint64_t)b + len / 2),
                    load_key<KT>(buf, (uint64_t)b + len - 1));
+}
+
+template <class KT>
+__device__ typename KT::K select_pivot_warp(const typename KT::T *buf, uint32_t b, uint32_t len, int rule,
+                                            uint32_t lane) {
+    using K = typename KT::K;
+    if (rule == BQ_PIVOT_SAMPLE64) return sample64_pivot_warp<KT>(buf, b, len, lane);
+    K p = 0;
+    if (lane == 0) p = select_pivot<KT>(buf, b, len, rule);
+    return __shfl_sync(0xffffffffu, p, 0);
 }
 
 }  // namespace bq

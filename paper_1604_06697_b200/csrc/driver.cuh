@@ -253,13 +253,13 @@ template <class KT>
 bq_status run_pivot(const typename KT::T *data, size_t n, int rule, uint64_t *key_out, void *ws,
                     size_t ws_bytes, cudaStream_t s) {
     if (n == 0) return set_error(BQ_ERR_INVALID_ARGUMENT, "pivot of an empty array");
-    if (rule != BQ_PIVOT_MO3 && rule != BQ_PIVOT_NINTHER)
+    if (rule != BQ_PIVOT_MO3 && rule != BQ_PIVOT_NINTHER && rule != BQ_PIVOT_SAMPLE64)
         return set_error(BQ_ERR_INVALID_ARGUMENT, "bad pivot rule %d", rule);
     bq_status st = validate<KT>(data, n, ws, ws_bytes);
     if (st != BQ_OK) return st;
     const Layout<KT> L = make_layout<KT>(n);
     uint64_t *misc = reinterpret_cast<uint64_t *>(static_cast<char *>(ws) + L.misc);
-    k_pivot<KT><<<1, 1, 0, s>>>(data, (uint32_t)n, rule, misc);
+    k_pivot<KT><<<1, 32, 0, s>>>(data, (uint32_t)n, rule, misc);
     BQ_CK_LAUNCH();
     BQ_CK(cudaMemcpyAsync(key_out, misc, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
     BQ_CK(cudaStreamSynchronize(s));
@@ -420,13 +420,13 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
     constexpr int NCLS = leaf_nclass<KT>();
     bq_sort_stats local;
     std::memset(&local, 0, sizeof local);
-    int rule = BQ_PIVOT_NINTHER, depth_limit = -1, timing = 0, ordered = 0;
+    int rule = BQ_PIVOT_SAMPLE64, depth_limit = -1, timing = 0, ordered = 0;
     if (opt) {
         rule = opt->pivot_rule;
         depth_limit = opt->depth_limit;
         timing = opt->timing;
         ordered = opt->ordered;
-        if (rule != BQ_PIVOT_MO3 && rule != BQ_PIVOT_NINTHER)
+        if (rule != BQ_PIVOT_MO3 && rule != BQ_PIVOT_NINTHER && rule != BQ_PIVOT_SAMPLE64)
             return set_error(BQ_ERR_INVALID_ARGUMENT, "bad pivot rule %d", rule);
         if (depth_limit >= MAX_LEVELS - 2)
             return set_error(BQ_ERR_INVALID_ARGUMENT, "depth_limit %d too large", depth_limit);

@@ -168,15 +168,25 @@ __device__ __forceinline__ void post_segment(const PostParams<KT> &Q, uint32_t s
     if (!Q.emit_children) return;
 
     __shared__ uint32_t s_idx[2], s_tb[2], s_nt[2];
+    __shared__ uint64_t s_piv[2];
     __syncthreads();   // the previous segment's readers of s_* are done
+    const uint8_t cp = sg.parity ^ 1;
+    const T *cbuf = cp ? P.bufs[1] : P.bufs[0];
+    const uint32_t cb[2] = {sg.begin, sg.begin + L + E};
+    const uint32_t cl[2] = {L, G};
+    const uint16_t cd = sg.depth + 1;
+    if (threadIdx.x < 32) {
+        // a1: warp 0 selects the pivots of the children that go to the next level
+#pragma unroll
+        for (int c = 0; c < 2; c++)
+            if (cl[c] > Q.leaf_max && (int)cd < Q.depth_limit) {
+                const K pk = select_pivot_warp<KT>(cbuf, cb[c], cl[c], Q.pivot_rule, threadIdx.x);
+                if (threadIdx.x == 0) s_piv[c] = (uint64_t)pk;
+            }
+    }
     if (threadIdx.x == 0) {
         atomicAdd(&C->element_passes, (unsigned long long)sg.len);
         atomicAdd(&C->band_elems, (unsigned long long)E);
-        const uint8_t cp = sg.parity ^ 1;
-        const T *cbuf = cp ? P.bufs[1] : P.bufs[0];
-        const uint32_t cb[2] = {sg.begin, sg.begin + L + E};
-        const uint32_t cl[2] = {L, G};
-        const uint16_t cd = sg.depth + 1;
 #pragma unroll
         for (int c = 0; c < 2; c++) {
             s_nt[c] = 0;
@@ -194,7 +204,7 @@ __device__ __forceinline__ void post_segment(const PostParams<KT> &Q, uint32_t s
                 Q.fallback[fi] = Leaf{cb[c], cl[c], cp, 0};
             } else {
                 Seg ch;
-                ch.pivot = (uint64_t)select_pivot<KT>(cbuf, cb[c], cl[c], Q.pivot_rule);
+                ch.pivot = s_piv[c];
                 ch.begin = cb[c];
                 ch.len = cl[c];
                 ch.ntiles = seg_ntiles(cb[c], cl[c], TILE);
@@ -288,9 +298,11 @@ __global__ void k_init_root(Seg *segs, uint32_t *tile_map, unsigned long long *c
                             uint64_t *status, LevelCtrl *root, const typename KT::T *buf, uint32_t n, int rule) {
     constexpr uint32_t TILE = (uint32_t)tile_elems<KT>();
     const uint32_t nt = seg_ntiles(0, n, TILE);
+    typename KT::K pk = 0;
+    if (blockIdx.x == 0 && threadIdx.x < 32) pk = select_pivot_warp<KT>(buf, 0, n, rule, threadIdx.x);
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         Seg s;
-        s.pivot = (uint64_t)select_pivot<KT>(buf, 0, n, rule);
+        s.pivot = (uint64_t)pk;
         s.begin = 0;
         s.len = n;
         s.tile_base = 0;
@@ -314,7 +326,8 @@ __global__ void k_init_root(Seg *segs, uint32_t *tile_map, unsigned long long *c
 // bq_pivot_*: the pivot key of buf[0, n).
 template <class KT>
 __global__ void k_pivot(const typename KT::T *buf, uint32_t n, int rule, uint64_t *out) {
-    *out = (uint64_t)select_pivot<KT>(buf, 0, n, rule);
+    const typename KT::K pk = select_pivot_warp<KT>(buf, 0, n, rule, threadIdx.x);   // one warp
+    if (threadIdx.x == 0) *out = (uint64_t)pk;
 }
 
 }  // namespace bq

@@ -90,7 +90,7 @@ def test_sort_edge_sizes(B, kind, dist):
 
 
 @pytest.mark.parametrize("kind", ["i32", "u64", "f64", "rec32"])
-@pytest.mark.parametrize("rule", [0, 1])
+@pytest.mark.parametrize("rule", [0, 1, 2])
 def test_sort_medium(B, kind, rule):
     for n in [100003, (1 << 20) + 17]:
         a = make(kind, n, seed=7)
@@ -346,10 +346,10 @@ def test_sort_large_levels(B):
 
 @pytest.mark.parametrize("kind", ["i32", "u64", "f64", "rec32"])
 def test_pivot_rules(B, kind):
-    for n in [1, 2, 3, 8, 9, 10, 1000, 123457]:
+    for n in [1, 2, 3, 8, 9, 10, 63, 64, 65, 1000, 123457]:
         a = make(kind, n, seed=n)
         t = to_dev(a)
-        for rule in [0, 1]:
+        for rule in [0, 1, 2]:
             got = B.pivot(t, rule)
             exp = oracle.pivot(a, rule)
             if kind == "f64":
