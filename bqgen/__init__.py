@@ -61,6 +61,8 @@ def _load():
             f = getattr(lib, name)
             f.restype = None
             f.argtypes = args
+        lib.bqgen_i32_pattern.restype = ctypes.c_int
+        lib.bqgen_i32_pattern.argtypes = [ctypes.c_int, u64, sz, vp]
         _lib = lib
     return _lib
 
@@ -151,3 +153,18 @@ def config(name: str, n: int | None = None, seed: int = 1,
     if name == "c5":
         return rec32(n, seed)
     raise KeyError(name)
+
+
+# --- the paper's structured workloads (bqgen.c) -----------
+
+PATTERNS = ("imodsqrt", "square", "pow8", "sorted", "reversed", "rotation",
+            "swaps_sqrt", "swaps_n", "swaps_nlogn", "halfhalf", "zeroone")
+
+
+def i32_pattern(name: str, n: int, seed: int = 1) -> np.ndarray:
+    """int32 input of one of the paper's Fig. 7/9/10/11 patterns."""
+    a = np.empty(n, dtype=np.int32)
+    rc = _load().bqgen_i32_pattern(PATTERNS.index(name), seed, n, _ptr(a))
+    if rc != 0:
+        raise ValueError(name)
+    return a

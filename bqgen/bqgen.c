@@ -162,3 +162,84 @@ void bqgen_rec32_dupkeys(uint64_t seed, size_t n, uint64_t m, uint64_t *out) {
         out[4 * i + 3] = i;
     }
 }
+
+/* ---- the paper's structured workloads -------------------
+ * int32 patterns of Figs. 7, 9, 10, 11, selected by
+ * `which`:
+ *   0 IModSqrtN      A[i] = i mod floor(sqrt(n))                 (Fig. 7 left)
+ *   1 SquarePattern  A[i] = (i^2 + n/2) mod n                    (Fig. 7 middle, R15)
+ *   2 Pow8Pattern    A[i] = (i^8 + n/2) mod n, i^8 by modular squaring (Fig. 7 right)
+ *   3 Sorted         A[i] = i                                    (Fig. 9 left)
+ *   4 Reversed       A[i] = n-1-i                                (Fig. 9 middle)
+ *   5 Rotation       A[i] = (i + n/2) mod n                      (Fig. 9 right)
+ *   6,7,8 NeighborSwaps: the sorted array after k swaps of uniformly random
+ *                    neighbours (A[j], A[j+1]), k = floor(sqrt n), n, n*floor(log2 n)
+ *                    (Fig. 10), j drawn from stream `seed`
+ *   9 HalfHalf       A[i] = 0 for i < n/2, else 1                (Fig. 11 middle)
+ *  10 RandomZeroOne  A[i] = top bit of u(seed, i)                (Fig. 11 right)
+ * Returns 0, or -1 for an unknown pattern. */
+static uint64_t mulmod(uint64_t a, uint64_t b, uint64_t m) {
+    return (uint64_t)(((__uint128_t)a * b) % m);
+}
+
+static uint64_t isqrt_floor(uint64_t n) {
+    uint64_t r = 0;
+    while ((r + 1) * (r + 1) <= n) r++;
+    return r;
+}
+
+int bqgen_i32_pattern(int which, uint64_t seed, size_t n, int32_t *out) {
+    if (n == 0) return (which >= 0 && which <= 10) ? 0 : -1;
+    const uint64_t N = n, half = N / 2;
+    switch (which) {
+    case 0: {
+        uint64_t r = isqrt_floor(N);
+        if (r == 0) r = 1;
+        for (uint64_t i = 0; i < N; i++) out[i] = (int32_t)(i % r);
+        return 0;
+    }
+    case 1:
+        for (uint64_t i = 0; i < N; i++) out[i] = (int32_t)((mulmod(i, i, N) + half) % N);
+        return 0;
+    case 2:
+        for (uint64_t i = 0; i < N; i++) {
+            uint64_t x = i % N;
+            x = mulmod(x, x, N);   /* i^2 */
+            x = mulmod(x, x, N);   /* i^4 */
+            x = mulmod(x, x, N);   /* i^8 */
+            out[i] = (int32_t)((x + half) % N);
+        }
+        return 0;
+    case 3:
+        for (uint64_t i = 0; i < N; i++) out[i] = (int32_t)i;
+        return 0;
+    case 4:
+        for (uint64_t i = 0; i < N; i++) out[i] = (int32_t)(N - 1 - i);
+        return 0;
+    case 5:
+        for (uint64_t i = 0; i < N; i++) out[i] = (int32_t)((i + half) % N);
+        return 0;
+    case 6: case 7: case 8: {
+        for (uint64_t i = 0; i < N; i++) out[i] = (int32_t)i;
+        uint64_t lg = 0;
+        while ((2ull << lg) <= N) lg++;
+        const uint64_t k = which == 6 ? isqrt_floor(N) : which == 7 ? N : N * lg;
+        if (N < 2) return 0;
+        stream_t s = stream_make(seed);
+        for (uint64_t t = 0; t < k; t++) {
+            const uint64_t j = bounded(&s, N - 1);
+            int32_t x = out[j]; out[j] = out[j + 1]; out[j + 1] = x;
+        }
+        return 0;
+    }
+    case 9:
+        for (uint64_t i = 0; i < N; i++) out[i] = i < half ? 0 : 1;
+        return 0;
+    case 10: {
+        uint64_t b = mix64(seed);
+        for (uint64_t i = 0; i < N; i++) out[i] = (int32_t)(mix64(b + (i + 1) * GAMMA) >> 63);
+        return 0;
+    }
+    }
+    return -1;
+}

@@ -365,6 +365,14 @@ void partition_value(T *A, long long n, const T &pivot, long long B, C &less,
     *n_equal = eqR - eqL;
 }
 
+/* SplitMix64's output function (Steele, Lea & Flood 2014), from its
+ * published definition: the counter-based generator of R19. */
+static inline uint64_t splitmix64_mix(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
 /* Pivot sample rules, used to pin the GPU pivot kernel (SURVEY §8(a) a1 and
  * §8(f) N1).
  * Mo3 over positions {0, floor(n/2), n-1} (P:313-317, P:1215 + R2);
@@ -374,12 +382,22 @@ void partition_value(T *A, long long n, const T &pivot, long long B, C &less,
 template <class T, class C>
 T pivot_value(const T *A, long long n, int rule, C &less) {
     if (rule == 2) {
-        /* median of a 64-key equidistant sample (R18, the paper's
-         * "median of a larger sample" idea, P:319-329 and P:729-736 with the
-         * sample size fixed at 64): positions floor(j*(n-1)/63), j = 0..63,
-         * sorted by insertion sort; the lower median (index 31) is the pivot. */
+        /* median of a 64-key sample (R18/R19: the paper's "median of
+         * a larger sample" idea, with the sample size
+         * fixed at 64, and its suggestion to pick the sample with a fast
+         * pseudo-random generator): key j is drawn from the j-th
+         * of 64 equal strata of [0, n), at an offset given by SplitMix64 of
+         * (segment begin = 0, n, j); the 64 keys are sorted by insertion sort
+         * and the lower median (index 31) is the pivot. */
         T smp[64];
-        for (int j = 0; j < 64; j++) smp[j] = A[((long long)j * (n - 1)) / 63];
+        const uint64_t un = (uint64_t)n;
+        for (int j = 0; j < 64; j++) {
+            const uint64_t s0 = ((uint64_t)j * un) >> 6, s1 = ((uint64_t)(j + 1) * un) >> 6;
+            const uint64_t r = splitmix64_mix(un + (uint64_t)(j + 1) * 0x9E3779B97F4A7C15ull) >> 32;
+            uint64_t pos = s0 + ((r * (s1 - s0)) >> 32);
+            if (pos > un - 1) pos = un - 1;
+            smp[j] = A[pos];
+        }
         for (int j = 1; j < 64; j++)
             for (int k = j; k > 0 && less(smp[k], smp[k - 1]); k--) swap_elems(&smp[k], &smp[k - 1]);
         return smp[31];

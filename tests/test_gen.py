@@ -72,3 +72,38 @@ def test_rec32_payload():
     assert (a[:, 1] == a[:, 2]).all() and (a[:, 2] == a[:, 3]).all()
     d = bqgen.rec32(1000, 5, dup_keys=10)
     assert d[:, 0].max() < 10
+
+
+# ---- the paper's structured workloads (N3) -------------------------------------
+
+def test_pattern_spec_examples():
+    # SPEC S:260-261 worked examples (direct evaluation of the Fig. 7/9 formulas)
+    assert bqgen.i32_pattern("rotation", 4).tolist() == [2, 3, 0, 1]
+    assert bqgen.i32_pattern("square", 8).tolist() == [4, 5, 0, 5, 4, 5, 0, 5]
+    # Fig. 7 caption: n/2 occurs about n^(7/8) times in the i^8 pattern
+    n = 1 << 10
+    m = int((bqgen.i32_pattern("pow8", n) == n // 2).sum())
+    assert n ** 0.875 / 2 <= m <= 2 * n ** 0.875          # within a factor 2
+
+
+def test_pattern_closed_forms():
+    n = 1000
+    i = np.arange(n)
+    assert np.array_equal(bqgen.i32_pattern("imodsqrt", n), i % 31)
+    assert np.array_equal(bqgen.i32_pattern("sorted", n), i)
+    assert np.array_equal(bqgen.i32_pattern("reversed", n), n - 1 - i)
+    assert np.array_equal(bqgen.i32_pattern("halfhalf", n), (i >= 500).astype(np.int32))
+    z = bqgen.i32_pattern("zeroone", 1 << 16, seed=3)
+    assert set(np.unique(z).tolist()) == {0, 1} and abs(z.mean() - 0.5) < 0.02
+    assert np.array_equal(bqgen.i32_pattern("pow8", 16), (i[:16] ** 8 + 8) % 16)
+
+
+def test_pattern_neighbour_swaps():
+    # Fig. 10: k swaps of random neighbours -> a permutation with at most k inversions
+    n = 4096
+    for name, k in [("swaps_sqrt", 64), ("swaps_n", n), ("swaps_nlogn", n * 12)]:
+        a = bqgen.i32_pattern(name, n, seed=5)
+        assert np.array_equal(np.sort(a), np.arange(n))
+        inv = sum(int((a[j + 1:] < a[j]).sum()) for j in range(n))
+        assert 0 < inv <= k
+        assert np.array_equal(a, bqgen.i32_pattern(name, n, seed=5))   # deterministic

@@ -373,3 +373,46 @@ def test_sort_host_e2e(B):
     dev = torch.empty_like(host, device="cuda")
     B.bq_sort_host(host, dev)
     assert np.array_equal(host.numpy(), oracle.sort(a))
+
+
+# ------------------------------------- the paper's structured inputs (N3) ------
+
+PATTERNS = ["imodsqrt", "square", "pow8", "sorted", "reversed", "rotation",
+            "swaps_sqrt", "swaps_n", "swaps_nlogn", "halfhalf", "zeroone"]
+
+
+def pattern_as(kind, p):
+    """The int32 pattern mapped order-preservingly into each kind (u64 above
+    2^63 and f64 negatives exercise the unsigned compare and the H0 codec)."""
+    if kind == "i32":
+        return p
+    if kind == "u64":
+        return p.astype(np.uint64) + np.uint64(1 << 63)
+    if kind == "f64":
+        return p.astype(np.float64) * 0.25 - 1000.0
+    r = np.empty((len(p), 4), dtype=np.uint64)
+    r[:, 0] = p.astype(np.uint64) * np.uint64(3)
+    r[:, 1] = r[:, 2] = r[:, 3] = np.arange(len(p), dtype=np.uint64)
+    return r
+
+
+@pytest.mark.parametrize("kind", ["i32", "u64", "f64", "rec32"])
+@pytest.mark.parametrize("name", PATTERNS)
+def test_sort_patterns(B, kind, name):
+    for n in [(1 << 16) + 3, (1 << 20) + 1]:
+        if name == "swaps_nlogn" and n > (1 << 17):
+            continue                       # the generator itself is O(n log n) serial swaps
+        a = pattern_as(kind, bqgen.i32_pattern(name, n, seed=3))
+        for rule in [1, 2]:
+            t = to_dev(a)
+            st = B.bq_sort_ex(t, pivot_rule=rule)
+            check_sorted_equal(kind, to_host(t, a), a)
+            assert st["fallback_segments"] == 0
+
+
+@pytest.mark.parametrize("name", ["pow8", "halfhalf", "rotation"])
+def test_sort_patterns_ordered_placement(B, name):
+    a = bqgen.i32_pattern(name, (1 << 20) + 5, seed=4)
+    t = to_dev(a)
+    B.bq_sort_ex(t, ordered=True)
+    assert np.array_equal(t.cpu().numpy(), oracle.sort(a))
