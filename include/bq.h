@@ -71,10 +71,13 @@ typedef enum { BQ_I32 = 0, BQ_U64 = 1, BQ_F64 = 2, BQ_REC32 = 3 } bq_kind;
  *           (Appendix B median_of_3, P:1069-1075, P:1215 read with e-1);
  *   NINTHER pseudomedian of 9 = median of the medians of three triples, at
  *           positions b + floor(k*(len-1)/8), k = 0..8;
- *   SAMPLE64 lower median (the 32nd smallest) of the 64 keys at positions
- *           b + floor(j*(len-1)/63), j = 0..63: the paper's "larger sample"
- *           idea (median of sqrt(n)) at a fixed sample
- *           size (R18); computed by one warp with a shuffle network. */
+ *   SAMPLE64 lower median (the 32nd smallest) of 64 keys, key j drawn from
+ *           the j-th of 64 equal strata of the segment at an offset given by
+ *           SplitMix64 of (segment begin, length, j): the paper's "larger
+ *           sample" idea (median of sqrt(n)) at a fixed
+ *           sample size, with the pseudo-random sample selection it suggests
+ *            (R18, R19); computed by one warp with a
+ *           shuffle network.  For bq_pivot_* the segment is [0, n). */
 typedef enum { BQ_PIVOT_MO3 = 0, BQ_PIVOT_NINTHER = 1, BQ_PIVOT_SAMPLE64 = 2 } bq_pivot_rule;
 
 /* 32-byte record: key + 24-byte payload, 16-byte aligned in device memory

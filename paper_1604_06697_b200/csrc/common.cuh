@@ -296,17 +296,31 @@ __device__ __forceinline__ typename KT::K load_key(const typename KT::T *buf, ui
     return KT::key(buf[i]);
 }
 
-// SAMPLE64 (N1, R18): one warp loads the 64 keys at
-// b + floor(j*(len-1)/63) (lane l holds j = l and j = l + 32), sorts them
-// with a bitonic network (register compare-exchange for index bit 5,
-// shuffles for bits 0-4) and returns the 32nd smallest to every lane.
+// SAMPLE64 (N1, R18/R19): one warp loads 64 keys, key j from the
+// j-th of 64 equal strata of the segment at an offset drawn by SplitMix64
+// from (segment begin, length, j) — the paper's suggestion of a fast
+// pseudo-random generator for sample selection, which keeps
+// periodic inputs from aliasing with the sample (lane l holds j = l and
+// j = l + 32); sorts them with a bitonic network (register compare-exchange
+// for index bit 5, shuffles for bits 0-4) and returns the 32nd smallest to
+// every lane.
+__device__ __forceinline__ uint64_t splitmix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+__device__ __forceinline__ uint64_t sample64_pos(uint32_t b, uint32_t len, uint32_t j) {
+    const uint64_t s0 = ((uint64_t)j * len) >> 6, s1 = ((uint64_t)(j + 1) * len) >> 6;
+    const uint64_t r = splitmix64((((uint64_t)b << 32) | len) + (uint64_t)(j + 1) * 0x9E3779B97F4A7C15ull) >> 32;
+    uint64_t pos = s0 + ((r * (s1 - s0)) >> 32);
+    return (uint64_t)b + (pos < len - 1 ? pos : len - 1);
+}
 template <class KT>
 __device__ typename KT::K sample64_pivot_warp(const typename KT::T *buf, uint32_t b, uint32_t len, uint32_t lane) {
     using K = typename KT::K;
     K v[2];
 #pragma unroll
-    for (int r = 0; r < 2; r++)
-        v[r] = load_key<KT>(buf, (uint64_t)b + ((uint64_t)(lane + 32 * r) * (len - 1)) / 63);
+    for (int r = 0; r < 2; r++) v[r] = load_key<KT>(buf, sample64_pos(b, len, lane + 32 * r));
 #pragma unroll
     for (int m = 1; m <= 6; m++) {
 #pragma unroll
