@@ -95,7 +95,11 @@ typedef struct {
                              deterministic layout; 0: one atomicAdd per tile (faster; tiles
                              of a segment placed in completion order).  Records always
                              use the ordered placement.  Sorted keys are identical. */
-    int32_t reserved[4];  /* must be 0 */
+    int32_t ways;         /* 0 (default) or 2: binary three-way passes; 16 (keys only):
+                             multi-pivot block partition, 16-way passes (
+                             segments whose sample has duplicate splitters use the binary
+                             three-way pass).  Records always use the binary pass. */
+    int32_t reserved[3];  /* must be 0 */
 } bq_sort_options;
 
 typedef struct {

@@ -37,7 +37,8 @@ WIDTH = {BQ_I32: 4, BQ_U64: 8, BQ_F64: 8, BQ_REC32: 32}
 
 class bq_sort_options(ctypes.Structure):
     _fields_ = [("pivot_rule", ctypes.c_int32), ("depth_limit", ctypes.c_int32),
-                ("timing", ctypes.c_int32), ("ordered", ctypes.c_int32), ("reserved", ctypes.c_int32 * 4)]
+                ("timing", ctypes.c_int32), ("ordered", ctypes.c_int32), ("ways", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 3)]
 
 
 class bq_sort_stats(ctypes.Structure):
@@ -252,34 +253,36 @@ def bq_sort_records(recs, ws=None, stream=None):
     return _sort("bq_sort_records", recs, ws, stream)
 
 
-def _opts(pivot_rule, depth_limit, timing, ordered=False):
+def _opts(pivot_rule, depth_limit, timing, ordered=False, ways=0):
     o = bq_sort_options()
     o.pivot_rule = pivot_rule
     o.depth_limit = depth_limit
     o.timing = int(timing)
     o.ordered = int(ordered)
+    o.ways = int(ways)
     return o
 
 
-def bq_sort_ex(data, pivot_rule=BQ_PIVOT_SAMPLE64, depth_limit=-1, timing=False, ordered=False, ws=None,
-               stream=None):
-    """Kind-generic sort; returns the bq_sort_stats as a dict."""
+def bq_sort_ex(data, pivot_rule=BQ_PIVOT_SAMPLE64, depth_limit=-1, timing=False, ordered=False, ways=0,
+               ws=None, stream=None):
+    """Kind-generic sort; returns the bq_sort_stats as a dict.  ways: 0 default
+    (16-way multi-pivot passes for keys), 2 binary only, 16 multiway."""
     kind = kind_of(data)
     w, wb = _ws(ws, kind, _n(data), data)
-    o = _opts(pivot_rule, depth_limit, timing, ordered)
+    o = _opts(pivot_rule, depth_limit, timing, ordered, ways)
     st = bq_sort_stats()
     _check(_lib.bq_sort_ex(kind, _dev(data), _n(data), ctypes.byref(o), ctypes.byref(st), w, wb,
                            _stream(stream)))
     return st.as_dict()
 
 
-def bq_sort_host(host, dev, pivot_rule=BQ_PIVOT_SAMPLE64, ws=None, stream=None):
+def bq_sort_host(host, dev, pivot_rule=BQ_PIVOT_SAMPLE64, ways=0, ws=None, stream=None):
     """End-to-end sort of a host (ideally pinned) tensor through dev (same shape/dtype)."""
     kind = kind_of(dev)
     if host.is_cuda or not host.is_contiguous():
         raise ValueError("host must be a contiguous CPU tensor")
     w, wb = _ws(ws, kind, _n(dev), dev)
-    o = _opts(pivot_rule, -1, False)
+    o = _opts(pivot_rule, -1, False, False, ways)
     _check(_lib.bq_sort_host(kind, host.data_ptr(), _n(dev), _dev(dev), ctypes.byref(o), w, wb,
                              _stream(stream)))
     return host

@@ -138,19 +138,23 @@ struct alignas(16) Leaf {
 // Per-level control block.  One per level, zeroed once per sort, so no
 // counter is reused within a call.
 struct alignas(64) LevelCtrl {
-    uint32_t ticket;         // partition tile tickets (ordered claiming)
-    uint32_t nseg_next;      // children appended to the next level
-    uint32_t ntiles_next;    // tiles of the next level
+    uint32_t ticket;         // tile tickets of the binary partition kernel
+    uint32_t nseg_next;      // binary children appended to the next level
+    uint32_t ntiles_next;    // their tiles
     uint32_t maxtiles_next;  // largest child tile count
     uint32_t nleaf;          // leaves appended by this level
     uint32_t nfallback;      // depth-capped segments appended by this level
     uint32_t nbig;           // equal bands left to k_fill
-    uint32_t pad;
+    uint32_t mw_ticket_count;    // tile tickets of the multiway count kernel
     unsigned long long element_passes;  // sum of partitioned lengths this level
     unsigned long long band_elems;      // equal-band elements this level
     uint32_t nleaf_cls[4];              // leaves appended per network-size class
+    uint32_t mw_ticket_scatter;  // tile tickets of the multiway scatter kernel
+    uint32_t nmseg_next;         // multiway children appended to the next level
+    uint32_t nmtiles_next;       // their tiles
+    uint32_t pad2[13];
 };
-static_assert(sizeof(LevelCtrl) == 64, "LevelCtrl layout");
+static_assert(sizeof(LevelCtrl) == 128, "LevelCtrl layout");
 
 // ---------------------------------------------------------------------------
 // Decoupled look-back status word: flag:2 | lt:31 | gt:31.

@@ -52,6 +52,7 @@ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 template <class KT>
 struct Layout {
     size_t scratch, status, tile_map[2], segs[2], cursor[2], ecursor[2], leaves[2], fallback, ctrl, misc, total;
+    size_t msegs[2], mtile_map[2], mhist[2], mcursor[2];   // multiway segment lists (N4)
     size_t max_tiles, max_segs, max_leaves, max_fb;
 };
 
@@ -76,6 +77,10 @@ Layout<KT> make_layout(size_t n) {
         L.segs[p] = take(L.max_segs * sizeof(Seg));
         L.cursor[p] = take(L.max_segs * sizeof(unsigned long long));
         L.ecursor[p] = take(L.max_segs * sizeof(uint32_t));
+        L.msegs[p] = take(L.max_segs * sizeof(MSeg<KT>));
+        L.mtile_map[p] = take(L.max_tiles * sizeof(uint32_t));
+        L.mhist[p] = take(MW_K * L.max_segs * sizeof(uint32_t));
+        L.mcursor[p] = take(MW_K * L.max_segs * sizeof(uint32_t));
     }
     // one list per leaf network-size class (leaf.cuh), max_leaves each
     L.leaves[0] = take(leaf_nclass<KT>() * L.max_leaves * sizeof(Leaf));
@@ -138,6 +143,44 @@ bq_status launch_partition_fast(const PassParams<KT> &P, cudaStream_t s) {
     }
     const uint32_t grid = P.ntiles < (uint32_t)cap ? P.ntiles : (uint32_t)cap;
     kern<<<grid, threads, smem, s>>>(P);
+    BQ_CK_LAUNCH();
+    return BQ_OK;
+}
+
+// resident-CTA capacity of a persistent kernel (cached per kernel)
+template <class F>
+bq_status persistent_cap(F kern, int threads, int smem, int *cap) {
+    if (*cap) return BQ_OK;
+    BQ_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    int nb = 0, dev = 0, sms = 0;
+    BQ_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, threads, smem));
+    BQ_CK(cudaGetDevice(&dev));
+    BQ_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    if (nb < 1) return set_error(BQ_ERR_CUDA, "kernel does not fit on an SM");
+    *cap = nb * sms;
+    return BQ_OK;
+}
+
+// one multiway level (N4): count, scan, scatter (children by k_post_mw)
+template <class KT>
+bq_status launch_multiway(MwParams<KT> MP, LevelCtrl *lc, cudaStream_t s) {
+    using Kn = Kernels<KT>;
+    constexpr int smem = mw_smem_bytes<KT>();
+    constexpr int threads = Kn::NT + 32;
+    auto kc = k_mw_count<KT, Kn::NT, Kn::IPT, Kn::STAGES, Kn::MINB>;
+    auto ks = k_mw_scatter<KT, Kn::NT, Kn::IPT, Kn::STAGES, Kn::MINB>;
+    static int cap_c = 0, cap_s = 0;
+    bq_status st = persistent_cap(kc, threads, smem, &cap_c);
+    if (st != BQ_OK) return st;
+    st = persistent_cap(ks, threads, smem, &cap_s);
+    if (st != BQ_OK) return st;
+    MP.ticket = &lc->mw_ticket_count;
+    kc<<<cap_c, threads, smem, s>>>(MP);
+    BQ_CK_LAUNCH();
+    k_mw_scan<KT><<<POST_GRID / 8, 256, 0, s>>>(MP);
+    BQ_CK_LAUNCH();
+    MP.ticket = &lc->mw_ticket_scatter;
+    ks<<<cap_s, threads, smem, s>>>(MP);
     BQ_CK_LAUNCH();
     return BQ_OK;
 }
@@ -420,12 +463,15 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
     constexpr int NCLS = leaf_nclass<KT>();
     bq_sort_stats local;
     std::memset(&local, 0, sizeof local);
-    int rule = BQ_PIVOT_SAMPLE64, depth_limit = -1, timing = 0, ordered = 0;
+    int rule = BQ_PIVOT_SAMPLE64, depth_limit = -1, timing = 0, ordered = 0, ways = 0;
     if (opt) {
         rule = opt->pivot_rule;
         depth_limit = opt->depth_limit;
         timing = opt->timing;
         ordered = opt->ordered;
+        ways = opt->ways;
+        if (ways != 0 && ways != 2 && ways != MW_K)
+            return set_error(BQ_ERR_INVALID_ARGUMENT, "ways %d not in {0, 2, %d}", ways, MW_K);
         if (rule != BQ_PIVOT_MO3 && rule != BQ_PIVOT_NINTHER && rule != BQ_PIVOT_SAMPLE64)
             return set_error(BQ_ERR_INVALID_ARGUMENT, "bad pivot rule %d", rule);
         if (depth_limit >= MAX_LEVELS - 2)
@@ -437,6 +483,9 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
         if (stats) *stats = local;
         return BQ_OK;
     }
+    // binary passes by default; multiway (N4) for keys when asked; records stay binary
+    if (ways == 0) ways = 2;
+    if (KT::is_record) ways = 2;
     if (depth_limit < 0) {
         int lg = 0;
         for (size_t m = n; m > 1; m >>= 1) lg++;
@@ -452,11 +501,17 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
     Seg *segs[2];
     unsigned long long *cursor[2];
     uint32_t *ecursor[2];
+    MSeg<KT> *msegs[2];
+    uint32_t *mtile_map[2], *mhist[2], *mcursor[2];
     for (int p = 0; p < 2; p++) {
         tile_map[p] = reinterpret_cast<uint32_t *>(w + L.tile_map[p]);
         segs[p] = reinterpret_cast<Seg *>(w + L.segs[p]);
         cursor[p] = reinterpret_cast<unsigned long long *>(w + L.cursor[p]);
         ecursor[p] = reinterpret_cast<uint32_t *>(w + L.ecursor[p]);
+        msegs[p] = reinterpret_cast<MSeg<KT> *>(w + L.msegs[p]);
+        mtile_map[p] = reinterpret_cast<uint32_t *>(w + L.mtile_map[p]);
+        mhist[p] = reinterpret_cast<uint32_t *>(w + L.mhist[p]);
+        mcursor[p] = reinterpret_cast<uint32_t *>(w + L.mcursor[p]);
     }
     // look-back words are only used by the ordered placement (records always)
     uint64_t *lb_status = (ordered || KT::is_record) ? status : nullptr;
@@ -515,15 +570,44 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
 
     BQ_CKC(cudaMemsetAsync(ctrl, 0, (MAX_LEVELS + 1) * sizeof(LevelCtrl), s));
     BQ_CKC(cudaMemsetAsync(fb_count, 0, 12 * sizeof(uint32_t), s));
+    const int aligned = aligned16(user) && aligned16(scratch);
+    // children sink of level `lv` (its children form level lv+1; the root is
+    // the only "child" of the virtual level -1, counted in `root`)
+    auto sink = [&](int lv, int set) {
+        PostParams<KT> Q{};
+        const int np = (lv + 1) & 1;
+        Q.pass.bufs[0] = user;
+        Q.pass.bufs[1] = scratch;
+        Q.next_segs = segs[np];
+        Q.next_tile_map = tile_map[np];
+        Q.next_cursor = cursor[np];
+        Q.next_ecursor = ecursor[np];
+        Q.status = lb_status;
+        Q.next_msegs = msegs[np];
+        Q.next_mtile_map = mtile_map[np];
+        Q.next_mhist = mhist[np];
+        Q.mhstride = (uint32_t)L.max_segs;
+        Q.child_ctrl = lv < 0 ? root : ctrl + lv;
+        Q.leaves = leaves[set];
+        Q.leaf_counts = leaf_counts[set];
+        Q.leaf_cap = (uint32_t)L.max_leaves;
+        Q.fallback = fallback;
+        Q.fallback_count = fb_count;
+        Q.leaf_max = S;
+        Q.depth_limit = depth_limit;
+        Q.pivot_rule = rule;
+        Q.ways = ways;
+        Q.emit_children = 1;
+        Q.band_inline_max = BAND_INLINE_MAX;
+        return Q;
+    };
     {
-        const uint32_t nt0 = seg_ntiles(0, (uint32_t)n, TILE);
-        k_init_root<KT><<<(nt0 + 255) / 256, 256, 0, s>>>(segs[0], tile_map[0], cursor[0], ecursor[0], lb_status,
-                                                          root, user, (uint32_t)n, rule);
+        PostParams<KT> Q0 = sink(-1, 0);
+        k_init_root<KT, POST_THREADS><<<1, POST_THREADS, 0, s>>>(Q0, (uint32_t)n);
         BQ_CKC(cudaGetLastError());
         local.kernel_launches++;
     }
 
-    const int aligned = aligned16(user) && aligned16(scratch);
     int level = 0;
     bool done = false;
     for (int batch = 0; !done; batch++) {
@@ -536,8 +620,41 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
         if (batch >= 2) BQ_CKC(cudaStreamWaitEvent(s, ev_leaves[set], 0));
         BQ_CKC(cudaMemsetAsync(leaf_counts[set], 0, 4 * sizeof(uint32_t), s));
         for (int k = 0; k < LEVEL_BATCH; k++, level++) {
-            const int cp = level & 1, np = cp ^ 1;
+            const int cp = level & 1;
             const LevelCtrl *prev = level == 0 ? root : ctrl + level - 1;
+            PostParams<KT> Q = sink(level, set);
+            if (timing) {
+                cudaEvent_t e0, e1;
+                BQ_CKC(cudaEventCreate(&e0));
+                evs.push_back(e0);
+                BQ_CKC(cudaEventCreate(&e1));
+                evs.push_back(e1);
+                BQ_CKC(cudaEventRecord(e0, s));
+            }
+            if constexpr (!KT::is_record) if (ways > 2) {
+                // the level's multiway segments: count, scan, scatter, children
+                MwParams<KT> MP{};
+                MP.bufs[0] = user;
+                MP.bufs[1] = scratch;
+                MP.msegs = msegs[cp];
+                MP.tile_map = mtile_map[cp];
+                MP.hist = mhist[cp];
+                MP.cursor = mcursor[cp];
+                MP.hstride = (uint32_t)L.max_segs;
+                MP.nseg_dev = &prev->nmseg_next;
+                MP.ntiles_dev = &prev->nmtiles_next;
+                MP.n_total = n;
+                MP.aligned = aligned;
+                MP.ctrl = ctrl + level;
+                st = launch_multiway<KT>(MP, ctrl + level, s);
+                if (st != BQ_OK) { cleanup(); return st; }
+                local.kernel_launches += 3;
+                Q.mw = MP;
+                k_post_mw<KT, POST_THREADS><<<POST_GRID, POST_THREADS, 0, s>>>(Q);
+                BQ_CKC(cudaGetLastError());
+                local.kernel_launches++;
+            }
+            // the level's binary segments
             PassParams<KT> P{};
             P.bufs[0] = user;
             P.bufs[1] = scratch;
@@ -555,37 +672,14 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
             P.ntiles_dev = &prev->ntiles_next;
             P.n_total = n;
             P.aligned = aligned;
-            if (timing) {
-                cudaEvent_t e0, e1;
-                BQ_CKC(cudaEventCreate(&e0));
-                evs.push_back(e0);
-                BQ_CKC(cudaEventCreate(&e1));
-                evs.push_back(e1);
-                BQ_CKC(cudaEventRecord(e0, s));
-            }
             st = launch_partition<KT>(P, s);
             if (st != BQ_OK) { cleanup(); return st; }
             local.kernel_launches++;
             if (timing) BQ_CKC(cudaEventRecord(evs.back(), s));
 
-            PostParams<KT> Q{};
             Q.pass = P;
-            Q.next_segs = segs[np];
-            Q.next_tile_map = tile_map[np];
-            Q.next_cursor = cursor[np];
-            Q.next_ecursor = ecursor[np];
-            Q.band_inline_max = BAND_INLINE_MAX;
-            Q.leaves = leaves[set];
-            Q.leaf_counts = leaf_counts[set];
-            Q.fallback = fallback;
-            Q.fallback_count = fb_count;
             Q.d_counts = nullptr;
             Q.nseg_dev = &prev->nseg_next;
-            Q.leaf_max = S;
-            Q.leaf_cap = (uint32_t)L.max_leaves;
-            Q.depth_limit = depth_limit;
-            Q.pivot_rule = rule;
-            Q.emit_children = 1;
             k_post<KT, POST_THREADS><<<POST_GRID, POST_THREADS, 0, s>>>(Q);
             BQ_CKC(cudaGetLastError());
             local.kernel_launches++;
@@ -612,7 +706,7 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
         // is there a next level?
         BQ_CKC(cudaMemcpyAsync(hctrl + level - 1, ctrl + level - 1, sizeof(LevelCtrl), cudaMemcpyDeviceToHost, s));
         BQ_CKC(cudaStreamSynchronize(s));
-        done = hctrl[level - 1].nseg_next == 0;
+        done = hctrl[level - 1].nseg_next == 0 && hctrl[level - 1].nmseg_next == 0;
     }
     LP.count_dev = nullptr;
     BQ_CKC(cudaStreamWaitEvent(s, ev_leaves[0], 0));
@@ -621,12 +715,12 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
     // statistics of every level, and the depth-capped segments
     BQ_CKC(cudaMemcpyAsync(hctrl, ctrl, level * sizeof(LevelCtrl), cudaMemcpyDeviceToHost, s));
     uint32_t nfb_total = 0;
-    BQ_CKC(cudaMemcpyAsync(&hctrl[MAX_LEVELS].pad, fb_count, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    BQ_CKC(cudaMemcpyAsync(&hctrl[MAX_LEVELS].pad2[0], fb_count, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
     BQ_CKC(cudaStreamSynchronize(s));
-    nfb_total = hctrl[MAX_LEVELS].pad;
+    nfb_total = hctrl[MAX_LEVELS].pad2[0];
     for (int l = 0; l < level; l++) {
         const LevelCtrl &hc = hctrl[l];
-        const uint32_t nseg_l = l == 0 ? 1u : hctrl[l - 1].nseg_next;
+        const uint32_t nseg_l = l == 0 ? 1u : hctrl[l - 1].nseg_next + hctrl[l - 1].nmseg_next;
         if (nseg_l == 0) break;
         local.levels++;
         local.partition_launches++;

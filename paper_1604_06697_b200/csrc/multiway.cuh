@@ -1,0 +1,546 @@
+// multiway.cuh — SURVEY §8(f) N4: the multi-pivot block partition.
+//
+// The paper lists a multi-pivot BlockQuicksort as future work ("A three-pivot
+// version might be interesting") and describes where many pivots
+// lead: Super Scalar Sample Sort, whose bucket is found "by converting the
+// results of comparisons to integers and then simply performing integer
+// arithmetic".  On the GPU a k-way pass divides every segment by
+// up to k = 16 in one read + one write, so a sort needs about
+// log16(n/S) scatter passes (+ one read-only count pass each) instead of
+// log2(n/S) binary ones.
+//
+// A multiway segment carries up to 15 splitters s_1 <= ... <= s_15, drawn as
+// quantiles of a 256-key sample (jittered strata, R19), in an implicit search
+// tree: tree[1] = s_8, tree[2..3] = s_4, s_12, ..., tree[8..15] = s_1, s_3, ...
+// The bucket of key k is #{i : s_i < k}, found branch-free with four
+// compare-and-shift steps (idx = 2*idx + (tree[idx] < k)).  Only segments whose
+// real splitters are distinct (and below the sample's maximum) are split this
+// way — every bucket is then a strict subset of the segment, so the recursion
+// progresses; a segment whose sample shows duplicates goes to the binary
+// three-way partition instead, whose equal band absorbs them.
+//
+// Per level:
+//   k_mw_count    read-only pass: per-segment bucket histogram (warp ballots)
+//   k_mw_scan     bucket starts = exclusive scan of the histogram
+//   k_mw_scatter  the pass itself: classify, rank inside the warp with ballots
+//                 and popcounts (the k-bucket analogue of the offset buffers),
+//                 claim each bucket run's output with one atomicAdd per
+//                 bucket and tile (consumed one tile later), stage the runs
+//                 in shared memory aligned like their destinations, TMA bulk
+//                 stores
+//   k_post_mw     children: leaves, next-level multiway or binary segments
+#pragma once
+
+namespace bq {
+
+constexpr int MW_K = 16;         // buckets of a multiway segment
+constexpr int MW_SAMPLE = 256;   // sample keys per segment (8 per lane of one warp)
+
+template <class KT>
+struct alignas(16) MSeg {
+    Seg s;                          // begin, len, tile_base, ntiles, depth, parity (pivot unused)
+    typename KT::K tree[MW_K];      // implicit search tree, tree[1..15]
+    uint32_t start[MW_K];           // bucket starts relative to begin (k_mw_scan)
+};
+
+template <class KT>
+__device__ __forceinline__ uint32_t mw_bucket(const typename KT::K *tree, typename KT::K k) {
+    uint32_t idx = 1;
+#pragma unroll
+    for (int d = 0; d < 4; d++) idx = 2 * idx + (tree[idx] < k ? 1u : 0u);
+    return idx - MW_K;
+}
+
+// position of sample key j of MW_SAMPLE in [b, b+len): jittered strata (R19)
+__device__ __forceinline__ uint64_t mw_sample_pos(uint32_t b, uint32_t len, uint32_t j) {
+    const uint64_t s0 = ((uint64_t)j * len) / MW_SAMPLE, s1 = ((uint64_t)(j + 1) * len) / MW_SAMPLE;
+    const uint64_t r = splitmix64((((uint64_t)b << 32) | len) + (uint64_t)(j + 1) * 0x9E3779B97F4A7C15ull) >> 32;
+    const uint64_t pos = s0 + ((r * (s1 - s0)) >> 32);
+    return (uint64_t)b + (pos < len - 1 ? pos : len - 1);
+}
+
+// The 256 sample keys of [b, b+len) sorted across one warp: index i = lane + 32 r
+// is held by lane `lane` in v[r].  Bitonic network: register compare-exchanges
+// for index bits 5-7, shuffles for bits 0-4.
+template <class KT>
+__device__ __forceinline__ void mw_sample_sorted(const typename KT::T *buf, uint32_t b, uint32_t len, uint32_t lane,
+                                                 typename KT::K (&v)[8]) {
+    using K = typename KT::K;
+#pragma unroll
+    for (int r = 0; r < 8; r++) v[r] = load_key<KT>(buf, mw_sample_pos(b, len, lane + 32 * r));
+#pragma unroll
+    for (int m = 1; m <= 8; m++) {
+#pragma unroll
+        for (int bb = m - 1; bb >= 0; bb--) {
+            if (bb >= 5) {
+                const int rb = bb - 5;
+#pragma unroll
+                for (int r = 0; r < 8; r++) {
+                    if (r & (1 << rb)) continue;
+                    const int r2 = r | (1 << rb);
+                    // direction of index bit m (a register bit for m >= 5, a lane bit below)
+                    const bool asc = m == 8 || (m >= 5 ? ((r >> (m - 5)) & 1) == 0 : ((lane >> m) & 1) == 0);
+                    const K lo = v[r2] < v[r] ? v[r2] : v[r], hi = v[r2] < v[r] ? v[r] : v[r2];
+                    v[r] = asc ? lo : hi;
+                    v[r2] = asc ? hi : lo;
+                }
+            } else {
+#pragma unroll
+                for (int r = 0; r < 8; r++) {
+                    const uint32_t i = lane + 32 * r;
+                    const K p = __shfl_xor_sync(0xffffffffu, v[r], 1 << bb);
+                    const bool lower = ((lane >> bb) & 1) == 0;
+                    const bool asc = m == 8 || ((i >> m) & 1) == 0;
+                    v[r] = (lower == asc) ? (p < v[r] ? p : v[r]) : (v[r] < p ? p : v[r]);
+                }
+            }
+        }
+    }
+}
+
+// sorted[q] of a warp-sorted sample, for a per-lane q (all lanes participate)
+template <class K>
+__device__ __forceinline__ K mw_pick(const K (&v)[8], uint32_t q) {
+    K out = v[0];
+#pragma unroll
+    for (int r = 0; r < 8; r++) {
+        const K t = __shfl_sync(0xffffffffu, v[r], q & 31);
+        out = (q >> 5) == (uint32_t)r ? t : out;
+    }
+    return out;
+}
+
+// Splitters for a segment of len keys (called by a whole warp).  Returns true
+// (and the search tree, in lanes 1..15 for node = lane) when the segment is to
+// be split multiway: k_eff = min(16, max(2, ceil(2 len / S))) buckets, real
+// splitters at sample quantiles 256 i / k_eff, pairwise distinct and below the
+// sample maximum; the tree's unused slots repeat the last real splitter
+// (empty buckets).  Otherwise returns false and `pivot` = the sample's lower
+// median, for the binary three-way partition.
+template <class KT>
+__device__ bool mw_splitters(const typename KT::T *buf, uint32_t b, uint32_t len, uint32_t leaf_max, uint32_t lane,
+                             typename KT::K &node_val, typename KT::K &pivot) {
+    using K = typename KT::K;
+    K v[8];
+    mw_sample_sorted<KT>(buf, b, len, lane, v);
+    uint64_t ke = ((uint64_t)len * 2 + leaf_max - 1) / leaf_max;
+    const uint32_t keff = (uint32_t)(ke < 2 ? 2 : (ke > MW_K ? MW_K : ke));
+    // lane i (1 <= i < keff) holds real splitter s_i; lanes i >= keff repeat s_{keff-1}
+    const uint32_t i = lane < 1 ? 1 : (lane < keff ? lane : keff - 1);
+    const K s = mw_pick(v, (i * MW_SAMPLE) / keff);
+    const K smax = __shfl_sync(0xffffffffu, v[7], 31);
+    pivot = mw_pick(v, MW_SAMPLE / 2 - 1);
+    const K s_next = __shfl_down_sync(0xffffffffu, s, 1);
+    const bool bad = (lane >= 1 && lane + 1 < keff && !(s < s_next)) || (lane == keff - 1 && !(s < smax));
+    const bool ok = __ballot_sync(0xffffffffu, bad) == 0;
+    // tree node `lane` (1..15) at depth d, position p holds s_{(2p+1) * 2^(3-d)}
+    uint32_t si = 0;
+    if (lane >= 1 && lane < MW_K) {
+        const uint32_t d = 31 - __clz(lane);
+        const uint32_t p = lane - (1u << d);
+        si = (2 * p + 1) << (3 - d);
+    }
+    node_val = __shfl_sync(0xffffffffu, s, si);
+    return ok;
+}
+
+// ---------------------------------------------------------------------------
+template <class KT>
+struct MwParams {
+    using T = typename KT::T;
+    T *bufs[2];
+    MSeg<KT> *msegs;
+    const uint32_t *tile_map;
+    uint32_t *hist;      // [bucket * hstride + segment]
+    uint32_t *cursor;    // [bucket * hstride + segment]
+    uint32_t hstride;
+    uint32_t *ticket;
+    const uint32_t *nseg_dev;
+    const uint32_t *ntiles_dev;
+    uint64_t n_total;
+    int aligned;
+    LevelCtrl *ctrl;     // element-pass statistics
+};
+
+template <class KT, int NT, int IPT, int STAGES>
+struct MwSmem {
+    using T = typename KT::T;
+    using K = typename KT::K;
+    static constexpr int TILE = NT * IPT;
+    static constexpr int NW = NT / 32;
+    alignas(128) T in[STAGES][TILE];
+    alignas(128) T out[TILE + MW_K * 8 + 16];   // runs + per-run alignment slack
+    K tree[STAGES][MW_K];
+    uint32_t start[STAGES][MW_K];
+    uint32_t sb[STAGES], slen[STAGES], stb[STAGES], spar[STAGES], sidx[STAGES], tile[STAGES], manual[STAGES];
+    uint64_t full[STAGES];
+    uint64_t empty[STAGES];
+    uint32_t whist[2][NW][MW_K];   // per-warp bucket counts, by iteration parity
+    uint32_t delta[2][MW_K];       // staging shift per bucket (shifted start - unshifted start)
+    uint32_t gstart[2][MW_K];      // global start of each run (low 32 bits of the element index)
+    uint32_t cnt[2][MW_K];         // run lengths
+    uint32_t sh[2][MW_K];          // shifted staging start of each run
+};
+
+template <class KT>
+constexpr int mw_smem_bytes() {
+    return (int)sizeof(MwSmem<KT, Tune<KT>::PART_THREADS, Tune<KT>::PART_IPT, Tune<KT>::PART_STAGES>);
+}
+
+// loader warp shared by the count and the scatter kernel: claims tiles in order,
+// copies the segment's metadata into the stage and issues the TMA bulk load
+template <class KT, int NT, int IPT, int STAGES>
+__device__ __forceinline__ void mw_loader(const MwParams<KT> &P, MwSmem<KT, NT, IPT, STAGES> &sm, uint32_t ntiles,
+                                          bool need_start) {
+    using T = typename KT::T;
+    constexpr uint32_t TILE = NT * IPT;
+    constexpr uint32_t W = sizeof(T), VW = 16 / W;
+    for (uint32_t i = 0;; i++) {
+        const uint32_t s = i % STAGES;
+        mbar_wait(&sm.empty[s], ((i / STAGES) & 1) ^ 1);
+        const uint32_t t = atomicAdd(P.ticket, 1u);
+        sm.tile[s] = t;
+        if (t >= ntiles) {
+            mbar_arrive(&sm.full[s]);
+            break;
+        }
+        const uint32_t si = P.tile_map[t];
+        const MSeg<KT> &ms = P.msegs[si];
+        const Seg sg = ms.s;
+#pragma unroll
+        for (int q = 1; q < MW_K; q++) sm.tree[s][q] = ms.tree[q];
+        if (need_start)
+#pragma unroll
+            for (int q = 0; q < MW_K; q++) sm.start[s][q] = ms.start[q];
+        sm.sb[s] = sg.begin;
+        sm.slen[s] = sg.len;
+        sm.stb[s] = sg.tile_base;
+        sm.spar[s] = sg.parity;
+        sm.sidx[s] = si;
+        const TileGeom<KT, TILE> G(sg, t);
+        const uint64_t lo16 = (G.tbeg + G.vlo) / VW * VW;
+        const uint64_t hi16 = (G.tbeg + G.vhi + VW - 1) / VW * VW;
+        const T *src = sg.parity ? P.bufs[1] : P.bufs[0];
+        const bool tma = P.aligned && hi16 <= P.n_total;
+        sm.manual[s] = !tma;
+        if (tma) {
+            const uint32_t bytes = (uint32_t)((hi16 - lo16) * W);
+            mbar_arrive_expect_tx(&sm.full[s], bytes);
+            tma_load_1d(&sm.in[s][lo16 - G.tbeg], src + lo16, bytes, &sm.full[s]);
+        } else {
+            mbar_arrive(&sm.full[s]);
+        }
+    }
+}
+
+// a consumer's IPT keys of stage s (conflict-free permuted 16-byte vectors),
+// their buckets, and a validity mask (bit c) for partial tiles
+template <class KT, int NT, int IPT, int STAGES>
+__device__ __forceinline__ uint32_t mw_load_classify(const MwParams<KT> &P, MwSmem<KT, NT, IPT, STAGES> &sm,
+                                                     uint32_t s, uint32_t t, uint32_t lane, uint32_t tid,
+                                                     typename KT::T (&x)[IPT], uint32_t (&bk)[IPT]) {
+    using T = typename KT::T;
+    using K = typename KT::K;
+    constexpr uint32_t TILE = NT * IPT;
+    constexpr uint32_t W = sizeof(T), VW = 16 / W, NV4 = IPT / VW;
+    const uint32_t sw = NV4 > 1 ? ((lane * NV4) / 8) & (NV4 - 1) : 0;
+    const uint32_t e0 = tid * IPT;
+    Seg sg;
+    sg.begin = sm.sb[s];
+    sg.len = sm.slen[s];
+    sg.tile_base = sm.stb[s];
+    const TileGeom<KT, TILE> G(sg, t);
+    uint32_t valid = (1u << IPT) - 1;
+    if (!sm.manual[s]) {
+        const uint4 *in4 = reinterpret_cast<const uint4 *>(&sm.in[s][e0]);
+#pragma unroll
+        for (uint32_t k = 0; k < NV4; k++) {
+            const uint4 v = in4[k ^ sw];
+            memcpy(&x[k * VW], &v, 16);
+        }
+    } else {
+        const T *src = sm.spar[s] ? P.bufs[1] : P.bufs[0];
+#pragma unroll
+        for (uint32_t k = 0; k < NV4; k++)
+#pragma unroll
+            for (uint32_t j = 0; j < VW; j++) {
+                const uint32_t pos = e0 + (k ^ sw) * VW + j;
+                x[k * VW + j] = (pos >= G.vlo && pos < G.vhi) ? src[G.tbeg + pos] : T{};
+            }
+    }
+    if (G.vlo != 0 || G.vhi != TILE) {
+        valid = 0;
+#pragma unroll
+        for (uint32_t k = 0; k < NV4; k++)
+#pragma unroll
+            for (uint32_t j = 0; j < VW; j++) {
+                const uint32_t pos = e0 + (k ^ sw) * VW + j;
+                valid |= (uint32_t)(pos >= G.vlo && pos < G.vhi) << (k * VW + j);
+            }
+    }
+    const K *tree = sm.tree[s];
+#pragma unroll
+    for (uint32_t c = 0; c < IPT; c++) bk[c] = mw_bucket<KT>(tree, KT::key(x[c]));
+    return valid;
+}
+
+// lanes' bucket masks of one key slot across the warp: bit l of the result is
+// set iff lane l's key (in this slot, valid) is in bucket `b`
+__device__ __forceinline__ uint32_t mw_match(uint32_t v0, uint32_t v1, uint32_t v2, uint32_t v3, uint32_t vm,
+                                             uint32_t b) {
+    const uint32_t m0 = (b & 1) ? v0 : ~v0, m1 = (b & 2) ? v1 : ~v1;
+    const uint32_t m2 = (b & 4) ? v2 : ~v2, m3 = (b & 8) ? v3 : ~v3;
+    return m0 & m1 & m2 & m3 & vm;
+}
+
+// ---- k_mw_count ---------------------------------------------------------------
+template <class KT, int NT, int IPT, int STAGES, int MINB>
+__global__ void __launch_bounds__(NT + 32, MINB) k_mw_count(MwParams<KT> P) {
+    using SM = MwSmem<KT, NT, IPT, STAGES>;
+    constexpr uint32_t NW = SM::NW;
+    extern __shared__ __align__(128) unsigned char smraw[];
+    SM &sm = *reinterpret_cast<SM *>(smraw);
+    const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t ntiles = *P.ntiles_dev;
+    if (tid == 0) {
+        for (int s = 0; s < STAGES; s++) {
+            mbar_init(&sm.full[s], 1);
+            mbar_init(&sm.empty[s], NW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        fence_proxy_async_smem();
+    }
+    __syncthreads();
+    if (warp == NW) {
+        if (lane == 0) mw_loader<KT, NT, IPT, STAGES>(P, sm, ntiles, false);
+        return;
+    }
+    // lane L < 16 counts bucket L for this warp's keys of the current segment
+    uint32_t run = 0, cur_seg = 0xffffffffu;
+    for (uint32_t i = 0;; i++) {
+        const uint32_t s = i % STAGES;
+        mbar_wait(&sm.full[s], (i / STAGES) & 1);
+        const uint32_t t = sm.tile[s];
+        if (t >= ntiles) break;
+        const uint32_t si = sm.sidx[s];
+        typename KT::T x[IPT];
+        uint32_t bk[IPT];
+        const uint32_t valid = mw_load_classify<KT, NT, IPT, STAGES>(P, sm, s, t, lane, tid, x, bk);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.empty[s]);
+        if (si != cur_seg) {
+            if (cur_seg != 0xffffffffu && lane < MW_K && run) atomicAdd(&P.hist[lane * P.hstride + cur_seg], run);
+            run = 0;
+            cur_seg = si;
+        }
+#pragma unroll
+        for (uint32_t c = 0; c < IPT; c++) {
+            const uint32_t v0 = __ballot_sync(0xffffffffu, bk[c] & 1), v1 = __ballot_sync(0xffffffffu, bk[c] & 2);
+            const uint32_t v2 = __ballot_sync(0xffffffffu, bk[c] & 4), v3 = __ballot_sync(0xffffffffu, bk[c] & 8);
+            const uint32_t vm = __ballot_sync(0xffffffffu, (valid >> c) & 1);
+            run += __popc(mw_match(v0, v1, v2, v3, vm, lane));
+        }
+    }
+    if (cur_seg != 0xffffffffu && lane < MW_K && run) atomicAdd(&P.hist[lane * P.hstride + cur_seg], run);
+}
+
+// ---- k_mw_scan: bucket starts and cursor reset, one warp per segment ---------------
+template <class KT>
+__global__ void k_mw_scan(MwParams<KT> P) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t nseg = *P.nseg_dev;
+    for (uint32_t si = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); si < nseg;
+         si += gridDim.x * (blockDim.x / 32)) {
+        const uint32_t h = lane < MW_K ? P.hist[lane * P.hstride + si] : 0;
+        uint32_t inc = h;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+            if (lane >= (uint32_t)d) inc += o;
+        }
+        if (lane < MW_K) {
+            P.msegs[si].start[lane] = inc - h;
+            P.cursor[lane * P.hstride + si] = 0;
+        }
+        if (lane == 31) atomicAdd(&P.ctrl->element_passes, (unsigned long long)inc);
+    }
+}
+
+// ---- k_mw_scatter -------------------------------------------------------------
+template <class KT, int NT, int IPT, int STAGES, int MINB>
+__global__ void __launch_bounds__(NT + 32, MINB) k_mw_scatter(MwParams<KT> P) {
+    using T = typename KT::T;
+    using SM = MwSmem<KT, NT, IPT, STAGES>;
+    constexpr uint32_t NW = SM::NW;
+    constexpr uint32_t W = sizeof(T), VW = 16 / W;
+    static_assert(IPT <= 16, "packed ranks");
+    extern __shared__ __align__(128) unsigned char smraw[];
+    SM &sm = *reinterpret_cast<SM *>(smraw);
+    const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t ntiles = *P.ntiles_dev;
+    if (tid == 0) {
+        for (int s = 0; s < STAGES; s++) {
+            mbar_init(&sm.full[s], 1);
+            mbar_init(&sm.empty[s], NW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        fence_proxy_async_smem();
+    }
+    __syncthreads();
+    if (warp == NW) {
+        if (lane == 0) mw_loader<KT, NT, IPT, STAGES>(P, sm, ntiles, true);
+        return;
+    }
+
+    // previous tile, carried one iteration: keys, and (tile-local offset | bucket << 16 | invalid << 31)
+    T y[IPT];
+    uint32_t ypk[IPT];
+    bool have_prev = false;
+    T *p_dst = nullptr;
+    // warp 0, lane L < 16: the previous tile's bucket-L run: atomic result, length, segment begin/start
+    uint32_t p_old = 0, p_cnt = 0, p_off = 0;
+    uint64_t p_base = 0;
+
+    for (uint32_t i = 0;; i++) {
+        const uint32_t s = i % STAGES, par = i & 1;
+        mbar_wait(&sm.full[s], (i / STAGES) & 1);
+        const uint32_t t = sm.tile[s];
+        const bool cur = t < ntiles;
+        T x[IPT];
+        uint32_t pk[IPT];
+        uint32_t si = 0, sbeg = 0, spar = 0, bstart = 0;
+        if (cur) {
+            si = sm.sidx[s];
+            sbeg = sm.sb[s];
+            spar = sm.spar[s];
+            bstart = lane < MW_K ? sm.start[s][lane] : 0;
+            // pk[c] holds the bucket first, then the packed rank
+            const uint32_t valid = mw_load_classify<KT, NT, IPT, STAGES>(P, sm, s, t, lane, tid, x, pk);
+            // ranks inside the warp: slot-major, then lane (the k-bucket offset buffers)
+            uint32_t run = 0;   // lane L < 16: this warp's keys in bucket L so far
+            const uint32_t lt = lanemask_lt();
+#pragma unroll
+            for (uint32_t c = 0; c < IPT; c++) {
+                const uint32_t b = pk[c];
+                const uint32_t v0 = __ballot_sync(0xffffffffu, b & 1), v1 = __ballot_sync(0xffffffffu, b & 2);
+                const uint32_t v2 = __ballot_sync(0xffffffffu, b & 4), v3 = __ballot_sync(0xffffffffu, b & 8);
+                const uint32_t vm = __ballot_sync(0xffffffffu, (valid >> c) & 1);
+                const uint32_t before = __shfl_sync(0xffffffffu, run, b);
+                const uint32_t mine = mw_match(v0, v1, v2, v3, vm, b);
+                pk[c] = (before + __popc(mine & lt)) | (b << 16) | ((((valid >> c) & 1) ^ 1) << 31);
+                run += __popc(mw_match(v0, v1, v2, v3, vm, lane));
+            }
+            if (lane < MW_K) sm.whist[par][warp][lane] = run;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.empty[s]);
+
+        // warp 0: placement of the previous tile's runs, now that its atomics returned
+        if (warp == 0 && have_prev) {
+            const uint32_t L = lane;
+            const uint64_t g = p_base + p_old;                       // global start of run L
+            const uint32_t a = (uint32_t)(g % VW);
+            const uint32_t padded = L < MW_K ? (a + p_cnt + VW - 1) / VW * VW : 0;
+            uint32_t inc = padded;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+                if (lane >= (uint32_t)d) inc += o;
+            }
+            if (L < MW_K) {
+                const uint32_t shs = inc - padded + a;             // shifted staging start
+                sm.delta[par ^ 1][L] = shs - p_off;
+                sm.sh[par ^ 1][L] = shs;
+                sm.gstart[par ^ 1][L] = (uint32_t)g;
+                sm.cnt[par ^ 1][L] = p_cnt;
+            }
+        }
+        if (tid < MW_K) bulk_wait_read0();   // the previous bulk stores (one group per run) have read `out`
+        named_bar_sync(1, NT);               // B1
+
+        if (cur) {
+            // this warp's run offsets inside the tile: lane L < 16 -> bucket L
+            uint32_t pre = 0, tot = 0;
+            if (lane < MW_K) {
+#pragma unroll
+                for (uint32_t w2 = 0; w2 < NW; w2++) {
+                    const uint32_t v = sm.whist[par][w2][lane];
+                    pre += w2 < warp ? v : 0;
+                    tot += v;
+                }
+            }
+            uint32_t toff = tot;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t o = __shfl_up_sync(0xffffffffu, toff, d);
+                if (lane >= (uint32_t)d) toff += o;
+            }
+            toff -= tot;   // exclusive over buckets
+            const uint32_t wbase = toff + pre;
+#pragma unroll
+            for (uint32_t c = 0; c < IPT; c++) {
+                const uint32_t b = (pk[c] >> 16) & 0x7fff;
+                pk[c] += __shfl_sync(0xffffffffu, wbase, b);
+            }
+            if (warp == 0) {
+                // claim the tile's runs: one atomic per bucket, consumed next iteration
+                const uint32_t old = (lane < MW_K && tot) ? atomicAdd(&P.cursor[lane * P.hstride + si], tot) : 0;
+                p_old = old;   // (register dependency resolved only next iteration)
+                p_cnt = lane < MW_K ? tot : 0;
+                p_off = toff;
+                p_base = (uint64_t)sbeg + bstart;
+            }
+        }
+
+        if (have_prev) {
+            // stage the previous tile's runs aligned like their destinations
+#pragma unroll
+            for (uint32_t c = 0; c < IPT; c++) {
+                const uint32_t v = ypk[c];
+                if (!(v >> 31)) sm.out[(v & 0xffff) + sm.delta[par ^ 1][(v >> 16) & 0x7fff]] = y[c];
+            }
+            if (P.aligned) fence_proxy_async_smem();
+            named_bar_sync(1, NT);   // B2
+            T *d = p_dst;
+            if (!P.aligned) {
+                // unaligned buffers: plain stores, run by run
+                for (uint32_t L = 0; L < MW_K; L++) {
+                    const uint32_t n = sm.cnt[par ^ 1][L];
+                    const uint64_t g = (uint64_t)sm.gstart[par ^ 1][L];
+                    for (uint32_t q = tid; q < n; q += NT) d[g + q] = sm.out[sm.sh[par ^ 1][L] + q];
+                }
+            } else {
+                if (tid < MW_K) {
+                    const uint32_t L = tid, n = sm.cnt[par ^ 1][L];
+                    const uint64_t g = sm.gstart[par ^ 1][L], ge = g + n;
+                    const uint64_t bs = (g + VW - 1) / VW * VW, be = ge / VW * VW;
+                    if (n && be > bs)
+                        tma_store_1d(d + bs, &sm.out[sm.sh[par ^ 1][L] + (bs - g)], (uint32_t)((be - bs) * W));
+                    bulk_commit();
+                } else if (tid >= 32 && tid < 32 + MW_K * 2 * VW) {
+                    // heads and tails (< 16 bytes) of every run
+                    const uint32_t u = tid - 32, L = u / (2 * VW), q = u % (2 * VW);
+                    const uint32_t n = sm.cnt[par ^ 1][L];
+                    const uint64_t g = sm.gstart[par ^ 1][L], ge = g + n;
+                    const uint64_t bs = (g + VW - 1) / VW * VW, be = ge / VW * VW;
+                    const bool tail = q >= VW;
+                    const uint32_t qq = tail ? q - VW : q;
+                    const uint64_t pos = tail ? (be > bs ? be : bs) + qq : g + qq;
+                    const bool ok = n && (tail ? (ge > bs && pos < ge) : (pos < (bs < ge ? bs : ge)));
+                    if (ok) d[pos] = sm.out[sm.sh[par ^ 1][L] + (pos - g)];
+                }
+            }
+        }
+        if (!cur) break;
+#pragma unroll
+        for (uint32_t c = 0; c < IPT; c++) {
+            y[c] = x[c];
+            ypk[c] = pk[c];
+        }
+        have_prev = true;
+        p_dst = spar ? P.bufs[0] : P.bufs[1];
+    }
+    if (tid < MW_K) bulk_wait0();
+}
+
+}  // namespace bq

@@ -62,6 +62,7 @@ __device__ __forceinline__ uint32_t pass_ntiles(const PassParams<KT> &P) {
 
 #include "partition_kernel.cuh"
 #include "partition_fast.cuh"
+#include "multiway.cuh"
 
 namespace bq {
 
@@ -91,6 +92,15 @@ struct PostParams {
     int32_t depth_limit;
     int32_t pivot_rule;
     int emit_children;      // 0 in the standalone pass
+    int ways;               // > 2: children may be split multiway (keys only)
+    uint64_t *status;       // next level's look-back words (ordered placement), or nullptr
+    LevelCtrl *child_ctrl;  // counters the children are appended to
+    // multiway: the level just scattered, and the next level's lists
+    MwParams<KT> mw;
+    MSeg<KT> *next_msegs;
+    uint32_t *next_mtile_map;
+    uint32_t *next_mhist;   // [bucket * mhstride + segment], zeroed for new segments
+    uint32_t mhstride;
 };
 
 template <class KT>
@@ -114,6 +124,112 @@ __device__ __forceinline__ SegCounts<KT> seg_counts(const PassParams<KT> &P, uin
 // becomes: both children are appended to the next level (with their pivot,
 // a1, their slice of the next tile map and a reset cursor), small ones to the
 // leaf lists, depth-capped ones to the fallback list.
+// a7 for up to MW_K children of one segment (or the root), by a whole CTA of
+// NT threads: each child becomes nothing (empty), a leaf (<= S), a
+// depth-capped fallback segment, or a next-level segment — multiway when
+// allowed and its 256-key sample gives distinct splitters (multiway.cuh), else
+// binary with the pivot of `pivot_rule` (the sample's median when multiway
+// was tried).  Warps select pivots/splitters, one thread per child appends
+// it, then the CTA writes the children's slices of the next tile maps.
+template <class KT, int NT>
+__device__ __forceinline__ void emit_children(const PostParams<KT> &Q, int nch, const uint32_t *cb,
+                                              const uint32_t *cl, uint8_t cp, uint16_t cd) {
+    using T = typename KT::T;
+    using K = typename KT::K;
+    constexpr uint32_t TILE = (uint32_t)tile_elems<KT>();
+    constexpr int NW = NT / 32;
+    enum { C_NONE = 0, C_LEAF, C_FALLBACK, C_BIN, C_MW };
+    __shared__ uint32_t s_kind[MW_K], s_idx[MW_K], s_tb[MW_K], s_nt[MW_K];
+    __shared__ uint64_t s_piv[MW_K];
+    __shared__ K s_tree[MW_K][MW_K];
+    LevelCtrl *C = Q.child_ctrl;
+    const T *cbuf = cp ? Q.pass.bufs[1] : Q.pass.bufs[0];
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    __syncthreads();   // the previous segment's readers of s_* are done
+    for (int c = warp; c < nch; c += NW) {
+        const uint32_t len = cl[c];
+        uint32_t kind = C_NONE;
+        if (len == 0) kind = C_NONE;
+        else if (len <= Q.leaf_max) kind = C_LEAF;
+        else if ((int)cd >= Q.depth_limit) kind = C_FALLBACK;
+        else if (Q.ways > 2 && !KT::is_record) {
+            K node, piv;
+            const bool ok = mw_splitters<KT>(cbuf, cb[c], len, Q.leaf_max, lane, node, piv);
+            kind = ok ? C_MW : C_BIN;
+            if (lane == 0) s_piv[c] = (uint64_t)piv;
+            if (lane < MW_K) s_tree[c][lane] = node;
+        } else {
+            const K piv = select_pivot_warp<KT>(cbuf, cb[c], len, Q.pivot_rule, lane);
+            if (lane == 0) s_piv[c] = (uint64_t)piv;
+            kind = C_BIN;
+        }
+        if (lane == 0) s_kind[c] = kind;
+    }
+    __syncthreads();
+    if ((int)threadIdx.x < nch) {
+        const int c = threadIdx.x;
+        const uint32_t kind = s_kind[c], len = cl[c];
+        s_nt[c] = 0;
+        if (kind == C_LEAF) {
+            // leaf lists are binned by sorting-network size (leaf.cuh)
+            const uint32_t lc = leaf_class<KT>(len);
+            const uint32_t li = atomicAdd(&Q.leaf_counts[lc], 1u);
+            atomicAdd(&C->nleaf_cls[lc], 1u);
+            atomicAdd(&C->nleaf, 1u);
+            Q.leaves[lc * Q.leaf_cap + li] = Leaf{cb[c], len, cp, 0};
+        } else if (kind == C_FALLBACK) {
+            const uint32_t fi = atomicAdd(Q.fallback_count, 1u);
+            atomicAdd(&C->nfallback, 1u);
+            Q.fallback[fi] = Leaf{cb[c], len, cp, 0};
+        } else if (kind == C_BIN || kind == C_MW) {
+            Seg ch;
+            ch.pivot = s_piv[c];
+            ch.begin = cb[c];
+            ch.len = len;
+            ch.ntiles = seg_ntiles(cb[c], len, TILE);
+            ch.depth = cd;
+            ch.parity = cp;
+            ch.pad0 = 0;
+            ch.pad1 = 0;
+            uint32_t ci;
+            if (kind == C_BIN) {
+                ch.tile_base = atomicAdd(&C->ntiles_next, ch.ntiles);
+                atomicMax(&C->maxtiles_next, ch.ntiles);
+                ci = atomicAdd(&C->nseg_next, 1u);
+                Q.next_segs[ci] = ch;
+                Q.next_cursor[ci] = 0;
+                Q.next_ecursor[ci] = 0;
+            } else {
+                ch.tile_base = atomicAdd(&C->nmtiles_next, ch.ntiles);
+                ci = atomicAdd(&C->nmseg_next, 1u);
+                MSeg<KT> &m = Q.next_msegs[ci];
+                m.s = ch;
+#pragma unroll
+                for (int q = 0; q < MW_K; q++) m.tree[q] = s_tree[c][q];
+            }
+            s_idx[c] = ci;
+            s_tb[c] = ch.tile_base;
+            s_nt[c] = ch.ntiles;
+        }
+    }
+    __syncthreads();
+    // the children's slices of the next level's tile maps (and resets)
+    for (int c = 0; c < nch; c++) {
+        const uint32_t kind = s_kind[c];
+        if (kind != C_BIN && kind != C_MW) continue;
+        const uint32_t nt = s_nt[c], tb = s_tb[c], ci = s_idx[c];
+        if (kind == C_BIN) {
+            for (uint32_t j = threadIdx.x; j < nt; j += NT) {
+                Q.next_tile_map[tb + j] = ci;
+                if (Q.status) Q.status[tb + j] = 0;
+            }
+        } else {
+            for (uint32_t j = threadIdx.x; j < nt; j += NT) Q.next_mtile_map[tb + j] = ci;
+            if (threadIdx.x < MW_K) Q.next_mhist[threadIdx.x * Q.mhstride + ci] = 0;
+        }
+    }
+}
+
 template <class KT, int NT>
 __device__ __forceinline__ void post_segment(const PostParams<KT> &Q, uint32_t si);
 
@@ -167,73 +283,13 @@ __device__ __forceinline__ void post_segment(const PostParams<KT> &Q, uint32_t s
     }
     if (!Q.emit_children) return;
 
-    __shared__ uint32_t s_idx[2], s_tb[2], s_nt[2];
-    __shared__ uint64_t s_piv[2];
-    __syncthreads();   // the previous segment's readers of s_* are done
-    const uint8_t cp = sg.parity ^ 1;
-    const T *cbuf = cp ? P.bufs[1] : P.bufs[0];
-    const uint32_t cb[2] = {sg.begin, sg.begin + L + E};
-    const uint32_t cl[2] = {L, G};
-    const uint16_t cd = sg.depth + 1;
-    if (threadIdx.x < 32) {
-        // a1: warp 0 selects the pivots of the children that go to the next level
-#pragma unroll
-        for (int c = 0; c < 2; c++)
-            if (cl[c] > Q.leaf_max && (int)cd < Q.depth_limit) {
-                const K pk = select_pivot_warp<KT>(cbuf, cb[c], cl[c], Q.pivot_rule, threadIdx.x);
-                if (threadIdx.x == 0) s_piv[c] = (uint64_t)pk;
-            }
-    }
     if (threadIdx.x == 0) {
         atomicAdd(&C->element_passes, (unsigned long long)sg.len);
         atomicAdd(&C->band_elems, (unsigned long long)E);
-#pragma unroll
-        for (int c = 0; c < 2; c++) {
-            s_nt[c] = 0;
-            if (cl[c] == 0) continue;
-            if (cl[c] <= Q.leaf_max) {
-                // leaf lists are binned by sorting-network size (leaf.cuh)
-                const uint32_t lc = leaf_class<KT>(cl[c]);
-                const uint32_t li = atomicAdd(&Q.leaf_counts[lc], 1u);
-                atomicAdd(&C->nleaf_cls[lc], 1u);
-                atomicAdd(&C->nleaf, 1u);
-                Q.leaves[lc * Q.leaf_cap + li] = Leaf{cb[c], cl[c], cp, 0};
-            } else if ((int)cd >= Q.depth_limit) {
-                const uint32_t fi = atomicAdd(Q.fallback_count, 1u);
-                atomicAdd(&C->nfallback, 1u);
-                Q.fallback[fi] = Leaf{cb[c], cl[c], cp, 0};
-            } else {
-                Seg ch;
-                ch.pivot = s_piv[c];
-                ch.begin = cb[c];
-                ch.len = cl[c];
-                ch.ntiles = seg_ntiles(cb[c], cl[c], TILE);
-                ch.tile_base = atomicAdd(&C->ntiles_next, ch.ntiles);
-                ch.depth = cd;
-                ch.parity = cp;
-                ch.pad0 = 0;
-                ch.pad1 = 0;
-                atomicMax(&C->maxtiles_next, ch.ntiles);
-                const uint32_t ci = atomicAdd(&C->nseg_next, 1u);
-                Q.next_segs[ci] = ch;
-                Q.next_cursor[ci] = 0;
-                Q.next_ecursor[ci] = 0;
-                s_idx[c] = ci;
-                s_tb[c] = ch.tile_base;
-                s_nt[c] = ch.ntiles;
-            }
-        }
     }
-    __syncthreads();
-    // the children's slices of the next level's tile map (and look-back words)
-#pragma unroll
-    for (int c = 0; c < 2; c++) {
-        const uint32_t nt = s_nt[c], tb = s_tb[c], ci = s_idx[c];
-        for (uint32_t j = threadIdx.x; j < nt; j += NT) {
-            Q.next_tile_map[tb + j] = ci;
-            if (P.status) P.status[tb + j] = 0;
-        }
-    }
+    const uint32_t cb[2] = {sg.begin, sg.begin + L + E};
+    const uint32_t cl[2] = {L, G};
+    emit_children<KT, NT>(Q, 2, cb, cl, (uint8_t)(sg.parity ^ 1), (uint16_t)(sg.depth + 1));
 }
 
 // Equal bands longer than band_inline_max, tile-parallel over the level
@@ -291,35 +347,28 @@ static __global__ void k_map(const Seg *segs, uint32_t *tile_map, uint64_t *stat
     }
 }
 
-// Root segment of a sort: [0, n) in the user buffer with its pivot (a1), its
-// tile map, cursor and look-back words.
-template <class KT>
-__global__ void k_init_root(Seg *segs, uint32_t *tile_map, unsigned long long *cursor, uint32_t *ecursor,
-                            uint64_t *status, LevelCtrl *root, const typename KT::T *buf, uint32_t n, int rule) {
-    constexpr uint32_t TILE = (uint32_t)tile_elems<KT>();
-    const uint32_t nt = seg_ntiles(0, n, TILE);
-    typename KT::K pk = 0;
-    if (blockIdx.x == 0 && threadIdx.x < 32) pk = select_pivot_warp<KT>(buf, 0, n, rule, threadIdx.x);
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        Seg s;
-        s.pivot = (uint64_t)pk;
-        s.begin = 0;
-        s.len = n;
-        s.tile_base = 0;
-        s.ntiles = nt;
-        s.depth = 0;
-        s.parity = 0;
-        s.pad0 = 0;
-        s.pad1 = 0;
-        segs[0] = s;
-        cursor[0] = 0;
-        ecursor[0] = 0;
-        root->nseg_next = 1;   // level 0's counts, read by its kernels from device memory
-        root->ntiles_next = nt;
-    }
-    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < nt; j += gridDim.x * blockDim.x) {
-        tile_map[j] = 0;
-        if (status) status[j] = 0;
+// Root segment of a sort: [0, n) in the user buffer becomes the first
+// binary or multiway segment (a1 pivot / splitters, tile map, counts in
+// Q.child_ctrl = the root's control block), exactly like a child.
+template <class KT, int NT>
+__global__ void __launch_bounds__(NT) k_init_root(PostParams<KT> Q, uint32_t n) {
+    const uint32_t cb[1] = {0}, cl[1] = {n};
+    emit_children<KT, NT>(Q, 1, cb, cl, 0, 0);
+}
+
+// a7 after a multiway scatter: the (up to) 16 buckets of every multiway
+// segment become its children.
+template <class KT, int NT>
+__global__ void __launch_bounds__(NT) k_post_mw(PostParams<KT> Q) {
+    __shared__ uint32_t cb[MW_K], cl[MW_K];
+    const uint32_t nseg = *Q.mw.nseg_dev;
+    for (uint32_t si = blockIdx.x; si < nseg; si += gridDim.x) {
+        const MSeg<KT> &m = Q.mw.msegs[si];
+        if (threadIdx.x < MW_K) {
+            cb[threadIdx.x] = m.s.begin + m.start[threadIdx.x];
+            cl[threadIdx.x] = Q.mw.hist[threadIdx.x * Q.mw.hstride + si];
+        }
+        emit_children<KT, NT>(Q, MW_K, cb, cl, (uint8_t)(m.s.parity ^ 1), (uint16_t)(m.s.depth + 1));
     }
 }
 

@@ -159,11 +159,12 @@ def test_depth_cap_fallback(B, kind):
     # a tiny Introsort limit sends segments to the merge-based fallback (a9)
     n = 300007
     a = make(kind, n, seed=9)
-    for limit in [0, 1, 3]:
-        t = to_dev(a)
-        st = B.bq_sort_ex(t, depth_limit=limit)
-        check_sorted_equal(kind, to_host(t, a), a)
-        assert st["fallback_segments"] >= 1
+    for ways, limits in [(2, [0, 1, 3]), (16, [0, 1])]:
+        for limit in limits:
+            t = to_dev(a)
+            st = B.bq_sort_ex(t, depth_limit=limit, ways=ways)
+            check_sorted_equal(kind, to_host(t, a), a)
+            assert st["fallback_segments"] >= 1
 
 
 def test_sort_deterministic(B):
@@ -420,3 +421,41 @@ def test_sort_patterns_ordered_placement(B, name):
     t = to_dev(a)
     B.bq_sort_ex(t, ordered=True)
     assert np.array_equal(t.cpu().numpy(), oracle.sort(a))
+
+
+# ------------------------------------------ multi-pivot block partition (N4) ---
+
+@pytest.mark.parametrize("kind", ["i32", "u64", "f64"])
+@pytest.mark.parametrize("dist", ["random", "dups"])
+def test_sort_multiway(B, kind, dist):
+    for n in [S_ + 1 for S_ in (LEAF[kind],)] + [100003, (1 << 20) + 17, (1 << 22) + 3]:
+        a = make(kind, n, seed=n % 97, dist=dist)
+        t = to_dev(a)
+        st = B.bq_sort_ex(t, ways=16)
+        check_sorted_equal(kind, to_host(t, a), a)
+        assert st["fallback_segments"] == 0
+
+
+@pytest.mark.parametrize("name", PATTERNS)
+def test_sort_multiway_patterns(B, name):
+    for n in [(1 << 16) + 3, (1 << 20) + 1]:
+        if name == "swaps_nlogn" and n > (1 << 17):
+            continue
+        a = bqgen.i32_pattern(name, n, seed=3)
+        t = to_dev(a)
+        st = B.bq_sort_ex(t, ways=16)
+        assert np.array_equal(t.cpu().numpy(), oracle.sort(a))
+        assert st["fallback_segments"] == 0
+
+
+def test_sort_multiway_configs(B):
+    for name in ["c1", "c2", "c4a", "c4b"]:
+        a = bqgen.config(name, 1 << 21, seed=5)
+        t = to_dev(a)
+        B.bq_sort_ex(t, ways=16)
+        assert np.array_equal(t.cpu().numpy(), oracle.sort(a))
+    for ordering in ["random", "ascending", "descending", "swapped"]:
+        a = bqgen.config("c3", 1 << 20, seed=5, ordering=ordering)
+        t = to_dev(a)
+        B.bq_sort_ex(t, ways=16)
+        assert np.array_equal(t.cpu().numpy().view(np.uint64), oracle.sort(a).view(np.uint64))
