@@ -167,8 +167,8 @@ bq_status launch_multiway(MwParams<KT> MP, LevelCtrl *lc, cudaStream_t s) {
     using Kn = Kernels<KT>;
     constexpr int smem = mw_smem_bytes<KT>();
     constexpr int threads = Kn::NT + 32;
-    auto kc = k_mw_count<KT, Kn::NT, Kn::IPT, Kn::STAGES, Kn::MINB>;
-    auto ks = k_mw_scatter<KT, Kn::NT, Kn::IPT, Kn::STAGES, Kn::MINB>;
+    auto kc = k_mw_count<KT, Kn::NT, Kn::IPT, MW_STAGES, Kn::MINB>;
+    auto ks = k_mw_scatter<KT, Kn::NT, Kn::IPT, MW_STAGES, Kn::MINB>;
     static int cap_c = 0, cap_s = 0;
     bq_status st = persistent_cap(kc, threads, smem, &cap_c);
     if (st != BQ_OK) return st;

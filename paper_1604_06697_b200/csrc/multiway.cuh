@@ -175,16 +175,42 @@ struct MwSmem {
     uint32_t sb[STAGES], slen[STAGES], stb[STAGES], spar[STAGES], sidx[STAGES], tile[STAGES], manual[STAGES];
     uint64_t full[STAGES];
     uint64_t empty[STAGES];
-    uint32_t whist[2][NW][MW_K];   // per-warp bucket counts, by iteration parity
+    // per-thread bucket counters, bucket-major (entry b*NT + t): thread t only
+    // touches its own column, so every access is free of bank conflicts; by
+    // iteration parity
+    uint32_t cnt_m[1][MW_K * NT];
+    uint32_t wtot[2][NW][MW_K / 2];   // per-warp bucket totals, two 16-bit fields per word
+    uint32_t wpre[2][NW][MW_K / 2];   // exclusive prefix of the warps' totals, packed likewise
+    uint32_t boff[2][MW_K + 1];       // bucket starts inside the tile (boff[16] = valid keys)
     uint32_t delta[2][MW_K];       // staging shift per bucket (shifted start - unshifted start)
     uint32_t gstart[2][MW_K];      // global start of each run (low 32 bits of the element index)
     uint32_t cnt[2][MW_K];         // run lengths
     uint32_t sh[2][MW_K];          // shifted staging start of each run
 };
 
+constexpr int MW_STAGES = 3;   // TMA ring depth of the multiway kernels (2 CTAs per SM)
+
 template <class KT>
 constexpr int mw_smem_bytes() {
-    return (int)sizeof(MwSmem<KT, Tune<KT>::PART_THREADS, Tune<KT>::PART_IPT, Tune<KT>::PART_STAGES>);
+    return (int)sizeof(MwSmem<KT, Tune<KT>::PART_THREADS, Tune<KT>::PART_IPT, MW_STAGES>);
+}
+
+// a thread's 16 bucket counters (its matrix column), packed two per word
+template <int NT>
+__device__ __forceinline__ void mw_read_column(const uint32_t *C, uint32_t tid, uint32_t (&q)[MW_K / 2]) {
+#pragma unroll
+    for (int k = 0; k < MW_K / 2; k++) q[k] = C[(2 * k) * NT + tid] | (C[(2 * k + 1) * NT + tid] << 16);
+}
+// inclusive scan of packed counters over the lanes of a warp
+__device__ __forceinline__ void mw_warp_scan(uint32_t (&q)[MW_K / 2], uint32_t lane) {
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+#pragma unroll
+        for (int k = 0; k < MW_K / 2; k++) {
+            const uint32_t o = __shfl_up_sync(0xffffffffu, q[k], d);
+            if (lane >= (uint32_t)d) q[k] += o;
+        }
+    }
 }
 
 // loader warp shared by the count and the scatter kernel: claims tiles in order,
@@ -294,10 +320,15 @@ __device__ __forceinline__ uint32_t mw_match(uint32_t v0, uint32_t v1, uint32_t 
 }
 
 // ---- k_mw_count ---------------------------------------------------------------
+// Per tile: every thread counts its keys' buckets in its column of the counter
+// matrix (one LDS + STS per key), then the 16 threads of each bucket's row
+// chunk reduce it and one of them adds the tile's count to the segment's
+// histogram.
 template <class KT, int NT, int IPT, int STAGES, int MINB>
 __global__ void __launch_bounds__(NT + 32, MINB) k_mw_count(MwParams<KT> P) {
     using SM = MwSmem<KT, NT, IPT, STAGES>;
     constexpr uint32_t NW = SM::NW;
+    static_assert(NT == MW_K * MW_K, "one 16-thread chunk per bucket row");
     extern __shared__ __align__(128) unsigned char smraw[];
     SM &sm = *reinterpret_cast<SM *>(smraw);
     const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -315,33 +346,44 @@ __global__ void __launch_bounds__(NT + 32, MINB) k_mw_count(MwParams<KT> P) {
         if (lane == 0) mw_loader<KT, NT, IPT, STAGES>(P, sm, ntiles, false);
         return;
     }
-    // lane L < 16 counts bucket L for this warp's keys of the current segment
-    uint32_t run = 0, cur_seg = 0xffffffffu;
+    // lane L < 16 accumulates this warp's count of bucket L for segment cur_seg
+    uint32_t acc = 0, cur_seg = 0xffffffffu;
+    uint32_t *C = sm.cnt_m[0];   // (columns are private: one matrix suffices)
     for (uint32_t i = 0;; i++) {
         const uint32_t s = i % STAGES;
         mbar_wait(&sm.full[s], (i / STAGES) & 1);
         const uint32_t t = sm.tile[s];
         if (t >= ntiles) break;
         const uint32_t si = sm.sidx[s];
+#pragma unroll
+        for (uint32_t b = 0; b < MW_K; b++) C[b * NT + tid] = 0;
         typename KT::T x[IPT];
         uint32_t bk[IPT];
         const uint32_t valid = mw_load_classify<KT, NT, IPT, STAGES>(P, sm, s, t, lane, tid, x, bk);
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.empty[s]);
-        if (si != cur_seg) {
-            if (cur_seg != 0xffffffffu && lane < MW_K && run) atomicAdd(&P.hist[lane * P.hstride + cur_seg], run);
-            run = 0;
-            cur_seg = si;
-        }
 #pragma unroll
         for (uint32_t c = 0; c < IPT; c++) {
-            const uint32_t v0 = __ballot_sync(0xffffffffu, bk[c] & 1), v1 = __ballot_sync(0xffffffffu, bk[c] & 2);
-            const uint32_t v2 = __ballot_sync(0xffffffffu, bk[c] & 4), v3 = __ballot_sync(0xffffffffu, bk[c] & 8);
-            const uint32_t vm = __ballot_sync(0xffffffffu, (valid >> c) & 1);
-            run += __popc(mw_match(v0, v1, v2, v3, vm, lane));
+            uint32_t *cp = &C[bk[c] * NT + tid];
+            if ((valid >> c) & 1) *cp = *cp + 1;
         }
+        uint32_t q[MW_K / 2];
+        mw_read_column<NT>(C, tid, q);
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1)
+#pragma unroll
+            for (int k = 0; k < MW_K / 2; k++) q[k] += __shfl_xor_sync(0xffffffffu, q[k], d);
+        if (si != cur_seg) {
+            if (cur_seg != 0xffffffffu && lane < MW_K && acc) atomicAdd(&P.hist[lane * P.hstride + cur_seg], acc);
+            acc = 0;
+            cur_seg = si;
+        }
+        uint32_t mine = 0;
+#pragma unroll
+        for (int k = 0; k < MW_K / 2; k++) mine = (lane >> 1) == (uint32_t)k ? q[k] : mine;
+        acc += (lane & 1) ? (mine >> 16) : (mine & 0xffff);
     }
-    if (cur_seg != 0xffffffffu && lane < MW_K && run) atomicAdd(&P.hist[lane * P.hstride + cur_seg], run);
+    if (cur_seg != 0xffffffffu && lane < MW_K && acc) atomicAdd(&P.hist[lane * P.hstride + cur_seg], acc);
 }
 
 // ---- k_mw_scan: bucket starts and cursor reset, one warp per segment ---------------
@@ -373,7 +415,7 @@ __global__ void __launch_bounds__(NT + 32, MINB) k_mw_scatter(MwParams<KT> P) {
     using SM = MwSmem<KT, NT, IPT, STAGES>;
     constexpr uint32_t NW = SM::NW;
     constexpr uint32_t W = sizeof(T), VW = 16 / W;
-    static_assert(IPT <= 16, "packed ranks");
+    static_assert(IPT <= 16 && NT == MW_K * MW_K, "packed ranks, one 16-thread chunk per bucket row");
     extern __shared__ __align__(128) unsigned char smraw[];
     SM &sm = *reinterpret_cast<SM *>(smraw);
     const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -392,12 +434,12 @@ __global__ void __launch_bounds__(NT + 32, MINB) k_mw_scatter(MwParams<KT> P) {
         return;
     }
 
-    // previous tile, carried one iteration: keys, and (tile-local offset | bucket << 16 | invalid << 31)
+    // previous tile, carried one iteration: keys and (tile offset | bucket << 16 | invalid << 31)
     T y[IPT];
     uint32_t ypk[IPT];
     bool have_prev = false;
     T *p_dst = nullptr;
-    // warp 0, lane L < 16: the previous tile's bucket-L run: atomic result, length, segment begin/start
+    // warp 0, lane L < 16: the previous tile's bucket-L run (atomic result, length, tile offset, base)
     uint32_t p_old = 0, p_cnt = 0, p_off = 0;
     uint64_t p_base = 0;
 
@@ -406,31 +448,38 @@ __global__ void __launch_bounds__(NT + 32, MINB) k_mw_scatter(MwParams<KT> P) {
         mbar_wait(&sm.full[s], (i / STAGES) & 1);
         const uint32_t t = sm.tile[s];
         const bool cur = t < ntiles;
+        uint32_t *C = sm.cnt_m[0];   // thread tid only ever touches its own column
         T x[IPT];
         uint32_t pk[IPT];
+        uint32_t q[MW_K / 2], own[MW_K / 2];
         uint32_t si = 0, sbeg = 0, spar = 0, bstart = 0;
         if (cur) {
             si = sm.sidx[s];
             sbeg = sm.sb[s];
             spar = sm.spar[s];
             bstart = lane < MW_K ? sm.start[s][lane] : 0;
-            // pk[c] holds the bucket first, then the packed rank
+#pragma unroll
+            for (uint32_t b = 0; b < MW_K; b++) C[b * NT + tid] = 0;
             const uint32_t valid = mw_load_classify<KT, NT, IPT, STAGES>(P, sm, s, t, lane, tid, x, pk);
-            // ranks inside the warp: slot-major, then lane (the k-bucket offset buffers)
-            uint32_t run = 0;   // lane L < 16: this warp's keys in bucket L so far
-            const uint32_t lt = lanemask_lt();
+            // the k-bucket offset buffers: rank of each key among this thread's
+            // keys of its bucket (counter in the thread's matrix column)
 #pragma unroll
             for (uint32_t c = 0; c < IPT; c++) {
                 const uint32_t b = pk[c];
-                const uint32_t v0 = __ballot_sync(0xffffffffu, b & 1), v1 = __ballot_sync(0xffffffffu, b & 2);
-                const uint32_t v2 = __ballot_sync(0xffffffffu, b & 4), v3 = __ballot_sync(0xffffffffu, b & 8);
-                const uint32_t vm = __ballot_sync(0xffffffffu, (valid >> c) & 1);
-                const uint32_t before = __shfl_sync(0xffffffffu, run, b);
-                const uint32_t mine = mw_match(v0, v1, v2, v3, vm, b);
-                pk[c] = (before + __popc(mine & lt)) | (b << 16) | ((((valid >> c) & 1) ^ 1) << 31);
-                run += __popc(mw_match(v0, v1, v2, v3, vm, lane));
+                uint32_t *cp = &C[b * NT + tid];
+                const bool v = (valid >> c) & 1;
+                const uint32_t r = *cp;
+                if (v) *cp = r + 1;
+                pk[c] = r | (b << 16) | ((uint32_t)!v << 31);
             }
-            if (lane < MW_K) sm.whist[par][warp][lane] = run;
+            // per-bucket scan over the threads: warp part (packed 16-bit counters)
+            mw_read_column<NT>(C, tid, q);
+#pragma unroll
+            for (int k = 0; k < MW_K / 2; k++) own[k] = q[k];
+            mw_warp_scan(q, lane);
+            if (lane == 31)
+#pragma unroll
+                for (int k = 0; k < MW_K / 2; k++) sm.wtot[par][warp][k] = q[k];
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.empty[s]);
@@ -456,42 +505,31 @@ __global__ void __launch_bounds__(NT + 32, MINB) k_mw_scatter(MwParams<KT> P) {
             }
         }
         if (tid < MW_K) bulk_wait_read0();   // the previous bulk stores (one group per run) have read `out`
-        named_bar_sync(1, NT);               // B1
+        named_bar_sync(1, NT);               // B1: warp totals and placement visible, `out` free
 
-        if (cur) {
-            // this warp's run offsets inside the tile: lane L < 16 -> bucket L
-            uint32_t pre = 0, tot = 0;
-            if (lane < MW_K) {
+        if (cur && warp == 0) {
+            // cross-warp part: lane k < 8 runs over the warps for packed pair k
+            if (lane < MW_K / 2) {
+                uint32_t run = 0;
 #pragma unroll
                 for (uint32_t w2 = 0; w2 < NW; w2++) {
-                    const uint32_t v = sm.whist[par][w2][lane];
-                    pre += w2 < warp ? v : 0;
-                    tot += v;
+                    sm.wpre[par][w2][lane] = run;
+                    run += sm.wtot[par][w2][lane];
                 }
-            }
-            uint32_t toff = tot;
+                // bucket totals -> bucket starts inside the tile (scan over the 16 fields)
+                const uint32_t lo = run & 0xffff, hi = run >> 16;
+                uint32_t pair = lo + hi, incp = pair;
 #pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const uint32_t o = __shfl_up_sync(0xffffffffu, toff, d);
-                if (lane >= (uint32_t)d) toff += o;
-            }
-            toff -= tot;   // exclusive over buckets
-            const uint32_t wbase = toff + pre;
-#pragma unroll
-            for (uint32_t c = 0; c < IPT; c++) {
-                const uint32_t b = (pk[c] >> 16) & 0x7fff;
-                pk[c] += __shfl_sync(0xffffffffu, wbase, b);
-            }
-            if (warp == 0) {
-                // claim the tile's runs: one atomic per bucket, consumed next iteration
-                const uint32_t old = (lane < MW_K && tot) ? atomicAdd(&P.cursor[lane * P.hstride + si], tot) : 0;
-                p_old = old;   // (register dependency resolved only next iteration)
-                p_cnt = lane < MW_K ? tot : 0;
-                p_off = toff;
-                p_base = (uint64_t)sbeg + bstart;
+                for (int d = 1; d < 8; d <<= 1) {
+                    const uint32_t o = __shfl_up_sync(0x000000ffu, incp, d);
+                    if (lane >= (uint32_t)d) incp += o;
+                }
+                const uint32_t ex = incp - pair;
+                sm.boff[par][2 * lane] = ex;
+                sm.boff[par][2 * lane + 1] = ex + lo;
+                if (lane == MW_K / 2 - 1) sm.boff[par][MW_K] = incp;
             }
         }
-
         if (have_prev) {
             // stage the previous tile's runs aligned like their destinations
 #pragma unroll
@@ -500,38 +538,62 @@ __global__ void __launch_bounds__(NT + 32, MINB) k_mw_scatter(MwParams<KT> P) {
                 if (!(v >> 31)) sm.out[(v & 0xffff) + sm.delta[par ^ 1][(v >> 16) & 0x7fff]] = y[c];
             }
             if (P.aligned) fence_proxy_async_smem();
-            named_bar_sync(1, NT);   // B2
+        }
+        named_bar_sync(1, NT);   // B2: prefixes visible, staging complete
+
+        if (have_prev) {
             T *d = p_dst;
             if (!P.aligned) {
-                // unaligned buffers: plain stores, run by run
                 for (uint32_t L = 0; L < MW_K; L++) {
                     const uint32_t n = sm.cnt[par ^ 1][L];
                     const uint64_t g = (uint64_t)sm.gstart[par ^ 1][L];
-                    for (uint32_t q = tid; q < n; q += NT) d[g + q] = sm.out[sm.sh[par ^ 1][L] + q];
+                    for (uint32_t qq = tid; qq < n; qq += NT) d[g + qq] = sm.out[sm.sh[par ^ 1][L] + qq];
                 }
-            } else {
-                if (tid < MW_K) {
-                    const uint32_t L = tid, n = sm.cnt[par ^ 1][L];
-                    const uint64_t g = sm.gstart[par ^ 1][L], ge = g + n;
-                    const uint64_t bs = (g + VW - 1) / VW * VW, be = ge / VW * VW;
-                    if (n && be > bs)
-                        tma_store_1d(d + bs, &sm.out[sm.sh[par ^ 1][L] + (bs - g)], (uint32_t)((be - bs) * W));
-                    bulk_commit();
-                } else if (tid >= 32 && tid < 32 + MW_K * 2 * VW) {
-                    // heads and tails (< 16 bytes) of every run
-                    const uint32_t u = tid - 32, L = u / (2 * VW), q = u % (2 * VW);
-                    const uint32_t n = sm.cnt[par ^ 1][L];
-                    const uint64_t g = sm.gstart[par ^ 1][L], ge = g + n;
-                    const uint64_t bs = (g + VW - 1) / VW * VW, be = ge / VW * VW;
-                    const bool tail = q >= VW;
-                    const uint32_t qq = tail ? q - VW : q;
-                    const uint64_t pos = tail ? (be > bs ? be : bs) + qq : g + qq;
-                    const bool ok = n && (tail ? (ge > bs && pos < ge) : (pos < (bs < ge ? bs : ge)));
-                    if (ok) d[pos] = sm.out[sm.sh[par ^ 1][L] + (pos - g)];
-                }
+            } else if (tid < MW_K) {
+                const uint32_t L = tid, n = sm.cnt[par ^ 1][L];
+                const uint64_t g = sm.gstart[par ^ 1][L], ge = g + n;
+                const uint64_t bs = (g + VW - 1) / VW * VW, be = ge / VW * VW;
+                if (n && be > bs) tma_store_1d(d + bs, &sm.out[sm.sh[par ^ 1][L] + (bs - g)], (uint32_t)((be - bs) * W));
+                bulk_commit();
+            } else if (tid >= 32 && tid < 32 + MW_K * 2 * VW) {
+                // heads and tails (< 16 bytes) of every run
+                const uint32_t u = tid - 32, L = u / (2 * VW), qv = u % (2 * VW);
+                const uint32_t n = sm.cnt[par ^ 1][L];
+                const uint64_t g = sm.gstart[par ^ 1][L], ge = g + n;
+                const uint64_t bs = (g + VW - 1) / VW * VW, be = ge / VW * VW;
+                const bool tail = qv >= VW;
+                const uint32_t qq = tail ? qv - VW : qv;
+                const uint64_t pos = tail ? (be > bs ? be : bs) + qq : g + qq;
+                const bool ok = n && (tail ? (ge > bs && pos < ge) : (pos < (bs < ge ? bs : ge)));
+                if (ok) d[pos] = sm.out[sm.sh[par ^ 1][L] + (pos - g)];
             }
         }
         if (!cur) break;
+
+        // every key's offset in the tile: bucket start + the preceding warps' and
+        // lanes' keys of its bucket + its rank in this thread
+        {
+#pragma unroll
+            for (int k = 0; k < MW_K / 2; k++) {
+                const uint32_t ex = q[k] - own[k] + sm.wpre[par][warp][k];   // exclusive, packed
+                C[(2 * k) * NT + tid] = (ex & 0xffff) + sm.boff[par][2 * k];
+                C[(2 * k + 1) * NT + tid] = (ex >> 16) + sm.boff[par][2 * k + 1];
+            }
+#pragma unroll
+            for (uint32_t c = 0; c < IPT; c++) {
+                const uint32_t b = (pk[c] >> 16) & 0x7fff;
+                pk[c] += C[b * NT + tid];
+            }
+        }
+        if (warp == 0) {
+            // claim this tile's runs: one atomic per bucket, consumed next iteration
+            const uint32_t st = lane < MW_K ? sm.boff[par][lane] : 0;
+            const uint32_t tot = lane < MW_K ? sm.boff[par][lane + 1] - st : 0;
+            p_old = (lane < MW_K && tot) ? atomicAdd(&P.cursor[lane * P.hstride + si], tot) : 0;
+            p_cnt = tot;
+            p_off = st;
+            p_base = (uint64_t)sbeg + bstart;
+        }
 #pragma unroll
         for (uint32_t c = 0; c < IPT; c++) {
             y[c] = x[c];

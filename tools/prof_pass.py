@@ -16,6 +16,8 @@ ap.add_argument("--n", type=int, default=1 << 28)
 ap.add_argument("--passes", type=int, default=4)
 ap.add_argument("--sort", type=int, default=0)
 ap.add_argument("--kind", default="i32")
+ap.add_argument("--fast", type=int, default=0, help="1: atomic-cursor (sort) placement")
+ap.add_argument("--ways", type=int, default=0)
 a = ap.parse_args()
 if a.kind == "i32":
     src = torch.from_numpy(bqgen.i32_full(a.n, 1)).cuda()
@@ -28,9 +30,9 @@ ws = bq.workspace(bq.kind_of(src), a.n)
 counts = torch.zeros(3, dtype=torch.int64, device="cuda")
 pv = bq.pivot(src, bq.BQ_PIVOT_MO3, ws=ws)
 for _ in range(a.passes):
-    bq.bq_partition_pass(src, dst, pv, counts, ws=ws)
+    bq.bq_partition_pass(src, dst, pv, counts, ordered=not a.fast, ws=ws)
 for _ in range(a.sort):
     dst.copy_(src)
-    st = bq.bq_sort_ex(dst, ws=ws)
+    st = bq.bq_sort_ex(dst, ws=ws, ways=a.ways)
 torch.cuda.synchronize()
 print("counts", counts.tolist(), "ok")
