@@ -95,8 +95,11 @@ template <> struct Tune<KU64> {
     static constexpr int LEAF = 4096, LEAF_THREADS = 512;
 };
 template <> struct Tune<KF64> : Tune<KU64> {};
+#ifndef BQ_REC_STAGES
+#define BQ_REC_STAGES 4
+#endif
 template <> struct Tune<KRec> {
-    static constexpr int PART_THREADS = 256, PART_IPT = 2, PART_STAGES = 4, PART_MINB = 2;   // 16 KB tiles
+    static constexpr int PART_THREADS = 256, PART_IPT = 2, PART_STAGES = BQ_REC_STAGES, PART_MINB = 2;   // 16 KB tiles
     static constexpr int LEAF = 2048, LEAF_THREADS = 512;
 };
 
@@ -348,12 +351,46 @@ __device__ typename KT::K sample64_pivot_warp(const typename KT::T *buf, uint32_
     }
     return __shfl_sync(0xffffffffu, v[0], 31);
 }
+// the same, plus whether the 31st or 33rd smallest sample key equals the pivot
+template <class KT>
+__device__ typename KT::K sample64_pivot_warp_dup(const typename KT::T *buf, uint32_t b, uint32_t len,
+                                                  uint32_t lane, bool *dup) {
+    using K = typename KT::K;
+    K v[2];
+#pragma unroll
+    for (int r = 0; r < 2; r++) v[r] = load_key<KT>(buf, sample64_pos(b, len, lane + 32 * r));
+#pragma unroll
+    for (int m = 1; m <= 6; m++) {
+#pragma unroll
+        for (int bb = m - 1; bb >= 0; bb--) {
+            if (bb == 5) {
+                const K lo = v[1] < v[0] ? v[1] : v[0], hi = v[1] < v[0] ? v[0] : v[1];
+                v[0] = lo;
+                v[1] = hi;
+                continue;
+            }
+#pragma unroll
+            for (int r = 0; r < 2; r++) {
+                const uint32_t i = lane + 32 * r;
+                const K p = __shfl_xor_sync(0xffffffffu, v[r], 1 << bb);
+                const bool lower = ((lane >> bb) & 1) == 0;
+                const bool asc = m == 6 || ((i >> m) & 1) == 0;
+                v[r] = (lower == asc) ? (p < v[r] ? p : v[r]) : (v[r] < p ? p : v[r]);
+            }
+        }
+    }
+    const K piv = __shfl_sync(0xffffffffu, v[0], 31);
+    const K below = __shfl_sync(0xffffffffu, v[0], 30), above = __shfl_sync(0xffffffffu, v[1], 0);
+    *dup = !(below < piv) || !(piv < above);
+    return piv;
+}
 
 // Pivot of buf[b, b+len) by `rule`, computed by a whole warp (all 32 lanes
-// must call it; every lane gets the result).
+// must call it; every lane gets the result).  *dup (if non-null) tells whether
+// another key of the rule's sample equals the pivot.
 template <class KT>
 __device__ typename KT::K select_pivot_warp(const typename KT::T *buf, uint32_t b, uint32_t len, int rule,
-                                            uint32_t lane);
+                                            uint32_t lane, bool *dup = nullptr);
 
 // Mo3 over {b, b+len/2, e-1}; ninther over b + floor(k*(len-1)/8), k=0..8.
 template <class KT>
@@ -377,11 +414,27 @@ __device__ typename KT::K select_pivot(const typename KT::T *buf, uint32_t b, ui
 
 template <class KT>
 __device__ typename KT::K select_pivot_warp(const typename KT::T *buf, uint32_t b, uint32_t len, int rule,
-                                            uint32_t lane) {
+                                            uint32_t lane, bool *dup) {
     using K = typename KT::K;
-    if (rule == BQ_PIVOT_SAMPLE64) return sample64_pivot_warp<KT>(buf, b, len, lane);
+    if (rule == BQ_PIVOT_SAMPLE64) {
+        if (dup) return sample64_pivot_warp_dup<KT>(buf, b, len, lane, dup);
+        return sample64_pivot_warp<KT>(buf, b, len, lane);
+    }
     K p = 0;
-    if (lane == 0) p = select_pivot<KT>(buf, b, len, rule);
+    uint32_t eq = 0;
+    if (lane == 0) {
+        p = select_pivot<KT>(buf, b, len, rule);
+        if (dup) {
+            // how many keys of the rule's sample equal the pivot
+            if (rule == BQ_PIVOT_NINTHER && len >= 9) {
+                for (int k = 0; k < 9; k++) eq += load_key<KT>(buf, (uint64_t)b + ((uint64_t)k * (len - 1)) / 8) == p;
+            } else {
+                eq = (load_key<KT>(buf, b) == p) + (load_key<KT>(buf, (uint64_t)b + len / 2) == p) +
+                     (load_key<KT>(buf, (uint64_t)b + len - 1) == p);
+            }
+        }
+    }
+    if (dup) *dup = __shfl_sync(0xffffffffu, eq, 0) >= 2;
     return __shfl_sync(0xffffffffu, p, 0);
 }
 

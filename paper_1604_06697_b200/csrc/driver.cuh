@@ -53,6 +53,7 @@ template <class KT>
 struct Layout {
     size_t scratch, status, tile_map[2], segs[2], cursor[2], ecursor[2], leaves[2], fallback, ctrl, misc, total;
     size_t msegs[2], mtile_map[2], mhist[2], mcursor[2];   // multiway segment lists (N4)
+    size_t copies[2], max_copies;                           // records: finished equal runs to copy
     size_t max_tiles, max_segs, max_leaves, max_fb;
 };
 
@@ -86,6 +87,9 @@ Layout<KT> make_layout(size_t n) {
     L.leaves[0] = take(leaf_nclass<KT>() * L.max_leaves * sizeof(Leaf));
     L.leaves[1] = take(leaf_nclass<KT>() * L.max_leaves * sizeof(Leaf));
     L.fallback = take(L.max_fb * sizeof(Leaf));
+    L.max_copies = KT::is_record ? LEVEL_BATCH * (L.max_segs + 2) + n / 65536 + 2 : 1;
+    L.copies[0] = take(L.max_copies * sizeof(Leaf));
+    L.copies[1] = take(L.max_copies * sizeof(Leaf));
     L.ctrl = take((MAX_LEVELS + 1) * sizeof(LevelCtrl));   // [MAX_LEVELS]: the root's counts
     L.misc = take(256);   // fallback count, leaf-list counts (2 sets x 4 classes), pass counts
     L.total = off;
@@ -185,11 +189,13 @@ bq_status launch_multiway(MwParams<KT> MP, LevelCtrl *lc, cudaStream_t s) {
     return BQ_OK;
 }
 
+// ordered: decoupled look-back (deterministic layout; the staging of equal
+// records needs it); otherwise the atomic-cursor kernel (keys three-way,
+// records two-way)
 template <class KT>
 bq_status launch_partition(const PassParams<KT> &P, cudaStream_t s) {
-    if (P.ordered || KT::is_record) return launch_partition_t<KT, true>(P, s);
-    if constexpr (!KT::is_record) return launch_partition_fast<KT>(P, s);
-    return launch_partition_t<KT, false>(P, s);
+    if (P.ordered) return launch_partition_t<KT, true>(P, s);
+    return launch_partition_fast<KT>(P, s);
 }
 
 template <class KT>
@@ -286,7 +292,7 @@ bq_status run_pass(const typename KT::T *src, typename KT::T *dst, typename KT::
     P.ntiles = ntiles;
     P.n_total = n;
     P.aligned = aligned16(src) && aligned16(dst);
-    P.ordered = ordered;
+    P.ordered = ordered || KT::is_record;   // the partition API is three-way for records too
     bq_status st = launch_partition<KT>(P, s);
     if (st != BQ_OK) return st;
     return launch_pass_post<KT>(P, 1, d_counts, s);
@@ -412,7 +418,7 @@ bq_status run_partition_segments(const typename KT::T *src, typename KT::T *dst,
     P.ntiles = (uint32_t)tiles;
     P.n_total = n;
     P.aligned = aligned16(src) && aligned16(dst);
-    P.ordered = ordered;
+    P.ordered = ordered || KT::is_record;
     st = launch_partition<KT>(P, s);
     if (st != BQ_OK) return st;
     st = launch_pass_post<KT>(P, (uint32_t)nseg, d_counts, s);
@@ -513,14 +519,16 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
         mhist[p] = reinterpret_cast<uint32_t *>(w + L.mhist[p]);
         mcursor[p] = reinterpret_cast<uint32_t *>(w + L.mcursor[p]);
     }
-    // look-back words are only used by the ordered placement (records always)
-    uint64_t *lb_status = (ordered || KT::is_record) ? status : nullptr;
+    // look-back words are only used by the ordered placement
+    uint64_t *lb_status = ordered ? status : nullptr;
     Leaf *leaves[2] = {reinterpret_cast<Leaf *>(w + L.leaves[0]), reinterpret_cast<Leaf *>(w + L.leaves[1])};
     Leaf *fallback = reinterpret_cast<Leaf *>(w + L.fallback);
     LevelCtrl *ctrl = reinterpret_cast<LevelCtrl *>(w + L.ctrl);
     LevelCtrl *root = ctrl + MAX_LEVELS;
     uint32_t *fb_count = reinterpret_cast<uint32_t *>(w + L.misc);
     uint32_t *leaf_counts[2] = {fb_count + 4, fb_count + 8};   // [set][class]
+    uint32_t *copy_counts[2] = {fb_count + 12, fb_count + 13};
+    Leaf *copies[2] = {reinterpret_cast<Leaf *>(w + L.copies[0]), reinterpret_cast<Leaf *>(w + L.copies[1])};
 
     LeafParams<KT> LP{};
     LP.bufs[0] = user;
@@ -569,7 +577,7 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
     }
 
     BQ_CKC(cudaMemsetAsync(ctrl, 0, (MAX_LEVELS + 1) * sizeof(LevelCtrl), s));
-    BQ_CKC(cudaMemsetAsync(fb_count, 0, 12 * sizeof(uint32_t), s));
+    BQ_CKC(cudaMemsetAsync(fb_count, 0, 14 * sizeof(uint32_t), s));
     const int aligned = aligned16(user) && aligned16(scratch);
     // children sink of level `lv` (its children form level lv+1; the root is
     // the only "child" of the virtual level -1, counted in `root`)
@@ -578,6 +586,9 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
         const int np = (lv + 1) & 1;
         Q.pass.bufs[0] = user;
         Q.pass.bufs[1] = scratch;
+        Q.pass.ordered = ordered;
+        Q.copies = copies[set];
+        Q.copy_count = copy_counts[set];
         Q.next_segs = segs[np];
         Q.next_tile_map = tile_map[np];
         Q.next_cursor = cursor[np];
@@ -619,6 +630,7 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
         // the side stream has finished the leaves of batch-2 (same set)
         if (batch >= 2) BQ_CKC(cudaStreamWaitEvent(s, ev_leaves[set], 0));
         BQ_CKC(cudaMemsetAsync(leaf_counts[set], 0, 4 * sizeof(uint32_t), s));
+        BQ_CKC(cudaMemsetAsync(copy_counts[set], 0, sizeof(uint32_t), s));
         for (int k = 0; k < LEVEL_BATCH; k++, level++) {
             const int cp = level & 1;
             const LevelCtrl *prev = level == 0 ? root : ctrl + level - 1;
@@ -700,6 +712,12 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
             LP.count_dev = leaf_counts[set] + c;
             st = launch_leaves<KT>(c, LP, 0, ls);
             if (st != BQ_OK) { cleanup(); return st; }
+            local.kernel_launches++;
+        }
+        if (KT::is_record && !ordered) {
+            k_copy_runs<KT, POST_THREADS><<<POST_GRID, POST_THREADS, 0, ls>>>(copies[set], copy_counts[set], user,
+                                                                               scratch);
+            BQ_CKC(cudaGetLastError());
             local.kernel_launches++;
         }
         BQ_CKC(cudaEventRecord(ev_leaves[set], ls));

@@ -101,6 +101,10 @@ struct PostParams {
     uint32_t *next_mtile_map;
     uint32_t *next_mhist;   // [bucket * mhstride + segment], zeroed for new segments
     uint32_t mhstride;
+    // records, two-way placement: finished runs of equal keys still in the
+    // scratch buffer, copied to the user buffer by k_copy_runs
+    Leaf *copies;
+    uint32_t *copy_count;
 };
 
 template <class KT>
@@ -131,15 +135,18 @@ __device__ __forceinline__ SegCounts<KT> seg_counts(const PassParams<KT> &P, uin
 // binary with the pivot of `pivot_rule` (the sample's median when multiway
 // was tried).  Warps select pivots/splitters, one thread per child appends
 // it, then the CTA writes the children's slices of the next tile maps.
+// hint[c] (optional): 0 = choose a pivot; 1 = follow-up pass [<= p | > p]
+// with p = hint_pivot; 2 = a finished run of equal keys (records)
 template <class KT, int NT>
 __device__ __forceinline__ void emit_children(const PostParams<KT> &Q, int nch, const uint32_t *cb,
-                                              const uint32_t *cl, uint8_t cp, uint16_t cd) {
+                                              const uint32_t *cl, uint8_t cp, uint16_t cd,
+                                              const uint8_t *hint = nullptr, uint64_t hint_pivot = 0) {
     using T = typename KT::T;
     using K = typename KT::K;
     constexpr uint32_t TILE = (uint32_t)tile_elems<KT>();
     constexpr int NW = NT / 32;
-    enum { C_NONE = 0, C_LEAF, C_FALLBACK, C_BIN, C_MW };
-    __shared__ uint32_t s_kind[MW_K], s_idx[MW_K], s_tb[MW_K], s_nt[MW_K];
+    enum { C_NONE = 0, C_LEAF, C_FALLBACK, C_BIN, C_MW, C_BAND };
+    __shared__ uint32_t s_kind[MW_K], s_idx[MW_K], s_tb[MW_K], s_nt[MW_K], s_mode[MW_K];
     __shared__ uint64_t s_piv[MW_K];
     __shared__ K s_tree[MW_K][MW_K];
     LevelCtrl *C = Q.child_ctrl;
@@ -148,11 +155,24 @@ __device__ __forceinline__ void emit_children(const PostParams<KT> &Q, int nch, 
     __syncthreads();   // the previous segment's readers of s_* are done
     for (int c = warp; c < nch; c += NW) {
         const uint32_t len = cl[c];
-        uint32_t kind = C_NONE;
+        const uint8_t h = hint ? hint[c] : 0;
+        uint32_t kind = C_NONE, mode = 0;
         if (len == 0) kind = C_NONE;
+        else if (h == 2) kind = C_BAND;
         else if (len <= Q.leaf_max) kind = C_LEAF;
         else if ((int)cd >= Q.depth_limit) kind = C_FALLBACK;
-        else if (Q.ways > 2 && !KT::is_record) {
+        else if (h == 1) {
+            kind = C_BIN;
+            mode = 1;
+            if (lane == 0) s_piv[c] = hint_pivot;
+        } else if (KT::is_record && !Q.pass.ordered) {
+            // two-way records: a pivot repeated in its sample gets a follow-up pass
+            bool dup = false;
+            const K piv = select_pivot_warp<KT>(cbuf, cb[c], len, Q.pivot_rule, lane, &dup);
+            if (lane == 0) s_piv[c] = (uint64_t)piv;
+            kind = C_BIN;
+            mode = dup ? 2 : 0;
+        } else if (Q.ways > 2 && !KT::is_record) {
             K node, piv;
             const bool ok = mw_splitters<KT>(cbuf, cb[c], len, Q.leaf_max, lane, node, piv);
             kind = ok ? C_MW : C_BIN;
@@ -163,7 +183,10 @@ __device__ __forceinline__ void emit_children(const PostParams<KT> &Q, int nch, 
             if (lane == 0) s_piv[c] = (uint64_t)piv;
             kind = C_BIN;
         }
-        if (lane == 0) s_kind[c] = kind;
+        if (lane == 0) {
+            s_kind[c] = kind;
+            s_mode[c] = mode;
+        }
     }
     __syncthreads();
     if ((int)threadIdx.x < nch) {
@@ -181,6 +204,13 @@ __device__ __forceinline__ void emit_children(const PostParams<KT> &Q, int nch, 
             const uint32_t fi = atomicAdd(Q.fallback_count, 1u);
             atomicAdd(&C->nfallback, 1u);
             Q.fallback[fi] = Leaf{cb[c], len, cp, 0};
+        } else if (kind == C_BAND) {
+            atomicAdd(&C->band_elems, (unsigned long long)len);
+            if (cp != 0)   // in the scratch buffer: copy to the user buffer in chunks
+                for (uint32_t off = 0; off < len; off += 65536) {
+                    const uint32_t ci = atomicAdd(Q.copy_count, 1u);
+                    Q.copies[ci] = Leaf{cb[c] + off, (len - off) < 65536u ? (len - off) : 65536u, cp, 0};
+                }
         } else if (kind == C_BIN || kind == C_MW) {
             Seg ch;
             ch.pivot = s_piv[c];
@@ -189,7 +219,7 @@ __device__ __forceinline__ void emit_children(const PostParams<KT> &Q, int nch, 
             ch.ntiles = seg_ntiles(cb[c], len, TILE);
             ch.depth = cd;
             ch.parity = cp;
-            ch.pad0 = 0;
+            ch.pad0 = (uint8_t)s_mode[c];   // records: bit 0 = [<= p | > p] pass, bit 1 = pivot duplicated
             ch.pad1 = 0;
             uint32_t ci;
             if (kind == C_BIN) {
@@ -287,6 +317,16 @@ __device__ __forceinline__ void post_segment(const PostParams<KT> &Q, uint32_t s
         atomicAdd(&C->element_passes, (unsigned long long)sg.len);
         atomicAdd(&C->band_elems, (unsigned long long)E);
     }
+    if (KT::is_record && !P.ordered) {
+        // two-way records (E == 0): [< p | >= p], the right side followed up by
+        // [<= p | > p] when p was duplicated in its sample; the left side of a
+        // follow-up pass is a finished run of keys equal to p
+        const uint32_t cb[2] = {sg.begin, sg.begin + L};
+        const uint32_t cl[2] = {L, G};
+        const uint8_t h[2] = {(uint8_t)((sg.pad0 & 1) ? 2 : 0), (uint8_t)((sg.pad0 & 1) ? 0 : ((sg.pad0 & 2) ? 1 : 0))};
+        emit_children<KT, NT>(Q, 2, cb, cl, (uint8_t)(sg.parity ^ 1), (uint16_t)(sg.depth + 1), h, sg.pivot);
+        return;
+    }
     const uint32_t cb[2] = {sg.begin, sg.begin + L + E};
     const uint32_t cl[2] = {L, G};
     emit_children<KT, NT>(Q, 2, cb, cl, (uint8_t)(sg.parity ^ 1), (uint16_t)(sg.depth + 1));
@@ -369,6 +409,18 @@ __global__ void __launch_bounds__(NT) k_post_mw(PostParams<KT> Q) {
             cl[threadIdx.x] = Q.mw.hist[threadIdx.x * Q.mw.hstride + si];
         }
         emit_children<KT, NT>(Q, MW_K, cb, cl, (uint8_t)(m.s.parity ^ 1), (uint16_t)(m.s.depth + 1));
+    }
+}
+
+// Finished runs of equal record keys still in the scratch buffer -> user
+// buffer (persistent grid over the copy list of one batch).
+template <class KT, int NT>
+__global__ void __launch_bounds__(NT) k_copy_runs(const Leaf *list, const uint32_t *count, typename KT::T *user,
+                                                  const typename KT::T *scratch) {
+    const uint32_t n = *count;
+    for (uint32_t li = blockIdx.x; li < n; li += gridDim.x) {
+        const Leaf l = list[li];
+        for (uint32_t j = threadIdx.x; j < l.len; j += NT) user[(uint64_t)l.begin + j] = scratch[(uint64_t)l.begin + j];
     }
 }
 

@@ -26,6 +26,11 @@
 // Keys equal to the pivot are dropped: k_post fills the equal band.  Keys
 // outside the segment in a partial tile are replaced by the pivot on load,
 // which drops them the same way.
+// Records (32 B) are never dropped: the split is two-way by the segment's
+// mode (Seg::pad0 bit 0): [< p | >= p], or [<= p | > p] for the follow-up pass
+// of a pivot that was duplicated in its sample, whose left side is then a
+// finished run of equal keys (k_post).  Positions outside the segment in a
+// partial tile are masked.
 #pragma once
 
 namespace bq {
@@ -57,13 +62,13 @@ __global__ void __launch_bounds__(NT + 32, MINB) k_part_fast(PassParams<KT> P) {
     using T = typename KT::T;
     using K = typename KT::K;
     using SM = FastSmem<KT, NT, IPT, STAGES>;
-    static_assert(!KT::is_record, "records use the ordered kernel");
+    constexpr bool REC = KT::is_record;
     constexpr uint32_t TILE = SM::TILE;
     constexpr uint32_t NW = SM::NW;
     constexpr uint32_t W = sizeof(T);
-    constexpr uint32_t VW = 16 / W;            // keys per 16-byte vector
-    constexpr uint32_t NV4 = IPT / VW;         // vectors per thread
-    static_assert(IPT % VW == 0 && NV4 >= 1 && NV4 <= 8 && (NV4 & (NV4 - 1)) == 0, "thread span");
+    constexpr uint32_t VW = W >= 16 ? 1 : 16 / W;   // elements per 16-byte vector
+    constexpr uint32_t NV4 = IPT * W / 16;          // vectors per thread
+    static_assert(REC || (IPT % VW == 0 && NV4 >= 1 && NV4 <= 8 && (NV4 & (NV4 - 1)) == 0), "thread span");
 
     extern __shared__ __align__(128) unsigned char smraw[];
     SM &sm = *reinterpret_cast<SM *>(smraw);
@@ -126,6 +131,7 @@ __global__ void __launch_bounds__(NT + 32, MINB) k_part_fast(PassParams<KT> P) {
     uint64_t p_b = 0, p_e = 0;
     K p_pk = 0;
     T *p_dst = nullptr;
+    uint32_t p_valid = 0, p_mode = 0;   // records: valid mask, split mode
     unsigned long long my_old = 0;   // thread 0: atomic result of the previous tile
 
     for (uint32_t i = 0;; i++) {
@@ -140,11 +146,38 @@ __global__ void __launch_bounds__(NT + 32, MINB) k_part_fast(PassParams<KT> P) {
 
         // ---- a2 + a3: load and classify tile i ---------------------------------
         T x[IPT];
-        uint32_t cnt = 0;
+        uint32_t cnt = 0, valid = (1u << IPT) - 1, mode = 0;
         Seg sg;
         uint64_t b = 0, e = 0;
         K pk = 0;
-        if (cur) {
+        if constexpr (REC) if (cur) {
+            sg = sm.seg[s];
+            const TileGeom<KT, TILE> G(sg, t);
+            b = G.b;
+            e = G.e;
+            pk = (K)sg.pivot;
+            mode = sg.pad0 & 1;
+            const T *src = sg.parity ? P.bufs[1] : P.bufs[0];
+#pragma unroll
+            for (uint32_t c = 0; c < IPT; c++) {
+                const uint32_t pos = e0 + c;
+                const bool v = pos >= G.vlo && pos < G.vhi;
+                if (!manual) x[c] = sm.in[s][pos];
+                else if (v) x[c] = src[G.tbeg + pos];
+                valid = v ? valid : (valid & ~(1u << c));
+            }
+            uint32_t cl = 0, cg = 0;
+#pragma unroll
+            for (uint32_t c = 0; c < IPT; c++) {
+                const K kk = KT::key(x[c]);
+                const bool v = (valid >> c) & 1;
+                const bool lt = mode ? !(pk < kk) : (kk < pk);
+                cl += v && lt;
+                cg += v && !lt;
+            }
+            cnt = cl | (cg << 16);
+        }
+        if constexpr (!REC) if (cur) {
             sg = sm.seg[s];
             const TileGeom<KT, TILE> G(sg, t);
             b = G.b;
@@ -233,7 +266,16 @@ __global__ void __launch_bounds__(NT + 32, MINB) k_part_fast(PassParams<KT> P) {
 #pragma unroll
             for (uint32_t c = 0; c < IPT; c++) {
                 const K kk = KT::key(y[c]);
-                const bool lt = kk < p_pk, gt = p_pk < kk;
+                bool lt, gt;
+                if constexpr (REC) {
+                    const bool v = (p_valid >> c) & 1;
+                    const bool l0 = p_mode ? !(p_pk < kk) : (kk < p_pk);
+                    lt = v && l0;
+                    gt = v && !l0;
+                } else {
+                    lt = kk < p_pk;
+                    gt = p_pk < kk;
+                }
                 const uint32_t idx = lt ? rl : rg;
                 if (lt || gt) sm.out[idx] = y[c];
                 rl += lt;
@@ -283,6 +325,8 @@ __global__ void __launch_bounds__(NT + 32, MINB) k_part_fast(PassParams<KT> P) {
         p_b = b;
         p_e = e;
         p_pk = pk;
+        p_valid = valid;
+        p_mode = mode;
         p_dst = sg.parity ? P.bufs[0] : P.bufs[1];
     }
     if (tid == 0) bulk_wait0();
