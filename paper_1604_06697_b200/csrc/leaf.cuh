@@ -52,10 +52,13 @@ struct RecKI {
     uint32_t i;
 };
 
+#ifndef BQ_LEAF_R32
+#define BQ_LEAF_R32 5
+#endif
 template <class KT>
 struct LeafTraits {
     using E = typename KT::K;
-    static constexpr int R = 5;                       // log2(keys per thread)
+    static constexpr int R = sizeof(E) == 4 ? BQ_LEAF_R32 : 5;   // log2(keys per thread)
     static constexpr int OCC = sizeof(E) == 4 ? 512 : 256;   // resident threads/SM the registers target
 };
 template <>
