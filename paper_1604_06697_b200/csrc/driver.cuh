@@ -167,10 +167,29 @@ bq_status persistent_cap(F kern, int threads, int smem, int *cap) {
 
 // one multiway level (N4): count, scan, scatter (children by k_post_mw)
 template <class KT>
-bq_status launch_multiway(MwParams<KT> MP, LevelCtrl *lc, cudaStream_t s) {
+bq_status launch_multiway(MwParams<KT> MP, LevelCtrl *lc, cudaStream_t s, int ways) {
     using Kn = Kernels<KT>;
-    constexpr int smem = mw_smem_bytes<KT>();
     constexpr int threads = Kn::NT + 32;
+    if (ways == MW8) {
+        constexpr int smem8 = mw8_smem_bytes<KT>();
+        auto kc8 = k_mw8_count<KT, Kn::NT, Kn::IPT, MW_STAGES, Kn::MINB>;
+        auto ks8 = k_mw8_scatter<KT, Kn::NT, Kn::IPT, MW_STAGES, Kn::MINB>;
+        static int cap_c8 = 0, cap_s8 = 0;
+        bq_status st = persistent_cap(kc8, threads, smem8, &cap_c8);
+        if (st != BQ_OK) return st;
+        st = persistent_cap(ks8, threads, smem8, &cap_s8);
+        if (st != BQ_OK) return st;
+        MP.ticket = &lc->mw_ticket_count;
+        kc8<<<cap_c8, threads, smem8, s>>>(MP);
+        BQ_CK_LAUNCH();
+        k_mw_scan<KT><<<POST_GRID / 8, 256, 0, s>>>(MP);
+        BQ_CK_LAUNCH();
+        MP.ticket = &lc->mw_ticket_scatter;
+        ks8<<<cap_s8, threads, smem8, s>>>(MP);
+        BQ_CK_LAUNCH();
+        return BQ_OK;
+    }
+    constexpr int smem = mw_smem_bytes<KT>();
     auto kc = k_mw_count<KT, Kn::NT, Kn::IPT, MW_STAGES, Kn::MINB>;
     auto ks = k_mw_scatter<KT, Kn::NT, Kn::IPT, MW_STAGES, Kn::MINB>;
     static int cap_c = 0, cap_s = 0;
@@ -476,8 +495,8 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
         timing = opt->timing;
         ordered = opt->ordered;
         ways = opt->ways;
-        if (ways != 0 && ways != 2 && ways != MW_K)
-            return set_error(BQ_ERR_INVALID_ARGUMENT, "ways %d not in {0, 2, %d}", ways, MW_K);
+        if (ways != 0 && ways != 2 && ways != MW8 && ways != MW_K)
+            return set_error(BQ_ERR_INVALID_ARGUMENT, "ways %d not in {0, 2, %d, %d}", ways, MW8, MW_K);
         if (rule != BQ_PIVOT_MO3 && rule != BQ_PIVOT_NINTHER && rule != BQ_PIVOT_SAMPLE64)
             return set_error(BQ_ERR_INVALID_ARGUMENT, "bad pivot rule %d", rule);
         if (depth_limit >= MAX_LEVELS - 2)
@@ -658,7 +677,7 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
                 MP.n_total = n;
                 MP.aligned = aligned;
                 MP.ctrl = ctrl + level;
-                st = launch_multiway<KT>(MP, ctrl + level, s);
+                st = launch_multiway<KT>(MP, ctrl + level, s, ways);
                 if (st != BQ_OK) { cleanup(); return st; }
                 local.kernel_launches += 3;
                 Q.mw = MP;

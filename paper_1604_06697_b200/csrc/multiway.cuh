@@ -119,12 +119,12 @@ __device__ __forceinline__ K mw_pick(const K (&v)[8], uint32_t q) {
 // median, for the binary three-way partition.
 template <class KT>
 __device__ bool mw_splitters(const typename KT::T *buf, uint32_t b, uint32_t len, uint32_t leaf_max, uint32_t lane,
-                             typename KT::K &node_val, typename KT::K &pivot) {
+                             typename KT::K &node_val, typename KT::K &pivot, uint32_t kmax = MW_K) {
     using K = typename KT::K;
     K v[8];
     mw_sample_sorted<KT>(buf, b, len, lane, v);
     uint64_t ke = ((uint64_t)len * 2 + leaf_max - 1) / leaf_max;
-    const uint32_t keff = (uint32_t)(ke < 2 ? 2 : (ke > MW_K ? MW_K : ke));
+    const uint32_t keff = (uint32_t)(ke < 2 ? 2 : (ke > kmax ? kmax : ke));
     // lane i (1 <= i < keff) holds real splitter s_i; lanes i >= keff repeat s_{keff-1}
     const uint32_t i = lane < 1 ? 1 : (lane < keff ? lane : keff - 1);
     const K s = mw_pick(v, (i * MW_SAMPLE) / keff);
@@ -135,10 +135,11 @@ __device__ bool mw_splitters(const typename KT::T *buf, uint32_t b, uint32_t len
     const bool ok = __ballot_sync(0xffffffffu, bad) == 0;
     // tree node `lane` (1..15) at depth d, position p holds s_{(2p+1) * 2^(3-d)}
     uint32_t si = 0;
-    if (lane >= 1 && lane < MW_K) {
+    const uint32_t depth = kmax == MW_K ? 3 : 2;   // tree of kmax - 1 splitters
+    if (lane >= 1 && lane < kmax) {
         const uint32_t d = 31 - __clz(lane);
         const uint32_t p = lane - (1u << d);
-        si = (2 * p + 1) << (3 - d);
+        si = (2 * p + 1) << (depth - d);
     }
     node_val = __shfl_sync(0xffffffffu, s, si);
     return ok;
@@ -215,9 +216,8 @@ __device__ __forceinline__ void mw_warp_scan(uint32_t (&q)[MW_K / 2], uint32_t l
 
 // loader warp shared by the count and the scatter kernel: claims tiles in order,
 // copies the segment's metadata into the stage and issues the TMA bulk load
-template <class KT, int NT, int IPT, int STAGES>
-__device__ __forceinline__ void mw_loader(const MwParams<KT> &P, MwSmem<KT, NT, IPT, STAGES> &sm, uint32_t ntiles,
-                                          bool need_start) {
+template <class KT, int NT, int IPT, int STAGES, class SM>
+__device__ __forceinline__ void mw_loader(const MwParams<KT> &P, SM &sm, uint32_t ntiles, bool need_start) {
     using T = typename KT::T;
     constexpr uint32_t TILE = NT * IPT;
     constexpr uint32_t W = sizeof(T), VW = 16 / W;
@@ -343,7 +343,7 @@ __global__ void __launch_bounds__(NT + 32, MINB) k_mw_count(MwParams<KT> P) {
     }
     __syncthreads();
     if (warp == NW) {
-        if (lane == 0) mw_loader<KT, NT, IPT, STAGES>(P, sm, ntiles, false);
+        if (lane == 0) mw_loader<KT, NT, IPT, STAGES, SM>(P, sm, ntiles, false);
         return;
     }
     // lane L < 16 accumulates this warp's count of bucket L for segment cur_seg
@@ -430,7 +430,7 @@ __global__ void __launch_bounds__(NT + 32, MINB) k_mw_scatter(MwParams<KT> P) {
     }
     __syncthreads();
     if (warp == NW) {
-        if (lane == 0) mw_loader<KT, NT, IPT, STAGES>(P, sm, ntiles, true);
+        if (lane == 0) mw_loader<KT, NT, IPT, STAGES, SM>(P, sm, ntiles, true);
         return;
     }
 

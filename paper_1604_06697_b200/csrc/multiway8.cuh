@@ -1,0 +1,375 @@
+// multiway8.cuh — the 8-way variant of the multi-pivot block partition (N4),
+// sized so that every per-key step stays in registers.
+//
+// Segment metadata, splitter choice, bucket scan and children are shared with
+// the 16-way form (multiway.cuh: MSeg, mw_splitters(kmax = 8), k_mw_scan,
+// k_post_mw); the tree uses nodes 1..7: tree[1] = s_4, tree[2..3] = s_2, s_6,
+// tree[4..7] = s_1, s_3, s_5, s_7.
+//   classify  the 7 splitters of the tile's segment are read once per tile
+//             into registers; a key's bucket (#{s_i < k}) is three compares
+//             with register selects in between — the paper's "converting the
+//             results of comparisons to integers";
+//   rank      each thread keeps 8-bit counters of its keys' buckets in one
+//             64-bit register (<= 16 keys per thread): rank = field b, then
+//             field b += 1 — the k-bucket form of the offset buffers and
+//             their branch-free counters (Alg. 3 l.8-9);
+//   scan      the counters, widened to 16-bit pairs, are scanned over the
+//             warp with shuffles and over the warps through shared memory;
+//   place     one atomicAdd per bucket and tile claims the runs (consumed one
+//             tile later), runs staged aligned like their destinations, TMA
+//             bulk stores.
+#pragma once
+
+namespace bq {
+
+constexpr int MW8 = 8;
+
+template <class KT, int NT, int IPT, int STAGES>
+struct Mw8Smem {
+    using T = typename KT::T;
+    using K = typename KT::K;
+    static constexpr int TILE = NT * IPT;
+    static constexpr int NW = NT / 32;
+    alignas(128) T in[STAGES][TILE];
+    alignas(128) T out[TILE + MW8 * 8 + 16];
+    K tree[STAGES][MW_K];
+    uint32_t start[STAGES][MW_K];
+    uint32_t sb[STAGES], slen[STAGES], stb[STAGES], spar[STAGES], sidx[STAGES], tile[STAGES], manual[STAGES];
+    uint64_t full[STAGES];
+    uint64_t empty[STAGES];
+    uint32_t wtot[2][NW][MW8 / 2];   // per-warp bucket totals, 16-bit pairs
+    uint32_t wpre[2][NW][MW8 / 2];   // exclusive prefix over the warps, packed likewise
+    uint32_t boff[2][MW8 + 1];       // bucket starts inside the tile
+    uint32_t delta[2][MW8], gstart[2][MW8], cnt[2][MW8], sh[2][MW8];
+};
+
+template <class KT>
+constexpr int mw8_smem_bytes() {
+    return (int)sizeof(Mw8Smem<KT, Tune<KT>::PART_THREADS, Tune<KT>::PART_IPT, MW_STAGES>);
+}
+
+// the keys of stage s for this thread (permuted conflict-free vectors) and
+// their validity mask
+template <class KT, int NT, int IPT, int STAGES, class SM>
+__device__ __forceinline__ uint32_t mw8_load(const MwParams<KT> &P, SM &sm, uint32_t s, uint32_t t, uint32_t lane,
+                                             uint32_t tid, typename KT::T (&x)[IPT]) {
+    using T = typename KT::T;
+    constexpr uint32_t TILE = NT * IPT;
+    constexpr uint32_t W = sizeof(T), VW = 16 / W, NV4 = IPT / VW;
+    const uint32_t sw = NV4 > 1 ? ((lane * NV4) / 8) & (NV4 - 1) : 0;
+    const uint32_t e0 = tid * IPT;
+    Seg sg;
+    sg.begin = sm.sb[s];
+    sg.len = sm.slen[s];
+    sg.tile_base = sm.stb[s];
+    const TileGeom<KT, TILE> G(sg, t);
+    uint32_t valid = (1u << IPT) - 1;
+    if (!sm.manual[s]) {
+        const uint4 *in4 = reinterpret_cast<const uint4 *>(&sm.in[s][e0]);
+#pragma unroll
+        for (uint32_t k = 0; k < NV4; k++) {
+            const uint4 v = in4[k ^ sw];
+            memcpy(&x[k * VW], &v, 16);
+        }
+    } else {
+        const T *src = sm.spar[s] ? P.bufs[1] : P.bufs[0];
+#pragma unroll
+        for (uint32_t k = 0; k < NV4; k++)
+#pragma unroll
+            for (uint32_t j = 0; j < VW; j++) {
+                const uint32_t pos = e0 + (k ^ sw) * VW + j;
+                x[k * VW + j] = (pos >= G.vlo && pos < G.vhi) ? src[G.tbeg + pos] : T{};
+            }
+    }
+    if (G.vlo != 0 || G.vhi != TILE) {
+        valid = 0;
+#pragma unroll
+        for (uint32_t k = 0; k < NV4; k++)
+#pragma unroll
+            for (uint32_t j = 0; j < VW; j++) {
+                const uint32_t pos = e0 + (k ^ sw) * VW + j;
+                valid |= (uint32_t)(pos >= G.vlo && pos < G.vhi) << (k * VW + j);
+            }
+    }
+    return valid;
+}
+
+// bucket of key k: #{s_i < k} over the register-resident tree t[1..7]
+template <class K>
+__device__ __forceinline__ uint32_t mw8_bucket(const K (&tr)[MW8], K k) {
+    const bool p0 = tr[1] < k;
+    const K n1 = p0 ? tr[3] : tr[2];
+    const bool p1 = n1 < k;
+    const K lo = p1 ? tr[5] : tr[4], hi = p1 ? tr[7] : tr[6];
+    const K n2 = p0 ? hi : lo;
+    const bool p2 = n2 < k;
+    return ((uint32_t)p0 << 2) | ((uint32_t)p1 << 1) | (uint32_t)p2;
+}
+
+// 8 counters of 8 bits -> 4 words of two 16-bit counters
+__device__ __forceinline__ void mw8_widen(uint64_t c, uint32_t (&q)[MW8 / 2]) {
+    const uint32_t lo = (uint32_t)c, hi = (uint32_t)(c >> 32);
+    q[0] = __byte_perm(lo, 0, 0x4140);   // bytes 0, 1 -> 16-bit fields
+    q[1] = __byte_perm(lo, 0, 0x4342);
+    q[2] = __byte_perm(hi, 0, 0x4140);
+    q[3] = __byte_perm(hi, 0, 0x4342);
+}
+
+// ---- k_mw8_count -----------------------------------------------------------------
+template <class KT, int NT, int IPT, int STAGES, int MINB>
+__global__ void __launch_bounds__(NT + 32, MINB) k_mw8_count(MwParams<KT> P) {
+    using K = typename KT::K;
+    using SM = Mw8Smem<KT, NT, IPT, STAGES>;
+    constexpr uint32_t NW = SM::NW;
+    static_assert(IPT <= 255, "8-bit counters");
+    extern __shared__ __align__(128) unsigned char smraw[];
+    SM &sm = *reinterpret_cast<SM *>(smraw);
+    const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t ntiles = *P.ntiles_dev;
+    if (tid == 0) {
+        for (int s = 0; s < STAGES; s++) {
+            mbar_init(&sm.full[s], 1);
+            mbar_init(&sm.empty[s], NW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        fence_proxy_async_smem();
+    }
+    __syncthreads();
+    if (warp == NW) {
+        if (lane == 0) mw_loader<KT, NT, IPT, STAGES, SM>(P, sm, ntiles, false);
+        return;
+    }
+    // lane L < 8 accumulates this warp's count of bucket L for segment cur_seg
+    uint32_t acc = 0, cur_seg = 0xffffffffu;
+    for (uint32_t i = 0;; i++) {
+        const uint32_t s = i % STAGES;
+        mbar_wait(&sm.full[s], (i / STAGES) & 1);
+        const uint32_t t = sm.tile[s];
+        if (t >= ntiles) break;
+        const uint32_t si = sm.sidx[s];
+        K tr[MW8];
+#pragma unroll
+        for (int q = 1; q < MW8; q++) tr[q] = sm.tree[s][q];
+        typename KT::T x[IPT];
+        const uint32_t valid = mw8_load<KT, NT, IPT, STAGES, SM>(P, sm, s, t, lane, tid, x);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.empty[s]);
+        uint64_t c64 = 0;
+#pragma unroll
+        for (uint32_t c = 0; c < IPT; c++) {
+            const uint32_t b = mw8_bucket(tr, KT::key(x[c]));
+            c64 += (uint64_t)((valid >> c) & 1) << (8 * b);
+        }
+        uint32_t q[MW8 / 2];
+        mw8_widen(c64, q);
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1)
+#pragma unroll
+            for (int k = 0; k < MW8 / 2; k++) q[k] += __shfl_xor_sync(0xffffffffu, q[k], d);
+        if (si != cur_seg) {
+            if (cur_seg != 0xffffffffu && lane < MW8 && acc) atomicAdd(&P.hist[lane * P.hstride + cur_seg], acc);
+            acc = 0;
+            cur_seg = si;
+        }
+        uint32_t mine = 0;
+#pragma unroll
+        for (int k = 0; k < MW8 / 2; k++) mine = (lane >> 1) == (uint32_t)k ? q[k] : mine;
+        acc += (lane & 1) ? (mine >> 16) : (mine & 0xffff);
+    }
+    if (cur_seg != 0xffffffffu && lane < MW8 && acc) atomicAdd(&P.hist[lane * P.hstride + cur_seg], acc);
+}
+
+// ---- k_mw8_scatter ---------------------------------------------------------------
+template <class KT, int NT, int IPT, int STAGES, int MINB>
+__global__ void __launch_bounds__(NT + 32, MINB) k_mw8_scatter(MwParams<KT> P) {
+    using T = typename KT::T;
+    using K = typename KT::K;
+    using SM = Mw8Smem<KT, NT, IPT, STAGES>;
+    constexpr uint32_t NW = SM::NW;
+    constexpr uint32_t W = sizeof(T), VW = 16 / W;
+    static_assert(IPT <= 16, "8-bit counters, packed ranks");
+    extern __shared__ __align__(128) unsigned char smraw[];
+    SM &sm = *reinterpret_cast<SM *>(smraw);
+    const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t ntiles = *P.ntiles_dev;
+    if (tid == 0) {
+        for (int s = 0; s < STAGES; s++) {
+            mbar_init(&sm.full[s], 1);
+            mbar_init(&sm.empty[s], NW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        fence_proxy_async_smem();
+    }
+    __syncthreads();
+    if (warp == NW) {
+        if (lane == 0) mw_loader<KT, NT, IPT, STAGES, SM>(P, sm, ntiles, true);
+        return;
+    }
+
+    T y[IPT];
+    uint32_t ypk[IPT];   // previous tile: tile offset | bucket << 16 | invalid << 31
+    bool have_prev = false;
+    T *p_dst = nullptr;
+    uint32_t p_old = 0, p_cnt = 0, p_off = 0;   // warp 0, lane L < 8: previous tile's run L
+    uint64_t p_base = 0;
+
+    for (uint32_t i = 0;; i++) {
+        const uint32_t s = i % STAGES, par = i & 1;
+        mbar_wait(&sm.full[s], (i / STAGES) & 1);
+        const uint32_t t = sm.tile[s];
+        const bool cur = t < ntiles;
+        T x[IPT];
+        uint32_t pk[IPT];
+        uint32_t q[MW8 / 2], own[MW8 / 2];
+        uint32_t si = 0, sbeg = 0, spar = 0, bstart = 0;
+        if (cur) {
+            si = sm.sidx[s];
+            sbeg = sm.sb[s];
+            spar = sm.spar[s];
+            bstart = lane < MW8 ? sm.start[s][lane] : 0;
+            K tr[MW8];
+#pragma unroll
+            for (int qq = 1; qq < MW8; qq++) tr[qq] = sm.tree[s][qq];
+            const uint32_t valid = mw8_load<KT, NT, IPT, STAGES, SM>(P, sm, s, t, lane, tid, x);
+            uint64_t c64 = 0;
+#pragma unroll
+            for (uint32_t c = 0; c < IPT; c++) {
+                const uint32_t b = mw8_bucket(tr, KT::key(x[c]));
+                const uint32_t v = (valid >> c) & 1;
+                pk[c] = ((uint32_t)(c64 >> (8 * b)) & 0xff) | (b << 16) | ((v ^ 1) << 31);
+                c64 += (uint64_t)v << (8 * b);
+            }
+            mw8_widen(c64, q);
+#pragma unroll
+            for (int k = 0; k < MW8 / 2; k++) own[k] = q[k];
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+#pragma unroll
+                for (int k = 0; k < MW8 / 2; k++) {
+                    const uint32_t o = __shfl_up_sync(0xffffffffu, q[k], d);
+                    if (lane >= (uint32_t)d) q[k] += o;
+                }
+            }
+            if (lane == 31)
+#pragma unroll
+                for (int k = 0; k < MW8 / 2; k++) sm.wtot[par][warp][k] = q[k];
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.empty[s]);
+
+        // warp 0: placement of the previous tile's runs, now that its atomics returned
+        if (warp == 0 && have_prev) {
+            const uint64_t g = p_base + p_old;
+            const uint32_t a = (uint32_t)(g % VW);
+            const uint32_t padded = lane < MW8 ? (a + p_cnt + VW - 1) / VW * VW : 0;
+            uint32_t inc = padded;
+#pragma unroll
+            for (int d = 1; d < MW8; d <<= 1) {
+                const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+                if (lane >= (uint32_t)d) inc += o;
+            }
+            if (lane < MW8) {
+                const uint32_t shs = inc - padded + a;
+                sm.delta[par ^ 1][lane] = shs - p_off;
+                sm.sh[par ^ 1][lane] = shs;
+                sm.gstart[par ^ 1][lane] = (uint32_t)g;
+                sm.cnt[par ^ 1][lane] = p_cnt;
+            }
+        }
+        if (tid < MW8) bulk_wait_read0();
+        named_bar_sync(1, NT);   // B1: warp totals and placement visible, `out` free
+
+        if (cur && warp == 0 && lane < MW8 / 2) {
+            uint32_t run = 0;
+#pragma unroll
+            for (uint32_t w2 = 0; w2 < NW; w2++) {
+                sm.wpre[par][w2][lane] = run;
+                run += sm.wtot[par][w2][lane];
+            }
+            const uint32_t lo = run & 0xffff, hi = run >> 16;
+            const uint32_t pair = lo + hi;
+            uint32_t incp = pair;
+#pragma unroll
+            for (int d = 1; d < MW8 / 2; d <<= 1) {
+                const uint32_t o = __shfl_up_sync(0x0000000fu, incp, d);
+                if (lane >= (uint32_t)d) incp += o;
+            }
+            const uint32_t ex = incp - pair;
+            sm.boff[par][2 * lane] = ex;
+            sm.boff[par][2 * lane + 1] = ex + lo;
+            if (lane == MW8 / 2 - 1) sm.boff[par][MW8] = incp;
+        }
+        if (have_prev) {
+#pragma unroll
+            for (uint32_t c = 0; c < IPT; c++) {
+                const uint32_t v = ypk[c];
+                if (!(v >> 31)) sm.out[(v & 0xffff) + sm.delta[par ^ 1][(v >> 16) & 0x7fff]] = y[c];
+            }
+            if (P.aligned) fence_proxy_async_smem();
+        }
+        named_bar_sync(1, NT);   // B2: prefixes visible, staging complete
+
+        if (have_prev) {
+            T *d = p_dst;
+            if (!P.aligned) {
+                for (uint32_t L = 0; L < MW8; L++) {
+                    const uint32_t n = sm.cnt[par ^ 1][L];
+                    const uint64_t g = (uint64_t)sm.gstart[par ^ 1][L];
+                    for (uint32_t qq = tid; qq < n; qq += NT) d[g + qq] = sm.out[sm.sh[par ^ 1][L] + qq];
+                }
+            } else if (tid < MW8) {
+                const uint32_t L = tid, n = sm.cnt[par ^ 1][L];
+                const uint64_t g = sm.gstart[par ^ 1][L], ge = g + n;
+                const uint64_t bs = (g + VW - 1) / VW * VW, be = ge / VW * VW;
+                if (n && be > bs) tma_store_1d(d + bs, &sm.out[sm.sh[par ^ 1][L] + (bs - g)], (uint32_t)((be - bs) * W));
+                bulk_commit();
+            } else if (tid >= 32 && tid < 32 + MW8 * 2 * VW) {
+                const uint32_t u = tid - 32, L = u / (2 * VW), qv = u % (2 * VW);
+                const uint32_t n = sm.cnt[par ^ 1][L];
+                const uint64_t g = sm.gstart[par ^ 1][L], ge = g + n;
+                const uint64_t bs = (g + VW - 1) / VW * VW, be = ge / VW * VW;
+                const bool tail = qv >= VW;
+                const uint32_t qq = tail ? qv - VW : qv;
+                const uint64_t pos = tail ? (be > bs ? be : bs) + qq : g + qq;
+                const bool ok = n && (tail ? (ge > bs && pos < ge) : (pos < (bs < ge ? bs : ge)));
+                if (ok) d[pos] = sm.out[sm.sh[par ^ 1][L] + (pos - g)];
+            }
+        }
+        if (!cur) break;
+
+        // each key's offset in the tile: bucket start + preceding warps' and lanes'
+        // keys of its bucket + its rank among this thread's keys of the bucket
+        {
+            uint32_t base[MW8 / 2];
+#pragma unroll
+            for (int k = 0; k < MW8 / 2; k++) {
+                base[k] = q[k] - own[k] + sm.wpre[par][warp][k] + (sm.boff[par][2 * k] | (sm.boff[par][2 * k + 1] << 16));
+            }
+#pragma unroll
+            for (uint32_t c = 0; c < IPT; c++) {
+                const uint32_t b = (pk[c] >> 16) & 0x7fff;
+                const uint32_t w01 = (b & 2) ? base[1] : base[0], w23 = (b & 2) ? base[3] : base[2];
+                const uint32_t w = (b & 4) ? w23 : w01;
+                pk[c] += (b & 1) ? (w >> 16) : (w & 0xffff);
+            }
+        }
+        if (warp == 0) {
+            const uint32_t st = lane < MW8 ? sm.boff[par][lane] : 0;
+            const uint32_t tot = lane < MW8 ? sm.boff[par][lane + 1] - st : 0;
+            p_old = (lane < MW8 && tot) ? atomicAdd(&P.cursor[lane * P.hstride + si], tot) : 0;
+            p_cnt = tot;
+            p_off = st;
+            p_base = (uint64_t)sbeg + bstart;
+        }
+#pragma unroll
+        for (uint32_t c = 0; c < IPT; c++) {
+            y[c] = x[c];
+            ypk[c] = pk[c];
+        }
+        have_prev = true;
+        p_dst = spar ? P.bufs[0] : P.bufs[1];
+    }
+    if (tid < MW8) bulk_wait0();
+}
+
+}  // namespace bq

@@ -63,6 +63,7 @@ __device__ __forceinline__ uint32_t pass_ntiles(const PassParams<KT> &P) {
 #include "partition_kernel.cuh"
 #include "partition_fast.cuh"
 #include "multiway.cuh"
+#include "multiway8.cuh"
 
 namespace bq {
 
@@ -174,7 +175,7 @@ __device__ __forceinline__ void emit_children(const PostParams<KT> &Q, int nch, 
             mode = dup ? 2 : 0;
         } else if (Q.ways > 2 && !KT::is_record) {
             K node, piv;
-            const bool ok = mw_splitters<KT>(cbuf, cb[c], len, Q.leaf_max, lane, node, piv);
+            const bool ok = mw_splitters<KT>(cbuf, cb[c], len, Q.leaf_max, lane, node, piv, (uint32_t)Q.ways);
             kind = ok ? C_MW : C_BIN;
             if (lane == 0) s_piv[c] = (uint64_t)piv;
             if (lane < MW_K) s_tree[c][lane] = node;

@@ -432,37 +432,40 @@ def test_sort_patterns_ordered_placement(B, name):
 
 # ------------------------------------------ multi-pivot block partition (N4) ---
 
+@pytest.mark.parametrize("ways", [8, 16])
 @pytest.mark.parametrize("kind", ["i32", "u64", "f64"])
 @pytest.mark.parametrize("dist", ["random", "dups"])
-def test_sort_multiway(B, kind, dist):
+def test_sort_multiway(B, kind, dist, ways):
     for n in [S_ + 1 for S_ in (LEAF[kind],)] + [100003, (1 << 20) + 17, (1 << 22) + 3]:
         a = make(kind, n, seed=n % 97, dist=dist)
         t = to_dev(a)
-        st = B.bq_sort_ex(t, ways=16)
+        st = B.bq_sort_ex(t, ways=ways)
         check_sorted_equal(kind, to_host(t, a), a)
         assert st["fallback_segments"] == 0
 
 
+@pytest.mark.parametrize("ways", [8, 16])
 @pytest.mark.parametrize("name", PATTERNS)
-def test_sort_multiway_patterns(B, name):
+def test_sort_multiway_patterns(B, name, ways):
     for n in [(1 << 16) + 3, (1 << 20) + 1]:
         if name == "swaps_nlogn" and n > (1 << 17):
             continue
         a = bqgen.i32_pattern(name, n, seed=3)
         t = to_dev(a)
-        st = B.bq_sort_ex(t, ways=16)
+        st = B.bq_sort_ex(t, ways=ways)
         assert np.array_equal(t.cpu().numpy(), oracle.sort(a))
         assert st["fallback_segments"] == 0
 
 
-def test_sort_multiway_configs(B):
+@pytest.mark.parametrize("ways", [8, 16])
+def test_sort_multiway_configs(B, ways):
     for name in ["c1", "c2", "c4a", "c4b"]:
         a = bqgen.config(name, 1 << 21, seed=5)
         t = to_dev(a)
-        B.bq_sort_ex(t, ways=16)
+        B.bq_sort_ex(t, ways=ways)
         assert np.array_equal(t.cpu().numpy(), oracle.sort(a))
     for ordering in ["random", "ascending", "descending", "swapped"]:
         a = bqgen.config("c3", 1 << 20, seed=5, ordering=ordering)
         t = to_dev(a)
-        B.bq_sort_ex(t, ways=16)
+        B.bq_sort_ex(t, ways=ways)
         assert np.array_equal(t.cpu().numpy().view(np.uint64), oracle.sort(a).view(np.uint64))

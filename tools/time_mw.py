@@ -9,7 +9,7 @@ src = torch.from_numpy(bqgen.i32_full(n, 1)).cuda()
 dst = torch.empty_like(src)
 ws = bq.workspace(bq.BQ_I32, n)
 ref = torch.sort(src)[0]
-for ways in (2, 16):
+for ways in (2, 8, 16):
     ts = []
     for i in range(4):
         dst.copy_(src)
