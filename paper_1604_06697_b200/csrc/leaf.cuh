@@ -355,19 +355,17 @@ constexpr size_t leaf_smem_bytes() {
     return b;
 }
 
+// One leaf, by the whole CTA.  For keys it is called out of line from the
+// persistent loop below: inlined, the compiler hoists the transposes'
+// per-thread addresses out of the loop and spills.
 template <class KT, int L>
-__global__ void __launch_bounds__(1 << (L - LeafTraits<KT>::R), (LeafTraits<KT>::OCC >> (L - LeafTraits<KT>::R)) > 0 ? (LeafTraits<KT>::OCC >> (L - LeafTraits<KT>::R)) : 1) k_leaf(LeafParams<KT> P) {
+__device__ __forceinline__ void leaf_body(const LeafParams<KT> &P, const Leaf lf, unsigned char *smem_raw) {
     using T = typename KT::T;
     using K = typename KT::K;
     using E = typename LeafTraits<KT>::E;
     constexpr int R = LeafTraits<KT>::R, IPT = 1 << R, NT = 1 << (L - R), NET = 1 << L;
-    extern __shared__ __align__(128) unsigned char smem_raw[];
     unsigned char *planes = smem_raw;
     const uint32_t t = threadIdx.x;
-    const uint32_t nleaves = P.count_dev ? *P.count_dev : gridDim.x;
-    for (uint32_t li = blockIdx.x; li < nleaves; li += gridDim.x) {
-    if (li != blockIdx.x) __syncthreads();   // the previous leaf's shared-memory readers are done
-    const Leaf lf = P.leaves[li];
     const uint32_t len = lf.len;
     T *srcbuf = lf.parity ? P.bufs[1] : P.bufs[0];
     T *out = P.out_inplace ? srcbuf : P.out;
@@ -412,6 +410,22 @@ __global__ void __launch_bounds__(1 << (L - LeafTraits<KT>::R), (LeafTraits<KT>:
             if (i < len) out[b + i] = KT::from_key((K)x[r]);
         }
     }
+}
+
+template <class KT, int L>
+__device__ __noinline__ void leaf_one(const LeafParams<KT> &P, const Leaf lf, unsigned char *smem_raw) {
+    leaf_body<KT, L>(P, lf, smem_raw);
+}
+
+template <class KT, int L>
+__global__ void __launch_bounds__(1 << (L - LeafTraits<KT>::R), (LeafTraits<KT>::OCC >> (L - LeafTraits<KT>::R)) > 0 ? (LeafTraits<KT>::OCC >> (L - LeafTraits<KT>::R)) : 1) k_leaf(LeafParams<KT> P) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const uint32_t nleaves = P.count_dev ? *P.count_dev : gridDim.x;
+    for (uint32_t li = blockIdx.x; li < nleaves; li += gridDim.x) {
+        if (li != blockIdx.x) __syncthreads();   // the previous leaf's shared-memory readers are done
+        // (keys: out of line, see leaf_one; records measured faster inlined)
+        if constexpr (KT::is_record) leaf_body<KT, L>(P, P.leaves[li], smem_raw);
+        else leaf_one<KT, L>(P, P.leaves[li], smem_raw);
     }
 }
 
