@@ -85,10 +85,13 @@ template <class KT> struct Tune;
 #ifndef BQ_I32_MINB
 #define BQ_I32_MINB 2
 #endif
+#ifndef BQ_I32_LEAF
+#define BQ_I32_LEAF 8192
+#endif
 template <> struct Tune<KI32> {
     static constexpr int PART_THREADS = 256, PART_IPT = BQ_I32_IPT, PART_STAGES = BQ_I32_STAGES,
                          PART_MINB = BQ_I32_MINB;
-    static constexpr int LEAF = 8192, LEAF_THREADS = 512;
+    static constexpr int LEAF = BQ_I32_LEAF, LEAF_THREADS = 512;
 };
 template <> struct Tune<KU64> {
     static constexpr int PART_THREADS = 256, PART_IPT = 8, PART_STAGES = 4, PART_MINB = 2;   // 16 KB tiles

@@ -78,7 +78,7 @@ constexpr int leaf_lmax() {
 }
 template <class KT>
 constexpr int leaf_nclass() { return leaf_lmax<KT>() - leaf_lmin<KT>() + 1; }
-constexpr int MAX_LEAF_CLASSES = 4;
+constexpr int MAX_LEAF_CLASSES = 4;   // LevelCtrl::nleaf_cls, leaf-count words per set
 
 // network-size class of a leaf of `len` keys: NET = 2^(lmin + class)
 template <class KT>
@@ -347,8 +347,12 @@ struct Net {
     }
 };
 
+template <class KT>
+constexpr bool leaf_classes_fit() { return leaf_nclass<KT>() <= MAX_LEAF_CLASSES; }
+
 template <class KT, int L>
 constexpr size_t leaf_smem_bytes() {
+    static_assert(leaf_classes_fit<KT>(), "S / 2^(R+5) network classes exceed MAX_LEAF_CLASSES");
     constexpr int NET = 1 << L;
     size_t b = (size_t)Planes<KT>::template bytes<NET>();
     if constexpr (KT::is_record) b += (size_t)NET * sizeof(typename KT::T);
