@@ -168,6 +168,22 @@ BQ_API bq_status bq_partition_pass(bq_kind kind, const void *src, void *dst, siz
                                    const void *pivot, uint64_t *d_counts, int ordered, void *ws,
                                    size_t ws_bytes, void *stream);
 
+/* ---- in-place partition (Alg. 3 at CTA granularity) ---------
+ * Permutes data[0, n) in place into [< pivot | == pivot | > pivot], split =
+ * #{k < pivot}, with no n-element scratch: every CTA runs the paper's block
+ * main loop on blocks claimed from both ends — offsets buffers of
+ * the misplaced elements, min(num_L, num_R) swaps, a neutralized block
+ * written back and the next one claimed — and the few blocks left when the
+ * two sides meet are rearranged in a small buffer ("compare and rearrange
+ * remaining elements", l.29).  The order inside each band is unspecified.
+ * `pivot` points to a HOST value of the kind's storage type (a uint64 key for
+ * records); `ws` needs bq_inplace_workspace_bytes(kind, n) bytes (about
+ * 1200 tiles, independent of n for large n).  Synchronises `stream`.  A NaN
+ * f64 pivot is BQ_ERR_INVALID_ARGUMENT. */
+BQ_API size_t bq_inplace_workspace_bytes(bq_kind kind, size_t n);
+BQ_API bq_status bq_partition_inplace(bq_kind kind, void *data, size_t n, const void *pivot, size_t *split,
+                                      size_t *n_equal, void *ws, size_t ws_bytes, void *stream);
+
 /* Batched pass over `nseg` disjoint segments of src (one breadth-first level
  * of the Quicksort recursion, executed at once): segment i is
  * [begins[i], begins[i] + lens[i]) with pivot pivots[i] (HOST arrays; pivots

@@ -68,6 +68,8 @@ _SIGS = {
     "bq_partition_f64": (_st, [_vp, _sz, ctypes.c_double, _psz, _psz, _vp, _sz, _vp]),
     "bq_partition_records": (_st, [_vp, _sz, ctypes.c_uint64, _psz, _psz, _vp, _sz, _vp]),
     "bq_partition_pass": (_st, [_st, _vp, _vp, _sz, _vp, _vp, _st, _vp, _sz, _vp]),
+    "bq_inplace_workspace_bytes": (_sz, [_st, _sz]),
+    "bq_partition_inplace": (_st, [_st, _vp, _sz, _vp, _psz, _psz, _vp, _sz, _vp]),
     "bq_partition_segments": (_st, [_st, _vp, _vp, _sz, _vp, _vp, _vp, _sz, _vp, _st, _vp, _sz, _vp]),
     "bq_sort_i32": (_st, [_vp, _sz, _vp, _sz, _vp]),
     "bq_sort_u64": (_st, [_vp, _sz, _vp, _sz, _vp]),
@@ -212,6 +214,24 @@ def bq_partition_pass(src, dst, pivot, d_counts, ordered=True, ws=None, stream=N
     pv = _PIVOT_CTYPE[kind](pivot)
     _check(_lib.bq_partition_pass(kind, _dev(src), _dev(dst), _n(src), ctypes.byref(pv),
                                   _dev(d_counts), int(ordered), w, wb, _stream(stream)))
+
+
+def bq_inplace_workspace_bytes(kind: int, n: int) -> int:
+    return int(_lib.bq_inplace_workspace_bytes(kind, n))
+
+
+def bq_partition_inplace(data, pivot, ws=None, stream=None):
+    """In-place three-way partition with a small workspace (N2); returns
+    (split, n_equal).  The order inside each band is unspecified."""
+    kind = kind_of(data)
+    if ws is None:
+        ws = torch.empty(bq_inplace_workspace_bytes(kind, _n(data)), dtype=torch.uint8, device=data.device)
+    pv = _PIVOT_CTYPE[kind](pivot)
+    s, e = ctypes.c_size_t(0), ctypes.c_size_t(0)
+    _check(_lib.bq_partition_inplace(kind, _dev(data), _n(data), ctypes.byref(pv), ctypes.byref(s),
+                                     ctypes.byref(e), ws.data_ptr(), ws.numel() * ws.element_size(),
+                                     _stream(stream)))
+    return s.value, e.value
 
 
 def bq_partition_segments(src, dst, begins, lens, pivots, d_counts, ordered=True, ws=None, stream=None):

@@ -73,6 +73,34 @@ BQ_API bq_status bq_partition_pass(bq_kind kind, const void *src, void *dst, siz
     return bq::set_error(BQ_ERR_INVALID_ARGUMENT, "bad kind %d", (int)kind);
 }
 
+BQ_API size_t bq_inplace_workspace_bytes(bq_kind kind, size_t n) {
+    switch (kind) {
+        case BQ_I32: return ipws_i32(n);
+        case BQ_U64: return ipws_u64(n);
+        case BQ_F64: return ipws_f64(n);
+        case BQ_REC32: return ipws_rec(n);
+    }
+    return 0;
+}
+
+BQ_API bq_status bq_partition_inplace(bq_kind kind, void *data, size_t n, const void *pivot, size_t *split,
+                                      size_t *n_equal, void *ws, size_t ws_bytes, void *stream) {
+    if (pivot == nullptr) return bq::set_error(BQ_ERR_INVALID_ARGUMENT, "NULL pivot");
+    cudaStream_t s = (cudaStream_t)stream;
+    switch (kind) {
+        case BQ_I32: return inplace_i32(data, n, pivot, split, n_equal, ws, ws_bytes, s);
+        case BQ_U64: return inplace_u64(data, n, pivot, split, n_equal, ws, ws_bytes, s);
+        case BQ_F64: {
+            double d;
+            std::memcpy(&d, pivot, 8);
+            if (d != d) return bq::set_error(BQ_ERR_INVALID_ARGUMENT, "NaN pivot");
+            return inplace_f64(data, n, pivot, split, n_equal, ws, ws_bytes, s);
+        }
+        case BQ_REC32: return inplace_rec(data, n, pivot, split, n_equal, ws, ws_bytes, s);
+    }
+    return bq::set_error(BQ_ERR_INVALID_ARGUMENT, "bad kind %d", (int)kind);
+}
+
 BQ_API bq_status bq_partition_segments(bq_kind kind, const void *src, void *dst, size_t n, const uint32_t *begins,
                                        const uint32_t *lens, const void *pivots, size_t nseg, uint64_t *d_counts,
                                        int ordered, void *ws, size_t ws_bytes, void *stream) {

@@ -5,6 +5,12 @@
 namespace bq {
 namespace detail {
 size_t ws_rec(size_t n) { return make_layout<KRec>(n).total; }
+size_t ipws_rec(size_t n) { return make_ip_layout<KRec>(n).total; }
+bq_status inplace_rec(void *data, size_t n, const void *pivot, size_t *split, size_t *neq, void *ws, size_t wsb,
+                      cudaStream_t s) {
+    return run_partition_inplace_ip<KRec>(static_cast<Rec32 *>(data), n, pivot_key_from<KRec>(pivot), split, neq,
+                                          ws, wsb, s);
+}
 bq_status sort_rec(void *data, size_t n, const bq_sort_options *opt, bq_sort_stats *st, void *ws, size_t wsb,
                    cudaStream_t s) {
     return run_sort<KRec>(static_cast<Rec32 *>(data), n, opt, st, ws, wsb, s);

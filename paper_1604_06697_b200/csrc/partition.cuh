@@ -64,6 +64,7 @@ __device__ __forceinline__ uint32_t pass_ntiles(const PassParams<KT> &P) {
 #include "partition_fast.cuh"
 #include "multiway.cuh"
 #include "multiway8.cuh"
+#include "inplace.cuh"
 
 namespace bq {
 

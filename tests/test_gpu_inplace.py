@@ -1,0 +1,149 @@
+"""N2: the in-place block partition, bq_partition_inplace, vs
+the oracle (-m gpu).
+
+The in-place variant places keys by block swaps (Alg. 3), so the
+order inside each band is unspecified; what is unique is checked exactly —
+split and n_equal against oracle.partition (bit-exact counts), the three band
+predicates, the multiset, and for records that every row travels whole.  Its
+workspace is O(#CTAs * T), independent of n (the paper's in-place property,
+P:157-161), which is pinned too.
+"""
+import numpy as np
+import pytest
+import torch
+
+import bqgen
+import oracle
+from gpu_util import to_dev, to_host
+from test_gpu_parity import TILE, _pivots, edge_sizes, f64_key, keys_of, make
+
+pytestmark = pytest.mark.gpu
+
+KINDS = ["i32", "u64", "f64", "rec32"]
+
+
+@pytest.fixture(scope="module")
+def B(bq):
+    assert torch.cuda.is_available()
+    return bq
+
+
+def _key(kind, a):
+    if kind == "f64":
+        return f64_key(a)
+    return keys_of(a)
+
+
+def _pk(kind, pv):
+    if kind == "f64":
+        return f64_key(np.array([pv]))[0]
+    if kind == "i32":
+        return np.int32(pv)
+    return np.uint64(pv)
+
+
+def check(B, kind, a, pv):
+    t = to_dev(a)
+    split, neq = B.bq_partition_inplace(t, pv)
+    _, s_o, e_o = oracle.partition(a, pv)
+    assert (split, neq) == (s_o, e_o)
+    got = to_host(t, a)
+    k, pk = _key(kind, got), _pk(kind, pv)
+    assert (k[:split] < pk).all()
+    assert (k[split:split + neq] == pk).all()
+    assert (k[split + neq:] > pk).all()
+    if kind == "rec32":
+        idx = got[:, 1].astype(np.int64)
+        assert np.array_equal(np.sort(idx), np.arange(len(a)))
+        assert (got[:, 1] == got[:, 2]).all() and (got[:, 2] == got[:, 3]).all()
+        assert np.array_equal(got[:, 0], a[idx, 0])
+    elif kind == "f64":
+        assert np.array_equal(np.sort(got.view(np.uint64)), np.sort(a.view(np.uint64)))
+    else:
+        assert np.array_equal(np.sort(got), np.sort(a))
+    return split, neq
+
+
+@pytest.mark.parametrize("kind", KINDS)
+@pytest.mark.parametrize("dist", ["random", "dups"])
+def test_inplace_vs_oracle_edge_sizes(B, kind, dist):
+    for n in edge_sizes(kind):
+        a = make(kind, n, seed=n + 9, dist=dist)
+        for p in _pivots(kind, a):
+            check(B, kind, a, float(p) if kind == "f64" else int(p))
+
+
+@pytest.mark.parametrize("kind", KINDS)
+@pytest.mark.parametrize("n_tiles", [7, 150, 1185, 3001])
+def test_inplace_many_blocks(B, kind, n_tiles):
+    """More blocks than resident CTAs (148 x occupancy) and a ragged tail, so
+    blocks are claimed repeatedly from both sides and leftovers occur."""
+    n = n_tiles * TILE[kind] + 37
+    for dist in ("random", "dups"):
+        a = make(kind, n, seed=n_tiles, dist=dist)
+        k = keys_of(a)
+        p = k[len(k) // 3]
+        check(B, kind, a, float(p) if kind == "f64" else int(p))
+
+
+@pytest.mark.parametrize("kind", ["i32", "f64"])
+@pytest.mark.parametrize("pattern", ["ascending", "descending", "all_left", "all_right", "all_equal"])
+def test_inplace_skewed(B, kind, pattern):
+    """One-sided inputs: all blocks neutralize from one end (the claim word
+    must not run past the meeting point), sorted / reverse-sorted ranges
+    (nothing / everything misplaced), and a constant range (only the equal
+    band)."""
+    n = 2000 * TILE[kind] + 11
+    a = make(kind, n, seed=5)
+    srt = np.sort(a)
+    if pattern == "ascending":
+        a, p = srt, srt[n // 2]
+    elif pattern == "descending":
+        a, p = srt[::-1].copy(), srt[n // 2]
+    elif pattern == "all_left":
+        p = srt[-1]
+    elif pattern == "all_right":
+        p = srt[0]
+    else:
+        a = np.full(n, srt[n // 2], dtype=a.dtype)
+        p = a[0]
+    check(B, kind, a, float(p) if kind == "f64" else int(p))
+
+
+def test_inplace_absent_pivot_and_extremes(B):
+    n = 1500 * TILE["u64"] + 5
+    a = make("u64", n, seed=3)
+    for pv in [0, (1 << 64) - 1, int(np.sort(a)[n // 2]) + 1]:
+        check(B, "u64", a, pv)
+
+
+def test_inplace_workspace_is_independent_of_n(B):
+    """The paper's in-place property: the workspace does not grow with n
+    (bounded by #CTAs blocks plus the cleanup's small buffers)."""
+    w1 = B.bq_inplace_workspace_bytes(B.BQ_I32, 1 << 24)
+    w2 = B.bq_inplace_workspace_bytes(B.BQ_I32, 1 << 30)
+    assert w1 == w2
+    assert w2 < (1 << 24) * 4
+    assert B.bq_inplace_workspace_bytes(B.BQ_I32, 100) < w1
+
+
+def test_inplace_c2_full(B):
+    """BASELINE config 2 at full size, in place, around the oracle's Mo3 pivot."""
+    a = bqgen.config("c2", seed=1)
+    t = to_dev(a)
+    p = B.bq_pivot_i32(t, B.BQ_PIVOT_MO3)
+    split, neq = B.bq_partition_inplace(t, p)
+    assert split == int(np.count_nonzero(a < p)) and neq == int(np.count_nonzero(a == p))
+    assert bool((t[:split] < p).all()) and bool((t[split:split + neq] == p).all())
+    assert bool((t[split + neq:] > p).all())
+    got = t.cpu().numpy()
+    assert np.array_equal(np.sort(got), np.sort(a))
+
+
+def test_inplace_invalid_arguments(B):
+    t = torch.zeros(10, dtype=torch.float64, device="cuda")
+    with pytest.raises(Exception):
+        B.bq_partition_inplace(t, float("nan"))
+    small = torch.empty(16, dtype=torch.uint8, device="cuda")
+    with pytest.raises(Exception):
+        B.bq_partition_inplace(torch.zeros(1 << 16, dtype=torch.int32, device="cuda"), 0, ws=small)
