@@ -358,162 +358,110 @@ bq_status run_partition_inplace(typename KT::T *data, size_t n, typename KT::K p
 }
 
 // ---- N2: in-place block partition (inplace.cuh) ------------------------------
-constexpr uint32_t IP_GMAX = 148 * 8;   // bound on the resident k_inplace CTAs
-
 template <class KT>
 struct IpLayout {
-    size_t state, leftover, pairs, counts, s1, s2, pass, total, vmax;
+    size_t passes, leftover, pairs, s1, s2, total, vmax;
 };
 template <class KT>
 IpLayout<KT> make_ip_layout(size_t n) {
     constexpr size_t TILE = tile_elems<KT>();
     IpLayout<KT> L;
-    L.vmax = (IP_GMAX + 1) * TILE < n ? (IP_GMAX + 1) * TILE : n;
+    L.vmax = (IP_GMAX + 1) * TILE + 16 < n ? (IP_GMAX + 1) * TILE + 16 : n;
     size_t off = 0;
     auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + bytes, 256); return o; };
-    L.state = take(sizeof(InplaceState));
+    L.passes = take(2 * sizeof(IpPass));
     L.leftover = take(2 * IP_GMAX * sizeof(uint32_t));
-    L.pairs = take(2 * IP_GMAX * sizeof(uint32_t));
-    L.counts = take(3 * sizeof(uint64_t));
+    L.pairs = take(4 * IP_GMAX * sizeof(uint32_t));
     L.s1 = take(L.vmax * sizeof(typename KT::T));
     L.s2 = take(L.vmax * sizeof(typename KT::T));
-    L.pass = take(make_layout<KT>(L.vmax).total);
     L.total = off;
     return L;
 }
 
-// One in-place two-way partition of base[0, n): mode 0 puts keys < p left,
-// mode 1 keys <= p.  Returns the size of the left part and the number of keys
-// equal to p.
-template <class KT>
-bq_status inplace_pass(typename KT::T *base, size_t n, typename KT::K pk, int mode, char *w, const IpLayout<KT> &L,
-                       cudaStream_t s, uint64_t *n_left, uint64_t *n_eq) {
-    using T = typename KT::T;
-    using Kn = Kernels<KT>;
-    constexpr uint32_t TILE = tile_elems<KT>();
-    InplaceState *dst = reinterpret_cast<InplaceState *>(w + L.state);
-    uint32_t *leftover = reinterpret_cast<uint32_t *>(w + L.leftover);
-    uint32_t *pairs = reinterpret_cast<uint32_t *>(w + L.pairs);
-    uint64_t *counts = reinterpret_cast<uint64_t *>(w + L.counts);
-    T *s1 = reinterpret_cast<T *>(w + L.s1);
-    T *s2 = reinterpret_cast<T *>(w + L.s2);
-    const uint32_t nb = (uint32_t)(n / TILE);
-    const uint64_t tail = n - (uint64_t)nb * TILE;
-
-    // phase 1: block neutralization from both ends
-    InplaceState hs;
-    std::memset(&hs, 0, sizeof hs);
-    hs.claim = ((unsigned long long)(IP_BIAS + nb) << 32) | IP_BIAS;
-    BQ_CK(cudaMemcpyAsync(dst, &hs, sizeof hs, cudaMemcpyHostToDevice, s));
-    if (nb) {
-        auto kern = k_inplace<KT, Kn::NT, Kn::IPT>;
-        constexpr int smem = inplace_smem_bytes<KT>();
-        static int cap = 0;
-        bq_status st = persistent_cap(kern, Kn::NT, smem, &cap);
-        if (st != BQ_OK) return st;
-        uint32_t grid = (uint32_t)cap < IP_GMAX ? (uint32_t)cap : IP_GMAX;
-        grid = nb < grid ? nb : grid;
-        InplaceParams<KT> P{base, nb, (uint64_t)pk, mode, dst, leftover};
-        kern<<<grid, Kn::NT, smem, s>>>(P);
-        BQ_CK_LAUNCH();
-    }
-    BQ_CK(cudaMemcpyAsync(&hs, dst, sizeof hs, cudaMemcpyDeviceToHost, s));
-    BQ_CK(cudaStreamSynchronize(s));
-    std::vector<uint32_t> lo(2 * hs.nleftover);
-    if (hs.nleftover) {
-        BQ_CK(cudaMemcpyAsync(lo.data(), leftover, lo.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-        BQ_CK(cudaStreamSynchronize(s));
-    }
-    const uint32_t X = hs.left_ok;   // blocks [0, X) were claimed from the left, [X, nb) from the right
-    std::vector<uint32_t> LL, RL;
-    for (uint32_t k = 0; k < hs.nleftover; k++) (lo[2 * k] < X ? LL : RL).push_back(lo[2 * k]);
-    std::sort(LL.begin(), LL.end());
-    std::sort(RL.begin(), RL.end());
-    const uint32_t a = (uint32_t)LL.size(), c = (uint32_t)RL.size();
-
-    // phase 2a: move the leftover blocks into the middle [X - a, X + c)
-    std::vector<uint32_t> pr;
-    {
-        std::vector<char> isL(a ? a : 1, 0), isR(c ? c : 1, 0);
-        std::vector<uint32_t> outL, inL, outR, inR;
-        for (uint32_t b : LL) (b < X - a ? outL.push_back(b) : (void)(isL[b - (X - a)] = 1));
-        for (uint32_t j = 0; j < a; j++) if (!isL[j]) inL.push_back(X - a + j);
-        for (uint32_t b : RL) (b >= X + c ? outR.push_back(b) : (void)(isR[b - X] = 1));
-        for (uint32_t j = 0; j < c; j++) if (!isR[j]) inR.push_back(X + j);
-        if (outL.size() != inL.size() || outR.size() != inR.size())
-            return set_error(BQ_ERR_CUDA, "in-place partition: inconsistent leftover blocks");
-        for (size_t k = 0; k < outL.size(); k++) { pr.push_back(outL[k]); pr.push_back(inL[k]); }
-        for (size_t k = 0; k < outR.size(); k++) { pr.push_back(outR[k]); pr.push_back(inR[k]); }
-    }
-    if (!pr.empty()) {
-        BQ_CK(cudaMemcpyAsync(pairs, pr.data(), pr.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
-        k_swap_blocks<KT, Kn::NT, Kn::IPT><<<(uint32_t)(pr.size() / 2), Kn::NT, 0, s>>>(base, pairs);
-        BQ_CK_LAUNCH();
-        BQ_CK(cudaStreamSynchronize(s));   // the host vector `pr` is read by the copy above
-    }
-
-    // phase 2b: "compare and rearrange remaining elements" (Alg. 3 l.29): the
-    // middle blocks and the tail, partitioned three-way out of place in V
-    const uint64_t o1 = (uint64_t)(X - a) * TILE, n1 = (uint64_t)(a + c) * TILE;
-    const uint64_t o2 = (uint64_t)nb * TILE, n2 = tail;
-    const uint64_t v = n1 + n2;
-    uint64_t lv = 0, ev = 0;
-    if (v) {
-        if (v > L.vmax) return set_error(BQ_ERR_CUDA, "in-place partition: middle of %llu > %zu", (unsigned long long)v, L.vmax);
-        const uint32_t g = (uint32_t)((v + 255) / 256 < 4096 ? (v + 255) / 256 : 4096);
-        k_gather2<KT><<<g, 256, 0, s>>>(base, s1, o1, n1, o2, n2, 0);
-        BQ_CK_LAUNCH();
-        bq_status st = run_pass<KT>(s1, s2, s1, (size_t)v, pk, counts, w + L.pass, s, KT::is_record ? 1 : 0);
-        if (st != BQ_OK) return st;
-        k_gather2<KT><<<g, 256, 0, s>>>(base, s2, o1, n1, o2, n2, 1);
-        BQ_CK_LAUNCH();
-        uint64_t h[3];
-        BQ_CK(cudaMemcpyAsync(h, counts, sizeof h, cudaMemcpyDeviceToHost, s));
-        BQ_CK(cudaStreamSynchronize(s));
-        lv = mode ? h[0] + h[1] : h[0];
-        ev = h[1];
-        // the middle's left part may run into the tail positions: those keys
-        // swap with the first keys of the right blocks that separate them
-        if (lv > n1 && o1 + n1 < o2) {
-            const uint64_t e = lv - n1;
-            k_swap_ranges<KT><<<(uint32_t)((e + 255) / 256), 256, 0, s>>>(base, o1 + n1, o2, e);
-            BQ_CK_LAUNCH();
-        }
-    }
-    *n_left = o1 + lv;
-    *n_eq = hs.n_equal + ev;
-    return BQ_OK;
-}
-
 // bq_partition_inplace: three-way in place with O(#CTAs * T) workspace —
-// [< p | >= p] then, if keys equal p exist, [= p | > p] on the right part.
+// pass 0 splits [< p | >= p]; pass 1, if keys equal to p exist, splits the
+// right part into [= p | > p].  Each pass: k_ip_setup, k_inplace (block
+// neutralization from both ends), k_ip_plan + k_swap_blocks (leftover blocks
+// into the middle), k_gather3 + k_vsplit + k_gather3 + k_ip_fix (Alg. 3
+// l.29's "remaining elements": head, middle and tail).  All sizes stay on the
+// device; the host reads the two results once at the end.
 template <class KT>
 bq_status run_partition_inplace_ip(typename KT::T *data, size_t n, typename KT::K pk, size_t *split,
                                    size_t *n_equal, void *ws, size_t ws_bytes, cudaStream_t s) {
+    using T = typename KT::T;
+    using Kn = Kernels<KT>;
+    constexpr uint32_t TILE = tile_elems<KT>();
     if (n > 0x7fffffffull) return set_error(BQ_ERR_INVALID_ARGUMENT, "n = %zu exceeds 2^31-1", n);
     if (n > 0 && data == nullptr) return set_error(BQ_ERR_INVALID_ARGUMENT, "NULL data with n > 0");
     if (KT::is_record && !aligned16(data)) return set_error(BQ_ERR_INVALID_ARGUMENT, "records must be 16-byte aligned");
+    if ((uintptr_t)data % sizeof(typename KT::K) != 0)
+        return set_error(BQ_ERR_INVALID_ARGUMENT, "data not aligned to its key size");
     const IpLayout<KT> L = make_ip_layout<KT>(n);
     if (ws == nullptr || ws_bytes < L.total)
         return set_error(BQ_ERR_WORKSPACE, "workspace %zu B < required %zu B", ws ? ws_bytes : 0, L.total);
     if (((uintptr_t)ws & 255) != 0) return set_error(BQ_ERR_WORKSPACE, "workspace not 256-byte aligned");
     bq_status st = check_device();
     if (st != BQ_OK) return st;
-    char *w = static_cast<char *>(ws);
-    uint64_t nl = 0, ne = 0;
-    if (n) {
-        st = inplace_pass<KT>(data, n, pk, 0, w, L, s, &nl, &ne);
-        if (st != BQ_OK) return st;
-        if (ne) {
-            uint64_t nl2 = 0, ne2 = 0;
-            st = inplace_pass<KT>(data + nl, n - nl, pk, 1, w, L, s, &nl2, &ne2);
-            if (st != BQ_OK) return st;
-            if (nl2 != ne) return set_error(BQ_ERR_CUDA, "in-place partition: equal band %llu != %llu",
-                                           (unsigned long long)nl2, (unsigned long long)ne);
-        }
+    if (n == 0) {
+        if (split) *split = 0;
+        if (n_equal) *n_equal = 0;
+        return BQ_OK;
     }
-    if (split) *split = (size_t)nl;
-    if (n_equal) *n_equal = (size_t)ne;
+    char *w = static_cast<char *>(ws);
+    IpPass *ps = reinterpret_cast<IpPass *>(w + L.passes);
+    uint32_t *leftover = reinterpret_cast<uint32_t *>(w + L.leftover);
+    uint32_t *pairs = reinterpret_cast<uint32_t *>(w + L.pairs);
+    T *s1 = reinterpret_cast<T *>(w + L.s1);
+    T *s2 = reinterpret_cast<T *>(w + L.s2);
+
+    auto kern = k_inplace<KT, Kn::NT, Kn::IPT>;
+    constexpr int smem = inplace_smem_bytes<KT>();
+    static int cap = 0;
+    st = persistent_cap(kern, Kn::NT, smem, &cap);
+    if (st != BQ_OK) return st;
+    uint32_t grid = (uint32_t)cap < IP_GMAX ? (uint32_t)cap : IP_GMAX;
+    const size_t nb_max = n / TILE;
+    if (nb_max < grid) grid = nb_max ? (uint32_t)nb_max : 1;
+    constexpr uint32_t VG = 148 * 4;   // cleanup kernels: grid-stride over <= vmax elements
+    // the compaction lists (E then G) reuse the cleanup buffers s1, s2
+    const uint64_t list_cap = L.vmax * sizeof(T) / sizeof(uint32_t);
+    uint32_t *lists = reinterpret_cast<uint32_t *>(s1);
+    for (int k = 0; k < 2; k++) {
+        IpPass *q = ps + k;
+        k_ip_setup<KT><<<1, 1, 0, s>>>(data, q, k ? ps : nullptr, n, list_cap);
+        BQ_CK_LAUNCH();
+        if (k == 1) {
+            k_eq_scan<KT, 256><<<148 * 8, 256, 0, s>>>(data, q, (uint64_t)pk, lists, lists + list_cap);
+            BQ_CK_LAUNCH();
+            k_eq_swap<KT><<<VG, 256, 0, s>>>(data, q, lists, lists + list_cap);
+            BQ_CK_LAUNCH();
+        }
+        kern<<<grid, Kn::NT, smem, s>>>(InplaceParams<KT>{data, q, (uint64_t)pk, k, leftover});
+        BQ_CK_LAUNCH();
+        k_ip_plan<KT, 1024><<<1, 1024, 0, s>>>(q, leftover, pairs);
+        BQ_CK_LAUNCH();
+        k_swap_blocks<KT, Kn::NT, Kn::IPT><<<grid, Kn::NT, 0, s>>>(data, q, pairs);
+        BQ_CK_LAUNCH();
+        k_gather3<KT><<<VG, 256, 0, s>>>(data, s1, q, 0);
+        BQ_CK_LAUNCH();
+        k_vsplit<KT, Kn::NT, Kn::IPT><<<VG, Kn::NT, 0, s>>>(s1, s2, q, (uint64_t)pk, k);
+        BQ_CK_LAUNCH();
+        k_gather3<KT><<<VG, 256, 0, s>>>(data, s2, q, 1);
+        BQ_CK_LAUNCH();
+        k_ip_fix<KT, 256><<<1, 256, 0, s>>>(data, q);
+        BQ_CK_LAUNCH();
+    }
+    IpPass h[2];
+    BQ_CK(cudaMemcpyAsync(h, ps, sizeof h, cudaMemcpyDeviceToHost, s));
+    BQ_CK(cudaStreamSynchronize(s));
+    if (h[1].compact && (h[1].cnt_eq != h[1].cnt_gt))
+        return set_error(BQ_ERR_CUDA, "in-place partition: equal band lists %llu != %llu",
+                         (unsigned long long)h[1].cnt_eq, (unsigned long long)h[1].cnt_gt);
+    if (h[1].active && h[1].n_left - h[0].n_left != h[0].n_eq)
+        return set_error(BQ_ERR_CUDA, "in-place partition: equal band %llu != %llu",
+                         (unsigned long long)(h[1].n_left - h[0].n_left), (unsigned long long)h[0].n_eq);
+    if (split) *split = (size_t)h[0].n_left;
+    if (n_equal) *n_equal = (size_t)h[0].n_eq;
     return BQ_OK;
 }
 

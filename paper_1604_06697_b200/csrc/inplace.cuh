@@ -22,43 +22,78 @@
 
 namespace bq {
 
+constexpr uint32_t IP_GMAX = 148 * 8;   // bound on the resident k_inplace CTAs (and so on the leftovers)
+
 // claim-word bias: lo and hi start at IP_BIAS and IP_BIAS + #blocks
 constexpr uint32_t IP_BIAS = 1u << 30;
+constexpr uint32_t IP_NONE = 0xffffffffu;
 
 struct InplaceState {
     unsigned long long claim;        // lo: next left block, hi: end of the right blocks
-    unsigned long long n_equal;      // keys equal to the pivot in the neutralized blocks
+    unsigned long long n_equal;      // keys equal to the pivot, over every block as loaded
+    unsigned long long n_equal_held; // ... of them in the blocks held at the end (the middle)
     uint32_t nleftover;              // blocks a CTA held when its partner side ran out
     uint32_t left_ok;                // blocks claimed from the left (= the meeting point)
-    uint32_t pad[10];
+    uint32_t pad[8];
 };
 static_assert(sizeof(InplaceState) == 64, "InplaceState layout");
+
+// One in-place pass over data[off, off + len), device-resident from set-up
+// (k_ip_setup) to result (k_ip_fix): the host launches the whole sequence
+// without reading anything back.
+struct IpPass {
+    InplaceState st;
+    unsigned long long off, len, h;      // the range and its head (< 16 bytes, to align the blocks)
+    unsigned long long o1, n1, o2, tail; // cleanup ranges, relative to off: middle [o1, o1+n1), tail [o2, len)
+    unsigned long long v;                // elements the cleanup partitions: h + n1 + tail
+    unsigned long long lcur, rcur, ev;   // k_vsplit: left / right cursors, keys equal to p
+    unsigned long long n_left, n_eq;     // results: end of the left part (absolute), keys equal to p
+    unsigned long long cnt_eq, cnt_gt;   // compaction (pass 1): keys = p past the band, keys > p inside it
+    uint32_t nb, active, npairs, compact;
+};
 
 template <class KT>
 struct InplaceParams {
     using T = typename KT::T;
-    T *base;                 // range start (any alignment of the element type)
-    uint32_t nblk;           // full blocks in the range
+    T *data;                 // the caller's array
+    IpPass *ps;              // this pass
     uint64_t pivot;          // pivot key (KT::K)
     int mode;                // 0: left <=> key < p; 1: left <=> key <= p
-    InplaceState *st;
     uint32_t *leftover;      // [2 * k]: block index, side (0 left, 1 right)
 };
 
+// Three block buffers: the left block, the right block and a spare that the
+// next block of the side about to be neutralized streams into (TMA) while
+// the current pair is rearranged.  Offsets buffers belong to the sides.
 template <class KT, int NT, int IPT>
 struct InplaceSmem {
     using T = typename KT::T;
     static constexpr int TILE = NT * IPT;
     static constexpr int NW = NT / 32;
-    T blk[2][TILE];                   // [0]: left block, [1]: right block
-    uint16_t off[2][TILE];            // offsets buffers of their misplaced elements
+    alignas(128) T buf[3][TILE];
+    uint16_t off[2][TILE];            // offsets buffers of the misplaced elements (Alg. 3 offsets_L/R)
+    uint64_t bar[3];                  // TMA completion, one per buffer
     uint32_t wsum[NW];
-    uint32_t idx[2], start[2], num[2], done[2];
+    uint32_t blk[3];                  // block index held by each buffer
+    uint32_t slot[2];                 // buffer of each side (3: the side is finished)
+    uint32_t spare;
+    uint32_t start[2], num[2], dirty[2], fresh[2];
 };
 
 template <class KT>
 constexpr int inplace_smem_bytes() {
     return (int)sizeof(InplaceSmem<KT, Tune<KT>::PART_THREADS, Tune<KT>::PART_IPT>);
+}
+
+// one fetch-and-add on the packed word decides a claim; a failed claim moves
+// lo past hi (or hi below lo), which keeps failing — IP_BIAS keeps both
+// halves clear of wrap-around (at most one failure per CTA and side)
+__device__ __forceinline__ uint32_t ip_claim(InplaceState *st, int side) {
+    const unsigned long long old = atomicAdd(&st->claim, side == 0 ? 1ull : 0xffffffff00000000ull);
+    const uint32_t lo = (uint32_t)old, hi = (uint32_t)(old >> 32);
+    if (lo >= hi) return IP_NONE;
+    if (side == 0) atomicAdd(&st->left_ok, 1u);
+    return (side == 0 ? lo : hi - 1) - IP_BIAS;
 }
 
 template <class KT, int NT, int IPT>
@@ -67,54 +102,77 @@ __global__ void __launch_bounds__(NT) k_inplace(InplaceParams<KT> P) {
     using K = typename KT::K;
     using SM = InplaceSmem<KT, NT, IPT>;
     constexpr uint32_t TILE = SM::TILE, NW = SM::NW;
+    constexpr uint32_t W = sizeof(T);
+    constexpr uint32_t BYTES = TILE * W;
+    constexpr uint32_t VW = W >= 16 ? 1 : 16 / W;   // keys per 16-byte vector
     static_assert(TILE <= 65536, "16-bit offsets");
+    static_assert(IPT <= 32 && IPT % VW == 0, "misplaced flags in one word");
+    static_assert(BYTES % 16 == 0, "bulk copies move 16-byte multiples");
     extern __shared__ __align__(128) unsigned char smraw[];
     SM &sm = *reinterpret_cast<SM *>(smraw);
     const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const K pk = (K)P.pivot;
+    if (!P.ps->active) return;
+    InplaceState *const st = &P.ps->st;
+    T *const base = P.data + P.ps->off + P.ps->h;   // 16-byte aligned first block
+
     if (tid == 0) {
-        sm.idx[0] = sm.idx[1] = 0xffffffffu;
-        sm.done[0] = sm.done[1] = 0;
-        sm.num[0] = sm.num[1] = 0;
+        for (int b = 0; b < 3; b++) mbar_init(&sm.bar[b], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        fence_proxy_async_smem();
+        sm.spare = 2;
+        for (int side = 0; side < 2; side++) {
+            const uint32_t got = ip_claim(st, side);
+            sm.dirty[side] = 0;
+            sm.num[side] = sm.start[side] = 0;
+            if (got == IP_NONE) {
+                sm.slot[side] = 3;
+                sm.fresh[side] = 0;
+            } else {
+                sm.slot[side] = side;
+                sm.blk[side] = got;
+                sm.fresh[side] = 1;
+                mbar_arrive_expect_tx(&sm.bar[side], BYTES);
+                tma_load_1d(sm.buf[side], base + (uint64_t)got * TILE, BYTES, &sm.bar[side]);
+            }
+        }
     }
     __syncthreads();
 
+    uint32_t phase = 0;   // mbarrier parity per buffer (bit b)
     for (;;) {
-        // refill the empty side(s): claim, load, scan (Alg. 3 l.5-18)
+        // scan phase of newly arrived blocks (Alg. 3 l.5-18): the offset of
+        // every element is formed, the buffer grows by the misplaced flag
         for (int side = 0; side < 2; side++) {
-            if (sm.idx[side] != 0xffffffffu || sm.done[side]) continue;   // uniform
-            __syncthreads();
-            if (tid == 0) {
-                // one fetch-and-add on the packed word decides the claim; a
-                // failed claim moves lo past hi (or hi below lo), which keeps
-                // failing — IP_BIAS keeps both halves clear of wrap-around
-                // (at most one failure per CTA and side)
-                uint32_t got = 0xffffffffu;
-                const unsigned long long old =
-                    atomicAdd(&P.st->claim, side == 0 ? 1ull : 0xffffffff00000000ull);   // lo += 1 | hi -= 1
-                const uint32_t lo = (uint32_t)old, hi = (uint32_t)(old >> 32);
-                if (lo < hi) {
-                    got = (side == 0 ? lo : hi - 1) - IP_BIAS;
-                    if (side == 0) atomicAdd(&P.st->left_ok, 1u);
+            if (!sm.fresh[side]) continue;   // uniform
+            const uint32_t b = sm.slot[side];
+            mbar_wait(&sm.bar[b], (phase >> b) & 1u);
+            phase ^= 1u << b;
+            const T *blk = sm.buf[b];
+            uint32_t mis = 0, ne = 0;
+            if constexpr (KT::is_record) {
+#pragma unroll
+                for (uint32_t j = 0; j < IPT; j++) {
+                    const K k = KT::key(blk[j * NT + tid]);
+                    const bool left = P.mode ? !(pk < k) : (k < pk);
+                    ne += !(k < pk) && !(pk < k);
+                    mis |= (uint32_t)(side == 0 ? !left : left) << j;
                 }
-                if (got == 0xffffffffu) sm.done[side] = 1;
-                sm.idx[side] = got;
-            }
-            __syncthreads();
-            const uint32_t b = sm.idx[side];
-            if (b == 0xffffffffu) continue;
-            const T *g = P.base + (uint64_t)b * TILE;
-            T x[IPT];
+            } else {
+                const uint4 *v4 = reinterpret_cast<const uint4 *>(blk);
 #pragma unroll
-            for (uint32_t j = 0; j < IPT; j++) x[j] = g[j * NT + tid];   // coalesced
-            // misplaced: on the left side elements that belong right, and vice versa
-            uint32_t mis = 0;
+                for (uint32_t j = 0; j < IPT / VW; j++) {
+                    const uint4 u = v4[j * NT + tid];
+                    T x[VW];
+                    memcpy(x, &u, 16);
 #pragma unroll
-            for (uint32_t j = 0; j < IPT; j++) {
-                const K k = KT::key(x[j]);
-                const bool left = P.mode ? !(pk < k) : (k < pk);
-                mis |= (uint32_t)(side == 0 ? !left : left) << j;
-                sm.blk[side][j * NT + tid] = x[j];
+                    for (uint32_t q = 0; q < VW; q++) {
+                        const K k = KT::key(x[q]);
+                        const bool left = P.mode ? !(pk < k) : (k < pk);
+                        ne += !(k < pk) && !(pk < k);
+                        mis |= (uint32_t)(side == 0 ? !left : left) << (j * VW + q);
+                    }
+                }
             }
             const uint32_t cnt = __popc(mis);
             uint32_t inc = cnt;
@@ -124,6 +182,9 @@ __global__ void __launch_bounds__(NT) k_inplace(InplaceParams<KT> P) {
                 if (lane >= (uint32_t)d) inc += o;
             }
             if (lane == 31) sm.wsum[warp] = inc;
+#pragma unroll
+            for (int d = 16; d > 0; d >>= 1) ne += __shfl_xor_sync(0xffffffffu, ne, d);
+            if (lane == 0 && ne) atomicAdd(&st->n_equal, (unsigned long long)ne);
             __syncthreads();
             uint32_t pre = 0, tot = 0;
 #pragma unroll
@@ -134,108 +195,418 @@ __global__ void __launch_bounds__(NT) k_inplace(InplaceParams<KT> P) {
             }
             uint32_t r = pre + inc - cnt;
 #pragma unroll
-            for (uint32_t j = 0; j < IPT; j++) {
-                // the offset is formed for every element; the buffer grows by the flag
-                if ((mis >> j) & 1) sm.off[side][r] = (uint16_t)(j * NT + tid);
-                r += (mis >> j) & 1;
+            for (uint32_t jj = 0; jj < IPT; jj++) {
+                const uint32_t e = KT::is_record ? jj * NT + tid : ((jj / VW) * NT + tid) * VW + jj % VW;
+                if ((mis >> jj) & 1) sm.off[side][r] = (uint16_t)e;
+                r += (mis >> jj) & 1;
             }
             if (tid == 0) {
                 sm.start[side] = 0;
                 sm.num[side] = tot;
+                sm.dirty[side] = 0;
+                sm.fresh[side] = 0;
             }
             __syncthreads();
         }
-        const bool hl = sm.idx[0] != 0xffffffffu, hr = sm.idx[1] != 0xffffffffu;
-        if (!(hl && hr)) break;   // one side is exhausted (uniform)
+        const uint32_t bL = sm.slot[0], bR = sm.slot[1];
+        if (bL == 3 || bR == 3) break;   // one side is exhausted (uniform)
 
         // rearrangement phase (l.19-21): swap num = min(num_L, num_R) pairs
         const uint32_t nL = sm.num[0], nR = sm.num[1], sL = sm.start[0], sR = sm.start[1];
         const uint32_t num = nL < nR ? nL : nR;
-        for (uint32_t q = tid; q < num; q += NT) {
-            const uint32_t a = sm.off[0][sL + q], c = sm.off[1][sR + q];
-            const T t0 = sm.blk[0][a];
-            sm.blk[0][a] = sm.blk[1][c];
-            sm.blk[1][c] = t0;
-        }
-        __syncthreads();
-        // l.24-27: advance; a side whose buffer ran empty is written back
-        for (int side = 0; side < 2; side++) {
-            const uint32_t left_now = (side == 0 ? nL : nR) - num;
-            if (left_now == 0) {
-                // neutralized: final in place; its keys equal to p are counted
-                // here (the middle blocks are counted by the cleanup)
-                T *g = P.base + (uint64_t)sm.idx[side] * TILE;
-                uint32_t ne = 0;
-#pragma unroll
-                for (uint32_t j = 0; j < IPT; j++) {
-                    const T x = sm.blk[side][j * NT + tid];
-                    const K k = KT::key(x);
-                    ne += !(k < pk) && !(pk < k);
-                    g[j * NT + tid] = x;
-                }
-#pragma unroll
-                for (int d = 16; d > 0; d >>= 1) ne += __shfl_xor_sync(0xffffffffu, ne, d);
-                if (lane == 0 && ne) atomicAdd(&P.st->n_equal, (unsigned long long)ne);
+        const bool e0 = nL == num, e1 = nR == num;   // sides neutralized by this round
+        const int pf = e0 ? 0 : 1;
+        uint32_t pf_blk = IP_NONE;
+        if (tid == 0) {
+            // claim the next block of the side about to be neutralized and
+            // stream it into the spare buffer while the swaps run
+            pf_blk = ip_claim(st, pf);
+            if (pf_blk != IP_NONE) {
+                const uint32_t sp = sm.spare;
+                bulk_wait_read0();   // the spare's last write-back has left shared memory
+                sm.blk[sp] = pf_blk;
+                mbar_arrive_expect_tx(&sm.bar[sp], BYTES);
+                tma_load_1d(sm.buf[sp], base + (uint64_t)pf_blk * TILE, BYTES, &sm.bar[sp]);
             }
         }
+        T *L = sm.buf[bL];
+        T *R = sm.buf[bR];
+        for (uint32_t q = tid; q < num; q += NT) {
+            const uint32_t a = sm.off[0][sL + q], c = sm.off[1][sR + q];
+            const T t0 = L[a];
+            L[a] = R[c];
+            R[c] = t0;
+        }
+        fence_proxy_async_smem();   // the swaps become visible to the bulk stores
         __syncthreads();
         if (tid == 0) {
+            // l.24-27: a neutralized block is final — written back if a swap touched it
+            const uint32_t d0 = sm.dirty[0] | (num > 0), d1 = sm.dirty[1] | (num > 0);
+            if (e0 && d0) tma_store_1d(base + (uint64_t)sm.blk[bL] * TILE, L, BYTES);
+            if (e1 && d1) tma_store_1d(base + (uint64_t)sm.blk[bR] * TILE, R, BYTES);
+            bulk_commit();
+            sm.dirty[0] = d0;
+            sm.dirty[1] = d1;
             for (int side = 0; side < 2; side++) {
-                sm.num[side] -= num;
                 sm.start[side] += num;
-                if (sm.num[side] == 0) sm.idx[side] = 0xffffffffu;
+                sm.num[side] -= num;
+            }
+            const uint32_t old = sm.slot[pf];
+            if (pf_blk != IP_NONE) {
+                sm.slot[pf] = sm.spare;
+                sm.fresh[pf] = 1;
+            } else {
+                sm.slot[pf] = 3;
+            }
+            sm.spare = old;
+            if (pf == 0 && e1) {
+                // both sides neutralized: the right one refills in place
+                const uint32_t got = pf_blk != IP_NONE ? ip_claim(st, 1) : IP_NONE;
+                if (got == IP_NONE) {
+                    sm.slot[1] = 3;
+                } else {
+                    bulk_wait_read0();
+                    sm.blk[bR] = got;
+                    sm.fresh[1] = 1;
+                    mbar_arrive_expect_tx(&sm.bar[bR], BYTES);
+                    tma_load_1d(R, base + (uint64_t)got * TILE, BYTES, &sm.bar[bR]);
+                }
             }
         }
         __syncthreads();
     }
-    // the block still held (at most one) goes back as is and is listed
+    // the block still held (at most one) is the cleanup's: written back if
+    // modified, its keys equal to p recounted there
     for (int side = 0; side < 2; side++) {
-        const uint32_t b = sm.idx[side];
-        if (b == 0xffffffffu) continue;
-        T *g = P.base + (uint64_t)b * TILE;
+        const uint32_t b = sm.slot[side];
+        if (b == 3) continue;
+        const T *blk = sm.buf[b];
+        uint32_t ne = 0;
 #pragma unroll
-        for (uint32_t j = 0; j < IPT; j++) g[j * NT + tid] = sm.blk[side][j * NT + tid];
+        for (uint32_t j = 0; j < IPT; j++) {
+            const K k = KT::key(blk[j * NT + tid]);
+            ne += !(k < pk) && !(pk < k);
+        }
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) ne += __shfl_xor_sync(0xffffffffu, ne, d);
+        if (lane == 0 && ne) atomicAdd(&st->n_equal_held, (unsigned long long)ne);
         if (tid == 0) {
-            const uint32_t k = atomicAdd(&P.st->nleftover, 1u);
-            P.leftover[2 * k] = b;
+            if (sm.dirty[side]) tma_store_1d(base + (uint64_t)sm.blk[b] * TILE, blk, BYTES);
+            bulk_commit();
+            const uint32_t k = atomicAdd(&st->nleftover, 1u);
+            P.leftover[2 * k] = sm.blk[b];
             P.leftover[2 * k + 1] = side;
         }
     }
+    if (tid == 0) bulk_wait0();
 }
 
-// block pairs (a, b) of the range swap their contents (one CTA per pair)
-template <class KT, int NT, int IPT>
-__global__ void __launch_bounds__(NT) k_swap_blocks(typename KT::T *base, const uint32_t *pairs) {
+// ---- the pass's set-up and cleanup (Alg. 3 l.29), all on the device ----------
+
+// the range of pass k: [0, n) for pass 0; for pass 1 (the equal band) the
+// right part of pass 0, if pass 0 met keys equal to p
+template <class KT>
+__global__ void k_ip_setup(const typename KT::T *data, IpPass *ps, const IpPass *prev, uint64_t n,
+                           uint64_t list_cap) {
     using T = typename KT::T;
-    constexpr uint32_t TILE = NT * IPT;
-    T *a = base + (uint64_t)pairs[2 * blockIdx.x] * TILE;
-    T *b = base + (uint64_t)pairs[2 * blockIdx.x + 1] * TILE;
-    for (uint32_t j = threadIdx.x; j < TILE; j += NT) {
-        const T x = a[j];
-        a[j] = b[j];
-        b[j] = x;
+    constexpr uint32_t TILE = tile_elems<KT>();
+    IpPass q;
+    memset(&q, 0, sizeof q);
+    if (prev == nullptr) {
+        q.off = 0;
+        q.active = n > 0;
+    } else {
+        // the equal band: by compaction when its size fits the lists,
+        // otherwise by a second block pass with mode 1 (left <=> key <= p)
+        q.off = prev->n_left;
+        const bool any = prev->active && prev->n_eq > 0;
+        q.compact = any && prev->n_eq <= list_cap;
+        q.active = any && !q.compact;
+        q.n_eq = prev->n_eq;
+    }
+    q.len = n - q.off;
+    const uint64_t mis16 = (uintptr_t)(data + q.off) & 15;
+    uint64_t h = mis16 ? (16 - mis16) / sizeof(T) : 0;
+    q.h = h < q.len ? h : q.len;
+    q.nb = (uint32_t)((q.len - q.h) / TILE);
+    q.st.claim = ((unsigned long long)(IP_BIAS + q.nb) << 32) | IP_BIAS;
+    q.n_left = q.compact ? q.off + q.n_eq : q.off;
+    *ps = q;
+}
+
+// where the leftover blocks go: the left ones to [X - a, X), the right ones
+// to [X, X + c), each swapping with a neutralized block found there
+template <class KT, int NT>
+__global__ void __launch_bounds__(NT) k_ip_plan(IpPass *ps, const uint32_t *leftover, uint32_t *pairs) {
+    constexpr uint32_t TILE = tile_elems<KT>();
+    __shared__ uint8_t win[IP_GMAX];
+    __shared__ uint32_t cnt[2], nout[2], nin[2];
+    const uint32_t tid = threadIdx.x;
+    if (!ps->active) return;
+    const uint32_t X = ps->st.left_ok, k = ps->st.nleftover;
+    if (tid < 2) cnt[tid] = nout[tid] = nin[tid] = 0;
+    for (uint32_t j = tid; j < IP_GMAX; j += NT) win[j] = 0;
+    __syncthreads();
+    for (uint32_t i = tid; i < k; i += NT) atomicAdd(&cnt[leftover[2 * i] < X ? 0 : 1], 1u);
+    __syncthreads();
+    const uint32_t a = cnt[0], c = cnt[1];
+    uint32_t *pl = pairs, *pr = pairs + 2 * IP_GMAX;
+    for (uint32_t i = tid; i < k; i += NT) {
+        const uint32_t b = leftover[2 * i];
+        if (b < X) {
+            if (b >= X - a) win[b - (X - a)] = 1;
+            else pl[2 * atomicAdd(&nout[0], 1u)] = b;
+        } else {
+            if (b < X + c) win[a + (b - X)] = 1;
+            else pr[2 * atomicAdd(&nout[1], 1u)] = b;
+        }
+    }
+    __syncthreads();
+    for (uint32_t j = tid; j < a + c; j += NT) {
+        if (win[j]) continue;
+        if (j < a) pl[2 * atomicAdd(&nin[0], 1u) + 1] = X - a + j;
+        else pr[2 * atomicAdd(&nin[1], 1u) + 1] = X + (j - a);
+    }
+    __syncthreads();
+    const uint32_t mL = nout[0], mR = nout[1];
+    for (uint32_t i = tid; i < 2 * mR; i += NT) pairs[2 * mL + i] = pr[i];   // right pairs after the left ones
+    if (tid == 0) {
+        ps->npairs = mL + mR;
+        ps->o1 = ps->h + (uint64_t)(X - a) * TILE;
+        ps->n1 = (uint64_t)(a + c) * TILE;
+        ps->o2 = ps->h + (uint64_t)ps->nb * TILE;
+        ps->tail = ps->len - ps->o2;
+        ps->v = ps->h + ps->n1 + ps->tail;
     }
 }
 
-// copy two ranges of `base` into one contiguous buffer (dir 0) or back (dir 1)
+// block pairs (a, b) swap their contents
+template <class KT, int NT, int IPT>
+__global__ void __launch_bounds__(NT) k_swap_blocks(typename KT::T *data, const IpPass *ps, const uint32_t *pairs) {
+    using T = typename KT::T;
+    constexpr uint32_t TILE = NT * IPT;
+    if (!ps->active) return;
+    T *base = data + ps->off + ps->h;
+    for (uint32_t q = blockIdx.x; q < ps->npairs; q += gridDim.x) {
+        T *a = base + (uint64_t)pairs[2 * q] * TILE;
+        T *b = base + (uint64_t)pairs[2 * q + 1] * TILE;
+        for (uint32_t j = threadIdx.x; j < TILE; j += NT) {
+            const T x = a[j];
+            a[j] = b[j];
+            b[j] = x;
+        }
+    }
+}
+
+// head, middle and tail of the range into one contiguous buffer (dir 0) or back (dir 1)
 template <class KT>
-__global__ void k_gather2(typename KT::T *base, typename KT::T *buf, uint64_t o1, uint64_t n1, uint64_t o2,
-                          uint64_t n2, int dir) {
-    const uint64_t n = n1 + n2;
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t g = i < n1 ? o1 + i : o2 + (i - n1);
+__global__ void k_gather3(typename KT::T *data, typename KT::T *buf, const IpPass *ps, int dir) {
+    if (!ps->active) return;
+    typename KT::T *base = data + ps->off;
+    const uint64_t h = ps->h, n1 = ps->n1, o1 = ps->o1, o2 = ps->o2, v = ps->v;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < v; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t g = i < h ? i : i < h + n1 ? o1 + (i - h) : o2 + (i - h - n1);
         if (dir == 0) buf[i] = base[g];
         else base[g] = buf[i];
     }
 }
 
-// swap base[a + i] <-> base[b + i] for i < len (the spill of the middle's left part)
-template <class KT>
-__global__ void k_swap_ranges(typename KT::T *base, uint64_t a, uint64_t b, uint64_t len) {
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < len; i += (uint64_t)gridDim.x * blockDim.x) {
-        const typename KT::T x = base[a + i];
+// two-way split of the gathered elements into [left | right] (their order is
+// free): chunks of NT*IPT, one cursor claim per side and chunk
+template <class KT, int NT, int IPT>
+__global__ void __launch_bounds__(NT) k_vsplit(const typename KT::T *src, typename KT::T *dst, IpPass *ps,
+                                                uint64_t pivot, int mode) {
+    using T = typename KT::T;
+    using K = typename KT::K;
+    constexpr uint32_t CH = NT * IPT, NW = NT / 32;
+    __shared__ uint32_t wl[NW], we[NW];
+    __shared__ unsigned long long lb, rb;
+    const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (!ps->active) return;
+    const uint64_t v = ps->v;
+    const K pk = (K)pivot;
+    for (uint64_t c0 = (uint64_t)blockIdx.x * CH; c0 < v; c0 += (uint64_t)gridDim.x * CH) {
+        T x[IPT];
+        uint32_t lf = 0, nl = 0, nr = 0, ne = 0;
+#pragma unroll
+        for (uint32_t j = 0; j < IPT; j++) {
+            const uint64_t i = c0 + j * NT + tid;
+            if (i < v) {
+                x[j] = src[i];
+                const K k = KT::key(x[j]);
+                const bool left = mode ? !(pk < k) : (k < pk);
+                lf |= (uint32_t)left << j;
+                nl += left;
+                nr += !left;
+                ne += !(k < pk) && !(pk < k);
+            }
+        }
+        // inclusive warp scans of the left / right counts
+        uint32_t il = nl, ir = nr;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t ol = __shfl_up_sync(0xffffffffu, il, d), orr = __shfl_up_sync(0xffffffffu, ir, d);
+            if (lane >= (uint32_t)d) { il += ol; ir += orr; }
+        }
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) ne += __shfl_xor_sync(0xffffffffu, ne, d);
+        if (lane == 31) { wl[warp] = il; we[warp] = ir; }
+        __syncthreads();
+        uint32_t pl = 0, pr = 0, tl = 0, tr = 0;
+#pragma unroll
+        for (uint32_t w2 = 0; w2 < NW; w2++) {
+            pl += w2 < warp ? wl[w2] : 0;
+            pr += w2 < warp ? we[w2] : 0;
+            tl += wl[w2];
+            tr += we[w2];
+        }
+        if (lane == 0 && ne) atomicAdd(&ps->ev, (unsigned long long)ne);
+        if (tid == 0) {
+            lb = tl ? atomicAdd(&ps->lcur, (unsigned long long)tl) : 0;
+            rb = tr ? atomicAdd(&ps->rcur, (unsigned long long)tr) : 0;
+        }
+        __syncthreads();
+        uint64_t ol = lb + pl + il - nl, orr = rb + pr + ir - nr;
+#pragma unroll
+        for (uint32_t j = 0; j < IPT; j++) {
+            const uint64_t i = c0 + j * NT + tid;
+            if (i < v) {
+                if ((lf >> j) & 1) dst[ol++] = x[j];
+                else dst[v - 1 - orr++] = x[j];
+            }
+        }
+        __syncthreads();   // wl/we/lb/rb are reused by the next chunk
+    }
+}
+
+// the split lands in the head, middle and tail positions in that order; two
+// cases leave right keys inside the left part, fixed by one range swap:
+// the head ends in right keys while left blocks follow (lv < h), or the left
+// part spills from the middle into the tail past right blocks.  Then the
+// pass's results.
+template <class KT, int NT>
+__global__ void __launch_bounds__(NT) k_ip_fix(typename KT::T *data, IpPass *ps) {
+    using T = typename KT::T;
+    if (!ps->active) return;
+    T *base = data + ps->off;
+    const uint64_t lv = ps->lcur, h = ps->h, o1 = ps->o1, n1 = ps->n1, o2 = ps->o2;
+    uint64_t a = 0, b = 0, e = 0;
+    if (lv < h) {
+        if (o1 > h) { e = h - lv; a = lv; b = o1 - e; }
+    } else if (lv - h > n1 && o1 + n1 < o2) {
+        e = lv - h - n1; a = o1 + n1; b = o2;
+    }
+    for (uint64_t i = threadIdx.x; i < e; i += NT) {
+        const T x = base[a + i];
         base[a + i] = base[b + i];
         base[b + i] = x;
+    }
+    if (threadIdx.x == 0) {
+        ps->n_left = ps->off + o1 - h + lv;
+        ps->n_eq = ps->st.n_equal - ps->st.n_equal_held + ps->ev;
+    }
+}
+
+// ---- the equal band by compaction ---------------------------------------------
+// The right part R = data[off, off + len) of pass 0 holds only keys >= p, and
+// n_eq of them equal p.  The band is R's first n_eq positions: every key > p
+// there (list G) swaps with a key = p found past it (list E); |G| = |E|.
+// One read of R, then 2|G| element moves.
+
+// append the positions of this thread's hits to a list, one atomic per warp
+__device__ __forceinline__ void warp_append(uint32_t cnt, uint32_t lane, unsigned long long *ctr, uint32_t *list,
+                                            const uint32_t *pos) {
+    uint32_t inc = cnt;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= (uint32_t)d) inc += o;
+    }
+    const uint32_t tot = __shfl_sync(0xffffffffu, inc, 31);
+    unsigned long long b = 0;
+    if (lane == 31 && tot) b = atomicAdd(ctr, (unsigned long long)tot);
+    b = __shfl_sync(0xffffffffu, b, 31);
+    const uint64_t r = b + inc - cnt;
+    for (uint32_t j = 0; j < cnt; j++) list[r + j] = pos[j];
+}
+
+template <class KT, int NT>
+__global__ void __launch_bounds__(NT) k_eq_scan(const typename KT::T *data, IpPass *ps, uint64_t pivot, uint32_t *E,
+                                                 uint32_t *G) {
+    using T = typename KT::T;
+    using K = typename KT::K;
+    if (!ps->compact) return;
+    const K pk = (K)pivot;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t off = ps->off, len = ps->len, band = ps->n_eq;
+    const T *R = data + off;
+    if constexpr (KT::is_record) {
+        const uint64_t step = (uint64_t)gridDim.x * NT;
+        for (uint64_t i0 = (uint64_t)blockIdx.x * NT; i0 < len; i0 += step) {
+            const uint64_t i = i0 + threadIdx.x;
+            uint32_t ce = 0, cg = 0, pe[1], pg[1];
+            if (i < len) {
+                const K k = KT::key(R[i]);
+                const bool eq = !(k < pk) && !(pk < k);
+                if (i < band && !eq) pg[cg++] = (uint32_t)i;
+                if (i >= band && eq) pe[ce++] = (uint32_t)i;
+            }
+            if (__any_sync(0xffffffffu, ce | cg)) {
+                warp_append(ce, lane, &ps->cnt_eq, E, pe);
+                warp_append(cg, lane, &ps->cnt_gt, G, pg);
+            }
+        }
+    } else {
+        // 16-byte units from the aligned address at or below R
+        constexpr uint32_t W = sizeof(T), U = 16 / W, UNR = 4;
+        const uintptr_t a0 = (uintptr_t)R & ~(uintptr_t)15;
+        const int64_t skew = (int64_t)(((uintptr_t)R - a0) / W);   // elements of the first unit before R
+        const uint64_t units = (len + skew + U - 1) / U;
+        const uint4 *V = reinterpret_cast<const uint4 *>(a0);
+        const uint64_t step = (uint64_t)gridDim.x * NT * UNR;
+        for (uint64_t u0 = (uint64_t)blockIdx.x * NT * UNR; u0 < units; u0 += step) {
+            uint4 x[UNR];
+#pragma unroll
+            for (uint32_t r = 0; r < UNR; r++) {
+                const uint64_t u = u0 + r * NT + threadIdx.x;
+                x[r] = u < units ? __ldcs(V + u) : make_uint4(0, 0, 0, 0);
+            }
+            uint32_t ce = 0, cg = 0, pe[U * UNR], pg[U * UNR];
+#pragma unroll
+            for (uint32_t r = 0; r < UNR; r++) {
+                const uint64_t u = u0 + r * NT + threadIdx.x;
+                T e[U];
+                memcpy(e, &x[r], 16);
+#pragma unroll
+                for (uint32_t q = 0; q < U; q++) {
+                    const int64_t i = (int64_t)(u * U + q) - skew;
+                    if (u < units && i >= 0 && (uint64_t)i < len) {
+                        const K k = KT::key(e[q]);
+                        const bool eq = !(k < pk) && !(pk < k);
+                        if ((uint64_t)i < band && !eq) pg[cg++] = (uint32_t)i;
+                        if ((uint64_t)i >= band && eq) pe[ce++] = (uint32_t)i;
+                    }
+                }
+            }
+            if (__any_sync(0xffffffffu, ce | cg)) {
+                warp_append(ce, lane, &ps->cnt_eq, E, pe);
+                warp_append(cg, lane, &ps->cnt_gt, G, pg);
+            }
+        }
+    }
+}
+
+template <class KT>
+__global__ void k_eq_swap(typename KT::T *data, const IpPass *ps, const uint32_t *E, const uint32_t *G) {
+    using T = typename KT::T;
+    if (!ps->compact) return;
+    T *R = data + ps->off;
+    const uint64_t m = ps->cnt_eq < ps->cnt_gt ? ps->cnt_eq : ps->cnt_gt;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
+        T *a = R + E[i], *b = R + G[i];
+        const T x = *a;
+        *a = *b;
+        *b = x;
     }
 }
 

@@ -147,3 +147,43 @@ def test_inplace_invalid_arguments(B):
     small = torch.empty(16, dtype=torch.uint8, device="cuda")
     with pytest.raises(Exception):
         B.bq_partition_inplace(torch.zeros(1 << 16, dtype=torch.int32, device="cuda"), 0, ws=small)
+
+
+@pytest.mark.parametrize("kind,offset", [("i32", 1), ("i32", 2), ("i32", 3), ("u64", 1), ("f64", 1)])
+def test_inplace_unaligned_start(B, kind, offset):
+    """A range that does not start on 16 bytes: the head before the first
+    aligned block goes to the cleanup (with every lv < head / lv >= head case
+    of the final fix-up: pivots at the minimum, inside, and above)."""
+    for n in [2, offset + 1, 5 * TILE[kind] + 3, 301 * TILE[kind] + 9]:
+        a = make(kind, n, seed=n + offset, dist="dups")
+        srt = np.sort(keys_of(a))
+        for p in [srt[0], srt[len(srt) // 2], srt[-1]]:
+            pv = float(p) if kind == "f64" else int(p)
+            t = to_dev(a, offset=offset)
+            split, neq = B.bq_partition_inplace(t, pv)
+            _, s_o, e_o = oracle.partition(a, pv)
+            assert (split, neq) == (s_o, e_o)
+            got = to_host(t, a)
+            k, pk = _key(kind, got), _pk(kind, pv)
+            assert (k[:split] < pk).all() and (k[split:split + neq] == pk).all() and (k[split + neq:] > pk).all()
+            assert np.array_equal(np.sort(_key(kind, got)), np.sort(_key(kind, a)))
+
+
+@pytest.mark.parametrize("kind,n", [("i32", 1 << 25), ("u64", 1 << 24), ("f64", 1 << 24), ("rec32", 1 << 22)])
+@pytest.mark.parametrize("nvals", [4, 64])
+def test_inplace_equal_band_both_ways(B, kind, n, nvals):
+    """The equal band is formed by compaction when it fits the cleanup
+    lists, otherwise by a second block pass (mode 1: left <=> key <= p):
+    4 distinct keys puts n/4 keys in the band (> the list capacity, second
+    pass), 64 puts n/64 (compaction)."""
+    a = make(kind, n, seed=nvals)
+    if kind == "rec32":
+        a[:, 0] = a[:, 0] % np.uint64(nvals)
+    elif kind == "f64":
+        a = np.floor(a * nvals / 2) / nvals
+    else:
+        a = (a % nvals).astype(a.dtype)
+    k = keys_of(a)
+    p = np.sort(k)[len(k) // 2]
+    split, neq = check(B, kind, a, float(p) if kind == "f64" else int(p))
+    assert neq > n // (2 * nvals)

@@ -18,10 +18,14 @@ import paper_1604_06697_b200 as bq
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--reps", type=int, default=5)
+ap.add_argument("--kinds", default="i32,u64,f64,rec32")
+ap.add_argument("--only", default="", help="time just this variant")
 a = ap.parse_args()
 
 cases = [("i32", 1 << 28), ("u64", 1 << 27), ("f64", 1 << 27), ("rec32", 1 << 25)]
 for kind, n in cases:
+    if kind not in a.kinds.split(","):
+        continue
     if kind == "i32":
         h = torch.from_numpy(bqgen.i32_full(n, 1))
     elif kind == "u64":
@@ -55,11 +59,12 @@ for kind, n in cases:
         ms.sort()
         return ms[len(ms) // 2]
 
-    res = {
-        "inplace": timed(lambda: bq.bq_partition_inplace(t, pv, ws=iws)),
-        "pass_fast": timed(lambda: bq.bq_partition_pass(t, dst, pv, counts, ordered=False, ws=ws)),
-        "pass_ordered": timed(lambda: bq.bq_partition_pass(t, dst, pv, counts, ordered=True, ws=ws)),
+    fns = {
+        "inplace": lambda: bq.bq_partition_inplace(t, pv, ws=iws),
+        "pass_fast": lambda: bq.bq_partition_pass(t, dst, pv, counts, ordered=False, ws=ws),
+        "pass_ordered": lambda: bq.bq_partition_pass(t, dst, pv, counts, ordered=True, ws=ws),
     }
+    res = {name: timed(fn) for name, fn in fns.items() if not a.only or name == a.only}
     for name, ms in res.items():
         print(json.dumps({"kind": kind, "n": n, "variant": name, "ms": round(ms, 4),
                           "tb_s_rw": round(2 * nbytes / ms / 1e9, 3),
