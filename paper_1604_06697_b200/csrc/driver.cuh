@@ -382,7 +382,7 @@ IpLayout<KT> make_ip_layout(size_t n) {
 // pass 0 splits [< p | >= p]; pass 1, if keys equal to p exist, splits the
 // right part into [= p | > p].  Each pass: k_ip_setup, k_inplace (block
 // neutralization from both ends), k_ip_plan + k_swap_blocks (leftover blocks
-// into the middle), k_gather3 + k_vsplit + k_gather3 + k_ip_fix (Alg. 3
+// into the middle), k_vsplit + k_gather3 + k_ip_fix (Alg. 3
 // l.29's "remaining elements": head, middle and tail).  All sizes stay on the
 // device; the host reads the two results once at the end.
 template <class KT>
@@ -442,9 +442,7 @@ bq_status run_partition_inplace_ip(typename KT::T *data, size_t n, typename KT::
         BQ_CK_LAUNCH();
         k_swap_blocks<KT, Kn::NT, Kn::IPT><<<grid, Kn::NT, 0, s>>>(data, q, pairs);
         BQ_CK_LAUNCH();
-        k_gather3<KT><<<VG, 256, 0, s>>>(data, s1, q, 0);
-        BQ_CK_LAUNCH();
-        k_vsplit<KT, Kn::NT, Kn::IPT><<<VG, Kn::NT, 0, s>>>(s1, s2, q, (uint64_t)pk, k);
+        k_vsplit<KT, Kn::NT, Kn::IPT><<<VG, Kn::NT, 0, s>>>(data, s2, q, (uint64_t)pk, k);
         BQ_CK_LAUNCH();
         k_gather3<KT><<<VG, 256, 0, s>>>(data, s2, q, 1);
         BQ_CK_LAUNCH();

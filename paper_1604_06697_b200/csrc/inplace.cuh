@@ -398,7 +398,7 @@ __global__ void __launch_bounds__(NT) k_swap_blocks(typename KT::T *data, const 
     }
 }
 
-// head, middle and tail of the range into one contiguous buffer (dir 0) or back (dir 1)
+// the buffer back into the head, middle and tail positions (dir 1), or the reverse
 template <class KT>
 __global__ void k_gather3(typename KT::T *data, typename KT::T *buf, const IpPass *ps, int dir) {
     if (!ps->active) return;
@@ -411,10 +411,10 @@ __global__ void k_gather3(typename KT::T *data, typename KT::T *buf, const IpPas
     }
 }
 
-// two-way split of the gathered elements into [left | right] (their order is
-// free): chunks of NT*IPT, one cursor claim per side and chunk
+// two-way split of the head, middle and tail into [left | right] in a buffer
+// (their order is free): chunks of NT*IPT, one cursor claim per side and chunk
 template <class KT, int NT, int IPT>
-__global__ void __launch_bounds__(NT) k_vsplit(const typename KT::T *src, typename KT::T *dst, IpPass *ps,
+__global__ void __launch_bounds__(NT) k_vsplit(const typename KT::T *data, typename KT::T *dst, IpPass *ps,
                                                 uint64_t pivot, int mode) {
     using T = typename KT::T;
     using K = typename KT::K;
@@ -423,7 +423,8 @@ __global__ void __launch_bounds__(NT) k_vsplit(const typename KT::T *src, typena
     __shared__ unsigned long long lb, rb;
     const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (!ps->active) return;
-    const uint64_t v = ps->v;
+    const uint64_t v = ps->v, h = ps->h, n1 = ps->n1, o1 = ps->o1, o2 = ps->o2;
+    const T *src = data + ps->off;   // gathered on the fly: head, middle, tail
     const K pk = (K)pivot;
     for (uint64_t c0 = (uint64_t)blockIdx.x * CH; c0 < v; c0 += (uint64_t)gridDim.x * CH) {
         T x[IPT];
@@ -432,7 +433,7 @@ __global__ void __launch_bounds__(NT) k_vsplit(const typename KT::T *src, typena
         for (uint32_t j = 0; j < IPT; j++) {
             const uint64_t i = c0 + j * NT + tid;
             if (i < v) {
-                x[j] = src[i];
+                x[j] = src[i < h ? i : i < h + n1 ? o1 + (i - h) : o2 + (i - h - n1)];
                 const K k = KT::key(x[j]);
                 const bool left = mode ? !(pk < k) : (k < pk);
                 lf |= (uint32_t)left << j;
@@ -513,9 +514,12 @@ __global__ void __launch_bounds__(NT) k_ip_fix(typename KT::T *data, IpPass *ps)
 // there (list G) swaps with a key = p found past it (list E); |G| = |E|.
 // One read of R, then 2|G| element moves.
 
-// append the positions of this thread's hits to a list, one atomic per warp
-__device__ __forceinline__ void warp_append(uint32_t cnt, uint32_t lane, unsigned long long *ctr, uint32_t *list,
-                                            const uint32_t *pos) {
+// append this thread's hits (bit b of `mask` <-> position pos0(b)) to a list,
+// one atomic per warp
+template <class F>
+__device__ __forceinline__ void warp_append(uint32_t mask, uint32_t lane, unsigned long long *ctr, uint32_t *list,
+                                            F pos_of) {
+    const uint32_t cnt = __popc(mask);
     uint32_t inc = cnt;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
@@ -523,11 +527,16 @@ __device__ __forceinline__ void warp_append(uint32_t cnt, uint32_t lane, unsigne
         if (lane >= (uint32_t)d) inc += o;
     }
     const uint32_t tot = __shfl_sync(0xffffffffu, inc, 31);
+    if (tot == 0) return;
     unsigned long long b = 0;
-    if (lane == 31 && tot) b = atomicAdd(ctr, (unsigned long long)tot);
+    if (lane == 31) b = atomicAdd(ctr, (unsigned long long)tot);
     b = __shfl_sync(0xffffffffu, b, 31);
-    const uint64_t r = b + inc - cnt;
-    for (uint32_t j = 0; j < cnt; j++) list[r + j] = pos[j];
+    uint64_t r = b + inc - cnt;
+    while (mask) {
+        const uint32_t bit = __ffs(mask) - 1;
+        mask &= mask - 1;
+        list[r++] = pos_of(bit);
+    }
 }
 
 template <class KT, int NT>
@@ -544,21 +553,22 @@ __global__ void __launch_bounds__(NT) k_eq_scan(const typename KT::T *data, IpPa
         const uint64_t step = (uint64_t)gridDim.x * NT;
         for (uint64_t i0 = (uint64_t)blockIdx.x * NT; i0 < len; i0 += step) {
             const uint64_t i = i0 + threadIdx.x;
-            uint32_t ce = 0, cg = 0, pe[1], pg[1];
+            uint32_t me = 0, mg = 0;
             if (i < len) {
                 const K k = KT::key(R[i]);
                 const bool eq = !(k < pk) && !(pk < k);
-                if (i < band && !eq) pg[cg++] = (uint32_t)i;
-                if (i >= band && eq) pe[ce++] = (uint32_t)i;
+                mg = i < band && !eq;
+                me = i >= band && eq;
             }
-            if (__any_sync(0xffffffffu, ce | cg)) {
-                warp_append(ce, lane, &ps->cnt_eq, E, pe);
-                warp_append(cg, lane, &ps->cnt_gt, G, pg);
+            if (__any_sync(0xffffffffu, me | mg)) {
+                warp_append(me, lane, &ps->cnt_eq, E, [&](uint32_t) { return (uint32_t)i; });
+                warp_append(mg, lane, &ps->cnt_gt, G, [&](uint32_t) { return (uint32_t)i; });
             }
         }
     } else {
-        // 16-byte units from the aligned address at or below R
-        constexpr uint32_t W = sizeof(T), U = 16 / W, UNR = 4;
+        // 16-byte units from the aligned address at or below R; bit r*U+q of
+        // a mask is key q of the thread's unit r
+        constexpr uint32_t W = sizeof(T), U = 16 / W, UNR = 4, FULL = (1u << U) - 1;
         const uintptr_t a0 = (uintptr_t)R & ~(uintptr_t)15;
         const int64_t skew = (int64_t)(((uintptr_t)R - a0) / W);   // elements of the first unit before R
         const uint64_t units = (len + skew + U - 1) / U;
@@ -571,26 +581,42 @@ __global__ void __launch_bounds__(NT) k_eq_scan(const typename KT::T *data, IpPa
                 const uint64_t u = u0 + r * NT + threadIdx.x;
                 x[r] = u < units ? __ldcs(V + u) : make_uint4(0, 0, 0, 0);
             }
-            uint32_t ce = 0, cg = 0, pe[U * UNR], pg[U * UNR];
+            uint32_t me = 0, mg = 0;
 #pragma unroll
             for (uint32_t r = 0; r < UNR; r++) {
                 const uint64_t u = u0 + r * NT + threadIdx.x;
+                if (u >= units) continue;
                 T e[U];
                 memcpy(e, &x[r], 16);
+                uint32_t eqb = 0;
 #pragma unroll
                 for (uint32_t q = 0; q < U; q++) {
-                    const int64_t i = (int64_t)(u * U + q) - skew;
-                    if (u < units && i >= 0 && (uint64_t)i < len) {
-                        const K k = KT::key(e[q]);
-                        const bool eq = !(k < pk) && !(pk < k);
-                        if ((uint64_t)i < band && !eq) pg[cg++] = (uint32_t)i;
-                        if ((uint64_t)i >= band && eq) pe[ce++] = (uint32_t)i;
-                    }
+                    const K k = KT::key(e[q]);
+                    eqb |= (uint32_t)(!(k < pk) && !(pk < k)) << q;
                 }
+                const int64_t i0 = (int64_t)(u * U) - skew;   // index of key 0 of the unit
+                uint32_t valid = FULL, inband;
+                if (i0 < 0 || i0 + U > len) {
+                    valid = 0;
+#pragma unroll
+                    for (uint32_t q = 0; q < U; q++) valid |= (uint32_t)(i0 + q >= 0 && (uint64_t)(i0 + q) < len) << q;
+                }
+                if (i0 + (int64_t)U <= (int64_t)band) inband = FULL;
+                else if (i0 >= (int64_t)band) inband = 0;
+                else {
+                    inband = 0;
+#pragma unroll
+                    for (uint32_t q = 0; q < U; q++) inband |= (uint32_t)(i0 + (int64_t)q < (int64_t)band) << q;
+                }
+                me |= (eqb & ~inband & valid) << (r * U);
+                mg |= (~eqb & inband & valid & FULL) << (r * U);
             }
-            if (__any_sync(0xffffffffu, ce | cg)) {
-                warp_append(ce, lane, &ps->cnt_eq, E, pe);
-                warp_append(cg, lane, &ps->cnt_gt, G, pg);
+            if (__any_sync(0xffffffffu, me | mg)) {
+                auto pos = [&](uint32_t bit) {
+                    return (uint32_t)((int64_t)((u0 + (bit / U) * NT + threadIdx.x) * U + bit % U) - skew);
+                };
+                warp_append(me, lane, &ps->cnt_eq, E, pos);
+                warp_append(mg, lane, &ps->cnt_gt, G, pos);
             }
         }
     }

@@ -63,6 +63,7 @@ for kind, n in cases:
         "inplace": lambda: bq.bq_partition_inplace(t, pv, ws=iws),
         "pass_fast": lambda: bq.bq_partition_pass(t, dst, pv, counts, ordered=False, ws=ws),
         "pass_ordered": lambda: bq.bq_partition_pass(t, dst, pv, counts, ordered=True, ws=ws),
+        "partition_api": lambda: bq.partition(t, pv, ws=ws),   # ordered pass + copy-back (n scratch)
     }
     res = {name: timed(fn) for name, fn in fns.items() if not a.only or name == a.only}
     for name, ms in res.items():
