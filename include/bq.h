@@ -64,7 +64,7 @@ typedef enum {
     BQ_ERR_UNSUPPORTED = 4       /* no CUDA device, or the device is not sm_100 */
 } bq_status;
 
-typedef enum { BQ_I32 = 0, BQ_U64 = 1, BQ_F64 = 2, BQ_REC32 = 3 } bq_kind;
+typedef enum { BQ_I32 = 0, BQ_U64 = 1, BQ_F64 = 2, BQ_REC32 = 3, BQ_KEYIDX16 = 4 } bq_kind;
 
 /* Pivot sample rules (§2; §4 "pivot selection" P:719-753):
  *   MO3     median of the keys at segment positions {b, b+floor(len/2), e-1}
@@ -87,6 +87,15 @@ typedef struct {
     uint64_t payload[3];
 } bq_record32;
 
+/* 16-byte key + index pair, 16-byte aligned (the key+index
+ * record variant).  Ordered by `key` only, like records; `idx` travels with
+ * its key.  bq_sort_records sorts (key, position) pairs of this type and
+ * then gathers every 32-byte record once (bq_sort_options.records). */
+typedef struct {
+    uint64_t key;
+    uint64_t idx;
+} bq_keyidx16;
+
 typedef struct {
     int32_t pivot_rule;   /* bq_pivot_rule for segments > leaf size; default SAMPLE64 */
     int32_t depth_limit;  /* < 0: Introsort limit 2*floor(log2 n)+3 */
@@ -99,7 +108,12 @@ typedef struct {
                              multi-pivot block partition, 16-way passes (
                              segments whose sample has duplicate splitters use the binary
                              three-way pass).  Records always use the binary pass. */
-    int32_t reserved[3];  /* must be 0 */
+    int32_t records;      /* records only: 0 (default) or 2: key+index path — the passes move
+                             16-byte (key, position) pairs (bq_keyidx16) instead of 32-byte
+                             records and every record is gathered once at the end (P:867-870:
+                             the cost of moving large elements); 1: the passes move the
+                             records themselves.  Sorted keys are identical. */
+    int32_t reserved[2];  /* must be 0 */
 } bq_sort_options;
 
 typedef struct {
@@ -118,7 +132,9 @@ typedef struct {
 
 /* Workspace bytes every call below needs for `n` elements of `kind`:
  * an n*w scratch buffer for the out-of-place partition passes plus O(n/T)
- * bytes of tile status words, segment descriptors and leaf lists. */
+ * bytes of tile status words, segment descriptors and leaf lists.  For
+ * BQ_REC32 it also covers the key+index sort path: 16n bytes of pairs, the
+ * workspace of BQ_KEYIDX16 and 4n bytes of gather indices (about 36n). */
 BQ_API size_t bq_workspace_bytes(bq_kind kind, size_t n);
 
 /* ---- pivot selection (hot-path step a1) -------------------------------------

@@ -7,8 +7,9 @@ if ``libbq.so`` is missing or fails to load, importing this module raises.
 
 Function names are the C names.  Tensors must be CUDA, contiguous, and of the
 kind's dtype: int32 (``i32``), uint64 or int64 (``u64``, reinterpreted as
-uint64), float64 (``f64``), and records as an (n, 4) uint64/int64 tensor whose
-column 0 is the key (``rec32``, 32 bytes per row).
+uint64), float64 (``f64``), records as an (n, 4) uint64/int64 tensor whose
+column 0 is the key (``rec32``, 32 bytes per row), and key+index pairs as an
+(n, 2) uint64/int64 tensor (``keyidx16``: key, index).
 """
 from __future__ import annotations
 
@@ -29,16 +30,18 @@ if not os.path.exists(LIB_PATH):
 _lib = ctypes.CDLL(LIB_PATH)
 
 BQ_OK, BQ_ERR_INVALID_ARGUMENT, BQ_ERR_WORKSPACE, BQ_ERR_CUDA, BQ_ERR_UNSUPPORTED = range(5)
-BQ_I32, BQ_U64, BQ_F64, BQ_REC32 = range(4)
+BQ_I32, BQ_U64, BQ_F64, BQ_REC32, BQ_KEYIDX16 = range(5)
 BQ_PIVOT_MO3, BQ_PIVOT_NINTHER, BQ_PIVOT_SAMPLE64 = range(3)
-KIND = {"i32": BQ_I32, "u64": BQ_U64, "f64": BQ_F64, "rec32": BQ_REC32}
-WIDTH = {BQ_I32: 4, BQ_U64: 8, BQ_F64: 8, BQ_REC32: 32}
+KIND = {"i32": BQ_I32, "u64": BQ_U64, "f64": BQ_F64, "rec32": BQ_REC32, "keyidx16": BQ_KEYIDX16}
+WIDTH = {BQ_I32: 4, BQ_U64: 8, BQ_F64: 8, BQ_REC32: 32, BQ_KEYIDX16: 16}
+# bq_sort_options.records: the records sort path
+RECORDS_DEFAULT, RECORDS_DIRECT, RECORDS_KEYIDX = 0, 1, 2
 
 
 class bq_sort_options(ctypes.Structure):
     _fields_ = [("pivot_rule", ctypes.c_int32), ("depth_limit", ctypes.c_int32),
                 ("timing", ctypes.c_int32), ("ordered", ctypes.c_int32), ("ways", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 3)]
+                ("records", ctypes.c_int32), ("reserved", ctypes.c_int32 * 2)]
 
 
 class bq_sort_stats(ctypes.Structure):
@@ -105,6 +108,8 @@ def _check(status: int):
 def kind_of(t: torch.Tensor) -> int:
     if t.dim() == 2 and t.shape[1] == 4 and t.dtype in (torch.uint64, torch.int64):
         return BQ_REC32
+    if t.dim() == 2 and t.shape[1] == 2 and t.dtype in (torch.uint64, torch.int64):
+        return BQ_KEYIDX16
     if t.dtype == torch.int32:
         return BQ_I32
     if t.dtype in (torch.uint64, torch.int64):
@@ -204,7 +209,7 @@ def bq_partition_records(recs, pivot_key, ws=None, stream=None):
 
 
 _PIVOT_CTYPE = {BQ_I32: ctypes.c_int32, BQ_U64: ctypes.c_uint64, BQ_F64: ctypes.c_double,
-                BQ_REC32: ctypes.c_uint64}
+                BQ_REC32: ctypes.c_uint64, BQ_KEYIDX16: ctypes.c_uint64}
 
 
 def bq_partition_pass(src, dst, pivot, d_counts, ordered=True, ws=None, stream=None):
@@ -243,7 +248,8 @@ def bq_partition_segments(src, dst, begins, lens, pivots, d_counts, ordered=True
     nseg = len(begins)
     b = np.ascontiguousarray(np.asarray(begins, dtype=np.uint32))
     ln = np.ascontiguousarray(np.asarray(lens, dtype=np.uint32))
-    pdt = {BQ_I32: np.int32, BQ_U64: np.uint64, BQ_F64: np.float64, BQ_REC32: np.uint64}[kind]
+    pdt = {BQ_I32: np.int32, BQ_U64: np.uint64, BQ_F64: np.float64, BQ_REC32: np.uint64,
+           BQ_KEYIDX16: np.uint64}[kind]
     pv = np.ascontiguousarray(np.asarray(pivots).astype(pdt))
     _check(_lib.bq_partition_segments(kind, _dev(src), _dev(dst), _n(src), b.ctypes.data, ln.ctypes.data,
                                       pv.ctypes.data, nseg, _dev(d_counts), int(ordered), w, wb,
@@ -273,8 +279,9 @@ def bq_sort_records(recs, ws=None, stream=None):
     return _sort("bq_sort_records", recs, ws, stream)
 
 
-def _opts(pivot_rule, depth_limit, timing, ordered=False, ways=0):
+def _opts(pivot_rule, depth_limit, timing, ordered=False, ways=0, records=0):
     o = bq_sort_options()
+    o.records = int(records)
     o.pivot_rule = pivot_rule
     o.depth_limit = depth_limit
     o.timing = int(timing)
@@ -284,12 +291,14 @@ def _opts(pivot_rule, depth_limit, timing, ordered=False, ways=0):
 
 
 def bq_sort_ex(data, pivot_rule=BQ_PIVOT_SAMPLE64, depth_limit=-1, timing=False, ordered=False, ways=0,
-               ws=None, stream=None):
-    """Kind-generic sort; returns the bq_sort_stats as a dict.  ways: 0 default
-    (16-way multi-pivot passes for keys), 2 binary only, 16 multiway."""
+               records=RECORDS_DEFAULT, ws=None, stream=None):
+    """Kind-generic sort; returns the bq_sort_stats as a dict.  ways: 0 / 2
+    binary passes (default), 8 or 16 multi-pivot passes (keys).  records:
+    RECORDS_DEFAULT / RECORDS_KEYIDX sort (key, index) pairs and gather the
+    records once, RECORDS_DIRECT moves the records in every pass."""
     kind = kind_of(data)
     w, wb = _ws(ws, kind, _n(data), data)
-    o = _opts(pivot_rule, depth_limit, timing, ordered, ways)
+    o = _opts(pivot_rule, depth_limit, timing, ordered, ways, records)
     st = bq_sort_stats()
     _check(_lib.bq_sort_ex(kind, _dev(data), _n(data), ctypes.byref(o), ctypes.byref(st), w, wb,
                            _stream(stream)))

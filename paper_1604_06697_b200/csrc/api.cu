@@ -51,6 +51,7 @@ BQ_API size_t bq_workspace_bytes(bq_kind kind, size_t n) {
         case BQ_U64: return ws_u64(n);
         case BQ_F64: return ws_f64(n);
         case BQ_REC32: return ws_rec(n);
+        case BQ_KEYIDX16: return ws_pair(n);
     }
     return 0;
 }
@@ -69,6 +70,7 @@ BQ_API bq_status bq_partition_pass(bq_kind kind, const void *src, void *dst, siz
             return pass_f64(src, dst, n, pivot, d_counts, ws, ws_bytes, s, ordered);
         }
         case BQ_REC32: return pass_rec(src, dst, n, pivot, d_counts, ws, ws_bytes, s, ordered);
+        case BQ_KEYIDX16: return pass_pair(src, dst, n, pivot, d_counts, ws, ws_bytes, s, ordered);
     }
     return bq::set_error(BQ_ERR_INVALID_ARGUMENT, "bad kind %d", (int)kind);
 }
@@ -79,6 +81,7 @@ BQ_API size_t bq_inplace_workspace_bytes(bq_kind kind, size_t n) {
         case BQ_U64: return ipws_u64(n);
         case BQ_F64: return ipws_f64(n);
         case BQ_REC32: return ipws_rec(n);
+        case BQ_KEYIDX16: return ipws_pair(n);
     }
     return 0;
 }
@@ -97,6 +100,7 @@ BQ_API bq_status bq_partition_inplace(bq_kind kind, void *data, size_t n, const 
             return inplace_f64(data, n, pivot, split, n_equal, ws, ws_bytes, s);
         }
         case BQ_REC32: return inplace_rec(data, n, pivot, split, n_equal, ws, ws_bytes, s);
+        case BQ_KEYIDX16: return inplace_pair(data, n, pivot, split, n_equal, ws, ws_bytes, s);
     }
     return bq::set_error(BQ_ERR_INVALID_ARGUMENT, "bad kind %d", (int)kind);
 }
@@ -117,6 +121,8 @@ BQ_API bq_status bq_partition_segments(bq_kind kind, const void *src, void *dst,
         case BQ_U64: return segs_u64(src, dst, n, begins, lens, pivots, nseg, d_counts, ws, ws_bytes, s, ordered);
         case BQ_F64: return segs_f64(src, dst, n, begins, lens, pivots, nseg, d_counts, ws, ws_bytes, s, ordered);
         case BQ_REC32: return segs_rec(src, dst, n, begins, lens, pivots, nseg, d_counts, ws, ws_bytes, s, ordered);
+        case BQ_KEYIDX16:
+            return segs_pair(src, dst, n, begins, lens, pivots, nseg, d_counts, ws, ws_bytes, s, ordered);
     }
     return bq::set_error(BQ_ERR_INVALID_ARGUMENT, "bad kind %d", (int)kind);
 }
@@ -129,14 +135,15 @@ BQ_API bq_status bq_sort_ex(bq_kind kind, void *data, size_t n, const bq_sort_op
         case BQ_U64: return sort_u64(data, n, opt, stats, ws, ws_bytes, s);
         case BQ_F64: return sort_f64(data, n, opt, stats, ws, ws_bytes, s);
         case BQ_REC32: return sort_rec(data, n, opt, stats, ws, ws_bytes, s);
+        case BQ_KEYIDX16: return sort_pair(data, n, opt, stats, ws, ws_bytes, s);
     }
     return bq::set_error(BQ_ERR_INVALID_ARGUMENT, "bad kind %d", (int)kind);
 }
 
 BQ_API bq_status bq_sort_host(bq_kind kind, void *host_data, size_t n, void *dev_data, const bq_sort_options *opt,
                               void *ws, size_t ws_bytes, void *stream) {
-    static const size_t W[4] = {4, 8, 8, 32};
-    if ((int)kind < 0 || (int)kind > 3) return bq::set_error(BQ_ERR_INVALID_ARGUMENT, "bad kind %d", (int)kind);
+    static const size_t W[5] = {4, 8, 8, 32, 16};
+    if ((int)kind < 0 || (int)kind > 4) return bq::set_error(BQ_ERR_INVALID_ARGUMENT, "bad kind %d", (int)kind);
     if (n > 0 && (host_data == nullptr || dev_data == nullptr))
         return bq::set_error(BQ_ERR_INVALID_ARGUMENT, "NULL buffer with n > 0");
     cudaStream_t s = (cudaStream_t)stream;

@@ -46,6 +46,7 @@ BQ_DETAIL_DECLS(i32)
 BQ_DETAIL_DECLS(u64)
 BQ_DETAIL_DECLS(f64)
 BQ_DETAIL_DECLS(rec)
+BQ_DETAIL_DECLS(pair)
 
 #define BQ_DETAIL_DEFS(SUF, KT)                                                                     \
     namespace bq {                                                                                  \

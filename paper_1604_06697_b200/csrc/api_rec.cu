@@ -3,8 +3,70 @@
 #include "api_kind.cuh"
 
 namespace bq {
+
+// ---- the key+index path -------------------------------------
+// Records are large elements with cheap comparisons: every
+// partition pass of the direct path moves 32 bytes per record.  Here the
+// passes move 16-byte (key, position) pairs, and each record moves once, in a
+// final gather.  Workspace: [pairs 16n | pair-sort workspace (its scratch
+// first) | gather indices 4n]; after the pair sort the gather target is the
+// first 32n bytes (the pairs and the pair scratch, no longer needed).
+__global__ void k_ki_extract(const Rec32 *r, KeyIdx16 *p, uint64_t n) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        p[i] = KeyIdx16{r[i].key, i};
+}
+__global__ void k_ki_index(const KeyIdx16 *p, uint32_t *idx, uint64_t n) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        idx[i] = (uint32_t)p[i].idx;
+}
+__global__ void k_ki_gather(const Rec32 *r, const uint32_t *idx, Rec32 *g, uint64_t n) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        g[i] = r[idx[i]];
+}
+
 namespace detail {
-size_t ws_rec(size_t n) { return make_layout<KRec>(n).total; }
+struct KiLayout {
+    size_t pairs, pws, pws_bytes, idx, total;
+};
+static KiLayout ki_layout(size_t n) {
+    KiLayout L;
+    L.pairs = 0;
+    L.pws = align_up(n * sizeof(KeyIdx16), 256);
+    L.pws_bytes = ws_pair(n);
+    L.idx = align_up(L.pws + L.pws_bytes, 256);
+    L.total = align_up(L.idx + n * sizeof(uint32_t), 256);
+    return L;
+}
+// records below this size are one leaf (or a few): the direct path
+constexpr size_t KI_MIN = 2 * (size_t)Tune<KRec>::LEAF;
+
+static bq_status sort_rec_ki(Rec32 *data, size_t n, const bq_sort_options *opt, bq_sort_stats *st, void *ws,
+                             size_t wsb, cudaStream_t s) {
+    const KiLayout L = ki_layout(n);
+    if (wsb < L.total) return set_error(BQ_ERR_WORKSPACE, "workspace %zu B < required %zu B", wsb, L.total);
+    char *w = static_cast<char *>(ws);
+    KeyIdx16 *pairs = reinterpret_cast<KeyIdx16 *>(w + L.pairs);
+    uint32_t *idx = reinterpret_cast<uint32_t *>(w + L.idx);
+    Rec32 *gath = reinterpret_cast<Rec32 *>(w);
+    const uint32_t grid = 148 * 8;
+    k_ki_extract<<<grid, 256, 0, s>>>(data, pairs, n);
+    BQ_CK_LAUNCH();
+    bq_status r = sort_pair(pairs, n, opt, st, w + L.pws, L.pws_bytes, s);
+    if (r != BQ_OK) return r;
+    k_ki_index<<<grid, 256, 0, s>>>(pairs, idx, n);
+    BQ_CK_LAUNCH();
+    k_ki_gather<<<grid, 256, 0, s>>>(data, idx, gath, n);
+    BQ_CK_LAUNCH();
+    BQ_CK(cudaMemcpyAsync(data, gath, n * sizeof(Rec32), cudaMemcpyDeviceToDevice, s));
+    if (st) st->kernel_launches += 3;
+    BQ_CK(cudaStreamSynchronize(s));
+    return BQ_OK;
+}
+
+size_t ws_rec(size_t n) {
+    const size_t a = make_layout<KRec>(n).total, b = ki_layout(n).total;
+    return a > b ? a : b;
+}
 size_t ipws_rec(size_t n) { return make_ip_layout<KRec>(n).total; }
 bq_status inplace_rec(void *data, size_t n, const void *pivot, size_t *split, size_t *neq, void *ws, size_t wsb,
                       cudaStream_t s) {
@@ -13,7 +75,13 @@ bq_status inplace_rec(void *data, size_t n, const void *pivot, size_t *split, si
 }
 bq_status sort_rec(void *data, size_t n, const bq_sort_options *opt, bq_sort_stats *st, void *ws, size_t wsb,
                    cudaStream_t s) {
-    return run_sort<KRec>(static_cast<Rec32 *>(data), n, opt, st, ws, wsb, s);
+    const int path = opt ? opt->records : 0;
+    if (path < 0 || path > 2) return set_error(BQ_ERR_INVALID_ARGUMENT, "records path %d", path);
+    Rec32 *r = static_cast<Rec32 *>(data);
+    if (path == 1 || n < KI_MIN) return run_sort<KRec>(r, n, opt, st, ws, wsb, s);
+    bq_status v = validate<KRec>(data, n, ws, wsb);
+    if (v != BQ_OK) return v;
+    return sort_rec_ki(r, n, opt, st, ws, wsb, s);
 }
 bq_status pass_rec(const void *src, void *dst, size_t n, const void *pivot, uint64_t *dc, void *ws, size_t wsb,
                    cudaStream_t s, int ordered) {
@@ -45,8 +113,7 @@ BQ_API bq_status bq_partition_records(bq_record32 *recs, size_t n, uint64_t pivo
 }
 
 BQ_API bq_status bq_sort_records(bq_record32 *recs, size_t n, void *ws, size_t ws_bytes, void *stream) {
-    return bq::run_sort<bq::KRec>(reinterpret_cast<bq::Rec32 *>(recs), n, nullptr, nullptr, ws, ws_bytes,
-                                  (cudaStream_t)stream);
+    return bq::detail::sort_rec(recs, n, nullptr, nullptr, ws, ws_bytes, (cudaStream_t)stream);
 }
 
 }

@@ -70,6 +70,23 @@ struct KRec {
     static constexpr K KMAX = ~0ull;
 };
 
+// key + index pair (bq_keyidx16): the key+index record path (SURVEY §8(f)
+// N3) sorts these and gathers the records once; also a public kind
+struct alignas(16) KeyIdx16 {
+    uint64_t key;
+    uint64_t idx;
+};
+
+struct KPair {
+    using T = KeyIdx16;
+    using K = uint64_t;
+    static constexpr bq_kind kind = BQ_KEYIDX16;
+    static constexpr int W = 16;
+    static constexpr bool is_record = true;
+    __host__ __device__ static K key(const T &r) { return r.key; }
+    static constexpr K KMAX = ~0ull;
+};
+
 // Per-kind tuning constants.  TILE = elements per partition tile (one CTA),
 // LEAF = largest segment finished by the shared-memory leaf sort (S).
 // PART_THREADS = consumer threads of the partition kernel (one more producer
@@ -104,6 +121,10 @@ template <> struct Tune<KF64> : Tune<KU64> {};
 template <> struct Tune<KRec> {
     static constexpr int PART_THREADS = 256, PART_IPT = 2, PART_STAGES = BQ_REC_STAGES, PART_MINB = 2;   // 16 KB tiles
     static constexpr int LEAF = 2048, LEAF_THREADS = 512;
+};
+template <> struct Tune<KPair> {
+    static constexpr int PART_THREADS = 256, PART_IPT = 4, PART_STAGES = 4, PART_MINB = 2;   // 16 KB tiles
+    static constexpr int LEAF = 4096, LEAF_THREADS = 512;
 };
 
 template <class KT> constexpr int tile_elems() { return Tune<KT>::PART_THREADS * Tune<KT>::PART_IPT; }

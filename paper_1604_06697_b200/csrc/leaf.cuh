@@ -68,6 +68,9 @@ struct LeafTraits<KRec> {
     static constexpr int OCC = 512;
 };
 
+template <>
+struct LeafTraits<KPair> : LeafTraits<KRec> {};   // pairs sort as (key, leaf index) like records
+
 template <class KT>
 constexpr int leaf_lmin() { return LeafTraits<KT>::R + 5; }   // one warp
 template <class KT>
@@ -248,6 +251,9 @@ struct Planes<KRec> {   // records: key plane (8 B) + index plane (4 B)
     }
 };
 
+template <>
+struct Planes<KPair> : Planes<KRec> {};
+
 // ---- the network ---------------------------------------------------------------
 template <class KT, int L>
 struct Net {
@@ -380,9 +386,10 @@ __device__ __forceinline__ void leaf_body(const LeafParams<KT> &P, const Leaf lf
         // leaf copy in shared memory (the output is gathered from it, so the
         // leaf may be sorted in place)
         T *sr = reinterpret_cast<T *>(smem_raw + Planes<KT>::template bytes<NET>());
+        constexpr uint32_t V = sizeof(T) / 16;   // 16-byte vectors per record
         const uint4 *g = reinterpret_cast<const uint4 *>(srcbuf + b);
         uint4 *s4 = reinterpret_cast<uint4 *>(sr);
-        for (uint32_t q = t; q < 2 * len; q += NT) s4[q] = g[q];
+        for (uint32_t q = t; q < V * len; q += NT) s4[q] = g[q];
         __syncthreads();
 #pragma unroll
         for (int r = 0; r < IPT; r++) {
@@ -396,9 +403,11 @@ __device__ __forceinline__ void leaf_body(const LeafParams<KT> &P, const Leaf lf
             if (i < len) {
                 const uint4 *s = reinterpret_cast<const uint4 *>(sr + x[r].i);
                 uint4 *d = reinterpret_cast<uint4 *>(out + b + i);
-                const uint4 v0 = s[0], v1 = s[1];
-                d[0] = v0;
-                d[1] = v1;
+                uint4 v[V];
+#pragma unroll
+                for (uint32_t c = 0; c < V; c++) v[c] = s[c];
+#pragma unroll
+                for (uint32_t c = 0; c < V; c++) d[c] = v[c];
             }
         }
     } else {
