@@ -54,6 +54,7 @@ struct Layout {
     size_t scratch, status, tile_map[2], segs[2], cursor[2], ecursor[2], leaves[2], fallback, ctrl, misc, total;
     size_t msegs[2], mtile_map[2], mhist[2], mcursor[2];   // multiway segment lists (N4)
     size_t copies[2], max_copies;                           // records: finished equal runs to copy
+    size_t subs[2];                                         // N1 subtree jobs (subtree.cuh)
     size_t max_tiles, max_segs, max_leaves, max_fb;
 };
 
@@ -90,6 +91,9 @@ Layout<KT> make_layout(size_t n) {
     L.max_copies = KT::is_record ? LEVEL_BATCH * (L.max_segs + 2) + n / 65536 + 2 : 1;
     L.copies[0] = take(L.max_copies * sizeof(Leaf));
     L.copies[1] = take(L.max_copies * sizeof(Leaf));
+    // N1 subtree jobs of one batch (disjoint segments > S), per set
+    L.subs[0] = take(L.max_segs * sizeof(Leaf));
+    L.subs[1] = take(L.max_segs * sizeof(Leaf));
     L.ctrl = take((MAX_LEVELS + 1) * sizeof(LevelCtrl));   // [MAX_LEVELS]: the root's counts
     L.misc = take(256);   // fallback count, leaf-list counts (2 sets x 4 classes), pass counts
     L.total = off;
@@ -162,6 +166,19 @@ bq_status persistent_cap(F kern, int threads, int smem, int *cap) {
     BQ_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     if (nb < 1) return set_error(BQ_ERR_CUDA, "kernel does not fit on an SM");
     *cap = nb * sms;
+    return BQ_OK;
+}
+
+// the batch's subtree jobs (N1): persistent, one 1024-thread CTA per SM
+template <class KT>
+bq_status launch_subtree(const SubParams<KT> &SP, cudaStream_t s) {
+    auto kern = k_subtree<KT, SUB_THREADS>;
+    constexpr int smem = sub_smem_bytes<KT>();
+    static int cap = 0;
+    bq_status st = persistent_cap(kern, SUB_THREADS, smem, &cap);
+    if (st != BQ_OK) return st;
+    kern<<<cap, SUB_THREADS, smem, s>>>(SP);
+    BQ_CK_LAUNCH();
     return BQ_OK;
 }
 
@@ -654,6 +671,12 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
     uint32_t *leaf_counts[2] = {fb_count + 4, fb_count + 8};   // [set][class]
     uint32_t *copy_counts[2] = {fb_count + 12, fb_count + 13};
     Leaf *copies[2] = {reinterpret_cast<Leaf *>(w + L.copies[0]), reinterpret_cast<Leaf *>(w + L.copies[1])};
+    Leaf *subs[2] = {reinterpret_cast<Leaf *>(w + L.subs[0]), reinterpret_cast<Leaf *>(w + L.subs[1])};
+    uint32_t *sub_counts[2] = {fb_count + 14, fb_count + 15};
+    uint32_t *overflow = fb_count + 16;
+    // N1: subtrees of <= SUB elements are finished on chip (opt-out: BQ_NO_SUBTREE=1)
+    static const bool sub_env_off = std::getenv("BQ_NO_SUBTREE") != nullptr;
+    const uint32_t sub_max = (sub_enabled<KT>() && !sub_env_off) ? sub_elems<KT>() : 0;
 
     LeafParams<KT> LP{};
     LP.bufs[0] = user;
@@ -702,7 +725,7 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
     }
 
     BQ_CKC(cudaMemsetAsync(ctrl, 0, (MAX_LEVELS + 1) * sizeof(LevelCtrl), s));
-    BQ_CKC(cudaMemsetAsync(fb_count, 0, 14 * sizeof(uint32_t), s));
+    BQ_CKC(cudaMemsetAsync(fb_count, 0, 17 * sizeof(uint32_t), s));
     const int aligned = aligned16(user) && aligned16(scratch);
     // children sink of level `lv` (its children form level lv+1; the root is
     // the only "child" of the virtual level -1, counted in `root`)
@@ -735,6 +758,9 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
         Q.ways = ways;
         Q.emit_children = 1;
         Q.band_inline_max = BAND_INLINE_MAX;
+        Q.subs = subs[set];
+        Q.sub_count = sub_counts[set];
+        Q.sub_max = sub_max;
         return Q;
     };
     {
@@ -756,6 +782,7 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
         if (batch >= 2) BQ_CKC(cudaStreamWaitEvent(s, ev_leaves[set], 0));
         BQ_CKC(cudaMemsetAsync(leaf_counts[set], 0, 4 * sizeof(uint32_t), s));
         BQ_CKC(cudaMemsetAsync(copy_counts[set], 0, sizeof(uint32_t), s));
+        if (batch > 0) BQ_CKC(cudaMemsetAsync(sub_counts[set], 0, sizeof(uint32_t), s));   // batch 0: the root may be one
         for (int k = 0; k < LEVEL_BATCH; k++, level++) {
             const int cp = level & 1;
             const LevelCtrl *prev = level == 0 ? root : ctrl + level - 1;
@@ -824,6 +851,28 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
             if (st != BQ_OK) { cleanup(); return st; }
             local.kernel_launches += KT::is_record ? 2 : 1;
         }
+        // the batch's subtrees (N1), on chip; their pieces join this batch's leaves
+        if (sub_max) {
+            SubParams<KT> SP{};
+            SP.bufs[0] = user;
+            SP.bufs[1] = scratch;
+            SP.jobs = subs[set];
+            SP.job_count = sub_counts[set];
+            SP.leaves = leaves[set];
+            SP.leaf_counts = leaf_counts[set];
+            SP.leaf_cap = (uint32_t)L.max_leaves;
+            SP.fallback = fallback;
+            SP.fallback_count = fb_count;
+            SP.ctrl = ctrl + level - 1;
+            SP.overflow = overflow;
+            SP.leaf_max = S;
+            SP.depth_limit = depth_limit;
+            SP.pivot_rule = rule;
+            SP.aligned = aligned;
+            st = launch_subtree<KT>(SP, s);
+            if (st != BQ_OK) { cleanup(); return st; }
+            local.kernel_launches++;
+        }
         // leaves of this batch on the side stream
 #ifndef BQ_LEAF_MAIN
         cudaStream_t ls = side;
@@ -861,6 +910,11 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
     BQ_CKC(cudaMemcpyAsync(&hctrl[MAX_LEVELS].pad2[0], fb_count, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
     BQ_CKC(cudaStreamSynchronize(s));
     nfb_total = hctrl[MAX_LEVELS].pad2[0];
+    if (sub_max) {
+        uint32_t ovf = 0;
+        BQ_CKC(cudaMemcpy(&ovf, overflow, sizeof ovf, cudaMemcpyDeviceToHost));
+        if (ovf) { cleanup(); return set_error(BQ_ERR_CUDA, "leaf list overflow in the subtree pass"); }
+    }
     for (int l = 0; l < level; l++) {
         const LevelCtrl &hc = hctrl[l];
         const uint32_t nseg_l = l == 0 ? 1u : hctrl[l - 1].nseg_next + hctrl[l - 1].nmseg_next;
