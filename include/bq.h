@@ -113,7 +113,11 @@ typedef struct {
                              records and every record is gathered once at the end (P:867-870:
                              the cost of moving large elements); 1: the passes move the
                              records themselves.  Sorted keys are identical. */
-    int32_t reserved[2];  /* must be 0 */
+    int32_t subtree;      /* != 0: segments of S < len <= 96 KB of elements are finished
+                             depth-first by one CTA in shared memory instead of by further
+                             level passes; 0 (default): level
+                             passes down to the leaf size */
+    int32_t reserved[1];  /* must be 0 */
 } bq_sort_options;
 
 typedef struct {

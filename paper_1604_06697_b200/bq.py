@@ -41,7 +41,7 @@ RECORDS_DEFAULT, RECORDS_DIRECT, RECORDS_KEYIDX = 0, 1, 2
 class bq_sort_options(ctypes.Structure):
     _fields_ = [("pivot_rule", ctypes.c_int32), ("depth_limit", ctypes.c_int32),
                 ("timing", ctypes.c_int32), ("ordered", ctypes.c_int32), ("ways", ctypes.c_int32),
-                ("records", ctypes.c_int32), ("reserved", ctypes.c_int32 * 2)]
+                ("records", ctypes.c_int32), ("subtree", ctypes.c_int32), ("reserved", ctypes.c_int32 * 1)]
 
 
 class bq_sort_stats(ctypes.Structure):
@@ -279,9 +279,10 @@ def bq_sort_records(recs, ws=None, stream=None):
     return _sort("bq_sort_records", recs, ws, stream)
 
 
-def _opts(pivot_rule, depth_limit, timing, ordered=False, ways=0, records=0):
+def _opts(pivot_rule, depth_limit, timing, ordered=False, ways=0, records=0, subtree=False):
     o = bq_sort_options()
     o.records = int(records)
+    o.subtree = int(subtree)
     o.pivot_rule = pivot_rule
     o.depth_limit = depth_limit
     o.timing = int(timing)
@@ -291,14 +292,15 @@ def _opts(pivot_rule, depth_limit, timing, ordered=False, ways=0, records=0):
 
 
 def bq_sort_ex(data, pivot_rule=BQ_PIVOT_SAMPLE64, depth_limit=-1, timing=False, ordered=False, ways=0,
-               records=RECORDS_DEFAULT, ws=None, stream=None):
+               records=RECORDS_DEFAULT, subtree=False, ws=None, stream=None):
     """Kind-generic sort; returns the bq_sort_stats as a dict.  ways: 0 / 2
     binary passes (default), 8 or 16 multi-pivot passes (keys).  records:
     RECORDS_DEFAULT / RECORDS_KEYIDX sort (key, index) pairs and gather the
-    records once, RECORDS_DIRECT moves the records in every pass."""
+    records once, RECORDS_DIRECT moves the records in every pass.  subtree:
+    finish segments of up to 96 KB in shared memory (N1)."""
     kind = kind_of(data)
     w, wb = _ws(ws, kind, _n(data), data)
-    o = _opts(pivot_rule, depth_limit, timing, ordered, ways, records)
+    o = _opts(pivot_rule, depth_limit, timing, ordered, ways, records, subtree)
     st = bq_sort_stats()
     _check(_lib.bq_sort_ex(kind, _dev(data), _n(data), ctypes.byref(o), ctypes.byref(st), w, wb,
                            _stream(stream)))

@@ -611,8 +611,9 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
     constexpr int NCLS = leaf_nclass<KT>();
     bq_sort_stats local;
     std::memset(&local, 0, sizeof local);
-    int rule = BQ_PIVOT_SAMPLE64, depth_limit = -1, timing = 0, ordered = 0, ways = 0;
+    int rule = BQ_PIVOT_SAMPLE64, depth_limit = -1, timing = 0, ordered = 0, ways = 0, subtree = 0;
     if (opt) {
+        subtree = opt->subtree;
         rule = opt->pivot_rule;
         depth_limit = opt->depth_limit;
         timing = opt->timing;
@@ -674,9 +675,8 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
     Leaf *subs[2] = {reinterpret_cast<Leaf *>(w + L.subs[0]), reinterpret_cast<Leaf *>(w + L.subs[1])};
     uint32_t *sub_counts[2] = {fb_count + 14, fb_count + 15};
     uint32_t *overflow = fb_count + 16;
-    // N1: subtrees of <= SUB elements are finished on chip (opt-out: BQ_NO_SUBTREE=1)
-    static const bool sub_env_off = std::getenv("BQ_NO_SUBTREE") != nullptr;
-    const uint32_t sub_max = (sub_enabled<KT>() && !sub_env_off) ? sub_elems<KT>() : 0;
+    // N1: subtrees of <= SUB elements finished on chip (bq_sort_options.subtree)
+    const uint32_t sub_max = (sub_enabled<KT>() && subtree) ? sub_elems<KT>() : 0;
 
     LeafParams<KT> LP{};
     LP.bufs[0] = user;

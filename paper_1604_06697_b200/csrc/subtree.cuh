@@ -18,14 +18,13 @@
 namespace bq {
 
 constexpr int SUB_THREADS = 1024;
-constexpr int SUB_BYTES = 128 * 1024;
+constexpr int SUB_BYTES = 96 * 1024;   // per buffer; two buffers (A, B) per CTA
 constexpr int SUB_STACK = 48;
 
 template <class KT>
 constexpr uint32_t sub_elems() { return (uint32_t)(SUB_BYTES / sizeof(typename KT::T)); }
-// the subtree path pays off when a subtree spans at least two leaf sizes
 template <class KT>
-constexpr bool sub_enabled() { return sub_elems<KT>() >= 2u * (uint32_t)Tune<KT>::LEAF; }
+constexpr bool sub_enabled() { return sub_elems<KT>() > (uint32_t)Tune<KT>::LEAF; }
 
 template <class KT>
 struct SubParams {
@@ -49,10 +48,11 @@ struct SubParams {
 template <class KT>
 struct SubSmem {
     using T = typename KT::T;
-    alignas(128) T a[sub_elems<KT>() + 16 / sizeof(T) + 1];   // + the job's 16-byte phase
+    static constexpr uint32_t CAP = sub_elems<KT>() + 16;   // + the job's 16-byte phase; a 16-byte multiple
+    alignas(128) T buf[2][CAP];
     uint64_t bar;
     uint32_t wl[SUB_THREADS / 32], we[SUB_THREADS / 32], wg[SUB_THREADS / 32];
-    uint32_t so[SUB_STACK], sm[SUB_STACK], sd[SUB_STACK];
+    uint32_t so[SUB_STACK], sm[SUB_STACK], sd[SUB_STACK], sb[SUB_STACK];   // offset, length, depth, buffer
     uint32_t sp, tot_l, tot_e;
     uint64_t piv;
     uint64_t passes, band;
@@ -62,21 +62,42 @@ struct SubSmem {
 template <class KT>
 constexpr int sub_smem_bytes() { return (int)sizeof(SubSmem<KT>); }
 
+// a final range dst[0, m) <- X[0, m) (same 16-byte phase).  Bulk: thread 0
+// alone (TMA body + the < 16-byte head and tail); the range is never written
+// again in this job, so the store is not waited for until the next job's
+// load.  Otherwise: plain stores by the whole CTA.
+template <class T, int NT>
+__device__ __forceinline__ void sub_store(T *dst, const T *X, uint32_t m, bool bulk) {
+    constexpr uint32_t W = sizeof(T), VW = W >= 16 ? 1 : 16 / W;
+    if (!bulk) {
+        for (uint32_t i = threadIdx.x; i < m; i += NT) dst[i] = X[i];
+        return;
+    }
+    if (threadIdx.x != 0) return;
+    const uint32_t ph = (uint32_t)(((uintptr_t)dst & 15) / W);
+    const uint32_t hb = ph ? (VW - ph < m ? VW - ph : m) : 0;
+    const uint32_t nb = (m - hb) / VW * VW;
+    if (nb) {
+        tma_store_1d(dst + hb, X + hb, nb * W);
+        bulk_commit();
+    }
+    for (uint32_t i = 0; i < hb; i++) dst[i] = X[i];
+    for (uint32_t i = hb + nb; i < m; i++) dst[i] = X[i];
+}
+
 template <class KT, int NT>
 __global__ void __launch_bounds__(NT, 1) k_subtree(SubParams<KT> P) {
     using T = typename KT::T;
     using K = typename KT::K;
-    constexpr uint32_t SUB = sub_elems<KT>();
-    constexpr uint32_t IPT = SUB / NT;
     constexpr uint32_t NW = NT / 32;
-    static_assert(SUB % NT == 0 && IPT <= 32, "elements per thread");
+    constexpr uint32_t W = sizeof(T);
+    constexpr uint32_t VW = W >= 16 ? 1 : 16 / W;   // elements per 16 bytes
     extern __shared__ __align__(128) unsigned char smraw[];
     SubSmem<KT> &sm = *reinterpret_cast<SubSmem<KT> *>(smraw);
     const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t njobs = *P.job_count;
-    constexpr uint32_t W = sizeof(T);
-    constexpr uint32_t VW = W >= 16 ? 1 : 16 / W;   // elements per 16 bytes
     T *const out = P.bufs[0];
+    const int prule = P.pivot_rule == BQ_PIVOT_MO3 ? BQ_PIVOT_MO3 : BQ_PIVOT_NINTHER;   // R20
     if (tid == 0) {
         sm.passes = 0;
         sm.band = 0;
@@ -91,44 +112,48 @@ __global__ void __launch_bounds__(NT, 1) k_subtree(SubParams<KT> P) {
         const Leaf jb = P.jobs[j];
         const T *src = P.bufs[jb.parity & 1] + jb.begin;
         const uint32_t len = jb.len;
-        // A[ph + i] <-> element i: the same 16-byte phase as the job in memory
+        // X[ph + i] <-> element i: the job's 16-byte phase in both buffers
         const uint32_t ph = (uint32_t)(((uintptr_t)src & 15) / W);
         const uint32_t hb = ph ? (VW - ph < len ? VW - ph : len) : 0;   // head before the first 16 B
         const uint32_t nb = (len - hb) / VW * VW;                         // aligned body
-        if (tid == 0) bulk_wait_read0();   // the previous job's bulk store has read A
-        __syncthreads();   // ... and its readers of A and the stack are done
-        T *const A = sm.a + ph;
+        if (tid == 0) bulk_wait_read0();   // the previous job's bulk stores have read the buffers
+        __syncthreads();                   // ... and its readers of the buffers and the stack are done
+        T *const X0 = sm.buf[0] + ph;
+        T *const X1 = sm.buf[1] + ph;
         if (P.aligned) {
             if (tid == 0) {
                 if (nb) {
                     mbar_arrive_expect_tx(&sm.bar, nb * W);
-                    tma_load_1d(A + hb, src + hb, nb * W, &sm.bar);
+                    tma_load_1d(X0 + hb, src + hb, nb * W, &sm.bar);
                 } else {
                     mbar_arrive(&sm.bar);
                 }
             }
-            for (uint32_t i = tid; i < hb; i += NT) A[i] = src[i];
-            for (uint32_t i = hb + nb + tid; i < len; i += NT) A[i] = src[i];
+            for (uint32_t i = tid; i < hb; i += NT) X0[i] = src[i];
+            for (uint32_t i = hb + nb + tid; i < len; i += NT) X0[i] = src[i];
             mbar_wait(&sm.bar, phase);
             phase ^= 1;
         } else {
-            for (uint32_t i = tid; i < len; i += NT) A[i] = src[i];
+            for (uint32_t i = tid; i < len; i += NT) X0[i] = src[i];
         }
         if (tid == 0) {
             sm.so[0] = 0;
             sm.sm[0] = len;
             sm.sd[0] = jb.pad;
+            sm.sb[0] = 0;
             sm.sp = 1;
         }
         __syncthreads();
         for (;;) {
             const uint32_t sp = sm.sp;
             if (sp == 0) break;
-            const uint32_t o = sm.so[sp - 1], m = sm.sm[sp - 1], d = sm.sd[sp - 1];
-            __syncthreads();   // everyone has read the top before it changes
+            const uint32_t o = sm.so[sp - 1], m = sm.sm[sp - 1], d = sm.sd[sp - 1], b = sm.sb[sp - 1];
+            const T *S = (b ? X1 : X0) + o;
+            T *D = (b ? X0 : X1) + o;
             if (m <= P.leaf_max || (int)d >= P.depth_limit) {
-                // a piece: to the leaf lists (or the depth-capped fallback list,
-                // P:293-299); A is written to the user buffer when the job ends
+                // a piece: stored when the job ends, then sorted by the leaf
+                // kernels (or the depth-capped fallback)
+                __syncthreads();   // everyone has read the top
                 if (tid == 0) {
                     sm.sp = sp - 1;
                     const Leaf lf{jb.begin + o, m, 0, 0};
@@ -143,33 +168,23 @@ __global__ void __launch_bounds__(NT, 1) k_subtree(SubParams<KT> P) {
                         atomicAdd(&P.ctrl->nfallback, 1u);
                     }
                 }
+                sub_store<T, NT>(out + jb.begin + o, S, m, P.aligned != 0);
                 __syncthreads();
                 continue;
             }
-            // a1: the pivot of A[o, o+m) (warp 0; generic loads from shared memory)
-            if (warp == 0) {
-                const K p = select_pivot_warp<KT>(A + o, 0, m, P.pivot_rule, lane);
-                if (lane == 0) sm.piv = (uint64_t)p;
-            }
+            // a1: ninther (Mo3 for the Mo3 rule) of S[0, m), lane 0 of warp 0
+            if (tid == 0) sm.piv = (uint64_t)select_pivot<KT>(S, 0, m, prule);
             __syncthreads();
             const K pk = (K)sm.piv;
-            // classify (branch-free counters) with the elements held in registers
-            T x[IPT];
-            uint32_t cl = 0, ce = 0, cg = 0, cls = 0, ceq = 0;
-#pragma unroll
-            for (uint32_t k = 0; k < IPT; k++) {
-                const uint32_t i = tid + k * NT;
-                if (i < m) {
-                    x[k] = A[o + i];
-                    const K kk = KT::key(x[k]);
-                    const bool lt = kk < pk, gt = pk < kk;
-                    cls |= (uint32_t)lt << k;
-                    ceq |= (uint32_t)(!lt && !gt) << k;
-                    cl += lt;
-                    ce += !lt && !gt;
-                    cg += gt;
-                }
+            // count (branch-free counters, Alg. 3 l.8-9)
+            uint32_t cl = 0, ce = 0;
+            for (uint32_t i = tid; i < m; i += NT) {
+                const K kk = KT::key(S[i]);
+                cl += kk < pk;
+                ce += !(kk < pk) && !(pk < kk);
             }
+            const uint32_t mine = (m > tid) ? (m - tid + NT - 1) / NT : 0;
+            const uint32_t cg = mine - cl - ce;
             // CTA scan of the three counts
             uint32_t il = cl, ie = ce, ig = cg;
 #pragma unroll
@@ -188,10 +203,10 @@ __global__ void __launch_bounds__(NT, 1) k_subtree(SubParams<KT> P) {
                 sm.we[warp] = ie;
                 sm.wg[warp] = ig;
             }
-            __syncthreads();   // also: every element of A[o, o+m) is in registers
+            __syncthreads();
             if (warp == 0) {
-                uint32_t vl = lane < NW ? sm.wl[lane] : 0, ve = lane < NW ? sm.we[lane] : 0;
-                uint32_t vg = lane < NW ? sm.wg[lane] : 0;
+                const uint32_t vl = lane < NW ? sm.wl[lane] : 0, ve = lane < NW ? sm.we[lane] : 0;
+                const uint32_t vg = lane < NW ? sm.wg[lane] : 0;
                 uint32_t sl = vl, se = ve, sg = vg;
 #pragma unroll
                 for (int dd = 1; dd < 32; dd <<= 1) {
@@ -216,61 +231,50 @@ __global__ void __launch_bounds__(NT, 1) k_subtree(SubParams<KT> P) {
             }
             __syncthreads();
             const uint32_t LT = sm.tot_l, EQ = sm.tot_e;
-            uint32_t rl = o + sm.wl[warp] + il - cl;
-            uint32_t re = o + LT + sm.we[warp] + ie - ce;
-            uint32_t rg = o + LT + EQ + sm.wg[warp] + ig - cg;
-#pragma unroll
-            for (uint32_t k = 0; k < IPT; k++) {
-                const uint32_t i = tid + k * NT;
-                if (i < m) {
-                    const bool lt = (cls >> k) & 1, eq = (ceq >> k) & 1;
-                    const uint32_t dst = lt ? rl : (eq ? re : rg);
-                    A[dst] = x[k];
-                    rl += lt;
-                    re += eq;
-                    rg += !lt && !eq;
-                }
+            uint32_t rl = sm.wl[warp] + il - cl;
+            uint32_t re = LT + sm.we[warp] + ie - ce;
+            uint32_t rg = LT + EQ + sm.wg[warp] + ig - cg;
+            // rearrangement: the same elements in the same order, into the other buffer
+            for (uint32_t i = tid; i < m; i += NT) {
+                const T x = S[i];
+                const K kk = KT::key(x);
+                const bool lt = kk < pk, gt = pk < kk;
+                D[lt ? rl : (gt ? rg : re)] = x;
+                rl += lt;
+                rg += gt;
+                re += !lt && !gt;
             }
+            if (P.aligned) fence_proxy_async_smem();   // D becomes visible to the bulk stores
             __syncthreads();
+            // the equal band is final (a6)
+            if (EQ) sub_store<T, NT>(out + jb.begin + o + LT, D + LT, EQ, P.aligned != 0);
             if (tid == 0) {
                 sm.passes += m;
                 sm.band += EQ;
                 const uint32_t G = m - LT - EQ;
-                // children: the larger one below, the smaller one on top (P:1238-1252)
                 uint32_t s = sp - 1;
+                // children: the larger one below, the smaller one on top (P:1238-1252)
                 const uint32_t bo = o + LT + EQ;
-                const bool gfirst = G >= LT;   // push the larger first
+                const bool gfirst = G >= LT;
                 const uint32_t o1 = gfirst ? bo : o, m1 = gfirst ? G : LT;
                 const uint32_t o2 = gfirst ? o : bo, m2 = gfirst ? LT : G;
                 if (m1 && s < SUB_STACK) {
                     sm.so[s] = o1;
                     sm.sm[s] = m1;
                     sm.sd[s] = d + 1;
+                    sm.sb[s] = b ^ 1;
                     s++;
                 }
                 if (m2 && s < SUB_STACK) {
                     sm.so[s] = o2;
                     sm.sm[s] = m2;
                     sm.sd[s] = d + 1;
+                    sm.sb[s] = b ^ 1;
                     s++;
                 }
                 sm.sp = s;
             }
             __syncthreads();
-        }
-        // the job's final layout (pieces for the leaves, finished equal bands)
-        T *dst = out + jb.begin;
-        if (P.aligned) {
-            fence_proxy_async_smem();
-            __syncthreads();
-            if (tid == 0 && nb) {
-                tma_store_1d(dst + hb, A + hb, nb * W);
-                bulk_commit();
-            }
-            for (uint32_t i = tid; i < hb; i += NT) dst[i] = A[i];
-            for (uint32_t i = hb + nb + tid; i < len; i += NT) dst[i] = A[i];
-        } else {
-            for (uint32_t i = tid; i < len; i += NT) dst[i] = A[i];
         }
     }
     if (tid == 0) bulk_wait0();

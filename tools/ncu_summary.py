@@ -25,7 +25,8 @@ stalls = sorted(((k.replace("smsp__pcsamp_warps_issue_stalled_", ""), float(x or
 tot = sum(x for _, x in stalls) or 1
 print("stall samples:", ", ".join(f"{k} {100*x/tot:.1f}%" for k, x in stalls[:8]))
 src = list(csv.reader(io.StringIO(run("--page", "source", "--csv", "--print-source", "sass"))))
-hh = src[1]; data = src[2:]
+hi = [i for i, r in enumerate(src) if "Source" in r and "Instructions Executed" in r][0]
+hh = src[hi]; data = [r for r in src[hi + 1:] if len(r) == len(hh) and "Source" not in r]
 iS, iE, iW = hh.index("Source"), hh.index("Instructions Executed"), hh.index("Warp Stall Sampling (All Samples)")
 print("top stall PCs:")
 for r in sorted(data, key=lambda r: -float(r[iW] or 0))[:top]:
