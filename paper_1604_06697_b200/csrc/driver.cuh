@@ -32,6 +32,13 @@ constexpr int MAX_LEVELS = 128;
 constexpr int LEVEL_BATCH = 4;
 constexpr uint32_t POST_GRID = 148 * 8;
 constexpr int POST_THREADS = 256;
+// the sort's per-level k_post: one small CTA (a warp per child) per segment,
+// many resident per SM — deep levels have tens of thousands of segments
+#ifndef BQ_POST_LEVEL_THREADS
+#define BQ_POST_LEVEL_THREADS 256
+#endif
+constexpr int POST_LEVEL_THREADS = BQ_POST_LEVEL_THREADS;
+constexpr uint32_t POST_LEVEL_GRID = 148 * (2048 / POST_LEVEL_THREADS < 32 ? 2048 / POST_LEVEL_THREADS : 32);
 constexpr int MERGE_THREADS = 256, MERGE_IPT = 8;
 
 bq_status set_error(bq_status st, const char *fmt, ...);
@@ -261,7 +268,10 @@ bq_status validate(const void *data, size_t n, void *ws, size_t ws_bytes) {
 constexpr uint32_t FILL_GRID = 148 * 8;
 // equal bands up to this many elements are filled by k_post's CTA for the
 // segment; longer ones (duplicate-heavy inputs) tile-parallel by k_fill
-constexpr uint32_t BAND_INLINE_MAX = 1u << 16;
+#ifndef BQ_BAND_INLINE_MAX
+#define BQ_BAND_INLINE_MAX (1u << 16)
+#endif
+constexpr uint32_t BAND_INLINE_MAX = BQ_BAND_INLINE_MAX;
 
 // Equal bands left to k_fill (records: both phases).
 template <class KT>
@@ -844,7 +854,7 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
             Q.pass = P;
             Q.d_counts = nullptr;
             Q.nseg_dev = &prev->nseg_next;
-            k_post<KT, POST_THREADS><<<POST_GRID, POST_THREADS, 0, s>>>(Q);
+            k_post<KT, POST_LEVEL_THREADS><<<POST_LEVEL_GRID, POST_LEVEL_THREADS, 0, s>>>(Q);
             BQ_CKC(cudaGetLastError());
             local.kernel_launches++;
             st = launch_fill<KT>(Q, s);   // exits at once unless a band was too long for k_post
