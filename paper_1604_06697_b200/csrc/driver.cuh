@@ -35,7 +35,7 @@ constexpr int POST_THREADS = 256;
 // the sort's per-level k_post: one small CTA (a warp per child) per segment,
 // many resident per SM — deep levels have tens of thousands of segments
 #ifndef BQ_POST_LEVEL_THREADS
-#define BQ_POST_LEVEL_THREADS 256
+#define BQ_POST_LEVEL_THREADS 128
 #endif
 constexpr int POST_LEVEL_THREADS = BQ_POST_LEVEL_THREADS;
 constexpr uint32_t POST_LEVEL_GRID = 148 * (2048 / POST_LEVEL_THREADS < 32 ? 2048 / POST_LEVEL_THREADS : 32);
