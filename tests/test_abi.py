@@ -82,3 +82,37 @@ def test_product_path_never_touches_oracle():
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt, f
                 assert "liboracle" not in txt and "bq_oracle" not in txt, f
+
+
+def test_workspace_sizes_of_the_next_rows(lib):
+    """Host-only sizing of the §8(f) rows: the key+index kind, the records
+    workspace covering the key+index path, and the in-place partition's
+    workspace, which does not grow with n (N2)."""
+    so, _ = lib
+    for f in (so.bq_workspace_bytes, so.bq_inplace_workspace_bytes):
+        f.restype = ctypes.c_size_t
+        f.argtypes = [ctypes.c_int, ctypes.c_size_t]
+    n = 1 << 22
+    pair = so.bq_workspace_bytes(4, n)
+    assert 16 * n <= pair < 16 * n + 4 * n
+    rec = so.bq_workspace_bytes(3, n)
+    assert rec >= 16 * n + pair + 4 * n
+    assert so.bq_workspace_bytes(5, n) == 0                       # unknown kind
+    for kind in range(5):
+        small = so.bq_inplace_workspace_bytes(kind, 1000)
+        big = so.bq_inplace_workspace_bytes(kind, 1 << 30)
+        assert 0 < small <= big == so.bq_inplace_workspace_bytes(kind, 1 << 28)
+        assert big < (64 << 20)
+
+
+def test_options_struct_layout():
+    """bq_sort_options / bq_sort_stats as the binding declares them match the
+    header's field lists (eight int32 options; the stats' sizes)."""
+    import paper_1604_06697_b200.bq as b
+    src = open(HEADER).read()
+    body = src[src.index("typedef struct {\n    int32_t pivot_rule;"):src.index("} bq_sort_options;")]
+    n_fields = sum(int(m.group(2) or 1) for m in re.finditer(r"int32_t (\w+)(?:\[(\d+)\])?;", body))
+    assert ctypes.sizeof(b.bq_sort_options) == 4 * n_fields == 32
+    assert [f for f, _ in b.bq_sort_options._fields_][:7] == ["pivot_rule", "depth_limit", "timing", "ordered",
+                                                               "ways", "records", "subtree"]
+    assert ctypes.sizeof(b.bq_sort_stats) == 72
