@@ -129,13 +129,18 @@ template <> struct Tune<KPair> {
 
 template <class KT> constexpr int tile_elems() { return Tune<KT>::PART_THREADS * Tune<KT>::PART_IPT; }
 
-// Tiles are anchored at absolute multiples of TILE so that every interior tile
-// is 16-byte aligned: a segment [b, e) covers the tiles
-// floor(b/T) .. ceil(e/T)-1.
-__host__ __device__ inline uint32_t seg_ntiles(uint32_t b, uint32_t len, uint32_t T) {
-    if (len == 0) return 0;
-    uint64_t e = (uint64_t)b + len;
-    return (uint32_t)((e + T - 1) / T - b / T);
+// Tiles are laid out from each segment's 16-byte-aligned begin: with
+// ab = b rounded down to VW elements (VW = elements per 16 bytes), tile j of
+// [b, e) covers [ab + j*T, ab + (j+1)*T) ∩ [b, e).  Every tile starts 16-byte
+// aligned (a 1D TMA copy), interior tiles are full, and a
+// segment has ceil((e - ab) / T) tiles — not the extra partial tile that
+// anchoring at absolute multiples of T costs small segments.
+template <class KT>
+__host__ __device__ constexpr uint32_t tile_vw() { return sizeof(typename KT::T) >= 16 ? 1u : 16u / (uint32_t)sizeof(typename KT::T); }
+template <class KT>
+__host__ __device__ inline uint32_t seg_tiles(uint32_t b, uint32_t len) {
+    constexpr uint32_t T = (uint32_t)tile_elems<KT>();
+    return (uint32_t)(((uint64_t)len + b % tile_vw<KT>() + T - 1) / T);
 }
 
 // ---------------------------------------------------------------------------

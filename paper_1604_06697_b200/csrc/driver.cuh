@@ -318,7 +318,7 @@ bq_status run_pass(const typename KT::T *src, typename KT::T *dst, typename KT::
         BQ_CK(cudaMemsetAsync(d_counts, 0, 3 * sizeof(uint64_t), s));
         return BQ_OK;
     }
-    const uint32_t ntiles = seg_ntiles(0, (uint32_t)n, TILE);
+    const uint32_t ntiles = seg_tiles<KT>(0, (uint32_t)n);
     if (ordered || KT::is_record) BQ_CK(cudaMemsetAsync(status, 0, ntiles * sizeof(uint64_t), s));
     BQ_CK(cudaMemsetAsync(ctrl, 0, sizeof(LevelCtrl), s));
     BQ_CK(cudaMemsetAsync(cursor, 0, sizeof(unsigned long long), s));
@@ -530,7 +530,7 @@ bq_status run_partition_segments(const typename KT::T *src, typename KT::T *dst,
     for (size_t i = 0; i < nseg; i++) {
         if (lens[i] == 0 || (uint64_t)begins[i] + lens[i] > n)
             return set_error(BQ_ERR_INVALID_ARGUMENT, "segment %zu out of range or empty", i);
-        const uint32_t nt = seg_ntiles(begins[i], lens[i], TILE);
+        const uint32_t nt = seg_tiles<KT>(begins[i], lens[i]);
         hs[i] = Seg{(uint64_t)pivot_keys[i], begins[i], lens[i], (uint32_t)tiles, nt, 0, 0, 0, 0};
         tiles += nt;
         maxtiles = nt > maxtiles ? nt : maxtiles;

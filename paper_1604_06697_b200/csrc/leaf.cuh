@@ -457,6 +457,9 @@ cudaError_t launch_leaf_l(const LeafParams<KT> &LP, uint32_t count, cudaStream_t
         if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_leaf<KT, L>, NT, smem)) != cudaSuccess) return e;
         if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
         if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+#ifdef BQ_LEAF_CTAS_PER_SM
+        if (nb > BQ_LEAF_CTAS_PER_SM) nb = BQ_LEAF_CTAS_PER_SM;   // leave room for co-resident partition CTAs
+#endif
         cap = (nb > 0 ? nb : 1) * sms;
     }
     k_leaf<KT, L><<<count ? count : (uint32_t)cap, NT, smem, s>>>(LP);

@@ -5,8 +5,9 @@
 // elements, stores *every* offset and advances a counter by the comparison
 // outcome (Alg. 3 l.8-9, 15-16), then swaps buffered pairs.  Here
 // one CTA owns a tile of TILE elements:
-//   a2  coalesced 128-bit loads of the tile (tiles anchored at absolute
-//       multiples of TILE, masked at segment ends);
+//   a2  coalesced 128-bit loads of the tile (tiles laid out from the
+//       segment's 16-byte-aligned begin, common.cuh seg_tiles; slots outside
+//       the segment masked);
 //   a3  three-way classification against the pivot; `__ballot_sync` per item
 //       slot + `__popc(mask & lanemask_lt)` give every key its rank among the
 //       < (resp. >, =) keys of its warp chunk — the offsets buffers — and one
@@ -226,7 +227,7 @@ __device__ __forceinline__ void emit_children(const PostParams<KT> &Q, int nch, 
             ch.pivot = s_piv[c];
             ch.begin = cb[c];
             ch.len = len;
-            ch.ntiles = seg_ntiles(cb[c], len, TILE);
+            ch.ntiles = seg_tiles<KT>(cb[c], len);
             ch.depth = cd;
             ch.parity = cp;
             ch.pad0 = (uint8_t)s_mode[c];   // records: bit 0 = [<= p | > p] pass, bit 1 = pivot duplicated
@@ -361,7 +362,7 @@ __global__ void __launch_bounds__(NT) k_fill(PostParams<KT> Q, int phase) {
         const SegCounts<KT> cn = seg_counts(P, si, sg);
         if (cn.E <= Q.band_inline_max) continue;
         const uint64_t b = sg.begin;
-        const uint64_t tbeg = (b / TILE) * TILE + (uint64_t)(t - sg.tile_base) * TILE;
+        const uint64_t tbeg = b / tile_vw<KT>() * tile_vw<KT>() + (uint64_t)(t - sg.tile_base) * TILE;
         const uint64_t band0 = b + cn.L, band1 = band0 + cn.E;
         const uint64_t x0 = tbeg > band0 ? tbeg : band0;
         const uint64_t x1 = (tbeg + TILE) < band1 ? (tbeg + TILE) : band1;

@@ -74,9 +74,10 @@ struct TileGeom {
     uint64_t b, e, tbeg;
     uint32_t vlo, vhi;   // valid tile-local range [vlo, vhi)
     __device__ TileGeom(const Seg &sg, uint32_t t) {
+        constexpr uint32_t VW = tile_vw<KT>();
         b = sg.begin;
         e = b + sg.len;
-        tbeg = (b / TILE) * TILE + (uint64_t)(t - sg.tile_base) * TILE;
+        tbeg = b / VW * VW + (uint64_t)(t - sg.tile_base) * TILE;   // common.cuh seg_tiles
         vlo = (uint32_t)((tbeg > b ? tbeg : b) - tbeg);
         vhi = (uint32_t)(((tbeg + TILE) < e ? (tbeg + TILE) : e) - tbeg);
     }
