@@ -110,9 +110,12 @@ template <> struct Tune<KI32> {
                          PART_MINB = BQ_I32_MINB;
     static constexpr int LEAF = BQ_I32_LEAF, LEAF_THREADS = 512;
 };
+#ifndef BQ_U64_LEAF
+#define BQ_U64_LEAF 4096
+#endif
 template <> struct Tune<KU64> {
     static constexpr int PART_THREADS = 256, PART_IPT = 8, PART_STAGES = 4, PART_MINB = 2;   // 16 KB tiles
-    static constexpr int LEAF = 4096, LEAF_THREADS = 512;
+    static constexpr int LEAF = BQ_U64_LEAF, LEAF_THREADS = 512;
 };
 template <> struct Tune<KF64> : Tune<KU64> {};
 #ifndef BQ_REC_STAGES
@@ -180,11 +183,11 @@ struct alignas(64) LevelCtrl {
     uint32_t mw_ticket_count;    // tile tickets of the multiway count kernel
     unsigned long long element_passes;  // sum of partitioned lengths this level
     unsigned long long band_elems;      // equal-band elements this level
-    uint32_t nleaf_cls[4];              // leaves appended per network-size class
+    uint32_t nleaf_cls[8];              // leaves appended per network-size class
     uint32_t mw_ticket_scatter;  // tile tickets of the multiway scatter kernel
     uint32_t nmseg_next;         // multiway children appended to the next level
     uint32_t nmtiles_next;       // their tiles
-    uint32_t pad2[13];
+    uint32_t pad2[9];
 };
 static_assert(sizeof(LevelCtrl) == 128, "LevelCtrl layout");
 

@@ -102,7 +102,7 @@ Layout<KT> make_layout(size_t n) {
     L.subs[0] = take(L.max_segs * sizeof(Leaf));
     L.subs[1] = take(L.max_segs * sizeof(Leaf));
     L.ctrl = take((MAX_LEVELS + 1) * sizeof(LevelCtrl));   // [MAX_LEVELS]: the root's counts
-    L.misc = take(256);   // fallback count, leaf-list counts (2 sets x 4 classes), pass counts
+    L.misc = take(256);   // fallback count, leaf-list counts (2 sets x 8 classes), copy/subtree counts; pass counts
     L.total = off;
     return L;
 }
@@ -679,12 +679,14 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
     LevelCtrl *ctrl = reinterpret_cast<LevelCtrl *>(w + L.ctrl);
     LevelCtrl *root = ctrl + MAX_LEVELS;
     uint32_t *fb_count = reinterpret_cast<uint32_t *>(w + L.misc);
-    uint32_t *leaf_counts[2] = {fb_count + 4, fb_count + 8};   // [set][class]
-    uint32_t *copy_counts[2] = {fb_count + 12, fb_count + 13};
+    // misc words: [0] fallback count, [4, 12) / [12, 20) leaf counts of set 0 / 1
+    // (by class), [20, 22) copy counts, [22, 24) subtree job counts, [24] overflow
+    uint32_t *leaf_counts[2] = {fb_count + 4, fb_count + 12};   // [set][class]
+    uint32_t *copy_counts[2] = {fb_count + 20, fb_count + 21};
     Leaf *copies[2] = {reinterpret_cast<Leaf *>(w + L.copies[0]), reinterpret_cast<Leaf *>(w + L.copies[1])};
     Leaf *subs[2] = {reinterpret_cast<Leaf *>(w + L.subs[0]), reinterpret_cast<Leaf *>(w + L.subs[1])};
-    uint32_t *sub_counts[2] = {fb_count + 14, fb_count + 15};
-    uint32_t *overflow = fb_count + 16;
+    uint32_t *sub_counts[2] = {fb_count + 22, fb_count + 23};
+    uint32_t *overflow = fb_count + 24;
     // N1: subtrees of <= SUB elements finished on chip (bq_sort_options.subtree)
     const uint32_t sub_max = (sub_enabled<KT>() && subtree) ? sub_elems<KT>() : 0;
 
@@ -735,7 +737,7 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
     }
 
     BQ_CKC(cudaMemsetAsync(ctrl, 0, (MAX_LEVELS + 1) * sizeof(LevelCtrl), s));
-    BQ_CKC(cudaMemsetAsync(fb_count, 0, 17 * sizeof(uint32_t), s));
+    BQ_CKC(cudaMemsetAsync(fb_count, 0, 25 * sizeof(uint32_t), s));
     const int aligned = aligned16(user) && aligned16(scratch);
     // children sink of level `lv` (its children form level lv+1; the root is
     // the only "child" of the virtual level -1, counted in `root`)
@@ -790,7 +792,7 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
         }
         // the side stream has finished the leaves of batch-2 (same set)
         if (batch >= 2) BQ_CKC(cudaStreamWaitEvent(s, ev_leaves[set], 0));
-        BQ_CKC(cudaMemsetAsync(leaf_counts[set], 0, 4 * sizeof(uint32_t), s));
+        BQ_CKC(cudaMemsetAsync(leaf_counts[set], 0, MAX_LEAF_CLASSES * sizeof(uint32_t), s));
         BQ_CKC(cudaMemsetAsync(copy_counts[set], 0, sizeof(uint32_t), s));
         if (batch > 0) BQ_CKC(cudaMemsetAsync(sub_counts[set], 0, sizeof(uint32_t), s));   // batch 0: the root may be one
         for (int k = 0; k < LEVEL_BATCH; k++, level++) {

@@ -55,17 +55,34 @@ struct RecKI {
 #ifndef BQ_LEAF_R32
 #define BQ_LEAF_R32 5
 #endif
+// 64-bit keys: 16 per thread at up to 1024 resident threads per SM (measured
+// on c3: 32 keys per thread at 256 threads left the SM latency-bound)
+#ifndef BQ_LEAF_R64
+#define BQ_LEAF_R64 4
+#endif
+#ifndef BQ_LEAF_OCC64
+#define BQ_LEAF_OCC64 1024
+#endif
+#ifndef BQ_LEAF_RREC
+#define BQ_LEAF_RREC 3
+#endif
+#ifndef BQ_LEAF_OCC32
+#define BQ_LEAF_OCC32 512
+#endif
+#ifndef BQ_LEAF_OCCREC
+#define BQ_LEAF_OCCREC 1024
+#endif
 template <class KT>
 struct LeafTraits {
     using E = typename KT::K;
-    static constexpr int R = sizeof(E) == 4 ? BQ_LEAF_R32 : 5;   // log2(keys per thread)
-    static constexpr int OCC = sizeof(E) == 4 ? 512 : 256;   // resident threads/SM the registers target
+    static constexpr int R = sizeof(E) == 4 ? BQ_LEAF_R32 : BQ_LEAF_R64;   // log2(keys per thread)
+    static constexpr int OCC = sizeof(E) == 4 ? BQ_LEAF_OCC32 : BQ_LEAF_OCC64;   // resident threads/SM the registers target
 };
 template <>
 struct LeafTraits<KRec> {
     using E = RecKI;
-    static constexpr int R = 4;
-    static constexpr int OCC = 512;
+    static constexpr int R = BQ_LEAF_RREC;
+    static constexpr int OCC = BQ_LEAF_OCCREC;
 };
 
 template <>
@@ -81,7 +98,7 @@ constexpr int leaf_lmax() {
 }
 template <class KT>
 constexpr int leaf_nclass() { return leaf_lmax<KT>() - leaf_lmin<KT>() + 1; }
-constexpr int MAX_LEAF_CLASSES = 4;   // LevelCtrl::nleaf_cls, leaf-count words per set
+constexpr int MAX_LEAF_CLASSES = 8;   // LevelCtrl::nleaf_cls, leaf-count words per set
 
 // network-size class of a leaf of `len` keys: NET = 2^(lmin + class)
 template <class KT>
