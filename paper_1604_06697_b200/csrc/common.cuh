@@ -121,13 +121,19 @@ template <> struct Tune<KF64> : Tune<KU64> {};
 #ifndef BQ_REC_STAGES
 #define BQ_REC_STAGES 4
 #endif
+#ifndef BQ_REC_LEAF
+#define BQ_REC_LEAF 2048
+#endif
+#ifndef BQ_PAIR_LEAF
+#define BQ_PAIR_LEAF 4096
+#endif
 template <> struct Tune<KRec> {
     static constexpr int PART_THREADS = 256, PART_IPT = 2, PART_STAGES = BQ_REC_STAGES, PART_MINB = 2;   // 16 KB tiles
-    static constexpr int LEAF = 2048, LEAF_THREADS = 512;
+    static constexpr int LEAF = BQ_REC_LEAF, LEAF_THREADS = 512;
 };
 template <> struct Tune<KPair> {
     static constexpr int PART_THREADS = 256, PART_IPT = 4, PART_STAGES = 4, PART_MINB = 2;   // 16 KB tiles
-    static constexpr int LEAF = 4096, LEAF_THREADS = 512;
+    static constexpr int LEAF = BQ_PAIR_LEAF, LEAF_THREADS = 512;
 };
 
 template <class KT> constexpr int tile_elems() { return Tune<KT>::PART_THREADS * Tune<KT>::PART_IPT; }
