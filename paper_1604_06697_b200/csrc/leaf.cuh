@@ -130,11 +130,22 @@ __device__ __forceinline__ void ce(RecKI &a, RecKI &b) {
     a = lo;
     b = hi;
 }
-__device__ __forceinline__ void flip_if(int32_t &a, uint32_t m) { a ^= (int32_t)m; }
-__device__ __forceinline__ void flip_if(uint64_t &a, uint32_t m) { a ^= (uint64_t)(int64_t)(int32_t)m; }
+// w ^ m for m in {0, ~0}, computed as w * (2m + 1) + m (m = ~0: -w - 1 = ~w)
+// with IMADs, which issue on the FMA pipe: the network's compare-exchanges
+// keep the ALU pipe busy, the FMA pipe is idle
+__device__ __forceinline__ uint32_t flip_w(uint32_t w, uint32_t m) {
+    uint32_t s, r;
+    asm("mad.lo.u32 %0, %1, 2, 1;" : "=r"(s) : "r"(m));
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(w), "r"(s), "r"(m));
+    return r;
+}
+__device__ __forceinline__ void flip_if(int32_t &a, uint32_t m) { a = (int32_t)flip_w((uint32_t)a, m); }
+__device__ __forceinline__ void flip_if(uint64_t &a, uint32_t m) {
+    a = ((uint64_t)flip_w((uint32_t)(a >> 32), m) << 32) | flip_w((uint32_t)a, m);
+}
 __device__ __forceinline__ void flip_if(RecKI &a, uint32_t m) {
-    a.k ^= (uint64_t)(int64_t)(int32_t)m;
-    a.i ^= m;
+    flip_if(a.k, m);
+    a.i = flip_w(a.i, m);
 }
 __device__ __forceinline__ int32_t shfl_x(int32_t v, int m) { return __shfl_xor_sync(0xffffffffu, v, m); }
 __device__ __forceinline__ uint64_t shfl_x(uint64_t v, int m) { return __shfl_xor_sync(0xffffffffu, v, m); }
