@@ -19,9 +19,37 @@ __global__ void k_ki_index(const KeyIdx16 *p, uint32_t *idx, uint64_t n) {
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
         idx[i] = (uint32_t)p[i].idx;
 }
+// the records in sorted order: random 32-byte reads, so each thread keeps
+// U of them in flight (their indices first, then the independent loads)
 __global__ void k_ki_gather(const Rec32 *r, const uint32_t *idx, Rec32 *g, uint64_t n) {
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
-        g[i] = r[idx[i]];
+    constexpr int U = 8;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    const uint4 *r4 = reinterpret_cast<const uint4 *>(r);
+    uint4 *g4 = reinterpret_cast<uint4 *>(g);
+    for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += stride * U) {
+        uint32_t k[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const uint64_t j = i0 + u * stride;
+            k[u] = j < n ? __ldcs(idx + j) : 0u;
+        }
+        uint4 v[U][2];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            if (i0 + u * stride < n) {
+                v[u][0] = __ldg(r4 + 2 * (uint64_t)k[u]);
+                v[u][1] = __ldg(r4 + 2 * (uint64_t)k[u] + 1);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const uint64_t j = i0 + u * stride;
+            if (j < n) {
+                __stcs(g4 + 2 * j, v[u][0]);
+                __stcs(g4 + 2 * j + 1, v[u][1]);
+            }
+        }
+    }
 }
 
 namespace detail {
