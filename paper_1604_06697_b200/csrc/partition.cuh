@@ -136,6 +136,44 @@ __device__ __forceinline__ SegCounts<KT> seg_counts(const PassParams<KT> &P, uin
 // becomes: both children are appended to the next level (with their pivot,
 // a1, their slice of the next tile map and a reset cursor), small ones to the
 // leaf lists, depth-capped ones to the fallback list.
+// Per-CTA statistics of the bookkeeping kernels: counted with shared-memory
+// atomics and added to the level's control block once per CTA (deep levels
+// have tens of thousands of segments; one global atomic per segment and
+// counter on the same address serialises in L2).
+struct PostStats {
+    unsigned long long passes, band_pass, band_child;
+    uint32_t nleaf, nfallback, maxtiles;
+    uint32_t nleaf_cls[MAX_LEAF_CLASSES];
+};
+__device__ __forceinline__ PostStats &post_stats() {
+    __shared__ PostStats s;
+    return s;
+}
+__device__ __forceinline__ void post_stats_init() {
+    if (threadIdx.x == 0) {
+        PostStats &st = post_stats();
+        st.passes = st.band_pass = st.band_child = 0;
+        st.nleaf = st.nfallback = st.maxtiles = 0;
+        for (int c = 0; c < MAX_LEAF_CLASSES; c++) st.nleaf_cls[c] = 0;
+    }
+    __syncthreads();
+}
+template <class KT>
+__device__ __forceinline__ void post_stats_flush(const PostParams<KT> &Q) {
+    __syncthreads();
+    if (threadIdx.x != 0 || !Q.emit_children) return;
+    const PostStats &st = post_stats();
+    LevelCtrl *P = Q.pass.ctrl, *C = Q.child_ctrl;
+    if (P && st.passes) atomicAdd(&P->element_passes, st.passes);
+    if (P && st.band_pass) atomicAdd(&P->band_elems, st.band_pass);
+    if (st.band_child) atomicAdd(&C->band_elems, st.band_child);
+    if (st.nleaf) atomicAdd(&C->nleaf, st.nleaf);
+    if (st.nfallback) atomicAdd(&C->nfallback, st.nfallback);
+    if (st.maxtiles) atomicMax(&C->maxtiles_next, st.maxtiles);
+    for (int c = 0; c < MAX_LEAF_CLASSES; c++)
+        if (st.nleaf_cls[c]) atomicAdd(&C->nleaf_cls[c], st.nleaf_cls[c]);
+}
+
 // a7 for up to MW_K children of one segment (or the root), by a whole CTA of
 // NT threads: each child becomes nothing (empty), a leaf (<= S), a
 // depth-capped fallback segment, or a next-level segment — multiway when
@@ -206,17 +244,17 @@ __device__ __forceinline__ void emit_children(const PostParams<KT> &Q, int nch, 
             // leaf lists are binned by sorting-network size (leaf.cuh)
             const uint32_t lc = leaf_class<KT>(len);
             const uint32_t li = atomicAdd(&Q.leaf_counts[lc], 1u);
-            atomicAdd(&C->nleaf_cls[lc], 1u);
-            atomicAdd(&C->nleaf, 1u);
+            atomicAdd(&post_stats().nleaf_cls[lc], 1u);
+            atomicAdd(&post_stats().nleaf, 1u);
             Q.leaves[lc * Q.leaf_cap + li] = Leaf{cb[c], len, cp, 0};
         } else if (kind == C_SUB) {
             Q.subs[atomicAdd(Q.sub_count, 1u)] = Leaf{cb[c], len, cp, cd};
         } else if (kind == C_FALLBACK) {
             const uint32_t fi = atomicAdd(Q.fallback_count, 1u);
-            atomicAdd(&C->nfallback, 1u);
+            atomicAdd(&post_stats().nfallback, 1u);
             Q.fallback[fi] = Leaf{cb[c], len, cp, 0};
         } else if (kind == C_BAND) {
-            atomicAdd(&C->band_elems, (unsigned long long)len);
+            atomicAdd(&post_stats().band_child, (unsigned long long)len);
             if (cp != 0)   // in the scratch buffer: copy to the user buffer in chunks
                 for (uint32_t off = 0; off < len; off += 65536) {
                     const uint32_t ci = atomicAdd(Q.copy_count, 1u);
@@ -235,7 +273,7 @@ __device__ __forceinline__ void emit_children(const PostParams<KT> &Q, int nch, 
             uint32_t ci;
             if (kind == C_BIN) {
                 ch.tile_base = atomicAdd(&C->ntiles_next, ch.ntiles);
-                atomicMax(&C->maxtiles_next, ch.ntiles);
+                atomicMax(&post_stats().maxtiles, ch.ntiles);
                 ci = atomicAdd(&C->nseg_next, 1u);
                 Q.next_segs[ci] = ch;
                 Q.next_cursor[ci] = 0;
@@ -277,7 +315,9 @@ __device__ __forceinline__ void post_segment(const PostParams<KT> &Q, uint32_t s
 template <class KT, int NT>
 __global__ void __launch_bounds__(NT) k_post(PostParams<KT> Q) {
     const uint32_t nseg = Q.nseg_dev ? *Q.nseg_dev : Q.nseg;
+    post_stats_init();
     for (uint32_t si = blockIdx.x; si < nseg; si += gridDim.x) post_segment<KT, NT>(Q, si);
+    post_stats_flush(Q);
 }
 
 template <class KT, int NT>
@@ -325,8 +365,8 @@ __device__ __forceinline__ void post_segment(const PostParams<KT> &Q, uint32_t s
     if (!Q.emit_children) return;
 
     if (threadIdx.x == 0) {
-        atomicAdd(&C->element_passes, (unsigned long long)sg.len);
-        atomicAdd(&C->band_elems, (unsigned long long)E);
+        atomicAdd(&post_stats().passes, (unsigned long long)sg.len);
+        atomicAdd(&post_stats().band_pass, (unsigned long long)E);
     }
     if (KT::is_record && !P.ordered) {
         // two-way records (E == 0): [< p | >= p], the right side followed up by
@@ -404,7 +444,9 @@ static __global__ void k_map(const Seg *segs, uint32_t *tile_map, uint64_t *stat
 template <class KT, int NT>
 __global__ void __launch_bounds__(NT) k_init_root(PostParams<KT> Q, uint32_t n) {
     const uint32_t cb[1] = {0}, cl[1] = {n};
+    post_stats_init();
     emit_children<KT, NT>(Q, 1, cb, cl, 0, 0);
+    post_stats_flush(Q);
 }
 
 // a7 after a multiway scatter: the (up to) 16 buckets of every multiway
@@ -413,6 +455,7 @@ template <class KT, int NT>
 __global__ void __launch_bounds__(NT) k_post_mw(PostParams<KT> Q) {
     __shared__ uint32_t cb[MW_K], cl[MW_K];
     const uint32_t nseg = *Q.mw.nseg_dev;
+    post_stats_init();
     for (uint32_t si = blockIdx.x; si < nseg; si += gridDim.x) {
         const MSeg<KT> &m = Q.mw.msegs[si];
         if (threadIdx.x < MW_K) {
@@ -421,6 +464,7 @@ __global__ void __launch_bounds__(NT) k_post_mw(PostParams<KT> Q) {
         }
         emit_children<KT, NT>(Q, MW_K, cb, cl, (uint8_t)(m.s.parity ^ 1), (uint16_t)(m.s.depth + 1));
     }
+    post_stats_flush(Q);
 }
 
 // Finished runs of equal record keys still in the scratch buffer -> user

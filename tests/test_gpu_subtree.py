@@ -56,12 +56,14 @@ def test_subtree_patterns(B, kind, pattern):
 
 
 def test_subtree_depth_cap_inside(B):
-    """A small depth limit makes pieces inside a subtree hit the cap: they go
-    to the fallback sort, and the output is still exact."""
+    """A small depth limit makes segments around the subtree size hit the cap
+    (at the level passes or inside a subtree, depending on the pivots the
+    atomic placement leads to): they go to the fallback sort, and the output
+    is still exact."""
     n = 200_000
     a = make("i32", n, seed=12)
     t = to_dev(a)
-    st = B.bq_sort_ex(t, subtree=True, depth_limit=6)
+    st = B.bq_sort_ex(t, subtree=True, depth_limit=4)
     check_sorted_equal("i32", to_host(t, a), a)
     assert st["fallback_segments"] > 0
 
