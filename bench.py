@@ -312,7 +312,18 @@ def main():
                 times.append(a.elapsed_time(b))
             return times[1:]
         times = passes(False)          # the sort's placement (atomic cursor)
-        times_ord = passes(True)       # bq_partition's deterministic layout (decoupled look-back)
+        times_ord = passes(True)       # the deterministic layout (decoupled look-back)
+        times_ip = []                  # bq_partition_i32: the in-place block partition (N2)
+        for _ in range(args.passes + 1):
+            data.copy_(src)
+            flush.fill_(1)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            bq.bq_partition_i32(data, pv, ws=ws, stream=stream)
+            b.record(stream)
+            torch.cuda.synchronize()
+            times_ip.append(a.elapsed_time(b))
+        times_ip = times_ip[1:]
         del flush
         pbytes = 2 * 4 * n
         med, mn = statistics.median(times), min(times)
@@ -324,10 +335,14 @@ def main():
                  "frac_of_8tbs_median": pbytes / (med * 1e-3) / 1e9 / 8000.0,
                  "ordered_ms_median": statistics.median(times_ord),
                  "ordered_gbs_median": pbytes / (statistics.median(times_ord) * 1e-3) / 1e9,
+                 "inplace_ms_median": statistics.median(times_ip),
+                 "inplace_gbs_median": pbytes / (statistics.median(times_ip) * 1e-3) / 1e9,
                  "note": "one bq_partition_pass (partition kernel + per-segment counts + band kernel) "
                          "over the pristine c2 input around its Mo3 pivot, atomic-cursor placement as "
                          "in the sort; L2 flushed (512 MiB write) before each; ordered_* = the "
-                         "decoupled look-back placement of bq_partition_*"}
+                         "deterministic decoupled look-back placement (bq_partition_pass ordered=1); "
+                         "inplace_* = bq_partition_i32, the in-place block partition (N2) with its "
+                         "equal band, input restored before each call"}
 
     # end to end through the public API with host buffers
     e2e = None

@@ -136,7 +136,8 @@ typedef struct {
 
 /* Workspace bytes every call below needs for `n` elements of `kind`:
  * an n*w scratch buffer for the out-of-place partition passes plus O(n/T)
- * bytes of tile status words, segment descriptors and leaf lists.  For
+ * bytes of tile status words, segment descriptors and leaf lists (and at
+ * least bq_inplace_workspace_bytes(kind, n)).  For
  * BQ_REC32 it also covers the key+index sort path: 16n bytes of pairs, the
  * workspace of BQ_KEYIDX16 and 4n bytes of gather indices (about 36n). */
 BQ_API size_t bq_workspace_bytes(bq_kind kind, size_t n);
@@ -159,10 +160,13 @@ BQ_API bq_status bq_pivot_records(const bq_record32 *recs, size_t n, bq_pivot_ru
  *     [0, split)                  < pivot
  *     [split, split + n_equal)   == pivot
  *     [split + n_equal, n)        > pivot
- * with split = #{k < pivot}, and preserves the multiset.  The layout is
- * deterministic: the < keys keep their input order, the > keys appear in
- * reverse input order.  Returns split and n_equal to the host (synchronises
- * `stream`).  A NaN f64 pivot is BQ_ERR_INVALID_ARGUMENT. */
+ * with split = #{k < pivot}, and preserves the multiset (records move whole).
+ * This is the in-place block partition (the same algorithm as
+ * bq_partition_inplace): blocks are neutralized from both ends by swapping
+ * misplaced keys, so the order inside each band is unspecified (for a
+ * deterministic layout use bq_partition_pass with ordered = 1).  Returns split
+ * and n_equal to the host (synchronises `stream`).  A NaN f64 pivot is
+ * BQ_ERR_INVALID_ARGUMENT. */
 BQ_API bq_status bq_partition_i32(int32_t *keys, size_t n, int32_t pivot, size_t *split,
                                   size_t *n_equal, void *ws, size_t ws_bytes, void *stream);
 BQ_API bq_status bq_partition_u64(uint64_t *keys, size_t n, uint64_t pivot, size_t *split,

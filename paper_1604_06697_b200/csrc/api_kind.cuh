@@ -51,7 +51,10 @@ BQ_DETAIL_DECLS(pair)
 #define BQ_DETAIL_DEFS(SUF, KT)                                                                     \
     namespace bq {                                                                                  \
     namespace detail {                                                                              \
-    size_t ws_##SUF(size_t n) { return make_layout<KT>(n).total; }                                  \
+    size_t ws_##SUF(size_t n) {                                                                     \
+        const size_t a = make_layout<KT>(n).total, b = make_ip_layout<KT>(n).total;                 \
+        return a > b ? a : b;                                                                       \
+    }                                                                                               \
     size_t ipws_##SUF(size_t n) { return make_ip_layout<KT>(n).total; }                             \
     bq_status inplace_##SUF(void *data, size_t n, const void *pivot, size_t *split, size_t *neq,     \
                             void *ws, size_t wsb, cudaStream_t s) {                                 \

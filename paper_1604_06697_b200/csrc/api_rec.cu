@@ -92,8 +92,8 @@ static bq_status sort_rec_ki(Rec32 *data, size_t n, const bq_sort_options *opt, 
 }
 
 size_t ws_rec(size_t n) {
-    const size_t a = make_layout<KRec>(n).total, b = ki_layout(n).total;
-    return a > b ? a : b;
+    const size_t a = make_layout<KRec>(n).total, b = ki_layout(n).total, c = make_ip_layout<KRec>(n).total;
+    return a > b ? (a > c ? a : c) : (b > c ? b : c);
 }
 size_t ipws_rec(size_t n) { return make_ip_layout<KRec>(n).total; }
 bq_status inplace_rec(void *data, size_t n, const void *pivot, size_t *split, size_t *neq, void *ws, size_t wsb,

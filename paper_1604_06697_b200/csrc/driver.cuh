@@ -361,27 +361,17 @@ bq_status run_pivot(const typename KT::T *data, size_t n, int rule, uint64_t *ke
     return BQ_OK;
 }
 
-// In-place three-way partition: keys -> scratch pass, copy back, read counts.
+// bq_partition_*: the in-place block partition (N2, run_partition_inplace_ip
+// below), after the checks every entry point makes.
+template <class KT>
+bq_status run_partition_inplace_ip(typename KT::T *data, size_t n, typename KT::K pk, size_t *split,
+                                   size_t *n_equal, void *ws, size_t ws_bytes, cudaStream_t s);
 template <class KT>
 bq_status run_partition_inplace(typename KT::T *data, size_t n, typename KT::K pivot_key, size_t *split,
                                 size_t *n_equal, void *ws, size_t ws_bytes, cudaStream_t s) {
-    using T = typename KT::T;
     bq_status st = validate<KT>(data, n, ws, ws_bytes);
     if (st != BQ_OK) return st;
-    const Layout<KT> L = make_layout<KT>(n);
-    char *w = static_cast<char *>(ws);
-    T *scratch = reinterpret_cast<T *>(w + L.scratch);
-    uint64_t *counts = reinterpret_cast<uint64_t *>(w + L.misc);
-    // records stage their equal elements in the (already consumed) input
-    st = run_pass<KT>(data, scratch, data, n, pivot_key, counts, ws, s, /*ordered=*/1);
-    if (st != BQ_OK) return st;
-    if (n) BQ_CK(cudaMemcpyAsync(data, scratch, n * sizeof(T), cudaMemcpyDeviceToDevice, s));
-    uint64_t h[3] = {0, 0, 0};
-    BQ_CK(cudaMemcpyAsync(h, counts, sizeof h, cudaMemcpyDeviceToHost, s));
-    BQ_CK(cudaStreamSynchronize(s));
-    if (split) *split = (size_t)h[0];
-    if (n_equal) *n_equal = (size_t)h[1];
-    return BQ_OK;
+    return run_partition_inplace_ip<KT>(data, n, pivot_key, split, n_equal, ws, ws_bytes, s);
 }
 
 // ---- N2: in-place block partition (inplace.cuh) ------------------------------

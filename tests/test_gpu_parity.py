@@ -200,18 +200,49 @@ def _pivots(kind, a):
     return ps
 
 
+def _bands_ok(kind, a, got, pv, split, neq):
+    """The partition invariants (the unique part of a partition's output):
+    the three bands hold exactly the keys <, == and > the pivot, and the
+    multiset (for records: every row whole) is preserved."""
+    if kind == "f64":
+        k, pk = f64_key(got), f64_key(np.array([pv]))[0]
+        assert np.array_equal(np.sort(got.view(np.uint64)), np.sort(a.view(np.uint64)))
+    elif kind == "rec32":
+        k, pk = got[:, 0], np.uint64(pv)
+        idx = got[:, 1].astype(np.int64)
+        assert np.array_equal(np.sort(idx), np.arange(len(a)))
+        assert (got[:, 1] == got[:, 2]).all() and (got[:, 2] == got[:, 3]).all()
+        assert np.array_equal(got[:, 0], a[idx, 0])
+    else:
+        k, pk = got, np.array(pv, dtype=a.dtype)
+        assert np.array_equal(np.sort(got), np.sort(a))
+    assert (k[:split] < pk).all() and (k[split:split + neq] == pk).all() and (k[split + neq:] > pk).all()
+
+
 @pytest.mark.parametrize("kind", ["i32", "u64", "f64", "rec32"])
 @pytest.mark.parametrize("dist", ["random", "dups"])
 def test_partition_vs_oracle(B, kind, dist):
+    """bq_partition_* (in place, N2): split and n_equal exactly the oracle's,
+    the band invariants and the multiset; the ordered out-of-place pass on the
+    same input: exactly the oracle's deterministic layout (the three-list
+    definition, gpu_util.three_list)."""
     for n in edge_sizes(kind):
         a = make(kind, n, seed=n + 5, dist=dist)
         for p in _pivots(kind, a):
-            t = to_dev(a)
             pv = float(p) if kind == "f64" else int(p)
-            split, neq = B.partition(t, pv)
             _, s_o, e_o = oracle.partition(a, pv)
+            t = to_dev(a)
+            split, neq = B.partition(t, pv)
             assert (split, neq) == (s_o, e_o)
-            got = to_host(t, a)
+            _bands_ok(kind, a, to_host(t, a), pv, split, neq)
+            if n == 0:
+                continue
+            src = to_dev(a)
+            dst = torch.empty_like(src)
+            counts = torch.zeros(3, dtype=torch.int64, device="cuda")
+            B.bq_partition_pass(src, dst, pv, counts, ordered=True)
+            assert counts.cpu().tolist()[:2] == [s_o, e_o]
+            got = to_host(dst, a)
             if kind == "f64":
                 exp = three_list(a, f64_key(np.array([pv]))[0], key=f64_key)
                 assert np.array_equal(got.view(np.uint64), exp.view(np.uint64))
