@@ -104,10 +104,12 @@ typedef struct {
                              deterministic layout; 0: one atomicAdd per tile (faster; tiles
                              of a segment placed in completion order).  Records always
                              use the ordered placement.  Sorted keys are identical. */
-    int32_t ways;         /* 0 (default) or 2: binary three-way passes; 16 (keys only):
-                             multi-pivot block partition, 16-way passes (
-                             segments whose sample has duplicate splitters use the binary
-                             three-way pass).  Records always use the binary pass. */
+    int32_t ways;         /* 0 (default): binary passes for int32 keys and 32-byte records,
+                             8-way passes for uint64/float64 keys and key+index pairs (so
+                             also for bq_sort_records' default path); 2: binary; 8 or 16:
+                             multi-pivot block partition (segments whose
+                             sample has duplicate splitters use the binary pass).  32-byte
+                             records always use the binary pass. */
     int32_t records;      /* records only: 0 (default) or 2: key+index path — the passes move
                              16-byte (key, position) pairs (bq_keyidx16) instead of 32-byte
                              records and every record is gathered once at the end (P:867-870:

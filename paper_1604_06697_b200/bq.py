@@ -293,8 +293,9 @@ def _opts(pivot_rule, depth_limit, timing, ordered=False, ways=0, records=0, sub
 
 def bq_sort_ex(data, pivot_rule=BQ_PIVOT_SAMPLE64, depth_limit=-1, timing=False, ordered=False, ways=0,
                records=RECORDS_DEFAULT, subtree=False, ws=None, stream=None):
-    """Kind-generic sort; returns the bq_sort_stats as a dict.  ways: 0 / 2
-    binary passes (default), 8 or 16 multi-pivot passes (keys).  records:
+    """Kind-generic sort; returns the bq_sort_stats as a dict.  ways: 0 the
+    default per kind (binary for int32 and records, 8-way for 64-bit keys and
+    key+index pairs), 2 binary, 8 or 16 multi-pivot passes.  records:
     RECORDS_DEFAULT / RECORDS_KEYIDX sort (key, index) pairs and gather the
     records once, RECORDS_DIRECT moves the records in every pass.  subtree:
     finish segments of up to 96 KB in shared memory (N1)."""

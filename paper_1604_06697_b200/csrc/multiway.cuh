@@ -34,6 +34,10 @@
 namespace bq {
 
 constexpr int MW_K = 16;         // buckets of a multiway segment
+// element types the multiway kernels move: keys, and the 16-byte key+index
+// pairs (one element per 16-byte vector); 32-byte records stay binary
+template <class KT>
+constexpr bool mw_capable() { return !KT::is_record || sizeof(typename KT::T) == 16; }
 constexpr int MW_SAMPLE = 256;   // sample keys per segment (8 per lane of one warp)
 
 template <class KT>

@@ -212,6 +212,15 @@ __device__ __forceinline__ void emit_children(const PostParams<KT> &Q, int nch, 
             kind = C_BIN;
             mode = 1;
             if (lane == 0) s_piv[c] = hint_pivot;
+        } else if (mw_capable<KT>() && Q.ways > 2 && !(KT::is_record && Q.pass.ordered)) {
+            K node, piv;
+            const bool ok = mw_splitters<KT>(cbuf, cb[c], len, Q.leaf_max, lane, node, piv, (uint32_t)Q.ways);
+            kind = ok ? C_MW : C_BIN;
+            if (lane == 0) s_piv[c] = (uint64_t)piv;
+            if (lane < MW_K) s_tree[c][lane] = node;
+            // records falling back to the binary pass: their sample showed
+            // duplicates, so the two-way pass gets its follow-up (mode bit 1)
+            if (KT::is_record && !ok) mode = 2;
         } else if (KT::is_record && !Q.pass.ordered) {
             // two-way records: a pivot repeated in its sample gets a follow-up pass
             bool dup = false;
@@ -219,12 +228,6 @@ __device__ __forceinline__ void emit_children(const PostParams<KT> &Q, int nch, 
             if (lane == 0) s_piv[c] = (uint64_t)piv;
             kind = C_BIN;
             mode = dup ? 2 : 0;
-        } else if (Q.ways > 2 && !KT::is_record) {
-            K node, piv;
-            const bool ok = mw_splitters<KT>(cbuf, cb[c], len, Q.leaf_max, lane, node, piv, (uint32_t)Q.ways);
-            kind = ok ? C_MW : C_BIN;
-            if (lane == 0) s_piv[c] = (uint64_t)piv;
-            if (lane < MW_K) s_tree[c][lane] = node;
         } else {
             const K piv = select_pivot_warp<KT>(cbuf, cb[c], len, Q.pivot_rule, lane);
             if (lane == 0) s_piv[c] = (uint64_t)piv;

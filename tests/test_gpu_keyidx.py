@@ -47,8 +47,11 @@ def edge_sizes():
                    3 * S_PAIR + 7, (1 << 16) + 3, (1 << 20) + 11})
 
 
+@pytest.mark.parametrize("ways", [0, 2, 16])
 @pytest.mark.parametrize("dist", ["random", "dups", "sorted", "reversed"])
-def test_sort_keyidx16(B, dist):
+def test_sort_keyidx16(B, dist, ways):
+    """Pairs sort by the multi-pivot passes by default (8-way, N4), by binary
+    two-way passes with ways = 2, 16-way with ways = 16."""
     for n in edge_sizes():
         k = bqgen.u64(n, n + 1)
         if dist == "dups":
@@ -59,7 +62,7 @@ def test_sort_keyidx16(B, dist):
             k = np.sort(k)[::-1].copy()
         a = pairs_from(k)
         t = to_dev(a)
-        st = B.bq_sort_ex(t)
+        st = B.bq_sort_ex(t, ways=ways)
         assert st["fallback_segments"] == 0
         check_pairs(a, to_host(t, a))
 
