@@ -125,7 +125,7 @@ template <> struct Tune<KF64> : Tune<KU64> {};
 #define BQ_REC_LEAF 2048
 #endif
 #ifndef BQ_PAIR_LEAF
-#define BQ_PAIR_LEAF 4096
+#define BQ_PAIR_LEAF 2048
 #endif
 template <> struct Tune<KRec> {
     static constexpr int PART_THREADS = 256, PART_IPT = 2, PART_STAGES = BQ_REC_STAGES, PART_MINB = 2;   // 16 KB tiles

@@ -17,7 +17,7 @@ from test_gpu_parity import check_sorted_equal, make
 
 pytestmark = pytest.mark.gpu
 
-T_PAIR, S_PAIR = 1024, 4096
+T_PAIR, S_PAIR = 1024, 2048
 
 
 @pytest.fixture(scope="module")
