@@ -104,9 +104,10 @@ typedef struct {
                              deterministic layout; 0: one atomicAdd per tile (faster; tiles
                              of a segment placed in completion order).  Records always
                              use the ordered placement.  Sorted keys are identical. */
-    int32_t ways;         /* 0 (default): binary passes for int32 keys and 32-byte records,
-                             8-way passes for uint64/float64 keys and key+index pairs (so
-                             also for bq_sort_records' default path); 2: binary; 8 or 16:
+    int32_t ways;         /* 0 (default): binary passes for int32 keys (8-way for
+                             2^17 < n <= 2^23) and 32-byte records, 8-way passes for
+                             uint64/float64 keys and key+index pairs (so also for
+                             bq_sort_records' default path); 2: binary; 8 or 16:
                              multi-pivot block partition (segments whose
                              sample has duplicate splitters use the binary pass).  32-byte
                              records always use the binary pass. */

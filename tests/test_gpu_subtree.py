@@ -63,7 +63,7 @@ def test_subtree_depth_cap_inside(B):
     n = 200_000
     a = make("i32", n, seed=12)
     t = to_dev(a)
-    st = B.bq_sort_ex(t, subtree=True, depth_limit=4)
+    st = B.bq_sort_ex(t, subtree=True, depth_limit=4, ways=2)
     check_sorted_equal("i32", to_host(t, a), a)
     assert st["fallback_segments"] > 0
 
