@@ -88,17 +88,23 @@ __global__ void __launch_bounds__(NT + 32, MINB) k_part_fast(PassParams<KT> P) {
     // -------------------------------------------------------------- loader ----
     if (warp == NW) {
         if (lane != 0) return;
+        // the next ticket is claimed one tile ahead, so the atomic's L2 round
+        // trip overlaps this tile's metadata reads and the wait for a free
+        // stage (a claimed ticket is always processed: the loop stops only on
+        // a ticket >= ntiles, and every later one is larger)
+        uint32_t t_next = atomicAdd(&P.ctrl->ticket, 1u);
         for (uint32_t i = 0;; i++) {
             const uint32_t s = i % STAGES;
+            const uint32_t t = t_next;
+            if (t < ntiles) t_next = atomicAdd(&P.ctrl->ticket, 1u);
+            const uint32_t si = (P.tile_map && t < ntiles) ? P.tile_map[t] : 0;
+            const Seg sg = P.tile_map ? P.segs[si] : P.seg0;
             mbar_wait(&sm.empty[s], ((i / STAGES) & 1) ^ 1);
-            const uint32_t t = atomicAdd(&P.ctrl->ticket, 1u);
             sm.tile[s] = t;
             if (t >= ntiles) {
                 mbar_arrive(&sm.full[s]);
                 break;
             }
-            const uint32_t si = P.tile_map ? P.tile_map[t] : 0;
-            const Seg sg = P.tile_map ? P.segs[si] : P.seg0;
             sm.seg[s] = sg;
             sm.segidx[s] = si;
             const TileGeom<KT, TILE> G(sg, t);
