@@ -225,16 +225,19 @@ __device__ __forceinline__ void mw_loader(const MwParams<KT> &P, SM &sm, uint32_
     using T = typename KT::T;
     constexpr uint32_t TILE = NT * IPT;
     constexpr uint32_t W = sizeof(T), VW = 16 / W;
+    // the next ticket is claimed one tile ahead (as in k_part_fast's loader)
+    uint32_t t_next = atomicAdd(P.ticket, 1u);
     for (uint32_t i = 0;; i++) {
         const uint32_t s = i % STAGES;
+        const uint32_t t = t_next;
+        if (t < ntiles) t_next = atomicAdd(P.ticket, 1u);
+        const uint32_t si = t < ntiles ? P.tile_map[t] : 0;
         mbar_wait(&sm.empty[s], ((i / STAGES) & 1) ^ 1);
-        const uint32_t t = atomicAdd(P.ticket, 1u);
         sm.tile[s] = t;
         if (t >= ntiles) {
             mbar_arrive(&sm.full[s]);
             break;
         }
-        const uint32_t si = P.tile_map[t];
         const MSeg<KT> &ms = P.msegs[si];
         const Seg sg = ms.s;
 #pragma unroll
