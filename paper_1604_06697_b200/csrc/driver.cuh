@@ -384,7 +384,7 @@ struct IpLayout {
 };
 template <class KT>
 IpLayout<KT> make_ip_layout(size_t n) {
-    constexpr size_t TILE = tile_elems<KT>();
+    constexpr size_t TILE = ip_tile<KT>();
     IpLayout<KT> L;
     L.vmax = (IP_GMAX + 1) * TILE + 16 < n ? (IP_GMAX + 1) * TILE + 16 : n;
     size_t off = 0;
@@ -410,7 +410,7 @@ bq_status run_partition_inplace_ip(typename KT::T *data, size_t n, typename KT::
                                    size_t *n_equal, void *ws, size_t ws_bytes, cudaStream_t s) {
     using T = typename KT::T;
     using Kn = Kernels<KT>;
-    constexpr uint32_t TILE = tile_elems<KT>();
+    constexpr uint32_t TILE = ip_tile<KT>();
     if (n > 0x7fffffffull) return set_error(BQ_ERR_INVALID_ARGUMENT, "n = %zu exceeds 2^31-1", n);
     if (n > 0 && data == nullptr) return set_error(BQ_ERR_INVALID_ARGUMENT, "NULL data with n > 0");
     if (KT::is_record && !aligned16(data)) return set_error(BQ_ERR_INVALID_ARGUMENT, "records must be 16-byte aligned");
@@ -434,7 +434,7 @@ bq_status run_partition_inplace_ip(typename KT::T *data, size_t n, typename KT::
     T *s1 = reinterpret_cast<T *>(w + L.s1);
     T *s2 = reinterpret_cast<T *>(w + L.s2);
 
-    auto kern = k_inplace<KT, Kn::NT, Kn::IPT>;
+    auto kern = k_inplace<KT, Kn::NT, ip_ipt<KT>()>;
     constexpr int smem = inplace_smem_bytes<KT>();
     static int cap = 0;
     st = persistent_cap(kern, Kn::NT, smem, &cap);
@@ -460,7 +460,7 @@ bq_status run_partition_inplace_ip(typename KT::T *data, size_t n, typename KT::
         BQ_CK_LAUNCH();
         k_ip_plan<KT, 1024><<<1, 1024, 0, s>>>(q, leftover, pairs);
         BQ_CK_LAUNCH();
-        k_swap_blocks<KT, Kn::NT, Kn::IPT><<<grid, Kn::NT, 0, s>>>(data, q, pairs);
+        k_swap_blocks<KT, Kn::NT, ip_ipt<KT>()><<<grid, Kn::NT, 0, s>>>(data, q, pairs);
         BQ_CK_LAUNCH();
         k_vsplit<KT, Kn::NT, Kn::IPT><<<VG, Kn::NT, 0, s>>>(data, s2, q, (uint64_t)pk, k);
         BQ_CK_LAUNCH();
