@@ -443,22 +443,30 @@ bq_status run_partition_inplace_ip(typename KT::T *data, size_t n, typename KT::
     const size_t nb_max = n / TILE;
     if (nb_max < grid) grid = nb_max ? (uint32_t)nb_max : 1;
     constexpr uint32_t VG = 148 * 4;   // cleanup kernels: grid-stride over <= vmax elements
-    // the compaction lists (E then G) reuse the cleanup buffers s1, s2
-    const uint64_t list_cap = L.vmax * sizeof(T) / sizeof(uint32_t);
-    uint32_t *lists = reinterpret_cast<uint32_t *>(s1);
+    // pass 0 records the positions of keys equal to p in its final right
+    // blocks in s1 (unused by the cleanup); the equal band's compaction lists
+    // (E, G) take the two halves of s2 (used by pass 0's cleanup, not by pass 1's)
+    const uint32_t eqcap = (uint32_t)(L.vmax * sizeof(T) / sizeof(uint64_t));
+    uint64_t *eqpos = reinterpret_cast<uint64_t *>(s1);
+    const uint64_t list_cap = L.vmax * sizeof(T) / (2 * sizeof(uint32_t));
+    uint32_t *lists = reinterpret_cast<uint32_t *>(s2);
     for (int k = 0; k < 2; k++) {
         IpPass *q = ps + k;
-        k_ip_setup<KT><<<1, 1, 0, s>>>(data, q, k ? ps : nullptr, n, list_cap);
+        k_ip_setup<KT><<<1, 1, 0, s>>>(data, q, k ? ps : nullptr, n, list_cap, eqcap);
         BQ_CK_LAUNCH();
         if (k == 1) {
             k_eq_scan<KT, 256><<<148 * 8, 256, 0, s>>>(data, q, (uint64_t)pk, lists, lists + list_cap);
             BQ_CK_LAUNCH();
+            k_eq_scan2<KT, 256><<<148 * 2, 256, 0, s>>>(data, q, ps, (uint64_t)pk, lists, lists + list_cap, eqpos,
+                                                         eqcap);
+            BQ_CK_LAUNCH();
             k_eq_swap<KT><<<VG, 256, 0, s>>>(data, q, lists, lists + list_cap);
             BQ_CK_LAUNCH();
         }
-        kern<<<grid, Kn::NT, smem, s>>>(InplaceParams<KT>{data, q, (uint64_t)pk, k, leftover});
+        kern<<<grid, Kn::NT, smem, s>>>(
+            InplaceParams<KT>{data, q, (uint64_t)pk, k, leftover, k == 0 ? eqpos : nullptr, eqcap});
         BQ_CK_LAUNCH();
-        k_ip_plan<KT, 1024><<<1, 1024, 0, s>>>(q, leftover, pairs);
+        k_ip_plan<KT, 1024><<<1, 1024, 0, s>>>(q, leftover, pairs, k == 0 ? eqpos : nullptr, eqcap);
         BQ_CK_LAUNCH();
         k_swap_blocks<KT, Kn::NT, ip_ipt<KT>()><<<grid, Kn::NT, 0, s>>>(data, q, pairs);
         BQ_CK_LAUNCH();

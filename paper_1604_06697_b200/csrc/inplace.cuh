@@ -34,7 +34,8 @@ struct InplaceState {
     unsigned long long n_equal_held; // ... of them in the blocks held at the end (the middle)
     uint32_t nleftover;              // blocks a CTA held when its partner side ran out
     uint32_t left_ok;                // blocks claimed from the left (= the meeting point)
-    uint32_t pad[8];
+    uint32_t neqpos;                 // pass 0: positions recorded of keys equal to p in final right blocks
+    uint32_t pad[7];
 };
 static_assert(sizeof(InplaceState) == 64, "InplaceState layout");
 
@@ -50,6 +51,7 @@ struct IpPass {
     unsigned long long n_left, n_eq;     // results: end of the left part (absolute), keys equal to p
     unsigned long long cnt_eq, cnt_gt;   // compaction (pass 1): keys = p past the band, keys > p inside it
     uint32_t nb, active, npairs, compact;
+    uint32_t fast_eq, pad2;              // compaction from pass 0's recorded positions (no full scan)
 };
 
 template <class KT>
@@ -60,6 +62,8 @@ struct InplaceParams {
     uint64_t pivot;          // pivot key (KT::K)
     int mode;                // 0: left <=> key < p; 1: left <=> key <= p
     uint32_t *leftover;      // [2 * k]: block index, side (0 left, 1 right)
+    uint64_t *eqpos;         // mode 0: (block << 32 | offset) of keys equal to p in final right blocks
+    uint32_t eqcap;          // its capacity (more: the equal band falls back to a full scan)
 };
 
 // Three block buffers: the left block, the right block and a spare that the
@@ -78,6 +82,8 @@ struct InplaceSmem {
     uint32_t slot[2];                 // buffer of each side (3: the side is finished)
     uint32_t spare;
     uint32_t start[2], num[2], dirty[2], fresh[2];
+    uint32_t eqcnt[2];                // keys equal to p in each side's block (mode 0)
+    uint32_t weq[NW];                 // per-warp equal counts of a fresh block
 };
 
 // blocks of the in-place partition: PART_THREADS x ip_ipt elements; keys use
@@ -199,6 +205,7 @@ __global__ void __launch_bounds__(NT) k_inplace(InplaceParams<KT> P) {
 #pragma unroll
             for (int d = 16; d > 0; d >>= 1) ne += __shfl_xor_sync(0xffffffffu, ne, d);
             if (lane == 0 && ne) atomicAdd(&st->n_equal, (unsigned long long)ne);
+            if (lane == 0) sm.weq[warp] = ne;
             __syncthreads();
             uint32_t pre = 0, tot = 0;
 #pragma unroll
@@ -219,6 +226,9 @@ __global__ void __launch_bounds__(NT) k_inplace(InplaceParams<KT> P) {
                 sm.num[side] = tot;
                 sm.dirty[side] = 0;
                 sm.fresh[side] = 0;
+                uint32_t eq = 0;
+                for (uint32_t w2 = 0; w2 < NW; w2++) eq += sm.weq[w2];
+                sm.eqcnt[side] = eq;
             }
             __syncthreads();
         }
@@ -245,14 +255,38 @@ __global__ void __launch_bounds__(NT) k_inplace(InplaceParams<KT> P) {
         }
         T *L = sm.buf[bL];
         T *R = sm.buf[bR];
+        uint32_t eq_in = 0;   // keys equal to p moving into the right block (mode 0)
         for (uint32_t q = tid; q < num; q += NT) {
             const uint32_t a = sm.off[0][sL + q], c = sm.off[1][sR + q];
             const T t0 = L[a];
             L[a] = R[c];
             R[c] = t0;
+            const K k0 = KT::key(t0);
+            eq_in += !(k0 < pk) && !(pk < k0);
+        }
+        if (P.eqpos) {
+            eq_in = __reduce_add_sync(0xffffffffu, eq_in);
+            if (lane == 0 && eq_in) atomicAdd(&sm.eqcnt[1], eq_in);
         }
         fence_proxy_async_smem();   // the swaps become visible to the bulk stores
         __syncthreads();
+        if (P.eqpos && e1 && sm.eqcnt[1]) {
+            // the neutralized right block is final: record where its keys equal
+            // to p sit, so the equal band needs no scan of the right part
+            const uint32_t rb = sm.blk[bR];
+            for (uint32_t j0 = 0; j0 < TILE; j0 += NT) {
+                const uint32_t j = j0 + tid;
+                const K kk = KT::key(R[j]);
+                const bool eq = !(kk < pk) && !(pk < kk);
+                const uint32_t m = __ballot_sync(0xffffffffu, eq);
+                if (!m) continue;
+                uint32_t b0 = 0;
+                if (lane == 0) b0 = atomicAdd(&st->neqpos, (uint32_t)__popc(m));
+                b0 = __shfl_sync(0xffffffffu, b0, 0) + __popc(m & lanemask_lt());
+                if (eq && b0 < P.eqcap) P.eqpos[b0] = ((uint64_t)rb << 32) | j;
+            }
+            __syncthreads();   // R is refilled below only after these reads
+        }
         if (tid == 0) {
             // l.24-27: a neutralized block is final — written back if a swap touched it
             const uint32_t d0 = sm.dirty[0] | (num > 0), d1 = sm.dirty[1] | (num > 0);
@@ -321,7 +355,7 @@ __global__ void __launch_bounds__(NT) k_inplace(InplaceParams<KT> P) {
 // right part of pass 0, if pass 0 met keys equal to p
 template <class KT>
 __global__ void k_ip_setup(const typename KT::T *data, IpPass *ps, const IpPass *prev, uint64_t n,
-                           uint64_t list_cap) {
+                           uint64_t list_cap, uint32_t eqcap) {
     using T = typename KT::T;
     constexpr uint32_t TILE = ip_tile<KT>();
     IpPass q;
@@ -337,6 +371,7 @@ __global__ void k_ip_setup(const typename KT::T *data, IpPass *ps, const IpPass 
         q.compact = any && prev->n_eq <= list_cap;
         q.active = any && !q.compact;
         q.n_eq = prev->n_eq;
+        q.fast_eq = q.compact && prev->st.neqpos <= eqcap;
     }
     q.len = n - q.off;
     const uint64_t mis16 = (uintptr_t)(data + q.off) & 15;
@@ -351,7 +386,8 @@ __global__ void k_ip_setup(const typename KT::T *data, IpPass *ps, const IpPass 
 // where the leftover blocks go: the left ones to [X - a, X), the right ones
 // to [X, X + c), each swapping with a neutralized block found there
 template <class KT, int NT>
-__global__ void __launch_bounds__(NT) k_ip_plan(IpPass *ps, const uint32_t *leftover, uint32_t *pairs) {
+__global__ void __launch_bounds__(NT) k_ip_plan(IpPass *ps, const uint32_t *leftover, uint32_t *pairs,
+                                                 uint64_t *eqpos, uint32_t eqcap) {
     constexpr uint32_t TILE = ip_tile<KT>();
     __shared__ uint8_t win[IP_GMAX];
     __shared__ uint32_t cnt[2], nout[2], nin[2];
@@ -383,6 +419,19 @@ __global__ void __launch_bounds__(NT) k_ip_plan(IpPass *ps, const uint32_t *left
     }
     __syncthreads();
     const uint32_t mL = nout[0], mR = nout[1];
+    if (eqpos) {
+        // recorded positions of keys equal to p follow their block when it
+        // moves out of the right window (it swaps with a leftover)
+        __shared__ uint32_t newblk[IP_GMAX];
+        for (uint32_t q = tid; q < mR; q += NT) newblk[pr[2 * q + 1] - X] = pr[2 * q];
+        __syncthreads();
+        const uint32_t ne = ps->st.neqpos < eqcap ? ps->st.neqpos : eqcap;
+        for (uint32_t i = tid; i < ne; i += NT) {
+            const uint64_t e = eqpos[i];
+            const uint32_t b = (uint32_t)(e >> 32);
+            if (b >= X && b < X + c) eqpos[i] = ((uint64_t)newblk[b - X] << 32) | (uint32_t)e;
+        }
+    }
     for (uint32_t i = tid; i < 2 * mR; i += NT) pairs[2 * mL + i] = pr[i];   // right pairs after the left ones
     if (tid == 0) {
         ps->npairs = mL + mR;
@@ -558,7 +607,7 @@ __global__ void __launch_bounds__(NT) k_eq_scan(const typename KT::T *data, IpPa
                                                  uint32_t *G) {
     using T = typename KT::T;
     using K = typename KT::K;
-    if (!ps->compact) return;
+    if (!ps->compact || ps->fast_eq) return;
     const K pk = (K)pivot;
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t off = ps->off, len = ps->len, band = ps->n_eq;
@@ -632,6 +681,54 @@ __global__ void __launch_bounds__(NT) k_eq_scan(const typename KT::T *data, IpPa
                 warp_append(me, lane, &ps->cnt_eq, E, pos);
                 warp_append(mg, lane, &ps->cnt_gt, G, pos);
             }
+        }
+    }
+}
+
+// The equal band from pass 0's records (fast_eq): the right part's keys
+// equal to p sit at recorded positions in the neutralized right blocks, or in
+// the cleanup's ranges (the middle's right part with the fixed-up head, and
+// the tail); only those, and the band itself, are read.
+template <class KT, int NT>
+__global__ void __launch_bounds__(NT) k_eq_scan2(const typename KT::T *data, IpPass *ps, const IpPass *p0,
+                                                  uint64_t pivot, uint32_t *E, uint32_t *G, const uint64_t *eqpos,
+                                                  uint32_t eqcap) {
+    using K = typename KT::K;
+    if (!ps->fast_eq) return;
+    constexpr uint32_t TILE = ip_tile<KT>();
+    const K pk = (K)pivot;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t nl = ps->off, band_end = nl + ps->n_eq, n = p0->off + p0->len;
+    const uint64_t h0 = p0->h, o1 = p0->o1, n1 = p0->n1, o2 = p0->o2, lv = p0->lcur;
+    const uint64_t e_spill = (lv >= h0 && lv - h0 > n1 && o1 + n1 < o2) ? lv - h0 - n1 : 0;
+    // element ranges, in pass 0's coordinates: S1 = [nl, o1+n1), S2 = [max(o2,
+    // nl), n), S3 = the band's part between them
+    const uint64_t s1b = nl, s1e = (o1 + n1 > nl) ? o1 + n1 : nl;
+    const uint64_t s2b = o2 > nl ? o2 : nl, s2e = n;   // the tail's right part
+    const uint64_t s3b = s1e, s3e = band_end < o2 ? (band_end > s1e ? band_end : s1e) : (o2 > s1e ? o2 : s1e);
+    const uint64_t l1 = s1e - s1b, l2 = s2e - s2b, l3 = s3e - s3b;
+    const uint32_t nrec = p0->st.neqpos < eqcap ? p0->st.neqpos : eqcap;
+    const uint64_t total = l1 + l2 + l3 + nrec;
+    const uint64_t step = (uint64_t)gridDim.x * NT;
+    for (uint64_t i0 = (uint64_t)blockIdx.x * NT; i0 < total; i0 += step) {
+        const uint64_t q = i0 + threadIdx.x;
+        uint32_t me = 0, mg = 0;
+        uint64_t idx = 0;
+        if (q < l1 + l2 + l3) {
+            idx = q < l1 ? s1b + q : q < l1 + l2 ? s2b + (q - l1) : s3b + (q - l1 - l2);
+            const K kk = KT::key(data[idx]);
+            const bool eq = !(kk < pk) && !(pk < kk);
+            mg = idx < band_end && !eq;
+            me = idx >= band_end && eq;
+        } else if (q < total) {
+            const uint64_t e = eqpos[q - l1 - l2 - l3];
+            idx = h0 + (e >> 32) * TILE + (uint32_t)e;
+            const bool moved = e_spill && idx >= o1 + n1 && idx < o1 + n1 + e_spill;
+            me = idx >= band_end && !moved;
+        }
+        if (__any_sync(0xffffffffu, me | mg)) {
+            warp_append(me, lane, &ps->cnt_eq, E, [&](uint32_t) { return (uint32_t)(idx - nl); });
+            warp_append(mg, lane, &ps->cnt_gt, G, [&](uint32_t) { return (uint32_t)(idx - nl); });
         }
     }
 }

@@ -187,3 +187,36 @@ def test_inplace_equal_band_both_ways(B, kind, n, nvals):
     p = np.sort(k)[len(k) // 2]
     split, neq = check(B, kind, a, float(p) if kind == "f64" else int(p))
     assert neq > n // (2 * nvals)
+
+
+@pytest.mark.parametrize("kind", ["i32", "u64", "rec32"])
+def test_inplace_equal_band_geometries(B, kind):
+    """The equal band from pass 0's recorded positions (no scan of the right
+    part) across many geometries: random sizes (ragged tails), unaligned
+    starts (heads), pivots anywhere (the head and tail fix-ups, leftover blocks
+    moved out of the right window with their recorded keys), and a few to a
+    few thousand keys equal to the pivot."""
+    rng = np.random.default_rng(17)
+    T = TILE[kind]
+    for case in range(24):
+        n = int(rng.integers(T, 600 * T)) + int(rng.integers(0, T))
+        offset = int(rng.integers(0, 4)) if kind != "rec32" else 0
+        a = make(kind, n, seed=case + 100)
+        k = keys_of(a)
+        # plant copies of one key (1 .. ~n/64 of them) at random positions
+        p = k[int(rng.integers(0, n))]
+        m = int(rng.integers(1, max(2, n // 64)))
+        pos = rng.integers(0, n, size=m)
+        if kind == "rec32":
+            a[pos, 0] = p
+        else:
+            a[pos] = p
+        pv = int(p)
+        t = to_dev(a, offset=offset)
+        split, neq = B.bq_partition_inplace(t, pv)
+        _, s_o, e_o = oracle.partition(a, pv)
+        assert (split, neq) == (s_o, e_o), case
+        got = to_host(t, a)
+        kk, pk = _key(kind, got), _pk(kind, pv)
+        assert (kk[:split] < pk).all() and (kk[split:split + neq] == pk).all() and (kk[split + neq:] > pk).all()
+        assert np.array_equal(np.sort(_key(kind, got)), np.sort(_key(kind, a)))
