@@ -105,7 +105,7 @@ typedef struct {
                              of a segment placed in completion order).  Records always
                              use the ordered placement.  Sorted keys are identical. */
     int32_t ways;         /* 0 (default): binary passes for int32 keys (8-way for
-                             2^17 < n <= 2^23) and 32-byte records, 8-way passes for
+                             2^17 < n <= 2^23, 16-way up to 2^24) and 32-byte records, 8-way passes for
                              uint64/float64 keys and key+index pairs (so also for
                              bq_sort_records' default path); 2: binary; 8 or 16:
                              multi-pivot block partition (segments whose

@@ -647,11 +647,13 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
     // the HBM roofline and the cheapest in ALU work per key), 8-way passes
     // (N4) for 64-bit keys, whose binary passes leave ALU headroom (c3:
     // 11.2 -> 10.4 ms random, 12.9 -> 10.3 ms sorted); records stay binary
-    // (int32: also 8-way for 2^17 < n <= 2^23, where a sort is a few levels
-    // and each level's fixed costs matter: c1 0.48 -> 0.39 ms)
+    // (int32: also multiway where a sort is only a few levels and each
+    // level's fixed costs matter: 8-way for 2^17 < n <= 2^23, 16-way up to
+    // 2^24 — c1 0.48 -> 0.39 ms, 2^24 0.99 -> 0.90 ms; profiles/r01/ways_sweep.jsonl)
     if (ways == 0) {
         if (sizeof(typename KT::K) == 8 && mw_capable<KT>()) ways = MW8;
         else if (!KT::is_record && n > (1u << 17) && n <= (1u << 23)) ways = MW8;
+        else if (!KT::is_record && n > (1u << 23) && n <= (1u << 24)) ways = MW_K;
         else ways = 2;
     }
     if (!mw_capable<KT>()) ways = 2;
