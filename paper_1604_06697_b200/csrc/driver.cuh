@@ -14,7 +14,6 @@
 #pragma once
 
 #include <algorithm>
-#include <type_traits>
 #include <cstdlib>
 #include <cstdarg>
 #include <cstdio>
@@ -66,7 +65,6 @@ struct Layout {
     size_t msegs[2], mtile_map[2], mhist[2], mcursor[2];   // multiway segment lists (N4)
     size_t copies[2], max_copies;                           // records: finished equal runs to copy
     size_t subs[2];                                         // N1 subtree jobs (subtree.cuh)
-    size_t merges[2];                                       // split leaves' merge jobs (leaf.cuh)
     size_t max_tiles, max_segs, max_leaves, max_fb;
 };
 
@@ -78,8 +76,7 @@ Layout<KT> make_layout(size_t n) {
     L.max_segs = n / (S + 1) + 2;                 // segments > S are disjoint
     L.max_tiles = n / TILE + 2 * L.max_segs + 2;
     // leaves of one batch of LEVEL_BATCH levels per class list; also fallback chunks
-    // (x2: a split leaf puts its second run into another class list)
-    L.max_leaves = 2 * (LEVEL_BATCH * (2 * L.max_segs + 2) + (n / S + 2));
+    L.max_leaves = LEVEL_BATCH * (2 * L.max_segs + 2) + (n / S + 2);
     L.max_fb = n / (S + 1) + 2;
     size_t off = 0;
     auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + bytes, 256); return o; };
@@ -107,8 +104,6 @@ Layout<KT> make_layout(size_t n) {
     // N1 subtree jobs of one batch (disjoint segments > S), per set
     L.subs[0] = take(L.max_segs * sizeof(Leaf));
     L.subs[1] = take(L.max_segs * sizeof(Leaf));
-    L.merges[0] = take(L.max_leaves * sizeof(Leaf));
-    L.merges[1] = take(L.max_leaves * sizeof(Leaf));
     L.ctrl = take((MAX_LEVELS + 1) * sizeof(LevelCtrl));   // [MAX_LEVELS]: the root's counts
     L.misc = take(256);   // fallback count, leaf-list counts (2 sets x 8 classes), copy/subtree counts; pass counts
     L.total = off;
@@ -704,13 +699,6 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
     Leaf *subs[2] = {reinterpret_cast<Leaf *>(w + L.subs[0]), reinterpret_cast<Leaf *>(w + L.subs[1])};
     uint32_t *sub_counts[2] = {fb_count + 22, fb_count + 23};
     uint32_t *overflow = fb_count + 24;
-    uint32_t *merge_counts[2] = {fb_count + 25, fb_count + 26};
-    Leaf *merges[2] = {reinterpret_cast<Leaf *>(w + L.merges[0]), reinterpret_cast<Leaf *>(w + L.merges[1])};
-    // split leaves (int32): leaves of 4097..8192 keys as 4096 + the rest + a merge
-#ifndef BQ_LEAF_SPLIT
-#define BQ_LEAF_SPLIT 1
-#endif
-    const uint32_t leaf_split = (BQ_LEAF_SPLIT && std::is_same<KT, KI32>::value) ? S / 2 : 0;
     // N1: subtrees of <= SUB elements finished on chip (bq_sort_options.subtree)
     const uint32_t sub_max = (sub_enabled<KT>() && subtree) ? sub_elems<KT>() : 0;
 
@@ -761,7 +749,7 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
     }
 
     BQ_CKC(cudaMemsetAsync(ctrl, 0, (MAX_LEVELS + 1) * sizeof(LevelCtrl), s));
-    BQ_CKC(cudaMemsetAsync(fb_count, 0, 27 * sizeof(uint32_t), s));
+    BQ_CKC(cudaMemsetAsync(fb_count, 0, 25 * sizeof(uint32_t), s));
     const int aligned = aligned16(user) && aligned16(scratch);
     // children sink of level `lv` (its children form level lv+1; the root is
     // the only "child" of the virtual level -1, counted in `root`)
@@ -797,9 +785,6 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
         Q.subs = subs[set];
         Q.sub_count = sub_counts[set];
         Q.sub_max = sub_max;
-        Q.leaf_split = leaf_split;
-        Q.merges = merges[set];
-        Q.merge_count = merge_counts[set];
         return Q;
     };
     {
@@ -822,7 +807,6 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
         BQ_CKC(cudaMemsetAsync(leaf_counts[set], 0, MAX_LEAF_CLASSES * sizeof(uint32_t), s));
         BQ_CKC(cudaMemsetAsync(copy_counts[set], 0, sizeof(uint32_t), s));
         if (batch > 0) BQ_CKC(cudaMemsetAsync(sub_counts[set], 0, sizeof(uint32_t), s));   // batch 0: the root may be one
-        BQ_CKC(cudaMemsetAsync(merge_counts[set], 0, sizeof(uint32_t), s));
         for (int k = 0; k < LEVEL_BATCH; k++, level++) {
             const int cp = level & 1;
             const LevelCtrl *prev = level == 0 ? root : ctrl + level - 1;
@@ -926,10 +910,6 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
             LP.count_dev = leaf_counts[set] + c;
             st = launch_leaves<KT>(c, LP, 0, ls);
             if (st != BQ_OK) { cleanup(); return st; }
-            local.kernel_launches++;
-        }
-        if (leaf_split) {
-            BQ_CKC(launch_leaf_merge<KT>(merges[set], merge_counts[set], user, ls));
             local.kernel_launches++;
         }
         if (KT::is_record && !ordered) {

@@ -470,72 +470,6 @@ __global__ void __launch_bounds__(1 << (L - LeafTraits<KT>::R), (LeafTraits<KT>:
     }
 }
 
-// A leaf split in two by emit_children (partition.cuh): its runs [b, b+l0)
-// and [b+l0, b+len), each sorted by its own power-of-two network into the
-// user buffer, merged here — the merge path over the two runs in shared
-// memory (A before B on ties), written back in place.  This replaces the
-// padding of a 4097..8192-key leaf to the 8192 network by a 4096 network, a
-// smaller one and one merge pass.
-template <class KT, int NT>
-__global__ void __launch_bounds__(NT) k_leaf_merge(const Leaf *jobs, const uint32_t *count, typename KT::T *out) {
-    using T = typename KT::T;
-    extern __shared__ __align__(16) unsigned char smraw[];
-    T *sa = reinterpret_cast<T *>(smraw);            // A = sa[0, la), B = sa[la, len)
-    T *sc = sa + Tune<KT>::LEAF;                      // the merged run
-    const uint32_t tid = threadIdx.x;
-    const uint32_t njobs = *count;
-    for (uint32_t q = blockIdx.x; q < njobs; q += gridDim.x) {
-        const Leaf jb = jobs[q];
-        const uint32_t b = jb.begin, len = jb.len, la = jb.parity, lb = len - la;
-        __syncthreads();   // the previous job's readers of sc are done
-        for (uint32_t i = tid; i < len; i += NT) sa[i] = out[(uint64_t)b + i];
-        __syncthreads();
-        const uint32_t per = (len + NT - 1) / NT;
-        const uint32_t d0 = tid * per < len ? tid * per : len, d1 = d0 + per < len ? d0 + per : len;
-        uint32_t lo = d0 > lb ? d0 - lb : 0, hi = d0 < la ? d0 : la;
-        while (lo < hi) {
-            const uint32_t mid = (lo + hi) >> 1;
-            if (!(KT::key(sa[la + d0 - 1 - mid]) < KT::key(sa[mid]))) lo = mid + 1;
-            else hi = mid;
-        }
-        uint32_t i = lo, j = d0 - lo;
-        // the heads of both runs stay in registers; only the consumed side
-        // is reloaded (one shared-memory load per output)
-        T va = i < la ? sa[i] : T{}, vb = j < lb ? sa[la + j] : T{};
-        for (uint32_t d = d0; d < d1; d++) {
-            const bool take_a = j >= lb || (i < la && !(KT::key(vb) < KT::key(va)));
-            sc[d] = take_a ? va : vb;
-            if (take_a) {
-                i++;
-                va = i < la ? sa[i] : va;
-            } else {
-                j++;
-                vb = j < lb ? sa[la + j] : vb;
-            }
-        }
-        __syncthreads();
-        for (uint32_t k = tid; k < len; k += NT) out[(uint64_t)b + k] = sc[k];
-    }
-}
-
-template <class KT>
-cudaError_t launch_leaf_merge(const Leaf *jobs, const uint32_t *count, typename KT::T *out, cudaStream_t s) {
-    constexpr int NT = 512;
-    constexpr size_t smem = 2 * (size_t)Tune<KT>::LEAF * sizeof(typename KT::T);
-    static int cap = 0;
-    if (cap == 0) {
-        cudaError_t e = cudaFuncSetAttribute(k_leaf_merge<KT, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        int nb = 0, dev = 0, sms = 0;
-        if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_leaf_merge<KT, NT>, NT, smem)) != cudaSuccess) return e;
-        if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
-        if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
-        cap = (nb > 0 ? nb : 1) * sms;
-    }
-    k_leaf_merge<KT, NT><<<cap, NT, smem, s>>>(jobs, count, out);
-    return cudaGetLastError();
-}
-
 // host: launch the leaf kernel of class c (NET = 2^(lmin + c)) over `count` leaves
 // count > 0: one CTA per leaf; count == 0: persistent grid (resident CTAs)
 // over LP.count_dev leaves

@@ -113,12 +113,6 @@ struct PostParams {
     Leaf *subs;
     uint32_t *sub_count;
     uint32_t sub_max;       // 0: off
-    // split leaves: a leaf of len > leaf_split is sorted as two leaves (the
-    // first leaf_split keys, and the rest, each on its own power-of-two
-    // network) plus a merge job (leaf.cuh k_leaf_merge); 0: off
-    uint32_t leaf_split;
-    Leaf *merges;
-    uint32_t *merge_count;
 };
 
 template <class KT>
@@ -251,21 +245,11 @@ __device__ __forceinline__ void emit_children(const PostParams<KT> &Q, int nch, 
         s_nt[c] = 0;
         if (kind == C_LEAF) {
             // leaf lists are binned by sorting-network size (leaf.cuh)
-            const bool split = Q.leaf_split && len > Q.leaf_split;
-            const uint32_t l0 = split ? Q.leaf_split : len;
-            const uint32_t lc = leaf_class<KT>(l0);
+            const uint32_t lc = leaf_class<KT>(len);
             const uint32_t li = atomicAdd(&Q.leaf_counts[lc], 1u);
             atomicAdd(&post_stats().nleaf_cls[lc], 1u);
             atomicAdd(&post_stats().nleaf, 1u);
-            Q.leaves[lc * Q.leaf_cap + li] = Leaf{cb[c], l0, cp, 0};
-            if (split) {
-                // the rest on its own (smaller) network, then one merge
-                const uint32_t l1 = len - l0, lc1 = leaf_class<KT>(l1);
-                const uint32_t lj = atomicAdd(&Q.leaf_counts[lc1], 1u);
-                atomicAdd(&post_stats().nleaf_cls[lc1], 1u);
-                Q.leaves[lc1 * Q.leaf_cap + lj] = Leaf{cb[c] + l0, l1, cp, 0};
-                Q.merges[atomicAdd(Q.merge_count, 1u)] = Leaf{cb[c], len, l0, 0};
-            }
+            Q.leaves[lc * Q.leaf_cap + li] = Leaf{cb[c], len, cp, 0};
         } else if (kind == C_SUB) {
             Q.subs[atomicAdd(Q.sub_count, 1u)] = Leaf{cb[c], len, cp, cd};
         } else if (kind == C_FALLBACK) {
