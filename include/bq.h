@@ -102,8 +102,8 @@ typedef struct {
     int32_t timing;       /* != 0: time every partition launch with CUDA events */
     int32_t ordered;      /* != 0: ticket-ordered tile placement (decoupled look-back),
                              deterministic layout; 0: one atomicAdd per tile (faster; tiles
-                             of a segment placed in completion order).  Records always
-                             use the ordered placement.  Sorted keys are identical. */
+                             of a segment placed in completion order; records then move
+                             by two-way passes).  Sorted keys are identical. */
     int32_t ways;         /* 0 (default): binary passes for int32 keys (8-way for
                              2^17 < n <= 2^23, 16-way up to 2^24) and 32-byte records, 8-way passes for
                              uint64/float64 keys and key+index pairs (so also for
@@ -189,7 +189,9 @@ BQ_API bq_status bq_partition_records(bq_record32 *recs, size_t n, uint64_t pivo
  * order, > keys reversed, tiles in ticket order, via decoupled look-back);
  * ordered == 0 places each tile's runs with one atomicAdd per tile (runs in
  * input order within a tile, tiles in completion order) — the sort's default.
- * Records always use the ordered placement.  This is the timed unit of the
+ * Records (32-byte, and key+index pairs) always use the ordered placement in
+ * this standalone pass (three-way, their equal elements staged in consumed
+ * input).  This is the timed unit of the
  * partition-pass roofline. */
 BQ_API bq_status bq_partition_pass(bq_kind kind, const void *src, void *dst, size_t n,
                                    const void *pivot, uint64_t *d_counts, int ordered, void *ws,

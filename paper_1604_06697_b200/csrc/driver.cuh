@@ -141,8 +141,9 @@ bq_status launch_partition_t(const PassParams<KT> &P, cudaStream_t s) {
     return BQ_OK;
 }
 
-// Records always use the ordered (look-back) mode: their equal elements are
-// staged in already-consumed input tiles, which needs ticket-ordered offsets.
+// The atomic-cursor pass (keys three-way, records two-way by Seg::pad0); the
+// standalone pass API keeps records on the ordered (look-back) mode, whose
+// equal elements are staged in already-consumed input tiles.
 template <class KT>
 bq_status launch_partition_fast(const PassParams<KT> &P, cudaStream_t s) {
     using Kn = Kernels<KT>;
