@@ -118,3 +118,87 @@ def test_sort_2pow30_int32(B):
     for i in [0, 12345, n // 3, n - 1]:
         v = t[i]
         assert int((src < v).sum()) <= i < int((src <= v).sum())
+
+
+NMAX = (1 << 31) - 1   # include/bq.h: n <= 2^31 - 1
+
+
+def _free_cuda():
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+
+
+def test_sort_max_n_int32(B):
+    """The largest n the C-ABI accepts (2^31 - 1 int32 keys, 8 GiB + 8 GiB of
+    workspace): equal to torch.sort (a library radix sort), sampled ranks on
+    the device."""
+    g = torch.Generator(device="cuda").manual_seed(12)
+    src = torch.randint(-(1 << 31), (1 << 31) - 1, (NMAX,), dtype=torch.int32, device="cuda", generator=g)
+    t = src.clone()
+    st = B.bq_sort_ex(t)
+    assert st["fallback_segments"] == 0
+    ref = torch.sort(src)[0]
+    assert bool(torch.equal(t, ref))
+    del ref
+    for i in [0, 777, NMAX // 2, NMAX - 1]:
+        v = t[i]
+        assert int((src < v).sum()) <= i < int((src <= v).sum())
+    del src, t
+    _free_cuda()
+
+
+def test_sort_max_n_uint64(B):
+    """2^31 - 1 uint64 keys (16 GiB), top bit clear so torch's int64 sort
+    orders them the same way; the default 8-way passes at the size limit."""
+    g = torch.Generator(device="cuda").manual_seed(13)
+    src = torch.randint(0, (1 << 62) - 1, (NMAX,), dtype=torch.int64, device="cuda", generator=g)
+    t = src.clone()
+    st = B.bq_sort_ex(t)
+    assert st["fallback_segments"] == 0
+    ref = torch.sort(src)[0]
+    assert bool(torch.equal(t, ref))
+    del src, t, ref
+    _free_cuda()
+
+
+def test_partition_max_n_int32(B):
+    """bq_partition_i32 (in place, N2) at 2^31 - 1 keys: the split and the
+    equal count equal the plain counts, the three bands hold, and the multiset
+    is unchanged (compared sorted)."""
+    g = torch.Generator(device="cuda").manual_seed(14)
+    src = torch.randint(-1000, 1000, (NMAX,), dtype=torch.int32, device="cuda", generator=g)
+    t = src.clone()
+    p = 17
+    split, neq = B.bq_partition_i32(t, p)
+    assert split == int((src < p).sum()) and neq == int((src == p).sum())
+    assert bool((t[:split] < p).all()) and bool((t[split:split + neq] == p).all())
+    assert bool((t[split + neq:] > p).all())
+    assert bool(torch.equal(torch.bincount(t.long() + 1000, minlength=2000),
+                            torch.bincount(src.long() + 1000, minlength=2000)))
+    del src, t
+    _free_cuda()
+
+
+def test_sort_records_2pow30(B):
+    """2^30 records (32 GiB) through the default key+index path: the keys come
+    out equal to torch.sort of the keys, every record travels whole (its
+    payload words are functions of its key and original position), and the
+    positions form a permutation (each names a record with that key)."""
+    n = 1 << 30
+    g = torch.Generator(device="cuda").manual_seed(15)
+    r = torch.empty((n, 4), dtype=torch.int64, device="cuda")
+    r[:, 0] = torch.randint(0, 1 << 40, (n,), dtype=torch.int64, device="cuda", generator=g)
+    r[:, 1] = torch.arange(n, dtype=torch.int64, device="cuda")
+    r[:, 2] = r[:, 0] ^ 0x5A5A5A5A
+    r[:, 3] = r[:, 1] * 3
+    keys = r[:, 0].clone()
+    st = B.bq_sort_ex(r)
+    assert st["fallback_segments"] == 0
+    assert bool(torch.equal(r[:, 0], torch.sort(keys)[0]))
+    assert bool(torch.equal(r[:, 2], r[:, 0] ^ 0x5A5A5A5A)) and bool(torch.equal(r[:, 3], r[:, 1] * 3))
+    assert bool(torch.equal(keys[r[:, 1]], r[:, 0]))
+    seen = torch.zeros(n, dtype=torch.bool, device="cuda")
+    seen[r[:, 1]] = True
+    assert bool(seen.all())
+    del r, keys, seen
+    _free_cuda()
