@@ -14,10 +14,12 @@
 // block on its side is claimed (l.26-27).  When one side is exhausted the CTA
 // writes back the block it still holds and lists it as a leftover.
 //
-// The host then (run_partition_inplace, driver.cuh) swaps the leftover
-// blocks into the middle of the range, partitions the middle (<= #CTAs + 1
-// blocks: "compare and rearrange remaining elements", l.29) out of place in
-// a small buffer, and repeats on the right part for the equal band.
+// The cleanup kernels that follow (k_ip_plan .. k_ip_fix, launched by
+// run_partition_inplace_ip in driver.cuh without host round trips) swap the
+// leftover blocks into the middle of the range and partition the middle
+// (<= #CTAs + 1 blocks: "compare and rearrange remaining elements", l.29)
+// out of place in a small buffer; pass 1 forms the equal band in the right
+// part (from recorded positions, by compaction, or by a second block pass).
 #pragma once
 
 namespace bq {
@@ -116,8 +118,11 @@ __device__ __forceinline__ uint32_t ip_claim(InplaceState *st, int side) {
     return (side == 0 ? lo : hi - 1) - IP_BIAS;
 }
 
+#ifndef BQ_IP_MINB
+#define BQ_IP_MINB 6
+#endif
 template <class KT, int NT, int IPT>
-__global__ void __launch_bounds__(NT) k_inplace(InplaceParams<KT> P) {
+__global__ void __launch_bounds__(NT, BQ_IP_MINB) k_inplace(InplaceParams<KT> P) {
     using T = typename KT::T;
     using K = typename KT::K;
     using SM = InplaceSmem<KT, NT, IPT>;
@@ -194,18 +199,23 @@ __global__ void __launch_bounds__(NT) k_inplace(InplaceParams<KT> P) {
                     }
                 }
             }
+            // one warp scan carries both counts: misplaced (low half, a
+            // prefix) and equal to p (high half, only the warp total is used);
+            // each is <= 32 * IPT <= 1024 per warp
             const uint32_t cnt = __popc(mis);
-            uint32_t inc = cnt;
+            uint32_t inc = cnt | (ne << 16);
 #pragma unroll
             for (int d = 1; d < 32; d <<= 1) {
                 const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
                 if (lane >= (uint32_t)d) inc += o;
             }
-            if (lane == 31) sm.wsum[warp] = inc;
-#pragma unroll
-            for (int d = 16; d > 0; d >>= 1) ne += __shfl_xor_sync(0xffffffffu, ne, d);
-            if (lane == 0 && ne) atomicAdd(&st->n_equal, (unsigned long long)ne);
-            if (lane == 0) sm.weq[warp] = ne;
+            if (lane == 31) {
+                const uint32_t we = inc >> 16;
+                sm.wsum[warp] = inc & 0xffffu;
+                sm.weq[warp] = we;
+                if (we) atomicAdd(&st->n_equal, (unsigned long long)we);
+            }
+            inc &= 0xffffu;
             __syncthreads();
             uint32_t pre = 0, tot = 0;
 #pragma unroll
