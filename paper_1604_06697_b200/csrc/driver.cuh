@@ -200,8 +200,8 @@ bq_status launch_multiway(MwParams<KT> MP, LevelCtrl *lc, cudaStream_t s, int wa
     constexpr int threads = Kn::NT + 32;
     if (ways == MW8) {
         constexpr int smem8 = mw8_smem_bytes<KT>();
-        auto kc8 = k_mw8_count<KT, Kn::NT, Kn::IPT, MW_STAGES, Kn::MINB>;
-        auto ks8 = k_mw8_scatter<KT, Kn::NT, Kn::IPT, MW_STAGES, Kn::MINB>;
+        auto kc8 = k_mw8_count<KT, Kn::NT, Kn::IPT, MW_STAGES, MW8_MINB>;
+        auto ks8 = k_mw8_scatter<KT, Kn::NT, Kn::IPT, MW_STAGES, MW8_MINB>;
         static int cap_c8 = 0, cap_s8 = 0;
         bq_status st = persistent_cap(kc8, threads, smem8, &cap_c8);
         if (st != BQ_OK) return st;

@@ -193,7 +193,14 @@ struct MwSmem {
     uint32_t sh[2][MW_K];          // shifted staging start of each run
 };
 
-constexpr int MW_STAGES = 3;   // TMA ring depth of the multiway kernels (2 CTAs per SM)
+#ifndef BQ_MW_STAGES
+#define BQ_MW_STAGES 3
+#endif
+#ifndef BQ_MW8_MINB
+#define BQ_MW8_MINB 2
+#endif
+constexpr int MW_STAGES = BQ_MW_STAGES;   // TMA ring depth of the multiway kernels (2 CTAs per SM)
+constexpr int MW8_MINB = BQ_MW8_MINB;     // resident CTAs per SM the 8-way kernels are compiled for
 
 template <class KT>
 constexpr int mw_smem_bytes() {

@@ -37,6 +37,8 @@ for name, kw in cases:
     ms = sorted(ts[1:])[1]
     n = len(src)
     print(json.dumps({"config": name, **kw, "records": args.records, "n": n, "ms": round(ms, 3), "Gkeys_s": round(n / ms / 1e6, 2),
-                      "levels": st["levels"], "element_passes": round(st["element_passes"] / n, 2)}), flush=True)
+                      "levels": st["levels"], "element_passes": round(st["element_passes"] / n, 2),
+                      "all_ms": [round(t, 3) for t in ts], "fallback_segments": st["fallback_segments"],
+                      "leaves": st.get("leaves"), "kernel_launches": st.get("kernel_launches")}), flush=True)
     del src, dst, ws
     torch.cuda.empty_cache()
