@@ -12,6 +12,39 @@
 namespace bq {
 
 // ---------------------------------------------------------------------------
+// Resident-CTA capacity of a kernel, cached per device: the library's only
+// mutable host state (include/bq.h: "an immutable per-device cache of launch
+// limits").  Each slot is written once, with the same value by any racing
+// caller, through atomic builtins; the shared-memory attribute is set on the
+// first launch per device.
+// ---------------------------------------------------------------------------
+constexpr int MAX_DEVICES = 64;
+struct CapCache {
+    int v[MAX_DEVICES];
+};
+template <class F>
+cudaError_t resident_ctas(F kern, int threads, size_t smem, CapCache &cc, int *cap, int per_sm_max = 0) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= MAX_DEVICES) return cudaErrorInvalidDevice;
+    int c = __atomic_load_n(&cc.v[dev], __ATOMIC_ACQUIRE);
+    if (c == 0) {
+        if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
+            return e;
+        int nb = 0, sms = 0;
+        if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, threads, smem)) != cudaSuccess) return e;
+        if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+        if (nb < 1) return cudaErrorInvalidConfiguration;   // the kernel does not fit on an SM
+        if (per_sm_max > 0 && nb > per_sm_max) nb = per_sm_max;
+        c = nb * sms;
+        __atomic_store_n(&cc.v[dev], c, __ATOMIC_RELEASE);
+    }
+    *cap = c;
+    return cudaSuccess;
+}
+
+// ---------------------------------------------------------------------------
 // Key traits.  `T` is the storage type moved by the passes, `K` the unsigned
 // or signed type compared.  H0: float64 is compared through the
 // order-preserving bijection  sign set -> ~bits, else bits | 2^63  (IEEE 754

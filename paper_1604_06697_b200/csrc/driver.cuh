@@ -125,16 +125,9 @@ bq_status launch_partition_t(const PassParams<KT> &P, cudaStream_t s) {
     auto kern = k_partition<KT, Kn::NT, Kn::IPT, Kn::STAGES, Kn::MINB, ORDERED>;
     constexpr int smem = part_smem_bytes<KT>();
     constexpr int threads = Kn::NT + (ORDERED ? 96 : 64);
-    static int cap = 0;
-    if (cap == 0) {
-        BQ_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        int nb = 0, dev = 0, sms = 0;
-        BQ_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, threads, smem));
-        BQ_CK(cudaGetDevice(&dev));
-        BQ_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        if (nb < 1) return set_error(BQ_ERR_CUDA, "partition kernel does not fit on an SM");
-        cap = nb * sms;
-    }
+    static CapCache cc;
+    int cap = 0;
+    BQ_CK(resident_ctas(kern, threads, smem, cc, &cap));
     const uint32_t grid = P.ntiles < (uint32_t)cap ? P.ntiles : (uint32_t)cap;
     kern<<<grid, threads, smem, s>>>(P);
     BQ_CK_LAUNCH();
@@ -150,16 +143,9 @@ bq_status launch_partition_fast(const PassParams<KT> &P, cudaStream_t s) {
     auto kern = k_part_fast<KT, Kn::NT, Kn::IPT, Kn::STAGES, Kn::MINB>;
     constexpr int smem = fast_smem_bytes<KT>();
     constexpr int threads = Kn::NT + 32;
-    static int cap = 0;
-    if (cap == 0) {
-        BQ_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        int nb = 0, dev = 0, sms = 0;
-        BQ_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, threads, smem));
-        BQ_CK(cudaGetDevice(&dev));
-        BQ_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        if (nb < 1) return set_error(BQ_ERR_CUDA, "partition kernel does not fit on an SM");
-        cap = nb * sms;
-    }
+    static CapCache cc;
+    int cap = 0;
+    BQ_CK(resident_ctas(kern, threads, smem, cc, &cap));
     const uint32_t grid = P.ntiles < (uint32_t)cap ? P.ntiles : (uint32_t)cap;
     kern<<<grid, threads, smem, s>>>(P);
     BQ_CK_LAUNCH();
@@ -168,15 +154,8 @@ bq_status launch_partition_fast(const PassParams<KT> &P, cudaStream_t s) {
 
 // resident-CTA capacity of a persistent kernel (cached per kernel)
 template <class F>
-bq_status persistent_cap(F kern, int threads, int smem, int *cap) {
-    if (*cap) return BQ_OK;
-    BQ_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    int nb = 0, dev = 0, sms = 0;
-    BQ_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, threads, smem));
-    BQ_CK(cudaGetDevice(&dev));
-    BQ_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    if (nb < 1) return set_error(BQ_ERR_CUDA, "kernel does not fit on an SM");
-    *cap = nb * sms;
+bq_status persistent_cap(F kern, int threads, int smem, CapCache &cc, int *cap) {
+    BQ_CK(resident_ctas(kern, threads, (size_t)smem, cc, cap));
     return BQ_OK;
 }
 
@@ -185,8 +164,9 @@ template <class KT>
 bq_status launch_subtree(const SubParams<KT> &SP, cudaStream_t s) {
     auto kern = k_subtree<KT, SUB_THREADS>;
     constexpr int smem = sub_smem_bytes<KT>();
-    static int cap = 0;
-    bq_status st = persistent_cap(kern, SUB_THREADS, smem, &cap);
+    static CapCache cc;
+    int cap = 0;
+    bq_status st = persistent_cap(kern, SUB_THREADS, smem, cc, &cap);
     if (st != BQ_OK) return st;
     kern<<<cap, SUB_THREADS, smem, s>>>(SP);
     BQ_CK_LAUNCH();
@@ -202,10 +182,11 @@ bq_status launch_multiway(MwParams<KT> MP, LevelCtrl *lc, cudaStream_t s, int wa
         constexpr int smem8 = mw8_smem_bytes<KT>();
         auto kc8 = k_mw8_count<KT, Kn::NT, Kn::IPT, MW_STAGES, MW8_MINB>;
         auto ks8 = k_mw8_scatter<KT, Kn::NT, Kn::IPT, MW_STAGES, MW8_MINB>;
-        static int cap_c8 = 0, cap_s8 = 0;
-        bq_status st = persistent_cap(kc8, threads, smem8, &cap_c8);
+        static CapCache cc_c8, cc_s8;
+        int cap_c8 = 0, cap_s8 = 0;
+        bq_status st = persistent_cap(kc8, threads, smem8, cc_c8, &cap_c8);
         if (st != BQ_OK) return st;
-        st = persistent_cap(ks8, threads, smem8, &cap_s8);
+        st = persistent_cap(ks8, threads, smem8, cc_s8, &cap_s8);
         if (st != BQ_OK) return st;
         MP.ticket = &lc->mw_ticket_count;
         kc8<<<cap_c8, threads, smem8, s>>>(MP);
@@ -220,10 +201,11 @@ bq_status launch_multiway(MwParams<KT> MP, LevelCtrl *lc, cudaStream_t s, int wa
     constexpr int smem = mw_smem_bytes<KT>();
     auto kc = k_mw_count<KT, Kn::NT, Kn::IPT, MW_STAGES, Kn::MINB>;
     auto ks = k_mw_scatter<KT, Kn::NT, Kn::IPT, MW_STAGES, Kn::MINB>;
-    static int cap_c = 0, cap_s = 0;
-    bq_status st = persistent_cap(kc, threads, smem, &cap_c);
+    static CapCache cc_c, cc_s;
+    int cap_c = 0, cap_s = 0;
+    bq_status st = persistent_cap(kc, threads, smem, cc_c, &cap_c);
     if (st != BQ_OK) return st;
-    st = persistent_cap(ks, threads, smem, &cap_s);
+    st = persistent_cap(ks, threads, smem, cc_s, &cap_s);
     if (st != BQ_OK) return st;
     MP.ticket = &lc->mw_ticket_count;
     kc<<<cap_c, threads, smem, s>>>(MP);
@@ -437,8 +419,9 @@ bq_status run_partition_inplace_ip(typename KT::T *data, size_t n, typename KT::
 
     auto kern = k_inplace<KT, Kn::NT, ip_ipt<KT>()>;
     constexpr int smem = inplace_smem_bytes<KT>();
-    static int cap = 0;
-    st = persistent_cap(kern, Kn::NT, smem, &cap);
+    static CapCache cc;
+    int cap = 0;
+    st = persistent_cap(kern, Kn::NT, smem, cc, &cap);
     if (st != BQ_OK) return st;
     uint32_t grid = (uint32_t)cap < IP_GMAX ? (uint32_t)cap : IP_GMAX;
     const size_t nb_max = n / TILE;

@@ -477,19 +477,15 @@ template <class KT, int L>
 cudaError_t launch_leaf_l(const LeafParams<KT> &LP, uint32_t count, cudaStream_t s) {
     constexpr size_t smem = leaf_smem_bytes<KT, L>();
     constexpr int NT = 1 << (L - LeafTraits<KT>::R);
-    static int cap = 0;
-    if (cap == 0) {
-        cudaError_t e = cudaFuncSetAttribute(k_leaf<KT, L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        int nb = 0, dev = 0, sms = 0;
-        if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_leaf<KT, L>, NT, smem)) != cudaSuccess) return e;
-        if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
-        if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+    static CapCache cc;
+    int cap = 0;
 #ifdef BQ_LEAF_CTAS_PER_SM
-        if (nb > BQ_LEAF_CTAS_PER_SM) nb = BQ_LEAF_CTAS_PER_SM;   // leave room for co-resident partition CTAs
+    constexpr int per_sm_max = BQ_LEAF_CTAS_PER_SM;   // leave room for co-resident partition CTAs
+#else
+    constexpr int per_sm_max = 0;
 #endif
-        cap = (nb > 0 ? nb : 1) * sms;
-    }
+    cudaError_t e = resident_ctas(k_leaf<KT, L>, NT, smem, cc, &cap, per_sm_max);
+    if (e != cudaSuccess) return e;
     k_leaf<KT, L><<<count ? count : (uint32_t)cap, NT, smem, s>>>(LP);
     return cudaGetLastError();
 }
