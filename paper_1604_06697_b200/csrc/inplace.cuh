@@ -501,7 +501,7 @@ __global__ void __launch_bounds__(NT) k_vsplit(const typename KT::T *data, typen
     const K pk = (K)pivot;
     for (uint64_t c0 = (uint64_t)blockIdx.x * CH; c0 < v; c0 += (uint64_t)gridDim.x * CH) {
         T x[IPT];
-        uint32_t lf = 0, nl = 0, nr = 0, ne = 0;
+        uint32_t lf = 0, vm = 0, ne = 0;
 #pragma unroll
         for (uint32_t j = 0; j < IPT; j++) {
             const uint64_t i = c0 + j * NT + tid;
@@ -510,21 +510,21 @@ __global__ void __launch_bounds__(NT) k_vsplit(const typename KT::T *data, typen
                 const K k = KT::key(x[j]);
                 const bool left = mode ? !(pk < k) : (k < pk);
                 lf |= (uint32_t)left << j;
-                nl += left;
-                nr += !left;
+                vm |= 1u << j;
                 ne += !(k < pk) && !(pk < k);
             }
         }
-        // inclusive warp scans of the left / right counts
-        uint32_t il = nl, ir = nr;
+        // warp-contiguous runs (ballots), so that the writes coalesce: the
+        // warp's left / right totals first, then the CTA's bases
+        uint32_t nl = 0, nr = 0;
 #pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const uint32_t ol = __shfl_up_sync(0xffffffffu, il, d), orr = __shfl_up_sync(0xffffffffu, ir, d);
-            if (lane >= (uint32_t)d) { il += ol; ir += orr; }
+        for (uint32_t j = 0; j < IPT; j++) {
+            const uint32_t bl = __ballot_sync(0xffffffffu, (lf >> j) & 1), bv = __ballot_sync(0xffffffffu, (vm >> j) & 1);
+            nl += __popc(bl);
+            nr += __popc(bv & ~bl);
         }
-#pragma unroll
-        for (int d = 16; d > 0; d >>= 1) ne += __shfl_xor_sync(0xffffffffu, ne, d);
-        if (lane == 31) { wl[warp] = il; we[warp] = ir; }
+        ne = __reduce_add_sync(0xffffffffu, ne);
+        if (lane == 0) { wl[warp] = nl; we[warp] = nr; }
         __syncthreads();
         uint32_t pl = 0, pr = 0, tl = 0, tr = 0;
 #pragma unroll
@@ -540,14 +540,16 @@ __global__ void __launch_bounds__(NT) k_vsplit(const typename KT::T *data, typen
             rb = tr ? atomicAdd(&ps->rcur, (unsigned long long)tr) : 0;
         }
         __syncthreads();
-        uint64_t ol = lb + pl + il - nl, orr = rb + pr + ir - nr;
+        uint64_t ol = lb + pl, orr = rb + pr;
+        const uint32_t lt = lanemask_lt();
 #pragma unroll
         for (uint32_t j = 0; j < IPT; j++) {
-            const uint64_t i = c0 + j * NT + tid;
-            if (i < v) {
-                if ((lf >> j) & 1) dst[ol++] = x[j];
-                else dst[v - 1 - orr++] = x[j];
-            }
+            const bool isl = (lf >> j) & 1, isv = (vm >> j) & 1;
+            const uint32_t bl = __ballot_sync(0xffffffffu, isl), br = __ballot_sync(0xffffffffu, isv && !isl);
+            if (isl) dst[ol + __popc(bl & lt)] = x[j];
+            else if (isv) dst[v - 1 - (orr + __popc(br & lt))] = x[j];
+            ol += __popc(bl);
+            orr += __popc(br);
         }
         __syncthreads();   // wl/we/lb/rb are reused by the next chunk
     }
