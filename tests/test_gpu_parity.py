@@ -532,3 +532,35 @@ def test_concurrent_sorts_on_streams(B):
     assert not errors, errors
     for (kind, _), a, t in zip(cases, arrays, tens):
         check_sorted_equal(kind, to_host(t, a), a)
+
+
+def _total_order_key(bits):
+    """IEEE 754 totalOrder as an unsigned key: negative values (sign bit set,
+    NaNs included) reversed below the positive ones."""
+    bits = bits.astype(np.uint64)
+    neg = (bits >> np.uint64(63)) == 1
+    return np.where(neg, ~bits, bits | np.uint64(1 << 63))
+
+
+@pytest.mark.parametrize("ways", [0, 2])
+def test_sort_nan_inputs_total_order(B, ways):
+    """NaNs are outside the contract (include/bq.h) but must not break the
+    sort: the output is a permutation of the input bit patterns, ordered by
+    IEEE 754 totalOrder (quiet and signalling NaNs of both signs beyond the
+    infinities), for the multi-pivot and the binary passes."""
+    rng = np.random.default_rng(21)
+    specials = np.array([0x7ff8000000000000, 0xfff8000000000000, 0x7ff0000000000001, 0xfff0000000000001,
+                         0x7fffffffffffffff, 0x7ff0000000000000, 0xfff0000000000000, 0x8000000000000000, 0],
+                        dtype=np.uint64)
+    for n in [9, 5000, 300_001]:
+        bits = rng.normal(size=n).view(np.uint64).copy()
+        pick = rng.random(n) < 0.2
+        bits[pick] = specials[rng.integers(0, len(specials), size=int(pick.sum()))]
+        a = bits.view(np.float64)
+        t = to_dev(a)
+        st = B.bq_sort_ex(t, ways=ways)
+        assert st["fallback_segments"] == 0
+        got = t.cpu().numpy().view(np.uint64)
+        assert np.array_equal(np.sort(got), np.sort(bits))
+        k = _total_order_key(got)
+        assert bool((k[1:] >= k[:-1]).all())
