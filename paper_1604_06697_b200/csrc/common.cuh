@@ -394,7 +394,8 @@ __device__ __forceinline__ uint64_t sample64_pos(uint32_t b, uint32_t len, uint3
     return (uint64_t)b + (pos < len - 1 ? pos : len - 1);
 }
 template <class KT>
-__device__ typename KT::K sample64_pivot_warp(const typename KT::T *buf, uint32_t b, uint32_t len, uint32_t lane) {
+__device__ typename KT::K sample64_pivot_warp(const typename KT::T *buf, uint32_t b, uint32_t len, uint32_t lane,
+                                              uint32_t q = 31) {
     using K = typename KT::K;
     K v[2];
 #pragma unroll
@@ -420,7 +421,8 @@ __device__ typename KT::K sample64_pivot_warp(const typename KT::T *buf, uint32_
             }
         }
     }
-    return __shfl_sync(0xffffffffu, v[0], 31);
+    // the (q+1)-th smallest sample key (q uniform; 31: the lower median)
+    return __shfl_sync(0xffffffffu, q < 32 ? v[0] : v[1], q & 31);
 }
 // the same, plus whether the 31st or 33rd smallest sample key equals the pivot
 template <class KT>
@@ -461,7 +463,7 @@ __device__ typename KT::K sample64_pivot_warp_dup(const typename KT::T *buf, uin
 // another key of the rule's sample equals the pivot.
 template <class KT>
 __device__ typename KT::K select_pivot_warp(const typename KT::T *buf, uint32_t b, uint32_t len, int rule,
-                                            uint32_t lane, bool *dup = nullptr);
+                                            uint32_t lane, bool *dup = nullptr, uint32_t q = 31);
 
 // Mo3 over {b, b+len/2, e-1}; ninther over b + floor(k*(len-1)/8), k=0..8.
 template <class KT>
@@ -485,11 +487,11 @@ __device__ typename KT::K select_pivot(const typename KT::T *buf, uint32_t b, ui
 
 template <class KT>
 __device__ typename KT::K select_pivot_warp(const typename KT::T *buf, uint32_t b, uint32_t len, int rule,
-                                            uint32_t lane, bool *dup) {
+                                            uint32_t lane, bool *dup, uint32_t q) {
     using K = typename KT::K;
     if (rule == BQ_PIVOT_SAMPLE64) {
         if (dup) return sample64_pivot_warp_dup<KT>(buf, b, len, lane, dup);
-        return sample64_pivot_warp<KT>(buf, b, len, lane);
+        return sample64_pivot_warp<KT>(buf, b, len, lane, q);
     }
     K p = 0;
     uint32_t eq = 0;

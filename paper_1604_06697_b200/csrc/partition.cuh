@@ -183,6 +183,9 @@ __device__ __forceinline__ void post_stats_flush(const PostParams<KT> &Q) {
 // it, then the CTA writes the children's slices of the next tile maps.
 // hint[c] (optional): 0 = choose a pivot; 1 = follow-up pass [<= p | > p]
 // with p = hint_pivot; 2 = a finished run of equal keys (records)
+#ifndef BQ_LEAF_AWARE
+#define BQ_LEAF_AWARE 1
+#endif
 template <class KT, int NT>
 __device__ __forceinline__ void emit_children(const PostParams<KT> &Q, int nch, const uint32_t *cb,
                                               const uint32_t *cl, uint8_t cp, uint16_t cd,
@@ -229,7 +232,24 @@ __device__ __forceinline__ void emit_children(const PostParams<KT> &Q, int nch, 
             kind = C_BIN;
             mode = dup ? 2 : 0;
         } else {
-            const K piv = select_pivot_warp<KT>(cbuf, cb[c], len, Q.pivot_rule, lane);
+            // Leaf-aware split of a segment that is one pass from its leaves
+            // (S < len <= 2 (S - m)): instead of the median, the sample
+            // quantile that leaves ~S - m keys on the left, m = len / 16 (one
+            // standard deviation of the 64-key sample's rank error, at most
+            // len sqrt(1/4 / 64)); both children then fit one leaf network, the
+            // left one nearly full, where two halves of ~len/2 would each pad
+            // an S network by up to half (R22)
+            uint32_t q = 31;
+#if BQ_LEAF_AWARE
+            if (Q.pivot_rule == BQ_PIVOT_SAMPLE64 && len > Q.leaf_max && len < 2 * Q.leaf_max) {
+                const uint32_t m = len / 16, t = Q.leaf_max - m;   // m < S / 8 here
+                if (len <= 2 * t) {
+                    const uint32_t k = (uint32_t)(((uint64_t)t * 64) / len);
+                    q = k < 1 ? 0 : (k > 63 ? 62 : k - 1);
+                }
+            }
+#endif
+            const K piv = select_pivot_warp<KT>(cbuf, cb[c], len, Q.pivot_rule, lane, nullptr, q);
             if (lane == 0) s_piv[c] = (uint64_t)piv;
             kind = C_BIN;
         }
