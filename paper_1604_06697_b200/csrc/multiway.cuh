@@ -38,6 +38,9 @@ constexpr int MW_K = 16;         // buckets of a multiway segment
 // pairs (one element per 16-byte vector); 32-byte records stay binary
 template <class KT>
 constexpr bool mw_capable() { return !KT::is_record || sizeof(typename KT::T) == 16; }
+#ifndef BQ_MW_FILL
+#define BQ_MW_FILL 50
+#endif
 constexpr int MW_SAMPLE = 256;   // sample keys per segment (8 per lane of one warp)
 
 template <class KT>
@@ -127,7 +130,8 @@ __device__ bool mw_splitters(const typename KT::T *buf, uint32_t b, uint32_t len
     using K = typename KT::K;
     K v[8];
     mw_sample_sorted<KT>(buf, b, len, lane, v);
-    uint64_t ke = ((uint64_t)len * 2 + leaf_max - 1) / leaf_max;
+    const uint64_t fl = (uint64_t)leaf_max * BQ_MW_FILL;   // buckets of about BQ_MW_FILL % of S
+    uint64_t ke = ((uint64_t)len * 100 + fl - 1) / fl;
     const uint32_t keff = (uint32_t)(ke < 2 ? 2 : (ke > kmax ? kmax : ke));
     // lane i (1 <= i < keff) holds real splitter s_i; lanes i >= keff repeat s_{keff-1}
     const uint32_t i = lane < 1 ? 1 : (lane < keff ? lane : keff - 1);

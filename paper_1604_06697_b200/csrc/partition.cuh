@@ -186,6 +186,9 @@ __device__ __forceinline__ void post_stats_flush(const PostParams<KT> &Q) {
 #ifndef BQ_LEAF_AWARE
 #define BQ_LEAF_AWARE 1
 #endif
+#ifndef BQ_LA_DIV
+#define BQ_LA_DIV 16   // margin len / 16: one standard deviation of the sample's rank error
+#endif
 template <class KT, int NT>
 __device__ __forceinline__ void emit_children(const PostParams<KT> &Q, int nch, const uint32_t *cb,
                                               const uint32_t *cl, uint8_t cp, uint16_t cd,
@@ -242,7 +245,7 @@ __device__ __forceinline__ void emit_children(const PostParams<KT> &Q, int nch, 
             uint32_t q = 31;
 #if BQ_LEAF_AWARE
             if (Q.pivot_rule == BQ_PIVOT_SAMPLE64 && len > Q.leaf_max && len < 2 * Q.leaf_max) {
-                const uint32_t m = len / 16, t = Q.leaf_max - m;   // m < S / 8 here
+                const uint32_t m = len / BQ_LA_DIV, t = Q.leaf_max - m;   // m < S / 4 here
                 if (len <= 2 * t) {
                     const uint32_t k = (uint32_t)(((uint64_t)t * 64) / len);
                     q = k < 1 ? 0 : (k > 63 ? 62 : k - 1);
