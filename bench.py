@@ -101,6 +101,7 @@ class ClockSampler:
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
         self.proc = None
+        self.offset = 0
         self.path = os.path.join(ROOT, "gpurun_out", f"clocks_rank{gpu_index}.csv")
 
     def start(self):
@@ -112,6 +113,20 @@ class ClockSampler:
                  "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
+            return
+        # nvidia-smi's start-up (driver attach) stalls CUDA calls of this
+        # process for tens of ms (measured: two 9 ms steps took 21-26 ms when
+        # it started inside the timed region); its steady 100 ms polling does
+        # not.  Wait for its first sample before the timed region begins.
+        t0 = time.time()
+        while time.time() - t0 < 5.0:
+            self.f.flush()
+            if os.path.getsize(self.path) > 0:
+                break
+            time.sleep(0.05)
+        time.sleep(0.2)
+        self.f.flush()
+        self.offset = os.path.getsize(self.path)   # samples from here on fall in (or just after) the timed region
 
     def stop(self):
         if self.proc is None:
@@ -123,11 +138,15 @@ class ClockSampler:
         except Exception:
             self.proc.kill()
         self.f.close()
-        rows = []
-        for line in open(self.path):
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) >= 9:
-                rows.append(parts)
+        def parse(text):
+            out = []
+            for line in text.splitlines():
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) >= 9:
+                    out.append(parts)
+            return out
+        text = open(self.path).read()
+        rows = parse(text[getattr(self, "offset", 0):]) or parse(text)
         if not rows:
             return None
         sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
