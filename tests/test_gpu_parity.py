@@ -564,3 +564,17 @@ def test_sort_nan_inputs_total_order(B, ways):
         assert np.array_equal(np.sort(got), np.sort(bits))
         k = _total_order_key(got)
         assert bool((k[1:] >= k[:-1]).all())
+
+
+@pytest.mark.parametrize("n", [8193, 9000, 12000, 13500])
+def test_leaf_aware_split(B, n):
+    """R22: an int32 segment one pass from its leaves (S < n <= 2(S - n/16),
+    S = 8192) is split at the sample quantile that leaves about S - n/16 keys
+    on the left: one binary pass still yields exactly two leaves (the
+    quantile never pushes the larger child past S) and the output equals the
+    oracle's."""
+    a = make("i32", n, seed=n)
+    t = to_dev(a)
+    st = B.bq_sort_ex(t, ways=2)
+    check_sorted_equal("i32", to_host(t, a), a)
+    assert st["levels"] == 1 and st["leaves"] == 2 and st["fallback_segments"] == 0
