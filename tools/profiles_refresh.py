@@ -41,7 +41,7 @@ Launch list of one c2 sort + 2 single passes (`tools/gpu_cmd_prof.sh`, ncu
 ```
 {part}```
 
-## k_leaf<KI32, 13> (ncu --set full, last of four launches)
+## k_leaf<KI32, 13> (ncu --set full; the longest captured launch)
 
 ```
 {leaf}```
