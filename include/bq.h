@@ -116,10 +116,9 @@ typedef struct {
                              records and every record is gathered once at the end (P:867-870:
                              the cost of moving large elements); 1: the passes move the
                              records themselves.  Sorted keys are identical. */
-    int32_t subtree;      /* != 0: segments of S < len <= 96 KB of elements are finished
-                             depth-first by one CTA in shared memory instead of by further
-                             level passes; 0 (default): level
-                             passes down to the leaf size */
+    int32_t subtree;      /* ignored (kept for ABI layout): the on-chip subtree pass it
+                             selected was superseded by leaves of S >= 9 Ki elements
+                              */
     int32_t reserved[1];  /* must be 0 */
 } bq_sort_options;
 
@@ -250,6 +249,12 @@ BQ_API bq_status bq_sort_ex(bq_kind kind, void *data, size_t n, const bq_sort_op
 BQ_API bq_status bq_sort_host(bq_kind kind, void *host_data, size_t n, void *dev_data,
                               const bq_sort_options *opt, void *ws, size_t ws_bytes,
                               void *stream);
+
+/* Tuning constants of `kind` (0 for a bad kind): the partition tile T (elements
+ * per tile of a pass) and the leaf size S (segments of at most S elements are
+ * finished by the shared-memory leaf sort, hot-path step a8). */
+BQ_API size_t bq_tile_elems(bq_kind kind);
+BQ_API size_t bq_leaf_elems(bq_kind kind);
 
 BQ_API const char *bq_status_string(bq_status s);
 BQ_API const char *bq_last_error(void);

@@ -12,7 +12,7 @@ from .bq import (  # noqa: F401
     bq_partition_u64,
     bq_pivot_f64, bq_pivot_i32, bq_pivot_records, bq_pivot_u64, bq_sort_ex, bq_sort_f64,
     bq_sort_host, bq_sort_i32, bq_sort_records, bq_sort_u64, bq_workspace_bytes, kind_of, partition,
-    pivot, sort, workspace, workspace_bytes, RECORDS_DEFAULT, RECORDS_DIRECT, RECORDS_KEYIDX,
+    pivot, sort, workspace, workspace_bytes, tile_elems, leaf_elems, KIND, RECORDS_DEFAULT, RECORDS_DIRECT, RECORDS_KEYIDX,
 )
 
 LIB_PATH = bq.LIB_PATH

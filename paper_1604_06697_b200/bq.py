@@ -84,6 +84,8 @@ _SIGS = {
     "bq_status_string": (ctypes.c_char_p, [_st]),
     "bq_last_error": (ctypes.c_char_p, []),
     "bq_version": (ctypes.c_int, []),
+    "bq_tile_elems": (_sz, [_st]),
+    "bq_leaf_elems": (_sz, [_st]),
 }
 for _name, (_res, _args) in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -345,3 +347,14 @@ def pivot(t, rule=BQ_PIVOT_MO3, ws=None, stream=None):
 
 def version() -> int:
     return int(_lib.bq_version())
+
+
+def tile_elems(kind: int) -> int:
+    """Partition tile T of `kind` (bq_tile_elems)."""
+    return int(_lib.bq_tile_elems(kind))
+
+
+def leaf_elems(kind: int) -> int:
+    """Leaf size S of `kind` (bq_leaf_elems): segments of <= S elements are
+    finished by the shared-memory leaf sort."""
+    return int(_lib.bq_leaf_elems(kind))

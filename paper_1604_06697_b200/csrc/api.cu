@@ -169,6 +169,28 @@ BQ_API const char *bq_status_string(bq_status s) {
 
 BQ_API const char *bq_last_error(void) { return bq::g_last_error; }
 
-BQ_API int bq_version(void) { return 100; }
+BQ_API int bq_version(void) { return 200; }
+
+BQ_API size_t bq_tile_elems(bq_kind kind) {
+    switch (kind) {
+        case BQ_I32: return bq::tile_elems<bq::KI32>();
+        case BQ_U64: return bq::tile_elems<bq::KU64>();
+        case BQ_F64: return bq::tile_elems<bq::KF64>();
+        case BQ_REC32: return bq::tile_elems<bq::KRec>();
+        case BQ_KEYIDX16: return bq::tile_elems<bq::KPair>();
+    }
+    return 0;
+}
+
+BQ_API size_t bq_leaf_elems(bq_kind kind) {
+    switch (kind) {
+        case BQ_I32: return bq::Tune<bq::KI32>::LEAF;
+        case BQ_U64: return bq::Tune<bq::KU64>::LEAF;
+        case BQ_F64: return bq::Tune<bq::KF64>::LEAF;
+        case BQ_REC32: return bq::Tune<bq::KRec>::LEAF;
+        case BQ_KEYIDX16: return bq::Tune<bq::KPair>::LEAF;
+    }
+    return 0;
+}
 
 }

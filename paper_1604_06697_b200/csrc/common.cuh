@@ -121,7 +121,10 @@ struct KPair {
 };
 
 // Per-kind tuning constants.  TILE = elements per partition tile (one CTA),
-// LEAF = largest segment finished by the shared-memory leaf sort (S).
+// LEAF = largest segment finished by the shared-memory leaf sort (S) =
+// LEAF_IPT keys per thread x LEAF_NT threads (leaf.cuh: a merge sort whose
+// runs start as per-thread register networks of LEAF_IPT keys; LEAF_IPT is
+// odd so that per-thread strided shared-memory accesses are conflict-free).
 // PART_THREADS = consumer threads of the partition kernel (one more producer
 // warp is added), PART_IPT = elements per consumer thread, PART_STAGES = TMA
 // load pipeline depth, PART_MINB = CTAs per SM the register budget targets.
@@ -135,38 +138,44 @@ template <class KT> struct Tune;
 #ifndef BQ_I32_MINB
 #define BQ_I32_MINB 2
 #endif
-#ifndef BQ_I32_LEAF
-#define BQ_I32_LEAF 8192
+#ifndef BQ_LEAF_IPT32
+#define BQ_LEAF_IPT32 31
+#endif
+#ifndef BQ_LEAF_NT32
+#define BQ_LEAF_NT32 1024
+#endif
+#ifndef BQ_LEAF_IPT64
+#define BQ_LEAF_IPT64 15
+#endif
+#ifndef BQ_LEAF_NT64
+#define BQ_LEAF_NT64 1024
+#endif
+#ifndef BQ_LEAF_IPTREC
+#define BQ_LEAF_IPTREC 9
+#endif
+#ifndef BQ_LEAF_NTREC
+#define BQ_LEAF_NTREC 1024
 #endif
 template <> struct Tune<KI32> {
     static constexpr int PART_THREADS = 256, PART_IPT = BQ_I32_IPT, PART_STAGES = BQ_I32_STAGES,
                          PART_MINB = BQ_I32_MINB;
-    static constexpr int LEAF = BQ_I32_LEAF, LEAF_THREADS = 512;
+    static constexpr int LEAF_IPT = BQ_LEAF_IPT32, LEAF_NT = BQ_LEAF_NT32, LEAF = LEAF_IPT * LEAF_NT;
 };
-#ifndef BQ_U64_LEAF
-#define BQ_U64_LEAF 4096
-#endif
 template <> struct Tune<KU64> {
     static constexpr int PART_THREADS = 256, PART_IPT = 8, PART_STAGES = 4, PART_MINB = 2;   // 16 KB tiles
-    static constexpr int LEAF = BQ_U64_LEAF, LEAF_THREADS = 512;
+    static constexpr int LEAF_IPT = BQ_LEAF_IPT64, LEAF_NT = BQ_LEAF_NT64, LEAF = LEAF_IPT * LEAF_NT;
 };
 template <> struct Tune<KF64> : Tune<KU64> {};
 #ifndef BQ_REC_STAGES
 #define BQ_REC_STAGES 4
 #endif
-#ifndef BQ_REC_LEAF
-#define BQ_REC_LEAF 2048
-#endif
-#ifndef BQ_PAIR_LEAF
-#define BQ_PAIR_LEAF 2048
-#endif
 template <> struct Tune<KRec> {
     static constexpr int PART_THREADS = 256, PART_IPT = 2, PART_STAGES = BQ_REC_STAGES, PART_MINB = 2;   // 16 KB tiles
-    static constexpr int LEAF = BQ_REC_LEAF, LEAF_THREADS = 512;
+    static constexpr int LEAF_IPT = BQ_LEAF_IPTREC, LEAF_NT = BQ_LEAF_NTREC, LEAF = LEAF_IPT * LEAF_NT;
 };
 template <> struct Tune<KPair> {
     static constexpr int PART_THREADS = 256, PART_IPT = 4, PART_STAGES = 4, PART_MINB = 2;   // 16 KB tiles
-    static constexpr int LEAF = BQ_PAIR_LEAF, LEAF_THREADS = 512;
+    static constexpr int LEAF_IPT = BQ_LEAF_IPTREC, LEAF_NT = BQ_LEAF_NTREC, LEAF = LEAF_IPT * LEAF_NT;
 };
 
 template <class KT> constexpr int tile_elems() { return Tune<KT>::PART_THREADS * Tune<KT>::PART_IPT; }

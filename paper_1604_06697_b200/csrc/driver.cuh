@@ -64,7 +64,6 @@ struct Layout {
     size_t scratch, status, tile_map[2], segs[2], cursor[2], ecursor[2], leaves[2], fallback, ctrl, misc, total;
     size_t msegs[2], mtile_map[2], mhist[2], mcursor[2];   // multiway segment lists (N4)
     size_t copies[2], max_copies;                           // records: finished equal runs to copy
-    size_t subs[2];                                         // N1 subtree jobs (subtree.cuh)
     size_t max_tiles, max_segs, max_leaves, max_fb;
 };
 
@@ -101,11 +100,8 @@ Layout<KT> make_layout(size_t n) {
     L.max_copies = KT::is_record ? LEVEL_BATCH * (L.max_segs + 2) + n / 65536 + 2 : 1;
     L.copies[0] = take(L.max_copies * sizeof(Leaf));
     L.copies[1] = take(L.max_copies * sizeof(Leaf));
-    // N1 subtree jobs of one batch (disjoint segments > S), per set
-    L.subs[0] = take(L.max_segs * sizeof(Leaf));
-    L.subs[1] = take(L.max_segs * sizeof(Leaf));
     L.ctrl = take((MAX_LEVELS + 1) * sizeof(LevelCtrl));   // [MAX_LEVELS]: the root's counts
-    L.misc = take(256);   // fallback count, leaf-list counts (2 sets x 8 classes), copy/subtree counts; pass counts
+    L.misc = take(256);   // fallback count, leaf-list counts (2 sets x 8 classes), copy counts, overflow flag; pass counts
     L.total = off;
     return L;
 }
@@ -156,20 +152,6 @@ bq_status launch_partition_fast(const PassParams<KT> &P, cudaStream_t s) {
 template <class F>
 bq_status persistent_cap(F kern, int threads, int smem, CapCache &cc, int *cap) {
     BQ_CK(resident_ctas(kern, threads, (size_t)smem, cc, cap));
-    return BQ_OK;
-}
-
-// the batch's subtree jobs (N1): persistent, one 1024-thread CTA per SM
-template <class KT>
-bq_status launch_subtree(const SubParams<KT> &SP, cudaStream_t s) {
-    auto kern = k_subtree<KT, SUB_THREADS>;
-    constexpr int smem = sub_smem_bytes<KT>();
-    static CapCache cc;
-    int cap = 0;
-    bq_status st = persistent_cap(kern, SUB_THREADS, smem, cc, &cap);
-    if (st != BQ_OK) return st;
-    kern<<<cap, SUB_THREADS, smem, s>>>(SP);
-    BQ_CK_LAUNCH();
     return BQ_OK;
 }
 
@@ -567,7 +549,7 @@ bq_status run_partition_segments(const typename KT::T *src, typename KT::T *dst,
 // Depth-capped segment: chunk leaf sorts + merge passes, result in the user buffer.
 template <class KT>
 bq_status run_fallback(const Leaf &f, typename KT::T *user, typename KT::T *scratch, Leaf *chunk_list,
-                       cudaStream_t s) {
+                       uint64_t n_total, cudaStream_t s) {
     using T = typename KT::T;
     constexpr uint32_t S = Tune<KT>::LEAF;
     T *bufs[2] = {user, scratch};
@@ -579,10 +561,12 @@ bq_status run_fallback(const Leaf &f, typename KT::T *user, typename KT::T *scra
     LP.bufs[0] = user;
     LP.bufs[1] = scratch;
     LP.out = nullptr;
-    LP.out_inplace = 1;
+    LP.out_other = 1;   // sorted chunks land in the other buffer
+    LP.n_total = n_total;
+    LP.aligned = aligned16(user) && aligned16(scratch);
     bq_status st = launch_leaves<KT>(leaf_nclass<KT>() - 1, LP, nch, s);
     if (st != BQ_OK) return st;
-    uint32_t cur = f.parity;
+    uint32_t cur = f.parity ^ 1;
     for (uint64_t w = S; w < f.len; w *= 2) {
         const uint64_t threads = (f.len + MERGE_IPT - 1) / MERGE_IPT;
         const uint32_t grid = (uint32_t)((threads + MERGE_THREADS - 1) / MERGE_THREADS);
@@ -606,9 +590,8 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
     constexpr int NCLS = leaf_nclass<KT>();
     bq_sort_stats local;
     std::memset(&local, 0, sizeof local);
-    int rule = BQ_PIVOT_SAMPLE64, depth_limit = -1, timing = 0, ordered = 0, ways = 0, subtree = 0;
+    int rule = BQ_PIVOT_SAMPLE64, depth_limit = -1, timing = 0, ordered = 0, ways = 0;
     if (opt) {
-        subtree = opt->subtree;
         rule = opt->pivot_rule;
         depth_limit = opt->depth_limit;
         timing = opt->timing;
@@ -676,21 +659,19 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
     LevelCtrl *root = ctrl + MAX_LEVELS;
     uint32_t *fb_count = reinterpret_cast<uint32_t *>(w + L.misc);
     // misc words: [0] fallback count, [4, 12) / [12, 20) leaf counts of set 0 / 1
-    // (by class), [20, 22) copy counts, [22, 24) subtree job counts, [24] overflow
+    // (by class), [20, 22) copy counts, [24] leaf-list overflow flag
     uint32_t *leaf_counts[2] = {fb_count + 4, fb_count + 12};   // [set][class]
     uint32_t *copy_counts[2] = {fb_count + 20, fb_count + 21};
     Leaf *copies[2] = {reinterpret_cast<Leaf *>(w + L.copies[0]), reinterpret_cast<Leaf *>(w + L.copies[1])};
-    Leaf *subs[2] = {reinterpret_cast<Leaf *>(w + L.subs[0]), reinterpret_cast<Leaf *>(w + L.subs[1])};
-    uint32_t *sub_counts[2] = {fb_count + 22, fb_count + 23};
     uint32_t *overflow = fb_count + 24;
-    // N1: subtrees of <= SUB elements finished on chip (bq_sort_options.subtree)
-    const uint32_t sub_max = (sub_enabled<KT>() && subtree) ? sub_elems<KT>() : 0;
 
     LeafParams<KT> LP{};
     LP.bufs[0] = user;
     LP.bufs[1] = scratch;
     LP.out = user;
-    LP.out_inplace = 0;
+    LP.out_other = 0;
+    LP.n_total = n;
+    LP.aligned = aligned16(user) && aligned16(scratch);
 
     if (n <= S) {
         k_single_leaf<<<1, 1, 0, s>>>(leaves[0], (uint32_t)n);
@@ -766,9 +747,7 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
         Q.ways = ways;
         Q.emit_children = 1;
         Q.band_inline_max = BAND_INLINE_MAX;
-        Q.subs = subs[set];
-        Q.sub_count = sub_counts[set];
-        Q.sub_max = sub_max;
+        Q.overflow = overflow;
         return Q;
     };
     {
@@ -790,7 +769,6 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
         if (batch >= 2) BQ_CKC(cudaStreamWaitEvent(s, ev_leaves[set], 0));
         BQ_CKC(cudaMemsetAsync(leaf_counts[set], 0, MAX_LEAF_CLASSES * sizeof(uint32_t), s));
         BQ_CKC(cudaMemsetAsync(copy_counts[set], 0, sizeof(uint32_t), s));
-        if (batch > 0) BQ_CKC(cudaMemsetAsync(sub_counts[set], 0, sizeof(uint32_t), s));   // batch 0: the root may be one
         for (int k = 0; k < LEVEL_BATCH; k++, level++) {
             const int cp = level & 1;
             const LevelCtrl *prev = level == 0 ? root : ctrl + level - 1;
@@ -859,28 +837,6 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
             if (st != BQ_OK) { cleanup(); return st; }
             local.kernel_launches += KT::is_record ? 2 : 1;
         }
-        // the batch's subtrees (N1), on chip; their pieces join this batch's leaves
-        if (sub_max) {
-            SubParams<KT> SP{};
-            SP.bufs[0] = user;
-            SP.bufs[1] = scratch;
-            SP.jobs = subs[set];
-            SP.job_count = sub_counts[set];
-            SP.leaves = leaves[set];
-            SP.leaf_counts = leaf_counts[set];
-            SP.leaf_cap = (uint32_t)L.max_leaves;
-            SP.fallback = fallback;
-            SP.fallback_count = fb_count;
-            SP.ctrl = ctrl + level - 1;
-            SP.overflow = overflow;
-            SP.leaf_max = S;
-            SP.depth_limit = depth_limit;
-            SP.pivot_rule = rule;
-            SP.aligned = aligned;
-            st = launch_subtree<KT>(SP, s);
-            if (st != BQ_OK) { cleanup(); return st; }
-            local.kernel_launches++;
-        }
         // leaves of this batch on the side stream
 #ifndef BQ_LEAF_MAIN
         cudaStream_t ls = side;
@@ -914,15 +870,11 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
 
     // statistics of every level, and the depth-capped segments
     BQ_CKC(cudaMemcpyAsync(hctrl, ctrl, level * sizeof(LevelCtrl), cudaMemcpyDeviceToHost, s));
-    uint32_t nfb_total = 0;
-    BQ_CKC(cudaMemcpyAsync(&hctrl[MAX_LEVELS].pad2[0], fb_count, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    uint32_t misc_h[25];
+    BQ_CKC(cudaMemcpyAsync(misc_h, fb_count, sizeof misc_h, cudaMemcpyDeviceToHost, s));
     BQ_CKC(cudaStreamSynchronize(s));
-    nfb_total = hctrl[MAX_LEVELS].pad2[0];
-    if (sub_max) {
-        uint32_t ovf = 0;
-        BQ_CKC(cudaMemcpy(&ovf, overflow, sizeof ovf, cudaMemcpyDeviceToHost));
-        if (ovf) { cleanup(); return set_error(BQ_ERR_CUDA, "leaf list overflow in the subtree pass"); }
-    }
+    const uint32_t nfb_total = misc_h[0];
+    if (misc_h[24]) { cleanup(); return set_error(BQ_ERR_CUDA, "leaf list overflow"); }
     for (int l = 0; l < level; l++) {
         const LevelCtrl &hc = hctrl[l];
         const uint32_t nseg_l = l == 0 ? 1u : hctrl[l - 1].nseg_next + hctrl[l - 1].nmseg_next;
@@ -941,7 +893,7 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
         BQ_CKC(cudaMemcpyAsync(fl.data(), fallback, nfb_total * sizeof(Leaf), cudaMemcpyDeviceToHost, s));
         BQ_CKC(cudaStreamSynchronize(s));
         for (const Leaf &f : fl) {
-            st = run_fallback<KT>(f, user, scratch, leaves[0], s);
+            st = run_fallback<KT>(f, user, scratch, leaves[0], n, s);
             if (st != BQ_OK) { cleanup(); return st; }
         }
     }

@@ -1,35 +1,35 @@
 // leaf.cuh — hot-path step a8: segments of at most S elements are finished on
-// one CTA by a bitonic sorting network (north_star (5): "small segments
-// finished in shared memory by a sorting network").  This is the role
-// Insertionsort plays below 17 elements in the paper (P:300-310,
-// P:1257-1258); the threshold is retuned for the on-chip memory of an SM.
+// one CTA in shared memory (north_star (5); "register
+// network for <= 32, then merge").  This is the role Insertionsort plays below
+// 17 elements in the paper; the threshold is retuned
+// to the on-chip memory of an SM (S = 31 Ki int32 keys, 15 Ki 64-bit keys,
+// 9 Ki key+index pairs), which removes the partition levels below it.
 //
-// Design (register-resident network, shared memory only for transposes).
-// A leaf of len keys is padded to a network of NET = 2^L >= len elements
-// (padding = the largest key, so it sorts last) and held in registers:
-// NT = 2^(L-R) threads x IPT = 2^R keys.  Element index i is spread over
-// (thread, register) by a *layout*: layout 0 puts index bits [0, R) in the
-// register number (thread t holds i = t*IPT + r), layout s >= 5 puts bits
-// [s, s+R) there.  Every compare-exchange of the network (stage bit b: i vs
-// i ^ 2^b) is done between two registers of one thread in a layout whose
-// register bits contain b; between stages whose bits live in different
-// layouts the keys are transposed through shared memory ("remap").  For
-// L = 13, R = 5 that is 19 remaps for the 91 stages of the network (the
-// previous version did all 91 stages in shared memory).  The few stages with
-// R <= b < 5 (records, R = 4) exchange between lanes with shuffles.
+// Algorithm (a merge sort whose base case is a sorting network):
+//   1. the leaf is loaded into a shared-memory plane (1D TMA bulk copy);
+//   2. thread t sorts the IPT keys at positions [t*IPT, (t+1)*IPT) in
+//      registers with Batcher's odd-even merge sort (a fixed network of
+//      compare-exchanges: no data-dependent branches);
+//   3. merge rounds: the runs of length RL = IPT * 2^r are merged pairwise
+//      until one run remains.  Every thread produces IPT consecutive outputs
+//      of its pair's merged run: it finds where its output range starts with
+//      a binary search on the "merge path" (the number of A keys among the
+//      first d outputs), then emits IPT outputs serially.  Runs are stored
+//      alternately ascending and descending, so the two runs of a pair form
+//      one bitonic sequence A-ascending | B-descending and every output is
+//      min(front of A, back of B): when one run is exhausted its pointer
+//      walks into the other run from that run's largest end, so the serial
+//      merge needs no bounds checks (a bitonic sequence's minimum is at one of
+//      its ends).  Outputs are written back in place after a barrier;
+//   4. the sorted plane is written to the user buffer with a TMA bulk store
+//      (keys), or the records are gathered by their leaf index (records and
+//      key+index pairs sort (key, index) and then move each record once).
+// Work per key: ~log2(IPT) network levels + ceil(log2(len / IPT)) merge
+// rounds of a handful of instructions, against the L(L+1)/2 compare-exchange
+// stages of a bitonic network of 2^L keys.
 //
-// Directions: instead of alternating ascending/descending compare-exchanges,
-// every compare-exchange is ascending on keys that are complemented (~x, an
-// order-reversing bijection) where the classic network sorts descending:
-// before merge m the keys whose index has bit m set are complemented, which
-// costs one LOP per key per merge.
-//
-// Shared memory: one plane per key component, element i at a swizzled byte
-// offset (16-byte chunk index XOR row bits) so that both the vector
-// (layout 0, 16-byte) and the scalar (layout s >= 5) accesses are free of
-// bank conflicts.  Records are sorted as (key, index) pairs (the index
-// breaks ties, so padding stays behind real keys) and gathered from a
-// shared-memory copy of the leaf at the end.
+// IPT is odd: thread t's keys sit at a stride of IPT words, so the per-thread
+// loads and stores of steps 2 and 3 are free of bank conflicts.
 #pragma once
 
 #include "common.cuh"
@@ -42,451 +42,454 @@ struct LeafParams {
     const Leaf *leaves;
     const uint32_t *count_dev;   // non-null: persistent grid over *count_dev leaves; else one leaf per CTA
     T *bufs[2];
-    T *out;            // destination buffer (the user buffer, or in-place for fallback chunks)
-    int out_inplace;   // 1: write back into bufs[parity] (fallback chunk sort)
+    T *out;            // destination buffer (the user buffer)
+    int out_other;     // 1: write into bufs[parity ^ 1] instead (fallback chunk sort)
+    uint64_t n_total;  // length of each data buffer (bounds the TMA reads)
+    int aligned;       // both data buffers (and out) 16-byte aligned -> TMA bulk copies
 };
 
-// ---- register element types and their compare-exchange --------------------
-struct RecKI {
+// ---- register element types -------------------------------------------------
+struct RecKI {   // record key + the record's position in its leaf
     uint64_t k;
     uint32_t i;
 };
 
-#ifndef BQ_LEAF_R32
-#define BQ_LEAF_R32 5
-#endif
-// 64-bit keys: 16 per thread at up to 1024 resident threads per SM (measured
-// on c3: 32 keys per thread at 256 threads left the SM latency-bound)
-#ifndef BQ_LEAF_R64
-#define BQ_LEAF_R64 4
-#endif
-#ifndef BQ_LEAF_OCC64
-#define BQ_LEAF_OCC64 1024
-#endif
-#ifndef BQ_LEAF_RREC
-#define BQ_LEAF_RREC 3
-#endif
-#ifndef BQ_LEAF_OCC32
-#define BQ_LEAF_OCC32 512
-#endif
-#ifndef BQ_LEAF_OCCREC
-#define BQ_LEAF_OCCREC 1024
-#endif
 template <class KT>
 struct LeafTraits {
     using E = typename KT::K;
-    static constexpr int R = sizeof(E) == 4 ? BQ_LEAF_R32 : BQ_LEAF_R64;   // log2(keys per thread)
-    static constexpr int OCC = sizeof(E) == 4 ? BQ_LEAF_OCC32 : BQ_LEAF_OCC64;   // resident threads/SM the registers target
+    static constexpr int IPT = Tune<KT>::LEAF_IPT, NTMAX = Tune<KT>::LEAF_NT;
 };
 template <>
 struct LeafTraits<KRec> {
     using E = RecKI;
-    static constexpr int R = BQ_LEAF_RREC;
-    static constexpr int OCC = BQ_LEAF_OCCREC;
+    static constexpr int IPT = Tune<KRec>::LEAF_IPT, NTMAX = Tune<KRec>::LEAF_NT;
+};
+template <>
+struct LeafTraits<KPair> {
+    using E = RecKI;
+    static constexpr int IPT = Tune<KPair>::LEAF_IPT, NTMAX = Tune<KPair>::LEAF_NT;
 };
 
-template <>
-struct LeafTraits<KPair> : LeafTraits<KRec> {};   // pairs sort as (key, leaf index) like records
-
+// Leaf classes: class c runs CTAs of 32 << c threads and takes leaves of up to
+// IPT * (32 << c) keys.
 template <class KT>
-constexpr int leaf_lmin() { return LeafTraits<KT>::R + 5; }   // one warp
-template <class KT>
-constexpr int leaf_lmax() {
-    int l = 0;
-    while ((1 << l) < Tune<KT>::LEAF) l++;
-    return l;
+constexpr int leaf_nclass() {
+    int c = 0;
+    while ((32 << c) < LeafTraits<KT>::NTMAX) c++;
+    return c + 1;
 }
-template <class KT>
-constexpr int leaf_nclass() { return leaf_lmax<KT>() - leaf_lmin<KT>() + 1; }
 constexpr int MAX_LEAF_CLASSES = 8;   // LevelCtrl::nleaf_cls, leaf-count words per set
-
-// network-size class of a leaf of `len` keys: NET = 2^(lmin + class)
 template <class KT>
 __host__ __device__ inline uint32_t leaf_class(uint32_t len) {
     uint32_t c = 0;
-    while ((1u << (leaf_lmin<KT>() + c)) < len) c++;
+    while ((uint32_t)LeafTraits<KT>::IPT * (32u << c) < len) c++;
     return c;
 }
 
+__device__ __forceinline__ bool e_less(int32_t a, int32_t b) { return a < b; }
+__device__ __forceinline__ bool e_less(uint64_t a, uint64_t b) { return a < b; }
+__device__ __forceinline__ bool e_less(const RecKI &a, const RecKI &b) {
+    return a.k < b.k || (a.k == b.k && a.i < b.i);
+}
 __device__ __forceinline__ void ce(int32_t &a, int32_t &b) {
     const int32_t lo = min(a, b), hi = max(a, b);
     a = lo;
     b = hi;
 }
-__device__ __forceinline__ void ce(uint64_t &a, uint64_t &b) {
-    const bool s = b < a;
-    const uint64_t lo = s ? b : a, hi = s ? a : b;
-    a = lo;
-    b = hi;
-}
-__device__ __forceinline__ bool e_less(const RecKI &a, const RecKI &b) {
-    return a.k < b.k || (a.k == b.k && a.i < b.i);
-}
-__device__ __forceinline__ bool e_less(int32_t a, int32_t b) { return a < b; }
-__device__ __forceinline__ bool e_less(uint64_t a, uint64_t b) { return a < b; }
-__device__ __forceinline__ void ce(RecKI &a, RecKI &b) {
+template <class E>
+__device__ __forceinline__ void ce(E &a, E &b) {
     const bool s = e_less(b, a);
-    const RecKI lo = s ? b : a, hi = s ? a : b;
+    const E lo = s ? b : a, hi = s ? a : b;
     a = lo;
     b = hi;
 }
-// w ^ m for m in {0, ~0}, computed as w * (2m + 1) + m (m = ~0: -w - 1 = ~w)
-// with IMADs, which issue on the FMA pipe: the network's compare-exchanges
-// keep the ALU pipe busy, the FMA pipe is idle
-__device__ __forceinline__ uint32_t flip_w(uint32_t w, uint32_t m) {
-    uint32_t s, r;
-    asm("mad.lo.u32 %0, %1, 2, 1;" : "=r"(s) : "r"(m));
-    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(w), "r"(s), "r"(m));
+
+// Batcher's odd-even merge sort on NP = 2^k >= N virtual elements, elements
+// N..NP-1 being +infinity: every comparator that touches them is a no-op and
+// is pruned at compile time (all comparators put the minimum at the lower
+// index, so an infinite element never moves).  The comparator list is built
+// by a constexpr function and applied by template recursion, so every
+// register index is a compile-time constant.
+constexpr int oem_np(int n) { return n <= 1 ? 1 : 2 * oem_np((n + 1) / 2); }
+struct OemNet {
+    int n;
+    short lo[640], hi[640];
+};
+constexpr OemNet oem_make(int N) {
+    OemNet r{};
+    const int NP = oem_np(N);
+    for (int p = 1; p < NP; p += p)
+        for (int k = p; k > 0; k /= 2)
+            for (int j = k % p; j + k < NP; j += k + k)
+                for (int i = 0; i < k && i + j + k < NP; i++) {
+                    const int lo = i + j, hi = i + j + k;
+                    if (hi < N && (lo / (p + p)) == (hi / (p + p))) {
+                        r.lo[r.n] = (short)lo;
+                        r.hi[r.n] = (short)hi;
+                        r.n++;
+                    }
+                }
     return r;
 }
-__device__ __forceinline__ void flip_if(int32_t &a, uint32_t m) { a = (int32_t)flip_w((uint32_t)a, m); }
-__device__ __forceinline__ void flip_if(uint64_t &a, uint32_t m) {
-    a = ((uint64_t)flip_w((uint32_t)(a >> 32), m) << 32) | flip_w((uint32_t)a, m);
+template <int N>
+struct OemConst {
+    static constexpr OemNet net = oem_make(N);
+};
+template <class E, int N, int I>
+__device__ __forceinline__ void oem_apply(E (&x)[N]) {
+    if constexpr (I < OemConst<N>::net.n) {
+        constexpr int lo = OemConst<N>::net.lo[I], hi = OemConst<N>::net.hi[I];
+        ce(x[lo], x[hi]);
+        oem_apply<E, N, I + 1>(x);
+    }
 }
-__device__ __forceinline__ void flip_if(RecKI &a, uint32_t m) {
-    flip_if(a.k, m);
-    a.i = flip_w(a.i, m);
-}
-__device__ __forceinline__ int32_t shfl_x(int32_t v, int m) { return __shfl_xor_sync(0xffffffffu, v, m); }
-__device__ __forceinline__ uint64_t shfl_x(uint64_t v, int m) { return __shfl_xor_sync(0xffffffffu, v, m); }
-__device__ __forceinline__ RecKI shfl_x(RecKI v, int m) {
-    return RecKI{__shfl_xor_sync(0xffffffffu, v.k, m), (uint32_t)__shfl_xor_sync(0xffffffffu, v.i, m)};
-}
-
-// ---- shared-memory planes -----------------------------------------------------
-// byte offset of element i in a plane of W-byte components whose layout-0
-// owner writes TB = IPT*W bytes: 16-byte chunk index XOR (row >> RS) & 7
-template <int W, int TB>
-__device__ __forceinline__ uint32_t swz(uint32_t i) {
-    constexpr int RS = TB >= 256 ? 1 + (TB >= 512) + (TB >= 1024) : 0;
-    const uint32_t b = i * W;
-    return b ^ ((((b >> 7) >> RS) & 7u) << 4);
+template <class E, int N>
+__device__ __forceinline__ void oem_sort(E (&x)[N]) {
+    static_assert(N <= 64, "per-thread network size");
+    oem_apply<E, N, 0>(x);
 }
 
-template <int L, int R, int S>
-__device__ __forceinline__ uint32_t lidx(uint32_t t, uint32_t r) {
-    if constexpr (S == 0)
-        return (t << R) + r;
-    else
-        return ((t >> S) << (S + R)) | (r << S) | (t & ((1u << S) - 1));
-}
+// ---- shared-memory planes ----------------------------------------------------
+// Slots are element indices of the leaf; a plane has SLACK slots of room on
+// both sides (the serial merge's pointers may run up to IPT + 1 slots past a
+// run's ends in outputs that are discarded) and VW more for the 16-byte
+// alignment offset of the TMA copies.
+constexpr int LEAF_SLACK = 64;
 
-// store / load one plane (component C of E) in layout S
-template <class KT>
-struct Planes;
-
-template <class KT>
-struct Planes {   // keys: one plane of K
+template <class KT, int NT>
+struct LeafSmem {
     using E = typename LeafTraits<KT>::E;
-    static constexpr int R = LeafTraits<KT>::R, IPT = 1 << R, W = sizeof(E), TB = IPT * W;
-    template <int NET>
-    static constexpr int bytes() { return NET * W; }
-    template <int L, int S>
-    static __device__ __forceinline__ void store(const E (&x)[IPT], unsigned char *sm, uint32_t t) {
-        if constexpr (S == 0) {
-            constexpr int PER = 16 / W;
-#pragma unroll
-            for (int c = 0; c < IPT / PER; c++) {
-                E tmp[PER];
-#pragma unroll
-                for (int j = 0; j < PER; j++) tmp[j] = x[c * PER + j];
-                uint4 v;
-                memcpy(&v, tmp, 16);
-                *reinterpret_cast<uint4 *>(sm + swz<W, TB>((t << R) + c * PER)) = v;
-            }
-        } else {
-#pragma unroll
-            for (int r = 0; r < IPT; r++) *reinterpret_cast<E *>(sm + swz<W, TB>(lidx<L, R, S>(t, r))) = x[r];
-        }
-    }
-    template <int L, int S>
-    static __device__ __forceinline__ void load(E (&x)[IPT], const unsigned char *sm, uint32_t t) {
-        if constexpr (S == 0) {
-            constexpr int PER = 16 / W;
-#pragma unroll
-            for (int c = 0; c < IPT / PER; c++) {
-                const uint4 v = *reinterpret_cast<const uint4 *>(sm + swz<W, TB>((t << R) + c * PER));
-                E tmp[PER];
-                memcpy(tmp, &v, 16);
-#pragma unroll
-                for (int j = 0; j < PER; j++) x[c * PER + j] = tmp[j];
-            }
-        } else {
-#pragma unroll
-            for (int r = 0; r < IPT; r++) x[r] = *reinterpret_cast<const E *>(sm + swz<W, TB>(lidx<L, R, S>(t, r)));
-        }
-    }
+    static constexpr int IPT = LeafTraits<KT>::IPT;
+    static constexpr int CAP = IPT * NT + 16 + 2 * LEAF_SLACK;   // slots per plane incl. slack
+    static constexpr bool REC = KT::is_record;
+    static constexpr size_t KEY_BYTES = (size_t)CAP * (REC ? 8 : sizeof(E));
+    static constexpr size_t bytes() { return 128 + KEY_BYTES + (REC ? (size_t)CAP * 4 : 0); }
+    // plane pointers at slot 0 (slots may be negative down to -LEAF_SLACK)
+    static __device__ __forceinline__ unsigned char *keyp(unsigned char *sm) { return sm + 128 + (size_t)LEAF_SLACK * (REC ? 8 : sizeof(E)); }
+    static __device__ __forceinline__ uint32_t *idxp(unsigned char *sm) { return reinterpret_cast<uint32_t *>(sm + 128 + KEY_BYTES) + LEAF_SLACK; }
 };
 
-template <>
-struct Planes<KRec> {   // records: key plane (8 B) + index plane (4 B)
-    using E = RecKI;
-    static constexpr int R = LeafTraits<KRec>::R, IPT = 1 << R;
-    template <int NET>
-    static constexpr int bytes() { return NET * 12; }
-    template <int L, int S>
-    static __device__ __forceinline__ void store(const E (&x)[IPT], unsigned char *sm, uint32_t t) {
-        constexpr int NET = 1 << L;
-        unsigned char *pk = sm, *pi = sm + NET * 8;
-        if constexpr (S == 0) {
-#pragma unroll
-            for (int c = 0; c < IPT / 2; c++) {
-                const uint4 v = make_uint4((uint32_t)x[2 * c].k, (uint32_t)(x[2 * c].k >> 32),
-                                           (uint32_t)x[2 * c + 1].k, (uint32_t)(x[2 * c + 1].k >> 32));
-                *reinterpret_cast<uint4 *>(pk + swz<8, IPT * 8>((t << R) + 2 * c)) = v;
-            }
-#pragma unroll
-            for (int c = 0; c < IPT / 4; c++) {
-                const uint4 v = make_uint4(x[4 * c].i, x[4 * c + 1].i, x[4 * c + 2].i, x[4 * c + 3].i);
-                *reinterpret_cast<uint4 *>(pi + swz<4, IPT * 4>((t << R) + 4 * c)) = v;
-            }
-        } else {
-#pragma unroll
-            for (int r = 0; r < IPT; r++) {
-                const uint32_t i = lidx<L, R, S>(t, r);
-                *reinterpret_cast<uint64_t *>(pk + swz<8, IPT * 8>(i)) = x[r].k;
-                *reinterpret_cast<uint32_t *>(pi + swz<4, IPT * 4>(i)) = x[r].i;
-            }
-        }
-    }
-    template <int L, int S>
-    static __device__ __forceinline__ void load(E (&x)[IPT], const unsigned char *sm, uint32_t t) {
-        constexpr int NET = 1 << L;
-        const unsigned char *pk = sm, *pi = sm + NET * 8;
-        if constexpr (S == 0) {
-#pragma unroll
-            for (int c = 0; c < IPT / 2; c++) {
-                const uint4 v = *reinterpret_cast<const uint4 *>(pk + swz<8, IPT * 8>((t << R) + 2 * c));
-                x[2 * c].k = (uint64_t)v.x | ((uint64_t)v.y << 32);
-                x[2 * c + 1].k = (uint64_t)v.z | ((uint64_t)v.w << 32);
-            }
-#pragma unroll
-            for (int c = 0; c < IPT / 4; c++) {
-                const uint4 v = *reinterpret_cast<const uint4 *>(pi + swz<4, IPT * 4>((t << R) + 4 * c));
-                x[4 * c].i = v.x;
-                x[4 * c + 1].i = v.y;
-                x[4 * c + 2].i = v.z;
-                x[4 * c + 3].i = v.w;
-            }
-        } else {
-#pragma unroll
-            for (int r = 0; r < IPT; r++) {
-                const uint32_t i = lidx<L, R, S>(t, r);
-                x[r].k = *reinterpret_cast<const uint64_t *>(pk + swz<8, IPT * 8>(i));
-                x[r].i = *reinterpret_cast<const uint32_t *>(pi + swz<4, IPT * 4>(i));
-            }
-        }
-    }
+// 32-bit shared-window accesses (explicit ld/st.shared: the loops below
+// walk byte addresses, with no generic-address conversion per access)
+__device__ __forceinline__ int32_t lds_e(uint32_t a, int32_t *) {
+    int32_t v;
+    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ uint64_t lds_e(uint32_t a, uint64_t *) {
+    uint64_t v;
+    asm volatile("ld.shared.b64 %0, [%1];" : "=l"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ uint32_t lds_e(uint32_t a, uint32_t *) {
+    uint32_t v;
+    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts_e(uint32_t a, int32_t v) { asm volatile("st.shared.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory"); }
+__device__ __forceinline__ void sts_e(uint32_t a, uint32_t v) { asm volatile("st.shared.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory"); }
+__device__ __forceinline__ void sts_e(uint32_t a, uint64_t v) { asm volatile("st.shared.b64 [%0], %1;" ::"r"(a), "l"(v) : "memory"); }
+
+// A plane seen through "cursors": keys walk byte addresses (cursor = address
+// of the slot, step W), records walk slot numbers over their two planes.
+template <class E>
+struct LPlane {   // keys: one plane of E
+    uint32_t k0;   // shared address of slot 0
+    static constexpr int STEP = (int)sizeof(E);
+    __device__ __forceinline__ uint32_t cur(int slot) const { return k0 + (uint32_t)(slot * STEP); }
+    __device__ __forceinline__ E ldc(uint32_t c) const { return lds_e(c, (E *)nullptr); }
+    __device__ __forceinline__ void stc(uint32_t c, E v) const { sts_e(c, v); }
 };
-
 template <>
-struct Planes<KPair> : Planes<KRec> {};
-
-// ---- the network ---------------------------------------------------------------
-template <class KT, int L>
-struct Net {
-    using E = typename LeafTraits<KT>::E;
-    using PL = Planes<KT>;
-    static constexpr int R = LeafTraits<KT>::R, IPT = 1 << R;
-    static_assert(L - R >= 5, "a network spans at least one warp");
-
-    template <int S1, int S2>
-    static __device__ __forceinline__ void remap(E (&x)[IPT], unsigned char *sm, uint32_t t) {
-        __syncthreads();   // previous readers of the plane are done
-        PL::template store<L, S1>(x, sm, t);
-        __syncthreads();
-        PL::template load<L, S2>(x, sm, t);
+struct LPlane<RecKI> {   // records: key plane (8 B) + index plane (4 B)
+    uint32_t k0, i0;
+    static constexpr int STEP = 1;
+    __device__ __forceinline__ uint32_t cur(int slot) const { return (uint32_t)slot; }
+    __device__ __forceinline__ RecKI ldc(uint32_t c) const {
+        return RecKI{lds_e(k0 + c * 8u, (uint64_t *)nullptr), lds_e(i0 + c * 4u, (uint32_t *)nullptr)};
     }
-
-    // compare-exchange of register pairs differing in register bit RB
-    template <int RB>
-    static __device__ __forceinline__ void regs(E (&x)[IPT]) {
-#pragma unroll
-        for (int r = 0; r < IPT; r++)
-            if (!(r & (1 << RB))) ce(x[r], x[r | (1 << RB)]);
-    }
-    // compare-exchange across lanes (layout 0, R <= B < 5)
-    template <int B>
-    static __device__ __forceinline__ void lanes(E (&x)[IPT], uint32_t t) {
-        constexpr int LB = B - R;
-        const bool upper = (t >> LB) & 1;
-#pragma unroll
-        for (int r = 0; r < IPT; r++) {
-            const E y = shfl_x(x[r], 1 << LB);
-            x[r] = (e_less(y, x[r]) != upper) ? y : x[r];
-        }
-    }
-
-    // stages for bits HB..0 of one merge, starting in layout CUR, ending in layout 0
-    template <int HB, int CUR>
-    static __device__ __forceinline__ void phase(E (&x)[IPT], unsigned char *sm, uint32_t t) {
-        if constexpr (HB < 0) {
-            if constexpr (CUR != 0) remap<CUR, 0>(x, sm, t);
-        } else if constexpr (HB >= 5 && HB >= R) {
-            constexpr int S = (HB - R + 1) > 5 ? (HB - R + 1) : 5;
-            if constexpr (S != CUR) remap<CUR, S>(x, sm, t);
-            bits_in<HB, S>(x);
-            phase<S - 1, S>(x, sm, t);
-        } else {
-            if constexpr (CUR != 0) remap<CUR, 0>(x, sm, t);
-            low_bits<HB>(x, t);
-        }
-    }
-    template <int B, int S>
-    static __device__ __forceinline__ void bits_in(E (&x)[IPT]) {   // B down to S, register bits of layout S
-        regs<B - S>(x);
-        if constexpr (B > S) bits_in<B - 1, S>(x);
-    }
-    template <int B>
-    static __device__ __forceinline__ void low_bits(E (&x)[IPT], uint32_t t) {   // B down to 0 in layout 0
-        if constexpr (B >= R)
-            lanes<B>(x, t);
-        else
-            regs<B>(x);
-        if constexpr (B > 0) low_bits<B - 1>(x, t);
-    }
-
-    // bit K of the index of (t, r) in layout 0, as a 0 / ~0 mask
-    template <int K>
-    static __device__ __forceinline__ uint32_t bitmask(uint32_t t, int r) {
-        if constexpr (K >= L) return 0u;
-        else if constexpr (K < R) return ((r >> K) & 1) ? ~0u : 0u;
-        else return ((t >> (K - R)) & 1) ? ~0u : 0u;
-    }
-    // merges M..L: during merge M the keys are complemented where index bit M
-    // is set (M < L), i.e. in the classic network's descending blocks; the
-    // transition from merge M-1 is an XOR with (bit M-1) ^ (bit M)
-    template <int M>
-    static __device__ __forceinline__ void merges(E (&x)[IPT], unsigned char *sm, uint32_t t) {
-#pragma unroll
-        for (int r = 0; r < IPT; r++) {
-            uint32_t m = bitmask<M>(t, r);
-            if constexpr (M > 1) m ^= bitmask<M - 1>(t, r);
-            flip_if(x[r], m);
-        }
-        phase<M - 1, 0>(x, sm, t);
-        if constexpr (M < L) merges<M + 1>(x, sm, t);
-    }
-
-    // sorts the NET keys held in layout S0 = L-R (thread t, register r: index
-    // r*NT + t); returns them sorted, in the same layout
-    static __device__ __forceinline__ void sort(E (&x)[IPT], unsigned char *sm, uint32_t t) {
-        constexpr int S0 = L - R;
-        __syncthreads();
-        PL::template store<L, S0>(x, sm, t);
-        __syncthreads();
-        PL::template load<L, 0>(x, sm, t);
-        merges<1>(x, sm, t);
-        remap<0, S0>(x, sm, t);
+    __device__ __forceinline__ void stc(uint32_t c, RecKI v) const {
+        sts_e(k0 + c * 8u, v.k);
+        sts_e(i0 + c * 4u, v.i);
     }
 };
 
 template <class KT>
-constexpr bool leaf_classes_fit() { return leaf_nclass<KT>() <= MAX_LEAF_CLASSES; }
-
-template <class KT, int L>
-constexpr size_t leaf_smem_bytes() {
-    static_assert(leaf_classes_fit<KT>(), "S / 2^(R+5) network classes exceed MAX_LEAF_CLASSES");
-    constexpr int NET = 1 << L;
-    size_t b = (size_t)Planes<KT>::template bytes<NET>();
-    if constexpr (KT::is_record) b += (size_t)NET * sizeof(typename KT::T);
-    return b;
+__device__ __forceinline__ typename LeafTraits<KT>::E leaf_pad() {
+    if constexpr (KT::is_record) return RecKI{~0ull, 0xffffffffu};   // after every real (key, index)
+    else return (typename LeafTraits<KT>::E)KT::KMAX;
 }
 
-// One leaf, by the whole CTA.  For keys it is called out of line from the
-// persistent loop below: inlined, the compiler hoists the transposes'
-// per-thread addresses out of the loop and spills.
-template <class KT, int L>
-__device__ __forceinline__ void leaf_body(const LeafParams<KT> &P, const Leaf lf, unsigned char *smem_raw) {
+// x[0, cnt) -> slots base + k * dir (dir = +1 ascending, -1 descending).
+// Full threads (cnt == IPT, all but at most one) store IPT consecutive
+// slots from their lowest one, each value selected from x[m] or x[IPT-1-m]:
+// one select and one store with an immediate offset per key.
+template <class E, int IPT, class PL>
+__device__ __forceinline__ void store_run(const PL &pl, const E (&x)[IPT], int cnt, int base, int dir) {
+    if (cnt == IPT) {
+        const bool rev = dir < 0;
+        const uint32_t c0 = pl.cur(rev ? base - (IPT - 1) : base);
+#pragma unroll
+        for (int m = 0; m < IPT; m++) pl.stc(c0 + (uint32_t)(m * PL::STEP), rev ? x[IPT - 1 - m] : x[m]);
+    } else {
+#pragma unroll
+        for (int k = 0; k < IPT; k++)
+            if (k < cnt) pl.stc(pl.cur(base + k * dir), x[k]);
+    }
+}
+
+// Barrier over the threads that share the runs of merge round r: a group of
+// G = 2^(r+1) threads reads and rewrites only its own slots, so rounds whose
+// groups fit a warp synchronise the warp, groups of up to 128 threads
+// synchronise their 128-thread slice on named barrier 1 + t / 128 (every use
+// of an id is by the same threads with the same count, so instances of
+// different rounds cannot mix), and larger groups the whole CTA.
+template <int NT>
+__device__ __forceinline__ void group_sync(int r, int t) {
+    const int G = 2 << r;
+    if (G <= 32) __syncwarp();
+    else if (G <= 128 && NT > 128) named_bar_sync(1u + ((uint32_t)t >> 7), 128u);
+    else __syncthreads();
+}
+
+// One leaf, by the whole CTA of NT threads.
+template <class KT, int NT>
+__device__ __forceinline__ void leaf_body(const LeafParams<KT> &P, const Leaf lf, unsigned char *sm, uint64_t *bar,
+                                          uint32_t &phase) {
     using T = typename KT::T;
     using K = typename KT::K;
     using E = typename LeafTraits<KT>::E;
-    constexpr int R = LeafTraits<KT>::R, IPT = 1 << R, NT = 1 << (L - R), NET = 1 << L;
-    unsigned char *planes = smem_raw;
-    const uint32_t t = threadIdx.x;
-    const uint32_t len = lf.len;
-    T *srcbuf = lf.parity ? P.bufs[1] : P.bufs[0];
-    T *out = P.out_inplace ? srcbuf : P.out;
+    using SM = LeafSmem<KT, NT>;
+    using PL = LPlane<E>;
+    constexpr int IPT = LeafTraits<KT>::IPT;
+    constexpr bool REC = KT::is_record;
+    constexpr uint32_t VW = REC ? 1u : 16u / (uint32_t)sizeof(T);
+    unsigned char *kp = SM::keyp(sm);
+    PL pl;
+    pl.k0 = smem_u32(kp);
+    if constexpr (REC) pl.i0 = smem_u32(SM::idxp(sm));
+    const int t = (int)threadIdx.x;
+    const int len = (int)lf.len;
+    T *src = lf.parity ? P.bufs[1] : P.bufs[0];
+    T *out = P.out_other ? (lf.parity ? P.bufs[0] : P.bufs[1]) : P.out;
     const uint64_t b = lf.begin;
 
-    E x[IPT];
-    if constexpr (KT::is_record) {
-        // leaf copy in shared memory (the output is gathered from it, so the
-        // leaf may be sorted in place)
-        T *sr = reinterpret_cast<T *>(smem_raw + Planes<KT>::template bytes<NET>());
-        constexpr uint32_t V = sizeof(T) / 16;   // 16-byte vectors per record
-        const uint4 *g = reinterpret_cast<const uint4 *>(srcbuf + b);
-        uint4 *s4 = reinterpret_cast<uint4 *>(sr);
-        for (uint32_t q = t; q < V * len; q += NT) s4[q] = g[q];
-        __syncthreads();
-#pragma unroll
-        for (int r = 0; r < IPT; r++) {
-            const uint32_t i = (uint32_t)r * NT + t;
-            x[r] = RecKI{i < len ? sr[i].key : ~0ull, i};
+    // ---- 1. load ------------------------------------------------------------
+    int off = 0;   // slot of leaf element 0 (keys: 16-byte alignment offset)
+    const T *gsrc = src;   // records: where the final gather reads from
+    if constexpr (!REC) {
+        off = (int)(b % VW);
+        const uint64_t lo16 = b - (uint64_t)off, hi16 = (b + (uint64_t)len + VW - 1) / VW * VW;
+        if (P.aligned && hi16 <= P.n_total) {
+            if (t == 0) {
+                fence_proxy_async_smem();   // earlier generic accesses of the plane precede the async write
+                const uint32_t bytes = (uint32_t)((hi16 - lo16) * sizeof(T));
+                mbar_arrive_expect_tx(bar, bytes);
+                tma_load_1d(kp, src + lo16, bytes, bar);
+            }
+            mbar_wait(bar, phase);
+            phase ^= 1;
+        } else {
+            for (int q = t; q < len; q += NT) reinterpret_cast<T *>(kp)[off + q] = src[b + q];
+            __syncthreads();
         }
-        Net<KT, L>::sort(x, planes, t);
+    } else {
+        // keys into the key plane; the gather reads the records from `src`,
+        // or, when the leaf already sits in the output buffer, from a copy of
+        // them in the same range of the other buffer (free: the segment owns
+        // [b, b + len) in both buffers)
+        T *other = lf.parity ? P.bufs[0] : P.bufs[1];
+        const bool copy = src == out;
+        if (copy) gsrc = other;
+        for (int q = t; q < len; q += NT) {
+            const T v = src[b + q];
+            reinterpret_cast<uint64_t *>(kp)[q] = KT::key(v);
+            if (copy) other[b + q] = v;
+        }
+        __syncthreads();
+    }
+
+    // ---- 2. per-thread network ---------------------------------------------------
+    E x[IPT];
+    const int nruns = (len + IPT - 1) / IPT;
+    {
+        const int s0 = t * IPT;
+        if constexpr (REC) {
 #pragma unroll
-        for (int r = 0; r < IPT; r++) {
-            const uint32_t i = (uint32_t)r * NT + t;
-            if (i < len) {
-                const uint4 *s = reinterpret_cast<const uint4 *>(sr + x[r].i);
-                uint4 *d = reinterpret_cast<uint4 *>(out + b + i);
+            for (int k = 0; k < IPT; k++) {
+                const int slot = s0 + k;
+                x[k] = slot < len ? RecKI{lds_e(pl.k0 + (uint32_t)slot * 8u, (uint64_t *)nullptr), (uint32_t)slot}
+                                  : leaf_pad<KT>();
+            }
+        } else {
+            const uint32_t c0 = pl.cur(off + s0);
+            if (s0 + IPT <= len) {
+#pragma unroll
+                for (int k = 0; k < IPT; k++) x[k] = (E)KT::key((T)pl.ldc(c0 + (uint32_t)(k * PL::STEP)));
+            } else {
+#pragma unroll
+                for (int k = 0; k < IPT; k++)
+                    x[k] = s0 + k < len ? (E)KT::key((T)pl.ldc(c0 + (uint32_t)(k * PL::STEP))) : leaf_pad<KT>();
+            }
+        }
+        oem_sort<E, IPT>(x);
+    }
+
+    // ---- 3. merge rounds ---------------------------------------------------------
+    // outputs of the current step: x[0, cnt) go to slots base + k * dir
+    int cnt = t < nruns ? min(IPT, len - t * IPT) : 0;
+    int base = t * IPT, dir = 1;
+    bool fin = nruns <= 1;
+    if (!fin && (t & 1)) {   // odd runs descending
+        base = t * IPT + cnt - 1;
+        dir = -1;
+    }
+    for (int r = 0; !fin; r++) {
+        // (the initial runs: each thread owns its slots, no barrier needed before)
+        store_run<E, IPT>(pl, x, cnt, off + base, dir);
+        group_sync<NT>(r, t);
+        const int RL = IPT << r;
+        const int g = t >> (r + 1), j = t & ((2 << r) - 1);
+        const int a0 = g * 2 * RL;
+        fin = 2 * RL >= len;
+        cnt = 0;
+        if (a0 < len) {
+            const int na = min(RL, len - a0), tot = min(2 * RL, len - a0), nb = tot - na;
+            const int d = j * IPT;
+            if (d < tot) {
+                cnt = min(IPT, tot - d);
+                // merge path: ai = #A keys among the first d outputs (ties: A first);
+                // B[q] sits at slot a0 + tot - 1 - q (descending): A[m] at cursor
+                // ca + m, B[d-1-m] at cursor cb + m
+                int lo = d > nb ? d - nb : 0, hi = d < na ? d : na;
+                const uint32_t ca = pl.cur(off + a0), cb = pl.cur(off + a0 + tot - d);
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    const uint32_t o = (uint32_t)(mid * PL::STEP);
+                    const E av = pl.ldc(ca + o), bv = pl.ldc(cb + o);
+                    if (e_less(bv, av)) hi = mid;
+                    else lo = mid + 1;
+                }
+                uint32_t pa = ca + (uint32_t)(lo * PL::STEP);
+                uint32_t pb = pl.cur(off + a0 + tot - 1 - (d - lo));
+                E ka = pl.ldc(pa), kb = pl.ldc(pb);
+#pragma unroll
+                for (int k = 0; k < IPT; k++) {
+                    const bool p = e_less(kb, ka);
+                    x[k] = p ? kb : ka;
+                    if (k + 1 < IPT) {
+                        pb -= p ? (uint32_t)PL::STEP : 0u;
+                        pa += p ? 0u : (uint32_t)PL::STEP;
+                        const E nv = pl.ldc(p ? pb : pa);
+                        if (p) kb = nv;
+                        else ka = nv;
+                    }
+                }
+                if (!fin && (g & 1)) {
+                    base = a0 + tot - 1 - d;
+                    dir = -1;
+                } else {
+                    base = a0 + d;
+                    dir = 1;
+                }
+            }
+        }
+        group_sync<NT>(r, t);   // the group has read its inputs before its slots are overwritten
+    }
+    __syncthreads();
+
+    // ---- 4. write out --------------------------------------------------------------
+    // x[0, cnt) are the outputs [base, base + cnt) of the sorted leaf (ascending)
+    if constexpr (REC) {
+#pragma unroll
+        for (int k = 0; k < IPT; k++) {
+            if (k < cnt) {
+                const uint32_t pos = (uint32_t)(base + k);
+                constexpr uint32_t V = sizeof(T) / 16;
+                const uint4 *s4 = reinterpret_cast<const uint4 *>(gsrc + b + x[k].i);
+                uint4 *d4 = reinterpret_cast<uint4 *>(out + b + pos);
                 uint4 v[V];
 #pragma unroll
-                for (uint32_t c = 0; c < V; c++) v[c] = s[c];
+                for (uint32_t c = 0; c < V; c++) v[c] = s4[c];
 #pragma unroll
-                for (uint32_t c = 0; c < V; c++) d[c] = v[c];
+                for (uint32_t c = 0; c < V; c++) d4[c] = v[c];
             }
         }
     } else {
+        T *plane = reinterpret_cast<T *>(kp);
+        E y[IPT];
 #pragma unroll
-        for (int r = 0; r < IPT; r++) {
-            const uint32_t i = (uint32_t)r * NT + t;
-            x[r] = i < len ? (E)KT::key(srcbuf[b + i]) : (E)KT::KMAX;
-        }
-        Net<KT, L>::sort(x, planes, t);
-#pragma unroll
-        for (int r = 0; r < IPT; r++) {
-            const uint32_t i = (uint32_t)r * NT + t;
-            if (i < len) out[b + i] = KT::from_key((K)x[r]);
+        for (int k = 0; k < IPT; k++) y[k] = (E)KT::from_key((K)x[k]);
+        store_run<E, IPT>(pl, y, cnt, off + base, 1);
+        if (P.aligned) {
+            fence_proxy_async_smem();
+            __syncthreads();
+            const uint64_t e = b + (uint64_t)len;
+            const uint64_t ls = (b + VW - 1) / VW * VW, le = e / VW * VW;
+            if (t == 0 && le > ls) {
+                tma_store_1d(out + ls, plane + off + (ls - b), (uint32_t)((le - ls) * sizeof(T)));
+                bulk_commit();
+            }
+            // head and tail (< 16 bytes each) outside the bulk body
+            if (t < 2 * (int)VW) {   // (NT may be a single warp)
+                const int u = t;
+                const bool tail = u >= (int)VW;
+                const uint64_t pos = tail ? (le > ls ? le : ls) + (uint64_t)(u - VW) : b + (uint64_t)u;
+                const bool ok = tail ? pos < e : pos < (ls < e ? ls : e);
+                if (ok) out[pos] = plane[off + (pos - b)];
+            }
+            if (t == 0) bulk_wait_read0();   // the plane may be reused once the store has read it
+        } else {
+            __syncthreads();
+            for (int q = t; q < len; q += NT) out[b + q] = plane[off + q];
         }
     }
 }
 
-template <class KT, int L>
-__device__ __noinline__ void leaf_one(const LeafParams<KT> &P, const Leaf lf, unsigned char *smem_raw) {
-    leaf_body<KT, L>(P, lf, smem_raw);
-}
-
-template <class KT, int L>
-__global__ void __launch_bounds__(1 << (L - LeafTraits<KT>::R), (LeafTraits<KT>::OCC >> (L - LeafTraits<KT>::R)) > 0 ? (LeafTraits<KT>::OCC >> (L - LeafTraits<KT>::R)) : 1) k_leaf(LeafParams<KT> P) {
+template <class KT, int NT>
+__global__ void __launch_bounds__(NT, (LeafTraits<KT>::NTMAX / NT) > 0 ? LeafTraits<KT>::NTMAX / NT : 1)
+    k_leaf(LeafParams<KT> P) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw);
+    if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    uint32_t phase = 0;
     const uint32_t nleaves = P.count_dev ? *P.count_dev : gridDim.x;
     for (uint32_t li = blockIdx.x; li < nleaves; li += gridDim.x) {
-        if (li != blockIdx.x) __syncthreads();   // the previous leaf's shared-memory readers are done
-        // (keys: out of line, see leaf_one; records measured faster inlined)
-        if constexpr (KT::is_record) leaf_body<KT, L>(P, P.leaves[li], smem_raw);
-        else leaf_one<KT, L>(P, P.leaves[li], smem_raw);
+        if (li != blockIdx.x) __syncthreads();   // the previous leaf's readers of the planes are done
+        if (threadIdx.x == 0 && li + gridDim.x < nleaves) {
+            // warm L2 with this CTA's next leaf while this one is sorted
+            const Leaf nx = P.leaves[li + gridDim.x];
+            const typename KT::T *nsrc = nx.parity ? P.bufs[1] : P.bufs[0];
+            const uint64_t a = (uint64_t)(nsrc + nx.begin) & ~15ull;
+            const uint64_t z = ((uint64_t)(nsrc + nx.begin + nx.len) + 15) & ~15ull;
+            if (P.aligned && z > a)
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"((uint32_t)(z - a)) : "memory");
+        }
+        leaf_body<KT, NT>(P, P.leaves[li], smem_raw, bar, phase);
     }
+    if (threadIdx.x == 0) bulk_wait0();
 }
 
-// host: launch the leaf kernel of class c (NET = 2^(lmin + c)) over `count` leaves
+template <class KT, int NT>
+constexpr size_t leaf_smem_bytes() {
+    return LeafSmem<KT, NT>::bytes();
+}
+
+// host: launch the leaf kernel of class c (NT = 32 << c) over `count` leaves
 // count > 0: one CTA per leaf; count == 0: persistent grid (resident CTAs)
 // over LP.count_dev leaves
-template <class KT, int L>
-cudaError_t launch_leaf_l(const LeafParams<KT> &LP, uint32_t count, cudaStream_t s) {
-    constexpr size_t smem = leaf_smem_bytes<KT, L>();
-    constexpr int NT = 1 << (L - LeafTraits<KT>::R);
+template <class KT, int NT>
+cudaError_t launch_leaf_nt(const LeafParams<KT> &LP, uint32_t count, cudaStream_t s) {
+    constexpr size_t smem = leaf_smem_bytes<KT, NT>();
     static CapCache cc;
     int cap = 0;
-#ifdef BQ_LEAF_CTAS_PER_SM
-    constexpr int per_sm_max = BQ_LEAF_CTAS_PER_SM;   // leave room for co-resident partition CTAs
-#else
-    constexpr int per_sm_max = 0;
-#endif
-    cudaError_t e = resident_ctas(k_leaf<KT, L>, NT, smem, cc, &cap, per_sm_max);
+    cudaError_t e = resident_ctas(k_leaf<KT, NT>, NT, smem, cc, &cap);
     if (e != cudaSuccess) return e;
-    k_leaf<KT, L><<<count ? count : (uint32_t)cap, NT, smem, s>>>(LP);
+    k_leaf<KT, NT><<<count ? count : (uint32_t)cap, NT, smem, s>>>(LP);
     return cudaGetLastError();
 }
 
@@ -495,7 +498,7 @@ cudaError_t launch_leaf_class(int cls, const LeafParams<KT> &LP, uint32_t count,
     if constexpr (C >= leaf_nclass<KT>()) {
         return cudaErrorInvalidValue;
     } else {
-        if (cls == C) return launch_leaf_l<KT, leaf_lmin<KT>() + C>(LP, count, s);
+        if (cls == C) return launch_leaf_nt<KT, (32 << C)>(LP, count, s);
         return launch_leaf_class<KT, C + 1>(cls, LP, count, s);
     }
 }

@@ -66,7 +66,6 @@ __device__ __forceinline__ uint32_t pass_ntiles(const PassParams<KT> &P) {
 #include "multiway.cuh"
 #include "multiway8.cuh"
 #include "inplace.cuh"
-#include "subtree.cuh"
 
 namespace bq {
 
@@ -109,10 +108,8 @@ struct PostParams {
     // scratch buffer, copied to the user buffer by k_copy_runs
     Leaf *copies;
     uint32_t *copy_count;
-    // N1 subtrees: children of S < len <= sub_max go to this list (subtree.cuh)
-    Leaf *subs;
-    uint32_t *sub_count;
-    uint32_t sub_max;       // 0: off
+    // set to 1 when a leaf list would overflow (the call then fails)
+    uint32_t *overflow;
 };
 
 template <class KT>
@@ -197,7 +194,7 @@ __device__ __forceinline__ void emit_children(const PostParams<KT> &Q, int nch, 
     using K = typename KT::K;
     constexpr uint32_t TILE = (uint32_t)tile_elems<KT>();
     constexpr int NW = NT / 32;
-    enum { C_NONE = 0, C_LEAF, C_FALLBACK, C_BIN, C_MW, C_BAND, C_SUB };
+    enum { C_NONE = 0, C_LEAF, C_FALLBACK, C_BIN, C_MW, C_BAND };
     __shared__ uint32_t s_kind[MW_K], s_idx[MW_K], s_tb[MW_K], s_nt[MW_K], s_mode[MW_K];
     __shared__ uint64_t s_piv[MW_K];
     __shared__ K s_tree[MW_K][MW_K];
@@ -213,7 +210,6 @@ __device__ __forceinline__ void emit_children(const PostParams<KT> &Q, int nch, 
         else if (h == 2) kind = C_BAND;
         else if (len <= Q.leaf_max) kind = C_LEAF;
         else if ((int)cd >= Q.depth_limit) kind = C_FALLBACK;
-        else if (h == 0 && len <= Q.sub_max) kind = C_SUB;
         else if (h == 1) {
             kind = C_BIN;
             mode = 1;
@@ -272,9 +268,8 @@ __device__ __forceinline__ void emit_children(const PostParams<KT> &Q, int nch, 
             const uint32_t li = atomicAdd(&Q.leaf_counts[lc], 1u);
             atomicAdd(&post_stats().nleaf_cls[lc], 1u);
             atomicAdd(&post_stats().nleaf, 1u);
-            Q.leaves[lc * Q.leaf_cap + li] = Leaf{cb[c], len, cp, 0};
-        } else if (kind == C_SUB) {
-            Q.subs[atomicAdd(Q.sub_count, 1u)] = Leaf{cb[c], len, cp, cd};
+            if (li < Q.leaf_cap) Q.leaves[lc * Q.leaf_cap + li] = Leaf{cb[c], len, cp, 0};
+            else if (Q.overflow) *Q.overflow = 1u;
         } else if (kind == C_FALLBACK) {
             const uint32_t fi = atomicAdd(Q.fallback_count, 1u);
             atomicAdd(&post_stats().nfallback, 1u);

@@ -17,7 +17,9 @@ from test_gpu_parity import check_sorted_equal, make
 
 pytestmark = pytest.mark.gpu
 
-T_PAIR, S_PAIR = 1024, 2048
+import paper_1604_06697_b200 as _bq
+
+T_PAIR, S_PAIR = _bq.tile_elems(_bq.BQ_KEYIDX16), _bq.leaf_elems(_bq.BQ_KEYIDX16)
 
 
 @pytest.fixture(scope="module")

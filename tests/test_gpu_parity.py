@@ -15,9 +15,11 @@ from gpu_util import three_list, to_dev, to_host
 
 pytestmark = pytest.mark.gpu
 
-# tile T and leaf S per kind (csrc/common.cuh Tune<>)
-TILE = {"i32": 4096, "u64": 2048, "f64": 2048, "rec32": 512}
-LEAF = {"i32": 8192, "u64": 4096, "f64": 4096, "rec32": 2048}
+import paper_1604_06697_b200 as _bq
+
+# tile T and leaf S per kind (csrc/common.cuh Tune<>, queried through the C-ABI)
+TILE = {k: _bq.tile_elems(_bq.KIND[k]) for k in ("i32", "u64", "f64", "rec32")}
+LEAF = {k: _bq.leaf_elems(_bq.KIND[k]) for k in ("i32", "u64", "f64", "rec32")}
 
 
 def edge_sizes(kind):
@@ -156,10 +158,11 @@ def test_sort_special_f64(B):
 
 @pytest.mark.parametrize("kind", ["i32", "f64", "rec32"])
 def test_depth_cap_fallback(B, kind):
-    # a tiny Introsort limit sends segments to the merge-based fallback (a9)
-    n = 300007
+    # a tiny Introsort limit sends segments to the merge-based fallback (a9):
+    # with n ~ 10 S, segments at depth <= 2 are still longer than S
+    n = 10 * LEAF[kind] + 7
     a = make(kind, n, seed=9)
-    for ways, limits in [(2, [0, 1, 3]), (16, [0, 1])]:
+    for ways, limits in [(2, [0, 1, 2]), (16, [0, 1])]:
         for limit in limits:
             t = to_dev(a)
             st = B.bq_sort_ex(t, depth_limit=limit, ways=ways)
@@ -566,13 +569,13 @@ def test_sort_nan_inputs_total_order(B, ways):
         assert bool((k[1:] >= k[:-1]).all())
 
 
-@pytest.mark.parametrize("n", [8193, 9000, 12000, 13500])
-def test_leaf_aware_split(B, n):
-    """R22: an int32 segment one pass from its leaves (S < n <= 2(S - n/16),
-    S = 8192) is split at the sample quantile that leaves about S - n/16 keys
-    on the left: one binary pass still yields exactly two leaves (the
-    quantile never pushes the larger child past S) and the output equals the
-    oracle's."""
+@pytest.mark.parametrize("frac", [1.0001, 1.1, 1.45, 1.65])
+def test_leaf_aware_split(B, frac):
+    """R22: an int32 segment one pass from its leaves (S < n <= 2(S - n/16))
+    is split at the sample quantile that leaves about S - n/16 keys on the
+    left: one binary pass still yields exactly two leaves (the quantile never
+    pushes the larger child past S) and the output equals the oracle's."""
+    n = int(LEAF["i32"] * frac) + 1
     a = make("i32", n, seed=n)
     t = to_dev(a)
     st = B.bq_sort_ex(t, ways=2)
