@@ -28,9 +28,10 @@
  *   - Errors are returned as bq_status; no exception crosses the ABI.  On
  *     BQ_ERR_CUDA the CUDA error text is available from bq_last_error()
  *     (thread-local).  A device that is not sm_100 gives BQ_ERR_UNSUPPORTED.
- *   - The library holds no global mutable state except an immutable per-device
- *     cache of launch limits; concurrent calls on disjoint data and distinct
- *     workspaces are safe.
+ *   - The library's only mutable host state is a per-device cache of launch
+ *     limits and a mutex-protected cache of instantiated sort graphs (see
+ *     bq_sort_*); concurrent calls on disjoint data and distinct workspaces are
+ *     safe.
  *
  * Orders
  *   - int32, uint64: natural order (signed / unsigned).
@@ -99,7 +100,8 @@ typedef struct {
 typedef struct {
     int32_t pivot_rule;   /* bq_pivot_rule for segments > leaf size; default SAMPLE64 */
     int32_t depth_limit;  /* < 0: Introsort limit 2*floor(log2 n)+3 */
-    int32_t timing;       /* != 0: time every partition launch with CUDA events */
+    int32_t timing;       /* != 0: host-driven level loop, CUDA events around every partition
+                             launch (bq_sort_stats.partition_ms); the call waits */
     int32_t ordered;      /* != 0: ticket-ordered tile placement (decoupled look-back),
                              deterministic layout; 0: one atomicAdd per tile (faster; tiles
                              of a segment placed in completion order; records then move
@@ -229,16 +231,30 @@ BQ_API bq_status bq_partition_segments(bq_kind kind, const void *src, void *dst,
                                        int ordered, void *ws, size_t ws_bytes, void *stream);
 
 /* ---- sort (hot-path steps a1-a9) ---------------------------------------------
- * Sorts data[0, n) ascending in place (orders above).  Enqueued on `stream`;
- * the level loop reads one small counter block back per partition level
- * (the call returns after the stream has drained). */
+ * Sorts data[0, n) ascending in place (orders above).  Fully asynchronous:
+ * the whole sort is enqueued on `stream` and the call returns without waiting
+ * for it (the sorted data is valid once the stream reaches that point; `ws`
+ * must stay allocated until then).  The breadth-first level loop that replaces
+ * the paper's explicit stack runs on the device: a CUDA graph
+ * whose WHILE node repeats a batch of partition levels while the last level
+ * produced children, sorting the previous batch's leaves concurrently, then
+ * finishes depth-capped segments (a9) under an IF node.  The instantiated
+ * graph is cached per (device, kind, data, n, ws, ws_bytes, options); the
+ * cache holds at most 32 graphs (least recently used evicted) and is the
+ * library's only mutable host state besides the launch-limit cache. */
 BQ_API bq_status bq_sort_i32(int32_t *keys, size_t n, void *ws, size_t ws_bytes, void *stream);
 BQ_API bq_status bq_sort_u64(uint64_t *keys, size_t n, void *ws, size_t ws_bytes, void *stream);
 BQ_API bq_status bq_sort_f64(double *keys, size_t n, void *ws, size_t ws_bytes, void *stream);
 BQ_API bq_status bq_sort_records(bq_record32 *recs, size_t n, void *ws, size_t ws_bytes,
                                  void *stream);
 
-/* Kind-generic sort with options (NULL = defaults) and statistics (NULL = none). */
+/* Kind-generic sort with options (NULL = defaults) and statistics (NULL =
+ * none).  Asynchronous like bq_sort_*, except that stats != NULL or
+ * opt->timing != 0 makes the call wait for the stream (the statistics are
+ * device counters; timing runs the level loop from the host with CUDA events
+ * around every partition launch).  A leaf-list overflow (never expected: the
+ * lists are sized for every child of a level) is reported as BQ_ERR_CUDA only
+ * when the call waits. */
 BQ_API bq_status bq_sort_ex(bq_kind kind, void *data, size_t n, const bq_sort_options *opt,
                             bq_sort_stats *stats, void *ws, size_t ws_bytes, void *stream);
 

@@ -3,6 +3,8 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
+#include <vector>
 
 #include "api_kind.cuh"
 
@@ -37,6 +39,44 @@ bq_status check_device() {
     }
     if (ok < 0) return set_error(BQ_ERR_UNSUPPORTED, "libbq.so is built for sm_100a only");
     return BQ_OK;
+}
+
+// Instantiated sort graphs (driver.cuh build_sort_graph), keyed by device,
+// kind, buffers, n and options: a small LRU list under a mutex.  The graphs
+// are never destroyed at exit (the CUDA context may already be gone).
+namespace {
+struct GraphSlot {
+    GraphKey key;
+    cudaGraphExec_t exec;
+    uint64_t used;
+};
+std::mutex g_graph_mu;
+std::vector<GraphSlot> *g_graphs = new std::vector<GraphSlot>();
+uint64_t g_graph_clock = 0;
+constexpr size_t GRAPH_SLOTS = 32;
+}  // namespace
+
+bool graph_cache_get(const GraphKey &k, cudaGraphExec_t *ex) {
+    std::lock_guard<std::mutex> lk(g_graph_mu);
+    for (auto &g : *g_graphs)
+        if (g.key == k) {
+            g.used = ++g_graph_clock;
+            *ex = g.exec;
+            return true;
+        }
+    return false;
+}
+
+void graph_cache_put(const GraphKey &k, cudaGraphExec_t ex) {
+    std::lock_guard<std::mutex> lk(g_graph_mu);
+    if (g_graphs->size() >= GRAPH_SLOTS) {
+        size_t lru = 0;
+        for (size_t i = 1; i < g_graphs->size(); i++)
+            if ((*g_graphs)[i].used < (*g_graphs)[lru].used) lru = i;
+        cudaGraphExecDestroy((*g_graphs)[lru].exec);
+        g_graphs->erase(g_graphs->begin() + lru);
+    }
+    g_graphs->push_back(GraphSlot{k, ex, ++g_graph_clock});
 }
 
 }  // namespace bq

@@ -87,7 +87,6 @@ static bq_status sort_rec_ki(Rec32 *data, size_t n, const bq_sort_options *opt, 
     BQ_CK_LAUNCH();
     BQ_CK(cudaMemcpyAsync(data, gath, n * sizeof(Rec32), cudaMemcpyDeviceToDevice, s));
     if (st) st->kernel_launches += 3;
-    BQ_CK(cudaStreamSynchronize(s));
     return BQ_OK;
 }
 

@@ -24,15 +24,10 @@
 #include "fallback.cuh"
 #include "leaf.cuh"
 #include "partition.cuh"
+#include "loop.cuh"
 
 namespace bq {
 
-constexpr int MAX_LEVELS = 128;
-// the level loop is enqueued LEVEL_BATCH levels at a time between host checks
-#ifndef BQ_LEVEL_BATCH
-#define BQ_LEVEL_BATCH 4
-#endif
-constexpr int LEVEL_BATCH = BQ_LEVEL_BATCH;
 constexpr uint32_t POST_GRID = 148 * 8;
 constexpr int POST_THREADS = 256;
 // the sort's per-level k_post: one small CTA (a warp per child) per segment,
@@ -42,7 +37,6 @@ constexpr int POST_THREADS = 256;
 #endif
 constexpr int POST_LEVEL_THREADS = BQ_POST_LEVEL_THREADS;
 constexpr uint32_t POST_LEVEL_GRID = 148 * (2048 / POST_LEVEL_THREADS < 32 ? 2048 / POST_LEVEL_THREADS : 32);
-constexpr int MERGE_THREADS = 256, MERGE_IPT = 8;
 
 bq_status set_error(bq_status st, const char *fmt, ...);
 bq_status check_device();
@@ -64,6 +58,7 @@ struct Layout {
     size_t scratch, status, tile_map[2], segs[2], cursor[2], ecursor[2], leaves[2], fallback, ctrl, misc, total;
     size_t msegs[2], mtile_map[2], mhist[2], mcursor[2];   // multiway segment lists (N4)
     size_t copies[2], max_copies;                           // records: finished equal runs to copy
+    size_t tprefix, fbst;                                   // a9 over the depth-capped segments
     size_t max_tiles, max_segs, max_leaves, max_fb;
 };
 
@@ -74,9 +69,12 @@ Layout<KT> make_layout(size_t n) {
     Layout<KT> L;
     L.max_segs = n / (S + 1) + 2;                 // segments > S are disjoint
     L.max_tiles = n / TILE + 2 * L.max_segs + 2;
-    // leaves of one batch of LEVEL_BATCH levels per class list; also fallback chunks
-    L.max_leaves = LEVEL_BATCH * (2 * L.max_segs + 2) + (n / S + 2);
     L.max_fb = n / (S + 1) + 2;
+    // the leaf lists of one level (set level & 1): at most kmax children per
+    // segment; set 0's class-0 list also holds the fallback's chunks at the end
+    const size_t per_level = L.max_segs * (mw_capable<KT>() ? MW_K : 2);
+    L.max_leaves = per_level;
+    if (L.max_leaves < n / S + L.max_fb + 2) L.max_leaves = n / S + L.max_fb + 2;
     size_t off = 0;
     auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + bytes, 256); return o; };
     L.scratch = take(n * sizeof(typename KT::T));
@@ -93,15 +91,17 @@ Layout<KT> make_layout(size_t n) {
         L.mhist[p] = take(MW_K * L.max_segs * sizeof(uint32_t));
         L.mcursor[p] = take(MW_K * L.max_segs * sizeof(uint32_t));
     }
-    // one list per leaf network-size class (leaf.cuh), max_leaves each
+    // per set, one list per leaf class (leaf.cuh), max_leaves each
     L.leaves[0] = take(leaf_nclass<KT>() * L.max_leaves * sizeof(Leaf));
     L.leaves[1] = take(leaf_nclass<KT>() * L.max_leaves * sizeof(Leaf));
     L.fallback = take(L.max_fb * sizeof(Leaf));
-    L.max_copies = KT::is_record ? LEVEL_BATCH * (L.max_segs + 2) + n / 65536 + 2 : 1;
+    L.max_copies = KT::is_record ? L.max_segs + 2 + n / 65536 + 2 : 1;
     L.copies[0] = take(L.max_copies * sizeof(Leaf));
     L.copies[1] = take(L.max_copies * sizeof(Leaf));
+    L.tprefix = take((L.max_fb + 1) * sizeof(uint32_t));
+    L.fbst = take(sizeof(FbState));
     L.ctrl = take((MAX_LEVELS + 1) * sizeof(LevelCtrl));   // [MAX_LEVELS]: the root's counts
-    L.misc = take(256);   // fallback count, leaf-list counts (2 sets x 8 classes), copy counts, overflow flag; pass counts
+    L.misc = take(256);   // LoopMisc (loop.cuh); bq_pivot_*: the pivot
     L.total = off;
     return L;
 }
@@ -170,12 +170,14 @@ bq_status launch_multiway(MwParams<KT> MP, LevelCtrl *lc, cudaStream_t s, int wa
         if (st != BQ_OK) return st;
         st = persistent_cap(ks8, threads, smem8, cc_s8, &cap_s8);
         if (st != BQ_OK) return st;
-        MP.ticket = &lc->mw_ticket_count;
+        MP.ticket = lc ? &lc->mw_ticket_count : nullptr;
+        MP.ticket_sel = 0;
         kc8<<<cap_c8, threads, smem8, s>>>(MP);
         BQ_CK_LAUNCH();
         k_mw_scan<KT><<<POST_GRID / 8, 256, 0, s>>>(MP);
         BQ_CK_LAUNCH();
-        MP.ticket = &lc->mw_ticket_scatter;
+        MP.ticket = lc ? &lc->mw_ticket_scatter : nullptr;
+        MP.ticket_sel = 1;
         ks8<<<cap_s8, threads, smem8, s>>>(MP);
         BQ_CK_LAUNCH();
         return BQ_OK;
@@ -189,12 +191,14 @@ bq_status launch_multiway(MwParams<KT> MP, LevelCtrl *lc, cudaStream_t s, int wa
     if (st != BQ_OK) return st;
     st = persistent_cap(ks, threads, smem, cc_s, &cap_s);
     if (st != BQ_OK) return st;
-    MP.ticket = &lc->mw_ticket_count;
+    MP.ticket = lc ? &lc->mw_ticket_count : nullptr;
+    MP.ticket_sel = 0;
     kc<<<cap_c, threads, smem, s>>>(MP);
     BQ_CK_LAUNCH();
     k_mw_scan<KT><<<POST_GRID / 8, 256, 0, s>>>(MP);
     BQ_CK_LAUNCH();
-    MP.ticket = &lc->mw_ticket_scatter;
+    MP.ticket = lc ? &lc->mw_ticket_scatter : nullptr;
+    MP.ticket_sel = 1;
     ks<<<cap_s, threads, smem, s>>>(MP);
     BQ_CK_LAUNCH();
     return BQ_OK;
@@ -211,7 +215,7 @@ bq_status launch_partition(const PassParams<KT> &P, cudaStream_t s) {
 
 template <class KT>
 bq_status launch_leaves(int cls, const LeafParams<KT> &LP, uint32_t count, cudaStream_t s) {
-    if (count == 0 && LP.count_dev == nullptr) return BQ_OK;   // count 0 + count_dev: persistent grid
+    if (count == 0 && LP.count_dev == nullptr && LP.level == nullptr) return BQ_OK;   // count 0 + a device count: persistent grid
     BQ_CK(launch_leaf_class<KT>(cls, LP, count, s));
     return BQ_OK;
 }
@@ -546,38 +550,340 @@ bq_status run_partition_segments(const typename KT::T *src, typename KT::T *dst,
     return BQ_OK;
 }
 
-// Depth-capped segment: chunk leaf sorts + merge passes, result in the user buffer.
+// ---- the sort (a1-a9) -----------------------------------------------------------
+// Everything the launches of one sort need: workspace pointers, options, and
+// the parameter templates of the level-loop kernels (their level-dependent
+// fields are resolved on the device, LoopPtrs).
 template <class KT>
-bq_status run_fallback(const Leaf &f, typename KT::T *user, typename KT::T *scratch, Leaf *chunk_list,
-                       uint64_t n_total, cudaStream_t s) {
+struct SortPlan {
+    using T = typename KT::T;
+    Layout<KT> L;
+    size_t n;
+    T *user, *scratch;
+    LoopPtrs<KT> lp;
+    LoopMisc *misc;
+    LevelCtrl *ctrl, *root;
+    Leaf *leaves[2], *fallback, *copies[2];
+    uint32_t *tprefix;
+    FbState *fbst;
+    int rule, depth_limit, ordered, ways, aligned;
+    PostParams<KT> Q;     // k_post / k_fill / k_post_mw of a level (dynamic)
+    PassParams<KT> P;     // the binary partition of a level (dynamic)
+    MwParams<KT> MP;      // the multiway kernels of a level (dynamic)
+    LeafParams<KT> LP;    // leaf kernels (count_dev per class)
+};
+
+template <class KT>
+bq_status make_plan(SortPlan<KT> &pl, typename KT::T *data, size_t n, void *ws, int rule, int depth_limit, int ordered,
+                    int ways) {
     using T = typename KT::T;
     constexpr uint32_t S = Tune<KT>::LEAF;
-    T *bufs[2] = {user, scratch};
-    const uint32_t nch = (f.len + S - 1) / S;
-    k_chunk_leaves<<<(nch + 255) / 256, 256, 0, s>>>(chunk_list, f.begin, f.len, f.parity, S);
-    BQ_CK_LAUNCH();
-    LeafParams<KT> LP{};
-    LP.leaves = chunk_list;
-    LP.bufs[0] = user;
-    LP.bufs[1] = scratch;
-    LP.out = nullptr;
-    LP.out_other = 1;   // sorted chunks land in the other buffer
-    LP.n_total = n_total;
-    LP.aligned = aligned16(user) && aligned16(scratch);
-    bq_status st = launch_leaves<KT>(leaf_nclass<KT>() - 1, LP, nch, s);
-    if (st != BQ_OK) return st;
-    uint32_t cur = f.parity ^ 1;
-    for (uint64_t w = S; w < f.len; w *= 2) {
-        const uint64_t threads = (f.len + MERGE_IPT - 1) / MERGE_IPT;
-        const uint32_t grid = (uint32_t)((threads + MERGE_THREADS - 1) / MERGE_THREADS);
-        k_merge<KT, MERGE_THREADS, MERGE_IPT><<<grid, MERGE_THREADS, 0, s>>>(bufs[cur], bufs[cur ^ 1], f.begin,
-                                                                          f.len, (uint32_t)w);
-        BQ_CK_LAUNCH();
-        cur ^= 1;
+    pl.L = make_layout<KT>(n);
+    const Layout<KT> &L = pl.L;
+    char *w = static_cast<char *>(ws);
+    pl.n = n;
+    pl.user = data;
+    pl.scratch = reinterpret_cast<T *>(w + L.scratch);
+    pl.rule = rule;
+    pl.depth_limit = depth_limit;
+    pl.ordered = ordered;
+    pl.ways = ways;
+    pl.aligned = aligned16(pl.user) && aligned16(pl.scratch);
+    pl.ctrl = reinterpret_cast<LevelCtrl *>(w + L.ctrl);
+    pl.root = pl.ctrl + MAX_LEVELS;
+    pl.misc = reinterpret_cast<LoopMisc *>(w + L.misc);
+    pl.leaves[0] = reinterpret_cast<Leaf *>(w + L.leaves[0]);
+    pl.leaves[1] = reinterpret_cast<Leaf *>(w + L.leaves[1]);
+    pl.fallback = reinterpret_cast<Leaf *>(w + L.fallback);
+    pl.copies[0] = reinterpret_cast<Leaf *>(w + L.copies[0]);
+    pl.copies[1] = reinterpret_cast<Leaf *>(w + L.copies[1]);
+    pl.tprefix = reinterpret_cast<uint32_t *>(w + L.tprefix);
+    pl.fbst = reinterpret_cast<FbState *>(w + L.fbst);
+    LoopPtrs<KT> &lp = pl.lp;
+    lp.level = &pl.misc->level;
+    for (int p = 0; p < 2; p++) {
+        lp.segs[p] = reinterpret_cast<Seg *>(w + L.segs[p]);
+        lp.tile_map[p] = reinterpret_cast<uint32_t *>(w + L.tile_map[p]);
+        lp.cursor[p] = reinterpret_cast<unsigned long long *>(w + L.cursor[p]);
+        lp.ecursor[p] = reinterpret_cast<uint32_t *>(w + L.ecursor[p]);
+        lp.msegs[p] = w + L.msegs[p];
+        lp.mtile_map[p] = reinterpret_cast<uint32_t *>(w + L.mtile_map[p]);
+        lp.mhist[p] = reinterpret_cast<uint32_t *>(w + L.mhist[p]);
+        lp.mcursor[p] = reinterpret_cast<uint32_t *>(w + L.mcursor[p]);
     }
-    if (cur != 0)
-        BQ_CK(cudaMemcpyAsync(user + f.begin, scratch + f.begin, (size_t)f.len * sizeof(T),
-                              cudaMemcpyDeviceToDevice, s));
+    lp.ctrl = pl.ctrl;
+    lp.root = pl.root;
+    for (int p = 0; p < 2; p++) {
+        lp.leaves[p] = pl.leaves[p];
+        lp.leaf_counts[p] = pl.misc->leaf_counts[p];
+        lp.copies[p] = pl.copies[p];
+        lp.copy_count[p] = &pl.misc->copy_count[p];
+    }
+
+    // the binary partition pass of a level
+    PassParams<KT> &P = pl.P;
+    P = PassParams<KT>{};
+    P.bufs[0] = pl.user;
+    P.bufs[1] = pl.scratch;
+    P.stage[0] = pl.user;
+    P.stage[1] = pl.scratch;
+    P.final_buf = pl.user;
+    P.status = ordered ? reinterpret_cast<uint64_t *>(w + L.status) : nullptr;
+    P.ordered = ordered;
+    P.ntiles = 0xffffffffu;   // upper bound: the grid is the resident capacity
+    P.n_total = n;
+    P.aligned = pl.aligned;
+    P.lp = lp;
+    // the multiway kernels of a level
+    MwParams<KT> &MP = pl.MP;
+    MP = MwParams<KT>{};
+    MP.bufs[0] = pl.user;
+    MP.bufs[1] = pl.scratch;
+    MP.hstride = (uint32_t)L.max_segs;
+    MP.n_total = n;
+    MP.aligned = pl.aligned;
+    MP.lp = lp;
+    // bookkeeping of a level (children, bands, leaves, fallback)
+    PostParams<KT> &Q = pl.Q;
+    Q = PostParams<KT>{};
+    Q.pass = P;
+    Q.mw = MP;
+    Q.mhstride = (uint32_t)L.max_segs;
+    Q.status = P.status;
+    Q.copies = pl.copies[0];
+    Q.copy_count = &pl.misc->copy_count[0];
+    Q.copy_cap = (uint32_t)L.max_copies;
+    Q.leaves = pl.leaves[0];
+    Q.leaf_counts = pl.misc->leaf_counts[0];
+    Q.leaf_cap = (uint32_t)L.max_leaves;
+    Q.fallback = pl.fallback;
+    Q.fallback_count = &pl.misc->fb_count;
+    Q.leaf_max = S;
+    Q.depth_limit = depth_limit;
+    Q.pivot_rule = rule;
+    Q.ways = ways;
+    Q.emit_children = 1;
+    Q.band_inline_max = BAND_INLINE_MAX;
+    Q.overflow = &pl.misc->overflow;
+    // leaves
+    LeafParams<KT> &LP = pl.LP;
+    LP = LeafParams<KT>{};
+    LP.bufs[0] = pl.user;
+    LP.bufs[1] = pl.scratch;
+    LP.out = pl.user;
+    LP.n_total = n;
+    LP.aligned = pl.aligned;
+    LP.level = &pl.misc->level;
+    for (int p = 0; p < 2; p++) {
+        LP.lsets[p] = pl.leaves[p];
+        LP.csets[p] = pl.misc->leaf_counts[p];
+    }
+    return BQ_OK;
+}
+
+// root: zero the control blocks, [0, n) becomes the first segment (level 0)
+template <class KT>
+bq_status enqueue_prefix(const SortPlan<KT> &pl, cudaStream_t s) {
+    BQ_CK(cudaMemsetAsync(pl.ctrl, 0, (MAX_LEVELS + 1) * sizeof(LevelCtrl), s));
+    BQ_CK(cudaMemsetAsync(pl.misc, 0, sizeof(LoopMisc), s));
+    PostParams<KT> Q0 = pl.Q;
+    Q0.pass.lp.level = nullptr;
+    Q0.mw.lp.level = nullptr;
+    Q0.next_segs = pl.lp.segs[0];
+    Q0.next_tile_map = pl.lp.tile_map[0];
+    Q0.next_cursor = pl.lp.cursor[0];
+    Q0.next_ecursor = pl.lp.ecursor[0];
+    Q0.next_msegs = static_cast<MSeg<KT> *>(pl.lp.msegs[0]);
+    Q0.next_mtile_map = pl.lp.mtile_map[0];
+    Q0.next_mhist = pl.lp.mhist[0];
+    Q0.child_ctrl = pl.root;
+    k_init_root<KT, POST_THREADS><<<1, POST_THREADS, 0, s>>>(Q0, (uint32_t)pl.n);
+    BQ_CK_LAUNCH();
+    return BQ_OK;
+}
+
+// one level of the recursion (every array resolved on the device); `ev`
+// (optional) brackets the binary partition launch
+template <class KT>
+bq_status enqueue_level(const SortPlan<KT> &pl, cudaStream_t s, int use_cond, cudaGraphConditionalHandle h_loop,
+                        cudaGraphConditionalHandle h_fb, cudaEvent_t ev0, cudaEvent_t ev1) {
+    if constexpr (mw_capable<KT>()) if (pl.ways > 2) {
+        MwParams<KT> MP = pl.MP;
+        bq_status st = launch_multiway<KT>(MP, nullptr, s, pl.ways);
+        if (st != BQ_OK) return st;
+        k_post_mw<KT, POST_THREADS><<<POST_GRID, POST_THREADS, 0, s>>>(pl.Q);
+        BQ_CK_LAUNCH();
+    }
+    if (ev0) BQ_CK(cudaEventRecord(ev0, s));
+    bq_status st = launch_partition<KT>(pl.P, s);
+    if (st != BQ_OK) return st;
+    if (ev1) BQ_CK(cudaEventRecord(ev1, s));
+    k_post<KT, POST_LEVEL_THREADS><<<POST_LEVEL_GRID, POST_LEVEL_THREADS, 0, s>>>(pl.Q);
+    BQ_CK_LAUNCH();
+    return launch_fill<KT>(pl.Q, s);   // exits at once unless a band was too long for k_post
+}
+template <class KT>
+bq_status enqueue_level_end(const SortPlan<KT> &pl, cudaStream_t s, int use_cond, cudaGraphConditionalHandle h_loop,
+                            cudaGraphConditionalHandle h_fb) {
+    k_level_end<KT><<<1, 1, 0, s>>>(pl.lp, pl.misc, use_cond, h_loop, h_fb);
+    BQ_CK_LAUNCH();
+    return BQ_OK;
+}
+
+// sort the previous level's leaves (set (level + 1) & 1; one persistent
+// launch per class), copy its finished equal-record runs, empty the set
+template <class KT>
+bq_status enqueue_flush(const SortPlan<KT> &pl, cudaStream_t s) {
+    for (int c = 0; c < leaf_nclass<KT>(); c++) {
+        LeafParams<KT> LP = pl.LP;
+        LP.lcls = (size_t)c * pl.L.max_leaves;
+        LP.cls = c;
+        bq_status st = launch_leaves<KT>(c, LP, 0, s);
+        if (st != BQ_OK) return st;
+    }
+    if (KT::is_record && !pl.ordered) {
+        k_copy_runs<KT, POST_THREADS><<<POST_GRID, POST_THREADS, 0, s>>>(pl.lp, &pl.misc->level, pl.user, pl.scratch);
+        BQ_CK_LAUNCH();
+    }
+    k_flush_reset<<<1, 1, 0, s>>>(pl.misc);
+    BQ_CK_LAUNCH();
+    return BQ_OK;
+}
+
+constexpr uint32_t FB_GRID = 148 * 8;
+
+// a9 over every depth-capped segment; npass < 0: merge passes under a
+// conditional WHILE node (graph), else that many passes
+template <class KT>
+bq_status enqueue_fb_setup(const SortPlan<KT> &pl, cudaStream_t s, int use_cond, cudaGraphConditionalHandle h) {
+    Leaf *chunks = pl.leaves[0];   // set 0, class 0: free after the last flush
+    k_fb_setup<<<1, 1024, 0, s>>>(pl.fallback, &pl.misc->fb_count, chunks, pl.tprefix, pl.fbst, Tune<KT>::LEAF, use_cond,
+                                  h);
+    BQ_CK_LAUNCH();
+    LeafParams<KT> LP = pl.LP;
+    LP.level = nullptr;
+    LP.leaves = chunks;
+    LP.count_dev = &pl.fbst->nchunk;
+    LP.out_other = 1;   // sorted chunks land in the other buffer
+    return launch_leaves<KT>(leaf_nclass<KT>() - 1, LP, 0, s);
+}
+template <class KT>
+bq_status enqueue_fb_pass(const SortPlan<KT> &pl, cudaStream_t s, int use_cond, cudaGraphConditionalHandle h) {
+    k_fb_merge<KT><<<FB_GRID, MERGE_THREADS, 0, s>>>(pl.fallback, pl.tprefix, pl.fbst, pl.user, pl.scratch);
+    BQ_CK_LAUNCH();
+    k_fb_next<<<1, 1, 0, s>>>(pl.fbst, use_cond, h);
+    BQ_CK_LAUNCH();
+    return BQ_OK;
+}
+template <class KT>
+bq_status enqueue_fb_finish(const SortPlan<KT> &pl, cudaStream_t s) {
+    k_fb_finish<KT><<<FB_GRID, MERGE_THREADS, 0, s>>>(pl.fallback, pl.tprefix, pl.fbst, pl.user, pl.scratch);
+    BQ_CK_LAUNCH();
+    return BQ_OK;
+}
+
+// ---- the graph of a sort, cached per (device, kind, buffers, n, options) --------
+struct GraphKey {
+    int dev, kind, rule, depth_limit, ordered, ways;
+    const void *data, *ws;
+    size_t n, ws_bytes;
+    bool operator==(const GraphKey &o) const {
+        return dev == o.dev && kind == o.kind && rule == o.rule && depth_limit == o.depth_limit &&
+               ordered == o.ordered && ways == o.ways && data == o.data && ws == o.ws && n == o.n &&
+               ws_bytes == o.ws_bytes;
+    }
+};
+bool graph_cache_get(const GraphKey &k, cudaGraphExec_t *ex);
+void graph_cache_put(const GraphKey &k, cudaGraphExec_t ex);
+
+// a conditional node at the capture point of stream s; returns its body graph
+inline cudaError_t add_cond_node(cudaStream_t s, cudaGraphConditionalHandle h, cudaGraphConditionalNodeType type,
+                                 cudaGraph_t *body) {
+    cudaStreamCaptureStatus cs;
+    cudaGraph_t g;
+    const cudaGraphNode_t *deps = nullptr;
+    size_t nd = 0;
+    cudaError_t e = cudaStreamGetCaptureInfo(s, &cs, nullptr, &g, &deps, &nd);
+    if (e != cudaSuccess) return e;
+    cudaGraphNodeParams p = {};
+    p.type = cudaGraphNodeTypeConditional;
+    p.conditional.handle = h;
+    p.conditional.type = type;
+    p.conditional.size = 1;
+    cudaGraphNode_t node;
+    if ((e = cudaGraphAddNode(&node, g, deps, nd, &p)) != cudaSuccess) return e;
+    *body = p.conditional.phGraph_out[0];
+    return cudaStreamUpdateCaptureDependencies(s, &node, 1, cudaStreamSetCaptureDependencies);
+}
+
+// Builds the graph: prefix; WHILE(the last level had children) { fork: [sort
+// the previous batch's leaves] || [partition LOOP_BATCH levels]; join };
+// sort the last level's leaves; IF(capped segments) { setup; chunk leaves;
+// WHILE(passes) merge; finish }.  Captured on private streams, instantiated once.
+template <class KT>
+bq_status build_sort_graph(const SortPlan<KT> &pl, cudaGraphExec_t *ex) {
+    cudaStream_t cs[5] = {};
+    cudaEvent_t ev[2] = {};
+    cudaGraph_t g = nullptr;
+    auto fail = [&](bq_status e) {
+        for (auto &x : cs) if (x) cudaStreamDestroy(x);
+        for (auto &x : ev) if (x) cudaEventDestroy(x);
+        if (g) cudaGraphDestroy(g);
+        return e;
+    };
+#define BQ_GK(call)                                                                                     \
+    do {                                                                                                \
+        cudaError_t e_ = (call);                                                                        \
+        if (e_ != cudaSuccess)                                                                          \
+            return fail(set_error(BQ_ERR_CUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, \
+                                  __LINE__));                                                           \
+    } while (0)
+#define BQ_GS(call)                       \
+    do {                                  \
+        bq_status s_ = (call);            \
+        if (s_ != BQ_OK) return fail(s_); \
+    } while (0)
+    for (auto &x : cs) BQ_GK(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
+    for (auto &x : ev) BQ_GK(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+    BQ_GK(cudaGraphCreate(&g, 0));
+    cudaGraphConditionalHandle h_loop, h_fbany;
+    BQ_GK(cudaGraphConditionalHandleCreate(&h_loop, g, 1, cudaGraphCondAssignDefault));
+    BQ_GK(cudaGraphConditionalHandleCreate(&h_fbany, g, 0, cudaGraphCondAssignDefault));
+    BQ_GK(cudaStreamBeginCaptureToGraph(cs[0], g, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+    BQ_GS(enqueue_prefix<KT>(pl, cs[0]));
+    // the level loop
+    cudaGraph_t body, fbbody, pbody, tmp;
+    BQ_GK(add_cond_node(cs[0], h_loop, cudaGraphCondTypeWhile, &body));
+    BQ_GK(cudaStreamBeginCaptureToGraph(cs[1], body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+    BQ_GK(cudaEventRecord(ev[0], cs[1]));
+    BQ_GK(cudaStreamWaitEvent(cs[2], ev[0], 0));          // fork
+    BQ_GS(enqueue_flush<KT>(pl, cs[2]));                    // the previous batch's leaves
+    for (uint32_t k = 0; k < LOOP_BATCH; k++) {
+        BQ_GS(enqueue_level<KT>(pl, cs[1], 1, h_loop, h_fbany, nullptr, nullptr));
+        if (k + 1 < LOOP_BATCH) BQ_GS(enqueue_level_end<KT>(pl, cs[1], 1, h_loop, h_fbany));
+    }
+    BQ_GK(cudaEventRecord(ev[1], cs[2]));
+    BQ_GK(cudaStreamWaitEvent(cs[1], ev[1], 0));          // join
+    BQ_GS(enqueue_level_end<KT>(pl, cs[1], 1, h_loop, h_fbany));
+    BQ_GK(cudaStreamEndCapture(cs[1], &tmp));
+    BQ_GS(enqueue_flush<KT>(pl, cs[0]));                    // the last level's leaves
+    // the depth-capped segments (a9)
+    BQ_GK(add_cond_node(cs[0], h_fbany, cudaGraphCondTypeIf, &fbbody));
+    BQ_GK(cudaStreamBeginCaptureToGraph(cs[3], fbbody, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+    cudaGraphConditionalHandle h_pass;
+    BQ_GK(cudaGraphConditionalHandleCreate(&h_pass, fbbody, 0, cudaGraphCondAssignDefault));
+    BQ_GS(enqueue_fb_setup<KT>(pl, cs[3], 1, h_pass));
+    BQ_GK(add_cond_node(cs[3], h_pass, cudaGraphCondTypeWhile, &pbody));
+    BQ_GK(cudaStreamBeginCaptureToGraph(cs[4], pbody, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+    BQ_GS(enqueue_fb_pass<KT>(pl, cs[4], 1, h_pass));
+    BQ_GK(cudaStreamEndCapture(cs[4], &tmp));
+    BQ_GS(enqueue_fb_finish<KT>(pl, cs[3]));
+    BQ_GK(cudaStreamEndCapture(cs[3], &tmp));
+    BQ_GK(cudaStreamEndCapture(cs[0], &g));
+    BQ_GK(cudaGraphInstantiate(ex, g, 0));
+    fail(BQ_OK);
+#undef BQ_GK
+#undef BQ_GS
     return BQ_OK;
 }
 
@@ -585,7 +891,6 @@ template <class KT>
 bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, bq_sort_stats *stats, void *ws,
                    size_t ws_bytes, cudaStream_t s) {
     using T = typename KT::T;
-    constexpr uint32_t TILE = tile_elems<KT>();
     constexpr uint32_t S = Tune<KT>::LEAF;
     constexpr int NCLS = leaf_nclass<KT>();
     bq_sort_stats local;
@@ -601,7 +906,7 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
             return set_error(BQ_ERR_INVALID_ARGUMENT, "ways %d not in {0, 2, %d, %d}", ways, MW8, MW_K);
         if (rule != BQ_PIVOT_MO3 && rule != BQ_PIVOT_NINTHER && rule != BQ_PIVOT_SAMPLE64)
             return set_error(BQ_ERR_INVALID_ARGUMENT, "bad pivot rule %d", rule);
-        if (depth_limit >= MAX_LEVELS - 2)
+        if (depth_limit >= MAX_LEVELS - (int)LOOP_BATCH - 2)
             return set_error(BQ_ERR_INVALID_ARGUMENT, "depth_limit %d too large", depth_limit);
     }
     bq_status st = validate<KT>(data, n, ws, ws_bytes);
@@ -612,11 +917,9 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
     }
     // default: binary passes for int32 keys (the binary pass is already near
     // the HBM roofline and the cheapest in ALU work per key), 8-way passes
-    // (N4) for 64-bit keys, whose binary passes leave ALU headroom (c3:
-    // 11.2 -> 10.4 ms random, 12.9 -> 10.3 ms sorted); records stay binary
+    // (N4) for 64-bit keys and key+index pairs; 32-byte records stay binary
     // (int32: also multiway where a sort is only a few levels and each
-    // level's fixed costs matter: 8-way for 2^17 < n <= 2^23, 16-way up to
-    // 2^24 — c1 0.48 -> 0.39 ms, 2^24 0.99 -> 0.90 ms; profiles/r01/ways_sweep.jsonl)
+    // level's fixed costs matter: 8-way for 2^17 < n <= 2^23, 16-way up to 2^24)
     if (ways == 0) {
         if (sizeof(typename KT::K) == 8 && mw_capable<KT>()) ways = MW8;
         else if (!KT::is_record && n > (1u << 17) && n <= (1u << 23)) ways = MW8;
@@ -630,286 +933,159 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
         depth_limit = 2 * lg + 3;   // P:295, P:1224 (2*ilogb(n)+3)
     }
 
-    const Layout<KT> L = make_layout<KT>(n);
-    char *w = static_cast<char *>(ws);
-    T *user = data;
-    T *scratch = reinterpret_cast<T *>(w + L.scratch);
-    uint64_t *status = reinterpret_cast<uint64_t *>(w + L.status);
-    uint32_t *tile_map[2];
-    Seg *segs[2];
-    unsigned long long *cursor[2];
-    uint32_t *ecursor[2];
-    MSeg<KT> *msegs[2];
-    uint32_t *mtile_map[2], *mhist[2], *mcursor[2];
-    for (int p = 0; p < 2; p++) {
-        tile_map[p] = reinterpret_cast<uint32_t *>(w + L.tile_map[p]);
-        segs[p] = reinterpret_cast<Seg *>(w + L.segs[p]);
-        cursor[p] = reinterpret_cast<unsigned long long *>(w + L.cursor[p]);
-        ecursor[p] = reinterpret_cast<uint32_t *>(w + L.ecursor[p]);
-        msegs[p] = reinterpret_cast<MSeg<KT> *>(w + L.msegs[p]);
-        mtile_map[p] = reinterpret_cast<uint32_t *>(w + L.mtile_map[p]);
-        mhist[p] = reinterpret_cast<uint32_t *>(w + L.mhist[p]);
-        mcursor[p] = reinterpret_cast<uint32_t *>(w + L.mcursor[p]);
-    }
-    // look-back words are only used by the ordered placement
-    uint64_t *lb_status = ordered ? status : nullptr;
-    Leaf *leaves[2] = {reinterpret_cast<Leaf *>(w + L.leaves[0]), reinterpret_cast<Leaf *>(w + L.leaves[1])};
-    Leaf *fallback = reinterpret_cast<Leaf *>(w + L.fallback);
-    LevelCtrl *ctrl = reinterpret_cast<LevelCtrl *>(w + L.ctrl);
-    LevelCtrl *root = ctrl + MAX_LEVELS;
-    uint32_t *fb_count = reinterpret_cast<uint32_t *>(w + L.misc);
-    // misc words: [0] fallback count, [4, 12) / [12, 20) leaf counts of set 0 / 1
-    // (by class), [20, 22) copy counts, [24] leaf-list overflow flag
-    uint32_t *leaf_counts[2] = {fb_count + 4, fb_count + 12};   // [set][class]
-    uint32_t *copy_counts[2] = {fb_count + 20, fb_count + 21};
-    Leaf *copies[2] = {reinterpret_cast<Leaf *>(w + L.copies[0]), reinterpret_cast<Leaf *>(w + L.copies[1])};
-    uint32_t *overflow = fb_count + 24;
+    SortPlan<KT> pl;
+    st = make_plan<KT>(pl, data, n, ws, rule, depth_limit, ordered, ways);
+    if (st != BQ_OK) return st;
 
-    LeafParams<KT> LP{};
-    LP.bufs[0] = user;
-    LP.bufs[1] = scratch;
-    LP.out = user;
-    LP.out_other = 0;
-    LP.n_total = n;
-    LP.aligned = aligned16(user) && aligned16(scratch);
-
-    if (n <= S) {
-        k_single_leaf<<<1, 1, 0, s>>>(leaves[0], (uint32_t)n);
+    if (n <= S) {   // one leaf
+        k_single_leaf<<<1, 1, 0, s>>>(pl.leaves[0], (uint32_t)n);
         BQ_CK_LAUNCH();
-        local.kernel_launches++;
-        LP.leaves = leaves[0];
+        LeafParams<KT> LP = pl.LP;
+        LP.level = nullptr;
+        LP.leaves = pl.leaves[0];
         st = launch_leaves<KT>((int)leaf_class<KT>((uint32_t)n), LP, 1, s);
         if (st != BQ_OK) return st;
-        local.kernel_launches++;
+        local.kernel_launches = 2;
         local.leaves = 1;
         if (stats) *stats = local;
         return BQ_OK;
     }
 
-    // Leaves are sorted on a side stream, concurrently with the deeper
-    // partition levels: a batch's leaf lists (set batch & 1) are consumed
-    // there while the main stream partitions the next batch into the other set.
-    cudaStream_t side = nullptr;
-    cudaEvent_t ev_levels[2] = {nullptr, nullptr}, ev_leaves[2] = {nullptr, nullptr};
-    std::vector<cudaEvent_t> evs;
-    std::vector<LevelCtrl> hvec(MAX_LEVELS + 1);   // host copy of the control blocks
-    LevelCtrl *hctrl = hvec.data();
+    // host-driven loop: with per-launch timing (CUDA events between the
+    // launches of a level), or BQ_HOST_LOOP=1 (diagnostics)
+    static const bool host_env = [] {
+        const char *e = std::getenv("BQ_HOST_LOOP");
+        return e && e[0] == '1';
+    }();
+    const bool host_loop = timing || host_env;
+    std::vector<cudaEvent_t> evs;   // timing: one pair per level
+    cudaStream_t side = nullptr;    // host-driven loop: the leaves' stream
+    cudaEvent_t efork = nullptr, ejoin = nullptr;
     auto cleanup = [&]() {
         for (auto e : evs) cudaEventDestroy(e);
-        for (int i = 0; i < 2; i++) {
-            if (ev_levels[i]) cudaEventDestroy(ev_levels[i]);
-            if (ev_leaves[i]) cudaEventDestroy(ev_leaves[i]);
-        }
         if (side) cudaStreamDestroy(side);
+        if (efork) cudaEventDestroy(efork);
+        if (ejoin) cudaEventDestroy(ejoin);
     };
-#define BQ_CKC(call)                \
-    do {                            \
+#define BQ_CKC(call)                                                         \
+    do {                                                                     \
         bq_status st_ = [&]() -> bq_status { BQ_CK(call); return BQ_OK; }(); \
+        if (st_ != BQ_OK) { cleanup(); return st_; }                          \
+    } while (0)
+#define BQ_SKC(call)                                 \
+    do {                                             \
+        bq_status st_ = (call);                      \
         if (st_ != BQ_OK) { cleanup(); return st_; } \
     } while (0)
-    BQ_CKC(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
-    for (int i = 0; i < 2; i++) {
-        BQ_CKC(cudaEventCreateWithFlags(&ev_levels[i], cudaEventDisableTiming));
-        BQ_CKC(cudaEventCreateWithFlags(&ev_leaves[i], cudaEventDisableTiming));
-    }
 
-    BQ_CKC(cudaMemsetAsync(ctrl, 0, (MAX_LEVELS + 1) * sizeof(LevelCtrl), s));
-    BQ_CKC(cudaMemsetAsync(fb_count, 0, 25 * sizeof(uint32_t), s));
-    const int aligned = aligned16(user) && aligned16(scratch);
-    // children sink of level `lv` (its children form level lv+1; the root is
-    // the only "child" of the virtual level -1, counted in `root`)
-    auto sink = [&](int lv, int set) {
-        PostParams<KT> Q{};
-        const int np = (lv + 1) & 1;
-        Q.pass.bufs[0] = user;
-        Q.pass.bufs[1] = scratch;
-        Q.pass.ordered = ordered;
-        Q.copies = copies[set];
-        Q.copy_count = copy_counts[set];
-        Q.next_segs = segs[np];
-        Q.next_tile_map = tile_map[np];
-        Q.next_cursor = cursor[np];
-        Q.next_ecursor = ecursor[np];
-        Q.status = lb_status;
-        Q.next_msegs = msegs[np];
-        Q.next_mtile_map = mtile_map[np];
-        Q.next_mhist = mhist[np];
-        Q.mhstride = (uint32_t)L.max_segs;
-        Q.child_ctrl = lv < 0 ? root : ctrl + lv;
-        Q.leaves = leaves[set];
-        Q.leaf_counts = leaf_counts[set];
-        Q.leaf_cap = (uint32_t)L.max_leaves;
-        Q.fallback = fallback;
-        Q.fallback_count = fb_count;
-        Q.leaf_max = S;
-        Q.depth_limit = depth_limit;
-        Q.pivot_rule = rule;
-        Q.ways = ways;
-        Q.emit_children = 1;
-        Q.band_inline_max = BAND_INLINE_MAX;
-        Q.overflow = overflow;
-        return Q;
-    };
-    {
-        PostParams<KT> Q0 = sink(-1, 0);
-        k_init_root<KT, POST_THREADS><<<1, POST_THREADS, 0, s>>>(Q0, (uint32_t)n);
-        BQ_CKC(cudaGetLastError());
-        local.kernel_launches++;
-    }
-
-    int level = 0;
-    bool done = false;
-    for (int batch = 0; !done; batch++) {
-        const int set = batch & 1;
-        if (level + LEVEL_BATCH >= MAX_LEVELS) {
-            cleanup();
-            return set_error(BQ_ERR_CUDA, "level loop did not terminate");
+    int host_levels = 0;
+    if (!host_loop) {
+        int dev = 0;
+        BQ_CK(cudaGetDevice(&dev));
+        const GraphKey key{dev, (int)KT::kind, rule, depth_limit, ordered, ways, data, ws, n, ws_bytes};
+        cudaGraphExec_t ex = nullptr;
+        if (!graph_cache_get(key, &ex)) {
+            st = build_sort_graph<KT>(pl, &ex);
+            if (st != BQ_OK) return st;
+            graph_cache_put(key, ex);
         }
-        // the side stream has finished the leaves of batch-2 (same set)
-        if (batch >= 2) BQ_CKC(cudaStreamWaitEvent(s, ev_leaves[set], 0));
-        BQ_CKC(cudaMemsetAsync(leaf_counts[set], 0, MAX_LEAF_CLASSES * sizeof(uint32_t), s));
-        BQ_CKC(cudaMemsetAsync(copy_counts[set], 0, sizeof(uint32_t), s));
-        for (int k = 0; k < LEVEL_BATCH; k++, level++) {
-            const int cp = level & 1;
-            const LevelCtrl *prev = level == 0 ? root : ctrl + level - 1;
-            PostParams<KT> Q = sink(level, set);
+        BQ_CK(cudaGraphLaunch(ex, s));
+    } else {
+        // the graph's structure with two streams: the previous level's leaves
+        // on `side` while `s` partitions the level
+        BQ_CKC(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+        BQ_CKC(cudaEventCreateWithFlags(&efork, cudaEventDisableTiming));
+        BQ_CKC(cudaEventCreateWithFlags(&ejoin, cudaEventDisableTiming));
+        BQ_SKC(enqueue_prefix<KT>(pl, s));
+        std::vector<LevelCtrl> hc(1);
+        for (int level = 0;; level++) {
+            if (level + (int)LOOP_BATCH + 1 >= MAX_LEVELS) {
+                cleanup();
+                return set_error(BQ_ERR_CUDA, "level loop did not terminate");
+            }
+            cudaEvent_t e0 = nullptr, e1 = nullptr;
             if (timing) {
-                cudaEvent_t e0, e1;
                 BQ_CKC(cudaEventCreate(&e0));
                 evs.push_back(e0);
                 BQ_CKC(cudaEventCreate(&e1));
                 evs.push_back(e1);
-                BQ_CKC(cudaEventRecord(e0, s));
             }
-            if constexpr (mw_capable<KT>()) if (ways > 2) {
-                // the level's multiway segments: count, scan, scatter, children
-                MwParams<KT> MP{};
-                MP.bufs[0] = user;
-                MP.bufs[1] = scratch;
-                MP.msegs = msegs[cp];
-                MP.tile_map = mtile_map[cp];
-                MP.hist = mhist[cp];
-                MP.cursor = mcursor[cp];
-                MP.hstride = (uint32_t)L.max_segs;
-                MP.nseg_dev = &prev->nmseg_next;
-                MP.ntiles_dev = &prev->nmtiles_next;
-                MP.n_total = n;
-                MP.aligned = aligned;
-                MP.ctrl = ctrl + level;
-                st = launch_multiway<KT>(MP, ctrl + level, s, ways);
-                if (st != BQ_OK) { cleanup(); return st; }
-                local.kernel_launches += 3;
-                Q.mw = MP;
-                k_post_mw<KT, POST_THREADS><<<POST_GRID, POST_THREADS, 0, s>>>(Q);
-                BQ_CKC(cudaGetLastError());
-                local.kernel_launches++;
+            if (level % LOOP_BATCH == 0) {   // fork
+                BQ_CKC(cudaEventRecord(efork, s));
+                BQ_CKC(cudaStreamWaitEvent(side, efork, 0));
+                BQ_SKC(enqueue_flush<KT>(pl, side));
+                BQ_CKC(cudaEventRecord(ejoin, side));
             }
-            // the level's binary segments
-            PassParams<KT> P{};
-            P.bufs[0] = user;
-            P.bufs[1] = scratch;
-            P.stage[0] = user;
-            P.stage[1] = scratch;
-            P.final_buf = user;
-            P.segs = segs[cp];
-            P.tile_map = tile_map[cp];
-            P.status = lb_status;
-            P.cursor = cursor[cp];
-            P.ecursor = ecursor[cp];
-            P.ordered = ordered;
-            P.ctrl = ctrl + level;
-            P.ntiles = 0xffffffffu;             // upper bound: the grid is the resident capacity
-            P.ntiles_dev = &prev->ntiles_next;
-            P.n_total = n;
-            P.aligned = aligned;
-            st = launch_partition<KT>(P, s);
-            if (st != BQ_OK) { cleanup(); return st; }
-            local.kernel_launches++;
-            if (timing) BQ_CKC(cudaEventRecord(evs.back(), s));
-
-            Q.pass = P;
-            Q.d_counts = nullptr;
-            Q.nseg_dev = &prev->nseg_next;
-            k_post<KT, POST_LEVEL_THREADS><<<POST_LEVEL_GRID, POST_LEVEL_THREADS, 0, s>>>(Q);
-            BQ_CKC(cudaGetLastError());
-            local.kernel_launches++;
-            st = launch_fill<KT>(Q, s);   // exits at once unless a band was too long for k_post
-            if (st != BQ_OK) { cleanup(); return st; }
-            local.kernel_launches += KT::is_record ? 2 : 1;
+            BQ_SKC(enqueue_level<KT>(pl, s, 0, 0, 0, e0, e1));
+            if (level % LOOP_BATCH == LOOP_BATCH - 1) BQ_CKC(cudaStreamWaitEvent(s, ejoin, 0));   // join
+            BQ_SKC(enqueue_level_end<KT>(pl, s, 0, 0, 0));
+            host_levels = level + 1;
+            if ((level + 1) % LOOP_BATCH == 0) {
+                BQ_CKC(cudaMemcpyAsync(hc.data(), pl.ctrl + level, sizeof(LevelCtrl), cudaMemcpyDeviceToHost, s));
+                BQ_CKC(cudaStreamSynchronize(s));
+                if (hc[0].nseg_next + hc[0].nmseg_next == 0) break;
+            }
         }
-        // leaves of this batch on the side stream
-#ifndef BQ_LEAF_MAIN
-        cudaStream_t ls = side;
-#else
-        cudaStream_t ls = s;
-#endif
-        BQ_CKC(cudaEventRecord(ev_levels[set], s));
-        BQ_CKC(cudaStreamWaitEvent(ls, ev_levels[set], 0));
-        for (int c = 0; c < NCLS; c++) {
-            LP.leaves = leaves[set] + (size_t)c * L.max_leaves;
-            LP.count_dev = leaf_counts[set] + c;
-            st = launch_leaves<KT>(c, LP, 0, ls);
-            if (st != BQ_OK) { cleanup(); return st; }
-            local.kernel_launches++;
-        }
-        if (KT::is_record && !ordered) {
-            k_copy_runs<KT, POST_THREADS><<<POST_GRID, POST_THREADS, 0, ls>>>(copies[set], copy_counts[set], user,
-                                                                               scratch);
-            BQ_CKC(cudaGetLastError());
-            local.kernel_launches++;
-        }
-        BQ_CKC(cudaEventRecord(ev_leaves[set], ls));
-        // is there a next level?
-        BQ_CKC(cudaMemcpyAsync(hctrl + level - 1, ctrl + level - 1, sizeof(LevelCtrl), cudaMemcpyDeviceToHost, s));
+        BQ_SKC(enqueue_flush<KT>(pl, s));   // (the loop always ends on a batch boundary)
+        // a9: the depth-capped segments
+        LoopMisc hm;
+        BQ_CKC(cudaMemcpyAsync(&hm, pl.misc, sizeof hm, cudaMemcpyDeviceToHost, s));
         BQ_CKC(cudaStreamSynchronize(s));
-        done = hctrl[level - 1].nseg_next == 0 && hctrl[level - 1].nmseg_next == 0;
-    }
-    LP.count_dev = nullptr;
-    BQ_CKC(cudaStreamWaitEvent(s, ev_leaves[0], 0));
-    BQ_CKC(cudaStreamWaitEvent(s, ev_leaves[1], 0));
-
-    // statistics of every level, and the depth-capped segments
-    BQ_CKC(cudaMemcpyAsync(hctrl, ctrl, level * sizeof(LevelCtrl), cudaMemcpyDeviceToHost, s));
-    uint32_t misc_h[25];
-    BQ_CKC(cudaMemcpyAsync(misc_h, fb_count, sizeof misc_h, cudaMemcpyDeviceToHost, s));
-    BQ_CKC(cudaStreamSynchronize(s));
-    const uint32_t nfb_total = misc_h[0];
-    if (misc_h[24]) { cleanup(); return set_error(BQ_ERR_CUDA, "leaf list overflow"); }
-    for (int l = 0; l < level; l++) {
-        const LevelCtrl &hc = hctrl[l];
-        const uint32_t nseg_l = l == 0 ? 1u : hctrl[l - 1].nseg_next + hctrl[l - 1].nmseg_next;
-        if (nseg_l == 0) break;
-        local.levels++;
-        local.partition_launches++;
-        local.partitioned_segments += nseg_l;
-        local.element_passes += hc.element_passes;
-        local.band_elements += hc.band_elems;
-        local.leaves += hc.nleaf;
-    }
-    local.fallback_segments = nfb_total;
-
-    if (nfb_total) {
-        std::vector<Leaf> fl(nfb_total);
-        BQ_CKC(cudaMemcpyAsync(fl.data(), fallback, nfb_total * sizeof(Leaf), cudaMemcpyDeviceToHost, s));
-        BQ_CKC(cudaStreamSynchronize(s));
-        for (const Leaf &f : fl) {
-            st = run_fallback<KT>(f, user, scratch, leaves[0], n, s);
-            if (st != BQ_OK) { cleanup(); return st; }
+        if (hm.fb_count) {
+            BQ_SKC(enqueue_fb_setup<KT>(pl, s, 0, 0));
+            FbState hf;
+            BQ_CKC(cudaMemcpyAsync(&hf, pl.fbst, sizeof hf, cudaMemcpyDeviceToHost, s));
+            BQ_CKC(cudaStreamSynchronize(s));
+            for (uint32_t p = 0; p < hf.npass; p++) BQ_SKC(enqueue_fb_pass<KT>(pl, s, 0, 0));
+            BQ_SKC(enqueue_fb_finish<KT>(pl, s));
         }
     }
-    local.partition_bytes = 2.0 * (double)sizeof(T) * (double)local.element_passes;
-    if (timing) {
+
+    // statistics (and the overflow check) need the device counters: only with
+    // stats != NULL or per-launch timing does the call wait for the stream
+    if (stats || timing) {
+        LoopMisc hm;
+        BQ_CKC(cudaMemcpyAsync(&hm, pl.misc, sizeof hm, cudaMemcpyDeviceToHost, s));
         BQ_CKC(cudaStreamSynchronize(s));
-        double ms = 0;
-        // only the launches of non-empty levels count
-        for (size_t i = 0; i + 1 < evs.size() && (int)(i / 2) < (int)local.levels; i += 2) {
-            float f = 0;
-            BQ_CKC(cudaEventElapsedTime(&f, evs[i], evs[i + 1]));
-            ms += f;
+        const int levels = (int)hm.level;
+        std::vector<LevelCtrl> hctrl(levels > 0 ? levels : 1);
+        if (levels > 0) BQ_CKC(cudaMemcpyAsync(hctrl.data(), pl.ctrl, levels * sizeof(LevelCtrl), cudaMemcpyDeviceToHost, s));
+        LevelCtrl hroot;
+        BQ_CKC(cudaMemcpyAsync(&hroot, pl.root, sizeof hroot, cudaMemcpyDeviceToHost, s));
+        BQ_CKC(cudaStreamSynchronize(s));
+        if (hm.overflow) {
+            cleanup();
+            return set_error(BQ_ERR_CUDA, "leaf list overflow");
         }
-        local.partition_ms = ms;
+        const int per_level = 4 + (KT::is_record ? 1 : 0) + (ways > 2 ? 4 : 0);
+        local.kernel_launches = 1 + levels * per_level + hm.nflush * (NCLS + 1 + (KT::is_record && !ordered ? 1 : 0)) +
+                                (hm.fb_count ? 4 : 0);
+        for (int l = 0; l < levels; l++) {
+            const LevelCtrl &h = hctrl[l];
+            const uint32_t nseg_l = l == 0 ? hroot.nseg_next + hroot.nmseg_next : hctrl[l - 1].nseg_next + hctrl[l - 1].nmseg_next;
+            if (nseg_l == 0) break;
+            local.levels++;
+            local.partition_launches++;
+            local.partitioned_segments += nseg_l;
+            local.element_passes += h.element_passes;
+            local.band_elements += h.band_elems;
+            local.leaves += h.nleaf;
+        }
+        local.leaves += hroot.nleaf;
+        local.fallback_segments = hm.fb_count;
+        local.partition_bytes = 2.0 * (double)sizeof(T) * (double)local.element_passes;
+        if (timing) {
+            double ms = 0;
+            for (size_t i = 0; i + 1 < evs.size() && (int)(i / 2) < (int)local.levels; i += 2) {
+                float f = 0;
+                BQ_CKC(cudaEventElapsedTime(&f, evs[i], evs[i + 1]));
+                ms += f;
+            }
+            local.partition_ms = ms;
+        }
     }
 #undef BQ_CKC
+#undef BQ_SKC
     cleanup();
     if (stats) *stats = local;
     return BQ_OK;

@@ -32,6 +32,8 @@
 // loads and stores of steps 2 and 3 are free of bank conflicts.
 #pragma once
 
+#include <utility>
+
 #include "common.cuh"
 
 namespace bq {
@@ -46,6 +48,13 @@ struct LeafParams {
     int out_other;     // 1: write into bufs[parity ^ 1] instead (fallback chunk sort)
     uint64_t n_total;  // length of each data buffer (bounds the TMA reads)
     int aligned;       // both data buffers (and out) 16-byte aligned -> TMA bulk copies
+    // level loop: non-null -> the leaves of the previous batch of levels, list
+    // lsets[loop_prev_set(*level)] (+ class offset lcls), count csets[..] + cls
+    const uint32_t *level;
+    const Leaf *lsets[2];
+    const uint32_t *csets[2];
+    size_t lcls;
+    int cls;
 };
 
 // ---- register element types -------------------------------------------------
@@ -135,18 +144,14 @@ template <int N>
 struct OemConst {
     static constexpr OemNet net = oem_make(N);
 };
-template <class E, int N, int I>
-__device__ __forceinline__ void oem_apply(E (&x)[N]) {
-    if constexpr (I < OemConst<N>::net.n) {
-        constexpr int lo = OemConst<N>::net.lo[I], hi = OemConst<N>::net.hi[I];
-        ce(x[lo], x[hi]);
-        oem_apply<E, N, I + 1>(x);
-    }
+template <class E, int N, size_t... I>
+__device__ __forceinline__ void oem_apply(E (&x)[N], std::index_sequence<I...>) {
+    (ce(x[OemConst<N>::net.lo[I]], x[OemConst<N>::net.hi[I]]), ...);
 }
 template <class E, int N>
 __device__ __forceinline__ void oem_sort(E (&x)[N]) {
     static_assert(N <= 64, "per-thread network size");
-    oem_apply<E, N, 0>(x);
+    oem_apply<E, N>(x, std::make_index_sequence<(size_t)OemConst<N>::net.n>{});
 }
 
 // ---- shared-memory planes ----------------------------------------------------
@@ -448,7 +453,7 @@ __device__ __forceinline__ void leaf_body(const LeafParams<KT> &P, const Leaf lf
 
 template <class KT, int NT>
 __global__ void __launch_bounds__(NT, (LeafTraits<KT>::NTMAX / NT) > 0 ? LeafTraits<KT>::NTMAX / NT : 1)
-    k_leaf(LeafParams<KT> P) {
+    k_leaf(const LeafParams<KT> Pin) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t *bar = reinterpret_cast<uint64_t *>(smem_raw);
     if (threadIdx.x == 0) {
@@ -457,6 +462,17 @@ __global__ void __launch_bounds__(NT, (LeafTraits<KT>::NTMAX / NT) > 0 ? LeafTra
     }
     __syncthreads();
     uint32_t phase = 0;
+    __shared__ LeafParams<KT> sP;
+    if (threadIdx.x == 0) {
+        sP = Pin;
+        if (sP.level) {
+            const uint32_t set = loop_prev_set(*sP.level);
+            sP.leaves = sP.lsets[set] + sP.lcls;
+            sP.count_dev = sP.csets[set] + sP.cls;
+        }
+    }
+    __syncthreads();
+    const LeafParams<KT> &P = sP;
     const uint32_t nleaves = P.count_dev ? *P.count_dev : gridDim.x;
     for (uint32_t li = blockIdx.x; li < nleaves; li += gridDim.x) {
         if (li != blockIdx.x) __syncthreads();   // the previous leaf's readers of the planes are done
@@ -489,7 +505,9 @@ cudaError_t launch_leaf_nt(const LeafParams<KT> &LP, uint32_t count, cudaStream_
     int cap = 0;
     cudaError_t e = resident_ctas(k_leaf<KT, NT>, NT, smem, cc, &cap);
     if (e != cudaSuccess) return e;
-    k_leaf<KT, NT><<<count ? count : (uint32_t)cap, NT, smem, s>>>(LP);
+    // persistent grids: at most 2 CTAs per SM (small classes hold few keys)
+    const uint32_t pgrid = (uint32_t)cap < 296u ? (uint32_t)cap : 296u;
+    k_leaf<KT, NT><<<count ? count : pgrid, NT, smem, s>>>(LP);
     return cudaGetLastError();
 }
 

@@ -169,7 +169,24 @@ struct MwParams {
     uint64_t n_total;
     int aligned;
     LevelCtrl *ctrl;     // element-pass statistics
+    LoopPtrs<KT> lp;     // lp.level != nullptr: the current level's lists (partition.cuh)
+    int ticket_sel;      // loop: 0 = the count kernel's ticket, 1 = the scatter kernel's
 };
+
+template <class KT>
+__device__ __forceinline__ void loop_resolve(MwParams<KT> &P) {
+    if (!P.lp.level) return;
+    const uint32_t lv = *P.lp.level, cp = lv & 1;
+    const LevelCtrl *prev = loop_prev(P.lp, lv);
+    P.msegs = static_cast<MSeg<KT> *>(P.lp.msegs[cp]);
+    P.tile_map = P.lp.mtile_map[cp];
+    P.hist = P.lp.mhist[cp];
+    P.cursor = P.lp.mcursor[cp];
+    P.nseg_dev = &prev->nmseg_next;
+    P.ntiles_dev = &prev->nmtiles_next;
+    P.ctrl = P.lp.ctrl + lv;
+    P.ticket = P.ticket_sel ? &P.ctrl->mw_ticket_scatter : &P.ctrl->mw_ticket_count;
+}
 
 template <class KT, int NT, int IPT, int STAGES>
 struct MwSmem {
@@ -343,7 +360,9 @@ __device__ __forceinline__ uint32_t mw_match(uint32_t v0, uint32_t v1, uint32_t 
 // chunk reduce it and one of them adds the tile's count to the segment's
 // histogram.
 template <class KT, int NT, int IPT, int STAGES, int MINB>
-__global__ void __launch_bounds__(NT + 32, MINB) k_mw_count(MwParams<KT> P) {
+__global__ void __launch_bounds__(NT + 32, MINB) k_mw_count(const MwParams<KT> Pin) {
+    __shared__ MwParams<KT> sP;
+    const MwParams<KT> &P = cta_params(Pin, sP);
     using SM = MwSmem<KT, NT, IPT, STAGES>;
     constexpr uint32_t NW = SM::NW;
     static_assert(NT == MW_K * MW_K, "one 16-thread chunk per bucket row");
@@ -406,7 +425,9 @@ __global__ void __launch_bounds__(NT + 32, MINB) k_mw_count(MwParams<KT> P) {
 
 // ---- k_mw_scan: bucket starts and cursor reset, one warp per segment ---------------
 template <class KT>
-__global__ void k_mw_scan(MwParams<KT> P) {
+__global__ void k_mw_scan(const MwParams<KT> Pin) {
+    __shared__ MwParams<KT> sP;
+    const MwParams<KT> &P = cta_params(Pin, sP);
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t nseg = *P.nseg_dev;
     for (uint32_t si = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); si < nseg;
@@ -428,7 +449,9 @@ __global__ void k_mw_scan(MwParams<KT> P) {
 
 // ---- k_mw_scatter -------------------------------------------------------------
 template <class KT, int NT, int IPT, int STAGES, int MINB>
-__global__ void __launch_bounds__(NT + 32, MINB) k_mw_scatter(MwParams<KT> P) {
+__global__ void __launch_bounds__(NT + 32, MINB) k_mw_scatter(const MwParams<KT> Pin) {
+    __shared__ MwParams<KT> sP;
+    const MwParams<KT> &P = cta_params(Pin, sP);
     using T = typename KT::T;
     using SM = MwSmem<KT, NT, IPT, STAGES>;
     constexpr uint32_t NW = SM::NW;

@@ -117,7 +117,9 @@ __device__ __forceinline__ void mw8_widen(uint64_t c, uint32_t (&q)[MW8 / 2]) {
 
 // ---- k_mw8_count -----------------------------------------------------------------
 template <class KT, int NT, int IPT, int STAGES, int MINB>
-__global__ void __launch_bounds__(NT + 32, MINB) k_mw8_count(MwParams<KT> P) {
+__global__ void __launch_bounds__(NT + 32, MINB) k_mw8_count(const MwParams<KT> Pin) {
+    __shared__ MwParams<KT> sP;
+    const MwParams<KT> &P = cta_params(Pin, sP);
     using K = typename KT::K;
     using SM = Mw8Smem<KT, NT, IPT, STAGES>;
     constexpr uint32_t NW = SM::NW;
@@ -181,7 +183,9 @@ __global__ void __launch_bounds__(NT + 32, MINB) k_mw8_count(MwParams<KT> P) {
 
 // ---- k_mw8_scatter ---------------------------------------------------------------
 template <class KT, int NT, int IPT, int STAGES, int MINB>
-__global__ void __launch_bounds__(NT + 32, MINB) k_mw8_scatter(MwParams<KT> P) {
+__global__ void __launch_bounds__(NT + 32, MINB) k_mw8_scatter(const MwParams<KT> Pin) {
+    __shared__ MwParams<KT> sP;
+    const MwParams<KT> &P = cta_params(Pin, sP);
     using T = typename KT::T;
     using K = typename KT::K;
     using SM = Mw8Smem<KT, NT, IPT, STAGES>;

@@ -34,6 +34,35 @@ struct PassParams;
 template <class KT>
 __device__ __forceinline__ uint32_t pass_ntiles(const PassParams<KT> &P);
 
+// Device-resident level state of the sort's level loop (the paper's explicit
+// stack, as breadth-first level arrays).  A kernel launched by
+// the loop reads the current level and picks that level's arrays (segment
+// lists and tile maps ping-pong by level parity), so one fixed sequence of
+// launches — the body of a CUDA-graph loop — serves every level.
+template <class KT>
+struct LoopPtrs {
+    const uint32_t *level;   // nullptr: the params are static (standalone pass, root)
+    Seg *segs[2];
+    uint32_t *tile_map[2];
+    unsigned long long *cursor[2];
+    uint32_t *ecursor[2];
+    void *msegs[2];          // MSeg<KT> (multiway.cuh)
+    uint32_t *mtile_map[2], *mhist[2], *mcursor[2];
+    LevelCtrl *ctrl;         // one control block per level
+    LevelCtrl *root;         // the root's counts (level -1)
+    // leaves (and finished equal-record runs) of level l go to set (l / 4) & 1:
+    // one iteration of the loop partitions 4 levels while it sorts the
+    // previous 4 levels' leaves (LOOP_BATCH, loop.cuh)
+    Leaf *leaves[2];
+    uint32_t *leaf_counts[2];
+    Leaf *copies[2];
+    uint32_t *copy_count[2];
+};
+template <class KT>
+__device__ __forceinline__ const LevelCtrl *loop_prev(const LoopPtrs<KT> &lp, uint32_t lv) {
+    return lv == 0 ? lp.root : lp.ctrl + lv - 1;
+}
+
 template <class KT>
 struct PassParams {
     using T = typename KT::T;
@@ -52,11 +81,38 @@ struct PassParams {
     uint64_t n_total;      // length of each data buffer (bounds the TMA reads)
     int aligned;           // both data buffers 16-byte aligned -> TMA bulk copies
     int ordered;           // 1: decoupled look-back (deterministic layout), 0: atomic cursor
+    LoopPtrs<KT> lp;       // lp.level != nullptr: segs .. ntiles_dev are the current level's
 };
 
 template <class KT>
 __device__ __forceinline__ uint32_t pass_ntiles(const PassParams<KT> &P) {
     return P.ntiles_dev ? *P.ntiles_dev : P.ntiles;
+}
+
+// Kernels of the loop keep their parameters in shared memory, resolved once
+// per CTA by thread 0 (a per-thread copy of a modified by-value parameter
+// struct would live in local memory):  `const auto &P = cta_params(Pin, sP);`
+template <class PP>
+__device__ __forceinline__ const PP &cta_params(const PP &in, PP &sm) {
+    if (threadIdx.x == 0) {
+        sm = in;
+        loop_resolve(sm);
+    }
+    __syncthreads();
+    return sm;
+}
+
+// the level's arrays (every kernel of the loop calls this first)
+template <class KT>
+__device__ __forceinline__ void loop_resolve(PassParams<KT> &P) {
+    if (!P.lp.level) return;
+    const uint32_t lv = *P.lp.level, cp = lv & 1;
+    P.segs = P.lp.segs[cp];
+    P.tile_map = P.lp.tile_map[cp];
+    P.cursor = P.lp.cursor[cp];
+    P.ecursor = P.lp.ecursor[cp];
+    P.ctrl = P.lp.ctrl + lv;
+    P.ntiles_dev = &loop_prev(P.lp, lv)->ntiles_next;
 }
 
 }  // namespace bq
@@ -108,9 +164,33 @@ struct PostParams {
     // scratch buffer, copied to the user buffer by k_copy_runs
     Leaf *copies;
     uint32_t *copy_count;
+    uint32_t copy_cap;
     // set to 1 when a leaf list would overflow (the call then fails)
     uint32_t *overflow;
 };
+
+template <class KT>
+__device__ __forceinline__ void loop_resolve(PostParams<KT> &Q) {
+    loop_resolve(Q.pass);
+    loop_resolve(Q.mw);
+    const LoopPtrs<KT> &lp = Q.pass.lp;
+    if (!lp.level) return;
+    const uint32_t lv = *lp.level, np = (lv & 1) ^ 1;
+    Q.next_segs = lp.segs[np];
+    Q.next_tile_map = lp.tile_map[np];
+    Q.next_cursor = lp.cursor[np];
+    Q.next_ecursor = lp.ecursor[np];
+    Q.next_msegs = static_cast<MSeg<KT> *>(lp.msegs[np]);
+    Q.next_mtile_map = lp.mtile_map[np];
+    Q.next_mhist = lp.mhist[np];
+    Q.child_ctrl = lp.ctrl + lv;
+    Q.nseg_dev = &loop_prev(lp, lv)->nseg_next;
+    const uint32_t set = (lv / LOOP_BATCH) & 1;
+    Q.leaves = lp.leaves[set];
+    Q.leaf_counts = lp.leaf_counts[set];
+    Q.copies = lp.copies[set];
+    Q.copy_count = lp.copy_count[set];
+}
 
 template <class KT>
 struct SegCounts {
@@ -279,7 +359,8 @@ __device__ __forceinline__ void emit_children(const PostParams<KT> &Q, int nch, 
             if (cp != 0)   // in the scratch buffer: copy to the user buffer in chunks
                 for (uint32_t off = 0; off < len; off += 65536) {
                     const uint32_t ci = atomicAdd(Q.copy_count, 1u);
-                    Q.copies[ci] = Leaf{cb[c] + off, (len - off) < 65536u ? (len - off) : 65536u, cp, 0};
+                    if (ci < Q.copy_cap) Q.copies[ci] = Leaf{cb[c] + off, (len - off) < 65536u ? (len - off) : 65536u, cp, 0};
+                    else if (Q.overflow) *Q.overflow = 1u;
                 }
         } else if (kind == C_BIN || kind == C_MW) {
             Seg ch;
@@ -334,7 +415,9 @@ template <class KT, int NT>
 __device__ __forceinline__ void post_segment(const PostParams<KT> &Q, uint32_t si);
 
 template <class KT, int NT>
-__global__ void __launch_bounds__(NT) k_post(PostParams<KT> Q) {
+__global__ void __launch_bounds__(NT) k_post(const PostParams<KT> Qin) {
+    __shared__ PostParams<KT> sQ;
+    const PostParams<KT> &Q = cta_params(Qin, sQ);
     const uint32_t nseg = Q.nseg_dev ? *Q.nseg_dev : Q.nseg;
     post_stats_init();
     for (uint32_t si = blockIdx.x; si < nseg; si += gridDim.x) post_segment<KT, NT>(Q, si);
@@ -410,10 +493,12 @@ __device__ __forceinline__ void post_segment(const PostParams<KT> &Q, uint32_t s
 // the staging area is the final buffer itself (it may overlap the band), into
 // the other buffer, from where phase 1 copies them into the final buffer.
 template <class KT, int NT>
-__global__ void __launch_bounds__(NT) k_fill(PostParams<KT> Q, int phase) {
+__global__ void __launch_bounds__(NT) k_fill(const PostParams<KT> Qin, int phase) {
     using T = typename KT::T;
     using K = typename KT::K;
     constexpr uint32_t TILE = (uint32_t)tile_elems<KT>();
+    __shared__ PostParams<KT> sQ;
+    const PostParams<KT> &Q = cta_params(Qin, sQ);
     const PassParams<KT> &P = Q.pass;
     if (Q.emit_children && P.ctrl->nbig == 0) return;   // sort: no long band this level
     const uint32_t ntiles = pass_ntiles(P);
@@ -473,8 +558,10 @@ __global__ void __launch_bounds__(NT) k_init_root(PostParams<KT> Q, uint32_t n) 
 // a7 after a multiway scatter: the (up to) 16 buckets of every multiway
 // segment become its children.
 template <class KT, int NT>
-__global__ void __launch_bounds__(NT) k_post_mw(PostParams<KT> Q) {
+__global__ void __launch_bounds__(NT) k_post_mw(const PostParams<KT> Qin) {
     __shared__ uint32_t cb[MW_K], cl[MW_K];
+    __shared__ PostParams<KT> sQ;
+    const PostParams<KT> &Q = cta_params(Qin, sQ);
     const uint32_t nseg = *Q.mw.nseg_dev;
     post_stats_init();
     for (uint32_t si = blockIdx.x; si < nseg; si += gridDim.x) {
@@ -489,11 +576,14 @@ __global__ void __launch_bounds__(NT) k_post_mw(PostParams<KT> Q) {
 }
 
 // Finished runs of equal record keys still in the scratch buffer -> user
-// buffer (persistent grid over the copy list of one batch).
+// buffer (persistent grid over one copy list; in the level loop the list of
+// the previous batch of levels, loop_prev_set).
 template <class KT, int NT>
-__global__ void __launch_bounds__(NT) k_copy_runs(const Leaf *list, const uint32_t *count, typename KT::T *user,
+__global__ void __launch_bounds__(NT) k_copy_runs(const LoopPtrs<KT> lp, const uint32_t *level, typename KT::T *user,
                                                   const typename KT::T *scratch) {
-    const uint32_t n = *count;
+    const uint32_t set = loop_prev_set(*level);
+    const Leaf *list = set ? lp.copies[1] : lp.copies[0];
+    const uint32_t n = set ? *lp.copy_count[1] : *lp.copy_count[0];
     for (uint32_t li = blockIdx.x; li < n; li += gridDim.x) {
         const Leaf l = list[li];
         for (uint32_t j = threadIdx.x; j < l.len; j += NT) user[(uint64_t)l.begin + j] = scratch[(uint64_t)l.begin + j];

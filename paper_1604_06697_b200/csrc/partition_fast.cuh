@@ -58,7 +58,9 @@ constexpr int fast_smem_bytes() {
 }
 
 template <class KT, int NT, int IPT, int STAGES, int MINB>
-__global__ void __launch_bounds__(NT + 32, MINB) k_part_fast(PassParams<KT> P) {
+__global__ void __launch_bounds__(NT + 32, MINB) k_part_fast(const PassParams<KT> Pin) {
+    __shared__ PassParams<KT> sP;
+    const PassParams<KT> &P = cta_params(Pin, sP);
     using T = typename KT::T;
     using K = typename KT::K;
     using SM = FastSmem<KT, NT, IPT, STAGES>;

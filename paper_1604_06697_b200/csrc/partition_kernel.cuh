@@ -84,7 +84,9 @@ struct TileGeom {
 };
 
 template <class KT, int NT, int IPT, int STAGES, int MINB, bool ORDERED>
-__global__ void __launch_bounds__(NT + (ORDERED ? 96 : 64), MINB) k_partition(PassParams<KT> P) {
+__global__ void __launch_bounds__(NT + (ORDERED ? 96 : 64), MINB) k_partition(const PassParams<KT> Pin) {
+    __shared__ PassParams<KT> sP;
+    const PassParams<KT> &P = cta_params(Pin, sP);
     using T = typename KT::T;
     using K = typename KT::K;
     using SM = PartSmem<KT, NT, IPT, STAGES>;

@@ -4,18 +4,16 @@ import torch
 
 
 def to_dev(a: np.ndarray, offset: int = 0) -> torch.Tensor:
-    """numpy -> contiguous CUDA tensor of the matching kind.  u64 keys and
-    records travel as int64 (the binding reinterprets them as uint64).
-    offset > 0 returns a view starting `offset` elements into a larger
-    allocation (unaligned-pointer tests)."""
-    if a.dtype == np.uint64:
+    """numpy -> contiguous CUDA tensor of the matching kind: u64 keys as
+    torch.uint64, records (2-D) as int64 rows whose column 0 the binding reads
+    as the unsigned key.  offset > 0 returns a view starting `offset` elements
+    into a larger allocation (unaligned-pointer tests)."""
+    if a.dtype == np.uint64 and a.ndim == 2:
         a = a.view(np.int64)
-    t = torch.from_numpy(np.ascontiguousarray(a))
     if offset:
-        pad = torch.zeros((offset,) + tuple(t.shape[1:]), dtype=t.dtype)
-        big = torch.cat([pad, t]).cuda()
-        return big[offset:]
-    return t.cuda()
+        a = np.concatenate([np.zeros((offset,) + a.shape[1:], dtype=a.dtype), a])
+    t = torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    return t[offset:] if offset else t
 
 
 def to_host(t: torch.Tensor, like: np.ndarray) -> np.ndarray:

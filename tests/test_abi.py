@@ -119,3 +119,19 @@ def test_options_struct_layout():
     assert [f for f, _ in b.bq_sort_options._fields_][:7] == ["pivot_rule", "depth_limit", "timing", "ordered",
                                                                "ways", "records", "subtree"]
     assert ctypes.sizeof(b.bq_sort_stats) == 72
+
+
+def test_binding_refuses_ambiguous_int64():
+    """A 1-D int64 tensor has no unambiguous order for libbq (uint64 keys are
+    compared unsigned): the binding refuses it; uint64, int32,
+    float64 and the 2-D record/pair shapes map to their kinds."""
+    import torch
+    import pytest
+    import paper_1604_06697_b200 as bq
+    with pytest.raises(TypeError):
+        bq.kind_of(torch.zeros(4, dtype=torch.int64))
+    assert bq.kind_of(torch.zeros(4, dtype=torch.uint64)) == bq.BQ_U64
+    assert bq.kind_of(torch.zeros(4, dtype=torch.int32)) == bq.BQ_I32
+    assert bq.kind_of(torch.zeros(4, dtype=torch.float64)) == bq.BQ_F64
+    assert bq.kind_of(torch.zeros((4, 4), dtype=torch.int64)) == bq.BQ_REC32
+    assert bq.kind_of(torch.zeros((4, 2), dtype=torch.int64)) == bq.BQ_KEYIDX16

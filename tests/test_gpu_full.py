@@ -153,7 +153,7 @@ def test_sort_max_n_uint64(B):
     g = torch.Generator(device="cuda").manual_seed(13)
     src = torch.randint(0, (1 << 62) - 1, (NMAX,), dtype=torch.int64, device="cuda", generator=g)
     t = src.clone()
-    st = B.bq_sort_ex(t)
+    st = B.bq_sort_ex(t.view(torch.uint64))
     assert st["fallback_segments"] == 0
     ref = torch.sort(src)[0]
     assert bool(torch.equal(t, ref))

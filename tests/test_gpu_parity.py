@@ -159,10 +159,11 @@ def test_sort_special_f64(B):
 @pytest.mark.parametrize("kind", ["i32", "f64", "rec32"])
 def test_depth_cap_fallback(B, kind):
     # a tiny Introsort limit sends segments to the merge-based fallback (a9):
-    # with n ~ 10 S, segments at depth <= 2 are still longer than S
-    n = 10 * LEAF[kind] + 7
-    a = make(kind, n, seed=9)
-    for ways, limits in [(2, [0, 1, 2]), (16, [0, 1])]:
+    # binary passes at n ~ 10 S leave segments longer than S down to depth 2;
+    # 16-way passes at n ~ 40 S leave children of ~2.5 S at depth 1
+    for ways, limits, m in [(2, [0, 1, 2], 10), (16, [0, 1], 40)]:
+        n = m * LEAF[kind] + 7
+        a = make(kind, n, seed=9)
         for limit in limits:
             t = to_dev(a)
             st = B.bq_sort_ex(t, depth_limit=limit, ways=ways)
@@ -581,3 +582,40 @@ def test_leaf_aware_split(B, frac):
     st = B.bq_sort_ex(t, ways=2)
     check_sorted_equal("i32", to_host(t, a), a)
     assert st["levels"] == 1 and st["leaves"] == 2 and st["fallback_segments"] == 0
+
+
+def test_async_graph_sorts_and_cache(B):
+    """bq_sort_* is enqueued without a host wait (a CUDA-graph level loop,
+    DESIGN.md §7): sorts on a side stream, the stream synchronised only at the
+    end; graphs are cached per (buffers, n, options) — a re-used buffer with new
+    contents, new buffers, and more distinct configurations than cache slots
+    (eviction) all sort correctly."""
+    s = torch.cuda.Stream()
+    arrs = [make("i32", 200_003 + 977 * k, seed=k) for k in range(40)]
+    outs = []
+    with torch.cuda.stream(s):
+        for k, a in enumerate(arrs):
+            t = to_dev(a)
+            B.bq_sort_i32(t, stream=s)            # no stats: fully asynchronous
+            outs.append(t)
+        t0 = outs[0]
+        t0.copy_(to_dev(arrs[1][: len(arrs[0])]))  # same buffer, new contents: cached graph
+        B.bq_sort_i32(t0, stream=s)
+    s.synchronize()
+    for k in range(1, len(arrs)):
+        assert np.array_equal(to_host(outs[k], arrs[k]), oracle.sort(arrs[k]))
+    assert np.array_equal(to_host(outs[0], arrs[0]), oracle.sort(arrs[1][: len(arrs[0])]))
+
+
+@pytest.mark.parametrize("kind", ["i32", "f64", "rec32"])
+def test_host_loop_matches_graph(B, kind):
+    """The host-driven level loop (timing=True: CUDA events per partition
+    launch) runs the same kernels as the graph: same levels and sorted keys."""
+    a = make(kind, 12 * LEAF[kind] + 5, seed=21)
+    t1, t2 = to_dev(a), to_dev(a)
+    s1 = B.bq_sort_ex(t1)
+    s2 = B.bq_sort_ex(t2, timing=True)
+    check_sorted_equal(kind, to_host(t1, a), a)
+    check_sorted_equal(kind, to_host(t2, a), a)
+    assert s1["levels"] == s2["levels"] and s1["element_passes"] == s2["element_passes"]
+    assert s2["partition_ms"] > 0
