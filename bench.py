@@ -53,15 +53,100 @@ def load_peak():
 
 
 def load_traffic():
-    """dram bytes per launch of the partition kernel from the committed ncu
-    summary (profiles/ncu_partition_summary.json), or None."""
-    p = os.path.join(ROOT, "profiles", "ncu_partition_summary.json")
+    """DRAM bytes (read + write) per launch of the partition kernel inside one
+    c2 sort, from the committed ncu capture summary, or None."""
+    p = os.path.join(ROOT, "profiles", "r02", "ncu_sort_dram.json")
     try:
         with open(p) as f:
             d = json.load(f)
-        return d.get("dram_bytes_per_element_pass"), d
+        return d["k_part_fast"]["dram_bytes_total"], "profiles/r02/ncu_sort_dram.json"
     except Exception:
         return None, None
+
+
+def partition_pass_by_config(bq, bqgen, dev, stream, passes, peak):
+    """north_star: "each partition pass at >= 60% of B200 peak HBM bandwidth" on
+    every config.  Binary passes: BASELINE.md's measurement (10 single
+    out-of-place passes around the Mo3 pivot of the pristine input, L2 flushed
+    before each, median).  Multiway (8-way, the sort's default for 64-bit keys
+    and key+index pairs): every multiway level of a sort of the config (count +
+    scan + scatter, CUDA events), algorithmic bytes 2 w per element like a
+    binary pass (the count pass's extra read counts against it)."""
+    import numpy as np
+    import torch
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+
+    def entry(ms, nbytes, **kw):
+        gbs = nbytes / (ms * 1e-3) / 1e9
+        return dict(kw, ms_median=ms, bytes=nbytes, gbs=gbs, frac_of_measured=gbs / peak,
+                    frac_of_8tbs=gbs / 8000.0, meets_bar=gbs >= 4800.0)
+
+    def time_passes(src, dst, pv, ordered, ws):
+        counts = torch.zeros(3, dtype=torch.int64, device=dev)
+        times = []
+        for _ in range(passes + 1):
+            flush.fill_(1)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            bq.bq_partition_pass(src, dst, pv, counts, ordered=ordered, ws=ws, stream=stream)
+            b.record(stream)
+            torch.cuda.synchronize()
+            times.append(a.elapsed_time(b))
+        return statistics.median(times[1:])
+
+    def time_mw(data, src, ws):
+        st = []
+        for _ in range(3):
+            data.copy_(src)
+            flush.fill_(1)
+            st.append(bq.bq_sort_ex(data, timing=True, ws=ws, stream=stream))
+        ms = statistics.median(s["multiway_ms"] for s in st)
+        return ms, st[-1]["multiway_element_passes"], st[-1]
+
+    out = {}
+    # c3: float64, n = 2^27, random
+    a = bqgen.config("c3", seed=1, ordering="random")
+    n3 = len(a)
+    src = torch.from_numpy(a).to(dev)
+    dst = torch.empty_like(src)
+    ws = bq.workspace(bq.BQ_F64, n3, dev)
+    pv = bq.bq_pivot_f64(src, bq.BQ_PIVOT_MO3, ws=ws, stream=stream)
+    out["c3_f64_binary_pass"] = entry(time_passes(src, dst, pv, False, ws), 16 * n3, n=n3)
+    ms, ep, st = time_mw(dst, src, ws)
+    out["c3_f64_8way_levels"] = entry(ms, 16 * ep, n=n3, element_passes=ep, levels=st["levels"])
+    del src, dst, ws
+    # c4a: int32, n = 2^28, 16384 distinct values
+    a = bqgen.config("c4a", seed=1)
+    n4 = len(a)
+    src = torch.from_numpy(a).to(dev)
+    dst = torch.empty_like(src)
+    ws = bq.workspace(bq.BQ_I32, n4, dev)
+    pv = bq.bq_pivot_i32(src, bq.BQ_PIVOT_MO3, ws=ws, stream=stream)
+    out["c4a_i32_binary_pass"] = entry(time_passes(src, dst, pv, False, ws), 8 * n4, n=n4)
+    del src, dst, ws
+    # c5: 32-byte records, n = 2^26: the records pass, the key+index pairs' pass
+    # and the pairs' 8-way levels (the records sort's default path)
+    r = bqgen.config("c5", seed=1)
+    n5 = len(r)
+    src = torch.from_numpy(r.view(np.int64)).to(dev)
+    dst = torch.empty_like(src)
+    ws = bq.workspace(bq.BQ_REC32, n5, dev)
+    pv = bq.bq_pivot_records(src, bq.BQ_PIVOT_MO3, ws=ws, stream=stream)
+    out["c5_rec32_pass"] = entry(time_passes(src, dst, pv, True, ws), 64 * n5, n=n5,
+                                 note="records: the standalone pass is the three-way ordered placement")
+    ms, ep, st = time_mw(dst, src, ws)
+    out["c5_pairs_8way_levels"] = entry(ms, 32 * ep, n=n5, element_passes=ep, levels=st["levels"],
+                                        note="key+index pairs (16 B) of the records sort")
+    pairs = torch.empty((n5, 2), dtype=torch.int64, device=dev)
+    pairs[:, 0] = src[:, 0]
+    pairs[:, 1] = torch.arange(n5, dtype=torch.int64, device=dev)
+    pdst = torch.empty_like(pairs)
+    del dst
+    out["c5_pairs_pass"] = entry(time_passes(pairs, pdst, pv, True, ws), 32 * n5, n=n5,
+                                 note="pairs: the standalone pass is the three-way ordered placement")
+    del src, pairs, pdst, ws, flush
+    torch.cuda.empty_cache()
+    return out
 
 
 # ------------------------------------------------------------ distributed ----
@@ -160,9 +245,25 @@ class ClockSampler:
 
 # ----------------------------------------------------------- cpu baselines ---
 
+def host_facts():
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    try:
+        usable = len(os.sched_getaffinity(0))
+    except Exception:
+        usable = None
+    return {"cpu_model": model, "nproc": os.cpu_count(), "usable_cores": usable}
+
+
 def cpu_baseline(keys_np, sample_n: int):
     """The oracle (as it stands) and std::sort, single-threaded, on the first
-    sample_n keys of the workload."""
+    sample_n keys of the workload (the full c2 n by default)."""
     import oracle
     s = keys_np[:sample_n].copy()
     t0 = time.perf_counter()
@@ -174,9 +275,11 @@ def cpu_baseline(keys_np, sample_n: int):
     t_std = time.perf_counter() - t0
     import numpy as np
     assert np.array_equal(out, s2)
+    full = sample_n == len(keys_np)
     return {"value": sample_n / t_or / 1e9, "unit": "Gkeys/s", "cores": 1, "kind": "oracle",
-            "sample": f"first {sample_n} keys of the c2 input (2^{int(math.log2(sample_n))}), one run",
-            "seconds": t_or,
+            "sample": (f"the whole c2 input (n = 2^{int(math.log2(sample_n))})" if full else
+                       f"first {sample_n} keys of the c2 input (2^{int(math.log2(sample_n))})") + ", one run",
+            "seconds": t_or, "host": host_facts(),
             "std_sort": {"value": sample_n / t_std / 1e9, "unit": "Gkeys/s", "cores": 1, "seconds": t_std}}
 
 
@@ -209,7 +312,7 @@ def run_reference(args, rank, world):
         "data": "synthetic",
         "config": {"workload": WORKLOAD, "sample": f"each step sorts the first 2^22 keys of the c2 input"},
         "cpu_baseline": {"value": value, "unit": "Gkeys/s", "cores": 1, "kind": "oracle",
-                         "sample": "first 2^22 keys of the c2 input per step"},
+                         "sample": "first 2^22 keys of the c2 input per step", "host": host_facts()},
         "e2e": {"value": value, "unit": "Gkeys/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -228,7 +331,8 @@ def main():
     ap.add_argument("--pivot-rule", type=int, default=2, help="0 Mo3, 1 ninther, 2 median of a 64-key sample")
     ap.add_argument("--passes", type=int, default=10)
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--cpu-sample", type=int, default=1 << 27)
+    ap.add_argument("--cpu-sample", type=int, default=1 << 28)
+    ap.add_argument("--no-configs", action="store_true", help="skip the per-config partition-pass table")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-verify", action="store_true")
     args = ap.parse_args()
@@ -261,8 +365,9 @@ def main():
     ws = bq.workspace(bq.BQ_I32, n, dev)
     stream = torch.cuda.current_stream(dev)
 
-    def step(timing=True):
-        return bq.bq_sort_ex(data, pivot_rule=args.pivot_rule, timing=timing, ws=ws, stream=stream)
+    def step():
+        # the product path: fully asynchronous graph launch, no host wait
+        bq.bq_sort_ex(data, pivot_rule=args.pivot_rule, ws=ws, stream=stream, stats=False)
 
     for _ in range(args.warmup):
         data.copy_(src)
@@ -274,11 +379,10 @@ def main():
     torch.cuda.synchronize()
     clocks.start()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    stats = []
     for i in range(args.steps):
         data.copy_(src)
         ev[i][0].record(stream)
-        stats.append(step())
+        step()
         ev[i][1].record(stream)
     torch.cuda.synchronize()
     barrier()
@@ -294,23 +398,35 @@ def main():
         verified = bool(torch.equal(ref, data))
         del ref
 
-    # roofline of the dominant kernel (partition), live from the timed steps
-    part_ms = sum(s["partition_ms"] for s in stats)
-    part_bytes = sum(s["partition_bytes"] for s in stats)
+    # statistics of one (untimed) step: the device counters of the same sort
+    data.copy_(src)
+    last = bq.bq_sort_ex(data, pivot_rule=args.pivot_rule, ws=ws, stream=stream)
+
+    # roofline of the dominant kernel (the tile-partition pass): the sort's
+    # host-driven mode records CUDA events around every partition launch on the
+    # launching stream (bq_sort_options.timing); same kernels, same levels
     peak, peak_src = load_peak()
+    tstats = []
+    for _ in range(3):
+        data.copy_(src)
+        tstats.append(bq.bq_sort_ex(data, pivot_rule=args.pivot_rule, timing=True, ws=ws, stream=stream))
+    part_ms = sum(s["partition_ms"] for s in tstats) / len(tstats)
+    part_bytes = sum(s["partition_bytes"] for s in tstats) / len(tstats)
+    launches = tstats[-1]["partition_launches"]
     achieved = part_bytes / (part_ms * 1e-3) / 1e9
-    elem_passes = stats[-1]["element_passes"]
-    traffic_per_ep, traffic_doc = load_traffic()
-    launches = stats[-1]["partition_launches"]
+    traffic_total, traffic_src = load_traffic()   # one whole c2 sort under ncu (same input, same levels)
     roofline = {
         "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
         "peak_source": peak_src,
-        "kernel": "k_part_fast (tile partition pass, every level of the sort; leaves run concurrently on a side stream)",
-        "algorithmic_bytes_per_launch": part_bytes / len(stats) / launches,
-        "launch_ms_avg": part_ms / len(stats) / launches,
+        "kernel": "k_part_fast (tile partition pass, every level of the sort)",
+        "algorithmic_bytes_per_launch": part_bytes / launches,
+        "launch_ms_avg": part_ms / launches,
         "launches_per_step": launches,
-        "share_of_step": part_ms / ms_total,
-        "traffic": (traffic_per_ep * elem_passes / launches) if traffic_per_ep else None,
+        "share_of_step": part_ms / ms_per_step,
+        "traffic": traffic_total / launches if traffic_total else None,
+        "traffic_source": traffic_src,
+        "how": "CUDA events around each partition launch (bq_sort_options.timing: the host-driven level "
+               "loop, same kernels as the graph) averaged over 3 sorts; share = that time / ms_per_step",
     }
 
     # BASELINE.md partition-pass measurement: 10 single passes, L2 flushed
@@ -363,6 +479,10 @@ def main():
                          "inplace_* = bq_partition_i32, the in-place block partition (N2) with its "
                          "equal band, input restored before each call"}
 
+    by_config = None
+    if args.passes > 0 and not args.no_configs and rank == 0:
+        by_config = partition_pass_by_config(bq, bqgen, dev, stream, args.passes, peak)
+
     # end to end through the public API with host buffers
     e2e = None
     if args.e2e_steps > 0:
@@ -390,7 +510,6 @@ def main():
         dist.destroy_process_group()
     if rank != 0:
         return 0
-    last = stats[-1]
     line = {
         "metric": METRIC, "value": value, "unit": "Gkeys/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
@@ -398,12 +517,14 @@ def main():
         "config": {"workload": WORKLOAD, "n_per_gpu": n, "pivot_rule": ["mo3", "ninther", "sample64"][args.pivot_rule],
                    "parallelism": f"replicas{world}" if world > 1 else "1gpu",
                    "l2": "inputs (1 GiB) larger than L2 (126 MB); restore copy between steps is untimed",
-                   "timing": "sum of per-step CUDA events around bq_sort on the launch stream"},
+                   "timing": "sum of per-step CUDA events around bq_sort (the asynchronous graph launch) "
+                             "on the launch stream"},
         "roofline": roofline,
         "partition_pass": ppass,
+        "partition_pass_by_config": by_config,
         "cpu_baseline": cpu,
         "e2e": e2e,
-        "gpu_launches": int(sum(s["kernel_launches"] for s in stats)),
+        "gpu_launches": int(last["kernel_launches"]) * args.steps,
         "clocks": clk,
         "sort_stats": {k: last[k] for k in ("levels", "partition_launches", "kernel_launches", "element_passes",
                                             "partitioned_segments", "leaves", "fallback_segments",

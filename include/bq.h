@@ -129,13 +129,16 @@ typedef struct {
     uint32_t partition_launches;   /* launches of the tile-partition kernel */
     uint32_t kernel_launches;      /* all libbq kernel launches of the call */
     uint32_t reserved0;
-    uint64_t element_passes;       /* sum of segment lengths over all partition passes */
+    uint64_t element_passes;       /* sum of segment lengths over all partition passes (binary + multiway) */
     uint64_t partitioned_segments; /* segments partitioned (calls of the partitioner) */
     uint64_t leaves;               /* segments finished by the shared-memory leaf sort */
     uint64_t fallback_segments;    /* segments that hit the depth limit (fallback sort) */
     uint64_t band_elements;        /* keys placed by the equal-band fill */
-    double partition_ms;           /* sum of partition-kernel times (timing != 0) */
-    double partition_bytes;        /* algorithmic bytes of those launches: 2*w*element_passes */
+    double partition_ms;           /* sum of binary partition-kernel times (timing != 0) */
+    double partition_bytes;        /* algorithmic bytes of those launches: 2*w*(element_passes -
+                                      multiway_element_passes) */
+    double multiway_ms;            /* sum of multiway level times: count + scan + scatter (timing != 0) */
+    uint64_t multiway_element_passes;  /* elements through multiway levels (also in element_passes) */
 } bq_sort_stats;
 
 /* Workspace bytes every call below needs for `n` elements of `kind`:

@@ -55,7 +55,8 @@ class bq_sort_stats(ctypes.Structure):
                 ("element_passes", ctypes.c_uint64), ("partitioned_segments", ctypes.c_uint64),
                 ("leaves", ctypes.c_uint64), ("fallback_segments", ctypes.c_uint64),
                 ("band_elements", ctypes.c_uint64), ("partition_ms", ctypes.c_double),
-                ("partition_bytes", ctypes.c_double)]
+                ("partition_bytes", ctypes.c_double), ("multiway_ms", ctypes.c_double),
+                ("multiway_element_passes", ctypes.c_uint64)]
 
     def as_dict(self):
         return {f: (getattr(self, f) if not isinstance(getattr(self, f), ctypes.Array) else None)

@@ -241,7 +241,9 @@ struct alignas(64) LevelCtrl {
     uint32_t mw_ticket_scatter;  // tile tickets of the multiway scatter kernel
     uint32_t nmseg_next;         // multiway children appended to the next level
     uint32_t nmtiles_next;       // their tiles
-    uint32_t pad2[9];
+    uint32_t pad1;
+    unsigned long long mw_element_passes;   // sum of multiway-partitioned lengths this level
+    uint32_t pad2[6];
 };
 static_assert(sizeof(LevelCtrl) == 128, "LevelCtrl layout");
 

@@ -706,11 +706,14 @@ bq_status enqueue_prefix(const SortPlan<KT> &pl, cudaStream_t s) {
 // (optional) brackets the binary partition launch
 template <class KT>
 bq_status enqueue_level(const SortPlan<KT> &pl, cudaStream_t s, int use_cond, cudaGraphConditionalHandle h_loop,
-                        cudaGraphConditionalHandle h_fb, cudaEvent_t ev0, cudaEvent_t ev1) {
+                        cudaGraphConditionalHandle h_fb, cudaEvent_t ev0, cudaEvent_t ev1, cudaEvent_t mev0 = nullptr,
+                        cudaEvent_t mev1 = nullptr) {
     if constexpr (mw_capable<KT>()) if (pl.ways > 2) {
         MwParams<KT> MP = pl.MP;
+        if (mev0) BQ_CK(cudaEventRecord(mev0, s));
         bq_status st = launch_multiway<KT>(MP, nullptr, s, pl.ways);
         if (st != BQ_OK) return st;
+        if (mev1) BQ_CK(cudaEventRecord(mev1, s));
         k_post_mw<KT, POST_THREADS><<<POST_GRID, POST_THREADS, 0, s>>>(pl.Q);
         BQ_CK_LAUNCH();
     }
@@ -959,10 +962,12 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
     }();
     const bool host_loop = timing || host_env;
     std::vector<cudaEvent_t> evs;   // timing: one pair per level
+    std::vector<cudaEvent_t> mevs;  // timing: one pair per level around the multiway step
     cudaStream_t side = nullptr;    // host-driven loop: the leaves' stream
     cudaEvent_t efork = nullptr, ejoin = nullptr;
     auto cleanup = [&]() {
         for (auto e : evs) cudaEventDestroy(e);
+        for (auto e : mevs) cudaEventDestroy(e);
         if (side) cudaStreamDestroy(side);
         if (efork) cudaEventDestroy(efork);
         if (ejoin) cudaEventDestroy(ejoin);
@@ -1003,12 +1008,18 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
                 cleanup();
                 return set_error(BQ_ERR_CUDA, "level loop did not terminate");
             }
-            cudaEvent_t e0 = nullptr, e1 = nullptr;
+            cudaEvent_t e0 = nullptr, e1 = nullptr, m0 = nullptr, m1 = nullptr;
             if (timing) {
                 BQ_CKC(cudaEventCreate(&e0));
                 evs.push_back(e0);
                 BQ_CKC(cudaEventCreate(&e1));
                 evs.push_back(e1);
+                if (ways > 2) {
+                    BQ_CKC(cudaEventCreate(&m0));
+                    mevs.push_back(m0);
+                    BQ_CKC(cudaEventCreate(&m1));
+                    mevs.push_back(m1);
+                }
             }
             if (level % LOOP_BATCH == 0) {   // fork
                 BQ_CKC(cudaEventRecord(efork, s));
@@ -1016,7 +1027,7 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
                 BQ_SKC(enqueue_flush<KT>(pl, side));
                 BQ_CKC(cudaEventRecord(ejoin, side));
             }
-            BQ_SKC(enqueue_level<KT>(pl, s, 0, 0, 0, e0, e1));
+            BQ_SKC(enqueue_level<KT>(pl, s, 0, 0, 0, e0, e1, m0, m1));
             if (level % LOOP_BATCH == LOOP_BATCH - 1) BQ_CKC(cudaStreamWaitEvent(s, ejoin, 0));   // join
             BQ_SKC(enqueue_level_end<KT>(pl, s, 0, 0, 0));
             host_levels = level + 1;
@@ -1067,13 +1078,14 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
             local.levels++;
             local.partition_launches++;
             local.partitioned_segments += nseg_l;
-            local.element_passes += h.element_passes;
+            local.element_passes += h.element_passes + h.mw_element_passes;
+            local.multiway_element_passes += h.mw_element_passes;
             local.band_elements += h.band_elems;
             local.leaves += h.nleaf;
         }
         local.leaves += hroot.nleaf;
         local.fallback_segments = hm.fb_count;
-        local.partition_bytes = 2.0 * (double)sizeof(T) * (double)local.element_passes;
+        local.partition_bytes = 2.0 * (double)sizeof(T) * (double)(local.element_passes - local.multiway_element_passes);
         if (timing) {
             double ms = 0;
             for (size_t i = 0; i + 1 < evs.size() && (int)(i / 2) < (int)local.levels; i += 2) {
@@ -1082,6 +1094,13 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
                 ms += f;
             }
             local.partition_ms = ms;
+            ms = 0;
+            for (size_t i = 0; i + 1 < mevs.size() && (int)(i / 2) < (int)local.levels; i += 2) {
+                float f = 0;
+                BQ_CKC(cudaEventElapsedTime(&f, mevs[i], mevs[i + 1]));
+                ms += f;
+            }
+            local.multiway_ms = ms;
         }
     }
 #undef BQ_CKC

@@ -443,7 +443,7 @@ __global__ void k_mw_scan(const MwParams<KT> Pin) {
             P.msegs[si].start[lane] = inc - h;
             P.cursor[lane * P.hstride + si] = 0;
         }
-        if (lane == 31) atomicAdd(&P.ctrl->element_passes, (unsigned long long)inc);
+        if (lane == 31) atomicAdd(&P.ctrl->mw_element_passes, (unsigned long long)inc);
     }
 }
 
