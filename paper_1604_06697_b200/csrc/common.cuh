@@ -4,12 +4,32 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdio>
 #include <cstddef>
 #include <cuda_runtime.h>
 
 #include "bq.h"
 
 namespace bq {
+
+// Bounds checks of the kernels' computed indices, compiled in only with
+// -DBQ_CHECKS (a checking build of the library, tools/variants.py; the pool's
+// compute-sanitizer is closed): a failed check prints where and traps, so the
+// call fails with a CUDA error instead of corrupting memory silently.
+#ifdef BQ_CHECKS
+#define BQ_CHECK(cond)                                                                          \
+    do {                                                                                        \
+        if (!(cond)) {                                                                          \
+            printf("BQ_CHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, __LINE__, \
+                   (int)blockIdx.x, (int)threadIdx.x);                                          \
+            __trap();                                                                           \
+        }                                                                                       \
+    } while (0)
+#else
+#define BQ_CHECK(cond) \
+    do {               \
+    } while (0)
+#endif
 
 // ---------------------------------------------------------------------------
 // Resident-CTA capacity of a kernel, cached per device: the library's only

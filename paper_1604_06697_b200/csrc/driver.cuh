@@ -665,6 +665,8 @@ bq_status make_plan(SortPlan<KT> &pl, typename KT::T *data, size_t n, void *ws, 
     Q.emit_children = 1;
     Q.band_inline_max = BAND_INLINE_MAX;
     Q.overflow = &pl.misc->overflow;
+    Q.nseg_cap = (uint32_t)L.max_segs;
+    Q.ntile_cap = (uint32_t)L.max_tiles;
     // leaves
     LeafParams<KT> &LP = pl.LP;
     LP = LeafParams<KT>{};

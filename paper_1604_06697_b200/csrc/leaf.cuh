@@ -231,6 +231,7 @@ __device__ __forceinline__ typename LeafTraits<KT>::E leaf_pad() {
 // one select and one store with an immediate offset per key.
 template <class E, int IPT, class PL>
 __device__ __forceinline__ void store_run(const PL &pl, const E (&x)[IPT], int cnt, int base, int dir) {
+    BQ_CHECK(cnt >= 0 && cnt <= IPT);
     if (cnt == IPT) {
         const bool rev = dir < 0;
         const uint32_t c0 = pl.cur(rev ? base - (IPT - 1) : base);
@@ -275,6 +276,7 @@ __device__ __forceinline__ void leaf_body(const LeafParams<KT> &P, const Leaf lf
     if constexpr (REC) pl.i0 = smem_u32(SM::idxp(sm));
     const int t = (int)threadIdx.x;
     const int len = (int)lf.len;
+    BQ_CHECK(len >= 0 && len <= IPT * NT && lf.begin + (uint64_t)len <= P.n_total);
     T *src = lf.parity ? P.bufs[1] : P.bufs[0];
     T *out = P.out_other ? (lf.parity ? P.bufs[0] : P.bufs[1]) : P.out;
     const uint64_t b = lf.begin;
@@ -375,6 +377,7 @@ __device__ __forceinline__ void leaf_body(const LeafParams<KT> &P, const Leaf lf
                     if (e_less(bv, av)) hi = mid;
                     else lo = mid + 1;
                 }
+                BQ_CHECK(lo >= 0 && lo <= na && d - lo >= 0 && d - lo <= nb && a0 + tot <= len);
                 uint32_t pa = ca + (uint32_t)(lo * PL::STEP);
                 uint32_t pb = pl.cur(off + a0 + tot - 1 - (d - lo));
                 E ka = pl.ldc(pa), kb = pl.ldc(pb);
@@ -410,6 +413,7 @@ __device__ __forceinline__ void leaf_body(const LeafParams<KT> &P, const Leaf lf
         for (int k = 0; k < IPT; k++) {
             if (k < cnt) {
                 const uint32_t pos = (uint32_t)(base + k);
+                BQ_CHECK(pos < (uint32_t)len && x[k].i < (uint32_t)len);
                 constexpr uint32_t V = sizeof(T) / 16;
                 const uint4 *s4 = reinterpret_cast<const uint4 *>(gsrc + b + x[k].i);
                 uint4 *d4 = reinterpret_cast<uint4 *>(out + b + pos);

@@ -174,6 +174,7 @@ __global__ void __launch_bounds__(MERGE_THREADS) k_fb_merge(const Leaf *fb, cons
             else hi = mid;
         }
         uint64_t i = lo, j = d - lo;
+        BQ_CHECK(i <= na && j <= nb && pair0 + na + nb <= len);
         const uint64_t end = (o + MERGE_IPT) < b1 ? (o + MERGE_IPT) : b1;
         for (uint64_t r = o; r < end; r++) {
             const bool takeA = j >= nb || (i < na && !(KT::key(B[j]) < KT::key(A[i])));

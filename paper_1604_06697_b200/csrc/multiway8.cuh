@@ -307,6 +307,7 @@ __global__ void __launch_bounds__(NT + 32, MINB) k_mw8_scatter(const MwParams<KT
 #pragma unroll
             for (uint32_t c = 0; c < IPT; c++) {
                 const uint32_t v = ypk[c];
+                BQ_CHECK((v >> 31) || (v & 0xffff) + sm.delta[par ^ 1][(v >> 16) & 0x7fff] < SM::TILE + MW8 * 8 + 16);
                 if (!(v >> 31)) sm.out[(v & 0xffff) + sm.delta[par ^ 1][(v >> 16) & 0x7fff]] = y[c];
             }
             if (P.aligned) fence_proxy_async_smem();

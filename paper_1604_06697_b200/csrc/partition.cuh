@@ -167,6 +167,7 @@ struct PostParams {
     uint32_t copy_cap;
     // set to 1 when a leaf list would overflow (the call then fails)
     uint32_t *overflow;
+    uint32_t nseg_cap, ntile_cap;   // list capacities (checked with -DBQ_CHECKS)
 };
 
 template <class KT>
@@ -353,6 +354,7 @@ __device__ __forceinline__ void emit_children(const PostParams<KT> &Q, int nch, 
         } else if (kind == C_FALLBACK) {
             const uint32_t fi = atomicAdd(Q.fallback_count, 1u);
             atomicAdd(&post_stats().nfallback, 1u);
+            BQ_CHECK(fi < Q.nseg_cap);
             Q.fallback[fi] = Leaf{cb[c], len, cp, 0};
         } else if (kind == C_BAND) {
             atomicAdd(&post_stats().band_child, (unsigned long long)len);
@@ -377,12 +379,14 @@ __device__ __forceinline__ void emit_children(const PostParams<KT> &Q, int nch, 
                 ch.tile_base = atomicAdd(&C->ntiles_next, ch.ntiles);
                 atomicMax(&post_stats().maxtiles, ch.ntiles);
                 ci = atomicAdd(&C->nseg_next, 1u);
+                BQ_CHECK(ci < Q.nseg_cap && ch.tile_base + ch.ntiles <= Q.ntile_cap);
                 Q.next_segs[ci] = ch;
                 Q.next_cursor[ci] = 0;
                 Q.next_ecursor[ci] = 0;
             } else {
                 ch.tile_base = atomicAdd(&C->nmtiles_next, ch.ntiles);
                 ci = atomicAdd(&C->nmseg_next, 1u);
+                BQ_CHECK(ci < Q.nseg_cap && ch.tile_base + ch.ntiles <= Q.ntile_cap);
                 MSeg<KT> &m = Q.next_msegs[ci];
                 m.s = ch;
 #pragma unroll

@@ -266,6 +266,7 @@ __global__ void __launch_bounds__(NT + 32, MINB) k_part_fast(const PassParams<KT
             const unsigned long long old = sm.offs[par ^ 1];
             const uint64_t lbase = p_b + (uint32_t)old;                 // first < destination
             const uint64_t g0 = p_e - (uint32_t)(old >> 32) - p_TG;      // lowest > destination
+            BQ_CHECK(lbase >= p_b && lbase + p_TL <= p_e && g0 >= p_b && g0 + p_TG <= p_e);
             const uint32_t aL = (uint32_t)(lbase % VW);
             const uint32_t oG = (aL + p_TL + VW - 1) / VW * VW;
             const uint32_t aG = (uint32_t)(g0 % VW);
@@ -285,6 +286,7 @@ __global__ void __launch_bounds__(NT + 32, MINB) k_part_fast(const PassParams<KT
                     gt = p_pk < kk;
                 }
                 const uint32_t idx = lt ? rl : rg;
+                BQ_CHECK(!(lt || gt) || idx < TILE + 16);
                 if (lt || gt) sm.out[idx] = y[c];
                 rl += lt;
                 rg += gt;

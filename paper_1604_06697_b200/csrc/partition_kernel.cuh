@@ -463,6 +463,7 @@ __global__ void __launch_bounds__(NT + (ORDERED ? 96 : 64), MINB) k_partition(co
 #pragma unroll
         for (uint32_t c = 0; c < IPT; c++) {
             const bool lt = (ltb >> c) & 1, gt = (gtb >> c) & 1;
+            BQ_CHECK(!(lt || gt) || (lt ? rl : rg) < sizeof(sm.out) / sizeof(sm.out[0]));
             if (lt || gt) sm.out[lt ? rl : rg] = x[c];
             rl += lt;
             rg -= gt;
