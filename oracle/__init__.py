@@ -70,6 +70,8 @@ def _load():
                     f.restype, f.argtypes = None, [vp, ll]
         lib.bq_oracle_depth_limit.restype = ctypes.c_int
         lib.bq_oracle_depth_limit.argtypes = [ll]
+        lib.bq_oracle_splitmix64_mix.restype = ctypes.c_uint64
+        lib.bq_oracle_splitmix64_mix.argtypes = [ctypes.c_uint64]
         _lib = lib
     return _lib
 
@@ -156,3 +158,8 @@ def std_sort(a: np.ndarray, inplace: bool = False):
 
 def depth_limit(n: int) -> int:
     return int(_load().bq_oracle_depth_limit(n))
+
+
+def splitmix64_mix(z: int) -> int:
+    """The oracle's SplitMix64 output function (R19), for its known-answer test."""
+    return int(_load().bq_oracle_splitmix64_mix(z))

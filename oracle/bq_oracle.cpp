@@ -501,4 +501,8 @@ uint64_t bq_oracle_pivot_rec32(const Rec32 *A, long long n, int rule) {
 /* Default depth limit of the paper for n (R4), exported for tests. */
 int bq_oracle_depth_limit(long long n) { return n >= 1 ? 2 * ilog2(n) + 3 : 0; }
 
+/* the SplitMix64 output function used by SAMPLE64 (R19), exported for its
+ * known-answer test (tests/test_oracle.py) */
+uint64_t bq_oracle_splitmix64_mix(uint64_t z) { return splitmix64_mix(z); }
+
 } // extern "C"

@@ -619,3 +619,40 @@ def test_host_loop_matches_graph(B, kind):
     check_sorted_equal(kind, to_host(t2, a), a)
     assert s1["levels"] == s2["levels"] and s1["element_passes"] == s2["element_passes"]
     assert s2["partition_ms"] > 0
+
+
+def mo3_adversary(n, S, depth):
+    """int32 keys on which the GPU's Mo3 rule with the ordered layout ([< in
+    input order | = | > in reverse input order], bq.h) picks, in every level,
+    the second smallest key of the segment as pivot: the samples at positions
+    b, b + len/2 get the two smallest remaining values, the one at e - 1 a
+    larger one, so each level peels two keys off — a median-of-3 killer
+    (Introsort's motivation) for this partition."""
+    val = np.full(n, -1, dtype=np.int64)
+    seg = np.arange(n)
+    nxt = 0
+    for _ in range(depth + 1):
+        L = len(seg)
+        if L <= S:
+            break
+        val[seg[0]], val[seg[L // 2]] = nxt, nxt + 1
+        nxt += 2
+        keep = np.ones(L, dtype=bool)
+        keep[0] = keep[L // 2] = False
+        seg = seg[keep][::-1]
+    rest = np.flatnonzero(val < 0)
+    val[rest] = nxt + np.arange(len(rest))
+    return val.astype(np.int32)
+
+
+def test_depth_cap_natural_trigger(B):
+    """a9 fires without a forced limit: on a Mo3 killer the recursion reaches
+    the Introsort depth 2 floor(log2 n) + 3 and the capped
+    segment is finished by the fallback; the output equals the oracle's."""
+    n = 1 << 17
+    a = mo3_adversary(n, LEAF["i32"], oracle.depth_limit(n))
+    t = to_dev(a)
+    st = B.bq_sort_ex(t, pivot_rule=B.BQ_PIVOT_MO3, ordered=True, ways=2)
+    assert st["fallback_segments"] >= 1
+    assert st["levels"] >= oracle.depth_limit(n)
+    check_sorted_equal("i32", to_host(t, a), a)

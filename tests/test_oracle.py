@@ -357,3 +357,18 @@ def test_sort_patterns(name):
         out, st = oracle.sort(a, stats=True)
         assert np.array_equal(out, np.sort(a))
         assert st["max_stack"] <= int(np.ceil(np.log2(n))) + 1
+
+
+def test_oracle_splitmix64_known_answer():
+    """The oracle's own SplitMix64 output function (SAMPLE64's sample
+    positions, R19): the published first output of SplitMix64 from state 0
+    (Vigna, splitmix64.c: 0xE220A8397B1DCDAF), mix(0) = 0, and agreement with
+    the independent copy in bqgen (whose stream is mix(mix(seed) + (i+1)*gamma))."""
+    import bqgen
+    g, m64 = 0x9E3779B97F4A7C15, (1 << 64) - 1
+    assert oracle.splitmix64_mix(g) == 0xE220A8397B1DCDAF
+    assert oracle.splitmix64_mix(0) == 0
+    for seed in (0, 1, 7, 12345):
+        s = oracle.splitmix64_mix(seed)
+        for i in range(4):
+            assert bqgen.u64_at(seed, i) == oracle.splitmix64_mix((s + (i + 1) * g) & m64)
