@@ -118,7 +118,11 @@ def test_options_struct_layout():
     assert ctypes.sizeof(b.bq_sort_options) == 4 * n_fields == 32
     assert [f for f, _ in b.bq_sort_options._fields_][:7] == ["pivot_rule", "depth_limit", "timing", "ordered",
                                                                "ways", "records", "subtree"]
-    assert ctypes.sizeof(b.bq_sort_stats) == 72
+    body = src[src.index("typedef struct {\n    uint32_t levels;"):src.index("} bq_sort_stats;")]
+    size = {"uint32_t": 4, "uint64_t": 8, "double": 8}
+    fields = re.findall(r"^\s*(uint32_t|uint64_t|double) (\w+);", body, re.M)
+    assert [f for f, _ in b.bq_sort_stats._fields_] == [nm for _, nm in fields]
+    assert ctypes.sizeof(b.bq_sort_stats) == sum(size[t] for t, _ in fields) == 88
 
 
 def test_binding_refuses_ambiguous_int64():
