@@ -8,37 +8,40 @@ namespace bq {
 // Records are large elements with cheap comparisons: every
 // partition pass of the direct path moves 32 bytes per record.  Here the
 // passes move 16-byte (key, position) pairs, and each record moves once, in a
-// final gather.  Workspace: [pairs 16n | pair-sort workspace (its scratch
-// first) | gather indices 4n]; after the pair sort the gather target is the
-// first 32n bytes (the pairs and the pair scratch, no longer needed).
-__global__ void k_ki_extract(const Rec32 *r, KeyIdx16 *p, uint64_t n) {
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
-        p[i] = KeyIdx16{r[i].key, i};
+// final gather.  Workspace: [pairs 16n | pair-sort workspace | records 32n]:
+// the extraction reads every record once and also copies it aside, so the
+// gather reads the copy and writes the user buffer directly.
+__global__ void k_ki_extract(const Rec32 *r, KeyIdx16 *p, Rec32 *copy, uint64_t n) {
+    const uint4 *r4 = reinterpret_cast<const uint4 *>(r);
+    uint4 *c4 = reinterpret_cast<uint4 *>(copy);
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint4 v0 = __ldcs(r4 + 2 * i), v1 = __ldcs(r4 + 2 * i + 1);
+        p[i] = KeyIdx16{(uint64_t)v0.x | ((uint64_t)v0.y << 32), i};
+        c4[2 * i] = v0;
+        c4[2 * i + 1] = v1;
+    }
 }
-__global__ void k_ki_index(const KeyIdx16 *p, uint32_t *idx, uint64_t n) {
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
-        idx[i] = (uint32_t)p[i].idx;
-}
-// the records in sorted order: random 32-byte reads, so each thread keeps
-// U of them in flight (their indices first, then the independent loads)
-__global__ void k_ki_gather(const Rec32 *r, const uint32_t *idx, Rec32 *g, uint64_t n) {
+// the records in sorted order: pair i names the record of rank i; random
+// 32-byte reads of the copy, so each thread keeps U of them in flight (their
+// positions first, then the independent loads)
+__global__ void k_ki_gather(const Rec32 *copy, const KeyIdx16 *p, Rec32 *out, uint64_t n) {
     constexpr int U = 8;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    const uint4 *r4 = reinterpret_cast<const uint4 *>(r);
-    uint4 *g4 = reinterpret_cast<uint4 *>(g);
+    const uint4 *r4 = reinterpret_cast<const uint4 *>(copy);
+    uint4 *g4 = reinterpret_cast<uint4 *>(out);
     for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += stride * U) {
-        uint32_t k[U];
+        uint64_t k[U];
 #pragma unroll
         for (int u = 0; u < U; u++) {
             const uint64_t j = i0 + u * stride;
-            k[u] = j < n ? __ldcs(idx + j) : 0u;
+            k[u] = j < n ? __ldcs(&p[j].idx) : 0u;
         }
         uint4 v[U][2];
 #pragma unroll
         for (int u = 0; u < U; u++) {
             if (i0 + u * stride < n) {
-                v[u][0] = __ldg(r4 + 2 * (uint64_t)k[u]);
-                v[u][1] = __ldg(r4 + 2 * (uint64_t)k[u] + 1);
+                v[u][0] = __ldg(r4 + 2 * k[u]);
+                v[u][1] = __ldg(r4 + 2 * k[u] + 1);
             }
         }
 #pragma unroll
@@ -54,15 +57,15 @@ __global__ void k_ki_gather(const Rec32 *r, const uint32_t *idx, Rec32 *g, uint6
 
 namespace detail {
 struct KiLayout {
-    size_t pairs, pws, pws_bytes, idx, total;
+    size_t pairs, pws, pws_bytes, copy, total;
 };
 static KiLayout ki_layout(size_t n) {
     KiLayout L;
     L.pairs = 0;
     L.pws = align_up(n * sizeof(KeyIdx16), 256);
     L.pws_bytes = ws_pair(n);
-    L.idx = align_up(L.pws + L.pws_bytes, 256);
-    L.total = align_up(L.idx + n * sizeof(uint32_t), 256);
+    L.copy = align_up(L.pws + L.pws_bytes, 256);
+    L.total = align_up(L.copy + n * sizeof(Rec32), 256);
     return L;
 }
 // records below this size are one leaf (or a few): the direct path
@@ -74,19 +77,15 @@ static bq_status sort_rec_ki(Rec32 *data, size_t n, const bq_sort_options *opt, 
     if (wsb < L.total) return set_error(BQ_ERR_WORKSPACE, "workspace %zu B < required %zu B", wsb, L.total);
     char *w = static_cast<char *>(ws);
     KeyIdx16 *pairs = reinterpret_cast<KeyIdx16 *>(w + L.pairs);
-    uint32_t *idx = reinterpret_cast<uint32_t *>(w + L.idx);
-    Rec32 *gath = reinterpret_cast<Rec32 *>(w);
+    Rec32 *copy = reinterpret_cast<Rec32 *>(w + L.copy);
     const uint32_t grid = 148 * 8;
-    k_ki_extract<<<grid, 256, 0, s>>>(data, pairs, n);
+    k_ki_extract<<<grid, 256, 0, s>>>(data, pairs, copy, n);
     BQ_CK_LAUNCH();
     bq_status r = sort_pair(pairs, n, opt, st, w + L.pws, L.pws_bytes, s);
     if (r != BQ_OK) return r;
-    k_ki_index<<<grid, 256, 0, s>>>(pairs, idx, n);
+    k_ki_gather<<<grid, 256, 0, s>>>(copy, pairs, data, n);
     BQ_CK_LAUNCH();
-    k_ki_gather<<<grid, 256, 0, s>>>(data, idx, gath, n);
-    BQ_CK_LAUNCH();
-    BQ_CK(cudaMemcpyAsync(data, gath, n * sizeof(Rec32), cudaMemcpyDeviceToDevice, s));
-    if (st) st->kernel_launches += 3;
+    if (st) st->kernel_launches += 2;
     return BQ_OK;
 }
 

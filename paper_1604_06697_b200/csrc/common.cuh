@@ -241,7 +241,10 @@ struct alignas(16) Leaf {
 constexpr int MAX_LEVELS = 128;   // control blocks of a sort's level loop (depth limit < MAX_LEVELS - 3)
 // levels per iteration of the level loop (driver.cuh), and the leaf set of the
 // batch before the one starting at `level`
-constexpr uint32_t LOOP_BATCH = 4;
+#ifndef BQ_LOOP_BATCH
+#define BQ_LOOP_BATCH 4
+#endif
+constexpr uint32_t LOOP_BATCH = BQ_LOOP_BATCH;
 __host__ __device__ inline uint32_t loop_prev_set(uint32_t level) { return (level / LOOP_BATCH + 1) & 1; }
 
 // Per-level control block.  One per level, zeroed once per sort, so no

@@ -100,6 +100,12 @@ __device__ __forceinline__ bool e_less(uint64_t a, uint64_t b) { return a < b; }
 __device__ __forceinline__ bool e_less(const RecKI &a, const RecKI &b) {
     return a.k < b.k || (a.k == b.k && a.i < b.i);
 }
+__device__ __forceinline__ int32_t e_min(int32_t a, int32_t b) { return min(a, b); }
+__device__ __forceinline__ int32_t e_max(int32_t a, int32_t b) { return max(a, b); }
+__device__ __forceinline__ uint64_t e_min(uint64_t a, uint64_t b) { return a < b ? a : b; }
+__device__ __forceinline__ uint64_t e_max(uint64_t a, uint64_t b) { return a < b ? b : a; }
+__device__ __forceinline__ RecKI e_min(const RecKI &a, const RecKI &b) { return e_less(b, a) ? b : a; }
+__device__ __forceinline__ RecKI e_max(const RecKI &a, const RecKI &b) { return e_less(b, a) ? a : b; }
 __device__ __forceinline__ void ce(int32_t &a, int32_t &b) {
     const int32_t lo = min(a, b), hi = max(a, b);
     a = lo;
@@ -232,6 +238,7 @@ __device__ __forceinline__ typename LeafTraits<KT>::E leaf_pad() {
 template <class E, int IPT, class PL>
 __device__ __forceinline__ void store_run(const PL &pl, const E (&x)[IPT], int cnt, int base, int dir) {
     BQ_CHECK(cnt >= 0 && cnt <= IPT);
+    if (cnt == 0) return;
     if (cnt == IPT) {
         const bool rev = dir < 0;
         const uint32_t c0 = pl.cur(rev ? base - (IPT - 1) : base);
@@ -380,17 +387,25 @@ __device__ __forceinline__ void leaf_body(const LeafParams<KT> &P, const Leaf lf
                 BQ_CHECK(lo >= 0 && lo <= na && d - lo >= 0 && d - lo <= nb && a0 + tot <= len);
                 uint32_t pa = ca + (uint32_t)(lo * PL::STEP);
                 uint32_t pb = pl.cur(off + a0 + tot - 1 - (d - lo));
-                E ka = pl.ldc(pa), kb = pl.ldc(pb);
+                // serial merge: out = min(head kept, head just loaded), keep the
+                // max, advance the side of the output (tA: side A)
+                const E ka = pl.ldc(pa), kb = pl.ldc(pb);
+                bool tA = !e_less(kb, ka);
+                x[0] = e_min(ka, kb);
+                E hv = e_max(ka, kb), nv;
+                if (tA) pa += (uint32_t)PL::STEP;
+                else pb -= (uint32_t)PL::STEP;
+                nv = pl.ldc(tA ? pa : pb);
 #pragma unroll
-                for (int k = 0; k < IPT; k++) {
-                    const bool p = e_less(kb, ka);
-                    x[k] = p ? kb : ka;
+                for (int k = 1; k < IPT; k++) {
+                    x[k] = e_min(hv, nv);
+                    const bool keep_side = e_less(nv, hv);   // the output is nv: same side again
+                    hv = e_max(hv, nv);
+                    tA = tA == keep_side;
                     if (k + 1 < IPT) {
-                        pb -= p ? (uint32_t)PL::STEP : 0u;
-                        pa += p ? 0u : (uint32_t)PL::STEP;
-                        const E nv = pl.ldc(p ? pb : pa);
-                        if (p) kb = nv;
-                        else ka = nv;
+                        if (tA) pa += (uint32_t)PL::STEP;
+                        else pb -= (uint32_t)PL::STEP;
+                        nv = pl.ldc(tA ? pa : pb);
                     }
                 }
                 if (!fin && (g & 1)) {
