@@ -361,6 +361,7 @@ __device__ __forceinline__ uint32_t mw_match(uint32_t v0, uint32_t v1, uint32_t 
 // histogram.
 template <class KT, int NT, int IPT, int STAGES, int MINB>
 __global__ void __launch_bounds__(NT + 32, MINB) k_mw_count(const MwParams<KT> Pin) {
+    if (const LevelCtrl *pv = loop_prev_ctrl(Pin.lp)) if (pv->nmseg_next == 0) return;
     __shared__ MwParams<KT> sP;
     const MwParams<KT> &P = cta_params(Pin, sP);
     using SM = MwSmem<KT, NT, IPT, STAGES>;
@@ -426,6 +427,7 @@ __global__ void __launch_bounds__(NT + 32, MINB) k_mw_count(const MwParams<KT> P
 // ---- k_mw_scan: bucket starts and cursor reset, one warp per segment ---------------
 template <class KT>
 __global__ void k_mw_scan(const MwParams<KT> Pin) {
+    if (const LevelCtrl *pv = loop_prev_ctrl(Pin.lp)) if (pv->nmseg_next == 0) return;
     __shared__ MwParams<KT> sP;
     const MwParams<KT> &P = cta_params(Pin, sP);
     const uint32_t lane = threadIdx.x & 31;
@@ -450,6 +452,7 @@ __global__ void k_mw_scan(const MwParams<KT> Pin) {
 // ---- k_mw_scatter -------------------------------------------------------------
 template <class KT, int NT, int IPT, int STAGES, int MINB>
 __global__ void __launch_bounds__(NT + 32, MINB) k_mw_scatter(const MwParams<KT> Pin) {
+    if (const LevelCtrl *pv = loop_prev_ctrl(Pin.lp)) if (pv->nmseg_next == 0) return;
     __shared__ MwParams<KT> sP;
     const MwParams<KT> &P = cta_params(Pin, sP);
     using T = typename KT::T;

@@ -118,6 +118,7 @@ __device__ __forceinline__ void mw8_widen(uint64_t c, uint32_t (&q)[MW8 / 2]) {
 // ---- k_mw8_count -----------------------------------------------------------------
 template <class KT, int NT, int IPT, int STAGES, int MINB>
 __global__ void __launch_bounds__(NT + 32, MINB) k_mw8_count(const MwParams<KT> Pin) {
+    if (const LevelCtrl *pv = loop_prev_ctrl(Pin.lp)) if (pv->nmseg_next == 0) return;
     __shared__ MwParams<KT> sP;
     const MwParams<KT> &P = cta_params(Pin, sP);
     using K = typename KT::K;
@@ -184,6 +185,7 @@ __global__ void __launch_bounds__(NT + 32, MINB) k_mw8_count(const MwParams<KT> 
 // ---- k_mw8_scatter ---------------------------------------------------------------
 template <class KT, int NT, int IPT, int STAGES, int MINB>
 __global__ void __launch_bounds__(NT + 32, MINB) k_mw8_scatter(const MwParams<KT> Pin) {
+    if (const LevelCtrl *pv = loop_prev_ctrl(Pin.lp)) if (pv->nmseg_next == 0) return;
     __shared__ MwParams<KT> sP;
     const MwParams<KT> &P = cta_params(Pin, sP);
     using T = typename KT::T;

@@ -92,6 +92,17 @@ __device__ __forceinline__ uint32_t pass_ntiles(const PassParams<KT> &P) {
 // Kernels of the loop keep their parameters in shared memory, resolved once
 // per CTA by thread 0 (a per-thread copy of a modified by-value parameter
 // struct would live in local memory):  `const auto &P = cta_params(Pin, sP);`
+// the level's control blocks before any parameter copy: loop kernels of a
+// level without work (the trailing levels of a batch) exit at once
+template <class KT>
+__device__ __forceinline__ const LevelCtrl *loop_prev_ctrl(const LoopPtrs<KT> &lp) {
+    return lp.level ? loop_prev(lp, *lp.level) : nullptr;
+}
+template <class KT>
+__device__ __forceinline__ const LevelCtrl *loop_cur_ctrl(const LoopPtrs<KT> &lp) {
+    return lp.level ? lp.ctrl + *lp.level : nullptr;
+}
+
 template <class PP>
 __device__ __forceinline__ const PP &cta_params(const PP &in, PP &sm) {
     if (threadIdx.x == 0) {
@@ -420,6 +431,7 @@ __device__ __forceinline__ void post_segment(const PostParams<KT> &Q, uint32_t s
 
 template <class KT, int NT>
 __global__ void __launch_bounds__(NT) k_post(const PostParams<KT> Qin) {
+    if (const LevelCtrl *pv = loop_prev_ctrl(Qin.pass.lp)) if (pv->nseg_next == 0) return;
     __shared__ PostParams<KT> sQ;
     const PostParams<KT> &Q = cta_params(Qin, sQ);
     const uint32_t nseg = Q.nseg_dev ? *Q.nseg_dev : Q.nseg;
@@ -498,6 +510,7 @@ __device__ __forceinline__ void post_segment(const PostParams<KT> &Q, uint32_t s
 // the other buffer, from where phase 1 copies them into the final buffer.
 template <class KT, int NT>
 __global__ void __launch_bounds__(NT) k_fill(const PostParams<KT> Qin, int phase) {
+    if (const LevelCtrl *cv = loop_cur_ctrl(Qin.pass.lp)) if (cv->nbig == 0) return;
     using T = typename KT::T;
     using K = typename KT::K;
     constexpr uint32_t TILE = (uint32_t)tile_elems<KT>();
@@ -564,6 +577,7 @@ __global__ void __launch_bounds__(NT) k_init_root(PostParams<KT> Q, uint32_t n) 
 template <class KT, int NT>
 __global__ void __launch_bounds__(NT) k_post_mw(const PostParams<KT> Qin) {
     __shared__ uint32_t cb[MW_K], cl[MW_K];
+    if (const LevelCtrl *pv = loop_prev_ctrl(Qin.pass.lp)) if (pv->nmseg_next == 0) return;
     __shared__ PostParams<KT> sQ;
     const PostParams<KT> &Q = cta_params(Qin, sQ);
     const uint32_t nseg = *Q.mw.nseg_dev;

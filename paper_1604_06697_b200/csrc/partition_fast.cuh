@@ -59,6 +59,7 @@ constexpr int fast_smem_bytes() {
 
 template <class KT, int NT, int IPT, int STAGES, int MINB>
 __global__ void __launch_bounds__(NT + 32, MINB) k_part_fast(const PassParams<KT> Pin) {
+    if (const LevelCtrl *pv = loop_prev_ctrl(Pin.lp)) if (pv->ntiles_next == 0) return;
     __shared__ PassParams<KT> sP;
     const PassParams<KT> &P = cta_params(Pin, sP);
     using T = typename KT::T;

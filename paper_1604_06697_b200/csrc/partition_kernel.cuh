@@ -85,6 +85,7 @@ struct TileGeom {
 
 template <class KT, int NT, int IPT, int STAGES, int MINB, bool ORDERED>
 __global__ void __launch_bounds__(NT + (ORDERED ? 96 : 64), MINB) k_partition(const PassParams<KT> Pin) {
+    if (const LevelCtrl *pv = loop_prev_ctrl(Pin.lp)) if (pv->ntiles_next == 0) return;
     __shared__ PassParams<KT> sP;
     const PassParams<KT> &P = cta_params(Pin, sP);
     using T = typename KT::T;
