@@ -498,6 +498,46 @@ __device__ typename KT::K sample64_pivot_warp_dup(const typename KT::T *buf, uin
     return piv;
 }
 
+// The duplicate check "dc" at the leaf boundary: the lower median
+// of the 64-key sample of a segment and the number of distinct keys in the
+// sample (whole warp).
+template <class KT>
+__device__ typename KT::K sample64_median_distinct(const typename KT::T *buf, uint32_t b, uint32_t len, uint32_t lane,
+                                                    uint32_t *distinct) {
+    using K = typename KT::K;
+    K v[2];
+#pragma unroll
+    for (int r = 0; r < 2; r++) v[r] = load_key<KT>(buf, sample64_pos(b, len, lane + 32 * r));
+#pragma unroll
+    for (int m = 1; m <= 6; m++) {
+#pragma unroll
+        for (int bb = m - 1; bb >= 0; bb--) {
+            if (bb == 5) {
+                const K lo = v[1] < v[0] ? v[1] : v[0], hi = v[1] < v[0] ? v[0] : v[1];
+                v[0] = lo;
+                v[1] = hi;
+                continue;
+            }
+#pragma unroll
+            for (int r = 0; r < 2; r++) {
+                const uint32_t i = lane + 32 * r;
+                const K p = __shfl_xor_sync(0xffffffffu, v[r], 1 << bb);
+                const bool lower = ((lane >> bb) & 1) == 0;
+                const bool asc = m == 6 || ((i >> m) & 1) == 0;
+                v[r] = (lower == asc) ? (p < v[r] ? p : v[r]) : (v[r] < p ? p : v[r]);
+            }
+        }
+    }
+    // sorted: index i = lane + 32 r; a new value starts where it differs from i - 1
+    const K prev0 = __shfl_up_sync(0xffffffffu, v[0], 1);
+    const K last0 = __shfl_sync(0xffffffffu, v[0], 31);
+    const K prev1 = __shfl_up_sync(0xffffffffu, v[1], 1);
+    const bool n0 = lane == 0 || prev0 != v[0];
+    const bool n1 = lane == 0 ? last0 != v[1] : prev1 != v[1];
+    *distinct = __popc(__ballot_sync(0xffffffffu, n0)) + __popc(__ballot_sync(0xffffffffu, n1));
+    return __shfl_sync(0xffffffffu, v[0], 31);
+}
+
 // Pivot of buf[b, b+len) by `rule`, computed by a whole warp (all 32 lanes
 // must call it; every lane gets the result).  *dup (if non-null) tells whether
 // another key of the rule's sample equals the pivot.

@@ -67,12 +67,15 @@ Layout<KT> make_layout(size_t n) {
     constexpr size_t TILE = tile_elems<KT>();
     constexpr size_t S = Tune<KT>::LEAF;
     Layout<KT> L;
-    L.max_segs = n / (S + 1) + 2;                 // segments > S are disjoint
+    // segments of a level are disjoint and longer than S, or (the duplicate
+    // check, keys) at least BQ_DC_MIN long
+    const size_t seg_min = KT::is_record ? S + 1 : (S + 1 < (size_t)BQ_DC_MIN ? S + 1 : (size_t)BQ_DC_MIN);
+    L.max_segs = n / seg_min + 2;
     L.max_tiles = n / TILE + 2 * L.max_segs + 2;
     L.max_fb = n / (S + 1) + 2;
     // the leaf lists of one level (set level & 1): at most kmax children per
     // segment; set 0's class-0 list also holds the fallback's chunks at the end
-    const size_t per_level = L.max_segs * (mw_capable<KT>() ? MW_K : 2);
+    const size_t per_level = (mw_capable<KT>() ? MW_K * (n / (S + 1) + 2) : 0) + 2 * L.max_segs;
     L.max_leaves = per_level;
     if (L.max_leaves < n / S + L.max_fb + 2) L.max_leaves = n / S + L.max_fb + 2;
     size_t off = 0;

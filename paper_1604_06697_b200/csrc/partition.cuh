@@ -275,6 +275,17 @@ __device__ __forceinline__ void post_stats_flush(const PostParams<KT> &Q) {
 #ifndef BQ_LEAF_AWARE
 #define BQ_LEAF_AWARE 1
 #endif
+// duplicate check at the leaf boundary (keys): a leaf-sized child of at least
+// BQ_DC_MIN keys whose 64-key sample holds at most BQ_DC_DISTINCT distinct
+// keys is partitioned three-way once more (its repeated keys leave as an
+// equal band) instead of merge-sorted; a pass costs a fraction of a leaf sort
+// per key (R23)
+#ifndef BQ_DC_MIN
+#define BQ_DC_MIN 2048
+#endif
+#ifndef BQ_DC_DISTINCT
+#define BQ_DC_DISTINCT 8
+#endif
 #ifndef BQ_LA_DIV
 #define BQ_LA_DIV 16   // margin len / 16: one standard deviation of the sample's rank error
 #endif
@@ -300,7 +311,17 @@ __device__ __forceinline__ void emit_children(const PostParams<KT> &Q, int nch, 
         uint32_t kind = C_NONE, mode = 0;
         if (len == 0) kind = C_NONE;
         else if (h == 2) kind = C_BAND;
-        else if (len <= Q.leaf_max) kind = C_LEAF;
+        else if (len <= Q.leaf_max) {
+            kind = C_LEAF;
+            if constexpr (!KT::is_record) if (len >= BQ_DC_MIN && (int)cd < Q.depth_limit) {
+                uint32_t distinct = 64;
+                const K piv = sample64_median_distinct<KT>(cbuf, cb[c], len, lane, &distinct);
+                if (distinct <= BQ_DC_DISTINCT) {
+                    kind = C_BIN;
+                    if (lane == 0) s_piv[c] = (uint64_t)piv;
+                }
+            }
+        }
         else if ((int)cd >= Q.depth_limit) kind = C_FALLBACK;
         else if (h == 1) {
             kind = C_BIN;

@@ -656,3 +656,21 @@ def test_depth_cap_natural_trigger(B):
     assert st["fallback_segments"] >= 1
     assert st["levels"] >= oracle.depth_limit(n)
     check_sorted_equal("i32", to_host(t, a), a)
+
+
+@pytest.mark.parametrize("kind", ["i32", "u64", "f64"])
+def test_duplicate_check_at_leaf_boundary(B, kind):
+    """R23: a leaf-sized segment whose 64-key sample holds few distinct keys is
+    partitioned three-way once more (its repeated keys become an equal band)
+    instead of being merge-sorted: leaves of 3 distinct values; the output
+    equals the oracle's and most keys were placed by the band fill."""
+    S = LEAF[kind]
+    n = 6 * S + 11
+    base = make(kind, n, seed=31)
+    vals = np.sort(base[:3]) if kind != "u64" else np.sort(base[:3])
+    rng = np.random.default_rng(5)
+    a = vals[rng.integers(0, 3, size=n)]
+    t = to_dev(a)
+    st = B.bq_sort_ex(t, ways=2)
+    check_sorted_equal(kind, to_host(t, a), a)
+    assert st["band_elements"] >= n // 2
