@@ -239,13 +239,16 @@ struct alignas(16) Leaf {
 };
 
 constexpr int MAX_LEVELS = 128;   // control blocks of a sort's level loop (depth limit < MAX_LEVELS - 3)
-// levels per iteration of the level loop (driver.cuh), and the leaf set of the
-// batch before the one starting at `level`
+// levels per iteration of the level loop (driver.cuh): at most LOOP_BATCH;
+// sorts of up to LOOP_SMALL_N keys use LOOP_BATCH_SMALL (fewer trailing empty
+// levels).  Leaves of a batch go to list set (level / batch) & 1, kept in
+// LoopMisc::set by k_level_end.
 #ifndef BQ_LOOP_BATCH
 #define BQ_LOOP_BATCH 4
 #endif
 constexpr uint32_t LOOP_BATCH = BQ_LOOP_BATCH;
-__host__ __device__ inline uint32_t loop_prev_set(uint32_t level) { return (level / LOOP_BATCH + 1) & 1; }
+constexpr uint32_t LOOP_BATCH_SMALL = 2;
+constexpr size_t LOOP_SMALL_N = (size_t)1 << 22;
 
 // Per-level control block.  One per level, zeroed once per sort, so no
 // counter is reused within a call.

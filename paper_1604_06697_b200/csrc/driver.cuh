@@ -218,7 +218,7 @@ bq_status launch_partition(const PassParams<KT> &P, cudaStream_t s) {
 
 template <class KT>
 bq_status launch_leaves(int cls, const LeafParams<KT> &LP, uint32_t count, cudaStream_t s) {
-    if (count == 0 && LP.count_dev == nullptr && LP.level == nullptr) return BQ_OK;   // count 0 + a device count: persistent grid
+    if (count == 0 && LP.count_dev == nullptr && LP.set == nullptr) return BQ_OK;   // count 0 + a device count: persistent grid
     BQ_CK(launch_leaf_class<KT>(cls, LP, count, s));
     return BQ_OK;
 }
@@ -570,6 +570,7 @@ struct SortPlan {
     uint32_t *tprefix;
     FbState *fbst;
     int rule, depth_limit, ordered, ways, aligned;
+    uint32_t batch;       // levels per loop iteration
     PostParams<KT> Q;     // k_post / k_fill / k_post_mw of a level (dynamic)
     PassParams<KT> P;     // the binary partition of a level (dynamic)
     MwParams<KT> MP;      // the multiway kernels of a level (dynamic)
@@ -592,6 +593,7 @@ bq_status make_plan(SortPlan<KT> &pl, typename KT::T *data, size_t n, void *ws, 
     pl.ordered = ordered;
     pl.ways = ways;
     pl.aligned = aligned16(pl.user) && aligned16(pl.scratch);
+    pl.batch = n <= LOOP_SMALL_N ? LOOP_BATCH_SMALL : LOOP_BATCH;
     pl.ctrl = reinterpret_cast<LevelCtrl *>(w + L.ctrl);
     pl.root = pl.ctrl + MAX_LEVELS;
     pl.misc = reinterpret_cast<LoopMisc *>(w + L.misc);
@@ -604,6 +606,7 @@ bq_status make_plan(SortPlan<KT> &pl, typename KT::T *data, size_t n, void *ws, 
     pl.fbst = reinterpret_cast<FbState *>(w + L.fbst);
     LoopPtrs<KT> &lp = pl.lp;
     lp.level = &pl.misc->level;
+    lp.set = &pl.misc->set;
     for (int p = 0; p < 2; p++) {
         lp.segs[p] = reinterpret_cast<Seg *>(w + L.segs[p]);
         lp.tile_map[p] = reinterpret_cast<uint32_t *>(w + L.tile_map[p]);
@@ -678,7 +681,7 @@ bq_status make_plan(SortPlan<KT> &pl, typename KT::T *data, size_t n, void *ws, 
     LP.out = pl.user;
     LP.n_total = n;
     LP.aligned = pl.aligned;
-    LP.level = &pl.misc->level;
+    LP.set = &pl.misc->set;
     for (int p = 0; p < 2; p++) {
         LP.lsets[p] = pl.leaves[p];
         LP.csets[p] = pl.misc->leaf_counts[p];
@@ -733,7 +736,7 @@ bq_status enqueue_level(const SortPlan<KT> &pl, cudaStream_t s, int use_cond, cu
 template <class KT>
 bq_status enqueue_level_end(const SortPlan<KT> &pl, cudaStream_t s, int use_cond, cudaGraphConditionalHandle h_loop,
                             cudaGraphConditionalHandle h_fb) {
-    k_level_end<KT><<<1, 1, 0, s>>>(pl.lp, pl.misc, use_cond, h_loop, h_fb);
+    k_level_end<KT><<<1, 1, 0, s>>>(pl.lp, pl.misc, pl.batch, use_cond, h_loop, h_fb);
     BQ_CK_LAUNCH();
     return BQ_OK;
 }
@@ -750,7 +753,7 @@ bq_status enqueue_flush(const SortPlan<KT> &pl, cudaStream_t s) {
         if (st != BQ_OK) return st;
     }
     if (KT::is_record && !pl.ordered) {
-        k_copy_runs<KT, POST_THREADS><<<POST_GRID, POST_THREADS, 0, s>>>(pl.lp, &pl.misc->level, pl.user, pl.scratch);
+        k_copy_runs<KT, POST_THREADS><<<POST_GRID, POST_THREADS, 0, s>>>(pl.lp, &pl.misc->level, pl.user, pl.scratch);   // (set: pl.lp.set)
         BQ_CK_LAUNCH();
     }
     k_flush_reset<<<1, 1, 0, s>>>(pl.misc);
@@ -769,7 +772,7 @@ bq_status enqueue_fb_setup(const SortPlan<KT> &pl, cudaStream_t s, int use_cond,
                                   h);
     BQ_CK_LAUNCH();
     LeafParams<KT> LP = pl.LP;
-    LP.level = nullptr;
+    LP.set = nullptr;
     LP.leaves = chunks;
     LP.count_dev = &pl.fbst->nchunk;
     LP.out_other = 1;   // sorted chunks land in the other buffer
@@ -866,9 +869,9 @@ bq_status build_sort_graph(const SortPlan<KT> &pl, cudaGraphExec_t *ex) {
     BQ_GK(cudaEventRecord(ev[0], cs[1]));
     BQ_GK(cudaStreamWaitEvent(cs[2], ev[0], 0));          // fork
     BQ_GS(enqueue_flush<KT>(pl, cs[2]));                    // the previous batch's leaves
-    for (uint32_t k = 0; k < LOOP_BATCH; k++) {
+    for (uint32_t k = 0; k < pl.batch; k++) {
         BQ_GS(enqueue_level<KT>(pl, cs[1], 1, h_loop, h_fbany, nullptr, nullptr));
-        if (k + 1 < LOOP_BATCH) BQ_GS(enqueue_level_end<KT>(pl, cs[1], 1, h_loop, h_fbany));
+        if (k + 1 < pl.batch) BQ_GS(enqueue_level_end<KT>(pl, cs[1], 1, h_loop, h_fbany));
     }
     BQ_GK(cudaEventRecord(ev[1], cs[2]));
     BQ_GK(cudaStreamWaitEvent(cs[1], ev[1], 0));          // join
@@ -949,7 +952,7 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
         k_single_leaf<<<1, 1, 0, s>>>(pl.leaves[0], (uint32_t)n);
         BQ_CK_LAUNCH();
         LeafParams<KT> LP = pl.LP;
-        LP.level = nullptr;
+        LP.set = nullptr;
         LP.leaves = pl.leaves[0];
         st = launch_leaves<KT>((int)leaf_class<KT>((uint32_t)n), LP, 1, s);
         if (st != BQ_OK) return st;
@@ -1026,17 +1029,18 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
                     mevs.push_back(m1);
                 }
             }
-            if (level % LOOP_BATCH == 0) {   // fork
+            const int B = (int)pl.batch;
+            if (level % B == 0) {   // fork
                 BQ_CKC(cudaEventRecord(efork, s));
                 BQ_CKC(cudaStreamWaitEvent(side, efork, 0));
                 BQ_SKC(enqueue_flush<KT>(pl, side));
                 BQ_CKC(cudaEventRecord(ejoin, side));
             }
             BQ_SKC(enqueue_level<KT>(pl, s, 0, 0, 0, e0, e1, m0, m1));
-            if (level % LOOP_BATCH == LOOP_BATCH - 1) BQ_CKC(cudaStreamWaitEvent(s, ejoin, 0));   // join
+            if (level % B == B - 1) BQ_CKC(cudaStreamWaitEvent(s, ejoin, 0));   // join
             BQ_SKC(enqueue_level_end<KT>(pl, s, 0, 0, 0));
             host_levels = level + 1;
-            if ((level + 1) % LOOP_BATCH == 0) {
+            if ((level + 1) % B == 0) {
                 BQ_CKC(cudaMemcpyAsync(hc.data(), pl.ctrl + level, sizeof(LevelCtrl), cudaMemcpyDeviceToHost, s));
                 BQ_CKC(cudaStreamSynchronize(s));
                 if (hc[0].nseg_next + hc[0].nmseg_next == 0) break;

@@ -49,8 +49,8 @@ struct LeafParams {
     uint64_t n_total;  // length of each data buffer (bounds the TMA reads)
     int aligned;       // both data buffers (and out) 16-byte aligned -> TMA bulk copies
     // level loop: non-null -> the leaves of the previous batch of levels, list
-    // lsets[loop_prev_set(*level)] (+ class offset lcls), count csets[..] + cls
-    const uint32_t *level;
+    // lsets[*set ^ 1] (+ class offset lcls), count csets[..] + cls
+    const uint32_t *set;
     const Leaf *lsets[2];
     const uint32_t *csets[2];
     size_t lcls;
@@ -484,8 +484,8 @@ __global__ void __launch_bounds__(NT, (LeafTraits<KT>::NTMAX / NT) > 0 ? LeafTra
     __shared__ LeafParams<KT> sP;
     if (threadIdx.x == 0) {
         sP = Pin;
-        if (sP.level) {
-            const uint32_t set = loop_prev_set(*sP.level);
+        if (sP.set) {
+            const uint32_t set = *sP.set ^ 1u;
             sP.leaves = sP.lsets[set] + sP.lcls;
             sP.count_dev = sP.csets[set] + sP.cls;
         }

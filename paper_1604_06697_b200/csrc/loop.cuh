@@ -24,7 +24,8 @@ struct LoopMisc {
     uint32_t overflow;                          // a leaf or copy list was full (the call fails)
     uint32_t leaf_counts[2][MAX_LEAF_CLASSES];  // fill of each leaf-class list, by set
     uint32_t copy_count[2];                     // records: finished equal runs to copy, by set
-    uint32_t pad[10];
+    uint32_t set;                               // list set of the current batch of levels
+    uint32_t pad[9];
 };
 static_assert(sizeof(LoopMisc) == 128, "LoopMisc layout");
 
@@ -34,12 +35,13 @@ static_assert(sizeof(LoopMisc) == 128, "LoopMisc layout");
 // end, the IF condition of the fallback); the host-driven mode reads the
 // control blocks instead.
 template <class KT>
-__global__ void k_level_end(LoopPtrs<KT> lp, LoopMisc *misc, int use_cond, cudaGraphConditionalHandle h_loop,
-                            cudaGraphConditionalHandle h_fb) {
+__global__ void k_level_end(LoopPtrs<KT> lp, LoopMisc *misc, uint32_t batch, int use_cond,
+                            cudaGraphConditionalHandle h_loop, cudaGraphConditionalHandle h_fb) {
     const uint32_t lv = misc->level;
     const LevelCtrl &c = lp.ctrl[lv];
     const bool more = (c.nseg_next + c.nmseg_next) > 0 && lv + LOOP_BATCH + 1 < (uint32_t)MAX_LEVELS;
     misc->level = lv + 1;
+    misc->set = ((lv + 1) / batch) & 1u;
     if (use_cond) {
         cudaGraphSetConditional(h_loop, more ? 1u : 0u);
         cudaGraphSetConditional(h_fb, (!more && misc->fb_count > 0) ? 1u : 0u);
@@ -48,7 +50,7 @@ __global__ void k_level_end(LoopPtrs<KT> lp, LoopMisc *misc, int use_cond, cudaG
 
 // after the previous level's leaves are sorted: their set is empty again
 static __global__ void k_flush_reset(LoopMisc *misc) {
-    const uint32_t set = loop_prev_set(misc->level);
+    const uint32_t set = misc->set ^ 1u;
     for (int k = 0; k < MAX_LEAF_CLASSES; k++) misc->leaf_counts[set][k] = 0;
     misc->copy_count[set] = 0;
     misc->nflush++;

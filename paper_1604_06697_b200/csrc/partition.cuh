@@ -42,6 +42,7 @@ __device__ __forceinline__ uint32_t pass_ntiles(const PassParams<KT> &P);
 template <class KT>
 struct LoopPtrs {
     const uint32_t *level;   // nullptr: the params are static (standalone pass, root)
+    const uint32_t *set;     // list set of the current batch of levels (LoopMisc::set)
     Seg *segs[2];
     uint32_t *tile_map[2];
     unsigned long long *cursor[2];
@@ -50,9 +51,9 @@ struct LoopPtrs {
     uint32_t *mtile_map[2], *mhist[2], *mcursor[2];
     LevelCtrl *ctrl;         // one control block per level
     LevelCtrl *root;         // the root's counts (level -1)
-    // leaves (and finished equal-record runs) of level l go to set (l / 4) & 1:
-    // one iteration of the loop partitions 4 levels while it sorts the
-    // previous 4 levels' leaves (LOOP_BATCH, loop.cuh)
+    // leaves (and finished equal-record runs) of a batch of levels go to list
+    // set `*set`: one iteration of the loop partitions a batch while it sorts
+    // the previous batch's leaves (loop.cuh)
     Leaf *leaves[2];
     uint32_t *leaf_counts[2];
     Leaf *copies[2];
@@ -197,7 +198,7 @@ __device__ __forceinline__ void loop_resolve(PostParams<KT> &Q) {
     Q.next_mhist = lp.mhist[np];
     Q.child_ctrl = lp.ctrl + lv;
     Q.nseg_dev = &loop_prev(lp, lv)->nseg_next;
-    const uint32_t set = (lv / LOOP_BATCH) & 1;
+    const uint32_t set = *lp.set;
     Q.leaves = lp.leaves[set];
     Q.leaf_counts = lp.leaf_counts[set];
     Q.copies = lp.copies[set];
@@ -620,7 +621,7 @@ __global__ void __launch_bounds__(NT) k_post_mw(const PostParams<KT> Qin) {
 template <class KT, int NT>
 __global__ void __launch_bounds__(NT) k_copy_runs(const LoopPtrs<KT> lp, const uint32_t *level, typename KT::T *user,
                                                   const typename KT::T *scratch) {
-    const uint32_t set = loop_prev_set(*level);
+    const uint32_t set = *lp.set ^ 1u;
     const Leaf *list = set ? lp.copies[1] : lp.copies[0];
     const uint32_t n = set ? *lp.copy_count[1] : *lp.copy_count[0];
     for (uint32_t li = blockIdx.x; li < n; li += gridDim.x) {
