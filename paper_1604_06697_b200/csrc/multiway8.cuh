@@ -106,6 +106,34 @@ __device__ __forceinline__ uint32_t mw8_bucket(const K (&tr)[MW8], K k) {
     return ((uint32_t)p0 << 2) | ((uint32_t)p1 << 1) | (uint32_t)p2;
 }
 
+// The classification of one key against the tile's splitters.  float64 keys
+// are compared as doubles (DSETP, the FP64 pipe) against the decoded
+// splitters: for non-NaN values the double order is the totalOrder with -0.0
+// and +0.0 merged, so #{s_i < k} still cuts the segment into contiguous
+// ranges of the total order (both zeros always share a bucket; R25)
+// and no key is encoded.  Other kinds compare their keys.
+template <class KT>
+struct Mw8Cls {
+    using K = typename KT::K;
+    K tr[MW8];
+    __device__ __forceinline__ void load(const K *tree) {
+#pragma unroll
+        for (int q = 1; q < MW8; q++) tr[q] = tree[q];
+    }
+    __device__ __forceinline__ uint32_t bucket(const typename KT::T &x) const { return mw8_bucket(tr, KT::key(x)); }
+};
+template <>
+struct Mw8Cls<KF64> {
+    double tr[MW8];
+    __device__ __forceinline__ void load(const uint64_t *tree) {
+#pragma unroll
+        for (int q = 1; q < MW8; q++) tr[q] = __longlong_as_double((long long)KF64::from_key(tree[q]));
+    }
+    __device__ __forceinline__ uint32_t bucket(const uint64_t &x) const {
+        return mw8_bucket(tr, __longlong_as_double((long long)x));
+    }
+};
+
 // 8 counters of 8 bits -> 4 words of two 16-bit counters
 __device__ __forceinline__ void mw8_widen(uint64_t c, uint32_t (&q)[MW8 / 2]) {
     const uint32_t lo = (uint32_t)c, hi = (uint32_t)(c >> 32);
@@ -150,9 +178,8 @@ __global__ void __launch_bounds__(NT + 32, MINB) k_mw8_count(const MwParams<KT> 
         const uint32_t t = sm.tile[s];
         if (t >= ntiles) break;
         const uint32_t si = sm.sidx[s];
-        K tr[MW8];
-#pragma unroll
-        for (int q = 1; q < MW8; q++) tr[q] = sm.tree[s][q];
+        Mw8Cls<KT> cls;
+        cls.load(sm.tree[s]);
         typename KT::T x[IPT];
         const uint32_t valid = mw8_load<KT, NT, IPT, STAGES, SM>(P, sm, s, t, lane, tid, x);
         __syncwarp();
@@ -160,7 +187,7 @@ __global__ void __launch_bounds__(NT + 32, MINB) k_mw8_count(const MwParams<KT> 
         uint64_t c64 = 0;
 #pragma unroll
         for (uint32_t c = 0; c < IPT; c++) {
-            const uint32_t b = mw8_bucket(tr, KT::key(x[c]));
+            const uint32_t b = cls.bucket(x[c]);
             c64 += (uint64_t)((valid >> c) & 1) << (8 * b);
         }
         uint32_t q[MW8 / 2];
@@ -233,14 +260,13 @@ __global__ void __launch_bounds__(NT + 32, MINB) k_mw8_scatter(const MwParams<KT
             sbeg = sm.sb[s];
             spar = sm.spar[s];
             bstart = lane < MW8 ? sm.start[s][lane] : 0;
-            K tr[MW8];
-#pragma unroll
-            for (int qq = 1; qq < MW8; qq++) tr[qq] = sm.tree[s][qq];
+            Mw8Cls<KT> cls;
+            cls.load(sm.tree[s]);
             const uint32_t valid = mw8_load<KT, NT, IPT, STAGES, SM>(P, sm, s, t, lane, tid, x);
             uint64_t c64 = 0;
 #pragma unroll
             for (uint32_t c = 0; c < IPT; c++) {
-                const uint32_t b = mw8_bucket(tr, KT::key(x[c]));
+                const uint32_t b = cls.bucket(x[c]);
                 const uint32_t v = (valid >> c) & 1;
                 pk[c] = ((uint32_t)(c64 >> (8 * b)) & 0xff) | (b << 16) | ((v ^ 1) << 31);
                 c64 += (uint64_t)v << (8 * b);
