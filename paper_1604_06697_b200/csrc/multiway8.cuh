@@ -130,7 +130,12 @@ struct Mw8Cls<KF64> {
         for (int q = 1; q < MW8; q++) tr[q] = __longlong_as_double((long long)KF64::from_key(tree[q]));
     }
     __device__ __forceinline__ uint32_t bucket(const uint64_t &x) const {
-        return mw8_bucket(tr, __longlong_as_double((long long)x));
+        const double d = __longlong_as_double((long long)x);
+        const uint32_t b = mw8_bucket(tr, d);
+        // NaN keys (outside the contract) keep their bit-pattern place: -NaN
+        // before every other key, +NaN after (R9); a NaN splitter only merges
+        // two adjacent buckets (its compares are constant)
+        return d != d ? ((x >> 63) ? 0u : MW8 - 1u) : b;
     }
 };
 
