@@ -253,16 +253,18 @@ __device__ __forceinline__ void store_run(const PL &pl, const E (&x)[IPT], int c
 
 // Barrier over the threads that share the runs of merge round r: a group of
 // G = 2^(r+1) threads reads and rewrites only its own slots, so rounds whose
-// groups fit a warp synchronise the warp, groups of up to 128 threads
-// synchronise their 128-thread slice on named barrier 1 + t / 128 (every use
-// of an id is by the same threads with the same count, so instances of
-// different rounds cannot mix), and larger groups the whole CTA.
+// groups fit a warp synchronise the warp, and larger groups their own slice
+// of 128, 256 or 512 threads on named barriers with ids of their own (every
+// use of an id is by the same threads with the same count, so instances of
+// different rounds cannot mix); a group of the whole CTA uses barrier 0.
 template <int NT>
 __device__ __forceinline__ void group_sync(int r, int t) {
     const int G = 2 << r;
     if (G <= 32) __syncwarp();
-    else if (G <= 128 && NT > 128) named_bar_sync(1u + ((uint32_t)t >> 7), 128u);
-    else __syncthreads();
+    else if (G >= NT) __syncthreads();
+    else if (G <= 128) named_bar_sync(1u + ((uint32_t)t >> 7), 128u);            // ids 1..8
+    else if (G == 256) named_bar_sync(9u + ((uint32_t)t >> 8), 256u);            // ids 9..12
+    else named_bar_sync(13u + ((uint32_t)t >> 9), 512u);                         // ids 13..14
 }
 
 // One leaf, by the whole CTA of NT threads.

@@ -292,7 +292,7 @@ __device__ __forceinline__ void post_stats_flush(const PostParams<KT> &Q) {
 #endif
 template <class KT, int NT>
 __device__ __forceinline__ void emit_children(const PostParams<KT> &Q, int nch, const uint32_t *cb,
-                                              const uint32_t *cl, uint8_t cp, uint16_t cd,
+                                              const uint32_t *cl, uint8_t cp, uint16_t cd, bool dups,
                                               const uint8_t *hint = nullptr, uint64_t hint_pivot = 0) {
     using T = typename KT::T;
     using K = typename KT::K;
@@ -314,7 +314,7 @@ __device__ __forceinline__ void emit_children(const PostParams<KT> &Q, int nch, 
         else if (h == 2) kind = C_BAND;
         else if (len <= Q.leaf_max) {
             kind = C_LEAF;
-            if constexpr (!KT::is_record) if (len >= BQ_DC_MIN && (int)cd < Q.depth_limit) {
+            if constexpr (!KT::is_record) if (dups && len >= BQ_DC_MIN && (int)cd < Q.depth_limit) {
                 uint32_t distinct = 64;
                 const K piv = sample64_median_distinct<KT>(cbuf, cb[c], len, lane, &distinct);
                 if (distinct <= BQ_DC_DISTINCT) {
@@ -517,12 +517,14 @@ __device__ __forceinline__ void post_segment(const PostParams<KT> &Q, uint32_t s
         const uint32_t cb[2] = {sg.begin, sg.begin + L};
         const uint32_t cl[2] = {L, G};
         const uint8_t h[2] = {(uint8_t)((sg.pad0 & 1) ? 2 : 0), (uint8_t)((sg.pad0 & 1) ? 0 : ((sg.pad0 & 2) ? 1 : 0))};
-        emit_children<KT, NT>(Q, 2, cb, cl, (uint8_t)(sg.parity ^ 1), (uint16_t)(sg.depth + 1), h, sg.pivot);
+        emit_children<KT, NT>(Q, 2, cb, cl, (uint8_t)(sg.parity ^ 1), (uint16_t)(sg.depth + 1), false, h, sg.pivot);
         return;
     }
     const uint32_t cb[2] = {sg.begin, sg.begin + L + E};
     const uint32_t cl[2] = {L, G};
-    emit_children<KT, NT>(Q, 2, cb, cl, (uint8_t)(sg.parity ^ 1), (uint16_t)(sg.depth + 1));
+    // R23's sample is drawn only below a pivot that was repeated (E >= 2):
+    // few distinct keys in a child imply many copies of its parent's pivot
+    emit_children<KT, NT>(Q, 2, cb, cl, (uint8_t)(sg.parity ^ 1), (uint16_t)(sg.depth + 1), E >= 2);
 }
 
 // Equal bands longer than band_inline_max, tile-parallel over the level
@@ -590,7 +592,7 @@ template <class KT, int NT>
 __global__ void __launch_bounds__(NT) k_init_root(PostParams<KT> Q, uint32_t n) {
     const uint32_t cb[1] = {0}, cl[1] = {n};
     post_stats_init();
-    emit_children<KT, NT>(Q, 1, cb, cl, 0, 0);
+    emit_children<KT, NT>(Q, 1, cb, cl, 0, 0, true);
     post_stats_flush(Q);
 }
 
@@ -610,7 +612,7 @@ __global__ void __launch_bounds__(NT) k_post_mw(const PostParams<KT> Qin) {
             cb[threadIdx.x] = m.s.begin + m.start[threadIdx.x];
             cl[threadIdx.x] = Q.mw.hist[threadIdx.x * Q.mw.hstride + si];
         }
-        emit_children<KT, NT>(Q, MW_K, cb, cl, (uint8_t)(m.s.parity ^ 1), (uint16_t)(m.s.depth + 1));
+        emit_children<KT, NT>(Q, MW_K, cb, cl, (uint8_t)(m.s.parity ^ 1), (uint16_t)(m.s.depth + 1), false);
     }
     post_stats_flush(Q);
 }
