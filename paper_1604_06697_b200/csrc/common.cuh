@@ -6,6 +6,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstddef>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 #include "bq.h"
@@ -176,13 +177,22 @@ template <class KT> struct Tune;
 #ifndef BQ_LEAF_NTREC
 #define BQ_LEAF_NTREC 1024
 #endif
+#ifndef BQ_MW8_MINB
+#define BQ_MW8_MINB 2
+#endif
+#ifndef BQ_MW8_MINB_PAIR
+#define BQ_MW8_MINB_PAIR 3
+#endif
+// MW8_MINB: resident CTAs per SM the 8-way kernels are compiled for (pairs:
+// 3, their 4-key threads fit 72 registers; 64-bit keys spill there)
 template <> struct Tune<KI32> {
     static constexpr int PART_THREADS = 256, PART_IPT = BQ_I32_IPT, PART_STAGES = BQ_I32_STAGES,
-                         PART_MINB = BQ_I32_MINB;
+                         PART_MINB = BQ_I32_MINB, MW8_MINB = BQ_MW8_MINB;
     static constexpr int LEAF_IPT = BQ_LEAF_IPT32, LEAF_NT = BQ_LEAF_NT32, LEAF = LEAF_IPT * LEAF_NT;
 };
 template <> struct Tune<KU64> {
-    static constexpr int PART_THREADS = 256, PART_IPT = 8, PART_STAGES = 4, PART_MINB = 2;   // 16 KB tiles
+    static constexpr int PART_THREADS = 256, PART_IPT = 8, PART_STAGES = 4, PART_MINB = 2,   // 16 KB tiles
+                         MW8_MINB = BQ_MW8_MINB;
     static constexpr int LEAF_IPT = BQ_LEAF_IPT64, LEAF_NT = BQ_LEAF_NT64, LEAF = LEAF_IPT * LEAF_NT;
 };
 template <> struct Tune<KF64> : Tune<KU64> {};
@@ -190,11 +200,13 @@ template <> struct Tune<KF64> : Tune<KU64> {};
 #define BQ_REC_STAGES 4
 #endif
 template <> struct Tune<KRec> {
-    static constexpr int PART_THREADS = 256, PART_IPT = 2, PART_STAGES = BQ_REC_STAGES, PART_MINB = 2;   // 16 KB tiles
+    static constexpr int PART_THREADS = 256, PART_IPT = 2, PART_STAGES = BQ_REC_STAGES, PART_MINB = 2,   // 16 KB tiles
+                         MW8_MINB = BQ_MW8_MINB;
     static constexpr int LEAF_IPT = BQ_LEAF_IPTREC, LEAF_NT = BQ_LEAF_NTREC, LEAF = LEAF_IPT * LEAF_NT;
 };
 template <> struct Tune<KPair> {
-    static constexpr int PART_THREADS = 256, PART_IPT = 4, PART_STAGES = 4, PART_MINB = 2;   // 16 KB tiles
+    static constexpr int PART_THREADS = 256, PART_IPT = 4, PART_STAGES = 4, PART_MINB = 2,   // 16 KB tiles
+                         MW8_MINB = BQ_MW8_MINB_PAIR;
     static constexpr int LEAF_IPT = BQ_LEAF_IPTREC, LEAF_NT = BQ_LEAF_NTREC, LEAF = LEAF_IPT * LEAF_NT;
 };
 

@@ -165,8 +165,8 @@ bq_status launch_multiway(MwParams<KT> MP, LevelCtrl *lc, cudaStream_t s, int wa
     constexpr int threads = Kn::NT + 32;
     if (ways == MW8) {
         constexpr int smem8 = mw8_smem_bytes<KT>();
-        auto kc8 = k_mw8_count<KT, Kn::NT, Kn::IPT, MW_STAGES, MW8_MINB>;
-        auto ks8 = k_mw8_scatter<KT, Kn::NT, Kn::IPT, MW_STAGES, MW8_MINB>;
+        auto kc8 = k_mw8_count<KT, Kn::NT, Kn::IPT, MW_STAGES, Tune<KT>::MW8_MINB>;
+        auto ks8 = k_mw8_scatter<KT, Kn::NT, Kn::IPT, MW_STAGES, Tune<KT>::MW8_MINB>;
         static CapCache cc_c8, cc_s8;
         int cap_c8 = 0, cap_s8 = 0;
         bq_status st = persistent_cap(kc8, threads, smem8, cc_c8, &cap_c8);

@@ -217,11 +217,11 @@ struct MwSmem {
 #ifndef BQ_MW_STAGES
 #define BQ_MW_STAGES 3
 #endif
-#ifndef BQ_MW8_MINB
-#define BQ_MW8_MINB 2
+#ifndef BQ_MW_CHUNK
+#define BQ_MW_CHUNK 4
 #endif
 constexpr int MW_STAGES = BQ_MW_STAGES;   // TMA ring depth of the multiway kernels (2 CTAs per SM)
-constexpr int MW8_MINB = BQ_MW8_MINB;     // resident CTAs per SM the 8-way kernels are compiled for
+constexpr uint32_t MW_CHUNK = BQ_MW_CHUNK;   // consecutive tiles per loader ticket
 
 template <class KT>
 constexpr int mw_smem_bytes() {
@@ -246,19 +246,34 @@ __device__ __forceinline__ void mw_warp_scan(uint32_t (&q)[MW_K / 2], uint32_t l
     }
 }
 
+// a splitter as the 8-way kernels compare it: float64 as the double's bits
+// (compared as doubles, R25), every other kind as its key
+template <class KT>
+__device__ __forceinline__ typename KT::K mw8_tree_word(typename KT::K k) {
+    if constexpr (std::is_same<KT, KF64>::value) return KF64::from_key(k);
+    else return k;
+}
+
 // loader warp shared by the count and the scatter kernel: claims tiles in order,
 // copies the segment's metadata into the stage and issues the TMA bulk load
 template <class KT, int NT, int IPT, int STAGES, class SM>
-__device__ __forceinline__ void mw_loader(const MwParams<KT> &P, SM &sm, uint32_t ntiles, bool need_start) {
+__device__ __forceinline__ void mw_loader(const MwParams<KT> &P, SM &sm, uint32_t ntiles, bool need_start,
+                                          bool decode = false) {
+    constexpr uint32_t CHUNK = MW_CHUNK;
     using T = typename KT::T;
     constexpr uint32_t TILE = NT * IPT;
     constexpr uint32_t W = sizeof(T), VW = 16 / W;
-    // the next ticket is claimed one tile ahead (as in k_part_fast's loader)
-    uint32_t t_next = atomicAdd(P.ticket, 1u);
+    // a ticket is a chunk of CHUNK consecutive tiles (mostly of one segment:
+    // the count kernel's per-segment accumulators flush rarely), the next
+    // one claimed a chunk ahead (as in k_part_fast's loader)
+    uint32_t c_next = atomicAdd(P.ticket, 1u) * CHUNK, j = 0;
     for (uint32_t i = 0;; i++) {
         const uint32_t s = i % STAGES;
-        const uint32_t t = t_next;
-        if (t < ntiles) t_next = atomicAdd(P.ticket, 1u);
+        const uint32_t t = c_next + j;
+        if (++j == CHUNK || t + 1 >= ntiles) {
+            if (t < ntiles) c_next = atomicAdd(P.ticket, 1u) * CHUNK;
+            j = 0;
+        }
         const uint32_t si = t < ntiles ? P.tile_map[t] : 0;
         mbar_wait(&sm.empty[s], ((i / STAGES) & 1) ^ 1);
         sm.tile[s] = t;
@@ -268,8 +283,12 @@ __device__ __forceinline__ void mw_loader(const MwParams<KT> &P, SM &sm, uint32_
         }
         const MSeg<KT> &ms = P.msegs[si];
         const Seg sg = ms.s;
+        if (decode)   // the 8-way kernels: float64 splitters as the doubles' bits (mw8_tree_word)
 #pragma unroll
-        for (int q = 1; q < MW_K; q++) sm.tree[s][q] = ms.tree[q];
+            for (int q = 1; q < MW_K; q++) sm.tree[s][q] = mw8_tree_word<KT>(ms.tree[q]);
+        else
+#pragma unroll
+            for (int q = 1; q < MW_K; q++) sm.tree[s][q] = ms.tree[q];
         if (need_start)
 #pragma unroll
             for (int q = 0; q < MW_K; q++) sm.start[s][q] = ms.start[q];

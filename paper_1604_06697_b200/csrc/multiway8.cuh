@@ -107,11 +107,13 @@ __device__ __forceinline__ uint32_t mw8_bucket(const K (&tr)[MW8], K k) {
 }
 
 // The classification of one key against the tile's splitters.  float64 keys
-// are compared as doubles (DSETP, the FP64 pipe) against the decoded
-// splitters: for non-NaN values the double order is the totalOrder with -0.0
-// and +0.0 merged, so #{s_i < k} still cuts the segment into contiguous
-// ranges of the total order (both zeros always share a bucket; R25)
-// and no key is encoded.  Other kinds compare their keys.
+// are compared as doubles (DSETP, the FP64 pipe) against the splitters the
+// loader decoded (mw8_tree_word): for non-NaN values the double order is the
+// totalOrder with -0.0 and +0.0 merged, so #{s_i < k} still cuts the segment
+// into contiguous ranges of the total order (both zeros always share a
+// bucket; R25) and no key is encoded.  NaN keys (outside the
+// contract) are only detected per key (one predicate OR); a thread that saw
+// one re-classifies its keys with fix().  Other kinds compare their keys.
 template <class KT>
 struct Mw8Cls {
     using K = typename KT::K;
@@ -120,24 +122,43 @@ struct Mw8Cls {
 #pragma unroll
         for (int q = 1; q < MW8; q++) tr[q] = tree[q];
     }
-    __device__ __forceinline__ uint32_t bucket(const typename KT::T &x) const { return mw8_bucket(tr, KT::key(x)); }
+    __device__ __forceinline__ uint32_t bucket(const typename KT::T &x, bool &) const {
+        return mw8_bucket(tr, KT::key(x));
+    }
+    __device__ __forceinline__ uint32_t fix(const typename KT::T &, uint32_t b) const { return b; }
 };
 template <>
 struct Mw8Cls<KF64> {
     double tr[MW8];
     __device__ __forceinline__ void load(const uint64_t *tree) {
 #pragma unroll
-        for (int q = 1; q < MW8; q++) tr[q] = __longlong_as_double((long long)KF64::from_key(tree[q]));
+        for (int q = 1; q < MW8; q++) tr[q] = __longlong_as_double((long long)tree[q]);
     }
-    __device__ __forceinline__ uint32_t bucket(const uint64_t &x) const {
+    __device__ __forceinline__ uint32_t bucket(const uint64_t &x, bool &nan) const {
         const double d = __longlong_as_double((long long)x);
-        const uint32_t b = mw8_bucket(tr, d);
-        // NaN keys (outside the contract) keep their bit-pattern place: -NaN
-        // before every other key, +NaN after (R9); a NaN splitter only merges
-        // two adjacent buckets (its compares are constant)
+        nan |= d != d;
+        return mw8_bucket(tr, d);
+    }
+    // NaN keys keep their bit-pattern place: -NaN before every other key,
+    // +NaN after (R9); a NaN splitter only merges two adjacent buckets (its
+    // compares are constant)
+    __device__ __forceinline__ uint32_t fix(const uint64_t &x, uint32_t b) const {
+        const double d = __longlong_as_double((long long)x);
         return d != d ? ((x >> 63) ? 0u : MW8 - 1u) : b;
     }
 };
+
+// the buckets of a thread's IPT keys (bk[c]), NaN fix-up included
+template <class KT, int IPT>
+__device__ __forceinline__ void mw8_classify(const Mw8Cls<KT> &cls, const typename KT::T (&x)[IPT],
+                                             uint32_t (&bk)[IPT]) {
+    bool nan = false;
+#pragma unroll
+    for (int c = 0; c < IPT; c++) bk[c] = cls.bucket(x[c], nan);
+    if (nan)
+#pragma unroll
+        for (int c = 0; c < IPT; c++) bk[c] = cls.fix(x[c], bk[c]);
+}
 
 // 8 counters of 8 bits -> 4 words of two 16-bit counters
 __device__ __forceinline__ void mw8_widen(uint64_t c, uint32_t (&q)[MW8 / 2]) {
@@ -146,6 +167,103 @@ __device__ __forceinline__ void mw8_widen(uint64_t c, uint32_t (&q)[MW8 / 2]) {
     q[1] = __byte_perm(lo, 0, 0x4342);
     q[2] = __byte_perm(hi, 0, 0x4140);
     q[3] = __byte_perm(hi, 0, 0x4342);
+}
+
+// four 4-bit fields (bits 0..15) -> four bytes
+__device__ __forceinline__ uint32_t nib_spread(uint32_t x) {
+    x = (x | (x << 8)) & 0x00ff00ffu;
+    return (x | (x << 4)) & 0x0f0f0f0fu;
+}
+
+// A thread's counters of its keys' buckets, the k-bucket form of the offset
+// buffers' branch-free counters (Alg. 3 l.8-9): 4-bit fields of
+// one word when a thread holds at most 15 keys, else 8-bit fields of two.
+template <int IPT>
+struct Mw8Ctr {
+    static constexpr bool NIB = IPT <= 15;
+    static_assert(IPT <= 255, "8-bit counters");
+    using W = typename std::conditional<NIB, uint32_t, uint64_t>::type;
+    W c = 0;
+    // rank of the next key of bucket b among this thread's; counted if v
+    __device__ __forceinline__ uint32_t take(uint32_t b, uint32_t v) {
+        const uint32_t sh = NIB ? 4 * b : 8 * b;
+        const uint32_t r = (uint32_t)(c >> sh) & (NIB ? 0xfu : 0xffu);
+        c += (W)v << sh;
+        return r;
+    }
+    __device__ __forceinline__ void add(uint32_t b, uint32_t v) { c += (W)v << (NIB ? 4 * b : 8 * b); }
+    // the counters as bytes: lo = buckets 0..3, hi = buckets 4..7
+    __device__ __forceinline__ void bytes(uint32_t &lo, uint32_t &hi) const {
+        if constexpr (NIB) {
+            lo = nib_spread((uint32_t)c & 0xffffu);
+            hi = nib_spread((uint32_t)c >> 16);
+        } else {
+            lo = (uint32_t)c;
+            hi = (uint32_t)((uint64_t)c >> 32);
+        }
+    }
+};
+
+// Warp scan of the 8 counters: ex = exclusive prefix over the lanes (16-bit
+// pairs: word k = buckets 2k, 2k+1), tot = the warp's totals (valid in lane
+// 31).  At most 8 keys per thread: the scan runs on the two byte words (every
+// exclusive prefix is <= 31 * 8 = 248; lane 31's inclusive one may reach 256
+// and wrap, but the difference incl - own is exact modulo 2^32 and fits).
+template <int IPT>
+__device__ __forceinline__ void mw8_scan(const Mw8Ctr<IPT> &ctr, uint32_t lane, uint32_t (&ex)[MW8 / 2],
+                                         uint32_t (&tot)[MW8 / 2]) {
+    uint32_t lo, hi, ow[MW8 / 2];
+    ctr.bytes(lo, hi);
+    mw8_widen((uint64_t)lo | ((uint64_t)hi << 32), ow);
+    if constexpr (IPT <= 8) {
+        uint32_t il = lo, ih = hi;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t ol = __shfl_up_sync(0xffffffffu, il, d), oh = __shfl_up_sync(0xffffffffu, ih, d);
+            if (lane >= (uint32_t)d) {
+                il += ol;
+                ih += oh;
+            }
+        }
+        mw8_widen((uint64_t)(il - lo) | ((uint64_t)(ih - hi) << 32), ex);
+#pragma unroll
+        for (int k = 0; k < MW8 / 2; k++) tot[k] = ex[k] + ow[k];
+    } else {
+        uint32_t q[MW8 / 2];
+#pragma unroll
+        for (int k = 0; k < MW8 / 2; k++) q[k] = ow[k];
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+#pragma unroll
+            for (int k = 0; k < MW8 / 2; k++) {
+                const uint32_t o = __shfl_up_sync(0xffffffffu, q[k], d);
+                if (lane >= (uint32_t)d) q[k] += o;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < MW8 / 2; k++) {
+            ex[k] = q[k] - ow[k];
+            tot[k] = q[k];
+        }
+    }
+}
+
+// the warp's total counts of the 8 buckets (two bytes words, per-lane byte
+// fields <= 248) added to hist[bucket][seg] by lanes 0..7
+template <class KT>
+__device__ __forceinline__ void mw8_count_flush(const MwParams<KT> &P, uint32_t lo, uint32_t hi, uint32_t seg,
+                                                uint32_t lane) {
+    uint32_t q[MW8 / 2];
+    mw8_widen((uint64_t)lo | ((uint64_t)hi << 32), q);
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1)
+#pragma unroll
+        for (int k = 0; k < MW8 / 2; k++) q[k] += __shfl_xor_sync(0xffffffffu, q[k], d);
+    uint32_t mine = 0;
+#pragma unroll
+    for (int k = 0; k < MW8 / 2; k++) mine = (lane >> 1) == (uint32_t)k ? q[k] : mine;
+    const uint32_t v = (lane & 1) ? (mine >> 16) : (mine & 0xffff);
+    if (lane < MW8 && v) atomicAdd(&P.hist[lane * P.hstride + seg], v);
 }
 
 // ---- k_mw8_count -----------------------------------------------------------------
@@ -172,46 +290,46 @@ __global__ void __launch_bounds__(NT + 32, MINB) k_mw8_count(const MwParams<KT> 
     }
     __syncthreads();
     if (warp == NW) {
-        if (lane == 0) mw_loader<KT, NT, IPT, STAGES, SM>(P, sm, ntiles, false);
+        if (lane == 0) mw_loader<KT, NT, IPT, STAGES, SM>(P, sm, ntiles, false, true);
         return;
     }
-    // lane L < 8 accumulates this warp's count of bucket L for segment cur_seg
-    uint32_t acc = 0, cur_seg = 0xffffffffu;
+    // Each thread accumulates its byte counters over the tiles of one segment
+    // (a loader ticket is a chunk of consecutive tiles); the warp reduces and
+    // flushes them when the segment changes or before a byte could overflow.
+    constexpr uint32_t FLUSH = 255 / IPT;
+    uint32_t alo = 0, ahi = 0, nacc = 0, cur_seg = 0xffffffffu, cls_seg = 0xffffffffu;
+    Mw8Cls<KT> cls;
     for (uint32_t i = 0;; i++) {
         const uint32_t s = i % STAGES;
         mbar_wait(&sm.full[s], (i / STAGES) & 1);
         const uint32_t t = sm.tile[s];
         if (t >= ntiles) break;
         const uint32_t si = sm.sidx[s];
-        Mw8Cls<KT> cls;
-        cls.load(sm.tree[s]);
+        if (si != cls_seg) {   // the splitters change with the segment only
+            cls.load(sm.tree[s]);
+            cls_seg = si;
+        }
         typename KT::T x[IPT];
         const uint32_t valid = mw8_load<KT, NT, IPT, STAGES, SM>(P, sm, s, t, lane, tid, x);
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.empty[s]);
-        uint64_t c64 = 0;
+        uint32_t bk[IPT];
+        mw8_classify<KT, IPT>(cls, x, bk);
+        Mw8Ctr<IPT> ctr;
 #pragma unroll
-        for (uint32_t c = 0; c < IPT; c++) {
-            const uint32_t b = cls.bucket(x[c]);
-            c64 += (uint64_t)((valid >> c) & 1) << (8 * b);
-        }
-        uint32_t q[MW8 / 2];
-        mw8_widen(c64, q);
-#pragma unroll
-        for (int d = 16; d > 0; d >>= 1)
-#pragma unroll
-            for (int k = 0; k < MW8 / 2; k++) q[k] += __shfl_xor_sync(0xffffffffu, q[k], d);
-        if (si != cur_seg) {
-            if (cur_seg != 0xffffffffu && lane < MW8 && acc) atomicAdd(&P.hist[lane * P.hstride + cur_seg], acc);
-            acc = 0;
+        for (uint32_t c = 0; c < IPT; c++) ctr.add(bk[c], (valid >> c) & 1);
+        if (si != cur_seg || nacc == FLUSH) {
+            if (cur_seg != 0xffffffffu) mw8_count_flush(P, alo, ahi, cur_seg, lane);
+            alo = ahi = nacc = 0;
             cur_seg = si;
         }
-        uint32_t mine = 0;
-#pragma unroll
-        for (int k = 0; k < MW8 / 2; k++) mine = (lane >> 1) == (uint32_t)k ? q[k] : mine;
-        acc += (lane & 1) ? (mine >> 16) : (mine & 0xffff);
+        uint32_t lo, hi;
+        ctr.bytes(lo, hi);
+        alo += lo;
+        ahi += hi;
+        nacc++;
     }
-    if (cur_seg != 0xffffffffu && lane < MW8 && acc) atomicAdd(&P.hist[lane * P.hstride + cur_seg], acc);
+    if (cur_seg != 0xffffffffu) mw8_count_flush(P, alo, ahi, cur_seg, lane);
 }
 
 // ---- k_mw8_scatter ---------------------------------------------------------------
@@ -240,7 +358,7 @@ __global__ void __launch_bounds__(NT + 32, MINB) k_mw8_scatter(const MwParams<KT
     }
     __syncthreads();
     if (warp == NW) {
-        if (lane == 0) mw_loader<KT, NT, IPT, STAGES, SM>(P, sm, ntiles, true);
+        if (lane == 0) mw_loader<KT, NT, IPT, STAGES, SM>(P, sm, ntiles, true, true);
         return;
     }
 
@@ -258,38 +376,29 @@ __global__ void __launch_bounds__(NT + 32, MINB) k_mw8_scatter(const MwParams<KT
         const bool cur = t < ntiles;
         T x[IPT];
         uint32_t pk[IPT];
-        uint32_t q[MW8 / 2], own[MW8 / 2];
+        uint32_t ex[MW8 / 2];
         uint32_t si = 0, sbeg = 0, spar = 0, bstart = 0;
         if (cur) {
             si = sm.sidx[s];
             sbeg = sm.sb[s];
             spar = sm.spar[s];
             bstart = lane < MW8 ? sm.start[s][lane] : 0;
-            Mw8Cls<KT> cls;
+            Mw8Cls<KT> cls;   // (reloaded per tile: kept live, it would spill)
             cls.load(sm.tree[s]);
             const uint32_t valid = mw8_load<KT, NT, IPT, STAGES, SM>(P, sm, s, t, lane, tid, x);
-            uint64_t c64 = 0;
+            uint32_t bk[IPT];
+            mw8_classify<KT, IPT>(cls, x, bk);
+            Mw8Ctr<IPT> ctr;
 #pragma unroll
             for (uint32_t c = 0; c < IPT; c++) {
-                const uint32_t b = cls.bucket(x[c]);
                 const uint32_t v = (valid >> c) & 1;
-                pk[c] = ((uint32_t)(c64 >> (8 * b)) & 0xff) | (b << 16) | ((v ^ 1) << 31);
-                c64 += (uint64_t)v << (8 * b);
+                pk[c] = ctr.take(bk[c], v) | (bk[c] << 16) | ((v ^ 1) << 31);
             }
-            mw8_widen(c64, q);
-#pragma unroll
-            for (int k = 0; k < MW8 / 2; k++) own[k] = q[k];
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-#pragma unroll
-                for (int k = 0; k < MW8 / 2; k++) {
-                    const uint32_t o = __shfl_up_sync(0xffffffffu, q[k], d);
-                    if (lane >= (uint32_t)d) q[k] += o;
-                }
-            }
+            uint32_t tot[MW8 / 2];
+            mw8_scan<IPT>(ctr, lane, ex, tot);
             if (lane == 31)
 #pragma unroll
-                for (int k = 0; k < MW8 / 2; k++) sm.wtot[par][warp][k] = q[k];
+                for (int k = 0; k < MW8 / 2; k++) sm.wtot[par][warp][k] = tot[k];
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.empty[s]);
@@ -381,7 +490,7 @@ __global__ void __launch_bounds__(NT + 32, MINB) k_mw8_scatter(const MwParams<KT
             uint32_t base[MW8 / 2];
 #pragma unroll
             for (int k = 0; k < MW8 / 2; k++) {
-                base[k] = q[k] - own[k] + sm.wpre[par][warp][k] + (sm.boff[par][2 * k] | (sm.boff[par][2 * k + 1] << 16));
+                base[k] = ex[k] + sm.wpre[par][warp][k] + (sm.boff[par][2 * k] | (sm.boff[par][2 * k + 1] << 16));
             }
 #pragma unroll
             for (uint32_t c = 0; c < IPT; c++) {
