@@ -265,33 +265,55 @@ __device__ __forceinline__ void mw_loader(const MwParams<KT> &P, SM &sm, uint32_
     constexpr uint32_t W = sizeof(T), VW = 16 / W;
     // a ticket is a chunk of CHUNK consecutive tiles (mostly of one segment:
     // the count kernel's per-segment accumulators flush rarely), the next
-    // one claimed a chunk ahead (as in k_part_fast's loader)
+    // one claimed a chunk ahead (as in k_part_fast's loader); the next tile's
+    // segment index is loaded one tile ahead, and a tile of the same segment
+    // as the previous one copies that stage's metadata instead of reloading
     uint32_t c_next = atomicAdd(P.ticket, 1u) * CHUNK, j = 0;
-    for (uint32_t i = 0;; i++) {
-        const uint32_t s = i % STAGES;
+    auto claim = [&]() -> uint32_t {
         const uint32_t t = c_next + j;
         if (++j == CHUNK || t + 1 >= ntiles) {
             if (t < ntiles) c_next = atomicAdd(P.ticket, 1u) * CHUNK;
             j = 0;
         }
-        const uint32_t si = t < ntiles ? P.tile_map[t] : 0;
+        return t;
+    };
+    uint32_t t = claim();
+    uint32_t si = t < ntiles ? P.tile_map[t] : 0, prev_si = 0xffffffffu;
+    for (uint32_t i = 0;; i++) {
+        const uint32_t s = i % STAGES, ps = (i + STAGES - 1) % STAGES;
+        const uint32_t tn = t < ntiles ? claim() : ntiles;
+        const uint32_t sin = tn < ntiles ? P.tile_map[tn] : 0;
         mbar_wait(&sm.empty[s], ((i / STAGES) & 1) ^ 1);
         sm.tile[s] = t;
         if (t >= ntiles) {
             mbar_arrive(&sm.full[s]);
             break;
         }
-        const MSeg<KT> &ms = P.msegs[si];
-        const Seg sg = ms.s;
-        if (decode)   // the 8-way kernels: float64 splitters as the doubles' bits (mw8_tree_word)
+        Seg sg;
+        if (si == prev_si) {
 #pragma unroll
-            for (int q = 1; q < MW_K; q++) sm.tree[s][q] = mw8_tree_word<KT>(ms.tree[q]);
-        else
+            for (int q = 1; q < MW_K; q++) sm.tree[s][q] = sm.tree[ps][q];
+            if (need_start)
 #pragma unroll
-            for (int q = 1; q < MW_K; q++) sm.tree[s][q] = ms.tree[q];
-        if (need_start)
+                for (int q = 0; q < MW_K; q++) sm.start[s][q] = sm.start[ps][q];
+            sg.begin = sm.sb[ps];
+            sg.len = sm.slen[ps];
+            sg.tile_base = sm.stb[ps];
+            sg.parity = (uint8_t)sm.spar[ps];
+        } else {
+            const MSeg<KT> &ms = P.msegs[si];
+            sg = ms.s;
+            if (decode)   // the 8-way kernels: float64 splitters as the doubles' bits (mw8_tree_word)
 #pragma unroll
-            for (int q = 0; q < MW_K; q++) sm.start[s][q] = ms.start[q];
+                for (int q = 1; q < MW_K; q++) sm.tree[s][q] = mw8_tree_word<KT>(ms.tree[q]);
+            else
+#pragma unroll
+                for (int q = 1; q < MW_K; q++) sm.tree[s][q] = ms.tree[q];
+            if (need_start)
+#pragma unroll
+                for (int q = 0; q < MW_K; q++) sm.start[s][q] = ms.start[q];
+        }
+        prev_si = si;
         sm.sb[s] = sg.begin;
         sm.slen[s] = sg.len;
         sm.stb[s] = sg.tile_base;
@@ -310,6 +332,8 @@ __device__ __forceinline__ void mw_loader(const MwParams<KT> &P, SM &sm, uint32_
         } else {
             mbar_arrive(&sm.full[s]);
         }
+        t = tn;
+        si = sin;
     }
 }
 
