@@ -210,6 +210,11 @@ template <> struct Tune<KPair> {
     static constexpr int LEAF_IPT = BQ_LEAF_IPTREC, LEAF_NT = BQ_LEAF_NTREC, LEAF = LEAF_IPT * LEAF_NT;
 };
 
+#ifndef BQ_PART_CHUNK
+#define BQ_PART_CHUNK 4
+#endif
+constexpr uint32_t PART_CHUNK = BQ_PART_CHUNK;   // consecutive tiles per ticket of k_part_fast's loader
+
 template <class KT> constexpr int tile_elems() { return Tune<KT>::PART_THREADS * Tune<KT>::PART_IPT; }
 
 // Tiles are laid out from each segment's 16-byte-aligned begin: with

@@ -91,17 +91,31 @@ __global__ void __launch_bounds__(NT + 32, MINB) k_part_fast(const PassParams<KT
     // -------------------------------------------------------------- loader ----
     if (warp == NW) {
         if (lane != 0) return;
-        // the next ticket is claimed one tile ahead, so the atomic's L2 round
-        // trip overlaps this tile's metadata reads and the wait for a free
-        // stage (a claimed ticket is always processed: the loop stops only on
-        // a ticket >= ntiles, and every later one is larger)
-        uint32_t t_next = atomicAdd(&P.ctrl->ticket, 1u);
+        // a ticket is a chunk of PART_CHUNK consecutive tiles, the next one
+        // claimed a chunk ahead, so the atomic's L2 round trip overlaps the
+        // tiles' metadata reads and the wait for a free stage (a claimed
+        // ticket is always processed: the loop stops only on a tile >=
+        // ntiles, and every later ticket is larger); the next tile's segment
+        // index is read a tile ahead and a segment's metadata once per run of
+        // its tiles
+        uint32_t c_next = atomicAdd(&P.ctrl->ticket, 1u) * PART_CHUNK, j = 0;
+        auto claim = [&]() -> uint32_t {
+            const uint32_t t = c_next + j;
+            if (++j == PART_CHUNK || t + 1 >= ntiles) {
+                if (t < ntiles) c_next = atomicAdd(&P.ctrl->ticket, 1u) * PART_CHUNK;
+                j = 0;
+            }
+            return t;
+        };
+        uint32_t t = claim();
+        uint32_t si = (P.tile_map && t < ntiles) ? P.tile_map[t] : 0, prev_si = 0xffffffffu;
+        Seg sg = P.seg0;
         for (uint32_t i = 0;; i++) {
             const uint32_t s = i % STAGES;
-            const uint32_t t = t_next;
-            if (t < ntiles) t_next = atomicAdd(&P.ctrl->ticket, 1u);
-            const uint32_t si = (P.tile_map && t < ntiles) ? P.tile_map[t] : 0;
-            const Seg sg = P.tile_map ? P.segs[si] : P.seg0;
+            const uint32_t tn = t < ntiles ? claim() : ntiles;
+            const uint32_t sin = (P.tile_map && tn < ntiles) ? P.tile_map[tn] : 0;
+            if (P.tile_map && si != prev_si) sg = P.segs[si];
+            prev_si = si;
             mbar_wait(&sm.empty[s], ((i / STAGES) & 1) ^ 1);
             sm.tile[s] = t;
             if (t >= ntiles) {
@@ -123,6 +137,8 @@ __global__ void __launch_bounds__(NT + 32, MINB) k_part_fast(const PassParams<KT
             } else {
                 mbar_arrive(&sm.full[s]);
             }
+            t = tn;
+            si = sin;
         }
         return;
     }
