@@ -210,6 +210,9 @@ template <> struct Tune<KPair> {
     static constexpr int LEAF_IPT = BQ_LEAF_IPTREC, LEAF_NT = BQ_LEAF_NTREC, LEAF = LEAF_IPT * LEAF_NT;
 };
 
+#ifndef BQ_MW8W
+#define BQ_MW8W 1   // 8-way levels: warp-private tiles with exact offsets (multiway8w.cuh)
+#endif
 #ifndef BQ_PART_CHUNK
 #define BQ_PART_CHUNK 4
 #endif

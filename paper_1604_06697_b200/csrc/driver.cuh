@@ -59,6 +59,7 @@ struct Layout {
     size_t msegs[2], mtile_map[2], mhist[2], mcursor[2];   // multiway segment lists (N4)
     size_t copies[2], max_copies;                           // records: finished equal runs to copy
     size_t tprefix, fbst;                                   // a9 over the depth-capped segments
+    size_t mtab, mblk;                                      // 8-way tile counts and block prefixes
     size_t max_tiles, max_segs, max_leaves, max_fb;
 };
 
@@ -101,6 +102,8 @@ Layout<KT> make_layout(size_t n) {
     L.max_copies = KT::is_record ? L.max_segs + 2 + n / 65536 + 2 : 1;
     L.copies[0] = take(L.max_copies * sizeof(Leaf));
     L.copies[1] = take(L.max_copies * sizeof(Leaf));
+    L.mtab = take(mw_capable<KT>() ? L.max_tiles * MW8 * sizeof(uint32_t) : 0);
+    L.mblk = take(mw_capable<KT>() ? (L.max_tiles / MWS_BR + 2) * MW8 * sizeof(uint32_t) : 0);
     L.tprefix = take((L.max_fb + 1) * sizeof(uint32_t));
     L.fbst = take(sizeof(FbState));
     L.ctrl = take((MAX_LEVELS + 1) * sizeof(LevelCtrl));   // [MAX_LEVELS]: the root's counts
@@ -163,6 +166,31 @@ template <class KT>
 bq_status launch_multiway(MwParams<KT> MP, LevelCtrl *lc, cudaStream_t s, int ways) {
     using Kn = Kernels<KT>;
     constexpr int threads = Kn::NT + 32;
+#if BQ_MW8W
+    if (ways == MW8) {   // warp-private tiles, exact offsets (multiway8w.cuh)
+        constexpr int IPTW = Mw8wTune<KT>::IPT, smemw = mw8w_smem_bytes<KT>(), tw = MW8W_WARPS * 32;
+        auto kc = k_mw8w_count<KT, IPTW>;
+        auto ks = k_mw8w_scatter<KT, IPTW>;
+        static CapCache cc_c, cc_s;
+        int cap_c = 0, cap_s = 0;
+        bq_status st = persistent_cap(kc, tw, 0, cc_c, &cap_c);
+        if (st != BQ_OK) return st;
+        st = persistent_cap(ks, tw, smemw, cc_s, &cap_s);
+        if (st != BQ_OK) return st;
+        kc<<<cap_c, tw, 0, s>>>(MP);
+        BQ_CK_LAUNCH();
+        const uint32_t nb = (MP.max_tiles + MWS_BR - 1) / MWS_BR;
+        k_mw8w_scan1<KT><<<nb < 592 ? nb : 592, 256, 0, s>>>(MP);
+        BQ_CK_LAUNCH();
+        k_mw8w_scan2<KT><<<1, 1024, 0, s>>>(MP);
+        BQ_CK_LAUNCH();
+        k_mw8w_seg<KT><<<POST_GRID / 8, 256, 0, s>>>(MP);
+        BQ_CK_LAUNCH();
+        ks<<<cap_s, tw, smemw, s>>>(MP);
+        BQ_CK_LAUNCH();
+        return BQ_OK;
+    }
+#endif
     if (ways == MW8) {
         constexpr int smem8 = mw8_smem_bytes<KT>();
         auto kc8 = k_mw8_count<KT, Kn::NT, Kn::IPT, MW_STAGES, Tune<KT>::MW8_MINB>;
@@ -646,6 +674,9 @@ bq_status make_plan(SortPlan<KT> &pl, typename KT::T *data, size_t n, void *ws, 
     MP.bufs[0] = pl.user;
     MP.bufs[1] = pl.scratch;
     MP.hstride = (uint32_t)L.max_segs;
+    MP.mtab = reinterpret_cast<uint32_t *>(w + L.mtab);
+    MP.mblk = reinterpret_cast<uint32_t *>(w + L.mblk);
+    MP.max_tiles = (uint32_t)L.max_tiles;
     MP.n_total = n;
     MP.aligned = pl.aligned;
     MP.lp = lp;
@@ -1077,7 +1108,7 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
             cleanup();
             return set_error(BQ_ERR_CUDA, "leaf list overflow");
         }
-        const int per_level = 4 + (KT::is_record ? 1 : 0) + (ways > 2 ? 4 : 0);
+        const int per_level = 4 + (KT::is_record ? 1 : 0) + (ways > 2 ? ((BQ_MW8W && ways == MW8) ? 6 : 4) : 0);
         local.kernel_launches = 1 + levels * per_level + hm.nflush * (NCLS + 1 + (KT::is_record && !ordered ? 1 : 0)) +
                                 (hm.fb_count ? 4 : 0);
         for (int l = 0; l < levels; l++) {

@@ -171,6 +171,9 @@ struct MwParams {
     LevelCtrl *ctrl;     // element-pass statistics
     LoopPtrs<KT> lp;     // lp.level != nullptr: the current level's lists (partition.cuh)
     int ticket_sel;      // loop: 0 = the count kernel's ticket, 1 = the scatter kernel's
+    uint32_t *mtab;      // 8-way (multiway8w.cuh): per-tile bucket counts, then their prefix
+    uint32_t *mblk;      // 8-way: per-block totals, then block prefixes
+    uint32_t max_tiles;  // rows of mtab
 };
 
 template <class KT>

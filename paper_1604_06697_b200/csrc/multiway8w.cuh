@@ -1,0 +1,392 @@
+// multiway8w.cuh — the 8-way multi-pivot level (N4) with warp-private tiles
+// and exact output offsets: no block barriers and no atomics on the data path.
+//
+// The paper's block partition keeps, per block, the offsets of the elements to
+// move and moves them in a second loop (Alg. 3); with k buckets the
+// offsets become k counters (Super Scalar Sample Sort's "oracle").
+// Here one warp owns a whole tile (TILE = tile_elems<KT>() keys, processed in
+// rounds of 32 x IPT keys), and a level is five launches:
+//   k_mw8w_count    every tile's 8 bucket counts -> tab[t][b]      (read pass)
+//   k_mw8w_scan1    prefix of tab over the tiles of blocks of MWS_BR tiles
+//   k_mw8w_scan2    block prefixes (one CTA)
+//   k_mw8w_seg      per segment: bucket totals (hist), bucket starts
+//                   (MSeg::start) and the bucket bases (cursor) such that
+//                   tile t's keys of bucket b go to
+//                   cursor[b][seg] + tab[t][b] + blk[t / MWS_BR][b]
+//   k_mw8w_scatter  per round: classify, rank inside the warp (packed counters
+//                   and a byte-field warp scan), stage the round bucket by
+//                   bucket in the warp's shared memory, store it coalesced
+// Tiles of a segment are consecutive and a bucket receives them in tile
+// order, so the layout of a level is deterministic.  Splitters, classification
+// (float64 compares as doubles, R25) and counters are multiway8.cuh's.
+#pragma once
+
+namespace bq {
+
+constexpr uint32_t MWS_BR = 2048;   // tiles per block of the tile-count scan (8 per thread)
+constexpr int MW8W_WARPS = 8;       // warps per CTA of the count and scatter kernels
+#ifndef BQ_MW8W_MINB
+#define BQ_MW8W_MINB 3
+#endif
+#ifndef BQ_MW8W_MINB_PAIR
+#define BQ_MW8W_MINB_PAIR 3
+#endif
+#ifndef BQ_MW8W_PF
+#define BQ_MW8W_PF 0   // load the next round's keys while the current round is placed
+#endif
+
+template <class KT> struct Mw8wTune;
+template <> struct Mw8wTune<KI32> { static constexpr int IPT = 8, MINB = BQ_MW8W_MINB; };
+template <> struct Mw8wTune<KU64> { static constexpr int IPT = 8, MINB = BQ_MW8W_MINB; };
+template <> struct Mw8wTune<KF64> { static constexpr int IPT = 8, MINB = BQ_MW8W_MINB; };
+template <> struct Mw8wTune<KRec> { static constexpr int IPT = 2, MINB = BQ_MW8W_MINB; };
+template <> struct Mw8wTune<KPair> { static constexpr int IPT = 4, MINB = BQ_MW8W_MINB_PAIR; };
+
+// per-warp staging of one round, double-buffered by round parity
+template <class KT, int IPT>
+struct Mw8wWarpSmem {
+    static constexpr int RK = 32 * IPT;
+    typename KT::T key[2][RK];
+    uint8_t tag[2][RK];          // the staged key's bucket
+    uint32_t ob[2][MW8];         // global index of staged slot 0 of each bucket's run
+};
+template <class KT>
+constexpr int mw8w_smem_bytes() {
+    return (int)(MW8W_WARPS * sizeof(Mw8wWarpSmem<KT, Mw8wTune<KT>::IPT>));
+}
+
+// the splitters of segment si as the 8-way classification compares them
+template <class KT>
+__device__ __forceinline__ void mw8w_load_cls(const MwParams<KT> &P, uint32_t si, Mw8Cls<KT> &cls) {
+    typename KT::K tr[MW8];
+#pragma unroll
+    for (int q = 1; q < MW8; q++) tr[q] = mw8_tree_word<KT>(P.msegs[si].tree[q]);
+    cls.load(tr);
+}
+
+// Round r0 (tile positions [r0, r0 + 32 IPT)) of the tile at src (= the
+// buffer + tbeg): element c = v VW + e of lane L sits at position
+// r0 + v 32 VW + L VW + e (VW elements per 16-byte vector: every vector load
+// of the warp covers 512 contiguous bytes).  Returns the validity mask.
+template <class KT, int IPT>
+__device__ __forceinline__ uint32_t mw8w_load(const typename KT::T *src, uint32_t r0, uint32_t vlo, uint32_t vhi,
+                                              uint32_t lane, bool vec, typename KT::T (&x)[IPT]) {
+    using T = typename KT::T;
+    constexpr uint32_t VW = sizeof(T) >= 16 ? 1u : 16u / (uint32_t)sizeof(T), NV = IPT / VW;
+    static_assert(IPT % VW == 0, "whole vectors per thread");
+    if (vec && r0 >= vlo && r0 + 32u * IPT <= vhi) {
+#pragma unroll
+        for (uint32_t v = 0; v < NV; v++) {
+            const uint4 q = ldg_stream(reinterpret_cast<const uint4 *>(src + r0 + v * 32 * VW + lane * VW));
+            memcpy(&x[v * VW], &q, 16);
+        }
+        return (1u << IPT) - 1;
+    }
+    uint32_t valid = 0;
+#pragma unroll
+    for (uint32_t v = 0; v < NV; v++)
+#pragma unroll
+        for (uint32_t e = 0; e < VW; e++) {
+            const uint32_t pos = r0 + v * 32 * VW + lane * VW + e;
+            const bool ok = pos >= vlo && pos < vhi;
+            x[v * VW + e] = ok ? src[pos] : T{};
+            valid |= (uint32_t)ok << (v * VW + e);
+        }
+    return valid;
+}
+
+// ---- k_mw8w_count ------------------------------------------------------------------
+template <class KT, int IPT>
+__global__ void __launch_bounds__(MW8W_WARPS * 32) k_mw8w_count(const MwParams<KT> Pin) {
+    if (const LevelCtrl *pv = loop_prev_ctrl(Pin.lp)) if (pv->nmseg_next == 0) return;
+    __shared__ MwParams<KT> sP;
+    const MwParams<KT> &P = cta_params(Pin, sP);
+    using T = typename KT::T;
+    constexpr uint32_t TILE = (uint32_t)tile_elems<KT>(), RK = 32u * IPT;
+    static_assert(TILE % RK == 0 && (TILE / 32) <= 255, "rounds per tile; byte counters");
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t ntiles = *P.ntiles_dev;
+    uint32_t cls_seg = 0xffffffffu;
+    Mw8Cls<KT> cls;
+    for (uint32_t t = blockIdx.x * MW8W_WARPS + (threadIdx.x >> 5); t < ntiles; t += gridDim.x * MW8W_WARPS) {
+        const uint32_t si = P.tile_map[t];
+        const Seg sg = P.msegs[si].s;
+        if (si != cls_seg) {
+            mw8w_load_cls<KT>(P, si, cls);
+            cls_seg = si;
+        }
+        const TileGeom<KT, TILE> G(sg, t);
+        const T *src = (sg.parity ? P.bufs[1] : P.bufs[0]) + G.tbeg;
+        uint32_t alo = 0, ahi = 0;   // byte counters: <= TILE / 32 per lane
+        for (uint32_t r0 = G.vlo / RK * RK; r0 < G.vhi; r0 += RK) {
+            T x[IPT];
+            const uint32_t valid = mw8w_load<KT, IPT>(src, r0, G.vlo, G.vhi, lane, P.aligned, x);
+            uint32_t bk[IPT];
+            mw8_classify<KT, IPT>(cls, x, bk);
+            Mw8Ctr<IPT> ctr;
+#pragma unroll
+            for (int c = 0; c < IPT; c++) ctr.add(bk[c], (valid >> c) & 1);
+            uint32_t lo, hi;
+            ctr.bytes(lo, hi);
+            alo += lo;
+            ahi += hi;
+        }
+        uint32_t q[MW8 / 2];
+        mw8_widen((uint64_t)alo | ((uint64_t)ahi << 32), q);
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1)
+#pragma unroll
+            for (int k = 0; k < MW8 / 2; k++) q[k] += __shfl_xor_sync(0xffffffffu, q[k], d);
+        uint32_t mine = 0;
+#pragma unroll
+        for (int k = 0; k < MW8 / 2; k++) mine = (lane >> 1) == (uint32_t)k ? q[k] : mine;
+        if (lane < MW8) P.mtab[(size_t)t * MW8 + lane] = (lane & 1) ? (mine >> 16) : (mine & 0xffff);
+    }
+}
+
+// ---- k_mw8w_scan1: exclusive prefix of the tile counts inside blocks of MWS_BR tiles
+template <class KT>
+__global__ void __launch_bounds__(256) k_mw8w_scan1(const MwParams<KT> Pin) {
+    if (const LevelCtrl *pv = loop_prev_ctrl(Pin.lp)) if (pv->nmseg_next == 0) return;
+    __shared__ MwParams<KT> sP;
+    const MwParams<KT> &P = cta_params(Pin, sP);
+    __shared__ uint32_t s_w[8][MW8];
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t ntiles = *P.ntiles_dev;
+    for (uint32_t blk = blockIdx.x; blk * MWS_BR < ntiles; blk += gridDim.x) {
+        const uint32_t t0 = blk * MWS_BR + tid * 8;
+        uint32_t sum[MW8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (uint32_t t = t0; t < t0 + 8 && t < ntiles; t++) {
+            const uint4 *row = reinterpret_cast<const uint4 *>(P.mtab + (size_t)t * MW8);
+            const uint4 a = row[0], b = row[1];
+            sum[0] += a.x; sum[1] += a.y; sum[2] += a.z; sum[3] += a.w;
+            sum[4] += b.x; sum[5] += b.y; sum[6] += b.z; sum[7] += b.w;
+        }
+        uint32_t inc[MW8];
+#pragma unroll
+        for (int k = 0; k < MW8; k++) inc[k] = sum[k];
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1)
+#pragma unroll
+            for (int k = 0; k < MW8; k++) {
+                const uint32_t o = __shfl_up_sync(0xffffffffu, inc[k], d);
+                if (lane >= (uint32_t)d) inc[k] += o;
+            }
+        __syncthreads();   // s_w of the previous block read
+        if (lane == 31)
+#pragma unroll
+            for (int k = 0; k < MW8; k++) s_w[warp][k] = inc[k];
+        __syncthreads();
+        uint32_t pre[MW8];
+#pragma unroll
+        for (int k = 0; k < MW8; k++) {
+            uint32_t w = 0, all = 0;
+#pragma unroll
+            for (uint32_t w2 = 0; w2 < 8; w2++) {
+                w += w2 < warp ? s_w[w2][k] : 0;
+                all += s_w[w2][k];
+            }
+            pre[k] = w + inc[k] - sum[k];
+            if (tid == 0) P.mblk[(size_t)blk * MW8 + k] = all;
+        }
+        for (uint32_t t = t0; t < t0 + 8 && t < ntiles; t++) {
+            uint4 *row = reinterpret_cast<uint4 *>(P.mtab + (size_t)t * MW8);
+            const uint4 a = row[0], b = row[1];
+            row[0] = make_uint4(pre[0], pre[1], pre[2], pre[3]);
+            row[1] = make_uint4(pre[4], pre[5], pre[6], pre[7]);
+            pre[0] += a.x; pre[1] += a.y; pre[2] += a.z; pre[3] += a.w;
+            pre[4] += b.x; pre[5] += b.y; pre[6] += b.z; pre[7] += b.w;
+        }
+    }
+}
+
+// ---- k_mw8w_scan2 (one CTA): exclusive prefixes of the block totals, the grand total
+template <class KT>
+__global__ void __launch_bounds__(1024) k_mw8w_scan2(const MwParams<KT> Pin) {
+    if (const LevelCtrl *pv = loop_prev_ctrl(Pin.lp)) if (pv->nmseg_next == 0) return;
+    __shared__ MwParams<KT> sP;
+    const MwParams<KT> &P = cta_params(Pin, sP);
+    __shared__ uint32_t s_w[32][MW8], s_carry[MW8];
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t ntiles = *P.ntiles_dev, nseg = *P.nseg_dev;
+    const uint32_t nblk = (ntiles + MWS_BR - 1) / MWS_BR;
+    if (tid < MW8) s_carry[tid] = 0;
+    // exclusive scan of the block totals, in place
+    for (uint32_t b0 = 0; b0 < nblk; b0 += 1024) {
+        const uint32_t bi = b0 + tid;
+        uint32_t v[MW8], inc[MW8];
+#pragma unroll
+        for (int k = 0; k < MW8; k++) v[k] = inc[k] = bi < nblk ? P.mblk[(size_t)bi * MW8 + k] : 0;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1)
+#pragma unroll
+            for (int k = 0; k < MW8; k++) {
+                const uint32_t o = __shfl_up_sync(0xffffffffu, inc[k], d);
+                if (lane >= (uint32_t)d) inc[k] += o;
+            }
+        __syncthreads();
+        if (lane == 31)
+#pragma unroll
+            for (int k = 0; k < MW8; k++) s_w[warp][k] = inc[k];
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < MW8; k++) {
+            uint32_t w = s_carry[k], all = s_carry[k];
+            for (uint32_t w2 = 0; w2 < 32; w2++) {
+                w += w2 < warp ? s_w[w2][k] : 0;
+                all += s_w[w2][k];
+            }
+            if (bi < nblk) P.mblk[(size_t)bi * MW8 + k] = w + inc[k] - v[k];
+            v[k] = all;
+        }
+        __syncthreads();
+        if (tid == 0)   // (every thread holds the same totals)
+#pragma unroll
+            for (int k = 0; k < MW8; k++) s_carry[k] = v[k];
+        __syncthreads();
+    }
+    __syncthreads();
+    // the totals over all tiles: row nblk
+    if (tid < MW8) P.mblk[(size_t)nblk * MW8 + tid] = s_carry[tid];
+}
+
+// ---- k_mw8w_seg: per segment, bucket totals (hist), starts and bases ---------------
+template <class KT>
+__global__ void __launch_bounds__(256) k_mw8w_seg(const MwParams<KT> Pin) {
+    if (const LevelCtrl *pv = loop_prev_ctrl(Pin.lp)) if (pv->nmseg_next == 0) return;
+    __shared__ MwParams<KT> sP;
+    const MwParams<KT> &P = cta_params(Pin, sP);
+    const uint32_t ntiles = *P.ntiles_dev, nseg = *P.nseg_dev;
+    const uint32_t nblk = (ntiles + MWS_BR - 1) / MWS_BR;
+    for (uint32_t si = blockIdx.x * blockDim.x + threadIdx.x; si < nseg; si += gridDim.x * blockDim.x) {
+        MSeg<KT> &m = P.msegs[si];
+        const Seg sg = m.s;
+        const uint32_t first = sg.tile_base, end = sg.tile_base + sg.ntiles;
+        uint32_t run = 0;
+#pragma unroll
+        for (int k = 0; k < MW8; k++) {
+            const uint32_t pf = P.mtab[(size_t)first * MW8 + k] + P.mblk[(size_t)(first / MWS_BR) * MW8 + k];
+            const uint32_t pe = end < ntiles ? P.mtab[(size_t)end * MW8 + k] + P.mblk[(size_t)(end / MWS_BR) * MW8 + k]
+                                             : P.mblk[(size_t)nblk * MW8 + k];
+            const uint32_t tot = pe - pf;
+            P.hist[k * P.hstride + si] = tot;
+            m.start[k] = run;
+            P.cursor[k * P.hstride + si] = sg.begin + run - pf;
+            run += tot;
+        }
+#pragma unroll
+        for (int k = MW8; k < MW_K; k++) {
+            P.hist[k * P.hstride + si] = 0;
+            m.start[k] = run;
+        }
+        BQ_CHECK(run == sg.len);
+        atomicAdd(&P.ctrl->mw_element_passes, (unsigned long long)sg.len);
+    }
+}
+
+// ---- k_mw8w_scatter ----------------------------------------------------------------
+template <class KT, int IPT>
+__global__ void __launch_bounds__(MW8W_WARPS * 32, Mw8wTune<KT>::MINB) k_mw8w_scatter(const MwParams<KT> Pin) {
+    if (const LevelCtrl *pv = loop_prev_ctrl(Pin.lp)) if (pv->nmseg_next == 0) return;
+    __shared__ MwParams<KT> sP;
+    const MwParams<KT> &P = cta_params(Pin, sP);
+    using T = typename KT::T;
+    using WS = Mw8wWarpSmem<KT, IPT>;
+    constexpr uint32_t TILE = (uint32_t)tile_elems<KT>(), RK = 32u * IPT;
+    static_assert(TILE % RK == 0 && IPT <= 8, "rounds per tile; byte-field scans");
+    extern __shared__ __align__(16) unsigned char smraw[];
+    WS &ws = reinterpret_cast<WS *>(smraw)[threadIdx.x >> 5];
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t ntiles = *P.ntiles_dev;
+    uint32_t cls_seg = 0xffffffffu, par = 0;
+    Mw8Cls<KT> cls;
+    for (uint32_t t = blockIdx.x * MW8W_WARPS + (threadIdx.x >> 5); t < ntiles; t += gridDim.x * MW8W_WARPS) {
+        const uint32_t si = P.tile_map[t];
+        const Seg sg = P.msegs[si].s;
+        if (si != cls_seg) {
+            mw8w_load_cls<KT>(P, si, cls);
+            cls_seg = si;
+        }
+        const TileGeom<KT, TILE> G(sg, t);
+        const T *src = (sg.parity ? P.bufs[1] : P.bufs[0]) + G.tbeg;
+        T *dst = sg.parity ? P.bufs[0] : P.bufs[1];
+        // lane b < 8: the global index of this tile's next key of bucket b
+        uint32_t off = 0;
+        if (lane < MW8)
+            off = P.cursor[lane * P.hstride + si] + P.mtab[(size_t)t * MW8 + lane] +
+                  P.mblk[(size_t)(t / MWS_BR) * MW8 + lane];
+        // rounds, the next one's keys loaded while the current one is placed
+        uint32_t r0 = G.vlo / RK * RK;
+#if BQ_MW8W_PF
+        T xn[IPT];
+        uint32_t vn = mw8w_load<KT, IPT>(src, r0, G.vlo, G.vhi, lane, P.aligned, xn);
+#endif
+        for (; r0 < G.vhi; r0 += RK, par ^= 1) {
+            T x[IPT];
+#if BQ_MW8W_PF
+#pragma unroll
+            for (int c = 0; c < IPT; c++) x[c] = xn[c];
+            const uint32_t valid = vn;
+            if (r0 + RK < G.vhi) vn = mw8w_load<KT, IPT>(src, r0 + RK, G.vlo, G.vhi, lane, P.aligned, xn);
+#else
+            const uint32_t valid = mw8w_load<KT, IPT>(src, r0, G.vlo, G.vhi, lane, P.aligned, x);
+#endif
+            // (full rounds, the common case, skip every validity test)
+            auto round = [&](auto full_tag) {
+                constexpr bool FULL = decltype(full_tag)::value;
+                uint32_t bk[IPT], rk[IPT];
+                mw8_classify<KT, IPT>(cls, x, bk);
+                Mw8Ctr<IPT> ctr;
+#pragma unroll
+                for (int c = 0; c < IPT; c++) rk[c] = ctr.take(bk[c], FULL ? 1u : (valid >> c) & 1);
+                uint32_t ex[MW8 / 2], tot[MW8 / 2];
+                mw8_scan<IPT>(ctr, lane, ex, tot);
+                // the round's bucket starts rs (16-bit pairs: word k = buckets 2k, 2k+1)
+                uint32_t rs[MW8 / 2], run = 0;
+#pragma unroll
+                for (int k = 0; k < MW8 / 2; k++) {
+                    tot[k] = __shfl_sync(0xffffffffu, tot[k], 31);
+                    const uint32_t lo = tot[k] & 0xffff;
+                    rs[k] = run | ((run + lo) << 16);
+                    run += lo + (tot[k] >> 16);
+                    ex[k] += rs[k];   // slot base of this lane's keys of each bucket
+                }
+                if (lane < MW8) {
+                    const uint32_t wb = (lane & 4) ? ((lane & 2) ? rs[3] : rs[2]) : ((lane & 2) ? rs[1] : rs[0]);
+                    const uint32_t tw = (lane & 4) ? ((lane & 2) ? tot[3] : tot[2]) : ((lane & 2) ? tot[1] : tot[0]);
+                    const uint32_t rsb = (lane & 1) ? (wb >> 16) : (wb & 0xffff);
+                    ws.ob[par][lane] = off - rsb;
+                    off += (lane & 1) ? (tw >> 16) : (tw & 0xffff);
+                }
+                // stage the round bucket by bucket
+#pragma unroll
+                for (int c = 0; c < IPT; c++) {
+                    if (FULL || ((valid >> c) & 1)) {
+                        const uint32_t b = bk[c];
+                        const uint32_t w01 = (b & 2) ? ex[1] : ex[0], w23 = (b & 2) ? ex[3] : ex[2];
+                        const uint32_t w = (b & 4) ? w23 : w01;
+                        const uint32_t slot = ((b & 1) ? (w >> 16) : (w & 0xffff)) + rk[c];
+                        BQ_CHECK(slot < RK);
+                        ws.key[par][slot] = x[c];
+                        ws.tag[par][slot] = (uint8_t)b;
+                    }
+                }
+                __syncwarp();
+                // store: slot j of bucket b goes to ob[b] + j (contiguous per bucket)
+#pragma unroll
+                for (uint32_t m = 0; m < (uint32_t)IPT; m++) {
+                    const uint32_t j = m * 32 + lane;
+                    if (FULL || j < run) {
+                        const uint32_t g = ws.ob[par][ws.tag[par][j]] + j;
+                        BQ_CHECK(g < P.n_total);
+                        dst[g] = ws.key[par][j];
+                    }
+                }
+            };
+            if (__all_sync(0xffffffffu, valid == (1u << IPT) - 1)) round(std::true_type{});
+            else round(std::false_type{});
+        }
+    }
+}
+
+}  // namespace bq

@@ -133,6 +133,7 @@ __device__ __forceinline__ void loop_resolve(PassParams<KT> &P) {
 #include "partition_fast.cuh"
 #include "multiway.cuh"
 #include "multiway8.cuh"
+#include "multiway8w.cuh"
 #include "inplace.cuh"
 
 namespace bq {
