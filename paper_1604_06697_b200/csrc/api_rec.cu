@@ -40,8 +40,12 @@ __global__ void k_ki_gather(const Rec32 *copy, const KeyIdx16 *p, Rec32 *out, ui
 #pragma unroll
         for (int u = 0; u < U; u++) {
             if (i0 + u * stride < n) {
-                v[u][0] = __ldg(r4 + 2 * k[u]);
-                v[u][1] = __ldg(r4 + 2 * k[u] + 1);
+                // one 32-byte load per record (sm_100's 256-bit LDG) with a 64-byte
+                // DRAM fetch hint: 2.1 B fetched per byte used instead of 4.2
+                asm volatile("ld.global.nc.L2::64B.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                             : "=r"(v[u][0].x), "=r"(v[u][0].y), "=r"(v[u][0].z), "=r"(v[u][0].w),
+                               "=r"(v[u][1].x), "=r"(v[u][1].y), "=r"(v[u][1].z), "=r"(v[u][1].w)
+                             : "l"(r4 + 2 * k[u]));
             }
         }
 #pragma unroll
