@@ -26,13 +26,10 @@ namespace bq {
 constexpr uint32_t MWS_BR = 2048;   // tiles per block of the tile-count scan (8 per thread)
 constexpr int MW8W_WARPS = 8;       // warps per CTA of the count and scatter kernels
 #ifndef BQ_MW8W_MINB
-#define BQ_MW8W_MINB 3
+#define BQ_MW8W_MINB 2
 #endif
 #ifndef BQ_MW8W_MINB_PAIR
-#define BQ_MW8W_MINB_PAIR 3
-#endif
-#ifndef BQ_MW8W_PF
-#define BQ_MW8W_PF 0   // load the next round's keys while the current round is placed
+#define BQ_MW8W_MINB_PAIR 2
 #endif
 
 template <class KT> struct Mw8wTune;
@@ -46,6 +43,7 @@ template <> struct Mw8wTune<KPair> { static constexpr int IPT = 4, MINB = BQ_MW8
 template <class KT, int IPT>
 struct Mw8wWarpSmem {
     static constexpr int RK = 32 * IPT;
+    uint4 in[2][RK * sizeof(typename KT::T) / 16];   // the next round's keys (cp.async), by parity
     typename KT::T key[2][RK];
     uint8_t tag[2][RK];          // the staged key's bucket
     uint32_t ob[2][MW8];         // global index of staged slot 0 of each bucket's run
@@ -284,7 +282,64 @@ __global__ void __launch_bounds__(256) k_mw8w_seg(const MwParams<KT> Pin) {
     }
 }
 
+// per-lane asynchronous 16-byte copies global -> shared (LDGSTS), one group per round
+__device__ __forceinline__ void cp_async16(void *sdst, const void *gsrc) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(sdst)),
+                 "l"(gsrc)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+// the tile a warp places next: its segment, source, destination and valid range
+template <class KT>
+struct Mw8wTile {
+    uint32_t t, si, vlo, vhi;
+    const typename KT::T *src;   // the buffer + the tile's first position
+    typename KT::T *dst;
+};
+template <class KT>
+__device__ __forceinline__ Mw8wTile<KT> mw8w_tile(const MwParams<KT> &P, uint32_t t) {
+    constexpr uint32_t TILE = (uint32_t)tile_elems<KT>();
+    Mw8wTile<KT> w;
+    w.t = t;
+    w.si = P.tile_map[t];
+    const Seg sg = P.msegs[w.si].s;
+    const TileGeom<KT, TILE> G(sg, t);
+    w.vlo = G.vlo;
+    w.vhi = G.vhi;
+    w.src = (sg.parity ? P.bufs[1] : P.bufs[0]) + G.tbeg;
+    w.dst = sg.parity ? P.bufs[0] : P.bufs[1];
+    return w;
+}
+
+// Round r0 of tile w into the lane's slots of a shared-memory input buffer
+// (vector v of lane L at in[v * 32 + L]: the layout mw8w_load reads from
+// global memory): whole valid vectors by asynchronous copies, vectors cut by
+// the valid range element by element (zeros outside it).
+template <class KT, int IPT>
+__device__ __forceinline__ void mw8w_issue(const Mw8wTile<KT> &w, uint32_t r0, uint32_t lane, bool vec, uint4 *in) {
+    using T = typename KT::T;
+    constexpr uint32_t VW = sizeof(T) >= 16 ? 1u : 16u / (uint32_t)sizeof(T), NV = IPT / VW;
+#pragma unroll
+    for (uint32_t v = 0; v < NV; v++) {
+        const uint32_t pos = r0 + v * 32 * VW + lane * VW;
+        uint4 *d = &in[v * 32 + lane];
+        if (vec && pos >= w.vlo && pos + VW <= w.vhi) {
+            cp_async16(d, w.src + pos);
+        } else {
+            T e[VW];
+#pragma unroll
+            for (uint32_t k = 0; k < VW; k++) e[k] = (pos + k >= w.vlo && pos + k < w.vhi) ? w.src[pos + k] : T{};
+            memcpy(d, e, 16);
+        }
+    }
+}
+
 // ---- k_mw8w_scatter ----------------------------------------------------------------
+// Each warp runs one pipeline over its rounds (across its tiles): the next
+// round's keys are copied into the other input buffer while the current
+// round is classified, ranked, staged and stored.
 template <class KT, int IPT>
 __global__ void __launch_bounds__(MW8W_WARPS * 32, Mw8wTune<KT>::MINB) k_mw8w_scatter(const MwParams<KT> Pin) {
     if (const LevelCtrl *pv = loop_prev_ctrl(Pin.lp)) if (pv->nmseg_next == 0) return;
@@ -293,99 +348,122 @@ __global__ void __launch_bounds__(MW8W_WARPS * 32, Mw8wTune<KT>::MINB) k_mw8w_sc
     using T = typename KT::T;
     using WS = Mw8wWarpSmem<KT, IPT>;
     constexpr uint32_t TILE = (uint32_t)tile_elems<KT>(), RK = 32u * IPT;
+    constexpr uint32_t VW = sizeof(T) >= 16 ? 1u : 16u / (uint32_t)sizeof(T), NV = IPT / VW;
     static_assert(TILE % RK == 0 && IPT <= 8, "rounds per tile; byte-field scans");
     extern __shared__ __align__(16) unsigned char smraw[];
     WS &ws = reinterpret_cast<WS *>(smraw)[threadIdx.x >> 5];
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t ntiles = *P.ntiles_dev;
-    uint32_t cls_seg = 0xffffffffu, par = 0;
+    const uint32_t stride = gridDim.x * MW8W_WARPS;
+    uint32_t t = blockIdx.x * MW8W_WARPS + (threadIdx.x >> 5);
+    if (t >= ntiles) return;
+    const bool vec = P.aligned;
+    Mw8wTile<KT> cur = mw8w_tile(P, t);
+    uint32_t r0 = cur.vlo / RK * RK, par = 0, cls_seg = 0xffffffffu, off = 0;
+    bool new_tile = true;
     Mw8Cls<KT> cls;
-    for (uint32_t t = blockIdx.x * MW8W_WARPS + (threadIdx.x >> 5); t < ntiles; t += gridDim.x * MW8W_WARPS) {
-        const uint32_t si = P.tile_map[t];
-        const Seg sg = P.msegs[si].s;
-        if (si != cls_seg) {
-            mw8w_load_cls<KT>(P, si, cls);
-            cls_seg = si;
+    mw8w_issue<KT, IPT>(cur, r0, lane, vec, ws.in[0]);
+    cp_async_commit();
+    for (;;) {
+        // the next round: of this tile, or the first of the warp's next tile
+        Mw8wTile<KT> nxt = cur;
+        uint32_t nr0 = r0 + RK;
+        bool more = true;
+        if (nr0 >= cur.vhi) {
+            if (cur.t + stride < ntiles) {
+                nxt = mw8w_tile(P, cur.t + stride);
+                nr0 = nxt.vlo / RK * RK;
+            } else {
+                more = false;
+            }
         }
-        const TileGeom<KT, TILE> G(sg, t);
-        const T *src = (sg.parity ? P.bufs[1] : P.bufs[0]) + G.tbeg;
-        T *dst = sg.parity ? P.bufs[0] : P.bufs[1];
-        // lane b < 8: the global index of this tile's next key of bucket b
-        uint32_t off = 0;
-        if (lane < MW8)
-            off = P.cursor[lane * P.hstride + si] + P.mtab[(size_t)t * MW8 + lane] +
-                  P.mblk[(size_t)(t / MWS_BR) * MW8 + lane];
-        // rounds, the next one's keys loaded while the current one is placed
-        uint32_t r0 = G.vlo / RK * RK;
-#if BQ_MW8W_PF
-        T xn[IPT];
-        uint32_t vn = mw8w_load<KT, IPT>(src, r0, G.vlo, G.vhi, lane, P.aligned, xn);
-#endif
-        for (; r0 < G.vhi; r0 += RK, par ^= 1) {
-            T x[IPT];
-#if BQ_MW8W_PF
-#pragma unroll
-            for (int c = 0; c < IPT; c++) x[c] = xn[c];
-            const uint32_t valid = vn;
-            if (r0 + RK < G.vhi) vn = mw8w_load<KT, IPT>(src, r0 + RK, G.vlo, G.vhi, lane, P.aligned, xn);
-#else
-            const uint32_t valid = mw8w_load<KT, IPT>(src, r0, G.vlo, G.vhi, lane, P.aligned, x);
-#endif
-            // (full rounds, the common case, skip every validity test)
-            auto round = [&](auto full_tag) {
-                constexpr bool FULL = decltype(full_tag)::value;
-                uint32_t bk[IPT], rk[IPT];
-                mw8_classify<KT, IPT>(cls, x, bk);
-                Mw8Ctr<IPT> ctr;
-#pragma unroll
-                for (int c = 0; c < IPT; c++) rk[c] = ctr.take(bk[c], FULL ? 1u : (valid >> c) & 1);
-                uint32_t ex[MW8 / 2], tot[MW8 / 2];
-                mw8_scan<IPT>(ctr, lane, ex, tot);
-                // the round's bucket starts rs (16-bit pairs: word k = buckets 2k, 2k+1)
-                uint32_t rs[MW8 / 2], run = 0;
-#pragma unroll
-                for (int k = 0; k < MW8 / 2; k++) {
-                    tot[k] = __shfl_sync(0xffffffffu, tot[k], 31);
-                    const uint32_t lo = tot[k] & 0xffff;
-                    rs[k] = run | ((run + lo) << 16);
-                    run += lo + (tot[k] >> 16);
-                    ex[k] += rs[k];   // slot base of this lane's keys of each bucket
-                }
-                if (lane < MW8) {
-                    const uint32_t wb = (lane & 4) ? ((lane & 2) ? rs[3] : rs[2]) : ((lane & 2) ? rs[1] : rs[0]);
-                    const uint32_t tw = (lane & 4) ? ((lane & 2) ? tot[3] : tot[2]) : ((lane & 2) ? tot[1] : tot[0]);
-                    const uint32_t rsb = (lane & 1) ? (wb >> 16) : (wb & 0xffff);
-                    ws.ob[par][lane] = off - rsb;
-                    off += (lane & 1) ? (tw >> 16) : (tw & 0xffff);
-                }
-                // stage the round bucket by bucket
-#pragma unroll
-                for (int c = 0; c < IPT; c++) {
-                    if (FULL || ((valid >> c) & 1)) {
-                        const uint32_t b = bk[c];
-                        const uint32_t w01 = (b & 2) ? ex[1] : ex[0], w23 = (b & 2) ? ex[3] : ex[2];
-                        const uint32_t w = (b & 4) ? w23 : w01;
-                        const uint32_t slot = ((b & 1) ? (w >> 16) : (w & 0xffff)) + rk[c];
-                        BQ_CHECK(slot < RK);
-                        ws.key[par][slot] = x[c];
-                        ws.tag[par][slot] = (uint8_t)b;
-                    }
-                }
-                __syncwarp();
-                // store: slot j of bucket b goes to ob[b] + j (contiguous per bucket)
-#pragma unroll
-                for (uint32_t m = 0; m < (uint32_t)IPT; m++) {
-                    const uint32_t j = m * 32 + lane;
-                    if (FULL || j < run) {
-                        const uint32_t g = ws.ob[par][ws.tag[par][j]] + j;
-                        BQ_CHECK(g < P.n_total);
-                        dst[g] = ws.key[par][j];
-                    }
-                }
-            };
-            if (__all_sync(0xffffffffu, valid == (1u << IPT) - 1)) round(std::true_type{});
-            else round(std::false_type{});
+        if (more) mw8w_issue<KT, IPT>(nxt, nr0, lane, vec, ws.in[par ^ 1]);
+        cp_async_commit();
+        if (new_tile) {
+            if (cur.si != cls_seg) {
+                mw8w_load_cls<KT>(P, cur.si, cls);
+                cls_seg = cur.si;
+            }
+            // lane b < 8: the global index of this tile's next key of bucket b
+            if (lane < MW8)
+                off = P.cursor[lane * P.hstride + cur.si] + P.mtab[(size_t)cur.t * MW8 + lane] +
+                      P.mblk[(size_t)(cur.t / MWS_BR) * MW8 + lane];
         }
+        cp_async_wait1();   // this round's copies (the lane reads only its own slots)
+        T x[IPT];
+#pragma unroll
+        for (uint32_t v = 0; v < NV; v++) {
+            const uint4 q = ws.in[par][v * 32 + lane];
+            memcpy(&x[v * VW], &q, 16);
+        }
+        uint32_t valid = 0;
+#pragma unroll
+        for (uint32_t v = 0; v < NV; v++)
+#pragma unroll
+            for (uint32_t e = 0; e < VW; e++) {
+                const uint32_t pos = r0 + v * 32 * VW + lane * VW + e;
+                valid |= (uint32_t)(pos >= cur.vlo && pos < cur.vhi) << (v * VW + e);
+            }
+        T *dst = cur.dst;
+        // (full rounds, the common case, skip every validity test)
+        auto round = [&](auto full_tag) {
+            constexpr bool FULL = decltype(full_tag)::value;
+            uint32_t bk[IPT], rk[IPT];
+            mw8_classify<KT, IPT>(cls, x, bk);
+            Mw8Ctr<IPT> ctr;
+#pragma unroll
+            for (int c = 0; c < IPT; c++) rk[c] = ctr.take(bk[c], FULL ? 1u : (valid >> c) & 1);
+            uint32_t ex[MW8 / 2], tot[MW8 / 2];
+            mw8_scan<IPT>(ctr, lane, ex, tot);
+            // the round's bucket starts rs (16-bit pairs: word k = buckets 2k, 2k+1)
+            uint32_t rs[MW8 / 2], run = 0;
+#pragma unroll
+            for (int k = 0; k < MW8 / 2; k++) {
+                tot[k] = __shfl_sync(0xffffffffu, tot[k], 31);
+                const uint32_t lo = tot[k] & 0xffff;
+                rs[k] = run | ((run + lo) << 16);
+                run += lo + (tot[k] >> 16);
+                ex[k] += rs[k];   // slot base of this lane's keys of each bucket
+            }
+            if (lane < MW8) {
+                const uint32_t wb = (lane & 4) ? ((lane & 2) ? rs[3] : rs[2]) : ((lane & 2) ? rs[1] : rs[0]);
+                const uint32_t tw = (lane & 4) ? ((lane & 2) ? tot[3] : tot[2]) : ((lane & 2) ? tot[1] : tot[0]);
+                const uint32_t rsb = (lane & 1) ? (wb >> 16) : (wb & 0xffff);
+                ws.ob[par][lane] = off - rsb;
+                off += (lane & 1) ? (tw >> 16) : (tw & 0xffff);
+            }
+            // stage the round bucket by bucket
+#pragma unroll
+            for (int c = 0; c < IPT; c++) {
+                if (FULL || ((valid >> c) & 1)) {
+                    const uint32_t b = bk[c];
+                    const uint32_t w01 = (b & 2) ? ex[1] : ex[0], w23 = (b & 2) ? ex[3] : ex[2];
+                    const uint32_t w = (b & 4) ? w23 : w01;
+                    const uint32_t slot = ((b & 1) ? (w >> 16) : (w & 0xffff)) + rk[c];
+                    BQ_CHECK(slot < RK);
+                    ws.key[par][slot] = x[c];
+                    ws.tag[par][slot] = (uint8_t)b;
+                }
+            }
+            __syncwarp();
+            // store: slot j of bucket b goes to ob[b] + j (contiguous per bucket)
+#pragma unroll
+            for (uint32_t m = 0; m < (uint32_t)IPT; m++) {
+                const uint32_t j = m * 32 + lane;
+                if (FULL || j < run) {
+                    const uint32_t g = ws.ob[par][ws.tag[par][j]] + j;
+                    BQ_CHECK(g < P.n_total);
+                    dst[g] = ws.key[par][j];
+                }
+            }
+        };
+        if (__all_sync(0xffffffffu, valid == (1u << IPT) - 1)) round(std::true_type{});
+        else round(std::false_type{});
+        par ^= 1;
+        if (!more) break;
+        new_tile = nxt.t != cur.t;
+        cur = nxt;
+        r0 = nr0;
     }
 }
 
