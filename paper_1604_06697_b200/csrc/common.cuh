@@ -287,7 +287,7 @@ struct alignas(64) LevelCtrl {
     uint32_t mw_ticket_scatter;  // tile tickets of the multiway scatter kernel
     uint32_t nmseg_next;         // multiway children appended to the next level
     uint32_t nmtiles_next;       // their tiles
-    uint32_t pad1;
+    uint32_t mw_scan_done;       // 8-way: blocks of the tile-count scan done (multiway8w.cuh)
     unsigned long long mw_element_passes;   // sum of multiway-partitioned lengths this level
     uint32_t pad2[6];
 };

@@ -180,11 +180,7 @@ bq_status launch_multiway(MwParams<KT> MP, LevelCtrl *lc, cudaStream_t s, int wa
         kc<<<cap_c, tw, 0, s>>>(MP);
         BQ_CK_LAUNCH();
         const uint32_t nb = (MP.max_tiles + MWS_BR - 1) / MWS_BR;
-        k_mw8w_scan1<KT><<<nb < 592 ? nb : 592, 256, 0, s>>>(MP);
-        BQ_CK_LAUNCH();
-        k_mw8w_scan2<KT><<<1, 1024, 0, s>>>(MP);
-        BQ_CK_LAUNCH();
-        k_mw8w_seg<KT><<<POST_GRID / 8, 256, 0, s>>>(MP);
+        k_mw8w_scan<KT><<<nb < 592 ? nb : 592, 256, 0, s>>>(MP);
         BQ_CK_LAUNCH();
         ks<<<cap_s, tw, smemw, s>>>(MP);
         BQ_CK_LAUNCH();
@@ -677,6 +673,7 @@ bq_status make_plan(SortPlan<KT> &pl, typename KT::T *data, size_t n, void *ws, 
     MP.mtab = reinterpret_cast<uint32_t *>(w + L.mtab);
     MP.mblk = reinterpret_cast<uint32_t *>(w + L.mblk);
     MP.max_tiles = (uint32_t)L.max_tiles;
+    MP.tabmode = (BQ_MW8W && pl.ways == MW8) ? 1 : 0;
     MP.n_total = n;
     MP.aligned = pl.aligned;
     MP.lp = lp;
@@ -1108,7 +1105,7 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
             cleanup();
             return set_error(BQ_ERR_CUDA, "leaf list overflow");
         }
-        const int per_level = 4 + (KT::is_record ? 1 : 0) + (ways > 2 ? ((BQ_MW8W && ways == MW8) ? 6 : 4) : 0);
+        const int per_level = 4 + (KT::is_record ? 1 : 0) + (ways > 2 ? 4 : 0);
         local.kernel_launches = 1 + levels * per_level + hm.nflush * (NCLS + 1 + (KT::is_record && !ordered ? 1 : 0)) +
                                 (hm.fb_count ? 4 : 0);
         for (int l = 0; l < levels; l++) {

@@ -174,6 +174,7 @@ struct MwParams {
     uint32_t *mtab;      // 8-way (multiway8w.cuh): per-tile bucket counts, then their prefix
     uint32_t *mblk;      // 8-way: per-block totals, then block prefixes
     uint32_t max_tiles;  // rows of mtab
+    int tabmode;         // 8-way levels by multiway8w.cuh: children from mtab / mblk
 };
 
 template <class KT>

@@ -5,17 +5,17 @@
 // move and moves them in a second loop (Alg. 3); with k buckets the
 // offsets become k counters (Super Scalar Sample Sort's "oracle").
 // Here one warp owns a whole tile (TILE = tile_elems<KT>() keys, processed in
-// rounds of 32 x IPT keys), and a level is five launches:
+// rounds of 32 x IPT keys), and a level is three launches (+ k_post_mw):
 //   k_mw8w_count    every tile's 8 bucket counts -> tab[t][b]      (read pass)
-//   k_mw8w_scan1    prefix of tab over the tiles of blocks of MWS_BR tiles
-//   k_mw8w_scan2    block prefixes (one CTA)
-//   k_mw8w_seg      per segment: bucket totals (hist), bucket starts
-//                   (MSeg::start) and the bucket bases (cursor) such that
-//                   tile t's keys of bucket b go to
-//                   cursor[b][seg] + tab[t][b] + blk[t / MWS_BR][b]
+//   k_mw8w_scan     prefixes of tab over the tiles (blocks of MWS_BR tiles, the
+//                   block prefixes by the CTA finishing last)
 //   k_mw8w_scatter  per round: classify, rank inside the warp (packed counters
 //                   and a byte-field warp scan), stage the round bucket by
-//                   bucket in the warp's shared memory, store it coalesced
+//                   bucket in the warp's shared memory, store it coalesced;
+//                   a segment's bucket b starts at its begin + the totals of
+//                   buckets < b (mw8w_seg_buckets), and tile t's keys of b
+//                   follow those of the segment's earlier tiles
+// (k_post_mw derives the children from the same table.)
 // Tiles of a segment are consecutive and a bucket receives them in tile
 // order, so the layout of a level is deterministic.  Splitters, classification
 // (float64 compares as doubles, R25) and counters are multiway8.cuh's.
@@ -142,16 +142,55 @@ __global__ void __launch_bounds__(MW8W_WARPS * 32) k_mw8w_count(const MwParams<K
     }
 }
 
-// ---- k_mw8w_scan1: exclusive prefix of the tile counts inside blocks of MWS_BR tiles
+// exclusive scan of 8 columns over the 256 threads of a CTA: ex = this
+// thread's prefix, the return value's columns = the totals (every thread)
+__device__ __forceinline__ void mw8w_cta_scan8(const uint32_t (&v)[MW8], uint32_t (&ex)[MW8], uint32_t (&tot)[MW8],
+                                               uint32_t (*s_w)[MW8]) {
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    uint32_t inc[MW8];
+#pragma unroll
+    for (int k = 0; k < MW8; k++) inc[k] = v[k];
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1)
+#pragma unroll
+        for (int k = 0; k < MW8; k++) {
+            const uint32_t o = __shfl_up_sync(0xffffffffu, inc[k], d);
+            if (lane >= (uint32_t)d) inc[k] += o;
+        }
+    __syncthreads();   // s_w of a previous use read
+    if (lane == 31)
+#pragma unroll
+        for (int k = 0; k < MW8; k++) s_w[warp][k] = inc[k];
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < MW8; k++) {
+        uint32_t w = 0, all = 0;
+#pragma unroll
+        for (uint32_t w2 = 0; w2 < 8; w2++) {
+            w += w2 < warp ? s_w[w2][k] : 0;
+            all += s_w[w2][k];
+        }
+        ex[k] = w + inc[k] - v[k];
+        tot[k] = all;
+    }
+}
+
+// ---- k_mw8w_scan: prefix of the tile counts --------------------------------------
+// Blocks of MWS_BR tiles: tab[t] becomes the prefix of t inside its block and
+// blk[i] the total of block i; the CTA that completes the last block turns
+// blk into exclusive block prefixes (row nblk: the grand total).  The global
+// prefix of tile t is then tab[t] + blk[t / MWS_BR].
 template <class KT>
-__global__ void __launch_bounds__(256) k_mw8w_scan1(const MwParams<KT> Pin) {
+__global__ void __launch_bounds__(256) k_mw8w_scan(const MwParams<KT> Pin) {
     if (const LevelCtrl *pv = loop_prev_ctrl(Pin.lp)) if (pv->nmseg_next == 0) return;
     __shared__ MwParams<KT> sP;
     const MwParams<KT> &P = cta_params(Pin, sP);
     __shared__ uint32_t s_w[8][MW8];
-    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint32_t ntiles = *P.ntiles_dev;
-    for (uint32_t blk = blockIdx.x; blk * MWS_BR < ntiles; blk += gridDim.x) {
+    __shared__ uint32_t s_last;
+    const uint32_t tid = threadIdx.x;
+    const uint32_t ntiles = *P.ntiles_dev, nblk = (ntiles + MWS_BR - 1) / MWS_BR;
+    uint32_t done = 0;
+    for (uint32_t blk = blockIdx.x; blk < nblk; blk += gridDim.x, done++) {
         const uint32_t t0 = blk * MWS_BR + tid * 8;
         uint32_t sum[MW8] = {0, 0, 0, 0, 0, 0, 0, 0};
         for (uint32_t t = t0; t < t0 + 8 && t < ntiles; t++) {
@@ -160,33 +199,11 @@ __global__ void __launch_bounds__(256) k_mw8w_scan1(const MwParams<KT> Pin) {
             sum[0] += a.x; sum[1] += a.y; sum[2] += a.z; sum[3] += a.w;
             sum[4] += b.x; sum[5] += b.y; sum[6] += b.z; sum[7] += b.w;
         }
-        uint32_t inc[MW8];
+        uint32_t pre[MW8], all[MW8];
+        mw8w_cta_scan8(sum, pre, all, s_w);
+        if (tid == 0)
 #pragma unroll
-        for (int k = 0; k < MW8; k++) inc[k] = sum[k];
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1)
-#pragma unroll
-            for (int k = 0; k < MW8; k++) {
-                const uint32_t o = __shfl_up_sync(0xffffffffu, inc[k], d);
-                if (lane >= (uint32_t)d) inc[k] += o;
-            }
-        __syncthreads();   // s_w of the previous block read
-        if (lane == 31)
-#pragma unroll
-            for (int k = 0; k < MW8; k++) s_w[warp][k] = inc[k];
-        __syncthreads();
-        uint32_t pre[MW8];
-#pragma unroll
-        for (int k = 0; k < MW8; k++) {
-            uint32_t w = 0, all = 0;
-#pragma unroll
-            for (uint32_t w2 = 0; w2 < 8; w2++) {
-                w += w2 < warp ? s_w[w2][k] : 0;
-                all += s_w[w2][k];
-            }
-            pre[k] = w + inc[k] - sum[k];
-            if (tid == 0) P.mblk[(size_t)blk * MW8 + k] = all;
-        }
+            for (int k = 0; k < MW8; k++) P.mblk[(size_t)blk * MW8 + k] = all[k];
         for (uint32_t t = t0; t < t0 + 8 && t < ntiles; t++) {
             uint4 *row = reinterpret_cast<uint4 *>(P.mtab + (size_t)t * MW8);
             const uint4 a = row[0], b = row[1];
@@ -196,90 +213,59 @@ __global__ void __launch_bounds__(256) k_mw8w_scan1(const MwParams<KT> Pin) {
             pre[4] += b.x; pre[5] += b.y; pre[6] += b.z; pre[7] += b.w;
         }
     }
-}
-
-// ---- k_mw8w_scan2 (one CTA): exclusive prefixes of the block totals, the grand total
-template <class KT>
-__global__ void __launch_bounds__(1024) k_mw8w_scan2(const MwParams<KT> Pin) {
-    if (const LevelCtrl *pv = loop_prev_ctrl(Pin.lp)) if (pv->nmseg_next == 0) return;
-    __shared__ MwParams<KT> sP;
-    const MwParams<KT> &P = cta_params(Pin, sP);
-    __shared__ uint32_t s_w[32][MW8], s_carry[MW8];
-    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint32_t ntiles = *P.ntiles_dev, nseg = *P.nseg_dev;
-    const uint32_t nblk = (ntiles + MWS_BR - 1) / MWS_BR;
-    if (tid < MW8) s_carry[tid] = 0;
-    // exclusive scan of the block totals, in place
-    for (uint32_t b0 = 0; b0 < nblk; b0 += 1024) {
-        const uint32_t bi = b0 + tid;
-        uint32_t v[MW8], inc[MW8];
-#pragma unroll
-        for (int k = 0; k < MW8; k++) v[k] = inc[k] = bi < nblk ? P.mblk[(size_t)bi * MW8 + k] : 0;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1)
-#pragma unroll
-            for (int k = 0; k < MW8; k++) {
-                const uint32_t o = __shfl_up_sync(0xffffffffu, inc[k], d);
-                if (lane >= (uint32_t)d) inc[k] += o;
-            }
-        __syncthreads();
-        if (lane == 31)
-#pragma unroll
-            for (int k = 0; k < MW8; k++) s_w[warp][k] = inc[k];
-        __syncthreads();
-#pragma unroll
-        for (int k = 0; k < MW8; k++) {
-            uint32_t w = s_carry[k], all = s_carry[k];
-            for (uint32_t w2 = 0; w2 < 32; w2++) {
-                w += w2 < warp ? s_w[w2][k] : 0;
-                all += s_w[w2][k];
-            }
-            if (bi < nblk) P.mblk[(size_t)bi * MW8 + k] = w + inc[k] - v[k];
-            v[k] = all;
-        }
-        __syncthreads();
-        if (tid == 0)   // (every thread holds the same totals)
-#pragma unroll
-            for (int k = 0; k < MW8; k++) s_carry[k] = v[k];
-        __syncthreads();
-    }
+    __threadfence();
     __syncthreads();
-    // the totals over all tiles: row nblk
-    if (tid < MW8) P.mblk[(size_t)nblk * MW8 + tid] = s_carry[tid];
-}
-
-// ---- k_mw8w_seg: per segment, bucket totals (hist), starts and bases ---------------
-template <class KT>
-__global__ void __launch_bounds__(256) k_mw8w_seg(const MwParams<KT> Pin) {
-    if (const LevelCtrl *pv = loop_prev_ctrl(Pin.lp)) if (pv->nmseg_next == 0) return;
-    __shared__ MwParams<KT> sP;
-    const MwParams<KT> &P = cta_params(Pin, sP);
-    const uint32_t ntiles = *P.ntiles_dev, nseg = *P.nseg_dev;
-    const uint32_t nblk = (ntiles + MWS_BR - 1) / MWS_BR;
-    for (uint32_t si = blockIdx.x * blockDim.x + threadIdx.x; si < nseg; si += gridDim.x * blockDim.x) {
-        MSeg<KT> &m = P.msegs[si];
-        const Seg sg = m.s;
-        const uint32_t first = sg.tile_base, end = sg.tile_base + sg.ntiles;
-        uint32_t run = 0;
+    if (tid == 0) s_last = done > 0 && atomicAdd(&P.ctrl->mw_scan_done, done) + done == nblk;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    uint32_t carry[MW8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (uint32_t b0 = 0; b0 < nblk; b0 += 256) {
+        const uint32_t bi = b0 + tid;
+        uint32_t v[MW8], ex[MW8], tot[MW8];
+#pragma unroll
+        for (int k = 0; k < MW8; k++) v[k] = bi < nblk ? __ldcg(&P.mblk[(size_t)bi * MW8 + k]) : 0;
+        mw8w_cta_scan8(v, ex, tot, s_w);
 #pragma unroll
         for (int k = 0; k < MW8; k++) {
-            const uint32_t pf = P.mtab[(size_t)first * MW8 + k] + P.mblk[(size_t)(first / MWS_BR) * MW8 + k];
-            const uint32_t pe = end < ntiles ? P.mtab[(size_t)end * MW8 + k] + P.mblk[(size_t)(end / MWS_BR) * MW8 + k]
-                                             : P.mblk[(size_t)nblk * MW8 + k];
-            const uint32_t tot = pe - pf;
-            P.hist[k * P.hstride + si] = tot;
-            m.start[k] = run;
-            P.cursor[k * P.hstride + si] = sg.begin + run - pf;
-            run += tot;
+            if (bi < nblk) P.mblk[(size_t)bi * MW8 + k] = carry[k] + ex[k];
+            carry[k] += tot[k];
         }
-#pragma unroll
-        for (int k = MW8; k < MW_K; k++) {
-            P.hist[k * P.hstride + si] = 0;
-            m.start[k] = run;
-        }
-        BQ_CHECK(run == sg.len);
-        atomicAdd(&P.ctrl->mw_element_passes, (unsigned long long)sg.len);
     }
+    if (tid == 0) {
+        unsigned long long all = 0;
+#pragma unroll
+        for (int k = 0; k < MW8; k++) {
+            P.mblk[(size_t)nblk * MW8 + k] = carry[k];
+            all += carry[k];
+        }
+        atomicAdd(&P.ctrl->mw_element_passes, all);
+    }
+}
+
+// Lanes b < 8 of a warp: segment si's bucket b total (tot) and start
+// (relative to its begin), and the global prefix of its first tile (pf);
+// every lane of the warp takes part (shuffles).
+template <class KT>
+__device__ __forceinline__ void mw8w_seg_buckets(const MwParams<KT> &P, uint32_t tile_base, uint32_t seg_tiles,
+                                                 uint32_t ntiles, uint32_t lane, uint32_t &tot, uint32_t &start,
+                                                 uint32_t &pf) {
+    const uint32_t first = tile_base, end = tile_base + seg_tiles, nblk = (ntiles + MWS_BR - 1) / MWS_BR;
+    tot = 0;
+    pf = 0;
+    if (lane < MW8) {
+        pf = P.mtab[(size_t)first * MW8 + lane] + P.mblk[(size_t)(first / MWS_BR) * MW8 + lane];
+        const uint32_t pe = end < ntiles ? P.mtab[(size_t)end * MW8 + lane] + P.mblk[(size_t)(end / MWS_BR) * MW8 + lane]
+                                         : P.mblk[(size_t)nblk * MW8 + lane];
+        tot = pe - pf;
+    }
+    uint32_t inc = tot;
+#pragma unroll
+    for (int d = 1; d < MW8; d <<= 1) {
+        const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= (uint32_t)d) inc += o;
+    }
+    start = inc - tot;
 }
 
 // per-lane asynchronous 16-byte copies global -> shared (LDGSTS), one group per round
@@ -294,7 +280,7 @@ __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_g
 // the tile a warp places next: its segment, source, destination and valid range
 template <class KT>
 struct Mw8wTile {
-    uint32_t t, si, vlo, vhi;
+    uint32_t t, si, vlo, vhi, begin, tile_base, ntiles;
     const typename KT::T *src;   // the buffer + the tile's first position
     typename KT::T *dst;
 };
@@ -308,6 +294,9 @@ __device__ __forceinline__ Mw8wTile<KT> mw8w_tile(const MwParams<KT> &P, uint32_
     const TileGeom<KT, TILE> G(sg, t);
     w.vlo = G.vlo;
     w.vhi = G.vhi;
+    w.begin = sg.begin;
+    w.tile_base = sg.tile_base;
+    w.ntiles = sg.ntiles;
     w.src = (sg.parity ? P.bufs[1] : P.bufs[0]) + G.tbeg;
     w.dst = sg.parity ? P.bufs[0] : P.bufs[1];
     return w;
@@ -359,7 +348,7 @@ __global__ void __launch_bounds__(MW8W_WARPS * 32, Mw8wTune<KT>::MINB) k_mw8w_sc
     if (t >= ntiles) return;
     const bool vec = P.aligned;
     Mw8wTile<KT> cur = mw8w_tile(P, t);
-    uint32_t r0 = cur.vlo / RK * RK, par = 0, cls_seg = 0xffffffffu, off = 0;
+    uint32_t r0 = cur.vlo / RK * RK, par = 0, cls_seg = 0xffffffffu, off = 0, seg_base = 0;
     bool new_tile = true;
     Mw8Cls<KT> cls;
     mw8w_issue<KT, IPT>(cur, r0, lane, vec, ws.in[0]);
@@ -382,12 +371,14 @@ __global__ void __launch_bounds__(MW8W_WARPS * 32, Mw8wTune<KT>::MINB) k_mw8w_sc
         if (new_tile) {
             if (cur.si != cls_seg) {
                 mw8w_load_cls<KT>(P, cur.si, cls);
+                uint32_t tot, start, pf;
+                mw8w_seg_buckets(P, cur.tile_base, cur.ntiles, ntiles, lane, tot, start, pf);
+                seg_base = cur.begin + start - pf;   // lane b: bucket b's output base minus its tiles' prefix
                 cls_seg = cur.si;
             }
             // lane b < 8: the global index of this tile's next key of bucket b
             if (lane < MW8)
-                off = P.cursor[lane * P.hstride + cur.si] + P.mtab[(size_t)cur.t * MW8 + lane] +
-                      P.mblk[(size_t)(cur.t / MWS_BR) * MW8 + lane];
+                off = seg_base + P.mtab[(size_t)cur.t * MW8 + lane] + P.mblk[(size_t)(cur.t / MWS_BR) * MW8 + lane];
         }
         cp_async_wait1();   // this round's copies (the lane reads only its own slots)
         T x[IPT];

@@ -609,7 +609,17 @@ __global__ void __launch_bounds__(NT) k_post_mw(const PostParams<KT> Qin) {
     post_stats_init();
     for (uint32_t si = blockIdx.x; si < nseg; si += gridDim.x) {
         const MSeg<KT> &m = Q.mw.msegs[si];
-        if (threadIdx.x < MW_K) {
+        if (Q.mw.tabmode) {   // 8-way levels (multiway8w.cuh): buckets from the tile-count table
+            if (threadIdx.x < 32) {
+                uint32_t tot, start, pf;
+                mw8w_seg_buckets(Q.mw, m.s.tile_base, m.s.ntiles, *Q.mw.ntiles_dev, threadIdx.x, tot, start, pf);
+                if (threadIdx.x < MW_K) {
+                    cb[threadIdx.x] = m.s.begin + start;
+                    cl[threadIdx.x] = threadIdx.x < MW8 ? tot : 0;
+                }
+                BQ_CHECK(__shfl_sync(0xffffffffu, start + tot, MW8 - 1) == m.s.len);
+            }
+        } else if (threadIdx.x < MW_K) {
             cb[threadIdx.x] = m.s.begin + m.start[threadIdx.x];
             cl[threadIdx.x] = Q.mw.hist[threadIdx.x * Q.mw.hstride + si];
         }
