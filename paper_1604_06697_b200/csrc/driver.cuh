@@ -102,8 +102,9 @@ Layout<KT> make_layout(size_t n) {
     L.max_copies = KT::is_record ? L.max_segs + 2 + n / 65536 + 2 : 1;
     L.copies[0] = take(L.max_copies * sizeof(Leaf));
     L.copies[1] = take(L.max_copies * sizeof(Leaf));
-    L.mtab = take(mw_capable<KT>() ? L.max_tiles * MW8 * sizeof(uint32_t) : 0);
-    L.mblk = take(mw_capable<KT>() ? (L.max_tiles / MWS_BR + 2) * MW8 * sizeof(uint32_t) : 0);
+    const size_t mrows = L.max_tiles + MW8W_ROWS_EXTRA;   // (units of small levels, multiway8w.cuh)
+    L.mtab = take(mw_capable<KT>() ? mrows * MW8 * sizeof(uint32_t) : 0);
+    L.mblk = take(mw_capable<KT>() ? (mrows / MWS_BR + 2) * MW8 * sizeof(uint32_t) : 0);
     L.tprefix = take((L.max_fb + 1) * sizeof(uint32_t));
     L.fbst = take(sizeof(FbState));
     L.ctrl = take((MAX_LEVELS + 1) * sizeof(LevelCtrl));   // [MAX_LEVELS]: the root's counts
@@ -179,7 +180,7 @@ bq_status launch_multiway(MwParams<KT> MP, LevelCtrl *lc, cudaStream_t s, int wa
         if (st != BQ_OK) return st;
         kc<<<cap_c, tw, 0, s>>>(MP);
         BQ_CK_LAUNCH();
-        const uint32_t nb = (MP.max_tiles + MWS_BR - 1) / MWS_BR;
+        const uint32_t nb = (MP.max_tiles + MW8W_ROWS_EXTRA + MWS_BR - 1) / MWS_BR;
         k_mw8w_scan<KT><<<nb < 592 ? nb : 592, 256, 0, s>>>(MP);
         BQ_CK_LAUNCH();
         ks<<<cap_s, tw, smemw, s>>>(MP);

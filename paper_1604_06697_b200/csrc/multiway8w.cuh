@@ -32,12 +32,28 @@ constexpr int MW8W_WARPS = 8;       // warps per CTA of the count and scatter ke
 #define BQ_MW8W_MINB_PAIR 2
 #endif
 
+// A level with fewer tiles than MW8W_UNIT_WARPS splits each tile into U units
+// (a power of two <= the rounds per tile) so that every warp has work; the
+// unit is the row of the count table.  count, scan, scatter and k_post_mw
+// derive the same U from the level's tile count.
+constexpr uint32_t MW8W_UNIT_WARPS = 2048;
+constexpr uint32_t MW8W_ROWS_EXTRA = 2 * MW8W_UNIT_WARPS;   // table rows beyond one per tile
+
 template <class KT> struct Mw8wTune;
 template <> struct Mw8wTune<KI32> { static constexpr int IPT = 8, MINB = BQ_MW8W_MINB; };
 template <> struct Mw8wTune<KU64> { static constexpr int IPT = 8, MINB = BQ_MW8W_MINB; };
 template <> struct Mw8wTune<KF64> { static constexpr int IPT = 8, MINB = BQ_MW8W_MINB; };
 template <> struct Mw8wTune<KRec> { static constexpr int IPT = 2, MINB = BQ_MW8W_MINB; };
 template <> struct Mw8wTune<KPair> { static constexpr int IPT = 4, MINB = BQ_MW8W_MINB_PAIR; };
+
+template <class KT>
+__host__ __device__ constexpr uint32_t mw8w_rounds() { return (uint32_t)tile_elems<KT>() / (32u * Mw8wTune<KT>::IPT); }
+template <class KT>
+__device__ __forceinline__ uint32_t mw8w_upt(uint32_t ntiles) {
+    uint32_t u = 1;
+    while (u < mw8w_rounds<KT>() && ntiles * u < MW8W_UNIT_WARPS) u <<= 1;
+    return u;
+}
 
 // per-warp staging of one round, double-buffered by round parity
 template <class KT, int IPT>
@@ -103,10 +119,11 @@ __global__ void __launch_bounds__(MW8W_WARPS * 32) k_mw8w_count(const MwParams<K
     constexpr uint32_t TILE = (uint32_t)tile_elems<KT>(), RK = 32u * IPT;
     static_assert(TILE % RK == 0 && (TILE / 32) <= 255, "rounds per tile; byte counters");
     const uint32_t lane = threadIdx.x & 31;
-    const uint32_t ntiles = *P.ntiles_dev;
+    const uint32_t ntiles = *P.ntiles_dev, U = mw8w_upt<KT>(ntiles), UL = TILE / U;
     uint32_t cls_seg = 0xffffffffu;
     Mw8Cls<KT> cls;
-    for (uint32_t t = blockIdx.x * MW8W_WARPS + (threadIdx.x >> 5); t < ntiles; t += gridDim.x * MW8W_WARPS) {
+    for (uint32_t u = blockIdx.x * MW8W_WARPS + (threadIdx.x >> 5); u < ntiles * U; u += gridDim.x * MW8W_WARPS) {
+        const uint32_t t = u / U, ub = (u % U) * UL;
         const uint32_t si = P.tile_map[t];
         const Seg sg = P.msegs[si].s;
         if (si != cls_seg) {
@@ -114,11 +131,12 @@ __global__ void __launch_bounds__(MW8W_WARPS * 32) k_mw8w_count(const MwParams<K
             cls_seg = si;
         }
         const TileGeom<KT, TILE> G(sg, t);
+        const uint32_t lo = G.vlo > ub ? G.vlo : ub, hi = G.vhi < ub + UL ? G.vhi : ub + UL;   // the unit's keys
         const T *src = (sg.parity ? P.bufs[1] : P.bufs[0]) + G.tbeg;
         uint32_t alo = 0, ahi = 0;   // byte counters: <= TILE / 32 per lane
-        for (uint32_t r0 = G.vlo / RK * RK; r0 < G.vhi; r0 += RK) {
+        for (uint32_t r0 = lo / RK * RK; r0 < hi; r0 += RK) {
             T x[IPT];
-            const uint32_t valid = mw8w_load<KT, IPT>(src, r0, G.vlo, G.vhi, lane, P.aligned, x);
+            const uint32_t valid = mw8w_load<KT, IPT>(src, r0, lo, hi, lane, P.aligned, x);
             uint32_t bk[IPT];
             mw8_classify<KT, IPT>(cls, x, bk);
             Mw8Ctr<IPT> ctr;
@@ -138,7 +156,7 @@ __global__ void __launch_bounds__(MW8W_WARPS * 32) k_mw8w_count(const MwParams<K
         uint32_t mine = 0;
 #pragma unroll
         for (int k = 0; k < MW8 / 2; k++) mine = (lane >> 1) == (uint32_t)k ? q[k] : mine;
-        if (lane < MW8) P.mtab[(size_t)t * MW8 + lane] = (lane & 1) ? (mine >> 16) : (mine & 0xffff);
+        if (lane < MW8) P.mtab[(size_t)u * MW8 + lane] = (lane & 1) ? (mine >> 16) : (mine & 0xffff);
     }
 }
 
@@ -188,7 +206,8 @@ __global__ void __launch_bounds__(256) k_mw8w_scan(const MwParams<KT> Pin) {
     __shared__ uint32_t s_w[8][MW8];
     __shared__ uint32_t s_last;
     const uint32_t tid = threadIdx.x;
-    const uint32_t ntiles = *P.ntiles_dev, nblk = (ntiles + MWS_BR - 1) / MWS_BR;
+    const uint32_t ntiles = *P.ntiles_dev * mw8w_upt<KT>(*P.ntiles_dev);   // table rows
+    const uint32_t nblk = (ntiles + MWS_BR - 1) / MWS_BR;
     uint32_t done = 0;
     for (uint32_t blk = blockIdx.x; blk < nblk; blk += gridDim.x, done++) {
         const uint32_t t0 = blk * MWS_BR + tid * 8;
@@ -243,9 +262,10 @@ __global__ void __launch_bounds__(256) k_mw8w_scan(const MwParams<KT> Pin) {
     }
 }
 
-// Lanes b < 8 of a warp: segment si's bucket b total (tot) and start
-// (relative to its begin), and the global prefix of its first tile (pf);
-// every lane of the warp takes part (shuffles).
+// Lanes b < 8 of a warp: the bucket b total (tot) and start (relative to the
+// segment's begin) of the segment owning table rows [tile_base, tile_base +
+// seg_tiles) of ntiles, and the global prefix of its first row (pf); every
+// lane of the warp takes part (shuffles).
 template <class KT>
 __device__ __forceinline__ void mw8w_seg_buckets(const MwParams<KT> &P, uint32_t tile_base, uint32_t seg_tiles,
                                                  uint32_t ntiles, uint32_t lane, uint32_t &tot, uint32_t &start,
@@ -280,23 +300,24 @@ __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_g
 // the tile a warp places next: its segment, source, destination and valid range
 template <class KT>
 struct Mw8wTile {
-    uint32_t t, si, vlo, vhi, begin, tile_base, ntiles;
+    uint32_t u, si, vlo, vhi, begin, tile_base, ntiles;   // unit, segment, the unit's keys, segment rows
     const typename KT::T *src;   // the buffer + the tile's first position
     typename KT::T *dst;
 };
 template <class KT>
-__device__ __forceinline__ Mw8wTile<KT> mw8w_tile(const MwParams<KT> &P, uint32_t t) {
+__device__ __forceinline__ Mw8wTile<KT> mw8w_tile(const MwParams<KT> &P, uint32_t u, uint32_t U) {
     constexpr uint32_t TILE = (uint32_t)tile_elems<KT>();
+    const uint32_t t = u / U, UL = TILE / U, ub = (u % U) * UL;
     Mw8wTile<KT> w;
-    w.t = t;
+    w.u = u;
     w.si = P.tile_map[t];
     const Seg sg = P.msegs[w.si].s;
     const TileGeom<KT, TILE> G(sg, t);
-    w.vlo = G.vlo;
-    w.vhi = G.vhi;
+    w.vlo = G.vlo > ub ? G.vlo : ub;
+    w.vhi = G.vhi < ub + UL ? G.vhi : ub + UL;
     w.begin = sg.begin;
-    w.tile_base = sg.tile_base;
-    w.ntiles = sg.ntiles;
+    w.tile_base = sg.tile_base * U;
+    w.ntiles = sg.ntiles * U;
     w.src = (sg.parity ? P.bufs[1] : P.bufs[0]) + G.tbeg;
     w.dst = sg.parity ? P.bufs[0] : P.bufs[1];
     return w;
@@ -342,12 +363,12 @@ __global__ void __launch_bounds__(MW8W_WARPS * 32, Mw8wTune<KT>::MINB) k_mw8w_sc
     extern __shared__ __align__(16) unsigned char smraw[];
     WS &ws = reinterpret_cast<WS *>(smraw)[threadIdx.x >> 5];
     const uint32_t lane = threadIdx.x & 31;
-    const uint32_t ntiles = *P.ntiles_dev;
+    const uint32_t U = mw8w_upt<KT>(*P.ntiles_dev), ntiles = *P.ntiles_dev * U;   // units (table rows)
     const uint32_t stride = gridDim.x * MW8W_WARPS;
-    uint32_t t = blockIdx.x * MW8W_WARPS + (threadIdx.x >> 5);
-    if (t >= ntiles) return;
+    const uint32_t u0 = blockIdx.x * MW8W_WARPS + (threadIdx.x >> 5);
+    if (u0 >= ntiles) return;
     const bool vec = P.aligned;
-    Mw8wTile<KT> cur = mw8w_tile(P, t);
+    Mw8wTile<KT> cur = mw8w_tile(P, u0, U);
     uint32_t r0 = cur.vlo / RK * RK, par = 0, cls_seg = 0xffffffffu, off = 0, seg_base = 0;
     bool new_tile = true;
     Mw8Cls<KT> cls;
@@ -359,8 +380,8 @@ __global__ void __launch_bounds__(MW8W_WARPS * 32, Mw8wTune<KT>::MINB) k_mw8w_sc
         uint32_t nr0 = r0 + RK;
         bool more = true;
         if (nr0 >= cur.vhi) {
-            if (cur.t + stride < ntiles) {
-                nxt = mw8w_tile(P, cur.t + stride);
+            if (cur.u + stride < ntiles) {
+                nxt = mw8w_tile(P, cur.u + stride, U);
                 nr0 = nxt.vlo / RK * RK;
             } else {
                 more = false;
@@ -378,7 +399,7 @@ __global__ void __launch_bounds__(MW8W_WARPS * 32, Mw8wTune<KT>::MINB) k_mw8w_sc
             }
             // lane b < 8: the global index of this tile's next key of bucket b
             if (lane < MW8)
-                off = seg_base + P.mtab[(size_t)cur.t * MW8 + lane] + P.mblk[(size_t)(cur.t / MWS_BR) * MW8 + lane];
+                off = seg_base + P.mtab[(size_t)cur.u * MW8 + lane] + P.mblk[(size_t)(cur.u / MWS_BR) * MW8 + lane];
         }
         cp_async_wait1();   // this round's copies (the lane reads only its own slots)
         T x[IPT];
@@ -452,7 +473,7 @@ __global__ void __launch_bounds__(MW8W_WARPS * 32, Mw8wTune<KT>::MINB) k_mw8w_sc
         else round(std::false_type{});
         par ^= 1;
         if (!more) break;
-        new_tile = nxt.t != cur.t;
+        new_tile = nxt.u != cur.u;
         cur = nxt;
         r0 = nr0;
     }

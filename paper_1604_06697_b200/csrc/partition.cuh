@@ -612,7 +612,9 @@ __global__ void __launch_bounds__(NT) k_post_mw(const PostParams<KT> Qin) {
         if (Q.mw.tabmode) {   // 8-way levels (multiway8w.cuh): buckets from the tile-count table
             if (threadIdx.x < 32) {
                 uint32_t tot, start, pf;
-                mw8w_seg_buckets(Q.mw, m.s.tile_base, m.s.ntiles, *Q.mw.ntiles_dev, threadIdx.x, tot, start, pf);
+                const uint32_t U = mw8w_upt<KT>(*Q.mw.ntiles_dev);
+                mw8w_seg_buckets(Q.mw, m.s.tile_base * U, m.s.ntiles * U, *Q.mw.ntiles_dev * U, threadIdx.x, tot, start,
+                                 pf);
                 if (threadIdx.x < MW_K) {
                     cb[threadIdx.x] = m.s.begin + start;
                     cl[threadIdx.x] = threadIdx.x < MW8 ? tot : 0;
