@@ -146,8 +146,8 @@ typedef struct {
  * bytes of tile status words, segment descriptors and leaf lists (and at
  * least bq_inplace_workspace_bytes(kind, n)).  For
  * BQ_REC32 it also covers the key+index sort path: 16n bytes of pairs, the
- * workspace of BQ_KEYIDX16 and a 32n-byte copy of the records that the final
- * gather reads (about 68n). */
+ * pair sort's own workspace (16n scratch + O(n/T)) and a 32n-byte copy of the
+ * records that the final gather reads (about 65n). */
 BQ_API size_t bq_workspace_bytes(bq_kind kind, size_t n);
 
 /* ---- pivot selection (hot-path step a1) -------------------------------------

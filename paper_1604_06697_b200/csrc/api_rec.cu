@@ -67,7 +67,7 @@ static KiLayout ki_layout(size_t n) {
     KiLayout L;
     L.pairs = 0;
     L.pws = align_up(n * sizeof(KeyIdx16), 256);
-    L.pws_bytes = ws_pair(n);
+    L.pws_bytes = make_layout<KPair>(n).total;   // the pair sort's own layout (not the in-place partition's)
     L.copy = align_up(L.pws + L.pws_bytes, 256);
     L.total = align_up(L.copy + n * sizeof(Rec32), 256);
     return L;
