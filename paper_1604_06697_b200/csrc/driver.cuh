@@ -102,7 +102,7 @@ Layout<KT> make_layout(size_t n) {
     L.max_copies = KT::is_record ? L.max_segs + 2 + n / 65536 + 2 : 1;
     L.copies[0] = take(L.max_copies * sizeof(Leaf));
     L.copies[1] = take(L.max_copies * sizeof(Leaf));
-    const size_t mrows = L.max_tiles + MW8W_ROWS_EXTRA;   // (units of small levels, multiway8w.cuh)
+    const size_t mrows = L.max_tiles * mw8w_umin<KT>() + MW8W_ROWS_EXTRA;   // (units of small levels, multiway8w.cuh)
     L.mtab = take(mw_capable<KT>() ? mrows * MW8 * sizeof(uint32_t) : 0);
     L.mblk = take(mw_capable<KT>() ? (mrows / MWS_BR + 2) * MW8 * sizeof(uint32_t) : 0);
     L.tprefix = take((L.max_fb + 1) * sizeof(uint32_t));
@@ -180,9 +180,25 @@ bq_status launch_multiway(MwParams<KT> MP, LevelCtrl *lc, cudaStream_t s, int wa
         if (st != BQ_OK) return st;
         kc<<<cap_c, tw, 0, s>>>(MP);
         BQ_CK_LAUNCH();
-        const uint32_t nb = (MP.max_tiles + MW8W_ROWS_EXTRA + MWS_BR - 1) / MWS_BR;
+        const uint32_t nb = (MP.max_tiles * mw8w_umin<KT>() + MW8W_ROWS_EXTRA + MWS_BR - 1) / MWS_BR;
         k_mw8w_scan<KT><<<nb < 592 ? nb : 592, 256, 0, s>>>(MP);
         BQ_CK_LAUNCH();
+#if BQ_MW8T
+#ifndef BQ_MW8T_PAIR
+#define BQ_MW8T_PAIR 1
+#endif
+        if (MP.aligned && (BQ_MW8T_PAIR || sizeof(typename KT::T) != 16)) {   // bucket runs staged per unit, bulk stores
+            constexpr int smemt = mw8t_smem_bytes<KT>();
+            auto kt = k_mw8t_scatter<KT, IPTW>;
+            static CapCache cc_t;
+            int cap_t = 0;
+            st = persistent_cap(kt, tw, smemt, cc_t, &cap_t);
+            if (st != BQ_OK) return st;
+            kt<<<cap_t, tw, smemt, s>>>(MP);
+            BQ_CK_LAUNCH();
+            return BQ_OK;
+        }
+#endif
         ks<<<cap_s, tw, smemw, s>>>(MP);
         BQ_CK_LAUNCH();
         return BQ_OK;
@@ -955,15 +971,15 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
         if (stats) *stats = local;
         return BQ_OK;
     }
-    // default: binary passes for int32 keys (the binary pass is already near
-    // the HBM roofline and the cheapest in ALU work per key), 8-way passes
-    // (N4) for 64-bit keys and key+index pairs; 32-byte records stay binary
-    // (int32: also multiway where a sort is only a few levels and each
-    // level's fixed costs matter: 8-way for 2^17 < n <= 2^23, 16-way up to 2^24)
+    // default: 8-way passes (N4) for 64-bit keys and key+index pairs, and for
+    // int32 keys above 2^17 (16-way for 2^21 < n <= 2^23; tools/ways_sweep.py,
+    // profiles/r02/mw8t.md: an 8-way level of the TMA-staged scatter costs
+    // less than the three binary levels it replaces); binary passes for
+    // small int32 sorts; 32-byte records stay binary
     if (ways == 0) {
         if (sizeof(typename KT::K) == 8 && mw_capable<KT>()) ways = MW8;
-        else if (!KT::is_record && n > (1u << 17) && n <= (1u << 23)) ways = MW8;
-        else if (!KT::is_record && n > (1u << 23) && n <= (1u << 24)) ways = MW_K;
+        else if (!KT::is_record && n > (1u << 21) && n <= (1u << 23)) ways = MW_K;
+        else if (!KT::is_record && n > (1u << 17)) ways = MW8;
         else ways = 2;
     }
     if (!mw_capable<KT>()) ways = 2;

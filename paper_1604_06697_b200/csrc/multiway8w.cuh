@@ -48,9 +48,25 @@ template <> struct Mw8wTune<KPair> { static constexpr int IPT = 4, MINB = BQ_MW8
 
 template <class KT>
 __host__ __device__ constexpr uint32_t mw8w_rounds() { return (uint32_t)tile_elems<KT>() / (32u * Mw8wTune<KT>::IPT); }
+// Table rows per tile at least: the TMA-staged scatter (k_mw8t_scatter) stages
+// a whole unit per warp, so units are at most BQ_MW8T_UNIT_BYTES (4 KB: four
+// rows per 16 KB tile; 16 warps of double-buffered input and one staging plane
+// per SM)
+#ifndef BQ_MW8T
+#define BQ_MW8T 1
+#endif
+#ifndef BQ_MW8T_UNIT_BYTES
+#define BQ_MW8T_UNIT_BYTES 4096
+#endif
+template <class KT>
+__host__ __device__ constexpr uint32_t mw8w_umin() {
+    constexpr uint32_t tb = (uint32_t)(tile_elems<KT>() * sizeof(typename KT::T));
+    return (BQ_MW8T && tb > BQ_MW8T_UNIT_BYTES) ? tb / BQ_MW8T_UNIT_BYTES : 1u;
+}
 template <class KT>
 __device__ __forceinline__ uint32_t mw8w_upt(uint32_t ntiles) {
-    uint32_t u = 1;
+    static_assert(mw8w_umin<KT>() <= mw8w_rounds<KT>(), "a unit holds whole rounds");
+    uint32_t u = mw8w_umin<KT>();
     while (u < mw8w_rounds<KT>() && ntiles * u < MW8W_UNIT_WARPS) u <<= 1;
     return u;
 }
@@ -119,11 +135,15 @@ __global__ void __launch_bounds__(MW8W_WARPS * 32) k_mw8w_count(const MwParams<K
     constexpr uint32_t TILE = (uint32_t)tile_elems<KT>(), RK = 32u * IPT;
     static_assert(TILE % RK == 0 && (TILE / 32) <= 255, "rounds per tile; byte counters");
     const uint32_t lane = threadIdx.x & 31;
-    const uint32_t ntiles = *P.ntiles_dev, U = mw8w_upt<KT>(ntiles), UL = TILE / U;
+    const uint32_t ntiles = *P.ntiles_dev, U = mw8w_upt<KT>(ntiles), lgU = __ffs(U) - 1, UL = TILE >> lgU;
+    // a warp's item: a whole tile (its U rows) on large levels, one unit on
+    // small ones (so that every warp has work)
+    const uint32_t lgG = ntiles * U >= 8192 ? lgU : 0, nitems = (ntiles * U) >> lgG;
+    constexpr int NR = sizeof(T) <= 4 ? 4 : 1;   // rounds loaded before the first is classified
     uint32_t cls_seg = 0xffffffffu;
     Mw8Cls<KT> cls;
-    for (uint32_t u = blockIdx.x * MW8W_WARPS + (threadIdx.x >> 5); u < ntiles * U; u += gridDim.x * MW8W_WARPS) {
-        const uint32_t t = u / U, ub = (u % U) * UL;
+    for (uint32_t it = blockIdx.x * MW8W_WARPS + (threadIdx.x >> 5); it < nitems; it += gridDim.x * MW8W_WARPS) {
+        const uint32_t u0 = it << lgG, t = u0 >> lgU;
         const uint32_t si = P.tile_map[t];
         const Seg sg = P.msegs[si].s;
         if (si != cls_seg) {
@@ -131,32 +151,49 @@ __global__ void __launch_bounds__(MW8W_WARPS * 32) k_mw8w_count(const MwParams<K
             cls_seg = si;
         }
         const TileGeom<KT, TILE> G(sg, t);
-        const uint32_t lo = G.vlo > ub ? G.vlo : ub, hi = G.vhi < ub + UL ? G.vhi : ub + UL;   // the unit's keys
         const T *src = (sg.parity ? P.bufs[1] : P.bufs[0]) + G.tbeg;
-        uint32_t alo = 0, ahi = 0;   // byte counters: <= TILE / 32 per lane
-        for (uint32_t r0 = lo / RK * RK; r0 < hi; r0 += RK) {
-            T x[IPT];
-            const uint32_t valid = mw8w_load<KT, IPT>(src, r0, lo, hi, lane, P.aligned, x);
-            uint32_t bk[IPT];
-            mw8_classify<KT, IPT>(cls, x, bk);
-            Mw8Ctr<IPT> ctr;
+        for (uint32_t u = u0; u < u0 + (1u << lgG); u++) {
+            const uint32_t ub = (u & (U - 1)) * UL;
+            const uint32_t lo = G.vlo > ub ? G.vlo : ub, hi = G.vhi < ub + UL ? G.vhi : ub + UL;   // the unit's keys
+            uint32_t alo = 0, ahi = 0;   // byte counters: <= TILE / 32 per lane
+            for (uint32_t r0 = lo / RK * RK; r0 < hi; r0 += NR * RK) {
+                T x[NR][IPT];
+                uint32_t valid[NR];
 #pragma unroll
-            for (int c = 0; c < IPT; c++) ctr.add(bk[c], (valid >> c) & 1);
-            uint32_t lo, hi;
-            ctr.bytes(lo, hi);
-            alo += lo;
-            ahi += hi;
+                for (int h = 0; h < NR; h++) valid[h] = mw8w_load<KT, IPT>(src, r0 + h * RK, lo, hi, lane, P.aligned, x[h]);
+#pragma unroll
+                for (int h = 0; h < NR; h++) {
+                    uint32_t inc[IPT];
+                    bool nan = false;
+#pragma unroll
+                    for (int c = 0; c < IPT; c++) inc[c] = cls.inc(x[h][c], nan);
+                    if (nan)
+#pragma unroll
+                        for (int c = 0; c < IPT; c++) inc[c] = 1u << cls.fix4(x[h][c], 31 - __clz(inc[c]));
+                    Mw8Ctr<IPT> ctr;
+                    if (valid[h] == (1u << IPT) - 1) {
+#pragma unroll
+                        for (int c = 0; c < IPT; c++) ctr.c += inc[c];
+                    } else {
+#pragma unroll
+                        for (int c = 0; c < IPT; c++)
+                            if ((valid[h] >> c) & 1) ctr.c += inc[c];
+                    }
+                    uint32_t lo, hi;
+                    ctr.bytes(lo, hi);
+                    alo += lo;
+                    ahi += hi;
+                }
+            }
+            uint32_t q[MW8 / 2];
+            mw8_widen((uint64_t)alo | ((uint64_t)ahi << 32), q);
+#pragma unroll
+            for (int k = 0; k < MW8 / 2; k++) q[k] = __reduce_add_sync(0xffffffffu, q[k]);   // (16-bit fields <= 4096)
+            uint32_t mine = 0;
+#pragma unroll
+            for (int k = 0; k < MW8 / 2; k++) mine = (lane >> 1) == (uint32_t)k ? q[k] : mine;
+            if (lane < MW8) P.mtab[(size_t)u * MW8 + lane] = (lane & 1) ? (mine >> 16) : (mine & 0xffff);
         }
-        uint32_t q[MW8 / 2];
-        mw8_widen((uint64_t)alo | ((uint64_t)ahi << 32), q);
-#pragma unroll
-        for (int d = 16; d > 0; d >>= 1)
-#pragma unroll
-            for (int k = 0; k < MW8 / 2; k++) q[k] += __shfl_xor_sync(0xffffffffu, q[k], d);
-        uint32_t mine = 0;
-#pragma unroll
-        for (int k = 0; k < MW8 / 2; k++) mine = (lane >> 1) == (uint32_t)k ? q[k] : mine;
-        if (lane < MW8) P.mtab[(size_t)u * MW8 + lane] = (lane & 1) ? (mine >> 16) : (mine & 0xffff);
     }
 }
 
@@ -307,7 +344,7 @@ struct Mw8wTile {
 template <class KT>
 __device__ __forceinline__ Mw8wTile<KT> mw8w_tile(const MwParams<KT> &P, uint32_t u, uint32_t U) {
     constexpr uint32_t TILE = (uint32_t)tile_elems<KT>();
-    const uint32_t t = u / U, UL = TILE / U, ub = (u % U) * UL;
+    const uint32_t lgU = __ffs(U) - 1, t = u >> lgU, UL = TILE >> lgU, ub = (u & (U - 1)) * UL;
     Mw8wTile<KT> w;
     w.u = u;
     w.si = P.tile_map[t];
@@ -477,6 +514,302 @@ __global__ void __launch_bounds__(MW8W_WARPS * 32, Mw8wTune<KT>::MINB) k_mw8w_sc
         cur = nxt;
         r0 = nr0;
     }
+}
+
+// ---- k_mw8t_scatter: bucket runs staged per unit, stored by TMA --------------------
+// The scatter of the 8-way level with the output moved like k_part_fast's: a
+// warp stages a whole unit (<= BQ_MW8T_UNIT_BYTES) bucket by bucket in its own
+// shared-memory plane, each bucket's run placed at a slot congruent to its
+// global destination modulo 16 bytes, and lanes 0..7 write the 16-byte aligned
+// body of their bucket's run with one bulk copy each (heads and tails < 16
+// bytes by plain stores).  The unit's input arrives by one bulk copy into a
+// double buffer (the next unit's copy is in flight while this one is placed).
+// Per key: classify, rank (packed counters, byte-field warp scan per round),
+// one shared-memory store; no per-key global store, no tags, no block barrier.
+// The layout is the one the count table fixes (unit u's keys of bucket b
+// follow those of the segment's earlier units), the order inside a unit's run
+// the (round, lane, key) order.
+template <class KT, int IPT>
+struct Mw8tWarpSmem {
+    using T = typename KT::T;
+    static constexpr uint32_t VW = tile_vw<KT>();
+    static constexpr uint32_t UNIT = (uint32_t)tile_elems<KT>() / mw8w_umin<KT>();   // largest unit
+    static constexpr uint32_t SCAP = (UNIT + MW8 * VW + VW + VW - 1) / VW * VW;     // runs + alignment gaps
+    alignas(16) T in[2][UNIT];
+    alignas(16) T stage[SCAP];
+    uint32_t exs[MW8 * 32];   // lane L's first slot of bucket b this round at [32 b + L] (conflict-free)
+    uint64_t bar[2];
+};
+template <class KT>
+constexpr int mw8t_smem_bytes() {
+    return (int)(MW8W_WARPS * sizeof(Mw8tWarpSmem<KT, Mw8wTune<KT>::IPT>));
+}
+template <class KT> struct Mw8tTune { static constexpr int MINB = 2; };
+
+// unit u: segment, the unit's valid tile positions [lo, hi), its first tile
+// position ub, the tile's buffers and whether its keys come by one bulk copy
+template <class KT>
+struct Mw8tUnit {
+    uint32_t u, si, ub, lo, hi, begin, row0, nrows;
+    bool tma;
+    const typename KT::T *src;   // the buffer + the tile's first position
+    typename KT::T *dst;
+};
+template <class KT>
+__device__ __forceinline__ Mw8tUnit<KT> mw8t_unit(const MwParams<KT> &P, uint32_t u, uint32_t U) {
+    constexpr uint32_t TILE = (uint32_t)tile_elems<KT>(), VW = tile_vw<KT>();
+    const uint32_t lgU = __ffs(U) - 1, t = u >> lgU, UL = TILE >> lgU;   // (U: a power of two)
+    Mw8tUnit<KT> w;
+    w.u = u;
+    w.ub = (u & (U - 1)) * UL;
+    w.si = P.tile_map[t];
+    const Seg sg = P.msegs[w.si].s;
+    const TileGeom<KT, TILE> G(sg, t);
+    w.lo = G.vlo > w.ub ? G.vlo : w.ub;
+    w.hi = G.vhi < w.ub + UL ? G.vhi : w.ub + UL;
+    w.begin = sg.begin;
+    w.row0 = sg.tile_base * U;
+    w.nrows = sg.ntiles * U;
+    w.src = (sg.parity ? P.bufs[1] : P.bufs[0]) + G.tbeg;
+    w.dst = sg.parity ? P.bufs[0] : P.bufs[1];
+    if (w.hi <= w.lo) w.lo = w.hi = w.ub;   // a unit outside the segment
+    w.tma = w.hi > w.lo && P.aligned && G.tbeg + (w.hi + VW - 1) / VW * VW <= P.n_total;
+    return w;
+}
+
+// the keys of unit w into in[] (slot i = tile position ub + i): one bulk copy
+// by lane 0 completing on bar, or plain loads by the warp
+template <class KT>
+__device__ __forceinline__ void mw8t_issue(const Mw8tUnit<KT> &w, typename KT::T *in, uint64_t *bar, uint32_t lane) {
+    using T = typename KT::T;
+    constexpr uint32_t VW = tile_vw<KT>();
+    if (w.tma) {
+        if (lane == 0) {
+            const uint32_t a = w.lo / VW * VW, z = (w.hi + VW - 1) / VW * VW;
+            const uint32_t bytes = (z - a) * (uint32_t)sizeof(T);
+            constexpr uint32_t UNIT = (uint32_t)tile_elems<KT>() / mw8w_umin<KT>();
+            BQ_CHECK(a >= w.ub && z - w.ub <= UNIT);
+            fence_proxy_async_smem();
+            mbar_arrive_expect_tx(bar, bytes);
+            tma_load_1d(in + (a - w.ub), w.src + a, bytes, bar);
+        }
+    } else {
+        for (uint32_t p = w.lo + lane; p < w.hi; p += 32) in[p - w.ub] = w.src[p];
+    }
+}
+
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
+    asm volatile("st.shared.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void sts_t(uint32_t a, uint32_t v) { sts32(a, v); }
+__device__ __forceinline__ void sts_t(uint32_t a, int32_t v) { sts32(a, (uint32_t)v); }
+__device__ __forceinline__ void sts_t(uint32_t a, uint64_t v) {
+    asm volatile("st.shared.b64 [%0], %1;" ::"r"(a), "l"(v) : "memory");
+}
+__device__ __forceinline__ void sts_t(uint32_t a, const uint4 &v) {
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+template <class T, class = typename std::enable_if<sizeof(T) == 16>::type>
+__device__ __forceinline__ void sts_t(uint32_t a, const T &v) {   // (after the uint4 overload it calls)
+    uint4 q;
+    memcpy(&q, &v, 16);
+    sts_t(a, q);
+}
+
+template <class KT, int IPT>
+__global__ void __launch_bounds__(MW8W_WARPS * 32, Mw8tTune<KT>::MINB) k_mw8t_scatter(const MwParams<KT> Pin) {
+    if (const LevelCtrl *pv = loop_prev_ctrl(Pin.lp)) if (pv->nmseg_next == 0) return;
+    __shared__ MwParams<KT> sP;
+    const MwParams<KT> &P = cta_params(Pin, sP);
+    using T = typename KT::T;
+    using WS = Mw8tWarpSmem<KT, IPT>;
+    constexpr uint32_t RK = 32u * IPT, VW = tile_vw<KT>(), NV = IPT / VW;
+    static_assert(IPT % VW == 0 && IPT <= 8 && WS::SCAP < 65536, "whole vectors; byte-field scans; 16-bit slots");
+    extern __shared__ __align__(16) unsigned char smraw[];
+    WS &ws = reinterpret_cast<WS *>(smraw)[threadIdx.x >> 5];
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t nt = *P.ntiles_dev, U = mw8w_upt<KT>(nt), rows = nt * U;
+    const uint32_t nblk = (rows + MWS_BR - 1) / MWS_BR;
+    const uint32_t stride = gridDim.x * MW8W_WARPS;
+    const uint32_t u0 = blockIdx.x * MW8W_WARPS + (threadIdx.x >> 5);
+    if (u0 >= rows) return;
+    if (lane == 0) {
+        mbar_init(&ws.bar[0], 1);
+        mbar_init(&ws.bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    const uint32_t exrow = smem_u32(&ws.exs[lane]), stage0 = smem_u32(ws.stage);
+    Mw8tUnit<KT> cur = mw8t_unit(P, u0, U);
+    mw8t_issue<KT>(cur, ws.in[0], &ws.bar[0], lane);
+    uint32_t par = 0, ph = 0, cls_seg = 0xffffffffu, seg_base = 0;
+    bool stores_out = false;   // lanes 0..7: a bulk store of the stage may still read it
+    Mw8Cls<KT> cls;
+    // global prefix of table row r, lane b < 8: bucket b (as the two words
+    // it sums, loaded a unit before they are added)
+    auto prefix2 = [&](uint32_t r) -> uint2 {
+        return r < rows ? make_uint2(P.mtab[(size_t)r * MW8 + lane], P.mblk[(size_t)(r / MWS_BR) * MW8 + lane])
+                        : make_uint2(P.mblk[(size_t)nblk * MW8 + lane], 0u);
+    };
+    uint2 pu = make_uint2(0, 0), pe = pu;   // lanes b < 8: global prefixes of the unit's row and the next row
+    if (lane < MW8) {
+        pu = prefix2(cur.u);
+        pe = prefix2(cur.u + 1);
+    }
+    for (;;) {
+        const bool more = cur.u + stride < rows;
+        Mw8tUnit<KT> nxt = cur;
+        uint2 pu_n = make_uint2(0, 0), pe_n = pu_n;
+        if (more) {
+            nxt = mw8t_unit(P, cur.u + stride, U);
+            mw8t_issue<KT>(nxt, ws.in[par ^ 1], &ws.bar[par ^ 1], lane);
+            if (lane < MW8) {   // (loaded a unit ahead)
+                pu_n = prefix2(nxt.u);
+                pe_n = prefix2(nxt.u + 1);
+            }
+        }
+        if (cur.si != cls_seg) {
+            mw8w_load_cls<KT>(P, cur.si, cls);
+            uint32_t tot, start, pf;
+            mw8w_seg_buckets(P, cur.row0, cur.nrows, rows, lane, tot, start, pf);
+            seg_base = cur.begin + start - pf;   // lane b: bucket b's output base minus its rows' prefix
+            cls_seg = cur.si;
+        }
+        // lanes b < 8: the unit's run of bucket b: global start G, length nb,
+        // stage slot S (S = G modulo VW)
+        uint32_t G = 0, nb = 0;
+        if (lane < MW8) {
+            const uint32_t p0 = pu.x + pu.y;
+            nb = pe.x + pe.y - p0;
+            G = seg_base + p0;
+        }
+        uint32_t S = nb + VW - 1;
+#pragma unroll
+        for (int d = 1; d < MW8; d <<= 1) {
+            const uint32_t o = __shfl_up_sync(0xffffffffu, S, d);
+            if (lane >= (uint32_t)d) S += o;
+        }
+        S -= nb + VW - 1;
+        S += (G - S) & (VW - 1);
+        BQ_CHECK(lane >= MW8 || (G + nb <= P.n_total && S + nb <= WS::SCAP));
+        uint32_t cw[MW8 / 2];   // the lane's next slot of each bucket, 16-bit pairs
+#pragma unroll
+        for (int k = 0; k < MW8 / 2; k++)
+            cw[k] = __shfl_sync(0xffffffffu, S, 2 * k) | (__shfl_sync(0xffffffffu, S, 2 * k + 1) << 16);
+        if (cur.tma) {
+            mbar_wait(&ws.bar[par], (ph >> par) & 1);
+            ph ^= 1u << par;
+        } else {
+            __syncwarp();
+        }
+        const T *in = ws.in[par];
+        const uint32_t lo = cur.lo - cur.ub, hi = cur.hi - cur.ub;
+        for (uint32_t r0 = lo / RK * RK; r0 < hi; r0 += RK) {
+            T x[IPT];
+#pragma unroll
+            for (uint32_t v = 0; v < NV; v++) {
+                const uint4 q = *reinterpret_cast<const uint4 *>(in + r0 + v * 32 * VW + lane * VW);
+                memcpy(&x[v * VW], &q, 16);
+            }
+            const bool full = r0 >= lo && r0 + RK <= hi;
+            // (full rounds, the common case, skip every validity test)
+            auto round = [&](auto full_tag) {
+                constexpr bool FULL = decltype(full_tag)::value;
+                uint32_t valid = (1u << IPT) - 1;
+                if (!FULL) {
+                    valid = 0;
+#pragma unroll
+                    for (uint32_t v = 0; v < NV; v++)
+#pragma unroll
+                        for (uint32_t e = 0; e < VW; e++) {
+                            const uint32_t pos = r0 + v * 32 * VW + lane * VW + e;
+                            valid |= (uint32_t)(pos >= lo && pos < hi) << (v * VW + e);
+                        }
+                }
+                uint32_t b4[IPT], rk[IPT], ra[IPT];   // ra: the key's bucket entry of the lane's row
+                {
+                    bool nan = false;
+#pragma unroll
+                    for (int c = 0; c < IPT; c++) ra[c] = cls.a128(x[c], exrow, nan);
+                    if (nan)
+#pragma unroll
+                        for (int c = 0; c < IPT; c++) ra[c] = exrow + 32u * cls.fix4(x[c], (ra[c] - exrow) >> 5);
+                }
+#pragma unroll
+                for (int c = 0; c < IPT; c++) b4[c] = (ra[c] - exrow) >> 5;
+                Mw8Ctr<IPT> ctr;
+#pragma unroll
+                for (int c = 0; c < IPT; c++) {
+                    if (FULL) rk[c] = ctr.take4(b4[c]);
+                    else rk[c] = ((valid >> c) & 1) ? ctr.take4(b4[c]) : 0u;
+                }
+                uint32_t ex[MW8 / 2], tot[MW8 / 2];
+                mw8_scan<IPT>(ctr, lane, ex, tot);
+#pragma unroll
+                for (int k = 0; k < MW8 / 2; k++) {
+                    tot[k] = __shfl_sync(0xffffffffu, tot[k], 31);
+                    const uint32_t f = ex[k] + cw[k];   // this lane's first slots of buckets 2k, 2k+1
+                    cw[k] += tot[k];
+                    sts32(exrow + 256u * k, f & 0xffffu);
+                    sts32(exrow + 256u * k + 128u, f >> 16);
+                }
+                if (stores_out) {   // the previous unit's bulk stores have read the stage
+                    bulk_wait_read0();
+                    stores_out = false;
+                }
+                __syncwarp();
+                uint32_t slot[IPT];   // (every base load issued before the first store)
+#pragma unroll
+                for (int c = 0; c < IPT; c++) slot[c] = lds32(ra[c]) + rk[c];
+#pragma unroll
+                for (int c = 0; c < IPT; c++) {
+                    if (FULL || ((valid >> c) & 1)) {
+                        BQ_CHECK(slot[c] < WS::SCAP);
+                        sts_t(stage0 + slot[c] * (uint32_t)sizeof(T), x[c]);
+                    }
+                }
+            };
+            if (full) round(std::true_type{});
+            else round(std::false_type{});
+        }
+        // the unit's runs -> dst: aligned bodies by bulk copies (lanes 0..7),
+        // heads and tails by plain stores (lane 4b + j: element j of bucket b's)
+        fence_proxy_async_smem();
+        __syncwarp();
+        {
+            const uint32_t b = lane >> 2, j = lane & 3;
+            const uint32_t Gb = __shfl_sync(0xffffffffu, G, b), nbb = __shfl_sync(0xffffffffu, nb, b);
+            const uint32_t Sb = __shfl_sync(0xffffffffu, S, b);
+            const uint32_t e = Gb + nbb, gs = (Gb + VW - 1) / VW * VW, ge = e / VW * VW;
+            const uint32_t hend = gs < e ? gs : e, tbeg = ge > hend ? ge : hend;
+            if (VW > 1) {
+                if (Gb + j < hend) cur.dst[Gb + j] = ws.stage[Sb + j];
+                if (tbeg + j < e) cur.dst[tbeg + j] = ws.stage[Sb + (tbeg - Gb) + j];
+            }
+        }
+        if (lane < MW8) {   // lane b: bucket b's body
+            const uint32_t e = G + nb, gs = (G + VW - 1) / VW * VW, ge = e / VW * VW;
+            if (ge > gs && gs < e) {
+                BQ_CHECK(((S + (gs - G)) % VW) == 0 && ge <= P.n_total);
+                tma_store_1d(cur.dst + gs, &ws.stage[S + (gs - G)], (ge - gs) * (uint32_t)sizeof(T));
+                bulk_commit();
+                stores_out = true;
+            }
+        }
+        if (!more) break;
+        __syncwarp();   // every lane is done with in[par] before it is refilled
+        cur = nxt;
+        pu = pu_n;
+        pe = pe_n;
+        par ^= 1;
+    }
+    if (lane < MW8) bulk_wait0();
 }
 
 }  // namespace bq

@@ -2,7 +2,8 @@
 (source page, cuda,sass view).  usage: ncu_lines.py REPORT [top]"""
 import csv, subprocess, sys
 rep = sys.argv[1]; top = int(sys.argv[2]) if len(sys.argv) > 2 else 40
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+KF = (["-k", "regex:" + __import__("os").environ["NCU_K"]] if __import__("os").environ.get("NCU_K") else [])
+out = subprocess.run(["ncu", "-i", rep] + KF + ["--page", "source", "--csv", "--print-source", "cuda,sass"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(out.splitlines()))
 res = []; fname = None; tot = 0

@@ -14,10 +14,10 @@ for kind in KINDS:
         if kind == "i32":
             h = torch.from_numpy(bqgen.i32_full(n, 1))
         elif kind == "u64":
-            h = torch.from_numpy(bqgen.u64(n, 1).view(np.int64))
+            h = torch.from_numpy(bqgen.u64(n, 1).view(np.int64)).view(torch.uint64)
         else:
             a = np.empty((n, 2), dtype=np.uint64); a[:, 0] = bqgen.u64(n, 1); a[:, 1] = np.arange(n, dtype=np.uint64)
-            h = torch.from_numpy(a.view(np.int64))
+            h = torch.from_numpy(a.view(np.int64))  # (n, 2): key+index pairs
         src = h.cuda(); t = torch.empty_like(src); ws = bq.workspace(bq.kind_of(src), n)
         res = {}
         for w in (2, 8, 16):
