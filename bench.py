@@ -13,9 +13,11 @@ Timing (device, CUDA events on the stream the library launches on):
     the bq_sort call; before each step the input is restored from a pristine
     device copy outside the events.  Inputs (1 GiB) are larger than the
     126 MB L2, and the restore copy streams 2 GiB through it as well.
-  * roofline: the dominant kernel is the tile-partition pass; the library
-    records CUDA events around each of its launches (bq_sort_options.timing);
-    achieved = algorithmic bytes (2 * 4 B * element_passes) / summed launch time.
+  * roofline: the kernel family with the largest share of the step (the
+    library's timing mode records CUDA events around the binary partition,
+    multiway count/scatter and leaf launches, bq_sort_options.timing);
+    achieved = its algorithmic bytes per sort / its summed launch time;
+    roofline_by_kernel lists every family.
   * partition_pass: BASELINE.md's roofline measurement — 10 single out-of-place
     passes over the pristine input around its Mo3 pivot, L2 flushed before each.
   * e2e: bq_sort_host (H2D from pinned memory + sort + D2H) per step.
@@ -52,16 +54,16 @@ def load_peak():
         return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
-def load_traffic():
-    """DRAM bytes (read + write) per launch of the partition kernel inside one
-    c2 sort, from the committed ncu capture summary, or None."""
+def load_traffic(kernel):
+    """DRAM bytes (read + write) of all launches of `kernel` inside one c2
+    sort and its active launches, from the committed ncu capture summary."""
     p = os.path.join(ROOT, "profiles", "r02", "ncu_sort_dram.json")
     try:
         with open(p) as f:
-            d = json.load(f)
-        return d["k_part_fast"]["dram_bytes_total"], "profiles/r02/ncu_sort_dram.json"
+            d = json.load(f)[kernel]
+        return d["dram_bytes_total"], max(d["active_launches"], 1), "profiles/r02/ncu_sort_dram.json"
     except Exception:
-        return None, None
+        return None, None, None
 
 
 def partition_pass_by_config(bq, bqgen, dev, stream, passes, peak):
@@ -402,31 +404,53 @@ def main():
     data.copy_(src)
     last = bq.bq_sort_ex(data, pivot_rule=args.pivot_rule, ws=ws, stream=stream)
 
-    # roofline of the dominant kernel (the tile-partition pass): the sort's
-    # host-driven mode records CUDA events around every partition launch on the
-    # launching stream (bq_sort_options.timing); same kernels, same levels
+    # roofline of the dominant kernel: the sort's host-driven mode
+    # (bq_sort_options.timing; same kernels, same levels as the graph) records
+    # CUDA events on the launching streams around the binary partition
+    # launches, the multiway count + scan and scatter launches of every level
+    # and the leaf launches; the kernel with the largest share of the step is
+    # reported, every kernel family in roofline_by_kernel
     peak, peak_src = load_peak()
     tstats = []
     for _ in range(3):
         data.copy_(src)
         tstats.append(bq.bq_sort_ex(data, pivot_rule=args.pivot_rule, timing=True, ws=ws, stream=stream))
-    part_ms = sum(s["partition_ms"] for s in tstats) / len(tstats)
-    part_bytes = sum(s["partition_bytes"] for s in tstats) / len(tstats)
-    launches = tstats[-1]["partition_launches"]
-    achieved = part_bytes / (part_ms * 1e-3) / 1e9
-    traffic_total, traffic_src = load_traffic()   # one whole c2 sort under ncu (same input, same levels)
+    avg = lambda k: sum(s[k] for s in tstats) / len(tstats)
+    mwp = avg("multiway_element_passes")
+    fams = {
+        "k_part_fast": ("tile partition pass (binary levels)", avg("partition_bytes"), avg("partition_ms"),
+                        tstats[-1]["partition_launches"] if avg("partition_bytes") > 0 else 0),
+        "k_mw8t_scatter": ("8-way scatter (multiway levels): read + write of every key", 8.0 * mwp,
+                           avg("mw_scatter_ms"), None),
+        "k_mw8w_count": ("8-way count + scan (multiway levels): read of every key", 4.0 * mwp, avg("mw_count_ms"), None),
+        "k_leaf": ("leaf sort (a8): read + write of every leaf key", 8.0 * N_FULL, avg("leaf_ms"), None),
+    }
+    by_kernel = {}
+    for kname, (desc, nbytes, ms, _) in fams.items():
+        if ms <= 0 or nbytes <= 0:
+            continue
+        ach = nbytes / (ms * 1e-3) / 1e9
+        by_kernel[kname] = {"what": desc, "bytes_per_sort": nbytes, "ms_per_sort": ms, "achieved": ach,
+                            "frac": ach / peak, "share_of_step": ms / ms_per_step}
+    dom = max(by_kernel, key=lambda k: by_kernel[k]["ms_per_sort"])
+    dk = by_kernel[dom]
+    traffic_total, active, traffic_src = load_traffic(dom)   # one whole c2 sort under ncu (same input, same levels)
     roofline = {
-        "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+        "bound": "hbm", "achieved": dk["achieved"], "peak": peak, "unit": "GB/s", "frac": dk["frac"],
         "peak_source": peak_src,
-        "kernel": "k_part_fast (tile partition pass, every level of the sort)",
-        "algorithmic_bytes_per_launch": part_bytes / launches,
-        "launch_ms_avg": part_ms / launches,
-        "launches_per_step": launches,
-        "share_of_step": part_ms / ms_per_step,
-        "traffic": traffic_total / launches if traffic_total else None,
+        "kernel": dom + " (" + dk["what"] + ")",
+        "algorithmic_bytes_per_sort": dk["bytes_per_sort"],
+        "ms_per_sort": dk["ms_per_sort"],
+        "share_of_step": dk["share_of_step"],
+        "active_launches": active,
+        "algorithmic_bytes_per_launch": dk["bytes_per_sort"] / active if active else None,
+        "traffic": traffic_total / active if traffic_total else None,
+        "traffic_per": "active launch (ncu, one whole c2 sort: the kernel's DRAM read + write over its launches "
+                       "longer than 20 us; algorithmic_bytes_per_launch uses the same divisor)",
         "traffic_source": traffic_src,
-        "how": "CUDA events around each partition launch (bq_sort_options.timing: the host-driven level "
-               "loop, same kernels as the graph) averaged over 3 sorts; share = that time / ms_per_step",
+        "how": "CUDA events on the launching stream around every launch of the kernel family (bq_sort_options."
+               "timing: the host-driven level loop, same kernels as the graph), averaged over 3 sorts; "
+               "achieved = algorithmic bytes / that time; share = that time / ms_per_step",
     }
 
     # BASELINE.md partition-pass measurement: 10 single passes, L2 flushed
@@ -520,6 +544,7 @@ def main():
                    "timing": "sum of per-step CUDA events around bq_sort (the asynchronous graph launch) "
                              "on the launch stream"},
         "roofline": roofline,
+        "roofline_by_kernel": by_kernel,
         "partition_pass": ppass,
         "partition_pass_by_config": by_config,
         "cpu_baseline": cpu,

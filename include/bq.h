@@ -139,6 +139,11 @@ typedef struct {
                                       multiway_element_passes) */
     double multiway_ms;            /* sum of multiway level times: count + scan + scatter (timing != 0) */
     uint64_t multiway_element_passes;  /* elements through multiway levels (also in element_passes) */
+    double mw_count_ms;            /* timing != 0: the multiway levels' count + scan launches */
+    double mw_scatter_ms;          /* timing != 0: the multiway levels' scatter launches */
+    double leaf_ms;                /* timing != 0: the leaf-sort launches (a8; on the leaves' own
+                                      stream, concurrent with partition levels where the loop
+                                      overlaps them) */
 } bq_sort_stats;
 
 /* Workspace bytes every call below needs for `n` elements of `kind`:

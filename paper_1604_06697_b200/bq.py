@@ -56,7 +56,8 @@ class bq_sort_stats(ctypes.Structure):
                 ("leaves", ctypes.c_uint64), ("fallback_segments", ctypes.c_uint64),
                 ("band_elements", ctypes.c_uint64), ("partition_ms", ctypes.c_double),
                 ("partition_bytes", ctypes.c_double), ("multiway_ms", ctypes.c_double),
-                ("multiway_element_passes", ctypes.c_uint64)]
+                ("multiway_element_passes", ctypes.c_uint64), ("mw_count_ms", ctypes.c_double),
+                ("mw_scatter_ms", ctypes.c_double), ("leaf_ms", ctypes.c_double)]
 
     def as_dict(self):
         return {f: (getattr(self, f) if not isinstance(getattr(self, f), ctypes.Array) else None)

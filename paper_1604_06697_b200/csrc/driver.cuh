@@ -164,7 +164,7 @@ bq_status persistent_cap(F kern, int threads, int smem, CapCache &cc, int *cap) 
 
 // one multiway level (N4): count, scan, scatter (children by k_post_mw)
 template <class KT>
-bq_status launch_multiway(MwParams<KT> MP, LevelCtrl *lc, cudaStream_t s, int ways) {
+bq_status launch_multiway(MwParams<KT> MP, LevelCtrl *lc, cudaStream_t s, int ways, cudaEvent_t mid = nullptr) {
     using Kn = Kernels<KT>;
     constexpr int threads = Kn::NT + 32;
 #if BQ_MW8W
@@ -183,6 +183,7 @@ bq_status launch_multiway(MwParams<KT> MP, LevelCtrl *lc, cudaStream_t s, int wa
         const uint32_t nb = (MP.max_tiles * mw8w_umin<KT>() + MW8W_ROWS_EXTRA + MWS_BR - 1) / MWS_BR;
         k_mw8w_scan<KT><<<nb < 592 ? nb : 592, 256, 0, s>>>(MP);
         BQ_CK_LAUNCH();
+        if (mid) BQ_CK(cudaEventRecord(mid, s));   // timing: count + scan | scatter
 #if BQ_MW8T
 #ifndef BQ_MW8T_PAIR
 #define BQ_MW8T_PAIR 1
@@ -220,6 +221,7 @@ bq_status launch_multiway(MwParams<KT> MP, LevelCtrl *lc, cudaStream_t s, int wa
         BQ_CK_LAUNCH();
         k_mw_scan<KT><<<POST_GRID / 8, 256, 0, s>>>(MP);
         BQ_CK_LAUNCH();
+        if (mid) BQ_CK(cudaEventRecord(mid, s));
         MP.ticket = lc ? &lc->mw_ticket_scatter : nullptr;
         MP.ticket_sel = 1;
         ks8<<<cap_s8, threads, smem8, s>>>(MP);
@@ -241,6 +243,7 @@ bq_status launch_multiway(MwParams<KT> MP, LevelCtrl *lc, cudaStream_t s, int wa
     BQ_CK_LAUNCH();
     k_mw_scan<KT><<<POST_GRID / 8, 256, 0, s>>>(MP);
     BQ_CK_LAUNCH();
+    if (mid) BQ_CK(cudaEventRecord(mid, s));
     MP.ticket = lc ? &lc->mw_ticket_scatter : nullptr;
     MP.ticket_sel = 1;
     ks<<<cap_s, threads, smem, s>>>(MP);
@@ -760,11 +763,11 @@ bq_status enqueue_prefix(const SortPlan<KT> &pl, cudaStream_t s) {
 template <class KT>
 bq_status enqueue_level(const SortPlan<KT> &pl, cudaStream_t s, int use_cond, cudaGraphConditionalHandle h_loop,
                         cudaGraphConditionalHandle h_fb, cudaEvent_t ev0, cudaEvent_t ev1, cudaEvent_t mev0 = nullptr,
-                        cudaEvent_t mev1 = nullptr) {
+                        cudaEvent_t mev1 = nullptr, cudaEvent_t mmid = nullptr) {
     if constexpr (mw_capable<KT>()) if (pl.ways > 2) {
         MwParams<KT> MP = pl.MP;
         if (mev0) BQ_CK(cudaEventRecord(mev0, s));
-        bq_status st = launch_multiway<KT>(MP, nullptr, s, pl.ways);
+        bq_status st = launch_multiway<KT>(MP, nullptr, s, pl.ways, mmid);
         if (st != BQ_OK) return st;
         if (mev1) BQ_CK(cudaEventRecord(mev1, s));
         k_post_mw<KT, POST_THREADS><<<POST_GRID, POST_THREADS, 0, s>>>(pl.Q);
@@ -789,7 +792,8 @@ bq_status enqueue_level_end(const SortPlan<KT> &pl, cudaStream_t s, int use_cond
 // sort the previous level's leaves (set (level + 1) & 1; one persistent
 // launch per class), copy its finished equal-record runs, empty the set
 template <class KT>
-bq_status enqueue_flush(const SortPlan<KT> &pl, cudaStream_t s) {
+bq_status enqueue_flush(const SortPlan<KT> &pl, cudaStream_t s, cudaEvent_t l0 = nullptr, cudaEvent_t l1 = nullptr) {
+    if (l0) BQ_CK(cudaEventRecord(l0, s));   // timing: around the leaf launches
     for (int c = 0; c < leaf_nclass<KT>(); c++) {
         LeafParams<KT> LP = pl.LP;
         LP.lcls = (size_t)c * pl.L.max_leaves;
@@ -797,6 +801,7 @@ bq_status enqueue_flush(const SortPlan<KT> &pl, cudaStream_t s) {
         bq_status st = launch_leaves<KT>(c, LP, 0, s);
         if (st != BQ_OK) return st;
     }
+    if (l1) BQ_CK(cudaEventRecord(l1, s));
     if (KT::is_record && !pl.ordered) {
         k_copy_runs<KT, POST_THREADS><<<POST_GRID, POST_THREADS, 0, s>>>(pl.lp, &pl.misc->level, pl.user, pl.scratch);   // (set: pl.lp.set)
         BQ_CK_LAUNCH();
@@ -1015,12 +1020,20 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
     }();
     const bool host_loop = timing || host_env;
     std::vector<cudaEvent_t> evs;   // timing: one pair per level
-    std::vector<cudaEvent_t> mevs;  // timing: one pair per level around the multiway step
+    std::vector<cudaEvent_t> mevs;  // timing: one triple per level around the multiway step (count+scan | scatter)
+    std::vector<cudaEvent_t> levs;  // timing: one pair per flush around the leaf launches
+    auto mkev = [&](std::vector<cudaEvent_t> &v) -> cudaEvent_t {
+        cudaEvent_t e = nullptr;
+        if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+        v.push_back(e);
+        return e;
+    };
     cudaStream_t side = nullptr;    // host-driven loop: the leaves' stream
     cudaEvent_t efork = nullptr, ejoin = nullptr;
     auto cleanup = [&]() {
         for (auto e : evs) cudaEventDestroy(e);
         for (auto e : mevs) cudaEventDestroy(e);
+        for (auto e : levs) cudaEventDestroy(e);
         if (side) cudaStreamDestroy(side);
         if (efork) cudaEventDestroy(efork);
         if (ejoin) cudaEventDestroy(ejoin);
@@ -1061,27 +1074,24 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
                 cleanup();
                 return set_error(BQ_ERR_CUDA, "level loop did not terminate");
             }
-            cudaEvent_t e0 = nullptr, e1 = nullptr, m0 = nullptr, m1 = nullptr;
+            cudaEvent_t e0 = nullptr, e1 = nullptr, m0 = nullptr, m1 = nullptr, mm = nullptr;
             if (timing) {
-                BQ_CKC(cudaEventCreate(&e0));
-                evs.push_back(e0);
-                BQ_CKC(cudaEventCreate(&e1));
-                evs.push_back(e1);
-                if (ways > 2) {
-                    BQ_CKC(cudaEventCreate(&m0));
-                    mevs.push_back(m0);
-                    BQ_CKC(cudaEventCreate(&m1));
-                    mevs.push_back(m1);
+                if (!(e0 = mkev(evs)) || !(e1 = mkev(evs))) { cleanup(); return set_error(BQ_ERR_CUDA, "event"); }
+                if (ways > 2 && (!(m0 = mkev(mevs)) || !(mm = mkev(mevs)) || !(m1 = mkev(mevs)))) {
+                    cleanup();
+                    return set_error(BQ_ERR_CUDA, "event");
                 }
             }
             const int B = (int)pl.batch;
             if (level % B == 0) {   // fork
+                cudaEvent_t l0 = nullptr, l1 = nullptr;
+                if (timing && (!(l0 = mkev(levs)) || !(l1 = mkev(levs)))) { cleanup(); return set_error(BQ_ERR_CUDA, "event"); }
                 BQ_CKC(cudaEventRecord(efork, s));
                 BQ_CKC(cudaStreamWaitEvent(side, efork, 0));
-                BQ_SKC(enqueue_flush<KT>(pl, side));
+                BQ_SKC(enqueue_flush<KT>(pl, side, l0, l1));
                 BQ_CKC(cudaEventRecord(ejoin, side));
             }
-            BQ_SKC(enqueue_level<KT>(pl, s, 0, 0, 0, e0, e1, m0, m1));
+            BQ_SKC(enqueue_level<KT>(pl, s, 0, 0, 0, e0, e1, m0, m1, mm));
             if (level % B == B - 1) BQ_CKC(cudaStreamWaitEvent(s, ejoin, 0));   // join
             BQ_SKC(enqueue_level_end<KT>(pl, s, 0, 0, 0));
             host_levels = level + 1;
@@ -1091,7 +1101,11 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
                 if (hc[0].nseg_next + hc[0].nmseg_next == 0) break;
             }
         }
-        BQ_SKC(enqueue_flush<KT>(pl, s));   // (the loop always ends on a batch boundary)
+        {
+            cudaEvent_t l0 = nullptr, l1 = nullptr;
+            if (timing && (!(l0 = mkev(levs)) || !(l1 = mkev(levs)))) { cleanup(); return set_error(BQ_ERR_CUDA, "event"); }
+            BQ_SKC(enqueue_flush<KT>(pl, s, l0, l1));   // (the loop always ends on a batch boundary)
+        }
         // a9: the depth-capped segments
         LoopMisc hm;
         BQ_CKC(cudaMemcpyAsync(&hm, pl.misc, sizeof hm, cudaMemcpyDeviceToHost, s));
@@ -1148,13 +1162,24 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
                 ms += f;
             }
             local.partition_ms = ms;
-            ms = 0;
-            for (size_t i = 0; i + 1 < mevs.size() && (int)(i / 2) < (int)local.levels; i += 2) {
-                float f = 0;
+            double mc = 0, msc = 0;
+            for (size_t i = 0; i + 2 < mevs.size() && (int)(i / 3) < (int)local.levels; i += 3) {
+                float f = 0, g = 0;
                 BQ_CKC(cudaEventElapsedTime(&f, mevs[i], mevs[i + 1]));
-                ms += f;
+                BQ_CKC(cudaEventElapsedTime(&g, mevs[i + 1], mevs[i + 2]));
+                mc += f;
+                msc += g;
             }
-            local.multiway_ms = ms;
+            local.multiway_ms = mc + msc;
+            local.mw_count_ms = mc;
+            local.mw_scatter_ms = msc;
+            double lm = 0;
+            for (size_t i = 0; i + 1 < levs.size(); i += 2) {
+                float f = 0;
+                BQ_CKC(cudaEventElapsedTime(&f, levs[i], levs[i + 1]));
+                lm += f;
+            }
+            local.leaf_ms = lm;
         }
     }
 #undef BQ_CKC

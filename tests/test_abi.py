@@ -127,7 +127,7 @@ def test_options_struct_layout():
     size = {"uint32_t": 4, "uint64_t": 8, "double": 8}
     fields = re.findall(r"^\s*(uint32_t|uint64_t|double) (\w+);", body, re.M)
     assert [f for f, _ in b.bq_sort_stats._fields_] == [nm for _, nm in fields]
-    assert ctypes.sizeof(b.bq_sort_stats) == sum(size[t] for t, _ in fields) == 88
+    assert ctypes.sizeof(b.bq_sort_stats) == sum(size[t] for t, _ in fields) == 112
 
 
 def test_binding_refuses_ambiguous_int64():
