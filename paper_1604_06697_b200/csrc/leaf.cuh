@@ -232,18 +232,17 @@ __device__ __forceinline__ typename LeafTraits<KT>::E leaf_pad() {
 }
 
 // x[0, cnt) -> slots base + k * dir (dir = +1 ascending, -1 descending).
-// Full threads (cnt == IPT, all but at most one) store IPT consecutive
-// slots from their lowest one, each value selected from x[m] or x[IPT-1-m]:
-// one select and one store with an immediate offset per key.
 template <class E, int IPT, class PL>
 __device__ __forceinline__ void store_run(const PL &pl, const E (&x)[IPT], int cnt, int base, int dir) {
     BQ_CHECK(cnt >= 0 && cnt <= IPT);
     if (cnt == 0) return;
     if (cnt == IPT) {
-        const bool rev = dir < 0;
-        const uint32_t c0 = pl.cur(rev ? base - (IPT - 1) : base);
+        // the address walks in the run's direction (an IMAD per key on the
+        // FMA pipe; a select of x[m] or x[IPT-1-m] would take the ALU pipe
+        // the merge loop saturates)
+        const uint32_t c0 = pl.cur(base), step = (uint32_t)(dir * PL::STEP);
 #pragma unroll
-        for (int m = 0; m < IPT; m++) pl.stc(c0 + (uint32_t)(m * PL::STEP), rev ? x[IPT - 1 - m] : x[m]);
+        for (int m = 0; m < IPT; m++) pl.stc(c0 + (uint32_t)m * step, x[m]);
     } else {
 #pragma unroll
         for (int k = 0; k < IPT; k++)
