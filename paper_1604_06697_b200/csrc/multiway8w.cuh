@@ -125,6 +125,76 @@ __device__ __forceinline__ uint32_t mw8w_load(const typename KT::T *src, uint32_
     return valid;
 }
 
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
+    asm volatile("st.shared.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+
+// ---- the splitter tree in shared memory ---------------------------------------------
+// Levels 1 and 2 of the three-compare bucket search read their splitter from
+// a per-warp copy of the tree in shared memory, and the key's leaf value (the
+// count kernel's one-hot counter increment) comes from a table there: per key
+// three compares, three selects, three predicated adds and three shared loads,
+// against the four register selects plus the increment's construction that
+// kept the ALU pipe saturated (int32 count: 17 instructions per key, ALU 75 %).
+// The addresses are built from p0 alone (selects issued beside the first
+// load) plus the later predicates; a linked variant (each record holding its
+// children's address) had fewer instructions but a longer dependent chain and
+// ran slower (profiles/r02/mw8t.md).
+template <class KT> struct Mw8CmpT { using type = typename KT::K; };
+template <> struct Mw8CmpT<KF64> { using type = double; };
+template <class KT>
+struct Mw8Smt {
+    typename Mw8CmpT<KT>::type node[MW8];   // node[j], j = 1..7 (heap order, mw_splitters)
+    uint32_t leaf[MW8];                     // leaf value of bucket b
+};
+__device__ __forceinline__ int32_t lds_ck(uint32_t a, int32_t *) { return (int32_t)lds32(a); }
+__device__ __forceinline__ uint64_t lds_ck(uint32_t a, uint64_t *) {
+    uint64_t v;
+    asm volatile("ld.shared.b64 %0, [%1];" : "=l"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ double lds_ck(uint32_t a, double *) { return __longlong_as_double((long long)lds_ck(a, (uint64_t *)nullptr)); }
+// the key as the classification compares it (float64: the double)
+template <class KT>
+__device__ __forceinline__ typename Mw8CmpT<KT>::type mw8_ckey(const typename KT::T &x) {
+    if constexpr (std::is_same<KT, KF64>::value) return __longlong_as_double((long long)x);
+    else return KT::key(x);
+}
+// lanes 0..7 write the tree of segment si (leaf value of bucket b: leaf(b))
+template <class KT, class F>
+__device__ __forceinline__ void mw8_smt_write(const MwParams<KT> &P, uint32_t si, Mw8Smt<KT> &t, uint32_t lane, F leaf) {
+    __syncwarp();   // the previous segment's readers are done
+    if (lane < MW8) {
+        const typename KT::K w = mw8_tree_word<KT>(P.msegs[si].tree[lane]);
+        if constexpr (std::is_same<KT, KF64>::value) t.node[lane] = __longlong_as_double((long long)w);
+        else t.node[lane] = w;
+        t.leaf[lane] = leaf(lane);
+    }
+    __syncwarp();
+}
+// the leaf value of key k: tb = the shared address of node[0], lb = of
+// leaf[0], t1 = node[1] (in a register)
+template <class CK>
+__device__ __forceinline__ uint32_t mw8_smt_leaf(uint32_t tb, uint32_t lb, CK t1, CK k) {
+    constexpr uint32_t SZ = sizeof(CK);
+    const bool p0 = t1 < k;
+    const uint32_t a1 = p0 ? tb + 3 * SZ : tb + 2 * SZ;
+    uint32_t a2 = p0 ? tb + 6 * SZ : tb + 4 * SZ;
+    uint32_t al = p0 ? lb + 16u : lb;
+    const CK n1 = lds_ck(a1, (CK *)nullptr);
+    const bool p1 = n1 < k;
+    if (p1) a2 += SZ;
+    if (p1) al += 8u;
+    const CK n2 = lds_ck(a2, (CK *)nullptr);
+    if (n2 < k) al += 4u;
+    return lds32(al);
+}
+
 // ---- k_mw8w_count ------------------------------------------------------------------
 template <class KT, int IPT>
 __global__ void __launch_bounds__(MW8W_WARPS * 32) k_mw8w_count(const MwParams<KT> Pin) {
@@ -139,9 +209,18 @@ __global__ void __launch_bounds__(MW8W_WARPS * 32) k_mw8w_count(const MwParams<K
     // a warp's item: a whole tile (its U rows) on large levels, one unit on
     // small ones (so that every warp has work)
     const uint32_t lgG = ntiles * U >= 8192 ? lgU : 0, nitems = (ntiles * U) >> lgG;
-    constexpr int NR = sizeof(T) <= 4 ? 4 : 1;   // rounds loaded before the first is classified
+#ifndef BQ_MW8_NR
+#define BQ_MW8_NR 4
+#endif
+    constexpr int NR = sizeof(T) <= 4 ? BQ_MW8_NR : 1;   // rounds loaded before the first is classified
+    using CK = typename Mw8CmpT<KT>::type;
+    __shared__ Mw8Smt<KT> s_tree[MW8W_WARPS];
+    Mw8Smt<KT> &smt = s_tree[threadIdx.x >> 5];
+    const uint32_t tb = smem_u32(smt.node), lb = smem_u32(smt.leaf);
     uint32_t cls_seg = 0xffffffffu;
     Mw8Cls<KT> cls;
+    CK t1{};
+    const bool aligned = P.aligned;
     for (uint32_t it = blockIdx.x * MW8W_WARPS + (threadIdx.x >> 5); it < nitems; it += gridDim.x * MW8W_WARPS) {
         const uint32_t u0 = it << lgG, t = u0 >> lgU;
         const uint32_t si = P.tile_map[t];
@@ -149,6 +228,8 @@ __global__ void __launch_bounds__(MW8W_WARPS * 32) k_mw8w_count(const MwParams<K
         if (si != cls_seg) {
             mw8w_load_cls<KT>(P, si, cls);
             cls_seg = si;
+            mw8_smt_write<KT>(P, si, smt, lane, [](uint32_t b) { return 1u << (4 * b); });
+            t1 = cls.tr[1];
         }
         const TileGeom<KT, TILE> G(sg, t);
         const T *src = (sg.parity ? P.bufs[1] : P.bufs[0]) + G.tbeg;
@@ -156,33 +237,57 @@ __global__ void __launch_bounds__(MW8W_WARPS * 32) k_mw8w_count(const MwParams<K
             const uint32_t ub = (u & (U - 1)) * UL;
             const uint32_t lo = G.vlo > ub ? G.vlo : ub, hi = G.vhi < ub + UL ? G.vhi : ub + UL;   // the unit's keys
             uint32_t alo = 0, ahi = 0;   // byte counters: <= TILE / 32 per lane
-            for (uint32_t r0 = lo / RK * RK; r0 < hi; r0 += NR * RK) {
-                T x[NR][IPT];
-                uint32_t valid[NR];
+            // one round's keys into the counters (valid: the keys inside the unit)
+            auto tally = [&](const T (&xr)[IPT], uint32_t valid) {
+                uint32_t inc[IPT];
+                bool nan = false;
 #pragma unroll
-                for (int h = 0; h < NR; h++) valid[h] = mw8w_load<KT, IPT>(src, r0 + h * RK, lo, hi, lane, P.aligned, x[h]);
+                for (int c = 0; c < IPT; c++) {
+                    const CK k = mw8_ckey<KT>(xr[c]);
+                    if constexpr (std::is_same<KT, KF64>::value) nan |= k != k;
+                    inc[c] = mw8_smt_leaf(tb, lb, t1, k);
+                }
+                if (nan)
 #pragma unroll
-                for (int h = 0; h < NR; h++) {
-                    uint32_t inc[IPT];
-                    bool nan = false;
+                    for (int c = 0; c < IPT; c++) inc[c] = 1u << cls.fix4(xr[c], 31 - __clz(inc[c]));
+                Mw8Ctr<IPT> ctr;
+                if (valid == (1u << IPT) - 1) {
 #pragma unroll
-                    for (int c = 0; c < IPT; c++) inc[c] = cls.inc(x[h][c], nan);
-                    if (nan)
+                    for (int c = 0; c < IPT; c++) ctr.c += inc[c];
+                } else {
 #pragma unroll
-                        for (int c = 0; c < IPT; c++) inc[c] = 1u << cls.fix4(x[h][c], 31 - __clz(inc[c]));
-                    Mw8Ctr<IPT> ctr;
-                    if (valid[h] == (1u << IPT) - 1) {
+                    for (int c = 0; c < IPT; c++)
+                        if ((valid >> c) & 1) ctr.c += inc[c];
+                }
+                uint32_t lo, hi;
+                ctr.bytes(lo, hi);
+                alo += lo;
+                ahi += hi;
+            };
+            if (aligned && lo == ub && hi == ub + UL && UL % (NR * RK) == 0) {
+                // a whole unit (the common case): one base pointer, no per-round checks
+                constexpr uint32_t VW = sizeof(T) >= 16 ? 1u : 16u / (uint32_t)sizeof(T), NV = IPT / VW;
+                const uint4 *p4 = reinterpret_cast<const uint4 *>(src + ub) + lane;
+                for (uint32_t s0 = 0; s0 < UL; s0 += NR * RK) {
+                    T x[NR][IPT];
 #pragma unroll
-                        for (int c = 0; c < IPT; c++) ctr.c += inc[c];
-                    } else {
+                    for (int h = 0; h < NR; h++)
 #pragma unroll
-                        for (int c = 0; c < IPT; c++)
-                            if ((valid[h] >> c) & 1) ctr.c += inc[c];
-                    }
-                    uint32_t lo, hi;
-                    ctr.bytes(lo, hi);
-                    alo += lo;
-                    ahi += hi;
+                        for (uint32_t v = 0; v < NV; v++) {
+                            const uint4 q = ldg_stream(p4 + (s0 + h * RK) / VW + v * 32);
+                            memcpy(&x[h][v * VW], &q, 16);
+                        }
+#pragma unroll
+                    for (int h = 0; h < NR; h++) tally(x[h], (1u << IPT) - 1);
+                }
+            } else {
+                for (uint32_t r0 = lo / RK * RK; r0 < hi; r0 += NR * RK) {
+                    T x[NR][IPT];
+                    uint32_t valid[NR];
+#pragma unroll
+                    for (int h = 0; h < NR; h++) valid[h] = mw8w_load<KT, IPT>(src, r0 + h * RK, lo, hi, lane, aligned, x[h]);
+#pragma unroll
+                    for (int h = 0; h < NR; h++) tally(x[h], valid[h]);
                 }
             }
             uint32_t q[MW8 / 2];
@@ -598,14 +703,6 @@ __device__ __forceinline__ void mw8t_issue(const Mw8tUnit<KT> &w, typename KT::T
     }
 }
 
-__device__ __forceinline__ uint32_t lds32(uint32_t a) {
-    uint32_t v;
-    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a));
-    return v;
-}
-__device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
-    asm volatile("st.shared.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
-}
 __device__ __forceinline__ void sts_t(uint32_t a, uint32_t v) { sts32(a, v); }
 __device__ __forceinline__ void sts_t(uint32_t a, int32_t v) { sts32(a, (uint32_t)v); }
 __device__ __forceinline__ void sts_t(uint32_t a, uint64_t v) {
@@ -651,6 +748,14 @@ __global__ void __launch_bounds__(MW8W_WARPS * 32, Mw8tTune<KT>::MINB) k_mw8t_sc
     uint32_t par = 0, ph = 0, cls_seg = 0xffffffffu, seg_base = 0;
     bool stores_out = false;   // lanes 0..7: a bulk store of the stage may still read it
     Mw8Cls<KT> cls;
+#ifndef BQ_MW8T_SMT
+#define BQ_MW8T_SMT 0
+#endif
+    using CK = typename Mw8CmpT<KT>::type;
+    __shared__ Mw8Smt<KT> s_tree[MW8W_WARPS];   // (BQ_MW8T_SMT: the splitter tree in shared memory)
+    Mw8Smt<KT> &smt = s_tree[threadIdx.x >> 5];
+    const uint32_t tb = smem_u32(smt.node), lb = smem_u32(smt.leaf);
+    CK t1{};
     // global prefix of table row r, lane b < 8: bucket b (as the two words
     // it sums, loaded a unit before they are added)
     auto prefix2 = [&](uint32_t r) -> uint2 {
@@ -676,6 +781,10 @@ __global__ void __launch_bounds__(MW8W_WARPS * 32, Mw8tTune<KT>::MINB) k_mw8t_sc
         }
         if (cur.si != cls_seg) {
             mw8w_load_cls<KT>(P, cur.si, cls);
+            if (BQ_MW8T_SMT) {
+                mw8_smt_write<KT>(P, cur.si, smt, lane, [](uint32_t b) { return 128u * b; });
+                t1 = cls.tr[1];
+            }
             uint32_t tot, start, pf;
             mw8w_seg_buckets(P, cur.row0, cur.nrows, rows, lane, tot, start, pf);
             seg_base = cur.begin + start - pf;   // lane b: bucket b's output base minus its rows' prefix
@@ -736,7 +845,15 @@ __global__ void __launch_bounds__(MW8W_WARPS * 32, Mw8tTune<KT>::MINB) k_mw8t_sc
                 {
                     bool nan = false;
 #pragma unroll
-                    for (int c = 0; c < IPT; c++) ra[c] = cls.a128(x[c], exrow, nan);
+                    for (int c = 0; c < IPT; c++) {
+                        if constexpr (BQ_MW8T_SMT) {
+                            const CK k = mw8_ckey<KT>(x[c]);
+                            if constexpr (std::is_same<KT, KF64>::value) nan |= k != k;
+                            ra[c] = exrow + mw8_smt_leaf(tb, lb, t1, k);
+                        } else {
+                            ra[c] = cls.a128(x[c], exrow, nan);
+                        }
+                    }
                     if (nan)
 #pragma unroll
                         for (int c = 0; c < IPT; c++) ra[c] = exrow + 32u * cls.fix4(x[c], (ra[c] - exrow) >> 5);
