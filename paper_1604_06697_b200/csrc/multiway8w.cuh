@@ -23,7 +23,12 @@
 
 namespace bq {
 
-constexpr uint32_t MWS_BR = 2048;   // tiles per block of the tile-count scan (8 per thread)
+#ifndef BQ_MWS_BR
+#define BQ_MWS_BR 512
+#endif
+constexpr uint32_t MWS_BR = BQ_MWS_BR;   // table rows per block of the row-count scan (256 threads)
+constexpr uint32_t MWS_RPT = MWS_BR / 256;   // rows per thread
+static_assert(MWS_BR % 256 == 0, "whole rows per thread");
 constexpr int MW8W_WARPS = 8;       // warps per CTA of the count and scatter kernels
 #ifndef BQ_MW8W_MINB
 #define BQ_MW8W_MINB 2
@@ -352,9 +357,9 @@ __global__ void __launch_bounds__(256) k_mw8w_scan(const MwParams<KT> Pin) {
     const uint32_t nblk = (ntiles + MWS_BR - 1) / MWS_BR;
     uint32_t done = 0;
     for (uint32_t blk = blockIdx.x; blk < nblk; blk += gridDim.x, done++) {
-        const uint32_t t0 = blk * MWS_BR + tid * 8;
+        const uint32_t t0 = blk * MWS_BR + tid * MWS_RPT;
         uint32_t sum[MW8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        for (uint32_t t = t0; t < t0 + 8 && t < ntiles; t++) {
+        for (uint32_t t = t0; t < t0 + MWS_RPT && t < ntiles; t++) {
             const uint4 *row = reinterpret_cast<const uint4 *>(P.mtab + (size_t)t * MW8);
             const uint4 a = row[0], b = row[1];
             sum[0] += a.x; sum[1] += a.y; sum[2] += a.z; sum[3] += a.w;
@@ -365,7 +370,7 @@ __global__ void __launch_bounds__(256) k_mw8w_scan(const MwParams<KT> Pin) {
         if (tid == 0)
 #pragma unroll
             for (int k = 0; k < MW8; k++) P.mblk[(size_t)blk * MW8 + k] = all[k];
-        for (uint32_t t = t0; t < t0 + 8 && t < ntiles; t++) {
+        for (uint32_t t = t0; t < t0 + MWS_RPT && t < ntiles; t++) {
             uint4 *row = reinterpret_cast<uint4 *>(P.mtab + (size_t)t * MW8);
             const uint4 a = row[0], b = row[1];
             row[0] = make_uint4(pre[0], pre[1], pre[2], pre[3]);
