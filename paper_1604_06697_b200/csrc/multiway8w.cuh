@@ -299,9 +299,8 @@ __global__ void __launch_bounds__(MW8W_WARPS * 32) k_mw8w_count(const MwParams<K
             mw8_widen((uint64_t)alo | ((uint64_t)ahi << 32), q);
 #pragma unroll
             for (int k = 0; k < MW8 / 2; k++) q[k] = __reduce_add_sync(0xffffffffu, q[k]);   // (16-bit fields <= 4096)
-            uint32_t mine = 0;
-#pragma unroll
-            for (int k = 0; k < MW8 / 2; k++) mine = (lane >> 1) == (uint32_t)k ? q[k] : mine;
+            // (selects with constant indices: a run-time index put q in local memory)
+            const uint32_t mine = (lane & 4) ? ((lane & 2) ? q[3] : q[2]) : ((lane & 2) ? q[1] : q[0]);
             if (lane < MW8) P.mtab[(size_t)u * MW8 + lane] = (lane & 1) ? (mine >> 16) : (mine & 0xffff);
         }
     }
@@ -507,7 +506,7 @@ __global__ void __launch_bounds__(MW8W_WARPS * 32, Mw8wTune<KT>::MINB) k_mw8w_sc
     constexpr uint32_t TILE = (uint32_t)tile_elems<KT>(), RK = 32u * IPT;
     constexpr uint32_t VW = sizeof(T) >= 16 ? 1u : 16u / (uint32_t)sizeof(T), NV = IPT / VW;
     static_assert(TILE % RK == 0 && IPT <= 8, "rounds per tile; byte-field scans");
-    extern __shared__ __align__(16) unsigned char smraw[];
+    extern __shared__ __align__(128) unsigned char smraw[];
     WS &ws = reinterpret_cast<WS *>(smraw)[threadIdx.x >> 5];
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t U = mw8w_upt<KT>(*P.ntiles_dev), ntiles = *P.ntiles_dev * U;   // units (table rows)
@@ -733,7 +732,7 @@ __global__ void __launch_bounds__(MW8W_WARPS * 32, Mw8tTune<KT>::MINB) k_mw8t_sc
     using WS = Mw8tWarpSmem<KT, IPT>;
     constexpr uint32_t RK = 32u * IPT, VW = tile_vw<KT>(), NV = IPT / VW;
     static_assert(IPT % VW == 0 && IPT <= 8 && WS::SCAP < 65536, "whole vectors; byte-field scans; 16-bit slots");
-    extern __shared__ __align__(16) unsigned char smraw[];
+    extern __shared__ __align__(128) unsigned char smraw[];
     WS &ws = reinterpret_cast<WS *>(smraw)[threadIdx.x >> 5];
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t nt = *P.ntiles_dev, U = mw8w_upt<KT>(nt), rows = nt * U;
