@@ -762,15 +762,14 @@ __global__ void __launch_bounds__(MW8W_WARPS * 32, Mw8tTune<KT>::MINB) k_mw8t_sc
     CK t1{};
     // global prefix of table row r, lane b < 8: bucket b (as the two words
     // it sums, loaded a unit before they are added)
+    // (every lane loads, lanes >= 8 the words of bucket 7, so no branch
+    // divides the warp around the loads)
+    const uint32_t lb7 = lane < MW8 ? lane : MW8 - 1;
     auto prefix2 = [&](uint32_t r) -> uint2 {
-        return r < rows ? make_uint2(P.mtab[(size_t)r * MW8 + lane], P.mblk[(size_t)(r / MWS_BR) * MW8 + lane])
-                        : make_uint2(P.mblk[(size_t)nblk * MW8 + lane], 0u);
+        return r < rows ? make_uint2(P.mtab[(size_t)r * MW8 + lb7], P.mblk[(size_t)(r / MWS_BR) * MW8 + lb7])
+                        : make_uint2(P.mblk[(size_t)nblk * MW8 + lb7], 0u);
     };
-    uint2 pu = make_uint2(0, 0), pe = pu;   // lanes b < 8: global prefixes of the unit's row and the next row
-    if (lane < MW8) {
-        pu = prefix2(cur.u);
-        pe = prefix2(cur.u + 1);
-    }
+    uint2 pu = prefix2(cur.u), pe = prefix2(cur.u + 1);   // global prefixes of the unit's row and the next row
     for (;;) {
         const bool more = cur.u + stride < rows;
         Mw8tUnit<KT> nxt = cur;
@@ -778,10 +777,8 @@ __global__ void __launch_bounds__(MW8W_WARPS * 32, Mw8tTune<KT>::MINB) k_mw8t_sc
         if (more) {
             nxt = mw8t_unit(P, cur.u + stride, U);
             mw8t_issue<KT>(nxt, ws.in[par ^ 1], &ws.bar[par ^ 1], lane);
-            if (lane < MW8) {   // (loaded a unit ahead)
-                pu_n = prefix2(nxt.u);
-                pe_n = prefix2(nxt.u + 1);
-            }
+            pu_n = prefix2(nxt.u);   // (loaded a unit ahead)
+            pe_n = prefix2(nxt.u + 1);
         }
         if (cur.si != cls_seg) {
             mw8w_load_cls<KT>(P, cur.si, cls);
@@ -796,12 +793,8 @@ __global__ void __launch_bounds__(MW8W_WARPS * 32, Mw8tTune<KT>::MINB) k_mw8t_sc
         }
         // lanes b < 8: the unit's run of bucket b: global start G, length nb,
         // stage slot S (S = G modulo VW)
-        uint32_t G = 0, nb = 0;
-        if (lane < MW8) {
-            const uint32_t p0 = pu.x + pu.y;
-            nb = pe.x + pe.y - p0;
-            G = seg_base + p0;
-        }
+        const uint32_t p0 = pu.x + pu.y;
+        const uint32_t nb = lane < MW8 ? pe.x + pe.y - p0 : 0u, G = lane < MW8 ? seg_base + p0 : 0u;
         uint32_t S = nb + VW - 1;
 #pragma unroll
         for (int d = 1; d < MW8; d <<= 1) {

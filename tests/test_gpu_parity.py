@@ -112,6 +112,21 @@ def test_sort_unaligned_pointer(B, kind):
         check_sorted_equal(kind, to_host(t, a), a)
 
 
+@pytest.mark.parametrize("kind", ["i32", "u64", "f64"])
+def test_sort_multiway_unaligned_pointer(B, kind):
+    """8-way levels over a buffer that is not 16-byte aligned: the scatter
+    without bulk copies (k_mw8w_scatter) places the keys; aligned, the same
+    input goes through the TMA-staged scatter (k_mw8t_scatter)."""
+    for n in [300007, (1 << 20) + 5]:
+        a = make(kind, n, seed=11)
+        for off in (1, 0):
+            t = to_dev(a, offset=off)
+            assert (t.data_ptr() % 16 != 0) == (off == 1)
+            st = B.bq_sort_ex(t, ways=8)
+            check_sorted_equal(kind, to_host(t, a), a)
+            assert st["multiway_element_passes"] > 0 and st["fallback_segments"] == 0
+
+
 def test_sort_configs_reduced(B):
     n = 1 << 20
     for name in ["c1", "c2", "c4a", "c4b", "c5"]:
