@@ -103,7 +103,22 @@ def partition_pass_by_config(bq, bqgen, dev, stream, passes, peak):
             flush.fill_(1)
             st.append(bq.bq_sort_ex(data, timing=True, ws=ws, stream=stream))
         ms = statistics.median(s["multiway_ms"] for s in st)
-        return ms, st[-1]["multiway_element_passes"], st[-1]
+        return ms, st[-1]["multiway_element_passes"], st[-1], {
+            "scatter_ms": statistics.median(s["mw_scatter_ms"] for s in st),
+            "count_scan_ms": statistics.median(s["mw_count_ms"] for s in st)}
+
+    def mw_entry(ms, ep, st, parts, w, **kw):
+        """an 8-way level: 2 w per element-pass against the whole level (the
+        count's extra read counts against it), and each kernel on its own bytes
+        (scatter: read + write, count: read)"""
+        e = entry(ms, 2 * w * ep, element_passes=ep, levels=st["levels"], **kw)
+        sc, cn = parts["scatter_ms"], parts["count_scan_ms"]
+        e["level_bytes_moved_frac_of_measured"] = 3 * w * ep / (ms * 1e-3) / 1e9 / peak
+        e["scatter"] = {"ms": sc, "gbs": 2 * w * ep / (sc * 1e-3) / 1e9,
+                        "frac_of_measured": 2 * w * ep / (sc * 1e-3) / 1e9 / peak}
+        e["count_scan"] = {"ms": cn, "gbs": w * ep / (cn * 1e-3) / 1e9,
+                           "frac_of_measured": w * ep / (cn * 1e-3) / 1e9 / peak}
+        return e
 
     out = {}
     # c3: float64, n = 2^27, random
@@ -114,8 +129,15 @@ def partition_pass_by_config(bq, bqgen, dev, stream, passes, peak):
     ws = bq.workspace(bq.BQ_F64, n3, dev)
     pv = bq.bq_pivot_f64(src, bq.BQ_PIVOT_MO3, ws=ws, stream=stream)
     out["c3_f64_binary_pass"] = entry(time_passes(src, dst, pv, False, ws), 16 * n3, n=n3)
-    ms, ep, st = time_mw(dst, src, ws)
-    out["c3_f64_8way_levels"] = entry(ms, 16 * ep, n=n3, element_passes=ep, levels=st["levels"])
+    out["c3_f64_8way_levels"] = mw_entry(*time_mw(dst, src, ws), 8, n=n3)
+    del src, dst, ws
+    # c2: int32, n = 2^28: the sort's 8-way levels (its default)
+    a = bqgen.config("c2", seed=1)
+    n2 = len(a)
+    src = torch.from_numpy(a).to(dev)
+    dst = torch.empty_like(src)
+    ws = bq.workspace(bq.BQ_I32, n2, dev)
+    out["c2_i32_8way_levels"] = mw_entry(*time_mw(dst, src, ws), 4, n=n2)
     del src, dst, ws
     # c4a: int32, n = 2^28, 16384 distinct values
     a = bqgen.config("c4a", seed=1)
@@ -136,9 +158,8 @@ def partition_pass_by_config(bq, bqgen, dev, stream, passes, peak):
     pv = bq.bq_pivot_records(src, bq.BQ_PIVOT_MO3, ws=ws, stream=stream)
     out["c5_rec32_pass"] = entry(time_passes(src, dst, pv, True, ws), 64 * n5, n=n5,
                                  note="records: the standalone pass is the three-way ordered placement")
-    ms, ep, st = time_mw(dst, src, ws)
-    out["c5_pairs_8way_levels"] = entry(ms, 32 * ep, n=n5, element_passes=ep, levels=st["levels"],
-                                        note="key+index pairs (16 B) of the records sort")
+    out["c5_pairs_8way_levels"] = mw_entry(*time_mw(dst, src, ws), 16, n=n5,
+                                           note="key+index pairs (16 B) of the records sort")
     pairs = torch.empty((n5, 2), dtype=torch.int64, device=dev)
     pairs[:, 0] = src[:, 0]
     pairs[:, 1] = torch.arange(n5, dtype=torch.int64, device=dev)
