@@ -166,6 +166,9 @@ __device__ __forceinline__ void oem_sort(E (&x)[N]) {
 // run's ends in outputs that are discarded) and VW more for the 16-byte
 // alignment offset of the TMA copies.
 constexpr int LEAF_SLACK = 64;
+#ifndef BQ_LEAF_PRED_ADV
+#define BQ_LEAF_PRED_ADV 1
+#endif
 
 template <class KT, int NT>
 struct LeafSmem {
@@ -404,8 +407,18 @@ __device__ __forceinline__ void leaf_body(const LeafParams<KT> &P, const Leaf lf
                     hv = e_max(hv, nv);
                     tA = tA == keep_side;
                     if (k + 1 < IPT) {
+#if BQ_LEAF_PRED_ADV
+                        // predicated pointer advances (one add each, on the
+                        // FMA pipe) instead of both advanced values computed
+                        // and the kept ones selected (two more ALU selects)
+                        asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t"
+                            "@q add.u32 %0, %0, %3;\n\t@!q sub.u32 %1, %1, %3;\n\t}"
+                            : "+r"(pa), "+r"(pb)
+                            : "r"((uint32_t)tA), "n"((int)PL::STEP));
+#else
                         if (tA) pa += (uint32_t)PL::STEP;
                         else pb -= (uint32_t)PL::STEP;
+#endif
                         nv = pl.ldc(tA ? pa : pb);
                     }
                 }
