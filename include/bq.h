@@ -100,16 +100,18 @@ typedef struct {
 typedef struct {
     int32_t pivot_rule;   /* bq_pivot_rule for segments > leaf size; default SAMPLE64 */
     int32_t depth_limit;  /* < 0: Introsort limit 2*floor(log2 n)+3 */
-    int32_t timing;       /* != 0: host-driven level loop, CUDA events around every partition
-                             launch (bq_sort_stats.partition_ms); the call waits */
+    int32_t timing;       /* != 0: host-driven level loop, CUDA events around every binary
+                             partition launch, each multiway level's count + scan and
+                             scatter, and the leaf launches (bq_sort_stats.partition_ms,
+                             mw_count_ms, mw_scatter_ms, leaf_ms); the call waits */
     int32_t ordered;      /* != 0: ticket-ordered tile placement (decoupled look-back),
                              deterministic layout; 0: one atomicAdd per tile (faster; tiles
                              of a segment placed in completion order; records then move
                              by two-way passes).  Sorted keys are identical. */
-    int32_t ways;         /* 0 (default): binary passes for int32 keys (8-way for
-                             2^17 < n <= 2^23, 16-way up to 2^24) and 32-byte records, 8-way passes for
-                             uint64/float64 keys and key+index pairs (so also for
-                             bq_sort_records' default path); 2: binary; 8 or 16:
+    int32_t ways;         /* 0 (default): 8-way passes for int32 keys above 2^17 (16-way for
+                             2^21 < n <= 2^23; binary up to 2^17), for uint64/float64 keys
+                             and key+index pairs (so also for bq_sort_records' default
+                             path); binary for 32-byte records; 2: binary; 8 or 16:
                              multi-pivot block partition (segments whose
                              sample has duplicate splitters use the binary pass).  32-byte
                              records always use the binary pass. */
@@ -261,7 +263,7 @@ BQ_API bq_status bq_sort_records(bq_record32 *recs, size_t n, void *ws, size_t w
  * none).  Asynchronous like bq_sort_*, except that stats != NULL or
  * opt->timing != 0 makes the call wait for the stream (the statistics are
  * device counters; timing runs the level loop from the host with CUDA events
- * around every partition launch).  A leaf-list overflow (never expected: the
+ * around the partition, multiway and leaf launches).  A leaf-list overflow (never expected: the
  * lists are sized for every child of a level) is reported as BQ_ERR_CUDA only
  * when the call waits. */
 BQ_API bq_status bq_sort_ex(bq_kind kind, void *data, size_t n, const bq_sort_options *opt,
