@@ -268,6 +268,9 @@ constexpr int MAX_LEVELS = 128;   // control blocks of a sort's level loop (dept
 #endif
 constexpr uint32_t LOOP_BATCH = BQ_LOOP_BATCH;
 constexpr uint32_t LOOP_BATCH_SMALL = 2;
+// multiway sorts run their predicted number of levels as one batch (no
+// trailing empty level slots), up to this many
+constexpr uint32_t LOOP_BATCH_MAX = 6;
 constexpr size_t LOOP_SMALL_N = (size_t)1 << 22;
 
 // Per-level control block.  One per level, zeroed once per sort, so no

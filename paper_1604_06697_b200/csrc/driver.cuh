@@ -638,6 +638,21 @@ bq_status make_plan(SortPlan<KT> &pl, typename KT::T *data, size_t n, void *ws, 
     pl.ways = ways;
     pl.aligned = aligned16(pl.user) && aligned16(pl.scratch);
     pl.batch = n <= LOOP_SMALL_N ? LOOP_BATCH_SMALL : LOOP_BATCH;
+    if (mw_capable<KT>() && ways > 2 && n > LOOP_SMALL_N) {
+        // the levels a multiway sort needs if every bucket gets its share —
+        // a level splits m keys into min(ways, ceil(m / (S * fill))) buckets
+        // (mw_splitters) — plus one for the buckets the sample makes larger:
+        // one batch of that many levels leaves few empty level slots behind
+        const uint64_t S = Tune<KT>::LEAF;
+        uint64_t m = n;
+        uint32_t lv = 0;
+        while (m > S && lv < LOOP_BATCH_MAX) {
+            const uint64_t k = std::min<uint64_t>((uint64_t)ways, (m * 100 + S * BQ_MW_FILL - 1) / (S * BQ_MW_FILL));
+            m = (m + k - 1) / std::max<uint64_t>(k, 2);
+            lv++;
+        }
+        pl.batch = std::min<uint32_t>(LOOP_BATCH_MAX, std::max<uint32_t>(2u, lv + 1));
+    }
     pl.ctrl = reinterpret_cast<LevelCtrl *>(w + L.ctrl);
     pl.root = pl.ctrl + MAX_LEVELS;
     pl.misc = reinterpret_cast<LoopMisc *>(w + L.misc);
@@ -967,7 +982,7 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
             return set_error(BQ_ERR_INVALID_ARGUMENT, "ways %d not in {0, 2, %d, %d}", ways, MW8, MW_K);
         if (rule != BQ_PIVOT_MO3 && rule != BQ_PIVOT_NINTHER && rule != BQ_PIVOT_SAMPLE64)
             return set_error(BQ_ERR_INVALID_ARGUMENT, "bad pivot rule %d", rule);
-        if (depth_limit >= MAX_LEVELS - (int)LOOP_BATCH - 2)
+        if (depth_limit >= MAX_LEVELS - (int)LOOP_BATCH_MAX - 2)
             return set_error(BQ_ERR_INVALID_ARGUMENT, "depth_limit %d too large", depth_limit);
     }
     bq_status st = validate<KT>(data, n, ws, ws_bytes);
@@ -1070,7 +1085,7 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
         BQ_SKC(enqueue_prefix<KT>(pl, s));
         std::vector<LevelCtrl> hc(1);
         for (int level = 0;; level++) {
-            if (level + (int)LOOP_BATCH + 1 >= MAX_LEVELS) {
+            if (level + (int)LOOP_BATCH_MAX + 1 >= MAX_LEVELS) {
                 cleanup();
                 return set_error(BQ_ERR_CUDA, "level loop did not terminate");
             }
