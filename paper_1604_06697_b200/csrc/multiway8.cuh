@@ -106,20 +106,6 @@ __device__ __forceinline__ uint32_t mw8_bucket(const K (&tr)[MW8], K k) {
     return ((uint32_t)p0 << 2) | ((uint32_t)p1 << 1) | (uint32_t)p2;
 }
 
-// 4 x the bucket of key k (the shift of its 4-bit counter): the same three
-// compares as mw8_bucket, the level-2 candidates picked by p0 alone so that
-// the last select waits only on p1, and the result built from the predicates
-template <class K>
-__device__ __forceinline__ uint32_t mw8_b4(const K (&tr)[MW8], K k) {
-    const bool p0 = tr[1] < k;
-    const K n1 = p0 ? tr[3] : tr[2];
-    const K c1 = p0 ? tr[7] : tr[5], c0 = p0 ? tr[6] : tr[4];
-    const bool p1 = n1 < k;
-    const K n2 = p1 ? c1 : c0;
-    const bool p2 = n2 < k;
-    return (p0 ? 16u : 0u) + (p1 ? 8u : 0u) + (p2 ? 4u : 0u);
-}
-
 // base + 4 x the bucket of key k, the offset added by predicated adds (the
 // FMA pipe) instead of built from the predicates on the ALU pipe
 template <class K, uint32_t M = 1>
@@ -135,21 +121,6 @@ __device__ __forceinline__ uint32_t mw8_a4(const K (&tr)[MW8], K k, uint32_t bas
     if (p2) a += 4u * M;
     return a;
 }
-// the one-hot increment of key k's 4-bit counter (1 << 4 x bucket)
-template <class K>
-__device__ __forceinline__ uint32_t mw8_inc(const K (&tr)[MW8], K k) {
-    const bool p0 = tr[1] < k;
-    const K n1 = p0 ? tr[3] : tr[2];
-    const K c1 = p0 ? tr[7] : tr[5], c0 = p0 ? tr[6] : tr[4];
-    uint32_t inc = p0 ? 0x10000u : 1u;
-    const bool p1 = n1 < k;
-    const K n2 = p1 ? c1 : c0;
-    if (p1) inc <<= 8;
-    const bool p2 = n2 < k;
-    if (p2) inc <<= 4;
-    return inc;
-}
-
 // The classification of one key against the tile's splitters.  float64 keys
 // are compared as doubles (DSETP, the FP64 pipe) against the splitters the
 // loader decoded (mw8_tree_word): for non-NaN values the double order is the
@@ -170,15 +141,10 @@ struct Mw8Cls {
         return mw8_bucket(tr, KT::key(x));
     }
     __device__ __forceinline__ uint32_t fix(const typename KT::T &, uint32_t b) const { return b; }
-    __device__ __forceinline__ uint32_t b4(const typename KT::T &x, bool &) const { return mw8_b4(tr, KT::key(x)); }
     __device__ __forceinline__ uint32_t fix4(const typename KT::T &, uint32_t b4) const { return b4; }
-    __device__ __forceinline__ uint32_t a4(const typename KT::T &x, uint32_t base, bool &) const {
-        return mw8_a4(tr, KT::key(x), base);
-    }
     __device__ __forceinline__ uint32_t a128(const typename KT::T &x, uint32_t base, bool &) const {
         return mw8_a4<typename KT::K, 32>(tr, KT::key(x), base);
     }
-    __device__ __forceinline__ uint32_t inc(const typename KT::T &x, bool &) const { return mw8_inc(tr, KT::key(x)); }
 };
 template <>
 struct Mw8Cls<KF64> {
@@ -199,29 +165,14 @@ struct Mw8Cls<KF64> {
         const double d = __longlong_as_double((long long)x);
         return d != d ? ((x >> 63) ? 0u : MW8 - 1u) : b;
     }
-    __device__ __forceinline__ uint32_t b4(const uint64_t &x, bool &nan) const {
-        const double d = __longlong_as_double((long long)x);
-        nan |= d != d;
-        return mw8_b4(tr, d);
-    }
     __device__ __forceinline__ uint32_t fix4(const uint64_t &x, uint32_t b4) const {
         const double d = __longlong_as_double((long long)x);
         return d != d ? ((x >> 63) ? 0u : 4u * (MW8 - 1u)) : b4;
-    }
-    __device__ __forceinline__ uint32_t a4(const uint64_t &x, uint32_t base, bool &nan) const {
-        const double d = __longlong_as_double((long long)x);
-        nan |= d != d;
-        return mw8_a4(tr, d, base);
     }
     __device__ __forceinline__ uint32_t a128(const uint64_t &x, uint32_t base, bool &nan) const {
         const double d = __longlong_as_double((long long)x);
         nan |= d != d;
         return mw8_a4<double, 32>(tr, d, base);
-    }
-    __device__ __forceinline__ uint32_t inc(const uint64_t &x, bool &nan) const {
-        const double d = __longlong_as_double((long long)x);
-        nan |= d != d;
-        return mw8_inc(tr, d);
     }
 };
 
@@ -235,18 +186,6 @@ __device__ __forceinline__ void mw8_classify(const Mw8Cls<KT> &cls, const typena
     if (nan)
 #pragma unroll
         for (int c = 0; c < IPT; c++) bk[c] = cls.fix(x[c], bk[c]);
-}
-
-// 4 x the buckets of a thread's IPT keys (b4[c]), NaN fix-up included
-template <class KT, int IPT>
-__device__ __forceinline__ void mw8_classify4(const Mw8Cls<KT> &cls, const typename KT::T (&x)[IPT],
-                                              uint32_t (&b4)[IPT]) {
-    bool nan = false;
-#pragma unroll
-    for (int c = 0; c < IPT; c++) b4[c] = cls.b4(x[c], nan);
-    if (nan)
-#pragma unroll
-        for (int c = 0; c < IPT; c++) b4[c] = cls.fix4(x[c], b4[c]);
 }
 
 // 8 counters of 8 bits -> 4 words of two 16-bit counters
@@ -288,10 +227,7 @@ struct Mw8Ctr {
         c += 1u << b4;
         return r;
     }
-    __device__ __forceinline__ void add4(uint32_t b4) {
-        static_assert(NIB, "4-bit counters");
-        c += 1u << b4;
-    }
+
     // the counters as bytes: lo = buckets 0..3, hi = buckets 4..7
     __device__ __forceinline__ void bytes(uint32_t &lo, uint32_t &hi) const {
         if constexpr (NIB) {

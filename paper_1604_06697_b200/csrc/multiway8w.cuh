@@ -752,14 +752,6 @@ __global__ void __launch_bounds__(MW8W_WARPS * 32, Mw8tTune<KT>::MINB) k_mw8t_sc
     uint32_t par = 0, ph = 0, cls_seg = 0xffffffffu, seg_base = 0;
     bool stores_out = false;   // lanes 0..7: a bulk store of the stage may still read it
     Mw8Cls<KT> cls;
-#ifndef BQ_MW8T_SMT
-#define BQ_MW8T_SMT 0
-#endif
-    using CK = typename Mw8CmpT<KT>::type;
-    __shared__ Mw8Smt<KT> s_tree[MW8W_WARPS];   // (BQ_MW8T_SMT: the splitter tree in shared memory)
-    Mw8Smt<KT> &smt = s_tree[threadIdx.x >> 5];
-    const uint32_t tb = smem_u32(smt.node), lb = smem_u32(smt.leaf);
-    CK t1{};
     // global prefix of table row r, lane b < 8: bucket b (as the two words
     // it sums, loaded a unit before they are added)
     // (every lane loads, lanes >= 8 the words of bucket 7, so no branch
@@ -782,10 +774,6 @@ __global__ void __launch_bounds__(MW8W_WARPS * 32, Mw8tTune<KT>::MINB) k_mw8t_sc
         }
         if (cur.si != cls_seg) {
             mw8w_load_cls<KT>(P, cur.si, cls);
-            if (BQ_MW8T_SMT) {
-                mw8_smt_write<KT>(P, cur.si, smt, lane, [](uint32_t b) { return 128u * b; });
-                t1 = cls.tr[1];
-            }
             uint32_t tot, start, pf;
             mw8w_seg_buckets(P, cur.row0, cur.nrows, rows, lane, tot, start, pf);
             seg_base = cur.begin + start - pf;   // lane b: bucket b's output base minus its rows' prefix
@@ -842,15 +830,7 @@ __global__ void __launch_bounds__(MW8W_WARPS * 32, Mw8tTune<KT>::MINB) k_mw8t_sc
                 {
                     bool nan = false;
 #pragma unroll
-                    for (int c = 0; c < IPT; c++) {
-                        if constexpr (BQ_MW8T_SMT) {
-                            const CK k = mw8_ckey<KT>(x[c]);
-                            if constexpr (std::is_same<KT, KF64>::value) nan |= k != k;
-                            ra[c] = exrow + mw8_smt_leaf(tb, lb, t1, k);
-                        } else {
-                            ra[c] = cls.a128(x[c], exrow, nan);
-                        }
-                    }
+                    for (int c = 0; c < IPT; c++) ra[c] = cls.a128(x[c], exrow, nan);
                     if (nan)
 #pragma unroll
                         for (int c = 0; c < IPT; c++) ra[c] = exrow + 32u * cls.fix4(x[c], (ra[c] - exrow) >> 5);
