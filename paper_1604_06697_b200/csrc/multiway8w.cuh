@@ -156,6 +156,7 @@ template <class KT>
 struct Mw8Smt {
     typename Mw8CmpT<KT>::type node[MW8];   // node[j], j = 1..7 (heap order, mw_splitters)
     uint32_t leaf[MW8];                     // leaf value of bucket b
+    uint2 l2[4];                            // 4-byte keys: level-2 node 4 + i as {splitter, leaf(2 i)}
 };
 __device__ __forceinline__ int32_t lds_ck(uint32_t a, int32_t *) { return (int32_t)lds32(a); }
 __device__ __forceinline__ uint64_t lds_ck(uint32_t a, uint64_t *) {
@@ -179,8 +180,22 @@ __device__ __forceinline__ void mw8_smt_write(const MwParams<KT> &P, uint32_t si
         if constexpr (std::is_same<KT, KF64>::value) t.node[lane] = __longlong_as_double((long long)w);
         else t.node[lane] = w;
         t.leaf[lane] = leaf(lane);
+        if constexpr (sizeof(typename Mw8CmpT<KT>::type) == 4)
+            if (lane >= 4) t.l2[lane - 4] = make_uint2((uint32_t)w, leaf(2 * (lane - 4)));
     }
     __syncwarp();
+}
+// 4-byte keys, leaf values of buckets 2 i + 1 = those of 2 i << 4 (the count's
+// one-hot increments): level 2 loads its splitter and the leaf value together
+__device__ __forceinline__ uint32_t mw8_smt_inc32(uint32_t tb, uint32_t l2b, int32_t t1, int32_t k) {
+    const bool p0 = t1 < k;
+    const uint32_t a1 = p0 ? tb + 12u : tb + 8u;
+    uint32_t a2 = p0 ? l2b + 16u : l2b;
+    const int32_t n1 = (int32_t)lds32(a1);
+    if (n1 < k) a2 += 8u;
+    uint32_t n2, inc;
+    asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(n2), "=r"(inc) : "r"(a2));
+    return (int32_t)n2 < k ? inc << 4 : inc;
 }
 // the leaf value of key k: tb = the shared address of node[0], lb = of
 // leaf[0], t1 = node[1] (in a register)
@@ -221,7 +236,7 @@ __global__ void __launch_bounds__(MW8W_WARPS * 32) k_mw8w_count(const MwParams<K
     using CK = typename Mw8CmpT<KT>::type;
     __shared__ Mw8Smt<KT> s_tree[MW8W_WARPS];
     Mw8Smt<KT> &smt = s_tree[threadIdx.x >> 5];
-    const uint32_t tb = smem_u32(smt.node), lb = smem_u32(smt.leaf);
+    const uint32_t tb = smem_u32(smt.node), lb = smem_u32(smt.leaf), l2b = smem_u32(smt.l2);
     uint32_t cls_seg = 0xffffffffu;
     Mw8Cls<KT> cls;
     CK t1{};
@@ -250,7 +265,8 @@ __global__ void __launch_bounds__(MW8W_WARPS * 32) k_mw8w_count(const MwParams<K
                 for (int c = 0; c < IPT; c++) {
                     const CK k = mw8_ckey<KT>(xr[c]);
                     if constexpr (std::is_same<KT, KF64>::value) nan |= k != k;
-                    inc[c] = mw8_smt_leaf(tb, lb, t1, k);
+                    if constexpr (std::is_same<KT, KI32>::value) inc[c] = mw8_smt_inc32(tb, l2b, t1, k);
+                    else inc[c] = mw8_smt_leaf(tb, lb, t1, k);
                 }
                 if (nan)
 #pragma unroll
