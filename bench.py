@@ -440,19 +440,21 @@ def main():
     mwp = avg("multiway_element_passes")
     fams = {
         "k_part_fast": ("tile partition pass (binary levels)", avg("partition_bytes"), avg("partition_ms"),
-                        tstats[-1]["partition_launches"] if avg("partition_bytes") > 0 else 0),
+                        "HBM (0.92 of the copy bandwidth in r02 session 1)"),
         "k_mw8t_scatter": ("8-way scatter (multiway levels): read + write of every key", 8.0 * mwp,
-                           avg("mw_scatter_ms"), None),
-        "k_mw8w_count": ("8-way count + scan (multiway levels): read of every key", 4.0 * mwp, avg("mw_count_ms"), None),
-        "k_leaf": ("leaf sort (a8): read + write of every leaf key", 8.0 * N_FULL, avg("leaf_ms"), None),
+                           avg("mw_scatter_ms"), "issue: ~45 instructions per key, ALU pipe 60 % (ncu, profiles/r02)"),
+        "k_mw8w_count": ("8-way count + scan (multiway levels): read of every key", 4.0 * mwp, avg("mw_count_ms"),
+                         "issue / HBM (ncu, profiles/r02)"),
+        "k_leaf": ("leaf sort (a8): read + write of every leaf key", 8.0 * N_FULL, avg("leaf_ms"),
+                   "shared memory: 78 % of the wavefront rate, issue 55 % (ncu, profiles/r02/ncu_full_r02.md)"),
     }
     by_kernel = {}
-    for kname, (desc, nbytes, ms, _) in fams.items():
+    for kname, (desc, nbytes, ms, bound) in fams.items():
         if ms <= 0 or nbytes <= 0:
             continue
         ach = nbytes / (ms * 1e-3) / 1e9
         by_kernel[kname] = {"what": desc, "bytes_per_sort": nbytes, "ms_per_sort": ms, "achieved": ach,
-                            "frac": ach / peak, "share_of_step": ms / ms_per_step}
+                            "frac": ach / peak, "share_of_step": ms / ms_per_step, "bound_by": bound}
     # the dominant family: the largest summed kernel time in the committed ncu
     # launch list of one c2 sort (serialised, per-kernel durations); the
     # timing mode's leaf span also holds the leaf classes' launch gaps and
