@@ -39,7 +39,7 @@ constexpr int MW_K = 16;         // buckets of a multiway segment
 template <class KT>
 constexpr bool mw_capable() { return !KT::is_record || sizeof(typename KT::T) == 16; }
 #ifndef BQ_MW_FILL
-#define BQ_MW_FILL 50
+#define BQ_MW_FILL 45
 #endif
 constexpr int MW_SAMPLE = 256;   // sample keys per segment (8 per lane of one warp)
 
