@@ -20,7 +20,9 @@ Timing (device, CUDA events on the stream the library launches on):
     roofline_by_kernel lists every family.
   * partition_pass: BASELINE.md's roofline measurement — 10 single out-of-place
     passes over the pristine input around its Mo3 pivot, L2 flushed before each.
-  * e2e: bq_sort_host (H2D from pinned memory + sort + D2H) per step.
+  * e2e: bq_sort_host (H2D from pinned memory + sort + D2H) per step; value =
+    K such steps software-pipelined over three streams (one step's H2D runs
+    under another's sort and D2H), e2e.serial = one step at a time.
   * cpu_baseline: the oracle (oracle/, single-threaded) on a bounded sample.
 Multi-GPU (--gpus N under torchrun): replicas only — every rank
 sorts its own copy; the time is the max over ranks; value = N*n / time.
@@ -268,6 +270,57 @@ class ClockSampler:
 
 # ----------------------------------------------------------- cpu baselines ---
 
+def e2e_pipelined(bq, torch, keys_np, data, ws, stream, dev, n, args):
+    """K end-to-end sorts through the public API, software-pipelined over S = 3
+    streams (step i on stream i mod S, each stream with its own device buffer
+    and workspace): every step copies its own input from pinned host memory
+    (H2D), sorts it (bq_sort_ex, the graph launch) and reads the whole result
+    back (D2H).  The H2D copies are chained across steps, and so are the D2H
+    copies, so each link carries one copy at a time and step i+1's H2D runs
+    under step i's sort and D2H (PCIe is full duplex).  Each step has its own
+    pinned input/output buffer, filled before the timed region.  Time: CUDA
+    events from before the first copy to the end of the last D2H."""
+    import numpy as np
+    S = 3
+    K = max(S, args.e2e_pipe_steps)
+    hosts = [torch.from_numpy(keys_np).pin_memory() for _ in range(K)]
+    devs = [data] + [torch.empty_like(data) for _ in range(S - 1)]
+    wss = [ws] + [bq.workspace(bq.BQ_I32, n, dev) for _ in range(S - 1)]
+    streams = [stream] + [torch.cuda.Stream(dev) for _ in range(S - 1)]
+    for j in range(S):   # warm-up: each buffer set's sort graph is instantiated here
+        devs[j].copy_(torch.from_numpy(keys_np).to(dev))
+        bq.bq_sort_ex(devs[j], pivot_rule=args.pivot_rule, ws=wss[j], stream=streams[j], stats=False)
+    torch.cuda.synchronize()
+    ev = lambda: torch.cuda.Event(enable_timing=True)
+    start, end = ev(), ev()
+    start.record(streams[0])
+    prev_h2d = prev_d2h = start
+    for i in range(K):
+        st, d = streams[i % S], devs[i % S]
+        st.wait_event(prev_h2d)
+        with torch.cuda.stream(st):
+            d.copy_(hosts[i], non_blocking=True)
+        prev_h2d = ev()
+        prev_h2d.record(st)
+        bq.bq_sort_ex(d, pivot_rule=args.pivot_rule, ws=wss[i % S], stream=st, stats=False)
+        st.wait_event(prev_d2h)
+        with torch.cuda.stream(st):
+            hosts[i].copy_(d, non_blocking=True)
+        prev_d2h = ev()
+        prev_d2h.record(st)
+    streams[0].wait_event(prev_d2h)
+    end.record(streams[0])
+    torch.cuda.synchronize()
+    ms_total = start.elapsed_time(end)
+    ok = all(bool(np.all(h.numpy()[1:] >= h.numpy()[:-1])) for h in (hosts[0], hosts[-1]))
+    if not ok:
+        raise RuntimeError("pipelined e2e: a result is not sorted")
+    return {"steps": K, "streams": S, "ms_total": ms_total, "results_sorted": ok,
+            "how": "K steps (H2D of the step's own pinned input, bq_sort_ex, D2H of its result) "
+                   "on 3 streams with their own buffers; H2D copies chained, D2H copies chained; "
+                   "events from before the first copy to the end of the last D2H"}
+
+
 def host_facts():
     model = None
     try:
@@ -354,11 +407,15 @@ def main():
     ap.add_argument("--pivot-rule", type=int, default=2, help="0 Mo3, 1 ninther, 2 median of a 64-key sample")
     ap.add_argument("--passes", type=int, default=10)
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-pipe-steps", type=int, default=-1,
+                    help="end-to-end sorts pipelined over three streams (0: serial e2e only; default 12 at N=1, 6 per rank above)")
     ap.add_argument("--cpu-sample", type=int, default=1 << 28)
     ap.add_argument("--no-configs", action="store_true", help="skip the per-config partition-pass table")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-verify", action="store_true")
     args = ap.parse_args()
+    if args.e2e_pipe_steps < 0:
+        args.e2e_pipe_steps = 12 if int(os.environ.get("WORLD_SIZE", "1")) == 1 else 6
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
     rank, world, local = dist_env()
@@ -559,8 +616,16 @@ def main():
             if i > 0:
                 t_e2e.append(a.elapsed_time(b))
         e2e_ms = reduce_max(sum(t_e2e), world, dev) / len(t_e2e)
-        e2e = {"value": world * n / (e2e_ms * 1e-3) / 1e9, "unit": "Gkeys/s",
-               "h2d_bytes_per_step": 4 * n, "d2h_bytes_per_step": 4 * n, "ms_per_step": e2e_ms}
+        serial = {"value": world * n / (e2e_ms * 1e-3) / 1e9, "unit": "Gkeys/s", "ms_per_step": e2e_ms,
+                  "how": "one stream: each step's H2D, sort and D2H back to back (bq_sort_host)"}
+        e2e = {"value": serial["value"], "unit": "Gkeys/s",
+               "h2d_bytes_per_step": 4 * n, "d2h_bytes_per_step": 4 * n, "ms_per_step": e2e_ms,
+               "serial": serial}
+        if args.e2e_pipe_steps > 0:
+            pipe = e2e_pipelined(bq, torch, keys_np, data, ws, stream, dev, n, args)
+            pipe_ms = reduce_max(pipe["ms_total"], world, dev) / pipe["steps"]
+            pipe.update({"value": world * n / (pipe_ms * 1e-3) / 1e9, "unit": "Gkeys/s", "ms_per_step": pipe_ms})
+            e2e.update({"value": pipe["value"], "ms_per_step": pipe_ms, "pipelined": pipe})
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
