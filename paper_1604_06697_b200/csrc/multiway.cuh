@@ -41,7 +41,21 @@ constexpr bool mw_capable() { return !KT::is_record || sizeof(typename KT::T) ==
 #ifndef BQ_MW_FILL
 #define BQ_MW_FILL 45
 #endif
-constexpr int MW_SAMPLE = 256;   // sample keys per segment (8 per lane of one warp)
+// Splitter sample keys per segment (NS / 32 per lane of one warp): 512 for
+// int32 keys (c2: the narrower bucket spread leaves fewer leaves above half
+// the leaf size, 6.54 -> 6.49 ms), 256 for the wider kinds (512 measured
+// slower on c5).
+#ifndef BQ_MW_SAMPLE
+#define BQ_MW_SAMPLE 256
+#endif
+#ifndef BQ_MW_SAMPLE32
+#define BQ_MW_SAMPLE32 512
+#endif
+constexpr int MW_SAMPLE = BQ_MW_SAMPLE;
+template <class KT>
+constexpr int mw_ns() { return std::is_same<KT, KI32>::value ? BQ_MW_SAMPLE32 : BQ_MW_SAMPLE; }
+constexpr int mw_logs(int ns) { return ns == 256 ? 8 : ns == 512 ? 9 : 10; }
+static_assert(mw_logs(BQ_MW_SAMPLE) <= 10 && mw_logs(BQ_MW_SAMPLE32) <= 10, "sample size");
 
 template <class KT>
 struct alignas(16) MSeg {
@@ -58,46 +72,48 @@ __device__ __forceinline__ uint32_t mw_bucket(const typename KT::K *tree, typena
     return idx - MW_K;
 }
 
-// position of sample key j of MW_SAMPLE in [b, b+len): jittered strata (R19)
+// position of sample key j of NS in [b, b+len): jittered strata (R19)
+template <int NS>
 __device__ __forceinline__ uint64_t mw_sample_pos(uint32_t b, uint32_t len, uint32_t j) {
-    const uint64_t s0 = ((uint64_t)j * len) / MW_SAMPLE, s1 = ((uint64_t)(j + 1) * len) / MW_SAMPLE;
+    const uint64_t s0 = ((uint64_t)j * len) / NS, s1 = ((uint64_t)(j + 1) * len) / NS;
     const uint64_t r = splitmix64((((uint64_t)b << 32) | len) + (uint64_t)(j + 1) * 0x9E3779B97F4A7C15ull) >> 32;
     const uint64_t pos = s0 + ((r * (s1 - s0)) >> 32);
     return (uint64_t)b + (pos < len - 1 ? pos : len - 1);
 }
 
-// The 256 sample keys of [b, b+len) sorted across one warp: index i = lane + 32 r
-// is held by lane `lane` in v[r].  Bitonic network: register compare-exchanges
-// for index bits 5-7, shuffles for bits 0-4.
-template <class KT>
+// The NS sample keys of [b, b+len) sorted across one warp: index i =
+// lane + 32 r is held by lane `lane` in v[r].  Bitonic network: register
+// compare-exchanges for the index bits above 4, shuffles for bits 0-4.
+template <class KT, int NS>
 __device__ __forceinline__ void mw_sample_sorted(const typename KT::T *buf, uint32_t b, uint32_t len, uint32_t lane,
-                                                 typename KT::K (&v)[8]) {
+                                                 typename KT::K (&v)[NS / 32]) {
     using K = typename KT::K;
+    constexpr int MW_SR = NS / 32, MW_LOGS = mw_logs(NS);
 #pragma unroll
-    for (int r = 0; r < 8; r++) v[r] = load_key<KT>(buf, mw_sample_pos(b, len, lane + 32 * r));
+    for (int r = 0; r < MW_SR; r++) v[r] = load_key<KT>(buf, mw_sample_pos<NS>(b, len, lane + 32 * r));
 #pragma unroll
-    for (int m = 1; m <= 8; m++) {
+    for (int m = 1; m <= MW_LOGS; m++) {
 #pragma unroll
         for (int bb = m - 1; bb >= 0; bb--) {
             if (bb >= 5) {
                 const int rb = bb - 5;
 #pragma unroll
-                for (int r = 0; r < 8; r++) {
+                for (int r = 0; r < MW_SR; r++) {
                     if (r & (1 << rb)) continue;
                     const int r2 = r | (1 << rb);
                     // direction of index bit m (a register bit for m >= 5, a lane bit below)
-                    const bool asc = m == 8 || (m >= 5 ? ((r >> (m - 5)) & 1) == 0 : ((lane >> m) & 1) == 0);
+                    const bool asc = m == MW_LOGS || (m >= 5 ? ((r >> (m - 5)) & 1) == 0 : ((lane >> m) & 1) == 0);
                     const K lo = v[r2] < v[r] ? v[r2] : v[r], hi = v[r2] < v[r] ? v[r] : v[r2];
                     v[r] = asc ? lo : hi;
                     v[r2] = asc ? hi : lo;
                 }
             } else {
 #pragma unroll
-                for (int r = 0; r < 8; r++) {
+                for (int r = 0; r < MW_SR; r++) {
                     const uint32_t i = lane + 32 * r;
                     const K p = __shfl_xor_sync(0xffffffffu, v[r], 1 << bb);
                     const bool lower = ((lane >> bb) & 1) == 0;
-                    const bool asc = m == 8 || ((i >> m) & 1) == 0;
+                    const bool asc = m == MW_LOGS || ((i >> m) & 1) == 0;
                     v[r] = (lower == asc) ? (p < v[r] ? p : v[r]) : (v[r] < p ? p : v[r]);
                 }
             }
@@ -106,11 +122,11 @@ __device__ __forceinline__ void mw_sample_sorted(const typename KT::T *buf, uint
 }
 
 // sorted[q] of a warp-sorted sample, for a per-lane q (all lanes participate)
-template <class K>
-__device__ __forceinline__ K mw_pick(const K (&v)[8], uint32_t q) {
+template <class K, int SR>
+__device__ __forceinline__ K mw_pick(const K (&v)[SR], uint32_t q) {
     K out = v[0];
 #pragma unroll
-    for (int r = 0; r < 8; r++) {
+    for (int r = 0; r < SR; r++) {
         const K t = __shfl_sync(0xffffffffu, v[r], q & 31);
         out = (q >> 5) == (uint32_t)r ? t : out;
     }
@@ -120,7 +136,7 @@ __device__ __forceinline__ K mw_pick(const K (&v)[8], uint32_t q) {
 // Splitters for a segment of len keys (called by a whole warp).  Returns true
 // (and the search tree, in lanes 1..15 for node = lane) when the segment is to
 // be split multiway: k_eff = min(16, max(2, ceil(2 len / S))) buckets, real
-// splitters at sample quantiles 256 i / k_eff, pairwise distinct and below the
+// splitters at sample quantiles NS i / k_eff, pairwise distinct and below the
 // sample maximum; the tree's unused slots repeat the last real splitter
 // (empty buckets).  Otherwise returns false and `pivot` = the sample's lower
 // median, for the binary three-way partition.
@@ -128,16 +144,17 @@ template <class KT>
 __device__ bool mw_splitters(const typename KT::T *buf, uint32_t b, uint32_t len, uint32_t leaf_max, uint32_t lane,
                              typename KT::K &node_val, typename KT::K &pivot, uint32_t kmax = MW_K) {
     using K = typename KT::K;
-    K v[8];
-    mw_sample_sorted<KT>(buf, b, len, lane, v);
+    constexpr int NS = mw_ns<KT>();
+    K v[NS / 32];
+    mw_sample_sorted<KT, NS>(buf, b, len, lane, v);
     const uint64_t fl = (uint64_t)leaf_max * BQ_MW_FILL;   // buckets of about BQ_MW_FILL % of S
     uint64_t ke = ((uint64_t)len * 100 + fl - 1) / fl;
     const uint32_t keff = (uint32_t)(ke < 2 ? 2 : (ke > kmax ? kmax : ke));
     // lane i (1 <= i < keff) holds real splitter s_i; lanes i >= keff repeat s_{keff-1}
     const uint32_t i = lane < 1 ? 1 : (lane < keff ? lane : keff - 1);
-    const K s = mw_pick(v, (i * MW_SAMPLE) / keff);
-    const K smax = __shfl_sync(0xffffffffu, v[7], 31);
-    pivot = mw_pick(v, MW_SAMPLE / 2 - 1);
+    const K s = mw_pick(v, (i * NS) / keff);
+    const K smax = __shfl_sync(0xffffffffu, v[NS / 32 - 1], 31);
+    pivot = mw_pick(v, NS / 2 - 1);
     const K s_next = __shfl_down_sync(0xffffffffu, s, 1);
     const bool bad = (lane >= 1 && lane + 1 < keff && !(s < s_next)) || (lane == keff - 1 && !(s < smax));
     const bool ok = __ballot_sync(0xffffffffu, bad) == 0;
