@@ -12,5 +12,5 @@ for c in c3 c5; do
   ncu --metrics $M --clock-control none --csv --log-file gpurun_out/launches_${c}_final.csv python tools/one_sort.py $c > gpurun_out/n_$c.log 2>&1; echo NCU_$c $?
 done
 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:'k_mw8t_scatter|k_mw8w_count' -s 0 -c 2 -o gpurun_out/final_mw8i python tools/prof_pass.py --passes 0 --sort 1 --fast 1 > gpurun_out/n7.log 2>&1; echo MW8I $?
-ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:'k_leaf.*KI32.*512' -s 2 -c 1 -o gpurun_out/final_leaf python tools/prof_pass.py --passes 0 --sort 1 --fast 1 > gpurun_out/n8.log 2>&1; echo LEAF $?
+ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:'k_leaf.*KI32.*512' -s 1 -c 1 -o gpurun_out/final_leaf python tools/prof_pass.py --passes 0 --sort 1 --fast 1 > gpurun_out/n8.log 2>&1; echo LEAF $?
 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:'k_mw8t_scatter|k_mw8w_count' -s 0 -c 2 -o gpurun_out/final_mw8w python tools/one_sort.py c3 > gpurun_out/n9.log 2>&1; echo MW8W $?

@@ -64,7 +64,7 @@ for c, what in (("c3", "2^27 float64"), ("c5", "2^26 32-byte records (key+index 
         "|---|---:|---:|---:|---:|\n" + big + "\n")
 parts = []
 for rep, title, k in (("final_mw8i", "k_mw8w_count / k_mw8t_scatter<KI32> (level 0 of the c2 sort)", None),
-                      ("final_leaf", "k_leaf<KI32, 1024> (c2)", None),
+                      ("final_leaf", "k_leaf<KI32, 512> (c2, the largest leaf launch)", None),
                       ("final_mw8w", "k_mw8w_count / k_mw8t_scatter<KF64> (level 0 of the c3 sort)", None)):
     path = os.path.join(G, rep + ".ncu-rep")
     parts.append(f"## {title}\n\n```\n{run('tools/ncu_brief.py', path)}```\n")
