@@ -622,10 +622,19 @@ def main():
                "h2d_bytes_per_step": 4 * n, "d2h_bytes_per_step": 4 * n, "ms_per_step": e2e_ms,
                "serial": serial}
         if args.e2e_pipe_steps > 0:
-            pipe = e2e_pipelined(bq, torch, keys_np, data, ws, stream, dev, n, args)
-            pipe_ms = reduce_max(pipe["ms_total"], world, dev) / pipe["steps"]
-            pipe.update({"value": world * n / (pipe_ms * 1e-3) / 1e9, "unit": "Gkeys/s", "ms_per_step": pipe_ms})
-            e2e.update({"value": pipe["value"], "ms_per_step": pipe_ms, "pipelined": pipe})
+            try:
+                pipe = e2e_pipelined(bq, torch, keys_np, data, ws, stream, dev, n, args)
+                pipe_ms = pipe["ms_total"] / pipe["steps"]
+            except (RuntimeError, MemoryError) as ex:   # e.g. pinned host memory exhausted
+                pipe, pipe_ms = {"error": str(ex)[:200]}, float("inf")
+            # (every rank reaches the reduction, a failed one with inf)
+            pipe_ms = reduce_max(pipe_ms, world, dev)
+            if "error" not in pipe and math.isfinite(pipe_ms):
+                pipe.update({"value": world * n / (pipe_ms * 1e-3) / 1e9, "unit": "Gkeys/s",
+                             "ms_per_step": pipe_ms})
+                e2e.update({"value": pipe["value"], "ms_per_step": pipe_ms, "pipelined": pipe})
+            else:
+                e2e["pipelined"] = pipe
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
