@@ -63,10 +63,33 @@ struct Layout {
     size_t max_tiles, max_segs, max_leaves, max_fb;
 };
 
+// The largest segment a sort of n keys hands to the leaf sort: S for large
+// inputs; smaller for small ones, whose few S-sized leaves would leave most
+// SMs idle (c1: 64 leaves of ~16 K keys on 148 SMs) — one more 8-way level
+// over an L2-resident input costs less than the long leaves it removes.
+// A multiple of the leaf classes' sizes, a function of (kind, n) only, so
+// bq_workspace_bytes stays one; BQ_LEAF_MAX overrides it (tools/leaf_sweep.py).
+template <class KT>
+inline uint32_t leaf_max_for(size_t n) {
+    constexpr uint32_t S = Tune<KT>::LEAF, C1 = (uint32_t)LeafTraits<KT>::IPT * 64u;
+    uint32_t lm = S;
+    if (const char *e = std::getenv("BQ_LEAF_MAX")) {
+        const long v = std::atol(e);
+        if (v > 0) lm = (uint32_t)std::min<long>(std::max<long>(v, C1), S);
+    }
+    (void)n;
+    return lm;
+}
+inline int batch_extra() {
+    if (const char *e = std::getenv("BQ_BATCH_EXTRA")) return std::atoi(e);
+    return 1;
+}
+
 template <class KT>
 Layout<KT> make_layout(size_t n) {
     constexpr size_t TILE = tile_elems<KT>();
-    constexpr size_t S = Tune<KT>::LEAF;
+    constexpr size_t S0 = Tune<KT>::LEAF;
+    const size_t S = leaf_max_for<KT>(n);   // segments of a level are longer than this
     Layout<KT> L;
     // segments of a level are disjoint and longer than S, or (the duplicate
     // check, keys) at least BQ_DC_MIN long
@@ -78,7 +101,7 @@ Layout<KT> make_layout(size_t n) {
     // segment; set 0's class-0 list also holds the fallback's chunks at the end
     const size_t per_level = (mw_capable<KT>() ? MW_K * (n / (S + 1) + 2) : 0) + 2 * L.max_segs;
     L.max_leaves = per_level;
-    if (L.max_leaves < n / S + L.max_fb + 2) L.max_leaves = n / S + L.max_fb + 2;
+    if (L.max_leaves < n / S0 + L.max_fb + 2) L.max_leaves = n / S0 + L.max_fb + 2;
     size_t off = 0;
     auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + bytes, 256); return o; };
     L.scratch = take(n * sizeof(typename KT::T));
@@ -614,6 +637,7 @@ struct SortPlan {
     uint32_t *tprefix;
     FbState *fbst;
     int rule, depth_limit, ordered, ways, aligned;
+    uint32_t leaf_max;    // leaf_max_for(n)
     uint32_t batch;       // levels per loop iteration
     PostParams<KT> Q;     // k_post / k_fill / k_post_mw of a level (dynamic)
     PassParams<KT> P;     // the binary partition of a level (dynamic)
@@ -637,13 +661,15 @@ bq_status make_plan(SortPlan<KT> &pl, typename KT::T *data, size_t n, void *ws, 
     pl.ordered = ordered;
     pl.ways = ways;
     pl.aligned = aligned16(pl.user) && aligned16(pl.scratch);
+    const uint32_t lm = leaf_max_for<KT>(n);
+    pl.leaf_max = lm;
     pl.batch = n <= LOOP_SMALL_N ? LOOP_BATCH_SMALL : LOOP_BATCH;
-    if (mw_capable<KT>() && ways > 2 && n > LOOP_SMALL_N) {
+    if (mw_capable<KT>() && ways > 2 && (n > LOOP_SMALL_N || lm < S)) {
         // the levels a multiway sort needs if every bucket gets its share —
         // a level splits m keys into min(ways, ceil(m / (S * fill))) buckets
         // (mw_splitters) — plus one for the buckets the sample makes larger:
         // one batch of that many levels leaves few empty level slots behind
-        const uint64_t S = Tune<KT>::LEAF;
+        const uint64_t S = lm;
         uint64_t m = n;
         uint32_t lv = 0;
         while (m > S && lv < LOOP_BATCH_MAX) {
@@ -651,7 +677,7 @@ bq_status make_plan(SortPlan<KT> &pl, typename KT::T *data, size_t n, void *ws, 
             m = (m + k - 1) / std::max<uint64_t>(k, 2);
             lv++;
         }
-        pl.batch = std::min<uint32_t>(LOOP_BATCH_MAX, std::max<uint32_t>(2u, lv + 1));
+        pl.batch = std::min<uint32_t>(LOOP_BATCH_MAX, std::max<uint32_t>(2u, lv + (n > LOOP_SMALL_N ? 1 : batch_extra())));
     }
     pl.ctrl = reinterpret_cast<LevelCtrl *>(w + L.ctrl);
     pl.root = pl.ctrl + MAX_LEVELS;
@@ -727,7 +753,7 @@ bq_status make_plan(SortPlan<KT> &pl, typename KT::T *data, size_t n, void *ws, 
     Q.leaf_cap = (uint32_t)L.max_leaves;
     Q.fallback = pl.fallback;
     Q.fallback_count = &pl.misc->fb_count;
-    Q.leaf_max = S;
+    Q.leaf_max = lm;
     Q.depth_limit = depth_limit;
     Q.pivot_rule = rule;
     Q.ways = ways;
@@ -807,14 +833,26 @@ bq_status enqueue_level_end(const SortPlan<KT> &pl, cudaStream_t s, int use_cond
 // sort the previous level's leaves (set (level + 1) & 1; one persistent
 // launch per class), copy its finished equal-record runs, empty the set
 template <class KT>
-bq_status enqueue_flush(const SortPlan<KT> &pl, cudaStream_t s, cudaEvent_t l0 = nullptr, cudaEvent_t l1 = nullptr) {
+bq_status enqueue_flush(const SortPlan<KT> &pl, cudaStream_t s, cudaEvent_t l0 = nullptr, cudaEvent_t l1 = nullptr,
+                        cudaStream_t *aux = nullptr, cudaEvent_t *aev = nullptr) {
     if (l0) BQ_CK(cudaEventRecord(l0, s));   // timing: around the leaf launches
+    // graph capture (aux, aev given): class c > 0 on its own branch aux[c - 1]
+    // (fork aev[0], joins aev[c]) — the classes' lists are disjoint, and a
+    // small sort's few large leaves of two classes then run side by side
+    if (aux && std::getenv("BQ_LEAF_SERIAL")) aux = nullptr;   // A/B switch (tools/gpu_var.sh)
+    if (aux) BQ_CK(cudaEventRecord(aev[0], s));
     for (int c = 0; c < leaf_nclass<KT>(); c++) {
         LeafParams<KT> LP = pl.LP;
         LP.lcls = (size_t)c * pl.L.max_leaves;
         LP.cls = c;
-        bq_status st = launch_leaves<KT>(c, LP, 0, s);
+        cudaStream_t sc = (aux && c > 0) ? aux[c - 1] : s;
+        if (aux && c > 0) BQ_CK(cudaStreamWaitEvent(sc, aev[0], 0));
+        bq_status st = launch_leaves<KT>(c, LP, 0, sc);
         if (st != BQ_OK) return st;
+        if (aux && c > 0) {
+            BQ_CK(cudaEventRecord(aev[c], sc));
+            BQ_CK(cudaStreamWaitEvent(s, aev[c], 0));
+        }
     }
     if (l1) BQ_CK(cudaEventRecord(l1, s));
     if (KT::is_record && !pl.ordered) {
@@ -861,11 +899,12 @@ bq_status enqueue_fb_finish(const SortPlan<KT> &pl, cudaStream_t s) {
 // ---- the graph of a sort, cached per (device, kind, buffers, n, options) --------
 struct GraphKey {
     int dev, kind, rule, depth_limit, ordered, ways;
+    uint32_t leaf_max, batch;
     const void *data, *ws;
     size_t n, ws_bytes;
     bool operator==(const GraphKey &o) const {
         return dev == o.dev && kind == o.kind && rule == o.rule && depth_limit == o.depth_limit &&
-               ordered == o.ordered && ways == o.ways && data == o.data && ws == o.ws && n == o.n &&
+               ordered == o.ordered && ways == o.ways && leaf_max == o.leaf_max && batch == o.batch && data == o.data && ws == o.ws && n == o.n &&
                ws_bytes == o.ws_bytes;
     }
 };
@@ -898,12 +937,17 @@ inline cudaError_t add_cond_node(cudaStream_t s, cudaGraphConditionalHandle h, c
 // WHILE(passes) merge; finish }.  Captured on private streams, instantiated once.
 template <class KT>
 bq_status build_sort_graph(const SortPlan<KT> &pl, cudaGraphExec_t *ex) {
+    constexpr int NC = leaf_nclass<KT>();
     cudaStream_t cs[5] = {};
     cudaEvent_t ev[2] = {};
+    cudaStream_t aux[2][MAX_LEAF_CLASSES] = {};   // leaf-class branches of the two flushes
+    cudaEvent_t aev[2][MAX_LEAF_CLASSES + 1] = {};
     cudaGraph_t g = nullptr;
     auto fail = [&](bq_status e) {
         for (auto &x : cs) if (x) cudaStreamDestroy(x);
         for (auto &x : ev) if (x) cudaEventDestroy(x);
+        for (auto &r : aux) for (auto &x : r) if (x) cudaStreamDestroy(x);
+        for (auto &r : aev) for (auto &x : r) if (x) cudaEventDestroy(x);
         if (g) cudaGraphDestroy(g);
         return e;
     };
@@ -921,6 +965,8 @@ bq_status build_sort_graph(const SortPlan<KT> &pl, cudaGraphExec_t *ex) {
     } while (0)
     for (auto &x : cs) BQ_GK(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
     for (auto &x : ev) BQ_GK(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+    for (auto &r : aux) for (int c = 0; c + 1 < NC; c++) BQ_GK(cudaStreamCreateWithFlags(&r[c], cudaStreamNonBlocking));
+    for (auto &r : aev) for (int c = 0; c < NC; c++) BQ_GK(cudaEventCreateWithFlags(&r[c], cudaEventDisableTiming));
     BQ_GK(cudaGraphCreate(&g, 0));
     cudaGraphConditionalHandle h_loop, h_fbany;
     BQ_GK(cudaGraphConditionalHandleCreate(&h_loop, g, 1, cudaGraphCondAssignDefault));
@@ -933,7 +979,7 @@ bq_status build_sort_graph(const SortPlan<KT> &pl, cudaGraphExec_t *ex) {
     BQ_GK(cudaStreamBeginCaptureToGraph(cs[1], body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
     BQ_GK(cudaEventRecord(ev[0], cs[1]));
     BQ_GK(cudaStreamWaitEvent(cs[2], ev[0], 0));          // fork
-    BQ_GS(enqueue_flush<KT>(pl, cs[2]));                    // the previous batch's leaves
+    BQ_GS(enqueue_flush<KT>(pl, cs[2], nullptr, nullptr, aux[0], aev[0]));   // the previous batch's leaves
     for (uint32_t k = 0; k < pl.batch; k++) {
         BQ_GS(enqueue_level<KT>(pl, cs[1], 1, h_loop, h_fbany, nullptr, nullptr));
         if (k + 1 < pl.batch) BQ_GS(enqueue_level_end<KT>(pl, cs[1], 1, h_loop, h_fbany));
@@ -942,7 +988,7 @@ bq_status build_sort_graph(const SortPlan<KT> &pl, cudaGraphExec_t *ex) {
     BQ_GK(cudaStreamWaitEvent(cs[1], ev[1], 0));          // join
     BQ_GS(enqueue_level_end<KT>(pl, cs[1], 1, h_loop, h_fbany));
     BQ_GK(cudaStreamEndCapture(cs[1], &tmp));
-    BQ_GS(enqueue_flush<KT>(pl, cs[0]));                    // the last level's leaves
+    BQ_GS(enqueue_flush<KT>(pl, cs[0], nullptr, nullptr, aux[1], aev[1]));   // the last level's leaves
     // the depth-capped segments (a9)
     BQ_GK(add_cond_node(cs[0], h_fbany, cudaGraphCondTypeIf, &fbbody));
     BQ_GK(cudaStreamBeginCaptureToGraph(cs[3], fbbody, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
@@ -1068,7 +1114,7 @@ bq_status run_sort(typename KT::T *data, size_t n, const bq_sort_options *opt, b
     if (!host_loop) {
         int dev = 0;
         BQ_CK(cudaGetDevice(&dev));
-        const GraphKey key{dev, (int)KT::kind, rule, depth_limit, ordered, ways, data, ws, n, ws_bytes};
+        const GraphKey key{dev, (int)KT::kind, rule, depth_limit, ordered, ways, pl.leaf_max, pl.batch, data, ws, n, ws_bytes};
         cudaGraphExec_t ex = nullptr;
         if (!graph_cache_get(key, &ex)) {
             st = build_sort_graph<KT>(pl, &ex);
