@@ -839,7 +839,9 @@ bq_status enqueue_flush(const SortPlan<KT> &pl, cudaStream_t s, cudaEvent_t l0 =
     // graph capture (aux, aev given): class c > 0 on its own branch aux[c - 1]
     // (fork aev[0], joins aev[c]) — the classes' lists are disjoint, and a
     // small sort's few large leaves of two classes then run side by side
-    if (aux && std::getenv("BQ_LEAF_SERIAL")) aux = nullptr;   // A/B switch (tools/gpu_var.sh)
+    // (keys only: the records' and pairs' classes measured 2 % slower side by
+    // side, c5 8.73 -> 8.9 ms; BQ_LEAF_SERIAL is the A/B switch of tools/gpu_var.sh)
+    if (KT::is_record || std::getenv("BQ_LEAF_SERIAL")) aux = nullptr;
     if (aux) BQ_CK(cudaEventRecord(aev[0], s));
     for (int c = 0; c < leaf_nclass<KT>(); c++) {
         LeafParams<KT> LP = pl.LP;
