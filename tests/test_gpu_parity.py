@@ -689,3 +689,24 @@ def test_duplicate_check_at_leaf_boundary(B, kind):
     st = B.bq_sort_ex(t, ways=2)
     check_sorted_equal(kind, to_host(t, a), a)
     assert st["band_elements"] >= n // 2
+
+
+@pytest.mark.parametrize("kind", ["i32", "f64", "rec32"])
+@pytest.mark.parametrize("div", [16, 4])
+def test_leaf_max_override(B, kind, div, monkeypatch):
+    """driver.cuh's leaf_max_for: a plan with a smaller leaf bound (the
+    BQ_LEAF_MAX override tools/leaf_sweep.py uses) sizes its own workspace,
+    runs more levels, and sorts to the oracle's output; dups exercise the
+    equal bands and the binary segments under the smaller bound."""
+    lm = LEAF[kind] // div
+    for dist in ("random", "dups"):
+        a = make(kind, 40 * LEAF[kind] + 13, seed=17, dist=dist)
+        base = B.bq_sort_ex(to_dev(a))
+        monkeypatch.setenv("BQ_LEAF_MAX", str(lm))
+        t = to_dev(a)
+        st = B.bq_sort_ex(t)
+        monkeypatch.delenv("BQ_LEAF_MAX")
+        check_sorted_equal(kind, to_host(t, a), a)
+        assert st["fallback_segments"] == 0
+        if dist == "random":
+            assert st["leaves"] > base["leaves"]
