@@ -804,8 +804,20 @@ bq_status enqueue_prefix(const SortPlan<KT> &pl, cudaStream_t s) {
 template <class KT>
 bq_status enqueue_level(const SortPlan<KT> &pl, cudaStream_t s, int use_cond, cudaGraphConditionalHandle h_loop,
                         cudaGraphConditionalHandle h_fb, cudaEvent_t ev0, cudaEvent_t ev1, cudaEvent_t mev0 = nullptr,
-                        cudaEvent_t mev1 = nullptr, cudaEvent_t mmid = nullptr) {
+                        cudaEvent_t mev1 = nullptr, cudaEvent_t mmid = nullptr, cudaStream_t sb = nullptr,
+                        cudaEvent_t *fj = nullptr) {
+    // graph capture of a multiway sort of keys (sb, fj given): the binary
+    // chain (pass, k_post, k_fill) is a branch beside the multiway chain —
+    // the two work on disjoint segments and append children, leaves and
+    // counts with atomics only, so a level's critical path is the longer
+    // chain, not their sum (mostly empty launches on one side)
+    cudaStream_t s2 = s;
     if constexpr (mw_capable<KT>()) if (pl.ways > 2) {
+        if (sb && !KT::is_record && !std::getenv("BQ_CHAIN_SERIAL")) {
+            s2 = sb;
+            BQ_CK(cudaEventRecord(fj[0], s));
+            BQ_CK(cudaStreamWaitEvent(s2, fj[0], 0));
+        }
         MwParams<KT> MP = pl.MP;
         if (mev0) BQ_CK(cudaEventRecord(mev0, s));
         bq_status st = launch_multiway<KT>(MP, nullptr, s, pl.ways, mmid);
@@ -814,13 +826,19 @@ bq_status enqueue_level(const SortPlan<KT> &pl, cudaStream_t s, int use_cond, cu
         k_post_mw<KT, POST_THREADS><<<POST_GRID, POST_THREADS, 0, s>>>(pl.Q);
         BQ_CK_LAUNCH();
     }
-    if (ev0) BQ_CK(cudaEventRecord(ev0, s));
-    bq_status st = launch_partition<KT>(pl.P, s);
+    if (ev0) BQ_CK(cudaEventRecord(ev0, s2));
+    bq_status st = launch_partition<KT>(pl.P, s2);
     if (st != BQ_OK) return st;
-    if (ev1) BQ_CK(cudaEventRecord(ev1, s));
-    k_post<KT, POST_LEVEL_THREADS><<<POST_LEVEL_GRID, POST_LEVEL_THREADS, 0, s>>>(pl.Q);
+    if (ev1) BQ_CK(cudaEventRecord(ev1, s2));
+    k_post<KT, POST_LEVEL_THREADS><<<POST_LEVEL_GRID, POST_LEVEL_THREADS, 0, s2>>>(pl.Q);
     BQ_CK_LAUNCH();
-    return launch_fill<KT>(pl.Q, s);   // exits at once unless a band was too long for k_post
+    st = launch_fill<KT>(pl.Q, s2);   // exits at once unless a band was too long for k_post
+    if (st != BQ_OK) return st;
+    if (s2 != s) {
+        BQ_CK(cudaEventRecord(fj[1], s2));
+        BQ_CK(cudaStreamWaitEvent(s, fj[1], 0));
+    }
+    return BQ_OK;
 }
 template <class KT>
 bq_status enqueue_level_end(const SortPlan<KT> &pl, cudaStream_t s, int use_cond, cudaGraphConditionalHandle h_loop,
@@ -940,8 +958,8 @@ inline cudaError_t add_cond_node(cudaStream_t s, cudaGraphConditionalHandle h, c
 template <class KT>
 bq_status build_sort_graph(const SortPlan<KT> &pl, cudaGraphExec_t *ex) {
     constexpr int NC = leaf_nclass<KT>();
-    cudaStream_t cs[5] = {};
-    cudaEvent_t ev[2] = {};
+    cudaStream_t cs[6] = {};
+    cudaEvent_t ev[2 + 2 * LOOP_BATCH_MAX] = {};   // [2 + 2k], [3 + 2k]: level slot k's chain fork and join
     cudaStream_t aux[2][MAX_LEAF_CLASSES] = {};   // leaf-class branches of the two flushes
     cudaEvent_t aev[2][MAX_LEAF_CLASSES + 1] = {};
     cudaGraph_t g = nullptr;
@@ -983,7 +1001,8 @@ bq_status build_sort_graph(const SortPlan<KT> &pl, cudaGraphExec_t *ex) {
     BQ_GK(cudaStreamWaitEvent(cs[2], ev[0], 0));          // fork
     BQ_GS(enqueue_flush<KT>(pl, cs[2], nullptr, nullptr, aux[0], aev[0]));   // the previous batch's leaves
     for (uint32_t k = 0; k < pl.batch; k++) {
-        BQ_GS(enqueue_level<KT>(pl, cs[1], 1, h_loop, h_fbany, nullptr, nullptr));
+        BQ_GS(enqueue_level<KT>(pl, cs[1], 1, h_loop, h_fbany, nullptr, nullptr, nullptr, nullptr, nullptr, cs[5],
+                                &ev[2 + 2 * k]));
         if (k + 1 < pl.batch) BQ_GS(enqueue_level_end<KT>(pl, cs[1], 1, h_loop, h_fbany));
     }
     BQ_GK(cudaEventRecord(ev[1], cs[2]));
