@@ -144,3 +144,29 @@ def test_binding_refuses_ambiguous_int64():
     assert bq.kind_of(torch.zeros(4, dtype=torch.float64)) == bq.BQ_F64
     assert bq.kind_of(torch.zeros((4, 4), dtype=torch.int64)) == bq.BQ_REC32
     assert bq.kind_of(torch.zeros((4, 2), dtype=torch.int64)) == bq.BQ_KEYIDX16
+
+
+def test_workspace_follows_the_leaf_bound(lib, monkeypatch):
+    """driver.cuh leaf_max_for: the plan's leaf bound sizes the workspace (more
+    segments and leaves under a smaller bound); the BQ_LEAF_MAX override is
+    clamped to [2 warps' keys, S] and a malformed value leaves the default."""
+    so, _ = lib
+    so.bq_workspace_bytes.restype = ctypes.c_size_t
+    so.bq_workspace_bytes.argtypes = [ctypes.c_int, ctypes.c_size_t]
+    so.bq_leaf_elems.restype = ctypes.c_size_t
+    so.bq_leaf_elems.argtypes = [ctypes.c_int]
+    n = 1 << 24
+    for kind in (0, 1, 2):
+        S = so.bq_leaf_elems(kind)
+        monkeypatch.delenv("BQ_LEAF_MAX", raising=False)
+        base = so.bq_workspace_bytes(kind, n)
+        monkeypatch.setenv("BQ_LEAF_MAX", str(S // 8))
+        small = so.bq_workspace_bytes(kind, n)
+        monkeypatch.setenv("BQ_LEAF_MAX", "1")            # clamped up to IPT * 64
+        tiny = so.bq_workspace_bytes(kind, n)
+        monkeypatch.setenv("BQ_LEAF_MAX", str(S // 16))   # = IPT * 64
+        assert so.bq_workspace_bytes(kind, n) == tiny
+        assert base < small < tiny
+        for bad in ("0", "-5", "abc", str(10 * S)):       # ignored / clamped down to S
+            monkeypatch.setenv("BQ_LEAF_MAX", bad)
+            assert so.bq_workspace_bytes(kind, n) == base
