@@ -955,6 +955,8 @@ inline cudaError_t add_cond_node(cudaStream_t s, cudaGraphConditionalHandle h, c
 // the previous batch's leaves] || [partition LOOP_BATCH levels]; join };
 // sort the last level's leaves; IF(capped segments) { setup; chunk leaves;
 // WHILE(passes) merge; finish }.  Captured on private streams, instantiated once.
+// Key sorts: a flush's leaf classes and a level's binary / multiway chains
+// are parallel branches (enqueue_flush, enqueue_level).
 template <class KT>
 bq_status build_sort_graph(const SortPlan<KT> &pl, cudaGraphExec_t *ex) {
     constexpr int NC = leaf_nclass<KT>();
