@@ -154,7 +154,11 @@ typedef struct {
  * least bq_inplace_workspace_bytes(kind, n)).  For
  * BQ_REC32 it also covers the key+index sort path: 16n bytes of pairs, the
  * pair sort's own workspace (16n scratch + O(n/T)) and a 32n-byte copy of the
- * records that the final gather reads (about 65n). */
+ * records that the final gather reads (about 65n).  A pure function of
+ * (kind, n) — unless the tuning override BQ_LEAF_MAX (environment; a smaller
+ * leaf bound than bq_leaf_elems(kind), used by tools/leaf_sweep.py and the
+ * tests) is set, which must then hold the same value for this call and the
+ * sort that uses the workspace (a sort checks ws_bytes against it). */
 BQ_API size_t bq_workspace_bytes(bq_kind kind, size_t n);
 
 /* ---- pivot selection (hot-path step a1) -------------------------------------
