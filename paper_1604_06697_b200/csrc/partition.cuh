@@ -452,6 +452,17 @@ __device__ __forceinline__ void emit_children(const PostParams<KT> &Q, int nch, 
 template <class KT, int NT>
 __device__ __forceinline__ void post_segment(const PostParams<KT> &Q, uint32_t si);
 
+// A key segment made of copies of its pivot only (L = G = 0) whose source is
+// the final buffer already is its own equal band: nothing to write (the key
+// codecs are bijections on bit patterns, so equal keys are equal bits).
+// The all-equal input of c4 and the single-value segments that end a
+// few-distinct-values sort take this exit.
+template <class KT>
+__device__ __forceinline__ bool band_in_place(const PassParams<KT> &P, const Seg &sg, uint32_t L, uint32_t G) {
+    if (KT::is_record) return false;
+    return L == 0 && G == 0 && (sg.parity ? P.bufs[1] : P.bufs[0]) == P.final_buf;
+}
+
 template <class KT, int NT>
 __global__ void __launch_bounds__(NT) k_post(const PostParams<KT> Qin) {
     if (const LevelCtrl *pv = loop_prev_ctrl(Qin.pass.lp)) if (pv->nseg_next == 0) return;
@@ -475,7 +486,8 @@ __device__ __forceinline__ void post_segment(const PostParams<KT> &Q, uint32_t s
     const uint64_t b = sg.begin;
     LevelCtrl *C = P.ctrl;
 
-    if (E > 0 && E <= Q.band_inline_max) {
+    const bool inplace = band_in_place<KT>(P, sg, L, G);
+    if (E > 0 && E <= Q.band_inline_max && !inplace) {
         const uint64_t band0 = b + L;
         if constexpr (KT::is_record) {
             // staged equal records: stage[parity][b + j], j < E
@@ -499,7 +511,7 @@ __device__ __forceinline__ void post_segment(const PostParams<KT> &Q, uint32_t s
             for (uint32_t j = threadIdx.x; j < E; j += NT) P.final_buf[band0 + j] = pv;
         }
     }
-    if (threadIdx.x == 0 && E > Q.band_inline_max && Q.emit_children) atomicAdd(&C->nbig, 1u);
+    if (threadIdx.x == 0 && E > Q.band_inline_max && Q.emit_children && !inplace) atomicAdd(&C->nbig, 1u);
     if (threadIdx.x == 0 && Q.d_counts) {
         Q.d_counts[3 * si + 0] = L;
         Q.d_counts[3 * si + 1] = E;
@@ -548,7 +560,7 @@ __global__ void __launch_bounds__(NT) k_fill(const PostParams<KT> Qin, int phase
         const uint32_t si = P.tile_map ? P.tile_map[t] : 0;
         const Seg sg = P.segs ? P.segs[si] : P.seg0;
         const SegCounts<KT> cn = seg_counts(P, si, sg);
-        if (cn.E <= Q.band_inline_max) continue;
+        if (cn.E <= Q.band_inline_max || band_in_place<KT>(P, sg, cn.L, cn.G)) continue;
         const uint64_t b = sg.begin;
         const uint64_t tbeg = b / tile_vw<KT>() * tile_vw<KT>() + (uint64_t)(t - sg.tile_base) * TILE;
         const uint64_t band0 = b + cn.L, band1 = band0 + cn.E;
@@ -565,8 +577,23 @@ __global__ void __launch_bounds__(NT) k_fill(const PostParams<KT> Qin, int phase
             }
         } else {
             if (phase != 0) continue;
+            // scalar head up to a 16-byte boundary, 16-byte stores, scalar tail
             const T pv = KT::from_key((K)sg.pivot);
-            for (uint64_t i = x0 + threadIdx.x; i < x1; i += NT) P.final_buf[i] = pv;
+            constexpr uint32_t V = 16 / sizeof(T);
+            T *o = P.final_buf;
+            if (x1 <= x0) continue;
+            uint64_t head = ((16 - (reinterpret_cast<uintptr_t>(o + x0) & 15)) & 15) / sizeof(T);
+            if (head > x1 - x0) head = x1 - x0;
+            const uint64_t nb = (x1 - x0 - head) / V;
+            T rep[V];
+#pragma unroll
+            for (uint32_t k = 0; k < V; k++) rep[k] = pv;
+            uint4 vv;
+            memcpy(&vv, rep, 16);
+            for (uint64_t i = x0 + threadIdx.x; i < x0 + head; i += NT) o[i] = pv;
+            uint4 *ov = reinterpret_cast<uint4 *>(o + x0 + head);
+            for (uint64_t j = threadIdx.x; j < nb; j += NT) ov[j] = vv;
+            for (uint64_t i = x0 + head + nb * V + threadIdx.x; i < x1; i += NT) o[i] = pv;
         }
     }
 }

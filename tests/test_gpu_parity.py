@@ -710,3 +710,41 @@ def test_leaf_max_override(B, kind, div, monkeypatch):
         assert st["fallback_segments"] == 0
         if dist == "random":
             assert st["leaves"] > base["leaves"]
+
+
+@pytest.mark.parametrize("kind", ["i32", "u64", "f64"])
+def test_equal_bands_in_place_and_filled(B, kind):
+    """a6: (1) an input of one repeated key is its own equal band — the pass
+    finds L = G = 0 with the source in the user buffer and writes nothing
+    (band_in_place); (2) a long band between smaller and larger keys (E above
+    the inline limit, odd offsets, a buffer off 16-byte alignment) is written
+    by k_fill's 16-byte stores with scalar head and tail; (3) few distinct
+    values: single-value segments end the recursion at both buffer parities."""
+    S = LEAF[kind]
+    base = make(kind, 4096, seed=41)
+    v = np.sort(base)[2048]
+    for n in (S + 1, 5 * S + 3, (1 << 20) + 7):
+        a = np.full(n, v, dtype=base.dtype)
+        for off in (0, 1):
+            t = to_dev(a, offset=off)
+            st = B.bq_sort_ex(t, ways=2)
+            check_sorted_equal(kind, to_host(t, a), a)
+            assert st["band_elements"] == n and st["leaves"] == 0
+    rng = np.random.default_rng(9)
+    lo, hi = base[base < v][:1001], base[base > v][:777]
+    for E in ((1 << 16) + 1, 300001):
+        a = np.concatenate([lo, np.full(E, v, dtype=base.dtype), hi])
+        rng.shuffle(a)
+        for off in (0, 1):
+            for ways in (2, 8):
+                t = to_dev(a, offset=off)
+                st = B.bq_sort_ex(t, ways=ways)
+                check_sorted_equal(kind, to_host(t, a), a)
+                assert st["band_elements"] >= E
+    vals = np.sort(base)[::512]   # 8 distinct values
+    a = vals[rng.integers(0, len(vals), size=12 * S + 5)]
+    for ways in (2, 8):
+        t = to_dev(a)
+        st = B.bq_sort_ex(t, ways=ways)
+        check_sorted_equal(kind, to_host(t, a), a)
+        assert st["band_elements"] >= len(a) // 2
